@@ -1,0 +1,127 @@
+/*
+ * vlq_gpu.h -- C ABI of the B200-native VLQ-ADC engine (libvlqgpu.so).
+ *
+ * This is the drop-in boundary for the reference's index API.  Every entry
+ * point below replaces one call site of the reference C++ library
+ * (/root/reference/proj) that its pybind11 binding
+ * (proj/python/bindings.cpp) wraps; the citation on each declaration names
+ * the interface it stands in for.  INTEGRATION.md shows the bindings a
+ * maintainer adds (ctypes, pybind11, cgo-style C).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Host pointers are owned by the caller;
+ *    the engine owns all device memory.  "_device" variants take device
+ *    pointers and a cudaStream_t passed as void*.
+ *  - Every call returns 0 on success or a negative status; it never throws
+ *    across the ABI.  vlq_last_error() returns the thread-local message,
+ *    which uses the reference's own text where one exists (e.g.
+ *    "first_level_scan: need 0 < w1 <= k", "deserialize_index: bad magic
+ *    in <path>", "index already holds a base set").
+ *  - One engine per index (or per shard of an index).  Calls on one engine
+ *    must be serialised by the caller, as with the reference's non-const
+ *    methods.
+ *  - There is no CPU fallback: without a CUDA device vlq_engine_create fails.
+ */
+#ifndef VLQ_GPU_H
+#define VLQ_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VLQ_OK 0
+#define VLQ_ERR_INVALID -1   /* bad argument / reference-level runtime_error */
+#define VLQ_ERR_CUDA -2      /* CUDA runtime error */
+#define VLQ_ERR_IO -3        /* file error (open / truncated / bad magic) */
+
+typedef struct vlq_engine vlq_engine;
+
+typedef struct {
+    int device;                /* CUDA ordinal */
+    int shard_rank;            /* regions i with i % shard_count == shard_rank live here */
+    int shard_count;           /* 1 = whole index on this device */
+    uint64_t workspace_bytes;  /* per-query-tile scratch budget (0 = 4 GiB) */
+    uint32_t max_tile;         /* max queries per tile (0 = 16384) */
+    int force_exact;           /* 1 = exact reference-order scan for every query */
+} vlq_config;
+
+typedef struct {
+    uint32_t dim, k, n, m;
+    int clamp_lambda;
+    float lambda_lo, lambda_hi;
+    uint64_t ntotal;         /* base_count (all shards) */
+    uint64_t local_entries;  /* posting entries held by this engine */
+} vlq_info;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* vlq_last_error(void);
+
+/* Engine lifetime.  Replaces constructing vlq::InvertedIndex
+ * (proj/include/vlq/index.hpp:38-72) / PyIndex (bindings.cpp:41-42). */
+int vlq_engine_create(const vlq_config* cfg, vlq_engine** out);
+void vlq_engine_destroy(vlq_engine* e);
+
+/* Index.load: deserialize_index (proj/src/index_io.cpp:100-159, VLQ1). */
+int vlq_engine_load_vlq1(vlq_engine* e, const char* path);
+
+/* Index.save: serialize_index (proj/src/index_io.cpp:63-98). */
+int vlq_engine_save_vlq1(vlq_engine* e, const char* path, int store_t3);
+
+/* Installs trained quantizers (the model half of Index.train,
+ * bindings.cpp:44-81; make_model in proj/tools/vlq_cli.cpp:19-34).  t3 may be
+ * NULL (computed exactly as compute_t3, proj/src/index.cpp:54-74). */
+int vlq_engine_set_model(vlq_engine* e, uint32_t dim, uint32_t k, uint32_t n, uint32_t m, int clamp_lambda,
+                         float lambda_lo, float lambda_hi, const float* centroids, const uint32_t* neighbor_ids,
+                         const float* edge_sq_len, const float* pq_sub_centroids, const float* t3_or_null);
+
+/* Index.add: build_index (proj/src/index.cpp:134-203) + once-only rule and
+ * observe_lambda_range for unclamped models (bindings.cpp:83-97). */
+int vlq_engine_add(vlq_engine* e, const float* base, uint64_t n, uint32_t dim);
+
+/* Index.search: search_batch (proj/src/search.cpp:169-191) with the
+ * binding's padding (bindings.cpp:111-125): out_ids/out_dists are nq*k,
+ * rows ascending by (dist, id), unfilled slots -1/+inf.  out_scanned
+ * (nullable) receives the per-query scanned-candidate count
+ * (SearchStats::scanned_candidates, search.cpp:163-165). */
+int vlq_engine_search(vlq_engine* e, const float* queries, uint64_t nq, uint32_t dim, uint32_t w1, float alpha,
+                      uint32_t k, int64_t* out_ids, float* out_dists, uint64_t* out_scanned);
+
+/* Same with device-resident queries/outputs, asynchronous on `stream`
+ * (cudaStream_t).  Call vlq_engine_sync to surface deferred errors. */
+int vlq_engine_search_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                             uint32_t k, int64_t* d_ids, float* d_dists, uint64_t* d_scanned, void* stream);
+int vlq_engine_sync(vlq_engine* e, void* stream);
+
+/* Index.k / n / m / dim / ntotal (bindings.cpp:222-232). */
+int vlq_engine_info(vlq_engine* e, vlq_info* out);
+
+/* Copies the (this shard's) posting lists back to the host:
+ * list_off[k*n+1], ids[local_entries], codes[local_entries*m], lambdas[...]. */
+int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8_t* codes, uint8_t* lambdas);
+
+/* Per-point add-path outputs without mutating the index: assign_point +
+ * assign_edge + residual + pq_encode + quantize_lambda (index.cpp:86-106,
+ * 167-188).  Any output pointer may be NULL. */
+int vlq_engine_encode(vlq_engine* e, const float* x, uint64_t n, uint32_t* cells, float* lambdas, uint8_t* codes,
+                      uint8_t* lambda_bytes);
+
+/* Merges nparts per-shard top-k result blocks [nparts][nq][k] (device
+ * pointers) into the global (dist, id) top-k (the paper's multi-GPU join,
+ * PAPER.md:498-499). */
+int vlq_merge_topk_device(int device, const int64_t* d_in_ids, const float* d_in_dists, uint32_t nparts, uint64_t nq,
+                          uint32_t k, int64_t* d_out_ids, float* d_out_dists, void* stream);
+
+/* brute_force_gt (proj/src/dataset.cpp:46-92): exact k-NN ids, ties by id. */
+int vlq_brute_force_gt(int device, const float* base, uint64_t nb, const float* queries, uint64_t nq, uint32_t dim,
+                       uint32_t k, uint32_t* out);
+
+/* gen_synthetic (proj/src/dataset.cpp:13-44): identical stream. */
+int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VLQ_GPU_H */

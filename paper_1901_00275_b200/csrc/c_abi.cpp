@@ -1,0 +1,237 @@
+// extern "C" boundary (include/vlq_gpu.h).  No exception crosses it.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <random>
+#include <string>
+
+#include "../../include/vlq_gpu.h"
+#include "engine.h"
+
+struct vlq_engine {
+    vlq::Engine* impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return VLQ_OK;
+    } catch (const vlq::CudaError& e) {
+        return fail(VLQ_ERR_CUDA, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(VLQ_ERR_INVALID, "out of host memory");
+    } catch (const std::exception& e) {
+        const char* w = e.what();
+        const bool io = std::strstr(w, "cannot open") || std::strstr(w, "truncated") || std::strstr(w, "bad magic") ||
+                        std::strstr(w, "unsupported version") || std::strstr(w, "invalid header") ||
+                        std::strstr(w, "write failed");
+        return fail(io ? VLQ_ERR_IO : VLQ_ERR_INVALID, w);
+    } catch (...) {
+        return fail(VLQ_ERR_INVALID, "unknown error");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vlq_last_error(void) { return g_last_error.c_str(); }
+
+int vlq_engine_create(const vlq_config* cfg, vlq_engine** out) {
+    if (!out) return fail(VLQ_ERR_INVALID, "vlq_engine_create: out is NULL");
+    *out = nullptr;
+    return guarded([&] {
+        vlq::EngineConfig c;
+        if (cfg) {
+            c.device = cfg->device;
+            c.shard_rank = cfg->shard_rank;
+            c.shard_count = cfg->shard_count ? cfg->shard_count : 1;
+            if (cfg->workspace_bytes) c.workspace_bytes = cfg->workspace_bytes;
+            if (cfg->max_tile) c.max_tile = cfg->max_tile;
+            c.force_exact = cfg->force_exact;
+        }
+        auto* e = new vlq_engine{nullptr};
+        try {
+            e->impl = new vlq::Engine(c);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
+void vlq_engine_destroy(vlq_engine* e) {
+    if (!e) return;
+    delete e->impl;
+    delete e;
+}
+
+#define ENGINE_OR_FAIL(e) \
+    if (!(e) || !(e)->impl) return fail(VLQ_ERR_INVALID, "engine handle is NULL")
+
+int vlq_engine_load_vlq1(vlq_engine* e, const char* path) {
+    ENGINE_OR_FAIL(e);
+    if (!path) return fail(VLQ_ERR_INVALID, "path is NULL");
+    return guarded([&] { e->impl->load_vlq1(path); });
+}
+
+int vlq_engine_save_vlq1(vlq_engine* e, const char* path, int store_t3) {
+    ENGINE_OR_FAIL(e);
+    if (!path) return fail(VLQ_ERR_INVALID, "path is NULL");
+    return guarded([&] { e->impl->save_vlq1(path, store_t3 != 0); });
+}
+
+int vlq_engine_set_model(vlq_engine* e, uint32_t dim, uint32_t k, uint32_t n, uint32_t m, int clamp_lambda,
+                         float lambda_lo, float lambda_hi, const float* centroids, const uint32_t* neighbor_ids,
+                         const float* edge_sq_len, const float* pq_sub_centroids, const float* t3_or_null) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (dim == 0 || k == 0 || n == 0 || n >= k || m == 0 || dim % m != 0)
+            throw std::runtime_error("set_model: invalid model header");
+        if (!centroids || !neighbor_ids || !edge_sq_len || !pq_sub_centroids)
+            throw std::runtime_error("set_model: NULL array");
+        vlq::HostModel hm;
+        hm.dim = dim;
+        hm.k = k;
+        hm.n = n;
+        hm.m = m;
+        hm.clamp = clamp_lambda != 0;
+        hm.lo = lambda_lo;
+        hm.hi = lambda_hi;
+        hm.centroids.assign(centroids, centroids + (size_t)k * dim);
+        hm.nbr.assign(neighbor_ids, neighbor_ids + (size_t)k * n);
+        hm.elen.assign(edge_sq_len, edge_sq_len + (size_t)k * n);
+        hm.pq.assign(pq_sub_centroids, pq_sub_centroids + (size_t)m * 256 * (dim / m));
+        if (t3_or_null) hm.t3.assign(t3_or_null, t3_or_null + (size_t)k * m * 256);
+        e->impl->set_model(hm);
+    });
+}
+
+int vlq_engine_add(vlq_engine* e, const float* base, uint64_t n, uint32_t dim) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!e->impl->has_model()) throw std::runtime_error("add: no model loaded");
+        if (e->impl->ntotal() != 0) throw std::runtime_error("index already holds a base set");
+        if (dim != e->impl->dim()) throw std::runtime_error("build_index: dimension mismatch");
+        if (n && !base) throw std::runtime_error("add: base is NULL");
+        e->impl->add_host(base, n);
+    });
+}
+
+int vlq_engine_search(vlq_engine* e, const float* queries, uint64_t nq, uint32_t dim, uint32_t w1, float alpha,
+                      uint32_t k, int64_t* out_ids, float* out_dists, uint64_t* out_scanned) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!e->impl->has_model()) throw std::runtime_error("search: no model loaded");
+        if (dim != e->impl->dim()) throw std::runtime_error("search_batch: dimension mismatch");
+        if (nq && (!queries || (k && (!out_ids || !out_dists)))) throw std::runtime_error("search: NULL buffer");
+        e->impl->search_host(queries, nq, w1, alpha, k, out_ids, out_dists, out_scanned);
+    });
+}
+
+int vlq_engine_search_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                             uint32_t k, int64_t* d_ids, float* d_dists, uint64_t* d_scanned, void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        e->impl->search_device(d_queries, nq, w1, alpha, k, d_ids, d_dists, d_scanned,
+                               stream ? (cudaStream_t)stream : e->impl->stream());
+    });
+}
+
+int vlq_engine_sync(vlq_engine* e, void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] { e->impl->check_device_errors(stream ? (cudaStream_t)stream : e->impl->stream()); });
+}
+
+int vlq_engine_info(vlq_engine* e, vlq_info* out) {
+    ENGINE_OR_FAIL(e);
+    if (!out) return fail(VLQ_ERR_INVALID, "info: out is NULL");
+    out->dim = e->impl->dim();
+    out->k = e->impl->k();
+    out->n = e->impl->n();
+    out->m = e->impl->m();
+    out->clamp_lambda = e->impl->clamp() ? 1 : 0;
+    out->lambda_lo = e->impl->lo();
+    out->lambda_hi = e->impl->hi();
+    out->ntotal = e->impl->ntotal();
+    out->local_entries = e->impl->local_entries();
+    return VLQ_OK;
+}
+
+int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8_t* codes, uint8_t* lambdas) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        vlq::HostLists L;
+        e->impl->get_lists(L);
+        if (list_off) std::memcpy(list_off, L.off.data(), L.off.size() * 8);
+        if (ids) std::memcpy(ids, L.ids.data(), L.ids.size() * 4);
+        if (codes) std::memcpy(codes, L.codes.data(), L.codes.size());
+        if (lambdas) std::memcpy(lambdas, L.lambdas.data(), L.lambdas.size());
+    });
+}
+
+int vlq_engine_encode(vlq_engine* e, const float* x, uint64_t n, uint32_t* cells, float* lambdas, uint8_t* codes,
+                      uint8_t* lambda_bytes) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (n == 0) return;
+        e->impl->encode_host(x, n, cells, lambdas, codes, lambda_bytes);
+    });
+}
+
+int vlq_merge_topk_device(int device, const int64_t* d_in_ids, const float* d_in_dists, uint32_t nparts, uint64_t nq,
+                          uint32_t k, int64_t* d_out_ids, float* d_out_dists, void* stream) {
+    return guarded([&] {
+        if (nparts == 0 || nparts * (uint64_t)k > 8192) throw std::runtime_error("merge_topk: nparts*k must be in [1, 8192]");
+        int prev = 0;
+        vlq::cuda_check(cudaGetDevice(&prev), "cudaGetDevice", __FILE__, __LINE__);
+        vlq::cuda_check(cudaSetDevice(device), "cudaSetDevice", __FILE__, __LINE__);
+        vlq::launch_merge_topk(d_in_ids, d_in_dists, nparts, nq, k, d_out_ids, d_out_dists, (cudaStream_t)stream);
+        cudaSetDevice(prev);
+    });
+}
+
+int vlq_brute_force_gt(int device, const float* base, uint64_t nb, const float* queries, uint64_t nq, uint32_t dim,
+                       uint32_t k, uint32_t* out) {
+    return guarded([&] {
+        if (dim == 0) throw std::runtime_error("brute_force_gt: dimension mismatch");
+        vlq::Engine::brute_force_gt(device, base, nb, queries, nq, dim, k, out);
+    });
+}
+
+// gen_synthetic (proj/src/dataset.cpp:13-44).  The stream is defined by
+// std::mt19937_64 and libstdc++'s uniform_real / normal / uniform_int
+// distributions, so this host generator reproduces the reference's data
+// bit-for-bit when built with the same standard library.
+int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed, float* out) {
+    return guarded([&] {
+        if (dim == 0 || clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
+        if (!(spread > 0)) throw std::runtime_error("gen_synthetic: spread must be positive");
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<float> unif(0.0f, 1.0f);
+        std::vector<float> centers((size_t)clusters * dim);
+        for (float& v : centers) v = unif(rng);
+        std::normal_distribution<float> gauss(0.0f, spread);
+        std::uniform_int_distribution<uint32_t> pick(0, clusters - 1);
+        for (uint64_t i = 0; i < count; i++) {
+            const uint32_t c = pick(rng);
+            const float* ctr = centers.data() + (size_t)c * dim;
+            float* row = out + i * dim;
+            for (uint32_t j = 0; j < dim; j++) row[j] = ctr[j] + gauss(rng);
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,672 @@
+// Engine orchestration: model upload, batched add/encode with stable
+// bucketing, tiled batched search, VLQ1 load/save.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <stdexcept>
+
+#include "engine.h"
+
+namespace vlq {
+
+namespace {
+
+uint32_t next_pow2(uint32_t v) {
+    uint32_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CUDA_CHECK(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+void h2d(DevBuf<T>& dst, const std::vector<T>& src, cudaStream_t st) {
+    dst.alloc(std::max<size_t>(src.size(), 1));
+    if (!src.empty()) CUDA_CHECK(cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+__global__ void k_mask_cells(uint32_t* cells, uint64_t n, uint32_t nedges, uint32_t shards, uint32_t rank,
+                             uint32_t sentinel) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t region = cells[i] / nedges;
+        if (region % shards != rank) cells[i] = sentinel;
+    }
+}
+
+}  // namespace
+
+// QueryParams::w2 (proj/include/vlq/search.hpp:16-20)
+uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
+    uint32_t full = w1 * n;
+    uint32_t w = (uint32_t)((double)alpha * full);
+    return w == 0 ? 1 : (w > full ? full : w);
+}
+
+Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
+    if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
+        throw std::runtime_error("engine: invalid shard configuration");
+    int ndev = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    if (cfg_.device < 0 || cfg_.device >= ndev) throw std::runtime_error("engine: invalid CUDA device");
+    DeviceGuard g(cfg_.device);
+    CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    err_.alloc(8);
+    CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 8 * sizeof(unsigned int), stream_));
+}
+
+Engine::~Engine() {
+    if (stream_) {
+        cudaSetDevice(cfg_.device);
+        cudaStreamSynchronize(stream_);
+        cudaStreamDestroy(stream_);
+    }
+}
+
+AddArgs Engine::add_args() const {
+    AddArgs a{};
+    a.dim = dim_;
+    a.k = k_;
+    a.n = n_;
+    a.m = m_;
+    a.clamp = clamp_;
+    a.lo = lo_;
+    a.hi = hi_;
+    a.centroids = centroids_.p;
+    a.nbr = nbr_.p;
+    a.elen = elen_.p;
+    a.pq = pq_.p;
+    a.t2 = t2_.p;
+    a.t3 = t3_.p;
+    a.error_flag = err_.p;
+    return a;
+}
+
+SearchArgs Engine::search_args() const {
+    SearchArgs a{};
+    a.dim = dim_;
+    a.k = k_;
+    a.n = n_;
+    a.m = m_;
+    a.lo = lo_;
+    a.hi = hi_;
+    a.lam_absmax = std::max(std::max(std::fabs(lo_), std::fabs(hi_)), 0.0f);
+    a.emax = emax_;
+    a.centroids = centroids_.p;
+    a.nbr = nbr_.p;
+    a.elen = elen_.p;
+    a.pq = pq_.p;
+    a.t2 = t2_.p;
+    a.t3 = t3_.p;
+    a.list_off = list_off_.p;
+    a.codes = codes_.p;
+    a.lambdas = lambdas_.p;
+    a.ids = ids_.p;
+    a.eterm = eterm_.p;
+    a.ws = ws_.p;
+    a.top = top_.p;
+    a.dbuf = dbuf_.p;
+    a.sel = sel_.p;
+    a.t5 = t5_.p;
+    a.cand = cand_.p;
+    a.meta = meta_.p;
+    a.error_flag = err_.p;
+    return a;
+}
+
+void Engine::set_model(const HostModel& m) {
+    if (m.dim == 0 || m.k == 0 || m.n == 0 || m.n >= m.k || m.m == 0 || m.dim % m.m != 0)
+        throw std::runtime_error("set_model: invalid model header");
+    if (m.centroids.size() != (size_t)m.k * m.dim || m.nbr.size() != (size_t)m.k * m.n ||
+        m.elen.size() != (size_t)m.k * m.n || m.pq.size() != (size_t)m.m * VLQ_KSUB * (m.dim / m.m) ||
+        (!m.t3.empty() && m.t3.size() != (size_t)m.k * m.m * VLQ_KSUB))
+        throw std::runtime_error("set_model: array sizes do not match the header");
+    for (uint32_t v : m.nbr)
+        if (v >= m.k) throw std::runtime_error("set_model: neighbour id out of range");
+    model_ = m;
+    dim_ = m.dim;
+    k_ = m.k;
+    n_ = m.n;
+    m_ = m.m;
+    clamp_ = m.clamp;
+    lo_ = m.lo;
+    hi_ = m.hi;
+    base_count_ = 0;
+    nent_ = 0;
+    emax_ = 0.0f;
+    upload_model();
+    HostLists empty;
+    empty.off.assign((size_t)k_ * n_ + 1, 0);
+    upload_lists(empty);
+    model_ok_ = true;
+}
+
+void Engine::upload_model() {
+    DeviceGuard g(cfg_.device);
+    h2d(centroids_, model_.centroids, stream_);
+    h2d(nbr_, model_.nbr, stream_);
+    h2d(elen_, model_.elen, stream_);
+    h2d(pq_, model_.pq, stream_);
+    t2_.alloc((size_t)m_ * VLQ_KSUB);
+    t3_.alloc(std::max<size_t>((size_t)k_ * m_ * VLQ_KSUB, 1));
+    // t2 (pq.cpp:11-18, recomputed on load: index_io.cpp:140) and t3
+    // (compute_t3, index.cpp:54-74) in the reference's exact order
+    launch_tables(centroids_.p, k_, dim_, pq_.p, m_, t2_.p, t3_.p, stream_);
+    if (!model_.t3.empty())
+        CUDA_CHECK(cudaMemcpyAsync(t3_.p, model_.t3.data(), model_.t3.size() * 4, cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::upload_lists(const HostLists& L) {
+    DeviceGuard g(cfg_.device);
+    h2d(list_off_, L.off, stream_);
+    h2d(ids_, L.ids, stream_);
+    h2d(codes_, L.codes, stream_);
+    h2d(lambdas_, L.lambdas, stream_);
+    nent_ = L.ids.size();
+    eterm_.alloc(std::max<uint64_t>(nent_, 1));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::compute_eterm() {
+    DeviceGuard g(cfg_.device);
+    CUDA_CHECK(cudaMemsetAsync(err_.p + 1, 0, sizeof(unsigned int), stream_));
+    launch_eterm_lists(add_args(), list_off_.p, k_ * n_, codes_.p, lambdas_.p, nent_, eterm_.p, err_.p + 1, stream_);
+    unsigned int bits = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&bits, err_.p + 1, 4, cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    std::memcpy(&emax_, &bits, 4);
+}
+
+void Engine::check_device_errors(cudaStream_t st) {
+    unsigned int flag = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&flag, err_.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (flag) {
+        CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        throw std::runtime_error("line_lambda: degenerate edge (c == 0)");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// add: build_index (index.cpp:134-203) on the device
+// ---------------------------------------------------------------------------
+void Engine::add_host(const float* base, uint64_t nb) {
+    if (!model_ok_) throw std::runtime_error("add: no model loaded");
+    if (base_count_ != 0) throw std::runtime_error("index already holds a base set");
+    if (nb == 0) throw std::runtime_error("build_index: empty base set");
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(nb, (256ull << 20) / (4ull * dim_)));
+    add_stream(nb, chunk, [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, base + first * dim_, count * dim_ * 4, cudaMemcpyHostToDevice, st));
+    });
+}
+
+void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
+    if (!model_ok_) throw std::runtime_error("add: no model loaded");
+    if (base_count_ != 0) throw std::runtime_error("index already holds a base set");
+    if (nb == 0) throw std::runtime_error("build_index: empty base set");
+    if (nb > 0xffffffffull) throw std::runtime_error("add: more than 2^32-1 points (VLQ1 ids are u32)");
+    DeviceGuard g(cfg_.device);
+    cudaStream_t st = stream_;
+    chunk = std::max<uint64_t>(1, std::min(chunk, nb));
+    DevBuf<float> X;
+    DevBuf<uint32_t> best;
+    DevBuf<float> lam;
+    X.alloc(chunk * dim_);
+    best.alloc(chunk);
+    lam.alloc(chunk);
+    CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 8 * sizeof(unsigned int), st));
+    // observe_lambda_range (index.cpp:110-132) for unclamped models
+    if (!clamp_) {
+        unsigned int init[2] = {0xffffffffu, 0u};
+        CUDA_CHECK(cudaMemcpyAsync(err_.p + 3, init, 8, cudaMemcpyHostToDevice, st));
+        AddArgs a = add_args();
+        for (uint64_t f = 0; f < nb; f += chunk) {
+            uint64_t c = std::min(chunk, nb - f);
+            src(f, c, X.p, st);
+            launch_assign_nearest(a, X.p, c, best.p, st);
+            launch_encode(a, X.p, c, best.p, 0, nullptr, lam.p, nullptr, nullptr, nullptr, nullptr, st);
+            launch_minmax(lam.p, c, reinterpret_cast<float*>(err_.p + 3), st);
+        }
+        unsigned int mm[2];
+        CUDA_CHECK(cudaMemcpyAsync(mm, err_.p + 3, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        auto unord = [](unsigned int u) {
+            u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+            float f;
+            std::memcpy(&f, &u, 4);
+            return f;
+        };
+        float lo = unord(mm[0]), hi = unord(mm[1]);
+        if (!(lo < hi)) hi = lo + 1.0f;
+        lo_ = lo;
+        hi_ = hi;
+        model_.lo = lo;
+        model_.hi = hi;
+    }
+    // encode pass: point-order outputs
+    DevBuf<uint32_t> cells;
+    DevBuf<uint8_t> codes_pt, lamb_pt;
+    DevBuf<float> eterm_pt;
+    cells.alloc(nb);
+    codes_pt.alloc(nb * m_);
+    lamb_pt.alloc(nb);
+    eterm_pt.alloc(nb);
+    {
+        AddArgs a = add_args();
+        for (uint64_t f = 0; f < nb; f += chunk) {
+            uint64_t c = std::min(chunk, nb - f);
+            src(f, c, X.p, st);
+            launch_assign_nearest(a, X.p, c, best.p, st);
+            launch_encode(a, X.p, c, best.p, clamp_ ? 1 : 0, cells.p + f, nullptr, codes_pt.p + f * m_, lamb_pt.p + f,
+                          eterm_pt.p + f, err_.p + 1, st);
+        }
+    }
+    X.reset();
+    best.reset();
+    lam.reset();
+    // stable bucketing by cell (index.cpp:189-200): ids ascend within a list
+    const uint32_t ncell = k_ * n_;
+    const uint32_t sentinel = ncell;
+    if (cfg_.shard_count > 1) {
+        k_mask_cells<<<1184, 256, 0, st>>>(cells.p, nb, n_, (uint32_t)cfg_.shard_count, (uint32_t)cfg_.shard_rank,
+                                           sentinel);
+        CUDA_LAUNCH_CHECK();
+    }
+    int end_bit = 1;
+    while ((1ull << end_bit) <= (uint64_t)sentinel) end_bit++;
+    DevBuf<uint32_t> cells_sorted, iota, order;
+    cells_sorted.alloc(nb);
+    iota.alloc(nb);
+    order.alloc(nb);
+    launch_iota(iota.p, nb, st);
+    size_t temp_bytes = 0;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, cells.p, cells_sorted.p, iota.p, order.p, nb, 0,
+                                               end_bit, st));
+    {
+        DevBuf<unsigned char> temp;
+        temp.alloc(temp_bytes);
+        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, cells.p, cells_sorted.p, iota.p, order.p, nb, 0,
+                                                   end_bit, st));
+    }
+    iota.reset();
+    DevBuf<unsigned long long> counts;
+    counts.alloc((size_t)ncell + 2);
+    CUDA_CHECK(cudaMemsetAsync(counts.p, 0, ((size_t)ncell + 2) * 8, st));
+    launch_histogram(cells_sorted.p, nb, counts.p, st);
+    list_off_.alloc((size_t)ncell + 1);
+    temp_bytes = 0;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, counts.p, reinterpret_cast<unsigned long long*>(list_off_.p),
+                                             (int)(ncell + 1), st));
+    {
+        DevBuf<unsigned char> temp;
+        temp.alloc(temp_bytes);
+        CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp.p, temp_bytes, counts.p,
+                                                 reinterpret_cast<unsigned long long*>(list_off_.p), (int)(ncell + 1), st));
+    }
+    uint64_t nloc = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&nloc, list_off_.p + ncell, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    cells.reset();
+    cells_sorted.reset();
+    counts.reset();
+    ids_.reset();
+    codes_.reset();
+    lambdas_.reset();
+    eterm_.reset();
+    ids_.alloc(std::max<uint64_t>(nloc, 1));
+    codes_.alloc(std::max<uint64_t>(nloc * m_, 1));
+    lambdas_.alloc(std::max<uint64_t>(nloc, 1));
+    eterm_.alloc(std::max<uint64_t>(nloc, 1));
+    launch_gather_entries(order.p, nloc, m_, 0, codes_pt.p, lamb_pt.p, eterm_pt.p, ids_.p, codes_.p, lambdas_.p,
+                          eterm_.p, st);
+    unsigned int flags[2];
+    CUDA_CHECK(cudaMemcpyAsync(flags, err_.p, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (flags[0]) {
+        CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
+        HostLists empty;
+        empty.off.assign((size_t)ncell + 1, 0);
+        upload_lists(empty);
+        throw std::runtime_error("line_lambda: degenerate edge (c == 0)");
+    }
+    std::memcpy(&emax_, &flags[1], 4);
+    nent_ = nloc;
+    base_count_ = nb;
+}
+
+void Engine::encode_host(const float* x, uint64_t nx, uint32_t* cells, float* lambdas, uint8_t* codes,
+                         uint8_t* lam_bytes) {
+    if (!model_ok_) throw std::runtime_error("encode: no model loaded");
+    DeviceGuard g(cfg_.device);
+    cudaStream_t st = stream_;
+    DevBuf<float> X, lam, et;
+    DevBuf<uint32_t> best, cl;
+    DevBuf<uint8_t> cd, lb;
+    X.alloc(std::max<uint64_t>(nx * dim_, 1));
+    lam.alloc(std::max<uint64_t>(nx, 1));
+    et.alloc(std::max<uint64_t>(nx, 1));
+    best.alloc(std::max<uint64_t>(nx, 1));
+    cl.alloc(std::max<uint64_t>(nx, 1));
+    cd.alloc(std::max<uint64_t>(nx * m_, 1));
+    lb.alloc(std::max<uint64_t>(nx, 1));
+    CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 8 * sizeof(unsigned int), st));
+    CUDA_CHECK(cudaMemcpyAsync(X.p, x, nx * dim_ * 4, cudaMemcpyHostToDevice, st));
+    AddArgs a = add_args();
+    launch_assign_nearest(a, X.p, nx, best.p, st);
+    launch_encode(a, X.p, nx, best.p, clamp_ ? 1 : 0, cl.p, lam.p, cd.p, lb.p, et.p, err_.p + 1, st);
+    if (cells) CUDA_CHECK(cudaMemcpyAsync(cells, cl.p, nx * 4, cudaMemcpyDeviceToHost, st));
+    if (lambdas) CUDA_CHECK(cudaMemcpyAsync(lambdas, lam.p, nx * 4, cudaMemcpyDeviceToHost, st));
+    if (codes) CUDA_CHECK(cudaMemcpyAsync(codes, cd.p, nx * m_, cudaMemcpyDeviceToHost, st));
+    if (lam_bytes) CUDA_CHECK(cudaMemcpyAsync(lam_bytes, lb.p, nx, cudaMemcpyDeviceToHost, st));
+    check_device_errors(st);
+}
+
+void Engine::get_lists(HostLists& out) {
+    DeviceGuard g(cfg_.device);
+    out.off.resize((size_t)k_ * n_ + 1);
+    out.ids.resize(nent_);
+    out.codes.resize(nent_ * m_);
+    out.lambdas.resize(nent_);
+    out.base_count = base_count_;
+    CUDA_CHECK(cudaMemcpyAsync(out.off.data(), list_off_.p, out.off.size() * 8, cudaMemcpyDeviceToHost, stream_));
+    if (nent_) {
+        CUDA_CHECK(cudaMemcpyAsync(out.ids.data(), ids_.p, nent_ * 4, cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaMemcpyAsync(out.codes.data(), codes_.p, nent_ * m_, cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaMemcpyAsync(out.lambdas.data(), lambdas_.p, nent_, cudaMemcpyDeviceToHost, stream_));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::get_tables(std::vector<float>& t2, std::vector<float>& t3) {
+    DeviceGuard g(cfg_.device);
+    t2.resize((size_t)m_ * VLQ_KSUB);
+    t3.resize((size_t)k_ * m_ * VLQ_KSUB);
+    CUDA_CHECK(cudaMemcpyAsync(t2.data(), t2_.p, t2.size() * 4, cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaMemcpyAsync(t3.data(), t3_.p, t3.size() * 4, cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+// ---------------------------------------------------------------------------
+// search: search_batch (search.cpp:169-191), tiled over queries
+// ---------------------------------------------------------------------------
+void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
+                           float* d_dists, uint64_t* d_scanned, cudaStream_t st) {
+    if (!model_ok_) throw std::runtime_error("search: no model loaded");
+    if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
+    if (topk > 1024) throw std::runtime_error("search: k > 1024 is not supported by the GPU engine");
+    if (nq == 0) return;
+    DeviceGuard g(cfg_.device);
+    const uint32_t w2 = w2_of(w1, alpha, n_);
+    const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+    const uint64_t per_q = 4ull * k_ + 4ull * w1 + 4ull * w1 * n_ + 4ull * w2 + 4ull * VLQ_KSUB * m_ + 8ull * keep +
+                           sizeof(QueryMeta) + 4;
+    uint64_t tile = std::max<uint64_t>(1, cfg_.workspace_bytes / per_q);
+    tile = std::min<uint64_t>(tile, cfg_.max_tile);
+    tile = std::min<uint64_t>(tile, nq);
+    ws_.alloc(tile * k_);
+    top_.alloc(tile * w1);
+    dbuf_.alloc(tile * (uint64_t)w1 * n_);
+    sel_.alloc(tile * w2);
+    t5_.alloc(tile * VLQ_KSUB * m_);
+    cand_.alloc(tile * keep);
+    meta_.alloc(tile);
+    qlist_.alloc(tile);
+    for (uint64_t t0 = 0; t0 < nq; t0 += tile) {
+        const uint64_t nt = std::min(tile, nq - t0);
+        search_tile(d_q + t0 * dim_, nt, w1, w2, topk, d_ids + t0 * topk, d_dists + t0 * topk,
+                    d_scanned ? d_scanned + t0 : nullptr, st);
+    }
+}
+
+void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
+                         float* d_dists, uint64_t* d_scanned, cudaStream_t st) {
+    SearchArgs a = search_args();
+    launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
+    launch_first_level(ws_.p, nt, k_, w1, top_.p, st);
+    launch_second_level(a, nt, w1, w2, st);
+    launch_term5(d_q, pq_.p, dim_, m_, t5_.p, meta_.p, nt, st);
+    const uint32_t keep_x = next_pow2(std::max<uint32_t>(32, topk));
+    const uint32_t buf_x = 2 * keep_x;
+    const uint32_t warps_x = std::min<uint32_t>(8, std::max<uint32_t>(1, 8192 / buf_x));
+    const bool fast = !cfg_.force_exact && topk > 0 && topk <= 768;
+    if (fast) {
+        const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+        launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
+        launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
+        CUDA_CHECK(cudaMemsetAsync(err_.p + 2, 0, 4, st));
+        launch_compact_flags(meta_.p, nt, qlist_.p, err_.p + 2, st);
+        launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, qlist_.p, err_.p + 2, st);
+        launch_emit_exact(a, qlist_.p, err_.p + 2, nt, keep_x, topk, d_ids, d_dists, st);
+    } else if (topk > 0) {
+        launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, nullptr, nullptr, st);
+        launch_emit_exact(a, nullptr, nullptr, nt, keep_x, topk, d_ids, d_dists, st);
+    }
+    if (d_scanned) launch_copy_scanned(meta_.p, nt, d_scanned, st);
+}
+
+void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
+                         float* dists, uint64_t* scanned) {
+    if (!model_ok_) throw std::runtime_error("search: no model loaded");
+    if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
+    if (nq == 0) return;
+    DeviceGuard g(cfg_.device);
+    cudaStream_t st = stream_;
+    DevBuf<float> dq, dd;
+    DevBuf<int64_t> di;
+    DevBuf<uint64_t> ds;
+    dq.alloc(nq * dim_);
+    di.alloc(std::max<uint64_t>(nq * topk, 1));
+    dd.alloc(std::max<uint64_t>(nq * topk, 1));
+    ds.alloc(nq);
+    CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
+    CUDA_CHECK(cudaMemcpyAsync(dq.p, q, nq * dim_ * 4, cudaMemcpyHostToDevice, st));
+    search_device(dq.p, nq, w1, alpha, topk, di.p, dd.p, ds.p, st);
+    if (topk) {
+        CUDA_CHECK(cudaMemcpyAsync(ids, di.p, nq * topk * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(dists, dd.p, nq * topk * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (scanned) CUDA_CHECK(cudaMemcpyAsync(scanned, ds.p, nq * 8, cudaMemcpyDeviceToHost, st));
+    check_device_errors(st);
+}
+
+// ---------------------------------------------------------------------------
+// brute_force_gt (proj/src/dataset.cpp:46-92) on the device
+// ---------------------------------------------------------------------------
+void Engine::brute_force_gt(int device, const float* base, uint64_t nb, const float* queries, uint64_t nq,
+                            uint32_t dim, uint32_t k, uint32_t* out) {
+    if ((uint64_t)k > nb) throw std::runtime_error("brute_force_gt: k exceeds base count");
+    if (nq == 0 || k == 0) return;
+    DeviceGuard g(device);
+    cudaStream_t st;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const uint64_t C = std::min<uint64_t>(nb, 32768);
+    const uint64_t T = std::min<uint64_t>(nq, std::max<uint64_t>(1, (1ull << 30) / (4 * C)));
+    DevBuf<float> B, Q, dist;
+    DevBuf<uint32_t> sel;
+    DevBuf<uint64_t> running;
+    B.alloc(C * dim);
+    Q.alloc(nq * dim);
+    dist.alloc(T * C);
+    sel.alloc(T * (uint64_t)k);
+    running.alloc(nq * (uint64_t)k);
+    CUDA_CHECK(cudaMemcpyAsync(Q.p, queries, nq * dim * 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemsetAsync(running.p, 0xff, nq * (uint64_t)k * 8, st));
+    for (uint64_t c0 = 0; c0 < nb; c0 += C) {
+        const uint64_t cn = std::min(C, nb - c0);
+        CUDA_CHECK(cudaMemcpyAsync(B.p, base + c0 * dim, cn * dim * 4, cudaMemcpyHostToDevice, st));
+        for (uint64_t q0 = 0; q0 < nq; q0 += T) {
+            const uint64_t tn = std::min(T, nq - q0);
+            launch_sqdist_matrix(Q.p + q0 * dim, tn, B.p, cn, dim, dist.p, cn, st);
+            const uint32_t L = (uint32_t)std::min<uint64_t>(k, cn);
+            launch_select_rows(dist.p, cn, tn, (uint32_t)cn, L, sel.p, st);
+            launch_gt_merge(dist.p, cn, tn, k, (uint32_t)cn, sel.p, c0, running.p + q0 * k, st);
+        }
+    }
+    std::vector<uint64_t> keys(nq * (uint64_t)k);
+    CUDA_CHECK(cudaMemcpyAsync(keys.data(), running.p, keys.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    CUDA_CHECK(cudaStreamDestroy(st));
+    for (size_t i = 0; i < keys.size(); i++) out[i] = (uint32_t)keys[i];
+}
+
+// ---------------------------------------------------------------------------
+// VLQ1 file (proj/src/index_io.cpp:63-159)
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr char kMagic[4] = {'V', 'L', 'Q', '1'};
+constexpr uint32_t kVersion = 1;
+constexpr uint32_t kFlagClamped = 1u << 0;
+constexpr uint32_t kFlagT3 = 1u << 1;
+
+struct Reader {
+    std::ifstream in;
+    std::string path;
+    explicit Reader(const std::string& p) : in(p, std::ios::binary), path(p) {
+        if (!in) throw std::runtime_error("deserialize_index: cannot open " + p);
+    }
+    void bytes(void* p, size_t n) {
+        in.read(reinterpret_cast<char*>(p), (std::streamsize)n);
+        if ((size_t)in.gcount() != n) throw std::runtime_error("deserialize_index: truncated file " + path);
+    }
+    uint32_t u32() {
+        uint32_t v;
+        bytes(&v, 4);
+        return v;
+    }
+    float f32() {
+        float v;
+        bytes(&v, 4);
+        return v;
+    }
+};
+
+struct Writer {
+    std::ofstream out;
+    explicit Writer(const std::string& path) : out(path, std::ios::binary | std::ios::trunc) {
+        if (!out) throw std::runtime_error("serialize_index: cannot open " + path);
+    }
+    void bytes(const void* p, size_t n) { out.write(reinterpret_cast<const char*>(p), (std::streamsize)n); }
+    void u32(uint32_t v) { bytes(&v, 4); }
+    void f32(float v) { bytes(&v, 4); }
+};
+
+}  // namespace
+
+void Engine::load_vlq1(const std::string& path) {
+    Reader r(path);
+    char magic[4];
+    r.bytes(magic, 4);
+    if (std::memcmp(magic, kMagic, 4) != 0) throw std::runtime_error("deserialize_index: bad magic in " + path);
+    if (r.u32() != kVersion) throw std::runtime_error("deserialize_index: unsupported version in " + path);
+    const uint32_t flags = r.u32();
+    HostModel m;
+    m.dim = r.u32();
+    m.k = r.u32();
+    m.n = r.u32();
+    m.m = r.u32();
+    const uint32_t base_count = r.u32();
+    if (m.dim == 0 || m.k == 0 || m.n == 0 || m.n >= m.k || m.m == 0 || m.dim % m.m != 0)
+        throw std::runtime_error("deserialize_index: invalid header in " + path);
+    m.clamp = (flags & kFlagClamped) != 0;
+    m.lo = r.f32();
+    m.hi = r.f32();
+    m.centroids.resize((size_t)m.k * m.dim);
+    r.bytes(m.centroids.data(), m.centroids.size() * 4);
+    m.nbr.resize((size_t)m.k * m.n);
+    r.bytes(m.nbr.data(), m.nbr.size() * 4);
+    m.elen.resize((size_t)m.k * m.n);
+    r.bytes(m.elen.data(), m.elen.size() * 4);
+    m.pq.resize((size_t)m.m * VLQ_KSUB * (m.dim / m.m));
+    r.bytes(m.pq.data(), m.pq.size() * 4);
+    if (flags & kFlagT3) {
+        m.t3.resize((size_t)m.k * m.m * VLQ_KSUB);
+        r.bytes(m.t3.data(), m.t3.size() * 4);
+    }
+    const size_t ncell = (size_t)m.k * m.n;
+    HostLists L;
+    L.off.assign(ncell + 1, 0);
+    std::vector<uint8_t> seen(base_count, 0);
+    bool bad_partition = false;
+    uint64_t total = 0;
+    std::vector<uint32_t> ids;
+    std::vector<uint8_t> codes;
+    for (size_t c = 0; c < ncell; c++) {
+        const uint32_t len = r.u32();
+        ids.resize(len);
+        r.bytes(ids.data(), (size_t)len * 4);
+        codes.resize((size_t)len * m.m + len);
+        r.bytes(codes.data(), codes.size());
+        for (uint32_t id : ids) {  // validate() partition check (index.cpp:23-52)
+            if (id >= base_count || seen[id]) bad_partition = true;
+            else seen[id] = 1;
+        }
+        total += len;
+        const bool own = owner((uint32_t)(c / m.n)) == cfg_.shard_rank;
+        if (own) {
+            L.ids.insert(L.ids.end(), ids.begin(), ids.end());
+            L.codes.insert(L.codes.end(), codes.begin(), codes.begin() + (size_t)len * m.m);
+            L.lambdas.insert(L.lambdas.end(), codes.begin() + (size_t)len * m.m, codes.end());
+        }
+        L.off[c + 1] = L.ids.size();
+    }
+    // validate() order (index.cpp:23-52): lambda range, partition, total
+    if (!(m.lo < m.hi)) throw std::runtime_error("InvertedIndex: bad lambda range");
+    if (bad_partition) throw std::runtime_error("InvertedIndex: ids do not partition the base set");
+    if (total != base_count) throw std::runtime_error("InvertedIndex: list lengths do not sum to N");
+    set_model(m);
+    upload_lists(L);
+    base_count_ = base_count;
+    compute_eterm();
+}
+
+void Engine::save_vlq1(const std::string& path, bool store_t3) {
+    if (!model_ok_) throw std::runtime_error("save: no model loaded");
+    if (cfg_.shard_count != 1) throw std::runtime_error("save: a sharded engine cannot write a complete VLQ1 index");
+    HostLists L;
+    get_lists(L);
+    std::vector<float> t2, t3;
+    if (store_t3) get_tables(t2, t3);
+    Writer w(path);
+    w.bytes(kMagic, 4);
+    w.u32(kVersion);
+    w.u32((clamp_ ? kFlagClamped : 0) | (store_t3 ? kFlagT3 : 0));
+    w.u32(dim_);
+    w.u32(k_);
+    w.u32(n_);
+    w.u32(m_);
+    w.u32((uint32_t)base_count_);
+    w.f32(lo_);
+    w.f32(hi_);
+    w.bytes(model_.centroids.data(), model_.centroids.size() * 4);
+    w.bytes(model_.nbr.data(), model_.nbr.size() * 4);
+    w.bytes(model_.elen.data(), model_.elen.size() * 4);
+    w.bytes(model_.pq.data(), model_.pq.size() * 4);
+    if (store_t3) w.bytes(t3.data(), t3.size() * 4);
+    const size_t ncell = (size_t)k_ * n_;
+    for (size_t c = 0; c < ncell; c++) {
+        const uint64_t b0 = L.off[c], b1 = L.off[c + 1];
+        w.u32((uint32_t)(b1 - b0));
+        w.bytes(L.ids.data() + b0, (b1 - b0) * 4);
+        w.bytes(L.codes.data() + b0 * m_, (b1 - b0) * m_);
+        w.bytes(L.lambdas.data() + b0, b1 - b0);
+    }
+    if (!w.out) throw std::runtime_error("serialize_index: write failed for " + path);
+}
+
+}  // namespace vlq

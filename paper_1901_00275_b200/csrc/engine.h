@@ -1,0 +1,158 @@
+// VLQ-ADC engine: one index (or one shard of it) resident on one B200.
+//
+// Host-side mirror of the reference InvertedIndex (proj/include/vlq/index.hpp:
+// 38-72) with the posting lists flattened into device SoA arrays:
+//   codes[N*m] u8 | lambdas[N] u8 | ids[N] u32 | eterm[N] f32 | list_off[K*n+1] u64
+// (cell = i*n + j, lists concatenated in cell order, ids ascending per list),
+// plus replicated coarse structures (codebook, graph, PQ, t2, t3).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace vlq {
+
+struct EngineConfig {
+    int device = 0;
+    int shard_rank = 0;    // this engine holds regions i with owner(i) == shard_rank
+    int shard_count = 1;
+    uint64_t workspace_bytes = 4ull << 30;  // per-query-tile scratch budget
+    uint32_t max_tile = 16384;
+    int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
+};
+
+// Trained quantizers (a VLQ1 "model": an index with zero points).
+struct HostModel {
+    uint32_t dim = 0, k = 0, n = 0, m = 0;
+    bool clamp = true;
+    float lo = 0.0f, hi = 1.0f;
+    std::vector<float> centroids;  // k*dim
+    std::vector<uint32_t> nbr;     // k*n
+    std::vector<float> elen;       // k*n
+    std::vector<float> pq;         // m*256*(dim/m)
+    std::vector<float> t3;         // k*m*256 or empty (computed)
+};
+
+struct HostLists {
+    std::vector<uint64_t> off;  // k*n+1
+    std::vector<uint32_t> ids;
+    std::vector<uint8_t> codes;
+    std::vector<uint8_t> lambdas;
+    uint64_t base_count = 0;
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count <= n && p) return;
+        reset();
+        if (count == 0) return;
+        CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    T* get() const { return p; }
+};
+
+class Engine {
+public:
+    explicit Engine(const EngineConfig& cfg);
+    ~Engine();
+
+    // model / index management
+    void set_model(const HostModel& m);
+    void load_vlq1(const std::string& path);
+    void save_vlq1(const std::string& path, bool store_t3);
+    bool has_model() const { return model_ok_; }
+    uint32_t dim() const { return dim_; }
+    uint32_t k() const { return k_; }
+    uint32_t n() const { return n_; }
+    uint32_t m() const { return m_; }
+    uint64_t ntotal() const { return base_count_; }
+    uint64_t local_entries() const { return nent_; }
+    bool clamp() const { return clamp_; }
+    float lo() const { return lo_; }
+    float hi() const { return hi_; }
+    int owner(uint32_t region) const { return (int)(region % (uint32_t)cfg_.shard_count); }
+
+    // add (Index.add, proj/python/bindings.cpp:83-97)
+    void add_host(const float* base, uint64_t nb);
+    // streamed add: the source writes points [first, first+count) to a device buffer
+    using ChunkSource = std::function<void(uint64_t first, uint64_t count, float* dst, cudaStream_t st)>;
+    void add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src);
+
+    // search (Index.search, bindings.cpp:99-126): device pointers, async on `st`
+    void search_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
+                       float* d_dists, uint64_t* d_scanned, cudaStream_t st);
+    void search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
+                     float* dists, uint64_t* scanned);
+    void check_device_errors(cudaStream_t st);
+
+    // per-point add-path outputs for parity tests (no index mutation)
+    void encode_host(const float* x, uint64_t nx, uint32_t* cells, float* lambdas, uint8_t* codes,
+                     uint8_t* lam_bytes);
+    void get_lists(HostLists& out);
+    void get_tables(std::vector<float>& t2, std::vector<float>& t3);
+
+    cudaStream_t stream() const { return stream_; }
+    const HostModel& model() const { return model_; }
+
+    // exact brute-force k-NN (dataset.cpp:46-92) on the device
+    static void brute_force_gt(int device, const float* base, uint64_t nb, const float* queries, uint64_t nq,
+                               uint32_t dim, uint32_t k, uint32_t* out);
+
+private:
+    void upload_model();
+    void upload_lists(const HostLists& L);
+    void compute_eterm();
+    AddArgs add_args() const;
+    SearchArgs search_args() const;
+    void search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
+                     float* d_dists, uint64_t* d_scanned, cudaStream_t st);
+
+    EngineConfig cfg_;
+    cudaStream_t stream_ = nullptr;
+    bool model_ok_ = false;
+    uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;
+    bool clamp_ = true;
+    float lo_ = 0.0f, hi_ = 1.0f;
+    uint64_t base_count_ = 0;  // global N (all shards)
+    uint64_t nent_ = 0;        // entries held by this shard
+    float emax_ = 0.0f;
+    HostModel model_;
+
+    DevBuf<float> centroids_, elen_, pq_, t2_, t3_;
+    DevBuf<uint32_t> nbr_;
+    DevBuf<uint64_t> list_off_;
+    DevBuf<uint8_t> codes_, lambdas_;
+    DevBuf<uint32_t> ids_;
+    DevBuf<float> eterm_;
+    DevBuf<unsigned int> err_;  // [0] error flag, [1] emax bits, [2] flagged count, [3..4] minmax
+
+    // search workspace
+    DevBuf<float> ws_, dbuf_, t5_;
+    DevBuf<uint32_t> top_, sel_, qlist_;
+    DevBuf<uint64_t> cand_;
+    DevBuf<QueryMeta> meta_;
+};
+
+uint32_t w2_of(uint32_t w1, float alpha, uint32_t n);
+
+}  // namespace vlq

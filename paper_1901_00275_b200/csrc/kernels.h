@@ -1,0 +1,101 @@
+// Kernel argument structs and launcher declarations shared by the engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace vlq {
+
+struct QueryMeta {
+    unsigned long long scanned;  // reference-semantics scanned candidates (search.cpp:163-165)
+    float dmax;                  // bound on |term1| over the query's selected cells
+    float s5max;                 // bound on |sum5|
+    uint32_t flag;               // 1: certificate failed -> exact fallback
+    uint32_t pad;
+};
+
+// Device views used by the search kernels (all pointers device-resident).
+struct SearchArgs {
+    // index (replicated coarse structures + this shard's posting lists)
+    uint32_t dim, k, n, m;
+    float lo, hi, lam_absmax, emax;
+    const float* centroids;
+    const uint32_t* nbr;
+    const float* elen;
+    const float* pq;
+    const float* t2;
+    const float* t3;
+    const uint64_t* list_off;
+    const uint8_t* codes;
+    const uint8_t* lambdas;
+    const uint32_t* ids;
+    const float* eterm;
+    // per-tile workspace
+    float* ws;        // [T, k] exact centroid distances
+    uint32_t* top;    // [T, w1]
+    float* dbuf;      // [T, w1*n]
+    uint32_t* sel;    // [T, w2] selected cell ids (ascending)
+    float* t5;        // [T, m, 256]
+    uint64_t* cand;   // [T, keep] fast-scan survivors (key = dist | pos)
+    QueryMeta* meta;  // [T]
+    unsigned int* error_flag;
+};
+
+// Add-path device views.
+struct AddArgs {
+    uint32_t dim, k, n, m;
+    int clamp;
+    float lo, hi;
+    const float* centroids;
+    const uint32_t* nbr;
+    const float* elen;
+    const float* pq;
+    const float* t2;
+    const float* t3;
+    unsigned int* error_flag;
+};
+
+void launch_sqdist_matrix(const float* Y, uint64_t ny, const float* C, uint64_t nc, uint32_t dim, float* out,
+                          uint64_t ldo, cudaStream_t st);
+void launch_first_level(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top, cudaStream_t st);
+void launch_second_level(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, cudaStream_t st);
+void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
+                  uint64_t nq, cudaStream_t st);
+size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);
+void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,
+                 bool fast, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st);
+void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
+                    cudaStream_t st);
+void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,
+                       uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d, cudaStream_t st);
+void launch_merge_topk(const int64_t* in_ids, const float* in_d, uint32_t nparts, uint64_t nq, uint32_t topk,
+                       int64_t* out_ids, float* out_d, cudaStream_t st);
+
+// add path
+void launch_tables(const float* centroids, uint32_t k, uint32_t dim, const float* pq, uint32_t m, float* t2,
+                   float* t3, cudaStream_t st);
+void launch_assign_nearest(const AddArgs& a, const float* X, uint64_t nx, uint32_t* best, cudaStream_t st);
+void launch_encode(const AddArgs& a, const float* X, uint64_t nx, const uint32_t* best, int clamp_for_edges,
+                   uint32_t* cell_out, float* lam_out, uint8_t* codes_out, uint8_t* lamb_out, float* eterm_out,
+                   unsigned int* emax_bits, cudaStream_t st);
+void launch_minmax(const float* v, uint64_t n, float* out2, cudaStream_t st);
+void launch_gather_entries(const uint32_t* order, uint64_t n, uint32_t m, uint64_t first_id,
+                           const uint8_t* codes_pt, const uint8_t* lamb_pt, const float* eterm_pt,
+                           uint32_t* ids, uint8_t* codes, uint8_t* lambdas, float* eterm, cudaStream_t st);
+void launch_histogram(const uint32_t* cells, uint64_t n, unsigned long long* counts, cudaStream_t st);
+
+}  // namespace vlq
+
+namespace vlq {
+void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st);
+void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st);
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+void launch_eterm_lists(const AddArgs& a, const uint64_t* list_off, uint32_t ncell, const uint8_t* codes,
+                        const uint8_t* lambdas, uint64_t nent, float* eterm, unsigned int* emax_bits, cudaStream_t st);
+void launch_gt_merge(const float* dist, uint64_t ldd, uint64_t nq, uint32_t k, uint32_t npos,
+                     const uint32_t* sel_pos, uint64_t base_id, uint64_t* running, cudaStream_t st);
+void launch_select_rows(const float* vals, uint64_t ld, uint64_t nrows, uint32_t len, uint32_t L, uint32_t* out,
+                        cudaStream_t st);
+}  // namespace vlq

@@ -1,0 +1,664 @@
+// Search-path kernels (Algorithm 3 of the paper; reference
+// proj/src/search.cpp:11-191).
+//
+//   k_sqdist_matrix     exact centroid distances (first_level_scan :11-36)
+//   k_first_level       top-w1 by (dist, id)
+//   k_second_level      line-subregion distances + top-w2 by (dist, cell)
+//                       (second_level_rank :38-78, line_quant.cpp:9-22)
+//   k_term5             t5 = <y_p, PQ[p][j]> (query_term5 :80-90)
+//   k_scan<...>         fused list scan + warp top-k' (adc_distance :92-120,
+//                       scan loop :154-162, select_topk :122-140)
+//   k_rescore           exact reference-order re-score of the k' survivors,
+//                       final (dist, id) top-k and the certificate that the
+//                       exact top-k is among them
+#include "kernels.h"
+#include "select.cuh"
+
+namespace vlq {
+namespace dev {
+
+// ---------------------------------------------------------------------------
+// Exact squared-distance matrix  out[q*ldo + c] = sqdist(Y[q], C[c]).
+// 64x64 output tile per CTA, 4x4 per thread, D streamed through shared
+// memory in 32-wide slabs.  Each output accumulates d = 0..D-1 in order with
+// __f*_rn, so it is bit-identical to the sequential reference sqdist.
+// ---------------------------------------------------------------------------
+constexpr int SQ_TILE = 64;
+constexpr int SQ_SLAB = 32;
+
+__global__ void __launch_bounds__(256) k_sqdist_matrix(const float* __restrict__ Y, uint64_t ny,
+                                                       const float* __restrict__ C, uint64_t nc,
+                                                       uint32_t dim, float* __restrict__ out,
+                                                       uint64_t ldo) {
+    __shared__ __align__(16) float Ys[SQ_SLAB][SQ_TILE + 4];
+    __shared__ __align__(16) float Cs[SQ_SLAB][SQ_TILE + 4];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t tx = tid & 15u, ty = tid >> 4;
+    const uint64_t q0 = (uint64_t)blockIdx.y * SQ_TILE, c0 = (uint64_t)blockIdx.x * SQ_TILE;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
+    for (uint32_t d0 = 0; d0 < dim; d0 += SQ_SLAB) {
+        const uint32_t dn = min((uint32_t)SQ_SLAB, dim - d0);
+        for (uint32_t e = tid; e < SQ_SLAB * SQ_TILE; e += 256) {
+            uint32_t row = e / SQ_SLAB, dd = e % SQ_SLAB;
+            float yv = 0.0f, cv = 0.0f;
+            if (dd < dn) {
+                if (q0 + row < ny) yv = Y[(q0 + row) * dim + d0 + dd];
+                if (c0 + row < nc) cv = C[(c0 + row) * dim + d0 + dd];
+            }
+            Ys[dd][row] = yv;
+            Cs[dd][row] = cv;
+        }
+        __syncthreads();
+        for (uint32_t dd = 0; dd < dn; dd++) {
+            float4 yv = *reinterpret_cast<const float4*>(&Ys[dd][ty * 4]);
+            float4 cv = *reinterpret_cast<const float4*>(&Cs[dd][tx * 4]);
+            float ya[4] = {yv.x, yv.y, yv.z, yv.w};
+            float ca[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) acc[a][b] = sq_step(acc[a][b], ya[a], ca[b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        uint64_t q = q0 + ty * 4 + a;
+        if (q >= ny) continue;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            uint64_t c = c0 + tx * 4 + b;
+            if (c < nc) out[q * ldo + c] = acc[a][b];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// First level: top-w1 centroids of each query's distance row, ascending ids.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_first_level(const float* __restrict__ ws, uint32_t k,
+                                                     uint32_t w1, uint32_t* __restrict__ top) {
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    const uint64_t q = blockIdx.x;
+    block_select_ordered(ws + q * k, k, w1, top + q * w1, hist, scan);
+}
+
+// ---------------------------------------------------------------------------
+// Second level: line-subregion distances of the w1*n edges, top-w2 by
+// (dist, centroid_id, edge_rank).  `top` is ascending, so edge position
+// r*n + j is ascending in cell id i*n + j and the positional tie-break of
+// block_select_ordered is exactly the reference's.  Also produces, per query,
+// the scanned-candidate count and the |term1| bound of the certificate.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_second_level(SearchArgs a, uint32_t w1, uint32_t w2) {
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    __shared__ unsigned long long s_scanned;
+    __shared__ float s_dmax;
+    const uint64_t q = blockIdx.x;
+    const uint32_t n = a.n;
+    const uint32_t total = w1 * n;
+    const float* wsq = a.ws + q * a.k;
+    const uint32_t* topq = a.top + q * w1;
+    float* dq = a.dbuf + q * (uint64_t)total;
+    if (threadIdx.x == 0) {
+        s_scanned = 0;
+        s_dmax = 0.0f;
+    }
+    for (uint32_t e = threadIdx.x; e < total; e += blockDim.x) {
+        uint32_t i = topq[e / n], j = e % n;
+        float av = wsq[i];
+        float bv = wsq[a.nbr[(uint64_t)i * n + j]];
+        float cv = a.elen[(uint64_t)i * n + j];
+        if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
+        float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
+        dq[e] = line_sqdist(av, bv, cv, lam);
+    }
+    __syncthreads();
+    uint32_t* selq = a.sel + q * w2;
+    block_select_ordered(dq, total, w2, selq, hist, scan);
+    __syncthreads();
+    // positions -> cell ids; scanned count; |d| bound for the certificate
+    const float lmax = a.lam_absmax;  // max |lambda| over dequantized values
+    unsigned long long cnt = 0;
+    float dmax = 0.0f;
+    for (uint32_t t = threadIdx.x; t < w2; t += blockDim.x) {
+        uint32_t e = selq[t];
+        uint32_t i = topq[e / n], j = e % n;
+        uint32_t cell = i * n + j;
+        selq[t] = cell;
+        cnt += a.list_off[cell + 1] - a.list_off[cell];
+        float av = wsq[i], bv = wsq[a.nbr[cell]], cv = a.elen[cell];
+        // |(1-l)a + (l^2-l)c + l b| <= (1+L)a + (L^2+L)c + L b for |l| <= L
+        float bound = (1.0f + lmax) * fabsf(av) + (lmax * lmax + lmax) * fabsf(cv) + lmax * fabsf(bv);
+        dmax = fmaxf(dmax, bound);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_scanned, cnt);
+        atomicMax(reinterpret_cast<unsigned int*>(&s_dmax), __float_as_uint(dmax));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.meta[q].scanned = s_scanned;
+        a.meta[q].dmax = s_dmax;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// term5 table (query_term5): t5[q][p][j] = dot(y_p, PQ[p][j]) in order; also
+// S5max = sum_p max_j |t5| for the certificate.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_term5(const float* __restrict__ Y, const float* __restrict__ pq,
+                                               uint32_t dim, uint32_t m, float* __restrict__ t5,
+                                               QueryMeta* __restrict__ meta) {
+    extern __shared__ float ys[];
+    __shared__ float s_max[32];
+    const uint64_t q = blockIdx.x;
+    const uint32_t dsub = dim / m;
+    for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
+    __syncthreads();
+    float s5 = 0.0f;
+    for (uint32_t p = 0; p < m; p++) {
+        float mx = 0.0f;
+        for (uint32_t j = threadIdx.x; j < VLQ_KSUB; j += blockDim.x) {
+            const float* c = pq + ((uint64_t)p * VLQ_KSUB + j) * dsub;
+            float acc = 0.0f;
+            for (uint32_t t = 0; t < dsub; t++) acc = dot_step(acc, ys[p * dsub + t], c[t]);
+            t5[(q * m + p) * VLQ_KSUB + j] = acc;
+            mx = fmaxf(mx, fabsf(acc));
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float v = 0.0f;
+            for (uint32_t w = 0; w < (blockDim.x + 31) / 32; w++) v = fmaxf(v, s_max[w]);
+            s5 += v;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) meta[q].s5max = s5;
+}
+
+// ---------------------------------------------------------------------------
+// Fused list scan.  One CTA per query, warps take the query's selected
+// cells round-robin, lanes take consecutive posting entries (coalesced code /
+// lambda / e loads).  Per entry:
+//   kFast:  dist = (term1 + e) - 2*sum5   with e = sum2 + 2(1-l)sum3 + 2l sum4
+//           precomputed at add time (query independent); key = (dist, pos)
+//   exact:  the reference's adc_distance op-for-op; key = (dist, id)
+// Every warp keeps its kKeep smallest keys in a shared buffer (threshold
+// insert + bitonic flush); warps share the best threshold seen so far (the
+// min over warps of their kKeep-th key bounds the block's kKeep-th key).
+// The warps' survivors are block-merged and the kKeep smallest written out.
+// ---------------------------------------------------------------------------
+template <int M>
+__device__ __forceinline__ void load_code(const uint8_t* __restrict__ codes, uint64_t e, uint32_t m,
+                                          uint8_t* out) {
+    if constexpr (M == 16) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(codes + e * 16));
+        *reinterpret_cast<uint4*>(out) = v;
+    } else if constexpr (M == 8) {
+        uint2 v = __ldg(reinterpret_cast<const uint2*>(codes + e * 8));
+        *reinterpret_cast<uint2*>(out) = v;
+    } else if constexpr (M == 4) {
+        uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(codes + e * 4));
+        *reinterpret_cast<uint32_t*>(out) = v;
+    } else {
+        for (uint32_t p = 0; p < m; p++) out[p] = __ldg(codes + e * m + p);
+    }
+}
+
+struct ScanShared {
+    unsigned long long tau;  // shared threshold (min over warps)
+};
+
+template <int M, bool kFast>
+__global__ void __launch_bounds__(256) k_scan(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t buf,
+                                              const uint32_t* __restrict__ qlist,
+                                              const unsigned int* __restrict__ qcount) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (qcount && blockIdx.x >= *qcount) return;
+    const uint32_t m = (M > 0) ? (uint32_t)M : a.m;
+    const uint32_t nwarps = blockDim.x >> 5;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t q = qlist ? qlist[blockIdx.x] : blockIdx.x;
+    float* lut = reinterpret_cast<float*>(smem);                        // m*256
+    uint64_t* bufs = reinterpret_cast<uint64_t*>(smem + (size_t)m * VLQ_KSUB * 4);  // nwarps*buf
+    __shared__ unsigned long long s_tau;
+    uint64_t* wbuf = bufs + (size_t)warp * buf;
+
+    const float* t5q = a.t5 + q * m * VLQ_KSUB;
+    for (uint32_t i = threadIdx.x; i < m * VLQ_KSUB; i += blockDim.x) lut[i] = t5q[i];
+    for (uint32_t i = threadIdx.x; i < nwarps * buf; i += blockDim.x) bufs[i] = ~0ull;
+    if (threadIdx.x == 0) s_tau = ~0ull;
+    __syncthreads();
+
+    const float* wsq = a.ws + q * a.k;
+    const uint32_t* selq = a.sel + q * w2;
+    const float lo = a.lo, hi = a.hi;
+    uint32_t cnt = 0;
+    uint64_t tau = ~0ull;
+
+    auto flush = [&]() {
+        // sort the warp buffer, keep the `keep` smallest, update thresholds
+        for (uint32_t i = cnt + lane; i < buf; i += 32) wbuf[i] = ~0ull;
+        __syncwarp();
+        bitonic_sort_u64<true>(wbuf, buf, lane, 32);
+        cnt = min(cnt, keep);
+        if (cnt == keep) {
+            uint64_t t = wbuf[keep - 1];
+            if (t < tau) tau = t;
+            if (lane == 0) atomicMin(&s_tau, (unsigned long long)t);
+        }
+        __syncwarp();
+    };
+
+    for (uint32_t ci = warp; ci < w2; ci += nwarps) {
+        const uint32_t cell = selq[ci];
+        const uint64_t b0 = a.list_off[cell], b1 = a.list_off[cell + 1];
+        if (b0 == b1) continue;
+        const uint32_t i = cell / a.n;
+        const uint32_t s = a.nbr[cell];
+        const float av = wsq[i], bv = wsq[s], cv = a.elen[cell];
+        const float* t3i = a.t3 + (uint64_t)i * m * VLQ_KSUB;
+        const float* t3s = a.t3 + (uint64_t)s * m * VLQ_KSUB;
+        for (uint64_t e0 = b0; e0 < b1; e0 += 32) {
+            const uint64_t e = e0 + lane;
+            uint64_t key = ~0ull;
+            if (e < b1) {
+                uint8_t code[(M > 0) ? M : 128];
+                load_code<M>(a.codes, e, m, code);
+                const uint32_t lb = __ldg(a.lambdas + e);
+                const float lam = dequantize_lambda(lb, lo, hi);
+                const float d = line_sqdist(av, bv, cv, lam);
+                if constexpr (kFast) {
+                    float sum5 = 0.0f;
+#pragma unroll
+                    for (uint32_t p = 0; p < ((M > 0) ? (uint32_t)M : m); p++)
+                        sum5 = __fadd_rn(sum5, lut[p * VLQ_KSUB + code[p]]);
+                    const float et = __ldg(a.eterm + e);
+                    const float dist = __fsub_rn(__fadd_rn(d, et), __fmul_rn(2.0f, sum5));
+                    key = make_key(dist, (uint32_t)e);
+                } else {
+                    float s2 = 0.0f, s3 = 0.0f, s4 = 0.0f, s5 = 0.0f;
+                    for (uint32_t p = 0; p < m; p++) {
+                        const uint32_t c = code[p];
+                        s2 = __fadd_rn(s2, __ldg(a.t2 + p * VLQ_KSUB + c));
+                        s3 = __fadd_rn(s3, __ldg(t3i + p * VLQ_KSUB + c));
+                        s4 = __fadd_rn(s4, __ldg(t3s + p * VLQ_KSUB + c));
+                        s5 = __fadd_rn(s5, lut[p * VLQ_KSUB + c]);
+                    }
+                    float r = __fadd_rn(d, s2);
+                    r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, __fsub_rn(1.0f, lam)), s3));
+                    r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, lam), s4));
+                    r = __fsub_rn(r, __fmul_rn(2.0f, s5));
+                    key = make_key(r, __ldg(a.ids + e));
+                }
+            }
+            const uint64_t shared_tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
+            const uint64_t th = tau < shared_tau ? tau : shared_tau;
+            const bool take = key < th;
+            const uint32_t bal = __ballot_sync(0xffffffffu, take);
+            if (bal) {
+                if (take) wbuf[cnt + __popc(bal & ((1u << lane) - 1u))] = key;
+                cnt += __popc(bal);
+                __syncwarp();
+                if (cnt > buf - 32) flush();
+            }
+        }
+    }
+    flush();
+    __syncthreads();
+    // block merge: every warp buffer now holds its sorted survivors then +inf
+    const uint32_t total = nwarps * buf;
+    bitonic_sort_u64<false>(bufs, total, threadIdx.x, blockDim.x);
+    uint64_t* candq = a.cand + q * keep;
+    for (uint32_t t = threadIdx.x; t < keep; t += blockDim.x) candq[t] = bufs[t];
+}
+
+// ---------------------------------------------------------------------------
+// Exact re-score of the fast-scan survivors (adc_distance op-for-op on the
+// global t2/t3/t5 tables), final (dist, id) top-k, padding, and the
+// certificate: with eps bounding |fast - exact| for every scanned entry,
+// fast_k' - eps > exact_k proves that no dropped entry can enter the top-k.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t find_cell(const uint64_t* __restrict__ off, uint32_t ncell,
+                                              uint64_t pos) {
+    // largest c with off[c] <= pos (and off[c+1] > pos)
+    uint32_t lo = 0, hi = ncell;  // invariant: off[lo] <= pos < off[hi]
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (off[mid] <= pos) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, uint32_t topk,
+                                                 int64_t* __restrict__ out_ids, float* __restrict__ out_d) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // keep (power of two)
+    __shared__ float s_fast_last;
+    const uint64_t q = blockIdx.x;
+    const uint32_t m = a.m;
+    const uint64_t* candq = a.cand + q * keep;
+    const float* wsq = a.ws + q * a.k;
+    const float* t5q = a.t5 + q * m * VLQ_KSUB;
+    const uint64_t scanned = a.meta[q].scanned;
+    const uint32_t have = (uint32_t)dev::umin64(scanned, keep);
+    const uint32_t ncell = a.k * a.n;
+    for (uint32_t t = threadIdx.x; t < keep; t += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (t < have) {
+            const uint64_t ck = candq[t];
+            const uint64_t pos = (uint32_t)ck;
+            const uint32_t cell = find_cell(a.list_off, ncell, pos);
+            const uint32_t i = cell / a.n;
+            const uint32_t s = a.nbr[cell];
+            const float lam = dequantize_lambda(a.lambdas[pos], a.lo, a.hi);
+            const float d = line_sqdist(wsq[i], wsq[s], a.elen[cell], lam);
+            const uint8_t* code = a.codes + pos * m;
+            const float* t3i = a.t3 + (uint64_t)i * m * VLQ_KSUB;
+            const float* t3s = a.t3 + (uint64_t)s * m * VLQ_KSUB;
+            float s2 = 0.0f, s3 = 0.0f, s4 = 0.0f, s5 = 0.0f;
+            for (uint32_t p = 0; p < m; p++) {
+                const uint32_t c = code[p];
+                s2 = __fadd_rn(s2, a.t2[p * VLQ_KSUB + c]);
+                s3 = __fadd_rn(s3, t3i[p * VLQ_KSUB + c]);
+                s4 = __fadd_rn(s4, t3s[p * VLQ_KSUB + c]);
+                s5 = __fadd_rn(s5, t5q[p * VLQ_KSUB + c]);
+            }
+            float r = __fadd_rn(d, s2);
+            r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, __fsub_rn(1.0f, lam)), s3));
+            r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, lam), s4));
+            r = __fsub_rn(r, __fmul_rn(2.0f, s5));
+            key = make_key(r, a.ids[pos]);
+            if (t == have - 1) s_fast_last = unord_float((uint32_t)(ck >> 32));
+        }
+        keys[t] = key;
+    }
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, keep, threadIdx.x, blockDim.x);
+    for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) {
+        if (t < have) {
+            out_ids[q * topk + t] = (int64_t)(uint32_t)keys[t];
+            out_d[q * topk + t] = unord_float((uint32_t)(keys[t] >> 32));
+        } else {
+            out_ids[q * topk + t] = -1;
+            out_d[q * topk + t] = __int_as_float(0x7f800000);
+        }
+    }
+    if (threadIdx.x == 0) {
+        uint32_t flag = 0;
+        if (scanned > keep && topk > 0) {
+            // every scanned entry x satisfies |fast_x - exact_x| <= eps
+            const QueryMeta mt = a.meta[q];
+            const double u = 5.9604644775390625e-08;  // 2^-24
+            const double eps = 1.25 * u * (8.0 * ((double)mt.dmax + (double)a.emax) + 4.0 * (double)mt.s5max) + 1e-30;
+            const double exact_k = (double)unord_float((uint32_t)(keys[topk - 1] >> 32));
+            const double fast_last = (double)s_fast_last;
+            if (!(fast_last - eps > exact_k)) flag = 1;
+        }
+        a.meta[q].flag = flag;
+    }
+}
+
+}  // namespace dev
+}  // namespace vlq
+
+// ---------------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------------
+namespace vlq {
+
+void launch_sqdist_matrix(const float* Y, uint64_t ny, const float* C, uint64_t nc, uint32_t dim, float* out,
+                          uint64_t ldo, cudaStream_t st) {
+    if (ny == 0 || nc == 0) return;
+    dim3 grid((unsigned)((nc + dev::SQ_TILE - 1) / dev::SQ_TILE), (unsigned)((ny + dev::SQ_TILE - 1) / dev::SQ_TILE));
+    dev::k_sqdist_matrix<<<grid, 256, 0, st>>>(Y, ny, C, nc, dim, out, ldo);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_first_level(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top, cudaStream_t st) {
+    dev::k_first_level<<<(unsigned)nq, 512, 0, st>>>(ws, k, w1, top);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_second_level(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, cudaStream_t st) {
+    dev::k_second_level<<<(unsigned)nq, 512, 0, st>>>(a, w1, w2);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
+                  uint64_t nq, cudaStream_t st) {
+    dev::k_term5<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(Y, pq, dim, m, t5, meta);
+    CUDA_LAUNCH_CHECK();
+}
+
+size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf) {
+    return (size_t)m * VLQ_KSUB * 4 + (size_t)nwarps * buf * 8;
+}
+
+template <int M, bool kFast>
+static void launch_scan_t(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf,
+                          uint32_t nwarps, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st) {
+    size_t smem = scan_smem_bytes(a.m, nwarps, buf);
+    auto fn = dev::k_scan<M, kFast>;
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)nblocks, nwarps * 32, smem, st>>>(a, w2, keep, buf, qlist, qcount);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,
+                 bool fast, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st) {
+    if (fast) {
+        switch (a.m) {
+            case 16: launch_scan_t<16, true>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+            case 8: launch_scan_t<8, true>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+            case 4: launch_scan_t<4, true>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+            default: launch_scan_t<0, true>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+        }
+    } else {
+        switch (a.m) {
+            case 16: launch_scan_t<16, false>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+            case 8: launch_scan_t<8, false>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+            case 4: launch_scan_t<4, false>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+            default: launch_scan_t<0, false>(a, nblocks, w2, keep, buf, nwarps, qlist, qcount, st); break;
+        }
+    }
+}
+
+void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
+                    cudaStream_t st) {
+    dev::k_rescore<<<(unsigned)nq, 256, keep * sizeof(uint64_t), st>>>(a, keep, topk, out_ids, out_d);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq
+
+// ---------------------------------------------------------------------------
+// Exact-fallback emit and the cross-shard (dist, id) merge (K9).
+// ---------------------------------------------------------------------------
+namespace vlq {
+namespace dev {
+
+__global__ void k_emit_exact(SearchArgs a, const uint32_t* __restrict__ qlist, const unsigned int* __restrict__ qcount,
+                             uint32_t keep, uint32_t topk, int64_t* __restrict__ out_ids, float* __restrict__ out_d) {
+    if (qcount && blockIdx.x >= *qcount) return;
+    const uint64_t q = qlist ? qlist[blockIdx.x] : blockIdx.x;
+    const uint64_t have = dev::umin64(a.meta[q].scanned, keep);
+    const uint64_t* candq = a.cand + q * keep;
+    for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) {
+        if (t < have) {
+            out_ids[q * topk + t] = (int64_t)(uint32_t)candq[t];
+            out_d[q * topk + t] = unord_float((uint32_t)(candq[t] >> 32));
+        } else {
+            out_ids[q * topk + t] = -1;
+            out_d[q * topk + t] = __int_as_float(0x7f800000);
+        }
+    }
+}
+
+// Merges nparts per-shard top-k rows (each ascending by (dist, id), padded
+// with -1/+inf) into the global top-k under the same total order.
+__global__ void k_merge_topk(const int64_t* __restrict__ in_ids, const float* __restrict__ in_d, uint32_t nparts,
+                             uint64_t nq, uint32_t topk, uint32_t npow2, int64_t* __restrict__ out_ids,
+                             float* __restrict__ out_d) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+    const uint64_t q = blockIdx.x;
+    for (uint32_t t = threadIdx.x; t < npow2; t += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (t < nparts * topk) {
+            const uint32_t part = t / topk, r = t % topk;
+            const uint64_t src = ((uint64_t)part * nq + q) * topk + r;
+            const int64_t id = in_ids[src];
+            if (id >= 0) key = make_key(in_d[src], (uint32_t)id);
+        }
+        keys[t] = key;
+    }
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, npow2, threadIdx.x, blockDim.x);
+    for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) {
+        const uint64_t key = keys[t];
+        if (key != ~0ull) {
+            out_ids[q * topk + t] = (int64_t)(uint32_t)key;
+            out_d[q * topk + t] = unord_float((uint32_t)(key >> 32));
+        } else {
+            out_ids[q * topk + t] = -1;
+            out_d[q * topk + t] = __int_as_float(0x7f800000);
+        }
+    }
+}
+
+}  // namespace dev
+
+void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,
+                       uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d, cudaStream_t st) {
+    if (nblocks == 0) return;
+    dev::k_emit_exact<<<(unsigned)nblocks, 128, 0, st>>>(a, qlist, qcount, keep, topk, out_ids, out_d);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_merge_topk(const int64_t* in_ids, const float* in_d, uint32_t nparts, uint64_t nq, uint32_t topk,
+                       int64_t* out_ids, float* out_d, cudaStream_t st) {
+    if (nq == 0 || topk == 0) return;
+    uint32_t n = 1;
+    while (n < nparts * topk) n <<= 1;
+    size_t smem = (size_t)n * 8;
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_merge_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_merge_topk<<<(unsigned)nq, 256, smem, st>>>(in_ids, in_d, nparts, nq, topk, n, out_ids, out_d);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq
+
+// ---------------------------------------------------------------------------
+// small helpers: flagged-query compaction and per-query scanned counts
+// ---------------------------------------------------------------------------
+namespace vlq {
+namespace dev {
+
+__global__ void k_compact_flags(const QueryMeta* __restrict__ meta, uint64_t nq, uint32_t* __restrict__ qlist,
+                                unsigned int* __restrict__ count) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x)
+        if (meta[q].flag) qlist[atomicAdd(count, 1u)] = (uint32_t)q;
+}
+
+__global__ void k_copy_scanned(const QueryMeta* __restrict__ meta, uint64_t nq, uint64_t* __restrict__ out) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x)
+        out[q] = meta[q].scanned;
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+
+}  // namespace dev
+
+void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st) {
+    dev::k_compact_flags<<<(unsigned)dev::umin64((nq + 255) / 256, 1184), 256, 0, st>>>(meta, nq, qlist, count);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st) {
+    dev::k_copy_scanned<<<(unsigned)dev::umin64((nq + 255) / 256, 1184), 256, 0, st>>>(meta, nq, out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {
+    if (n == 0) return;
+    dev::k_iota<<<(unsigned)dev::umin64((n + 255) / 256, 4736), 256, 0, st>>>(v, n);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq
+
+// ---------------------------------------------------------------------------
+// brute-force ground truth helpers (dataset.cpp:46-92): per-row ordered
+// selection and a (dist, id) merge into each query's running top-k.
+// ---------------------------------------------------------------------------
+namespace vlq {
+namespace dev {
+
+__global__ void __launch_bounds__(512) k_select_rows(const float* __restrict__ vals, uint64_t ld, uint32_t len,
+                                                     uint32_t L, uint32_t* __restrict__ out) {
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    const uint64_t r = blockIdx.x;
+    block_select_ordered(vals + r * ld, len, L, out + r * L, hist, scan);
+}
+
+__global__ void k_gt_merge(const float* __restrict__ dist, uint64_t ldd, uint32_t k, uint32_t npos,
+                           const uint32_t* __restrict__ sel_pos, uint64_t base_id, uint64_t* __restrict__ running,
+                           uint32_t npow2) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+    const uint64_t q = blockIdx.x;
+    const uint32_t L = min(k, npos);
+    for (uint32_t t = threadIdx.x; t < npow2; t += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (t < k) key = running[q * k + t];
+        else if (t < k + L) {
+            const uint32_t pos = sel_pos[q * L + (t - k)];
+            key = make_key(dist[q * ldd + pos], (uint32_t)(base_id + pos));
+        }
+        keys[t] = key;
+    }
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, npow2, threadIdx.x, blockDim.x);
+    for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) running[q * k + t] = keys[t];
+}
+
+}  // namespace dev
+
+void launch_select_rows(const float* vals, uint64_t ld, uint64_t nrows, uint32_t len, uint32_t L, uint32_t* out,
+                        cudaStream_t st) {
+    if (nrows == 0) return;
+    dev::k_select_rows<<<(unsigned)nrows, 512, 0, st>>>(vals, ld, len, L, out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_gt_merge(const float* dist, uint64_t ldd, uint64_t nq, uint32_t k, uint32_t npos, const uint32_t* sel_pos,
+                     uint64_t base_id, uint64_t* running, cudaStream_t st) {
+    if (nq == 0) return;
+    uint32_t n = 1;
+    while (n < 2 * k) n <<= 1;
+    size_t smem = (size_t)n * 8;
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_gt_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_gt_merge<<<(unsigned)nq, 256, smem, st>>>(dist, ldd, k, npos, sel_pos, base_id, running, n);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq

@@ -1,0 +1,132 @@
+// Block- and warp-level selection primitives (top-L smallest under the
+// reference's total orders).
+#pragma once
+
+#include "common.cuh"
+
+namespace vlq {
+namespace dev {
+
+// Block-wide exclusive scan of a packed u32 (two 16-bit counters).  Returns
+// the exclusive prefix for this thread; *total receives the block total.
+// `ws` must hold >= 33 u32 of shared scratch.  All threads must call.
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* ws, uint32_t* total) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t nwarps = (blockDim.x + 31u) >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < nwarps ? ws[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= (uint32_t)o) w += y;
+        }
+        if (lane < nwarps) ws[lane] = w;  // inclusive per-warp totals
+        if (lane == nwarps - 1) ws[32] = w;
+    }
+    __syncthreads();
+    uint32_t excl = x - v + (warp ? ws[warp - 1] : 0u);
+    *total = ws[32];
+    __syncthreads();
+    return excl;
+}
+
+// Selects the L smallest of vals[0..len) under the order (value, position)
+// -- the reference's (dist, id) comparator when position == id
+// (proj/src/search.cpp:28-33) -- and writes their positions to out[0..L) in
+// ASCENDING position order.  Radix select on the order-preserving u32 key in
+// three digit passes (11/11/10 bits), then one ordered collection pass that
+// keeps every key < T and the first r keys == T in position order.
+// Shared scratch: hist[2048] + scan[40].  All threads of the block call.
+__device__ void block_select_ordered(const float* __restrict__ vals, uint32_t len, uint32_t L,
+                                     uint32_t* __restrict__ out, uint32_t* hist, uint32_t* scan) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    if (L >= len) {
+        for (uint32_t i = tid; i < len; i += nt) out[i] = i;
+        return;
+    }
+    uint32_t prefix = 0, pmask = 0, remaining = L;  // remaining: 1-based rank inside the prefix group
+    const int shifts[3] = {21, 10, 0};
+    const int widths[3] = {11, 11, 10};
+    for (int pass = 0; pass < 3; pass++) {
+        const int sh = shifts[pass];
+        const uint32_t nb = 1u << widths[pass], dmask = nb - 1u;
+        for (uint32_t b = tid; b < nb; b += nt) hist[b] = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < len; i += nt) {
+            uint32_t k = ord_float(vals[i]);
+            if ((k & pmask) == prefix) atomicAdd(&hist[(k >> sh) & dmask], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of the histogram, 'per' bins per thread
+        const uint32_t per = (nb + nt - 1) / nt;
+        uint32_t local = 0;
+        for (uint32_t b = tid * per; b < min(nb, (tid + 1) * per); b++) local += hist[b];
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, scan, &total);
+        // the bin where the cumulative count crosses `remaining`
+        for (uint32_t b = tid * per; b < min(nb, (tid + 1) * per); b++) {
+            uint32_t h = hist[b];
+            if (run < remaining && remaining <= run + h) {
+                scan[34] = b;
+                scan[35] = run;
+            }
+            run += h;
+        }
+        __syncthreads();
+        const uint32_t bsel = scan[34];
+        remaining -= scan[35];
+        prefix |= bsel << sh;
+        pmask |= dmask << sh;
+        __syncthreads();
+    }
+    const uint32_t T = prefix;  // exact key of the L-th smallest value
+    const uint32_t r = remaining;  // how many keys == T to take (in position order)
+    uint32_t lt_run = 0, eq_run = 0;
+    for (uint32_t base = 0; base < len; base += nt) {
+        uint32_t i = base + tid;
+        uint32_t k = i < len ? ord_float(vals[i]) : 0xffffffffu;
+        uint32_t lt = (i < len && k < T) ? 1u : 0u;
+        uint32_t eq = (i < len && k == T) ? 1u : 0u;
+        uint32_t total;
+        uint32_t ex = block_excl_scan_u32(lt | (eq << 16), scan, &total);
+        uint32_t lt_before = lt_run + (ex & 0xffffu);
+        uint32_t eq_before = eq_run + (ex >> 16);
+        if (lt || (eq && eq_before < r)) out[lt_before + min(eq_before, r)] = i;
+        lt_run += total & 0xffffu;
+        eq_run += total >> 16;
+    }
+}
+
+// In-shared-memory bitonic sort (ascending) of n = power of two u64 keys by
+// the calling threads [t0, t0+nthreads).  `sync` is either a warp or block
+// barrier supplied by the caller through the template parameter.
+template <bool kWarpOnly>
+__device__ __forceinline__ void bitonic_sort_u64(uint64_t* a, uint32_t n, uint32_t t, uint32_t nthreads) {
+    for (uint32_t size = 2; size <= n; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t p = t; p < (n >> 1); p += nthreads) {
+                uint32_t lo = 2 * p - (p & (stride - 1));
+                uint32_t hi = lo + stride;
+                bool up = ((lo & size) == 0);
+                uint64_t x = a[lo], y = a[hi];
+                if ((x > y) == up) {
+                    a[lo] = y;
+                    a[hi] = x;
+                }
+            }
+            if (kWarpOnly) __syncwarp();
+            else __syncthreads();
+        }
+    }
+}
+
+}  // namespace dev
+}  // namespace vlq

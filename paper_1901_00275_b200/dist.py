@@ -1,0 +1,76 @@
+"""Multi-GPU search: posting lists sharded by first-level region across the GPUs
+of one box (one process per GPU), coarse quantizer replicated, per-shard
+top-k merged by (dist, id) (the paper's "split the index into b parts, search
+locally, join").
+
+Each rank's engine holds regions i with i % world_size == rank.  A query batch
+is searched on every rank against its shard; the local exact top-k rows are
+exchanged with one NCCL all-gather and merged by the K9 kernel
+(vlq_merge_topk_device).  Because every shard returns its exact local top-k
+under the reference's total order, the merge is exactly the single-engine
+answer regardless of shard order.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+
+
+def merge_topk(ids, dists, stream: int | None = None):
+    """ids int64 [G, nq, k], dists float32 [G, nq, k] (CUDA tensors) -> the
+    merged (nq, k) top-k under (dist, id)."""
+    import torch
+    G, nq, k = ids.shape
+    ids = ids.contiguous()
+    dists = dists.contiguous()
+    out_i = torch.empty((nq, k), dtype=torch.int64, device=ids.device)
+    out_d = torch.empty((nq, k), dtype=torch.float32, device=ids.device)
+    st = torch.cuda.current_stream(ids.device).cuda_stream if stream is None else stream
+    _lib.check(_lib.lib().vlq_merge_topk_device(ids.device.index, ctypes.c_void_p(ids.data_ptr()),
+                                                ctypes.c_void_p(dists.data_ptr()), G, nq, k,
+                                                ctypes.c_void_p(out_i.data_ptr()), ctypes.c_void_p(out_d.data_ptr()),
+                                                ctypes.c_void_p(st)))
+    return out_i, out_d
+
+
+def gather_parts(local_ids, local_dists, group=None):
+    """All-gathers every rank's [nq, k] result block into [world, nq, k]."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    gi = torch.empty((world,) + tuple(local_ids.shape), dtype=local_ids.dtype, device=local_ids.device)
+    gd = torch.empty((world,) + tuple(local_dists.shape), dtype=local_dists.dtype, device=local_dists.device)
+    dist.all_gather_into_tensor(gi, local_ids.contiguous(), group=group)
+    dist.all_gather_into_tensor(gd, local_dists.contiguous(), group=group)
+    return gi, gd
+
+
+class ShardedIndex:
+    """One rank's shard of a VLQ1 index plus the collective search."""
+
+    def __init__(self, index, group=None):
+        self.index = index
+        self.group = group
+
+    @classmethod
+    def load(cls, path: str, rank: int, world: int, device: int, group=None, **kw):
+        from .vlqadc import Index
+        return cls(Index.load(path, device=device, shard_rank=rank, shard_count=world, **kw), group)
+
+    def search_device(self, d_queries, w1: int, alpha: float, k: int):
+        """d_queries: CUDA float32 [nq, dim] tensor (same batch on every rank).
+        Returns the merged (ids, dists) CUDA tensors and the local scanned
+        counts."""
+        import torch
+        nq = d_queries.shape[0]
+        dev = d_queries.device
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        scanned = torch.empty((nq,), dtype=torch.int64, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        self.index.search_device(d_queries.data_ptr(), nq, w1, alpha, k, ids.data_ptr(), dists.data_ptr(),
+                                 scanned.data_ptr(), st)
+        gi, gd = gather_parts(ids, dists, self.group)
+        mi, md = merge_topk(gi, gd, st)
+        return mi, md, scanned

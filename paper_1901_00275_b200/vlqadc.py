@@ -1,0 +1,298 @@
+"""Drop-in ``vlqadc`` module backed by the B200 engine.
+
+Mirrors the reference Python surface (/root/reference/proj/python/bindings.cpp
+:143-233, re-exported by python/vlqadc/__init__.py:8-24):
+
+    Index.train / Index.load / index.add / index.search / index.save
+    index.k, .n, .m, .dim, .ntotal
+    gen_synthetic, brute_force_gt, read_vecs, write_vecs, set_max_threads
+
+Argument names, defaults, return shapes/dtypes, padding (-1 / +inf) and the
+error texts (raised as RuntimeError) follow the reference.  Everything that
+computes runs in libvlqgpu.so on the GPU; there is no CPU fallback.
+
+Extensions beyond the reference API (for sharding, benchmarks and parity
+tests) are keyword-only or separately named: ``Index.from_model``,
+``Index.search_device``, ``Index.encode``, ``Index.lists``,
+``shard_rank/shard_count`` and ``device`` on the constructors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+
+import numpy as np
+
+from . import _lib
+
+KSUB = 256
+
+
+def _default_device() -> int:
+    for var in ("VLQ_DEVICE", "LOCAL_RANK"):
+        if var in os.environ:
+            return int(os.environ[var])
+    return 0
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _to_vecset(arr) -> np.ndarray:
+    """to_vecset + VectorSet::validate (bindings.cpp:23-31, vecset.cpp:8-20)."""
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    if a.ndim != 2:
+        raise RuntimeError("expected a 2-D float array")
+    if a.size and not np.isfinite(a).all():
+        raise RuntimeError("VectorSet: non-finite value")
+    return a
+
+
+class Index:
+    """Two-level (vector + line quantization) inverted index on one B200."""
+
+    def __init__(self, *, device: int | None = None, shard_rank: int = 0, shard_count: int = 1,
+                 workspace_bytes: int = 0, max_tile: int = 0, force_exact: bool = False):
+        L = _lib.lib()
+        cfg = _lib.VlqConfig(_default_device() if device is None else device, shard_rank, shard_count,
+                             workspace_bytes, max_tile, int(force_exact))
+        h = ctypes.c_void_p()
+        _lib.check(L.vlq_engine_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self._device = cfg.device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().vlq_engine_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---- construction -------------------------------------------------------
+    @staticmethod
+    def train(train, k: int = 1024, n: int = 16, m: int = 8, iters: int = 10, seed: int = 42,
+              clamp_lambda: bool = True, **engine_kw) -> "Index":
+        """Index.train (bindings.cpp:44-81) -- trains on the GPU (see train.py)."""
+        from .train import train_model
+        t = _to_vecset(train)
+        model = train_model(t, k, n, m, iters, seed, clamp_lambda, device=engine_kw.get("device"))
+        return Index.from_model(**model, **engine_kw)
+
+    @staticmethod
+    def load(path: str, **engine_kw) -> "Index":
+        """Index.load: VLQ1 deserialize_index (index_io.cpp:100-159)."""
+        idx = Index(**engine_kw)
+        _lib.check(_lib.lib().vlq_engine_load_vlq1(idx._h, os.fsencode(str(path))))
+        return idx
+
+    @staticmethod
+    def from_model(dim: int, k: int, n: int, m: int, clamp: bool, lo: float, hi: float, centroids, nbr, elen, pq,
+                   t3=None, **engine_kw) -> "Index":
+        """An empty index over trained quantizers (a VLQ1 'model')."""
+        idx = Index(**engine_kw)
+        cent = np.ascontiguousarray(centroids, np.float32)
+        nb = np.ascontiguousarray(nbr, np.uint32)
+        el = np.ascontiguousarray(elen, np.float32)
+        pqa = np.ascontiguousarray(pq, np.float32)
+        t3a = None if t3 is None else np.ascontiguousarray(t3, np.float32)
+        _lib.check(_lib.lib().vlq_engine_set_model(idx._h, dim, k, n, m, int(clamp), lo, hi, _p(cent), _p(nb),
+                                                   _p(el), _p(pqa), _p(t3a)))
+        return idx
+
+    # ---- the reference API --------------------------------------------------
+    def add(self, base) -> None:
+        """Index.add (bindings.cpp:83-97): ids are the row numbers."""
+        b = _to_vecset(base)
+        _lib.check(_lib.lib().vlq_engine_add(self._h, _p(b), b.shape[0], b.shape[1] if b.shape[0] else self.dim))
+
+    def search(self, queries, w1: int = 64, alpha: float = 0.25, k: int = 10, *, return_scanned: bool = False):
+        """Index.search (bindings.cpp:99-126) -> (ids int64[nq,k], dists float32[nq,k])."""
+        q = _to_vecset(queries)
+        nq = q.shape[0]
+        ids = np.empty((nq, k), np.int64)
+        dists = np.empty((nq, k), np.float32)
+        scanned = np.zeros(nq, np.uint64)
+        dim = q.shape[1] if q.size else self.dim
+        if q.shape[1] != self.dim:
+            raise RuntimeError("search_batch: dimension mismatch")
+        _lib.check(_lib.lib().vlq_engine_search(self._h, _p(q), nq, dim, w1, alpha, k, _p(ids), _p(dists),
+                                                _p(scanned)))
+        if return_scanned:
+            return ids, dists, scanned
+        return ids, dists
+
+    def save(self, path: str) -> None:
+        """Index.save: serialize_index with t3 stored (bindings.cpp:128-131)."""
+        _lib.check(_lib.lib().vlq_engine_save_vlq1(self._h, os.fsencode(str(path)), 1))
+
+    def _info(self) -> _lib.VlqInfo:
+        info = _lib.VlqInfo()
+        _lib.check(_lib.lib().vlq_engine_info(self._h, ctypes.byref(info)))
+        return info
+
+    @property
+    def k(self) -> int:
+        return int(self._info().k)
+
+    @property
+    def n(self) -> int:
+        return int(self._info().n)
+
+    @property
+    def m(self) -> int:
+        return int(self._info().m)
+
+    @property
+    def dim(self) -> int:
+        return int(self._info().dim)
+
+    @property
+    def ntotal(self) -> int:
+        return int(self._info().ntotal)
+
+    # ---- extensions ------------------------------------------------------------
+    @property
+    def device(self) -> int:
+        return self._device
+
+    @property
+    def lambda_range(self) -> tuple[float, float]:
+        info = self._info()
+        return float(info.lambda_lo), float(info.lambda_hi)
+
+    @property
+    def local_entries(self) -> int:
+        return int(self._info().local_entries)
+
+    def search_device(self, d_queries: int, nq: int, w1: int, alpha: float, k: int, d_ids: int, d_dists: int,
+                      d_scanned: int | None = None, stream: int | None = None) -> None:
+        """Asynchronous search on device pointers (e.g. torch tensors' data_ptr())."""
+        _lib.check(_lib.lib().vlq_engine_search_device(self._h, ctypes.c_void_p(d_queries), nq, w1, alpha, k,
+                                                       ctypes.c_void_p(d_ids), ctypes.c_void_p(d_dists),
+                                                       ctypes.c_void_p(d_scanned) if d_scanned else None,
+                                                       ctypes.c_void_p(stream) if stream else None))
+
+    def sync(self, stream: int | None = None) -> None:
+        _lib.check(_lib.lib().vlq_engine_sync(self._h, ctypes.c_void_p(stream) if stream else None))
+
+    def encode(self, x):
+        """Per-point (cell, exact lambda, code, lambda byte) of the add path."""
+        a = _to_vecset(x)
+        nx = a.shape[0]
+        m = self.m
+        cells = np.empty(nx, np.uint32)
+        lams = np.empty(nx, np.float32)
+        codes = np.empty((nx, m), np.uint8)
+        lb = np.empty(nx, np.uint8)
+        _lib.check(_lib.lib().vlq_engine_encode(self._h, _p(a), nx, _p(cells), _p(lams), _p(codes), _p(lb)))
+        return cells, lams, codes, lb
+
+    def lists(self):
+        """This engine's posting lists: (list_off u64[k*n+1], ids u32, codes u8[.,m], lambdas u8)."""
+        info = self._info()
+        ne = int(info.local_entries)
+        off = np.empty(info.k * info.n + 1, np.uint64)
+        ids = np.empty(ne, np.uint32)
+        codes = np.empty((ne, info.m), np.uint8)
+        lams = np.empty(ne, np.uint8)
+        _lib.check(_lib.lib().vlq_engine_get_lists(self._h, _p(off), _p(ids), _p(codes), _p(lams)))
+        return off, ids, codes, lams
+
+
+# ---- module functions ---------------------------------------------------------
+_MAX_THREADS = 0
+
+
+def set_max_threads(threads: int) -> None:
+    """set_max_threads (parallel.cpp:13-15).  The GPU engine has no CPU worker
+    pool; the value is recorded and results never depend on it."""
+    global _MAX_THREADS
+    _MAX_THREADS = max(0, int(threads))
+
+
+def gen_synthetic(count: int, dim: int, clusters: int = 200, spread: float = 0.05, seed: int = 42) -> np.ndarray:
+    """gen_synthetic (dataset.cpp:13-44); bit-identical stream."""
+    out = np.empty((count, dim), np.float32)
+    _lib.check(_lib.lib().vlq_gen_synthetic(count, dim, clusters, spread, seed, _p(out)))
+    return out
+
+
+def brute_force_gt(base, queries, k: int, *, device: int | None = None) -> np.ndarray:
+    """brute_force_gt (dataset.cpp:46-92) on the GPU: exact ids, ties by id."""
+    b = _to_vecset(base)
+    q = _to_vecset(queries)
+    if b.shape[1] != q.shape[1]:
+        raise RuntimeError("brute_force_gt: dimension mismatch")
+    out = np.empty((q.shape[0], k), np.uint32)
+    _lib.check(_lib.lib().vlq_brute_force_gt(_default_device() if device is None else device, _p(b), b.shape[0],
+                                             _p(q), q.shape[0], b.shape[1], k, _p(out)))
+    return out
+
+
+def _kind(path: str) -> str:
+    if path.endswith(".bvecs"):
+        return "b"
+    if path.endswith(".ivecs"):
+        return "i"
+    return "f"
+
+
+def read_vecs(path: str) -> np.ndarray:
+    """read_vecs (vecs_io.cpp:29-86): byte and int payloads widen to float."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise RuntimeError(f"read_vecs: cannot open {path}") from None
+    kind = _kind(path)
+    vsz = 1 if kind == "b" else 4
+    rows, pos, dim = [], 0, None
+    while pos < len(raw):
+        if pos + 4 > len(raw):
+            raise RuntimeError(f"read_vecs: truncated record header in {path}")
+        (d,) = struct.unpack_from("<i", raw, pos)
+        pos += 4
+        if d <= 0:
+            raise RuntimeError(f"read_vecs: non-positive dimension in {path}")
+        if dim is None:
+            dim = d
+        elif d != dim:
+            raise RuntimeError(f"read_vecs: mismatched record dimension in {path}")
+        if pos + d * vsz > len(raw):
+            raise RuntimeError(f"read_vecs: truncated record payload in {path}")
+        dt = {"f": "<f4", "b": np.uint8, "i": "<i4"}[kind]
+        rows.append(np.frombuffer(raw, dt, count=d, offset=pos).astype(np.float32))
+        pos += d * vsz
+    if not rows:
+        raise RuntimeError(f"read_vecs: no records in {path}")
+    out = np.stack(rows)
+    if not np.isfinite(out).all():
+        raise RuntimeError("VectorSet: non-finite value")
+    return out
+
+
+def write_vecs(array, path: str) -> None:
+    """write_vecs (vecs_io.cpp:88-126)."""
+    a = _to_vecset(array)
+    kind = _kind(path)
+    n, d = a.shape
+    if kind == "b":
+        if ((a < 0) | (a > 255) | (a != np.floor(a))).any():
+            raise RuntimeError("write_vecs: value not representable as byte")
+        payload = a.astype(np.uint8)
+    elif kind == "i":
+        payload = a.astype(np.int32)
+    else:
+        payload = a
+    try:
+        with open(path, "wb") as f:
+            hdr = np.full((n, 1), d, "<i4").view(np.uint8)
+            f.write(np.concatenate([hdr, payload.view(np.uint8).reshape(n, -1)], axis=1).tobytes())
+    except OSError:
+        raise RuntimeError(f"write_vecs: cannot open {path}") from None
+
+
+__all__ = ["Index", "brute_force_gt", "gen_synthetic", "read_vecs", "set_max_threads", "write_vecs"]

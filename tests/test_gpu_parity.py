@@ -1,0 +1,250 @@
+"""GPU parity tests: the CUDA engine (libvlqgpu.so through the C ABI) against
+the reference's golden outputs and the C oracle, bit-exact.
+
+Parity bar (BASELINE.json north_star): ids and PQ codes bit-exact; distances
+within 1e-4 relative.  The engine reproduces the reference's fp32 operation
+order, so every check below is exact equality (a stricter bar)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ALL_CASES, PY_CASES, ROOT, grid_of, load_golden, regen_base
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vlqadc():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1901_00275_b200 import vlqadc as mod
+    return mod
+
+
+def same_f32(a, b):
+    return np.array_equal(np.asarray(a, np.float32).view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
+
+
+@pytest.mark.parametrize("name", ALL_CASES)
+@pytest.mark.parametrize("force_exact", [False, True])
+def test_search_matches_reference_golden(vlqadc, name, force_exact):
+    z, index_path, _ = load_golden(name)
+    idx = vlqadc.Index.load(index_path, force_exact=force_exact)
+    for gi, (w1, alpha, k) in enumerate(grid_of(z)):
+        ids, dists, scanned = idx.search(z["queries"], w1=w1, alpha=alpha, k=k, return_scanned=True)
+        assert np.array_equal(ids, z[f"ids_{gi}"]), (name, gi)
+        assert same_f32(dists, z[f"dists_{gi}"]), (name, gi)
+        assert int(scanned.sum()) == int(z[f"scanned_{gi}"]), (name, gi)
+
+
+@pytest.mark.parametrize("name", PY_CASES)
+def test_add_matches_reference_lists_and_file(vlqadc, name, tmp_path):
+    """Index.load(model) + add(base) == the reference-built index, byte for
+    byte after save (lists, lambda bytes, codes, t3, header)."""
+    z, index_path, model_path = load_golden(name)
+    base = regen_base(z)
+    idx = vlqadc.Index.load(model_path)
+    assert idx.ntotal == 0
+    idx.add(base)
+    assert idx.ntotal == len(base)
+    out = str(tmp_path / "gpu.vlq")
+    idx.save(out)
+    assert open(out, "rb").read() == open(index_path, "rb").read()
+    # and it searches exactly like the reference
+    for gi, (w1, alpha, k) in enumerate(grid_of(z)):
+        ids, dists = idx.search(z["queries"], w1=w1, alpha=alpha, k=k)
+        assert np.array_equal(ids, z[f"ids_{gi}"]) and same_f32(dists, z[f"dists_{gi}"])
+
+
+def test_add_per_point_replay_matches_oracle(vlqadc, oracle_mod):
+    """Per-point (cell, exact lambda, code, lambda byte): test_index.cpp:161-189."""
+    z, index_path, model_path = load_golden("accept_small")
+    base = regen_base(z)
+    idx = vlqadc.Index.load(index_path)
+    cells, lams, codes, lb = idx.encode(base)
+    o = oracle_mod.OracleIndex.load(index_path)
+    oc, ol, ocd, olb = o.assign(base)
+    assert np.array_equal(cells, oc)
+    assert same_f32(lams, ol)
+    assert np.array_equal(codes, ocd)
+    assert np.array_equal(lb, olb)
+
+
+def test_exhaustive_search_equals_full_scan(vlqadc, oracle_mod):
+    """w1 = K, alpha = 1 (test_search.cpp:286-313, acceptance C3)."""
+    z, index_path, _ = load_golden("accept_small")
+    idx = vlqadc.Index.load(index_path)
+    o = oracle_mod.OracleIndex.load(index_path)
+    q = z["queries"][:20]
+    for k in (1, 10, 100):
+        ids, dists = idx.search(q, w1=idx.k, alpha=1.0, k=k)
+        oids, odists, _ = o.search(q, idx.k, 1.0, k)
+        assert np.array_equal(ids, oids) and same_f32(dists, odists)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed):
+    rng = np.random.default_rng(seed)
+    for name in ALL_CASES:
+        z, index_path, _ = load_golden(name)
+        idx = vlqadc.Index.load(index_path)
+        o = oracle_mod.OracleIndex.load(index_path)
+        for _ in range(3):
+            w1 = int(rng.integers(1, idx.k + 1))
+            alpha = float(np.float32(rng.uniform(0.01, 1.0)))
+            k = int(rng.choice([1, 3, 10, 64, 100, 300]))
+            ids, dists, sc = idx.search(z["queries"], w1=w1, alpha=alpha, k=k, return_scanned=True)
+            oids, od, osc = o.search(z["queries"], w1, alpha, k)
+            assert np.array_equal(ids, oids), (name, w1, alpha, k)
+            assert same_f32(dists, od)
+            assert np.array_equal(sc, osc)
+
+
+def test_padding_and_short_results(vlqadc, oracle_mod):
+    """S_q < k -> padded with -1 / +inf (bindings.cpp:116-124)."""
+    z, index_path, _ = load_golden("m1")
+    idx = vlqadc.Index.load(index_path)
+    ids, dists = idx.search(z["queries"], w1=1, alpha=0.01, k=1000)
+    oids, od, _ = oracle_mod.OracleIndex.load(index_path).search(z["queries"], 1, 0.01, 1000)
+    assert np.array_equal(ids, oids) and same_f32(dists, od)
+    assert (ids == -1).any() and np.isinf(dists[ids == -1]).all()
+
+
+def test_errors_mirror_reference(vlqadc, tmp_path):
+    z, index_path, model_path = load_golden("smoke")
+    idx = vlqadc.Index.load(index_path)
+    q = z["queries"]
+    with pytest.raises(RuntimeError, match="first_level_scan: need 0 < w1 <= k"):
+        idx.search(q, w1=0)
+    with pytest.raises(RuntimeError, match="first_level_scan: need 0 < w1 <= k"):
+        idx.search(q, w1=idx.k + 1)
+    with pytest.raises(RuntimeError, match="dimension mismatch"):
+        idx.search(np.zeros((3, idx.dim + 1), np.float32))
+    with pytest.raises(RuntimeError, match="expected a 2-D float array"):
+        idx.search(np.zeros(16, np.float32))
+    with pytest.raises(RuntimeError, match="non-finite"):
+        idx.search(np.full((2, 16), np.nan, np.float32))
+    with pytest.raises(RuntimeError, match="index already holds a base set"):
+        idx.add(q)
+    bad = tmp_path / "bad.vlq"
+    raw = open(index_path, "rb").read()
+    bad.write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(RuntimeError, match="bad magic"):
+        vlqadc.Index.load(str(bad))
+    bad.write_bytes(raw[: len(raw) // 2])
+    with pytest.raises(RuntimeError, match="truncated"):
+        vlqadc.Index.load(str(bad))
+    with pytest.raises(RuntimeError, match="cannot open"):
+        vlqadc.Index.load(str(tmp_path / "missing.vlq"))
+    m = vlqadc.Index.load(model_path)
+    with pytest.raises(RuntimeError, match="build_index: empty base set"):
+        m.add(np.zeros((0, 16), np.float32))
+
+
+def test_degenerate_edge_raises(vlqadc):
+    """line_lambda throws on c <= 0 (line_quant.cpp:10-12)."""
+    from oracle import vlq1
+    _, _, model_path = load_golden("smoke")
+    mdl = vlq1.read(model_path)
+    elen = mdl.elen.copy()
+    elen[0, 0] = 0.0
+    idx = vlqadc.Index.from_model(mdl.dim, mdl.k, mdl.n, mdl.m, mdl.clamp, mdl.lo, mdl.hi, mdl.centroids, mdl.nbr,
+                                  elen, mdl.pq)
+    with pytest.raises(RuntimeError, match="degenerate edge"):
+        idx.search(mdl.centroids[:4], w1=mdl.k, alpha=1.0, k=5)
+
+
+def test_single_point_base(vlqadc, oracle_mod):
+    """test_search.cpp:316-330: a one-point base returns that point."""
+    z, _, model_path = load_golden("m1")
+    idx = vlqadc.Index.load(model_path)
+    idx.add(np.array([[0.5, 0.25, -0.5, 1.0]], np.float32))
+    ids, dists = idx.search(np.full((1, 4), 0.1, np.float32), w1=idx.k, alpha=1.0, k=5)
+    assert ids[0, 0] == 0 and (ids[0, 1:] == -1).all()
+
+
+def test_centroids_land_in_own_region_rank0(vlqadc):
+    """test_index.cpp:138-159."""
+    from oracle import vlq1
+    _, _, model_path = load_golden("smoke")
+    mdl = vlq1.read(model_path)
+    idx = vlqadc.Index.load(model_path)
+    cells, lams, _, lb = idx.encode(mdl.centroids)
+    assert np.array_equal(cells, np.arange(mdl.k) * mdl.n)
+    assert (lb == 0).all()
+
+
+def test_identical_queries_identical_results(vlqadc):
+    z, index_path, _ = load_golden("smoke")
+    idx = vlqadc.Index.load(index_path)
+    q = np.repeat(z["queries"][5:6], 3, axis=0)
+    ids, dists = idx.search(q, w1=8, alpha=0.5, k=10)
+    assert (ids == ids[0]).all() and (dists == dists[0]).all()
+
+
+def test_tiling_independence(vlqadc):
+    """Results do not depend on the query tile size (determinism contract,
+    README.md:55-56)."""
+    z, index_path, _ = load_golden("accept_small")
+    a = vlqadc.Index.load(index_path)
+    b = vlqadc.Index.load(index_path, max_tile=7)
+    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100)]:
+        ia, da = a.search(z["queries"], w1=w1, alpha=alpha, k=k)
+        ib, db = b.search(z["queries"], w1=w1, alpha=alpha, k=k)
+        assert np.array_equal(ia, ib) and same_f32(da, db)
+
+
+def test_brute_force_gt_matches_reference(vlqadc):
+    z, _, _ = load_golden("smoke")
+    base = regen_base(z)
+    gt = vlqadc.brute_force_gt(base, z["queries"], 10)
+    assert np.array_equal(gt, z["gt10"])
+
+
+def test_sharded_engines_merge_to_the_single_engine_result(vlqadc):
+    """Lists sharded by region over 3 engines on one device; the (dist, id)
+    merge (K9) of per-shard top-k equals the unsharded result."""
+    import torch
+    from paper_1901_00275_b200 import dist as vdist
+    z, index_path, _ = load_golden("accept_small")
+    full = vlqadc.Index.load(index_path)
+    shards = [vlqadc.Index.load(index_path, shard_rank=r, shard_count=3) for r in range(3)]
+    assert sum(s.local_entries for s in shards) == full.ntotal
+    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100)]:
+        want_ids, want_d = full.search(z["queries"], w1=w1, alpha=alpha, k=k)
+        parts = [s.search(z["queries"], w1=w1, alpha=alpha, k=k) for s in shards]
+        pi = torch.from_numpy(np.stack([p[0] for p in parts])).cuda()
+        pd = torch.from_numpy(np.stack([p[1] for p in parts])).cuda()
+        got_i, got_d = vdist.merge_topk(pi, pd)
+        assert np.array_equal(got_i.cpu().numpy(), want_ids)
+        assert same_f32(got_d.cpu().numpy(), want_d)
+
+
+@pytest.mark.slow
+def test_acceptance_c7_trend_kats(vlqadc, tmp_path):
+    """acceptance.cpp:330-363 on the reference's 'big' instance, built by the
+    reference (oracle/_ref/ref_tools): recall@10 for w1 = 8/16/32/64 and the
+    scanned totals for alpha = 0.25/0.40/0.50 must equal the reference's
+    golden numbers."""
+    tools = os.path.join(ROOT, "oracle", "_ref", "ref_tools")
+    if not os.path.exists(tools):
+        pytest.skip("oracle/_ref not built")
+    from oracle import vlq1
+    prefix = str(tmp_path / "big")
+    subprocess.run([tools, "instance", "1000000", "32", "200", "1024", "16", "8", "6", "100000", "500", "2000",
+                    "0.25", prefix], check=True, timeout=1500)
+    idx = vlqadc.Index.load(prefix + ".vlq")
+    base = vlq1.read_fvecs(prefix + ".base.fvecs")
+    q = vlq1.read_fvecs(prefix + ".queries.fvecs")
+    gt = vlqadc.brute_force_gt(base, q, 10)
+    want_r10 = {8: 0.6700, 16: 0.7560, 32: 0.8260, 64: 0.8740}
+    for w1, r10 in want_r10.items():
+        ids, _ = idx.search(q, w1=w1, alpha=1.0, k=10)
+        rec = np.mean([gt[i, 0] in ids[i] for i in range(len(q))])
+        assert round(rec, 4) == r10, (w1, rec)
+    want_scan = {0.25: 7746348, 0.4: 12339928, 0.5: 15436084}
+    for alpha, total in want_scan.items():
+        _, _, sc = idx.search(q, w1=64, alpha=alpha, k=10, return_scanned=True)
+        assert int(sc.sum()) == total, (alpha, int(sc.sum()))
