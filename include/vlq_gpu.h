@@ -76,6 +76,12 @@ int vlq_engine_set_model(vlq_engine* e, uint32_t dim, uint32_t k, uint32_t n, ui
                          float lambda_lo, float lambda_hi, const float* centroids, const uint32_t* neighbor_ids,
                          const float* edge_sq_len, const float* pq_sub_centroids, const float* t3_or_null);
 
+/* Index.train (bindings.cpp:44-81) on the device: k-means codebook, exact
+ * n-NN centroid graph, anchor displacements, per-subspace PQ; installs the
+ * model into `e` (an index with zero points). */
+int vlq_engine_train(vlq_engine* e, const float* train, uint64_t nt, uint32_t dim, uint32_t k, uint32_t n, uint32_t m,
+                     uint32_t iters, uint64_t seed, int clamp_lambda);
+
 /* Index.add: build_index (proj/src/index.cpp:134-203) + once-only rule and
  * observe_lambda_range for unclamped models (bindings.cpp:83-97). */
 int vlq_engine_add(vlq_engine* e, const float* base, uint64_t n, uint32_t dim);

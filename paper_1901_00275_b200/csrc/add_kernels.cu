@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_encode(AddArgs a, const floa
                                                          float* __restrict__ lam_out, uint8_t* __restrict__ codes_out,
                                                          uint8_t* __restrict__ lamb_out,
                                                          float* __restrict__ eterm_out,
-                                                         unsigned int* __restrict__ emax_bits) {
+                                                         unsigned int* __restrict__ emax_bits,
+                                                         float* __restrict__ resid_out) {
     extern __shared__ float sm[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t dim = a.dim, n = a.n, m = a.m, dsub = dim / m;
@@ -168,17 +169,21 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_encode(AddArgs a, const floa
     best_j = __shfl_sync(0xffffffffu, best_j, 0);
     best_lam = __shfl_sync(0xffffffffu, best_lam, 0);
     const uint32_t cell = best * n + best_j;
-    if (!codes_out) {  // observe_lambda_range pre-pass: lambda only
+    if (!codes_out && !resid_out) {  // observe_lambda_range pre-pass: lambda only
         if (lane == 0) lam_out[pt] = best_lam;
         return;
     }
-    // residual at the exact lambda (index.cpp:181-184)
+    // residual at the exact lambda (index.cpp:181-184; training
+    // displacements, bindings.cpp:59-71)
     const float* ci = a.centroids + (uint64_t)best * dim;
     const float* sj = a.centroids + (uint64_t)a.nbr[cell] * dim;
     const float oml = __fsub_rn(1.0f, best_lam);
-    for (uint32_t d = lane; d < dim; d += 32)
+    for (uint32_t d = lane; d < dim; d += 32) {
         rs[d] = __fsub_rn(xs[d], __fadd_rn(__fmul_rn(oml, ci[d]), __fmul_rn(best_lam, sj[d])));
+        if (resid_out) resid_out[pt * dim + d] = rs[d];
+    }
     __syncwarp();
+    if (!codes_out) return;
     // pq_encode (pq.cpp:52-67): per sub-space argmin over 256 sub-centroids
     uint8_t* code = codes_out + pt * m;
     for (uint32_t p = 0; p < m; p++) {
@@ -277,12 +282,12 @@ void launch_assign_nearest(const AddArgs& a, const float* X, uint64_t nx, uint32
 
 void launch_encode(const AddArgs& a, const float* X, uint64_t nx, const uint32_t* best, int clamp_for_edges,
                    uint32_t* cell_out, float* lam_out, uint8_t* codes_out, uint8_t* lamb_out, float* eterm_out,
-                   unsigned int* emax_bits, cudaStream_t st) {
+                   unsigned int* emax_bits, cudaStream_t st, float* resid_out) {
     if (nx == 0) return;
     size_t smem = (size_t)dev::ENC_WARPS * (2 * a.dim + a.n + 1 + 32) * sizeof(float);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dev::k_encode<<<(unsigned)((nx + dev::ENC_WARPS - 1) / dev::ENC_WARPS), dev::ENC_WARPS * 32, smem, st>>>(
-        a, X, nx, best, clamp_for_edges, cell_out, lam_out, codes_out, lamb_out, eterm_out, emax_bits);
+        a, X, nx, best, clamp_for_edges, cell_out, lam_out, codes_out, lamb_out, eterm_out, emax_bits, resid_out);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -119,6 +119,17 @@ int vlq_engine_set_model(vlq_engine* e, uint32_t dim, uint32_t k, uint32_t n, ui
     });
 }
 
+int vlq_engine_train(vlq_engine* e, const float* train, uint64_t nt, uint32_t dim, uint32_t k, uint32_t n, uint32_t m,
+                     uint32_t iters, uint64_t seed, int clamp_lambda) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (nt && !train) throw std::runtime_error("train: NULL array");
+        vlq::HostModel hm =
+            vlq::train_model_device(e->impl->device(), train, nt, dim, k, n, m, iters, seed, clamp_lambda != 0);
+        e->impl->set_model(hm);
+    });
+}
+
 int vlq_engine_add(vlq_engine* e, const float* base, uint64_t n, uint32_t dim) {
     ENGINE_OR_FAIL(e);
     return guarded([&] {

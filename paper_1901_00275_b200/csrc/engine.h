@@ -112,6 +112,7 @@ public:
     void get_tables(std::vector<float>& t2, std::vector<float>& t3);
 
     cudaStream_t stream() const { return stream_; }
+    int device() const { return cfg_.device; }
     const HostModel& model() const { return model_; }
 
     // exact brute-force k-NN (dataset.cpp:46-92) on the device
@@ -154,5 +155,9 @@ private:
 };
 
 uint32_t w2_of(uint32_t w1, float alpha, uint32_t n);
+
+// Index.train on the device (train.cu); t3 is left empty (computed on upload).
+HostModel train_model_device(int device, const float* train, uint64_t nt, uint32_t dim, uint32_t k, uint32_t n,
+                             uint32_t m, uint32_t iters, uint64_t seed, bool clamp);
 
 }  // namespace vlq

@@ -79,7 +79,7 @@ void launch_tables(const float* centroids, uint32_t k, uint32_t dim, const float
 void launch_assign_nearest(const AddArgs& a, const float* X, uint64_t nx, uint32_t* best, cudaStream_t st);
 void launch_encode(const AddArgs& a, const float* X, uint64_t nx, const uint32_t* best, int clamp_for_edges,
                    uint32_t* cell_out, float* lam_out, uint8_t* codes_out, uint8_t* lamb_out, float* eterm_out,
-                   unsigned int* emax_bits, cudaStream_t st);
+                   unsigned int* emax_bits, cudaStream_t st, float* resid_out = nullptr);
 void launch_minmax(const float* v, uint64_t n, float* out2, cudaStream_t st);
 void launch_gather_entries(const uint32_t* order, uint64_t n, uint32_t m, uint64_t first_id,
                            const uint8_t* codes_pt, const uint8_t* lamb_pt, const float* eterm_pt,

@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* ws
 // three digit passes (11/11/10 bits), then one ordered collection pass that
 // keeps every key < T and the first r keys == T in position order.
 // Shared scratch: hist[2048] + scan[40].  All threads of the block call.
-__device__ void block_select_ordered(const float* __restrict__ vals, uint32_t len, uint32_t L,
+__device__ __noinline__ static void block_select_ordered(const float* __restrict__ vals, uint32_t len, uint32_t L,
                                      uint32_t* __restrict__ out, uint32_t* hist, uint32_t* scan) {
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     if (L >= len) {

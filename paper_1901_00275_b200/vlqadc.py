@@ -76,11 +76,16 @@ class Index:
     @staticmethod
     def train(train, k: int = 1024, n: int = 16, m: int = 8, iters: int = 10, seed: int = 42,
               clamp_lambda: bool = True, **engine_kw) -> "Index":
-        """Index.train (bindings.cpp:44-81) -- trains on the GPU (see train.py)."""
-        from .train import train_model
+        """Index.train (bindings.cpp:44-81), on the GPU (csrc/train.cu).  Same
+        pipeline and error texts as the reference; the codebooks are not
+        bit-identical to the reference's (different k-means seeding)."""
         t = _to_vecset(train)
-        model = train_model(t, k, n, m, iters, seed, clamp_lambda, device=engine_kw.get("device"))
-        return Index.from_model(**model, **engine_kw)
+        if m == 0 or t.shape[1] % m != 0:
+            raise RuntimeError("m must divide the vector dimension")
+        idx = Index(**engine_kw)
+        _lib.check(_lib.lib().vlq_engine_train(idx._h, _p(t), t.shape[0], t.shape[1], k, n, m, iters, seed,
+                                               int(clamp_lambda)))
+        return idx
 
     @staticmethod
     def load(path: str, **engine_kw) -> "Index":
