@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""VLQ-ADC batched search benchmark (BASELINE.json metric: QPS at fixed
+recall@100 on synthetic data, B200 vs the reference CPU implementation).
+
+A "step" is one batched search of the workload's full query batch (nq = 10k)
+through the engine: coarse distances, first/second level selection, term5,
+fused list scan + top-k', exact re-score.  Setup (untimed): GPU training of
+the model on a prefix sample, streamed GPU add of the synthetic base, exact
+GPU ground truth for a query subset.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+Under torchrun (N > 1) each rank holds the regions i % N == rank of the same
+index; the batch is searched on every shard and the per-shard exact top-k are
+all-gathered (NCCL) and merged by (dist, id) -- scaling "strong" (the index
+and batch are fixed, the lists are split).
+
+`value` is device-timed (CUDA events, queries resident in HBM, L2 flushed
+between steps, max over ranks).  `e2e` is the same metric through the public
+API with host buffers (Index.search on numpy arrays: H2D of the queries and
+D2H of ids/dists/scanned inside the timed region).  `cpu_baseline` times the
+REFERENCE implementation (oracle/_ref, built from /root/reference/proj)
+searching the same index (exported as VLQ1) on a bounded query sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QPS at fixed recall@100, 1B×96 synthetic, 1/2/4/8 B200 vs CPU ref"
+
+# BASELINE.json configs; SURVEY.md §8d parameters (sigma = 0.05, base seed 42,
+# query seed 43, n = 32 edges, w1 = 64, alpha = 0.25, k = 100)
+WORKLOADS = {
+    "tiny": dict(desc="tiny smoke workload: 200k x 32, K=256 x 16 lines, PQ 8 B", n=200_000, dim=32, k=256,
+                 edges=16, m=8, clusters=256, ntrain=50_000),
+    "c1": dict(desc="SIFT1M-shaped synthetic (configs[0]): 1M x 128, K=1024 x 32 lines, PQ 8 B, nq=10k, k=100",
+               n=1_000_000, dim=128, k=1024, edges=32, m=8, clusters=1000, ntrain=100_000),
+    "c2": dict(desc="DEEP10M-shaped synthetic (configs[1]): 10M x 96, K=4096 x 32 lines, PQ 16 B, nq=10k, k=100",
+               n=10_000_000, dim=96, k=4096, edges=32, m=16, clusters=4000, ntrain=200_000),
+    "c3": dict(desc="SIFT100M-shaped synthetic (configs[2]): 100M x 128, K=65536 x 32 lines, PQ 8 B, nq=10k",
+               n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=262_144),
+    "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k",
+               n=1_000_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536, ntrain=262_144),
+}
+SPREAD, BASE_SEED, QUERY_SEED, TRAIN_SEED = 0.05, 42, 43, 1
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [r for r in self.rows if r[7].isdigit() and int(r[7]) > 0] or self.rows
+        sm = [float(r[0]) for r in busy if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(busy)}
+
+
+def build_index(vlqadc, w, device, rank=0, world=1):
+    """Untimed setup: GPU training on a prefix sample, streamed GPU add."""
+    import torch
+    t0 = time.time()
+    sample = torch.empty((w["ntrain"], w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
+    vlqadc.gen_synthetic_device(0, w["ntrain"], w["dim"], w["clusters"], SPREAD, BASE_SEED, sample.data_ptr(),
+                                device=device)
+    torch.cuda.synchronize(device)
+    idx = vlqadc.Index.train(sample.cpu().numpy(), k=w["k"], n=w["edges"], m=w["m"], iters=10, seed=TRAIN_SEED,
+                             device=device, shard_rank=rank, shard_count=world)
+    t1 = time.time()
+    idx.add_synthetic(w["n"], clusters=w["clusters"], spread=SPREAD, seed=BASE_SEED)
+    t2 = time.time()
+    log(f"[setup] rank {rank}: train {t1 - t0:.1f}s, add {w['n']} points {t2 - t1:.1f}s, "
+        f"local entries {idx.local_entries}")
+    return idx, {"train_s": round(t1 - t0, 2), "add_s": round(t2 - t1, 2)}
+
+
+def make_queries(vlqadc, w, nq, device):
+    import torch
+    q = torch.empty((nq, w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
+    vlqadc.gen_synthetic_device(0, nq, w["dim"], w["clusters"], SPREAD, QUERY_SEED, q.data_ptr(), device=device)
+    torch.cuda.synchronize(device)
+    return q
+
+
+def recall_at(ids: np.ndarray, gt: np.ndarray, k: int) -> float:
+    """recall_at (proj/src/eval.cpp:13-36): true NN = gt column 0 in the first k ids."""
+    hit = (ids[:, :k] == gt[:, :1].astype(np.int64)).any(axis=1)
+    return float(hit.mean())
+
+
+def ref_module():
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "vlqadc")):
+        raise RuntimeError("oracle/_ref not built (run __graft_entry__.build() where /root/reference exists)")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import vlqadc as refmod  # the reference's own pybind11 module
+    return refmod
+
+
+def time_reference(ref_idx, refmod, queries: np.ndarray, w1, alpha, k, budget_s: float, warm: int = 100):
+    """Reference Index.search on a bounded sample with all host threads
+    (set_max_threads(0) = hardware_concurrency, parallel.cpp:17-24)."""
+    refmod.set_max_threads(0)
+    ref_idx.search(queries[:warm], w1=w1, alpha=alpha, k=k)  # warm-up excluded (eval.cpp:91)
+    probe = queries[warm:warm + 200]
+    t = time.perf_counter()
+    ref_idx.search(probe, w1=w1, alpha=alpha, k=k)
+    rate = len(probe) / max(time.perf_counter() - t, 1e-6)
+    ns = int(min(len(queries) - warm, max(200, rate * budget_s)))
+    sample = queries[warm:warm + ns]
+    t = time.perf_counter()
+    ids, dists = ref_idx.search(sample, w1=w1, alpha=alpha, k=k)
+    dt = time.perf_counter() - t
+    return ns / dt, ns, dt, ids, dists, warm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nq", type=int, default=10_000)
+    ap.add_argument("--w1", type=int, default=64)
+    ap.add_argument("--alpha", type=float, default=0.25)
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--gt-queries", type=int, default=1000)
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of reference CPU work per sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="wrap the timed steps in cudaProfilerStart/Stop (for ncu --profile-from-start off) and exit")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    os.environ["VLQ_DEVICE"] = str(local)
+    w = WORKLOADS[args.workload]
+    cfg = {"workload": w["desc"], "n_base": w["n"], "dim": w["dim"], "K": w["k"], "n_edges": w["edges"],
+           "m_bytes": w["m"], "nq": args.nq, "w1": args.w1, "alpha": args.alpha, "k": args.k,
+           "parallelism": f"region-sharded x{world}" if world > 1 else "single GPU",
+           "l2": "flushed between steps (512 MiB write)", "data": "synthetic Gaussian mixture (sigma 0.05)"}
+
+    if args.impl == "reference":
+        run_reference_arm(args, w, cfg, rank, world, local)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    from paper_1901_00275_b200 import vlqadc
+    from paper_1901_00275_b200.dist import merge_topk, gather_parts
+
+    idx, setup = build_index(vlqadc, w, local, rank, world)
+    q = make_queries(vlqadc, w, args.nq, local)
+    nq, k = args.nq, args.k
+    ids = torch.empty((nq, k), dtype=torch.int64, device=q.device)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=q.device)
+    scanned = torch.empty((nq,), dtype=torch.int64, device=q.device)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=q.device)
+    stream = torch.cuda.current_stream(q.device)
+    st = stream.cuda_stream
+
+    def step():
+        idx.search_device(q.data_ptr(), nq, args.w1, args.alpha, k, ids.data_ptr(), dists.data_ptr(),
+                          scanned.data_ptr(), st)
+        if world > 1:
+            gi, gd = gather_parts(ids, dists)
+            return merge_topk(gi, gd, st)
+        return ids, dists
+
+    for _ in range(args.warmup):
+        step()
+    idx.sync(st)
+    torch.cuda.synchronize()
+    idx.set_profiling(True)
+    idx.stats(reset=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if args.profile:
+        torch.cuda.profiler.start()
+    with ClockSampler(local) as clocks:
+        for s in range(args.steps):
+            flush.zero_()
+            ev[s][0].record(stream)
+            out_ids, out_d = step()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    if args.profile:
+        torch.cuda.profiler.stop()
+        log(f"[profile] {args.steps} steps, {sum(a.elapsed_time(b) for a, b in ev):.3f} ms (under profiler: not a bench value)")
+        return
+    if world > 1:
+        dist.barrier()
+    idx.sync(st)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    stats = idx.stats()
+    idx.set_profiling(False)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=q.device)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    value = nq * args.steps / (ms_max / 1e3)
+
+    # algorithmic bytes of the dominant kernel (the fused list scan): S_q*(m+5)
+    local_scanned = int(scanned.sum().item())
+    scan_bytes_per_step = local_scanned * (w["m"] + 5)
+    scan_ms = stats["phase_ms"]["scan"] / args.steps
+    res_ids = out_ids.cpu().numpy()
+    res_d = out_d.cpu().numpy()
+
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = scan_bytes_per_step / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", f"scan_traffic_{args.workload}.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": "k_scan<M,fast> (fused list scan + warp top-k')",
+                "achieved": round(achieved, 1) if achieved else None, "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4) if achieved else None, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
+                "algorithmic_bytes_per_launch": scan_bytes_per_step,
+                "bytes_per_candidate": w["m"] + 5, "scan_ms_per_launch": round(scan_ms, 4),
+                "phase_ms_per_step": {p: round(v / args.steps, 4) for p, v in stats["phase_ms"].items()},
+                "scan_share_of_step": round(scan_ms / (ms_max / args.steps), 4)}
+
+    # recall on the exact ground truth of a query subset
+    ngt = min(args.gt_queries, nq)
+    qh = q.cpu().numpy()
+    gt = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], SPREAD, BASE_SEED, qh[:ngt], 1,
+                                         device=local)
+    recall = {f"recall@{r}": round(recall_at(res_ids[:ngt], gt, r), 4) for r in (1, 10, 100) if r <= k}
+
+    # e2e: public API with host buffers (H2D queries + D2H results per step)
+    e2e = None
+    if world == 1:
+        idx.search(qh, w1=args.w1, alpha=args.alpha, k=k)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            e_ids, e_d = idx.search(qh, w1=args.w1, alpha=args.alpha, k=k)
+        e2e_s = time.perf_counter() - t
+        assert np.array_equal(e_ids, res_ids)
+        e2e = {"value": round(nq * args.steps / e2e_s, 1), "unit": "queries/s",
+               "h2d_bytes_per_step": int(qh.nbytes), "d2h_bytes_per_step": int(nq * k * 12 + nq * 8),
+               "api": "paper_1901_00275_b200.vlqadc.Index.search (numpy in/out)"}
+
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            refmod = ref_module()
+            with tempfile.TemporaryDirectory() as tmp:
+                path = os.path.join(tmp, "bench.vlq")
+                idx.save(path)
+                ref_idx = refmod.Index.load(path)
+            qps, ns, dt, rids, rd, off = time_reference(ref_idx, refmod, qh, args.w1, np.float32(args.alpha), k,
+                                                        args.cpu_budget)
+            parity = bool(np.array_equal(rids, res_ids[off:off + ns]) and
+                          np.array_equal(rd.view(np.uint32), res_d[off:off + ns].view(np.uint32)))
+            cpu = {"value": round(qps, 2), "unit": "queries/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"{ns} of the {nq} benchmark queries (after 100 warm-up), same VLQ1 index, "
+                             f"Index.search with set_max_threads(0), {dt:.1f} s",
+                   "ids_and_dists_bit_exact_vs_gpu": parity}
+            del ref_idx
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
+
+    clk = clocks.summary()
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (exact reference order) + u8 codes",
+            "data": "synthetic", "config": cfg, "recall": recall, "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
+            "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
+            "fallback_queries_per_step": stats["flagged"] / args.steps}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference_arm(args, w, cfg, rank, world, local):
+    """--impl reference: the reference's own CPU search (oracle/_ref) on the
+    same workload.  The index is built once on the GPU (the reference needs
+    hours to train/add at these sizes) and handed to the reference
+    as a VLQ1 file; the timed path is the unmodified reference Index.search."""
+    if rank != 0:
+        return
+    from paper_1901_00275_b200 import vlqadc
+    refmod = ref_module()
+    idx, _ = build_index(vlqadc, w, local)
+    qh = make_queries(vlqadc, w, args.nq, local).cpu().numpy()
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "bench.vlq")
+        idx.save(path)
+        del idx
+        ref_idx = refmod.Index.load(path)
+    refmod.set_max_threads(0)
+    alpha = np.float32(args.alpha)
+    ref_idx.search(qh[:100], w1=args.w1, alpha=alpha, k=args.k)
+    t = time.perf_counter()
+    ref_idx.search(qh[100:300], w1=args.w1, alpha=alpha, k=args.k)
+    rate = 200 / max(time.perf_counter() - t, 1e-6)
+    per_step = int(max(50, min(args.nq, rate * 6.0)))
+    times = []
+    for s in range(args.warmup + args.steps):
+        lo = (s * per_step) % max(1, args.nq - per_step)
+        t = time.perf_counter()
+        ref_idx.search(qh[lo:lo + per_step], w1=args.w1, alpha=alpha, k=args.k)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t)
+    value = per_step * len(times) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(cfg, reference_sample=f"{per_step} queries per step"),
+            "cpu_baseline": {"value": round(value, 2), "unit": "queries/s", "cores": os.cpu_count(),
+                             "kind": "reference",
+                             "sample": f"{per_step} queries per step, reference Index.search, set_max_threads(0)"},
+            "e2e": {"value": round(value, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

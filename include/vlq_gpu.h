@@ -55,6 +55,14 @@ typedef struct {
     uint64_t local_entries;  /* posting entries held by this engine */
 } vlq_info;
 
+typedef struct {
+    uint64_t launches;      /* engine kernels launched by search calls */
+    uint64_t tiles;         /* query tiles processed */
+    uint64_t flagged;       /* queries whose certificate failed -> exact scan (profiling on) */
+    double phase_ms[8];     /* CUDA-event ms per phase (profiling on): coarse, first-level,
+                               second-level, term5, scan, rescore, fallback, output */
+} vlq_stats;
+
 /* Thread-local message of the last failing call on this thread. */
 const char* vlq_last_error(void);
 
@@ -99,6 +107,26 @@ int vlq_engine_search(vlq_engine* e, const float* queries, uint64_t nq, uint32_t
 int vlq_engine_search_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
                              uint32_t k, int64_t* d_ids, float* d_dists, uint64_t* d_scanned, void* stream);
 int vlq_engine_sync(vlq_engine* e, void* stream);
+
+/* Streamed Index.add of the engine's counter-based synthetic generator
+ * (the reference's Gaussian-mixture law, dataset.cpp:13-44): rows are
+ * generated on the device chunk by chunk, so 1e8-1e9-point bases never touch
+ * host memory.  Same once-only / error semantics as vlq_engine_add. */
+int vlq_engine_add_synthetic(vlq_engine* e, uint64_t n, uint32_t clusters, float spread, uint64_t seed);
+
+/* Rows [first, first+count) of that generator into device memory. */
+int vlq_gen_synthetic_device(int device, uint64_t first, uint64_t count, uint32_t dim, uint32_t clusters, float spread,
+                             uint64_t seed, float* d_out, void* stream);
+
+/* Exact brute-force k-NN of host queries against rows [0, nb) of the device
+ * generator (ground truth at scale). */
+int vlq_brute_force_gt_synthetic(int device, uint64_t nb, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
+                                 const float* queries, uint64_t nq, uint32_t k, uint32_t* out);
+
+/* Per-phase CUDA-event timing (recorded on the search stream) and counters. */
+int vlq_engine_set_profiling(vlq_engine* e, int on);
+int vlq_engine_get_stats(vlq_engine* e, vlq_stats* out);
+int vlq_engine_reset_stats(vlq_engine* e);
 
 /* Index.k / n / m / dim / ntotal (bindings.cpp:222-232). */
 int vlq_engine_info(vlq_engine* e, vlq_info* out);

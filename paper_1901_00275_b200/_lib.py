@@ -22,6 +22,13 @@ class VlqConfig(ctypes.Structure):
                 ("workspace_bytes", c_u64), ("max_tile", c_u32), ("force_exact", c_i32)]
 
 
+class VlqStats(ctypes.Structure):
+    _fields_ = [("launches", c_u64), ("tiles", c_u64), ("flagged", c_u64), ("phase_ms", ctypes.c_double * 8)]
+
+
+PHASES = ["coarse", "first_level", "second_level", "term5", "scan", "rescore", "fallback", "output"]
+
+
 class VlqInfo(ctypes.Structure):
     _fields_ = [("dim", c_u32), ("k", c_u32), ("n", c_u32), ("m", c_u32), ("clamp_lambda", c_i32),
                 ("lambda_lo", c_f32), ("lambda_hi", c_f32), ("ntotal", c_u64), ("local_entries", c_u64)]
@@ -41,6 +48,12 @@ _SIGS = {
     "vlq_engine_search_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_sync": (c_i32, [c_vp, c_vp]),
     "vlq_engine_info": (c_i32, [c_vp, ctypes.POINTER(VlqInfo)]),
+    "vlq_engine_add_synthetic": (c_i32, [c_vp, c_u64, c_u32, c_f32, c_u64]),
+    "vlq_gen_synthetic_device": (c_i32, [c_i32, c_u64, c_u64, c_u32, c_u32, c_f32, c_u64, c_vp, c_vp]),
+    "vlq_brute_force_gt_synthetic": (c_i32, [c_i32, c_u64, c_u32, c_u32, c_f32, c_u64, c_vp, c_u64, c_u32, c_vp]),
+    "vlq_engine_set_profiling": (c_i32, [c_vp, c_i32]),
+    "vlq_engine_get_stats": (c_i32, [c_vp, ctypes.POINTER(VlqStats)]),
+    "vlq_engine_reset_stats": (c_i32, [c_vp]),
     "vlq_engine_get_lists": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_encode": (c_i32, [c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "vlq_merge_topk_device": (c_i32, [c_i32, c_vp, c_vp, c_u32, c_u64, c_u32, c_vp, c_vp, c_vp]),

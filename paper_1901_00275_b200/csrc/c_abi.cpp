@@ -1,6 +1,7 @@
 // extern "C" boundary (include/vlq_gpu.h).  No exception crosses it.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <random>
@@ -164,6 +165,69 @@ int vlq_engine_search_device(vlq_engine* e, const float* d_queries, uint64_t nq,
 int vlq_engine_sync(vlq_engine* e, void* stream) {
     ENGINE_OR_FAIL(e);
     return guarded([&] { e->impl->check_device_errors(stream ? (cudaStream_t)stream : e->impl->stream()); });
+}
+
+int vlq_engine_add_synthetic(vlq_engine* e, uint64_t n, uint32_t clusters, float spread, uint64_t seed) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!e->impl->has_model()) throw std::runtime_error("add: no model loaded");
+        if (e->impl->ntotal() != 0) throw std::runtime_error("index already holds a base set");
+        if (clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
+        if (!(spread > 0)) throw std::runtime_error("gen_synthetic: spread must be positive");
+        const uint32_t dim = e->impl->dim();
+        const uint64_t chunk = std::max<uint64_t>(1, (512ull << 20) / (4ull * dim));
+        e->impl->add_stream(n, chunk, [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+            vlq::launch_synth(first, count, dim, clusters, spread, seed, dst, st);
+        });
+    });
+}
+
+int vlq_gen_synthetic_device(int device, uint64_t first, uint64_t count, uint32_t dim, uint32_t clusters, float spread,
+                             uint64_t seed, float* d_out, void* stream) {
+    return guarded([&] {
+        if (dim == 0 || clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
+        if (!(spread > 0)) throw std::runtime_error("gen_synthetic: spread must be positive");
+        int prev = 0;
+        vlq::cuda_check(cudaGetDevice(&prev), "cudaGetDevice", __FILE__, __LINE__);
+        vlq::cuda_check(cudaSetDevice(device), "cudaSetDevice", __FILE__, __LINE__);
+        vlq::launch_synth(first, count, dim, clusters, spread, seed, d_out, (cudaStream_t)stream);
+        cudaSetDevice(prev);
+    });
+}
+
+int vlq_brute_force_gt_synthetic(int device, uint64_t nb, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
+                                 const float* queries, uint64_t nq, uint32_t k, uint32_t* out) {
+    return guarded([&] {
+        if (dim == 0 || clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
+        vlq::Engine::brute_force_gt_source(
+            device,
+            [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+                vlq::launch_synth(first, count, dim, clusters, spread, seed, dst, st);
+            },
+            nb, queries, nq, dim, k, out);
+    });
+}
+
+int vlq_engine_set_profiling(vlq_engine* e, int on) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] { e->impl->set_profiling(on != 0); });
+}
+
+int vlq_engine_get_stats(vlq_engine* e, vlq_stats* out) {
+    ENGINE_OR_FAIL(e);
+    if (!out) return fail(VLQ_ERR_INVALID, "stats: out is NULL");
+    const vlq::EngineStats& s = e->impl->stats();
+    out->launches = s.launches;
+    out->tiles = s.tiles;
+    out->flagged = s.flagged;
+    for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
+    return VLQ_OK;
+}
+
+int vlq_engine_reset_stats(vlq_engine* e) {
+    ENGINE_OR_FAIL(e);
+    e->impl->reset_stats();
+    return VLQ_OK;
 }
 
 int vlq_engine_info(vlq_engine* e, vlq_info* out) {

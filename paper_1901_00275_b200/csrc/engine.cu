@@ -69,6 +69,8 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
 }
 
 Engine::~Engine() {
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
     if (stream_) {
         cudaSetDevice(cfg_.device);
         cudaStreamSynchronize(stream_);
@@ -436,27 +438,74 @@ void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alp
 void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                          float* d_dists, uint64_t* d_scanned, cudaStream_t st) {
     SearchArgs a = search_args();
+    auto mark = [&](int ph) {
+        if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
+    };
+    uint64_t launches = 0;
+    mark(PH_COARSE);
     launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
+    mark(PH_FIRST);
     launch_first_level(ws_.p, nt, k_, w1, top_.p, st);
+    mark(PH_SECOND);
     launch_second_level(a, nt, w1, w2, st);
+    mark(PH_TERM5);
     launch_term5(d_q, pq_.p, dim_, m_, t5_.p, meta_.p, nt, st);
+    launches += 4;
     const uint32_t keep_x = next_pow2(std::max<uint32_t>(32, topk));
     const uint32_t buf_x = 2 * keep_x;
     const uint32_t warps_x = std::min<uint32_t>(8, std::max<uint32_t>(1, 8192 / buf_x));
     const bool fast = !cfg_.force_exact && topk > 0 && topk <= 768;
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+        mark(PH_SCAN);
         launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
+        mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
+        mark(PH_FALLBACK);
         CUDA_CHECK(cudaMemsetAsync(err_.p + 2, 0, 4, st));
         launch_compact_flags(meta_.p, nt, qlist_.p, err_.p + 2, st);
         launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, qlist_.p, err_.p + 2, st);
         launch_emit_exact(a, qlist_.p, err_.p + 2, nt, keep_x, topk, d_ids, d_dists, st);
-    } else if (topk > 0) {
-        launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, nullptr, nullptr, st);
-        launch_emit_exact(a, nullptr, nullptr, nt, keep_x, topk, d_ids, d_dists, st);
+        launches += 5;
+    } else {
+        mark(PH_SCAN);
+        mark(PH_RESCORE);
+        mark(PH_FALLBACK);
+        if (topk > 0) {
+            launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, nullptr, nullptr, st);
+            launch_emit_exact(a, nullptr, nullptr, nt, keep_x, topk, d_ids, d_dists, st);
+            launches += 2;
+        }
     }
-    if (d_scanned) launch_copy_scanned(meta_.p, nt, d_scanned, st);
+    mark(PH_OUT);
+    if (d_scanned) {
+        launch_copy_scanned(meta_.p, nt, d_scanned, st);
+        launches += 1;
+    }
+    mark(PH_COUNT);
+    stats_.launches += launches;
+    stats_.tiles += 1;
+    if (profiling_) {
+        CUDA_CHECK(cudaEventSynchronize(ev_[PH_COUNT]));
+        for (int p = 0; p < PH_COUNT; p++) {
+            float ms = 0.0f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[p], ev_[p + 1]));
+            stats_.phase_ms[p] += ms;
+        }
+        if (fast) {
+            unsigned int nflag = 0;
+            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            stats_.flagged += nflag;
+        }
+    }
+}
+
+void Engine::set_profiling(bool on) {
+    DeviceGuard g(cfg_.device);
+    if (on && !ev_[0])
+        for (auto& e : ev_) CUDA_CHECK(cudaEventCreate(&e));
+    profiling_ = on;
 }
 
 void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
@@ -489,13 +538,24 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
 // ---------------------------------------------------------------------------
 void Engine::brute_force_gt(int device, const float* base, uint64_t nb, const float* queries, uint64_t nq,
                             uint32_t dim, uint32_t k, uint32_t* out) {
+    brute_force_gt_source(
+        device,
+        [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+            CUDA_CHECK(cudaMemcpyAsync(dst, base + first * dim, count * dim * 4, cudaMemcpyHostToDevice, st));
+        },
+        nb, queries, nq, dim, k, out);
+}
+
+void Engine::brute_force_gt_source(int device, const BaseSource& src, uint64_t nb, const float* queries, uint64_t nq,
+                                   uint32_t dim, uint32_t k, uint32_t* out) {
     if ((uint64_t)k > nb) throw std::runtime_error("brute_force_gt: k exceeds base count");
     if (nq == 0 || k == 0) return;
+    if (k > 4096) throw std::runtime_error("brute_force_gt: k > 4096 is not supported by the GPU engine");
     DeviceGuard g(device);
     cudaStream_t st;
     CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    const uint64_t C = std::min<uint64_t>(nb, 32768);
-    const uint64_t T = std::min<uint64_t>(nq, std::max<uint64_t>(1, (1ull << 30) / (4 * C)));
+    const uint64_t C = std::min<uint64_t>(nb, 65536);
+    const uint64_t T = std::min<uint64_t>(nq, std::max<uint64_t>(1, (2ull << 30) / (4 * C)));
     DevBuf<float> B, Q, dist;
     DevBuf<uint32_t> sel;
     DevBuf<uint64_t> running;
@@ -508,7 +568,7 @@ void Engine::brute_force_gt(int device, const float* base, uint64_t nb, const fl
     CUDA_CHECK(cudaMemsetAsync(running.p, 0xff, nq * (uint64_t)k * 8, st));
     for (uint64_t c0 = 0; c0 < nb; c0 += C) {
         const uint64_t cn = std::min(C, nb - c0);
-        CUDA_CHECK(cudaMemcpyAsync(B.p, base + c0 * dim, cn * dim * 4, cudaMemcpyHostToDevice, st));
+        src(c0, cn, B.p, st);
         for (uint64_t q0 = 0; q0 < nq; q0 += T) {
             const uint64_t tn = std::min(T, nq - q0);
             launch_sqdist_matrix(Q.p + q0 * dim, tn, B.p, cn, dim, dist.p, cn, st);

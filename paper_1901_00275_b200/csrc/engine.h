@@ -71,6 +71,15 @@ struct DevBuf {
     T* get() const { return p; }
 };
 
+enum Phase { PH_COARSE = 0, PH_FIRST, PH_SECOND, PH_TERM5, PH_SCAN, PH_RESCORE, PH_FALLBACK, PH_OUT, PH_COUNT };
+
+struct EngineStats {
+    uint64_t launches = 0;      // kernels launched by search calls
+    uint64_t tiles = 0;
+    uint64_t flagged = 0;       // queries that took the exact fallback
+    double phase_ms[PH_COUNT] = {0};  // CUDA-event time per phase (profiling on)
+};
+
 class Engine {
 public:
     explicit Engine(const EngineConfig& cfg);
@@ -118,6 +127,13 @@ public:
     // exact brute-force k-NN (dataset.cpp:46-92) on the device
     static void brute_force_gt(int device, const float* base, uint64_t nb, const float* queries, uint64_t nq,
                                uint32_t dim, uint32_t k, uint32_t* out);
+    using BaseSource = std::function<void(uint64_t first, uint64_t count, float* dst, cudaStream_t st)>;
+    static void brute_force_gt_source(int device, const BaseSource& src, uint64_t nb, const float* queries,
+                                      uint64_t nq, uint32_t dim, uint32_t k, uint32_t* out);
+
+    void set_profiling(bool on);
+    const EngineStats& stats() const { return stats_; }
+    void reset_stats() { stats_ = EngineStats(); }
 
 private:
     void upload_model();
@@ -130,6 +146,9 @@ private:
 
     EngineConfig cfg_;
     cudaStream_t stream_ = nullptr;
+    bool profiling_ = false;
+    cudaEvent_t ev_[PH_COUNT + 1] = {};
+    EngineStats stats_;
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;
     bool clamp_ = true;

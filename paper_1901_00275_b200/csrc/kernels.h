@@ -92,6 +92,8 @@ namespace vlq {
 void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st);
 void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+void launch_synth(uint64_t first, uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
+                  float* out, cudaStream_t st);
 void launch_eterm_lists(const AddArgs& a, const uint64_t* list_off, uint32_t ncell, const uint8_t* codes,
                         const uint8_t* lambdas, uint64_t nent, float* eterm, unsigned int* emax_bits, cudaStream_t st);
 void launch_gt_merge(const float* dist, uint64_t ldd, uint64_t nq, uint32_t k, uint32_t npos,

@@ -184,6 +184,21 @@ class Index:
     def sync(self, stream: int | None = None) -> None:
         _lib.check(_lib.lib().vlq_engine_sync(self._h, ctypes.c_void_p(stream) if stream else None))
 
+    def add_synthetic(self, n: int, clusters: int = 200, spread: float = 0.05, seed: int = 42) -> None:
+        """Streamed add of n rows of the device synthetic generator."""
+        _lib.check(_lib.lib().vlq_engine_add_synthetic(self._h, n, clusters, spread, seed))
+
+    def set_profiling(self, on: bool = True) -> None:
+        _lib.check(_lib.lib().vlq_engine_set_profiling(self._h, int(on)))
+
+    def stats(self, reset: bool = False) -> dict:
+        s = _lib.VlqStats()
+        _lib.check(_lib.lib().vlq_engine_get_stats(self._h, ctypes.byref(s)))
+        if reset:
+            _lib.check(_lib.lib().vlq_engine_reset_stats(self._h))
+        return {"launches": int(s.launches), "tiles": int(s.tiles), "flagged": int(s.flagged),
+                "phase_ms": dict(zip(_lib.PHASES, [float(x) for x in s.phase_ms]))}
+
     def encode(self, x):
         """Per-point (cell, exact lambda, code, lambda byte) of the add path."""
         a = _to_vecset(x)
@@ -235,6 +250,24 @@ def brute_force_gt(base, queries, k: int, *, device: int | None = None) -> np.nd
     out = np.empty((q.shape[0], k), np.uint32)
     _lib.check(_lib.lib().vlq_brute_force_gt(_default_device() if device is None else device, _p(b), b.shape[0],
                                              _p(q), q.shape[0], b.shape[1], k, _p(out)))
+    return out
+
+
+def gen_synthetic_device(first: int, count: int, dim: int, clusters: int, spread: float, seed: int,
+                         d_out: int, *, device: int | None = None, stream: int | None = None) -> None:
+    """Rows [first, first+count) of the counter-based device generator."""
+    _lib.check(_lib.lib().vlq_gen_synthetic_device(_default_device() if device is None else device, first, count,
+                                                   dim, clusters, spread, seed, ctypes.c_void_p(d_out),
+                                                   ctypes.c_void_p(stream) if stream else None))
+
+
+def brute_force_gt_synthetic(nb: int, dim: int, clusters: int, spread: float, seed: int, queries, k: int, *,
+                             device: int | None = None) -> np.ndarray:
+    """Exact k-NN of queries against rows [0, nb) of the device generator."""
+    q = _to_vecset(queries)
+    out = np.empty((q.shape[0], k), np.uint32)
+    _lib.check(_lib.lib().vlq_brute_force_gt_synthetic(_default_device() if device is None else device, nb, dim,
+                                                       clusters, spread, seed, _p(q), q.shape[0], k, _p(out)))
     return out
 
 
