@@ -50,6 +50,9 @@ WORKLOADS = {
                n=1_000_000, dim=128, k=1024, edges=32, m=8, clusters=1000, ntrain=100_000),
     "c2": dict(desc="DEEP10M-shaped synthetic (configs[1]): 10M x 96, K=4096 x 32 lines, PQ 16 B, nq=10k, k=100",
                n=10_000_000, dim=96, k=4096, edges=32, m=16, clusters=4000, ntrain=200_000),
+    "deep100m": dict(desc="DEEP100M-shaped synthetic (HBM-resident scan study): 100M x 96, K=4096 x 32 lines, PQ 16 B, "
+                          "nq=10k, k=100", n=100_000_000, dim=96, k=4096, edges=32, m=16, clusters=4000,
+                     ntrain=200_000),
     "c3": dict(desc="SIFT100M-shaped synthetic (configs[2]): 100M x 128, K=65536 x 32 lines, PQ 8 B, nq=10k",
                n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=262_144),
     "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k",

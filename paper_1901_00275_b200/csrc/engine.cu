@@ -458,7 +458,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
         mark(PH_SCAN);
-        launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
+        if (!launch_scan_fast(a, nt, w2, keep, st)) launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
         mark(PH_FALLBACK);

@@ -404,7 +404,10 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, ui
             // every scanned entry x satisfies |fast_x - exact_x| <= eps
             const QueryMeta mt = a.meta[q];
             const double u = 5.9604644775390625e-08;  // 2^-24
-            const double eps = 1.25 * u * (8.0 * ((double)mt.dmax + (double)a.emax) + 4.0 * (double)mt.s5max) + 1e-30;
+            // |term1_fast - term1_exact| <= 19u*Dmax (FFMA lambda/term1 vs the
+            // reference op order), the reassociated e-sum 8u*(Dmax+Emax), the
+            // final subtraction 4u*S5max; 1.25x margin
+            const double eps = 1.25 * u * (27.0 * (double)mt.dmax + 8.0 * (double)a.emax + 4.0 * (double)mt.s5max) + 1e-30;
             const double exact_k = (double)unord_float((uint32_t)(keys[topk - 1] >> 32));
             const double fast_last = (double)s_fast_last;
             if (!(fast_last - eps > exact_k)) flag = 1;
