@@ -102,66 +102,175 @@ __device__ __forceinline__ void bitonic_merge_warp(uint64_t* a, uint32_t n, uint
     }
 }
 
+// Block-wide radix select over the block-shared candidate buffer: keeps
+// exactly the `keep` smallest u64 keys (compacted, unordered) and returns the
+// largest kept key.  Keys are unique (dist bits | entry position).  Digits of
+// 8 bits from the top; stops early once the selected bin is taken whole.
+__device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep, uint32_t* hist,
+                                      unsigned int* s_misc) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint64_t prefix = 0, pmask = 0;
+    uint32_t remaining = keep;
+    int sh = 56;
+    for (; sh >= 0; sh -= 8) {
+        for (uint32_t b = tid; b < 256; b += nt) hist[b] = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += nt) {
+            const uint64_t k = cbuf[i];
+            if ((k & pmask) == prefix) atomicAdd(&hist[(uint32_t)(k >> sh) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {  // warp 0: scan 256 bins (8 per lane), find the crossing bin
+            uint32_t v[8], s = 0;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                v[j] = hist[tid * 8 + j];
+                s += v[j];
+            }
+            uint32_t incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= (uint32_t)o) incl += y;
+            }
+            uint32_t run = incl - s;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (run < remaining && remaining <= run + v[j]) {
+                    s_misc[0] = tid * 8 + j;
+                    s_misc[1] = run;
+                    s_misc[2] = v[j];
+                }
+                run += v[j];
+            }
+        }
+        __syncthreads();
+        const uint32_t b = s_misc[0], before = s_misc[1], inbin = s_misc[2];
+        __syncthreads();
+        prefix |= (uint64_t)b << sh;
+        pmask |= 0xFFull << sh;
+        remaining -= before;
+        if (inbin == remaining) break;  // the whole bin is kept
+    }
+    const uint64_t T = sh > 0 ? (prefix | ((1ull << sh) - 1ull)) : prefix;  // keep keys <= T
+    // in-place ordered compaction, one block-sized chunk at a time
+    uint32_t written = 0;
+    for (uint32_t base = 0; base < n; base += nt) {
+        const uint32_t i = base + tid;
+        const uint64_t k = i < n ? cbuf[i] : ~0ull;
+        const uint32_t take = (i < n && k <= T) ? 1u : 0u;
+        uint32_t total;
+        const uint32_t ex = block_excl_scan_u32(take, s_misc + 8, &total);
+        if (take) cbuf[written + ex] = k;
+        written += total;
+        __syncthreads();
+    }
+    return T;
+}
+
 template <int M, int U>
-__global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2, uint32_t keep) {
+__global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = (M + 3) / 4;
-    const uint32_t buf = 2 * keep;
+    constexpr uint32_t CH = 32 * U;  // entries per chunk
     const uint32_t nwarps = blockDim.x >> 5;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t q = blockIdx.x;
     unsigned char* lut = smem;
-    uint64_t* bufs = reinterpret_cast<uint64_t*>(smem + 4 * LutPlan<M>::words());
-    uint64_t* wbuf = bufs + (size_t)warp * buf;
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + 4 * LutPlan<M>::words());   // cap keys
+    uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);                       // w2 + 1
+    __shared__ uint32_t hist[256];
+    __shared__ unsigned int s_misc[48];
+    __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
 
-    // replicate the query's term5 table into the banked LUT
+    // 1. replicate the query's term5 table into the banked LUT (4 copies per STS.128)
     const float* t5q = a.t5 + q * M * VLQ_KSUB;
-    float* lutf = reinterpret_cast<float*>(lut);
-#pragma unroll 1
+    float4* lut4 = reinterpret_cast<float4*>(lut);
+#pragma unroll
     for (int p = 0; p < M; p++) {
+        constexpr int dummy = 0;
+        (void)dummy;
         const int lg = LutPlan<M>::lg(p);
-        const int base = LutPlan<M>::off(p);
-        for (uint32_t i = threadIdx.x; i < (256u << lg); i += blockDim.x)
-            lutf[base + i] = t5q[p * VLQ_KSUB + (i >> lg)];
+        const int base4 = LutPlan<M>::off(p) >> 2;
+        const uint32_t n4 = 256u << (lg - 2);
+        for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) {
+            const float v = __ldg(t5q + p * VLQ_KSUB + (i >> (lg - 2)));
+            lut4[base4 + i] = make_float4(v, v, v, v);
+        }
     }
-    for (uint32_t i = threadIdx.x; i < nwarps * buf; i += blockDim.x) bufs[i] = ~0ull;
-    if (threadIdx.x == 0) s_tau = ~0ull;
-    __syncthreads();
-
-    const float* wsq = a.ws + q * a.k;
+    // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
+    {
+        const uint32_t per = (w2 + blockDim.x - 1) / blockDim.x;
+        uint32_t local = 0;
+        for (uint32_t t = threadIdx.x * per; t < min(w2, (threadIdx.x + 1) * per); t++) {
+            const uint32_t c = selq[t];
+            const uint32_t len = (uint32_t)(a.list_off[c + 1] - a.list_off[c]);
+            cpref[t] = (len + CH - 1) / CH;
+            local += cpref[t];
+        }
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, s_misc + 8, &total);
+        for (uint32_t t = threadIdx.x * per; t < min(w2, (threadIdx.x + 1) * per); t++) {
+            const uint32_t c = cpref[t];
+            cpref[t] = run;
+            run += c;
+        }
+        if (threadIdx.x == 0) {
+            cpref[w2] = total;
+            s_count = 0;
+            s_tau = ~0ull;
+        }
+    }
+    __syncthreads();
+    const uint32_t nchunks = cpref[w2];
+    // balanced contiguous chunk range per warp
+    const uint32_t c_lo = (uint32_t)(((uint64_t)nchunks * warp) / nwarps);
+    const uint32_t c_hi = (uint32_t)(((uint64_t)nchunks * (warp + 1)) / nwarps);
+    const uint32_t rounds = (nchunks + nwarps - 1) / nwarps;  // >= chunks of any warp
+    // locate the first cell of this warp's range (warp-uniform binary search)
+    uint32_t t = 0;
+    {
+        uint32_t lo = 0, hi = w2;  // largest t with cpref[t] <= c_lo
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cpref[mid] <= c_lo) lo = mid;
+            else hi = mid;
+        }
+        t = lo;
+    }
+    const float* wsq = a.ws + q * a.k;
     const float delta = (a.hi - a.lo) * (1.0f / 256.0f);
     const float lam0 = a.lo + 0.5f * delta;
-    uint32_t cnt = 0;
-    uint64_t tau = ~0ull;
+    uint32_t cell = 0, L = 0, pos0 = 0;
+    const uint8_t* codes_c = nullptr;
+    const uint8_t* lam_c = nullptr;
+    const float* e_c = nullptr;
+    float av = 0.f, Bc = 0.f, cv = 0.f;
+    uint32_t loaded_t = 0xffffffffu;
+    const uint32_t flush_at = cap - nwarps * CH;
 
-    auto flush = [&]() {
-        for (uint32_t i = cnt + lane; i < buf; i += 32) wbuf[i] = ~0ull;
-        __syncwarp();
-        bitonic_sort_u64<true>(wbuf, buf, lane, 32);
-        cnt = min(cnt, keep);
-        if (cnt == keep) {
-            const uint64_t t = wbuf[keep - 1];
-            if (t < tau) tau = t;
-            if (lane == 0) atomicMin(&s_tau, (unsigned long long)t);
-        }
-        __syncwarp();
-    };
-
-    for (uint32_t ci = warp; ci < w2; ci += nwarps) {
-        const uint32_t cell = selq[ci];
-        const uint64_t b0 = a.list_off[cell];
-        const uint32_t L = (uint32_t)(a.list_off[cell + 1] - b0);
-        if (L == 0) continue;
-        const uint32_t i = cell / a.n;
-        const float av = wsq[i], bv = wsq[a.nbr[cell]], cv = a.elen[cell];
-        const float Bc = (bv - av) - cv;
-        const uint8_t* codes_c = a.codes + b0 * M;
-        const uint8_t* lam_c = a.lambdas + b0;
-        const float* e_c = a.eterm + b0;
-        const uint32_t pos0 = (uint32_t)b0;
-        for (uint32_t o = 0; o < L; o += 32 * U) {
+    for (uint32_t r = 0; r < rounds; r++) {
+        const uint32_t g = c_lo + r;
+        if (g < c_hi) {
+            while (cpref[t + 1] <= g) t++;
+            if (t != loaded_t) {
+                loaded_t = t;
+                cell = selq[t];
+                const uint64_t b0 = a.list_off[cell];
+                L = (uint32_t)(a.list_off[cell + 1] - b0);
+                pos0 = (uint32_t)b0;
+                const uint32_t i = cell / a.n;
+                av = wsq[i];
+                const float bv = wsq[a.nbr[cell]];
+                cv = a.elen[cell];
+                Bc = (bv - av) - cv;
+                codes_c = a.codes + b0 * M;
+                lam_c = a.lambdas + b0;
+                e_c = a.eterm + b0;
+            }
+            const uint32_t o = (g - cpref[t]) * CH;
             uint32_t cw[U][NW];
             uint32_t lb[U];
             float ev[U];
@@ -174,12 +283,14 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
                     ev[u] = __ldg(e_c + idx);
                 } else {
 #pragma unroll
-                    for (int t = 0; t < NW; t++) cw[u][t] = 0;
+                    for (int w = 0; w < NW; w++) cw[u][w] = 0;
                     lb[u] = 0;
                     ev[u] = 0.0f;
                 }
             }
+            const uint64_t tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
             uint64_t key[U];
+            uint32_t ntake = 0;
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const uint32_t idx = o + u * 32 + lane;
@@ -190,42 +301,48 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
                 uint32_t ub = __float_as_uint(dist);
                 ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
                 key[u] = idx < L ? (((uint64_t)ub << 32) | (pos0 + idx)) : ~0ull;
+                ntake += key[u] < tau ? 1u : 0u;
             }
-            const uint64_t st = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
-            const uint64_t th = tau < st ? tau : st;
-            bool any = false;
+            // one shared atomic per warp and chunk
+            uint32_t incl = ntake;
 #pragma unroll
-            for (int u = 0; u < U; u++) any |= key[u] < th;
-            if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const bool take = key[u] < th;
-                    const uint32_t bal = __ballot_sync(0xffffffffu, take);
-                    if (bal) {
-                        if (take) wbuf[cnt + __popc(bal & ((1u << lane) - 1u))] = key[u];
-                        cnt += __popc(bal);
-                        __syncwarp();
-                        if (cnt > buf - 32) flush();
-                    }
-                }
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= (uint32_t)off) incl += y;
             }
-        }
-    }
-    flush();
-    __syncthreads();
-    // merge tree: after round s, warp w (w % 2s == 0) holds the sorted best
-    // `keep` of warps [w, w + 2s) in wbuf[0, keep)
-    for (uint32_t s = 1; s < nwarps; s <<= 1) {
-        if ((warp % (2 * s)) == 0 && warp + s < nwarps) {
-            const uint64_t* other = bufs + (size_t)(warp + s) * buf;
-            for (uint32_t t = lane; t < keep; t += 32) wbuf[keep + t] = other[keep - 1 - t];
-            __syncwarp();
-            bitonic_merge_warp(wbuf, buf, lane);
+            const uint32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
+            if (wtotal) {
+                uint32_t base = 0;
+                if (lane == 31) base = atomicAdd(&s_count, wtotal);
+                base = __shfl_sync(0xffffffffu, base, 31) + incl - ntake;
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (key[u] < tau) cbuf[base++] = key[u];
+            }
         }
         __syncthreads();
+        if (s_count > flush_at) {  // block-uniform
+            const uint64_t T = block_select_keep(cbuf, s_count, keep, hist, s_misc);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_count = keep;
+                s_tau = T + 1;  // insert only keys <= T
+            }
+            __syncthreads();
+        }
     }
+    // final: exactly min(count, keep) smallest keys, sorted, padded with +inf
+    uint32_t n = s_count;
+    if (n > keep) {
+        block_select_keep(cbuf, n, keep, hist, s_misc);
+        n = keep;
+    }
+    __syncthreads();
+    for (uint32_t i = n + threadIdx.x; i < keep; i += blockDim.x) cbuf[i] = ~0ull;
+    __syncthreads();
+    bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
     uint64_t* candq = a.cand + q * keep;
-    for (uint32_t t = threadIdx.x; t < keep; t += blockDim.x) candq[t] = bufs[t];
+    for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
 }
 
 }  // namespace dev
@@ -234,15 +351,17 @@ template <int M>
 static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
     constexpr int U = 2;
     const uint32_t nwarps = 16;
-    const size_t smem = 4 * (size_t)dev::LutPlan<M>::words() + (size_t)nwarps * 2 * keep * 8;
+    const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
+    const size_t smem = 4 * (size_t)dev::LutPlan<M>::words() + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
     auto fn = dev::k_scan_fast<M, U>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)nq, nwarps * 32, smem, st>>>(a, w2, keep);
+    fn<<<(unsigned)nq, nwarps * 32, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
 }
 
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
-    if (keep > 256) return false;
+    // cap (2048) must exceed keep + one round of insertions (16 warps x 64)
+    if (keep > 512 || w2 > 4096) return false;
     switch (a.m) {
         case 16: launch_fast_t<16>(a, nq, w2, keep, st); return true;
         case 8: launch_fast_t<8>(a, nq, w2, keep, st); return true;
