@@ -4,6 +4,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -57,6 +58,7 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 }
 
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
+    if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
         throw std::runtime_error("engine: invalid shard configuration");
     int ndev = 0;
@@ -458,7 +460,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
         mark(PH_SCAN);
-        if (!launch_scan_fast(a, nt, w2, keep, st)) launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
+        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, st)) launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
         mark(PH_FALLBACK);

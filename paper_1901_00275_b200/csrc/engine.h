@@ -26,6 +26,7 @@ struct EngineConfig {
     uint64_t workspace_bytes = 4ull << 30;  // per-query-tile scratch budget
     uint32_t max_tile = 16384;
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
+    int scan_variant = 0;  // 0 auto (replicated LUT), 1 generic warp-buffer scan, 3 single-table LUT
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).

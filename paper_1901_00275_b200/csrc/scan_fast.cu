@@ -24,11 +24,12 @@
 namespace vlq {
 namespace dev {
 
-template <int M>
+template <int M, int R = 2>
 struct LutPlan {
-    // log2(copies) of sub-space p
+    // log2(copies) of sub-space p.  R = 2: full replication (<= 160 KB, one
+    // CTA per SM); R = 1: 4 copies; R = 0: a single table (several CTAs/SM)
     __host__ __device__ static constexpr int lg(int p) {
-        return M == 16 ? (p < 8 ? 4 : 2) : (M == 8 ? 4 : (M == 4 ? 5 : (M == 2 ? 5 : 5)));
+        return R == 0 ? 0 : (R == 1 ? 2 : (M == 16 ? (p < 8 ? 4 : 2) : (M == 8 ? 4 : 5)));
     }
     __host__ __device__ static constexpr int copies(int p) { return 1 << lg(p); }
     __host__ __device__ static constexpr int off(int p) {  // word offset of sub-space p
@@ -68,20 +69,21 @@ __device__ __forceinline__ uint32_t lut_index(uint32_t w, int k, uint32_t lane_o
     return (v & mask) | lane_off;
 }
 
-template <int M>
+template <int M, int R>
 __device__ __forceinline__ float lut_sum(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], uint32_t lane) {
     float s = 0.0f;
 #pragma unroll
     for (int p = 0; p < M; p++) {
         constexpr int dummy = 0;
         (void)dummy;
-        const int LG = LutPlan<M>::lg(p);
+        const int LG = LutPlan<M, R>::lg(p);
         const uint32_t lane_off = (lane & ((1u << LG) - 1u)) << 2;
         uint32_t idx;
         if (LG == 5) idx = lut_index<5>(w[p >> 2], p & 3, lane_off);
         else if (LG == 4) idx = lut_index<4>(w[p >> 2], p & 3, lane_off);
-        else idx = lut_index<2>(w[p >> 2], p & 3, lane_off);
-        s = __fadd_rn(s, *reinterpret_cast<const float*>(lut + 4 * LutPlan<M>::off(p) + idx));
+        else if (LG == 2) idx = lut_index<2>(w[p >> 2], p & 3, lane_off);
+        else idx = lut_index<0>(w[p >> 2], p & 3, lane_off);
+        s = __fadd_rn(s, *reinterpret_cast<const float*>(lut + 4 * LutPlan<M, R>::off(p) + idx));
     }
     return s;
 }
@@ -168,20 +170,22 @@ __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep,
     return T;
 }
 
-template <int M, int U>
-__global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
+template <int M, int U, int R>
+__global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 : 3)) k_scan_fast(SearchArgs a, uint32_t w2, uint32_t keep,
+                                                                      uint32_t cap) {
     extern __shared__ __align__(16) unsigned char smem[];
+    using Plan = LutPlan<M, R>;
     constexpr int NW = (M + 3) / 4;
     constexpr uint32_t CH = 32 * U;  // entries per chunk
     const uint32_t nwarps = blockDim.x >> 5;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t q = blockIdx.x;
     unsigned char* lut = smem;
-    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + 4 * LutPlan<M>::words());   // cap keys
-    uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);                       // w2 + 1
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + 4 * Plan::words());   // cap keys
+    uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);                 // w2 + 1
     __shared__ uint32_t hist[256];
     __shared__ unsigned int s_misc[48];
-    __shared__ unsigned int s_count;
+    __shared__ unsigned int s_count, s_overflow;
     __shared__ unsigned long long s_tau;
 
     // 1. replicate the query's term5 table into the banked LUT (4 copies per STS.128)
@@ -189,14 +193,17 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
     float4* lut4 = reinterpret_cast<float4*>(lut);
 #pragma unroll
     for (int p = 0; p < M; p++) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int lg = LutPlan<M>::lg(p);
-        const int base4 = LutPlan<M>::off(p) >> 2;
-        const uint32_t n4 = 256u << (lg - 2);
-        for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) {
-            const float v = __ldg(t5q + p * VLQ_KSUB + (i >> (lg - 2)));
-            lut4[base4 + i] = make_float4(v, v, v, v);
+        const int lg = Plan::lg(p);
+        if (lg >= 2) {
+            const int base4 = Plan::off(p) >> 2;
+            const uint32_t n4 = 256u << (lg - 2);
+            for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) {
+                const float v = __ldg(t5q + p * VLQ_KSUB + (i >> (lg - 2)));
+                lut4[base4 + i] = make_float4(v, v, v, v);
+            }
+        } else {
+            float* lutf = reinterpret_cast<float*>(lut) + Plan::off(p);
+            for (uint32_t i = threadIdx.x; i < 256u; i += blockDim.x) lutf[i] = __ldg(t5q + p * VLQ_KSUB + i);
         }
     }
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
@@ -220,6 +227,7 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
         if (threadIdx.x == 0) {
             cpref[w2] = total;
             s_count = 0;
+            s_overflow = 0;
             s_tau = ~0ull;
         }
     }
@@ -228,8 +236,7 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
     // balanced contiguous chunk range per warp
     const uint32_t c_lo = (uint32_t)(((uint64_t)nchunks * warp) / nwarps);
     const uint32_t c_hi = (uint32_t)(((uint64_t)nchunks * (warp + 1)) / nwarps);
-    const uint32_t rounds = (nchunks + nwarps - 1) / nwarps;  // >= chunks of any warp
-    // locate the first cell of this warp's range (warp-uniform binary search)
+    const uint32_t per_warp_max = (nchunks + nwarps - 1) / nwarps;
     uint32_t t = 0;
     {
         uint32_t lo = 0, hi = w2;  // largest t with cpref[t] <= c_lo
@@ -243,86 +250,129 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
     const float* wsq = a.ws + q * a.k;
     const float delta = (a.hi - a.lo) * (1.0f / 256.0f);
     const float lam0 = a.lo + 0.5f * delta;
-    uint32_t cell = 0, L = 0, pos0 = 0;
+    uint32_t L = 0, pos0 = 0;
     const uint8_t* codes_c = nullptr;
     const uint8_t* lam_c = nullptr;
     const float* e_c = nullptr;
     float av = 0.f, Bc = 0.f, cv = 0.f;
     uint32_t loaded_t = 0xffffffffu;
-    const uint32_t flush_at = cap - nwarps * CH;
 
-    for (uint32_t r = 0; r < rounds; r++) {
-        const uint32_t g = c_lo + r;
-        if (g < c_hi) {
-            while (cpref[t + 1] <= g) t++;
-            if (t != loaded_t) {
-                loaded_t = t;
-                cell = selq[t];
-                const uint64_t b0 = a.list_off[cell];
-                L = (uint32_t)(a.list_off[cell + 1] - b0);
-                pos0 = (uint32_t)b0;
-                const uint32_t i = cell / a.n;
-                av = wsq[i];
-                const float bv = wsq[a.nbr[cell]];
-                cv = a.elen[cell];
-                Bc = (bv - av) - cv;
-                codes_c = a.codes + b0 * M;
-                lam_c = a.lambdas + b0;
-                e_c = a.eterm + b0;
+    // chunk data double buffer (registers; static indices only)
+    uint32_t cw[U][NW], ncw[U][NW];
+    uint32_t lb[U], nlb[U];
+    float ev[U], nev[U];
+    uint32_t o_cur = 0, L_cur = 0, pos_cur = 0;
+    float av_cur = 0.f, Bc_cur = 0.f, cv_cur = 0.f;
+
+    auto locate = [&](uint32_t g) {  // walks t forward to the cell holding chunk g
+        while (cpref[t + 1] <= g) t++;
+        if (t != loaded_t) {
+            loaded_t = t;
+            const uint32_t cell = selq[t];
+            const uint64_t b0 = a.list_off[cell];
+            L = (uint32_t)(a.list_off[cell + 1] - b0);
+            pos0 = (uint32_t)b0;
+            const uint32_t i = cell / a.n;
+            av = wsq[i];
+            const float bv = wsq[a.nbr[cell]];
+            cv = a.elen[cell];
+            Bc = (bv - av) - cv;
+            codes_c = a.codes + b0 * M;
+            lam_c = a.lambdas + b0;
+            e_c = a.eterm + b0;
+        }
+        return (g - cpref[t]) * CH;
+    };
+    auto issue = [&](uint32_t (&xcw)[U][NW], uint32_t (&xlb)[U], float (&xev)[U], uint32_t o) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t idx = o + u * 32 + lane;
+            if (idx < L) {
+                load_code_vec<M>(codes_c + (size_t)idx * M, xcw[u]);
+                xlb[u] = __ldg(lam_c + idx);
+                xev[u] = __ldg(e_c + idx);
+            } else {
+#pragma unroll
+                for (int w = 0; w < NW; w++) xcw[u][w] = 0;
+                xlb[u] = 0;
+                xev[u] = 0.0f;
             }
-            const uint32_t o = (g - cpref[t]) * CH;
-            uint32_t cw[U][NW];
-            uint32_t lb[U];
-            float ev[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t idx = o + u * 32 + lane;
-                if (idx < L) {
-                    load_code_vec<M>(codes_c + (size_t)idx * M, cw[u]);
-                    lb[u] = __ldg(lam_c + idx);
-                    ev[u] = __ldg(e_c + idx);
-                } else {
-#pragma unroll
-                    for (int w = 0; w < NW; w++) cw[u][w] = 0;
-                    lb[u] = 0;
-                    ev[u] = 0.0f;
-                }
+        }
+    };
+
+    uint32_t g = c_lo;        // next chunk to issue
+    uint32_t done = 0;        // chunks consumed by this warp
+    uint32_t n_seen = 0;      // block-wide entries processed before this round (estimate)
+    if (g < c_hi) {
+        const uint32_t o = locate(g);
+        issue(cw, lb, ev, o);
+        o_cur = o; L_cur = L; pos_cur = pos0; av_cur = av; Bc_cur = Bc; cv_cur = cv;
+        g++;
+    }
+    uint32_t rlen = 1;
+    while (done < per_warp_max) {  // block-uniform trip count
+        for (uint32_t r = 0; r < rlen && done < per_warp_max; r++, done++) {
+            if (c_lo + done >= c_hi) continue;
+            // prefetch the next chunk into the other slot
+            uint32_t o_nx = 0, L_nx = 0, pos_nx = 0;
+            float av_nx = 0.f, Bc_nx = 0.f, cv_nx = 0.f;
+            if (g < c_hi) {
+                o_nx = locate(g);
+                issue(ncw, nlb, nev, o_nx);
+                L_nx = L; pos_nx = pos0; av_nx = av; Bc_nx = Bc; cv_nx = cv;
             }
             const uint64_t tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
             uint64_t key[U];
-            uint32_t ntake = 0;
+            uint32_t tk = 0;
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const uint32_t idx = o + u * 32 + lane;
+                const uint32_t idx = o_cur + u * 32 + lane;
                 const float lam = fmaf((float)lb[u], delta, lam0);
-                const float t1 = fmaf(lam, fmaf(lam, cv, Bc), av);
-                const float s5 = lut_sum<M>(lut, cw[u], lane);
+                const float t1 = fmaf(lam, fmaf(lam, cv_cur, Bc_cur), av_cur);
+                const float s5 = lut_sum<M, R>(lut, cw[u], lane);
                 const float dist = fmaf(-2.0f, s5, t1 + ev[u]);
                 uint32_t ub = __float_as_uint(dist);
                 ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
-                key[u] = idx < L ? (((uint64_t)ub << 32) | (pos0 + idx)) : ~0ull;
-                ntake += key[u] < tau ? 1u : 0u;
+                key[u] = idx < L_cur ? (((uint64_t)ub << 32) | (pos_cur + idx)) : ~0ull;
+                tk |= (key[u] < tau ? 1u : 0u) << u;
             }
-            // one shared atomic per warp and chunk
-            uint32_t incl = ntake;
+            uint32_t bal[U], wtot = 0;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= (uint32_t)off) incl += y;
+            for (int u = 0; u < U; u++) {
+                bal[u] = __ballot_sync(0xffffffffu, (tk >> u) & 1u);
+                wtot += __popc(bal[u]);
             }
-            const uint32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
-            if (wtotal) {
+            if (wtot) {
                 uint32_t base = 0;
-                if (lane == 31) base = atomicAdd(&s_count, wtotal);
-                base = __shfl_sync(0xffffffffu, base, 31) + incl - ntake;
+                if (lane == 0) base = atomicAdd(&s_count, wtot);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-                for (int u = 0; u < U; u++)
-                    if (key[u] < tau) cbuf[base++] = key[u];
+                for (int u = 0; u < U; u++) {
+                    if ((tk >> u) & 1u) {
+                        const uint32_t pos = base + __popc(bal[u] & lt);
+                        if (pos < cap) cbuf[pos] = key[u];
+                        else s_overflow = 1;  // correctness kept by the exact fallback
+                    }
+                    base += __popc(bal[u]);
+                }
             }
+            // rotate the double buffer
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+#pragma unroll
+                for (int w = 0; w < NW; w++) cw[u][w] = ncw[u][w];
+                lb[u] = nlb[u];
+                ev[u] = nev[u];
+            }
+            o_cur = o_nx; L_cur = L_nx; pos_cur = pos_nx; av_cur = av_nx; Bc_cur = Bc_nx; cv_cur = cv_nx;
+            if (g < c_hi) g++;
         }
         __syncthreads();
-        if (s_count > flush_at) {  // block-uniform
-            const uint64_t T = block_select_keep(cbuf, s_count, keep, hist, s_misc);
+        n_seen += rlen * nwarps * CH;
+        const uint32_t cnt = min(s_count, cap);
+        if (cnt > keep && (cnt > cap / 2 || done >= per_warp_max)) {  // block-uniform
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
             __syncthreads();
             if (threadIdx.x == 0) {
                 s_count = keep;
@@ -330,9 +380,17 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
             }
             __syncthreads();
         }
+        // next round length: expected insertions ~ keep * (new entries) / n_seen
+        // must fit the free space with a 2x margin; overflow -> exact fallback
+        const uint32_t free_slots = cap - min(s_count, cap);
+        const uint64_t per_chunk_round = (uint64_t)nwarps * CH;
+        uint64_t rn = (s_tau == ~0ull) ? free_slots / per_chunk_round
+                                       : ((uint64_t)free_slots * n_seen) / (2ull * keep * per_chunk_round);
+        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > 64 ? 64ull : rn));
+        __syncthreads();
     }
     // final: exactly min(count, keep) smallest keys, sorted, padded with +inf
-    uint32_t n = s_count;
+    uint32_t n = min(s_count, cap);
     if (n > keep) {
         block_select_keep(cbuf, n, keep, hist, s_misc);
         n = keep;
@@ -343,31 +401,42 @@ __global__ void __launch_bounds__(512, 1) k_scan_fast(SearchArgs a, uint32_t w2,
     bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
     uint64_t* candq = a.cand + q * keep;
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
+    if (threadIdx.x == 0 && s_overflow) a.meta[q].flag = 2;  // read by k_rescore
 }
 
 }  // namespace dev
 
-template <int M>
+template <int M, int R>
 static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
     constexpr int U = 2;
-    const uint32_t nwarps = 16;
+    const uint32_t nwarps = R == 2 ? 16 : 8;
     const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
-    const size_t smem = 4 * (size_t)dev::LutPlan<M>::words() + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
-    auto fn = dev::k_scan_fast<M, U>;
+    const size_t smem = 4 * (size_t)dev::LutPlan<M, R>::words() + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
+    auto fn = dev::k_scan_fast<M, U, R>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)nq, nwarps * 32, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
 }
 
-bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
-    // cap (2048) must exceed keep + one round of insertions (16 warps x 64)
-    if (keep > 512 || w2 > 4096) return false;
+bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, cudaStream_t st) {
+    // variant: 0 = default (replicated LUT), 1 = generic warp-buffer scan (not
+    // here), 2 = replicated, 3 = four copies, 4 = single table
+    if (keep > 512 || w2 > 4096 || variant == 1) return false;
+    const int r = variant == 3 ? 1 : (variant == 4 ? 0 : 2);
+#define VLQ_FAST(MM)                                                  \
+    do {                                                              \
+        if (r == 2) launch_fast_t<MM, 2>(a, nq, w2, keep, st);        \
+        else if (r == 1) launch_fast_t<MM, 1>(a, nq, w2, keep, st);   \
+        else launch_fast_t<MM, 0>(a, nq, w2, keep, st);               \
+        return true;                                                  \
+    } while (0)
     switch (a.m) {
-        case 16: launch_fast_t<16>(a, nq, w2, keep, st); return true;
-        case 8: launch_fast_t<8>(a, nq, w2, keep, st); return true;
-        case 4: launch_fast_t<4>(a, nq, w2, keep, st); return true;
+        case 16: VLQ_FAST(16);
+        case 8: VLQ_FAST(8);
+        case 4: VLQ_FAST(4);
         default: return false;
     }
+#undef VLQ_FAST
 }
 
 }  // namespace vlq

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(512) k_second_level(SearchArgs a, uint32_t w1,
     if (threadIdx.x == 0) {
         a.meta[q].scanned = s_scanned;
         a.meta[q].dmax = s_dmax;
+        a.meta[q].flag = 0;  // the fast scan may set 2 (candidate overflow)
     }
 }
 
@@ -399,8 +400,8 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, ui
         }
     }
     if (threadIdx.x == 0) {
-        uint32_t flag = 0;
-        if (scanned > keep && topk > 0) {
+        uint32_t flag = a.meta[q].flag == 2 ? 1u : 0u;
+        if (!flag && scanned > keep && topk > 0) {
             // every scanned entry x satisfies |fast_x - exact_x| <= eps
             const QueryMeta mt = a.meta[q];
             const double u = 5.9604644775390625e-08;  // 2^-24
