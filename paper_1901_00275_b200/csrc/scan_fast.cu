@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
     uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);                 // w2 + 1
     __shared__ uint32_t hist[256];
     __shared__ unsigned int s_misc[48];
-    __shared__ unsigned int s_count, s_overflow;
+    __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
 
     // 1. replicate the query's term5 table into the banked LUT (4 copies per STS.128)
@@ -227,7 +227,6 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
         if (threadIdx.x == 0) {
             cpref[w2] = total;
             s_count = 0;
-            s_overflow = 0;
             s_tau = ~0ull;
         }
     }
@@ -236,7 +235,6 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
     // balanced contiguous chunk range per warp
     const uint32_t c_lo = (uint32_t)(((uint64_t)nchunks * warp) / nwarps);
     const uint32_t c_hi = (uint32_t)(((uint64_t)nchunks * (warp + 1)) / nwarps);
-    const uint32_t per_warp_max = (nchunks + nwarps - 1) / nwarps;
     uint32_t t = 0;
     {
         uint32_t lo = 0, hi = w2;  // largest t with cpref[t] <= c_lo
@@ -302,7 +300,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
 
     uint32_t g = c_lo;        // next chunk to issue
     uint32_t done = 0;        // chunks consumed by this warp
-    uint32_t n_seen = 0;      // block-wide entries processed before this round (estimate)
+    uint64_t n_seen = 0;      // block-wide entries processed before this round (estimate)
     if (g < c_hi) {
         const uint32_t o = locate(g);
         issue(cw, lb, ev, o);
@@ -310,9 +308,13 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
         g++;
     }
     uint32_t rlen = 1;
-    while (done < per_warp_max) {  // block-uniform trip count
-        for (uint32_t r = 0; r < rlen && done < per_warp_max; r++, done++) {
-            if (c_lo + done >= c_hi) continue;
+    const uint32_t my_total = c_hi - c_lo;
+    // Rounds: every warp processes up to rlen chunks, then the block meets
+    // and flushes the shared buffer if needed.  A warp whose insertions do not
+    // fit the buffer writes nothing for that chunk and retries it next round
+    // (its chunk data is still in registers), so nothing is ever dropped.
+    while (__syncthreads_or(done < my_total)) {
+        for (uint32_t r = 0; r < rlen && done < my_total; r++) {
             // prefetch the next chunk into the other slot
             uint32_t o_nx = 0, L_nx = 0, pos_nx = 0;
             float av_nx = 0.f, Bc_nx = 0.f, cv_nx = 0.f;
@@ -344,16 +346,25 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
             }
             if (wtot) {
                 uint32_t base = 0;
-                if (lane == 0) base = atomicAdd(&s_count, wtot);
+                if (lane == 0) {
+                    // reserve only if the whole chunk fits
+                    unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&s_count);
+                    base = 0xffffffffu;
+                    while (cur + wtot <= cap) {
+                        const unsigned int prev = atomicCAS(&s_count, cur, cur + wtot);
+                        if (prev == cur) {
+                            base = cur;
+                            break;
+                        }
+                        cur = prev;
+                    }
+                }
                 base = __shfl_sync(0xffffffffu, base, 0);
+                if (base == 0xffffffffu) break;  // buffer full: retry this chunk after the flush
                 const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    if ((tk >> u) & 1u) {
-                        const uint32_t pos = base + __popc(bal[u] & lt);
-                        if (pos < cap) cbuf[pos] = key[u];
-                        else s_overflow = 1;  // correctness kept by the exact fallback
-                    }
+                    if ((tk >> u) & 1u) cbuf[base + __popc(bal[u] & lt)] = key[u];
                     base += __popc(bal[u]);
                 }
             }
@@ -367,11 +378,12 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
             }
             o_cur = o_nx; L_cur = L_nx; pos_cur = pos_nx; av_cur = av_nx; Bc_cur = Bc_nx; cv_cur = cv_nx;
             if (g < c_hi) g++;
+            done++;
         }
         __syncthreads();
         n_seen += rlen * nwarps * CH;
-        const uint32_t cnt = min(s_count, cap);
-        if (cnt > keep && (cnt > cap / 2 || done >= per_warp_max)) {  // block-uniform
+        const uint32_t cnt = s_count;
+        if (cnt > keep && cnt > cap / 2) {  // block-uniform
             const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -381,16 +393,15 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
             __syncthreads();
         }
         // next round length: expected insertions ~ keep * (new entries) / n_seen
-        // must fit the free space with a 2x margin; overflow -> exact fallback
-        const uint32_t free_slots = cap - min(s_count, cap);
+        // with a 4x margin; an underestimate only costs a retried chunk
+        const uint32_t free_slots = cap - s_count;
         const uint64_t per_chunk_round = (uint64_t)nwarps * CH;
         uint64_t rn = (s_tau == ~0ull) ? free_slots / per_chunk_round
-                                       : ((uint64_t)free_slots * n_seen) / (2ull * keep * per_chunk_round);
-        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > 64 ? 64ull : rn));
-        __syncthreads();
+                                       : ((uint64_t)free_slots * n_seen) / (4ull * keep * per_chunk_round);
+        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > 32 ? 32ull : rn));
     }
     // final: exactly min(count, keep) smallest keys, sorted, padded with +inf
-    uint32_t n = min(s_count, cap);
+    uint32_t n = s_count;
     if (n > keep) {
         block_select_keep(cbuf, n, keep, hist, s_misc);
         n = keep;
@@ -401,7 +412,6 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
     bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
     uint64_t* candq = a.cand + q * keep;
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
-    if (threadIdx.x == 0 && s_overflow) a.meta[q].flag = 2;  // read by k_rescore
 }
 
 }  // namespace dev
@@ -419,10 +429,11 @@ static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_
 }
 
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, cudaStream_t st) {
-    // variant: 0 = default (replicated LUT), 1 = generic warp-buffer scan (not
-    // here), 2 = replicated, 3 = four copies, 4 = single table
+    // variant: 0 = default (single table: more CTAs/SM beat fewer bank
+    // conflicts on B200), 1 = generic warp-buffer scan (not
+    // here), 2 = fully replicated LUT, 3 = four copies, 4 = single table
     if (keep > 512 || w2 > 4096 || variant == 1) return false;
-    const int r = variant == 3 ? 1 : (variant == 4 ? 0 : 2);
+    const int r = variant == 2 ? 2 : (variant == 3 ? 1 : 0);  // default: single table (measured best)
 #define VLQ_FAST(MM)                                                  \
     do {                                                              \
         if (r == 2) launch_fast_t<MM, 2>(a, nq, w2, keep, st);        \
