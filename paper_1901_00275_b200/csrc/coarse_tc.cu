@@ -1,0 +1,337 @@
+// K1: query/point -> first-level-centroid distances on the 5th-gen tensor
+// cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM).
+//
+//   approx(x, c) = |c|^2 - 2 <x, c>        (|x|^2 is row-constant, omitted)
+//
+// One CTA per 128 rows of X.  X's tile stays resident in shared memory; the
+// centroid matrix streams through a 3-stage ring of 128-centroid tiles
+// (cp.async.bulk into mbarrier-tracked stages).  The centroids are stored
+// once, at model upload, in the UMMA K-major "interleaved" core-matrix layout
+// ([tile][row/8][k/4][row%8][4 floats]), so every stage is ONE contiguous bulk
+// copy.  Warp 0 = producer, warp 1 = MMA issuer (one elected lane, 12
+// tcgen05.mma per tile at D = 96), warps 2..9 = epilogue (TMEM lane quadrant =
+// warp % 4, two warps per quadrant split the 128 accumulator columns); TMEM
+// holds two 128-column accumulators so tile t+1's MMAs overlap tile t's
+// epilogue.
+//
+// Epilogues:  ARGMIN keeps each row's 4 smallest (approx, centroid) pairs
+// (add path: assign_point, index.cpp:86-106);  STORE writes the approximate
+// row (coarse search stage: first_level_scan, search.cpp:11-36).  Neither is
+// the final answer: the refine kernels recompute exact reference-order
+// distances for every candidate within the TF32 error bound of the best and
+// certify that no other centroid can win (else an exact CUDA-core fallback).
+#include <cfloat>
+
+#include "kernels.h"
+#include "select.cuh"
+
+namespace vlq {
+namespace dev {
+
+constexpr int TC_M = 128;      // rows of X per CTA (UMMA M)
+constexpr int TC_N = 128;      // centroids per tile (UMMA N)
+constexpr int TC_STAGES = 3;
+constexpr int TC_THREADS = 320;  // 10 warps
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // SWIZZLE_NONE K-major canonical layout, Blackwell descriptor version 1
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int MODE>  // 0 = ARGMIN (top-4 per row), 1 = STORE (approx row)
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_coarse_tc(const float* __restrict__ X, uint64_t nx, uint32_t dim, const float* __restrict__ cent_tc,
+                const float* __restrict__ cnorm_pad, uint32_t ntiles, uint32_t kvalid, float* __restrict__ out_row,
+                uint64_t ldo, uint32_t* __restrict__ top_idx, float* __restrict__ top_d) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t tile_bytes = TC_N * dim * 4;  // one centroid tile
+    const uint32_t a_bytes = TC_M * dim * 4;
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + a_bytes;                                   // STAGES x tile_bytes
+    float* sNorm = reinterpret_cast<float*>(sB + TC_STAGES * tile_bytes);  // STAGES x TC_N
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sNorm + TC_STAGES * TC_N);
+    uint64_t* full = bars;                   // [STAGES]
+    uint64_t* empty = bars + TC_STAGES;      // [STAGES]
+    uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;            // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sMerge = reinterpret_cast<float*>(tmem_slot + 4);  // 128 rows x 4 (d) + 128 x 4 (idx)
+
+    const uint64_t row0 = (uint64_t)blockIdx.x * TC_M;
+    // ---- A tile: row-major global -> interleaved K-major smem (all threads)
+    const uint32_t nchunk = dim / 4;  // 16-byte chunks per row
+    for (uint32_t t = threadIdx.x; t < TC_M * nchunk; t += blockDim.x) {
+        const uint32_t r = t / nchunk, c = t % nchunk;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row0 + r < nx) v = __ldg(reinterpret_cast<const float4*>(X + (row0 + r) * dim) + c);
+        const uint32_t off = (r >> 3) * (nchunk * 128) + c * 128 + (r & 7) * 16;
+        *reinterpret_cast<float4*>(sA + off) = v;
+    }
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < TC_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // TMEM: two 128-column fp32 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A tile -> async proxy
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer: centroid tiles -> smem ring
+        if (lane == 0) {
+            for (uint32_t t = 0; t < ntiles; t++) {
+                const uint32_t s = t % TC_STAGES, ph = (t / TC_STAGES) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_expect_tx(&full[s], tile_bytes + TC_N * 4);
+                bulk_g2s(sB + s * tile_bytes, cent_tc + (size_t)t * TC_N * dim, tile_bytes, &full[s]);
+                bulk_g2s(sNorm + s * TC_N, cnorm_pad + (size_t)t * TC_N, TC_N * 4, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+                               ((uint32_t)(TC_M >> 4) << 24);
+        const uint32_t sbo = nchunk * 128, lbo = 128;
+        const uint32_t a_addr = smem_u32(sA);
+        for (uint32_t t = 0; t < ntiles; t++) {
+            const uint32_t s = t % TC_STAGES, ph = (t / TC_STAGES) & 1u;
+            const uint32_t b = t & 1u, bph = (t >> 1) & 1u;
+            mbar_wait(&tempty[b], bph ^ 1u);
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t b_addr = smem_u32(sB + s * tile_bytes);
+                for (uint32_t k = 0; k < dim / 8; k++) {  // K = 8 tf32 per MMA = two 16-B chunks
+                    const uint64_t ad = umma_desc(a_addr + k * 256, lbo, sbo);
+                    const uint64_t bd = umma_desc(b_addr + k * 256, lbo, sbo);
+                    umma_tf32(tmem_base + b * TC_N, ad, bd, idesc, k > 0 ? 1u : 0u);
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&tfull[b]);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- epilogue warps 2..9
+        const uint32_t quad = warp & 3u;            // TMEM lanes 32*quad ..
+        const uint32_t half = (warp - 2u) >> 2;     // column half 0/1
+        const uint32_t r = quad * 32 + lane;        // row within the tile
+        const uint64_t grow = row0 + r;
+        float bd[4] = {FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX};
+        uint32_t bi[4] = {0, 0, 0, 0};
+        for (uint32_t t = 0; t < ntiles; t++) {
+            const uint32_t b = t & 1u, bph = (t >> 1) & 1u;
+            const uint32_t s = t % TC_STAGES;
+            mbar_wait(&tfull[b], bph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float* nrm = sNorm + s * TC_N;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                uint32_t acc[32];
+                const uint32_t col = half * 64 + h * 32;
+                tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TC_N + col, acc);
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const uint32_t cidx = t * TC_N + col + j;
+                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), nrm[col + j]);
+                    if constexpr (MODE == 0) {
+                        if (d < bd[3]) {  // sorted insert, ties keep the lower index (earlier)
+                            if (d < bd[2]) {
+                                bd[3] = bd[2]; bi[3] = bi[2];
+                                if (d < bd[1]) {
+                                    bd[2] = bd[1]; bi[2] = bi[1];
+                                    if (d < bd[0]) { bd[1] = bd[0]; bi[1] = bi[0]; bd[0] = d; bi[0] = cidx; }
+                                    else { bd[1] = d; bi[1] = cidx; }
+                                } else { bd[2] = d; bi[2] = cidx; }
+                            } else { bd[3] = d; bi[3] = cidx; }
+                        }
+                    } else {
+                        if (grow < nx && cidx < kvalid) out_row[grow * ldo + cidx] = d;
+                    }
+                }
+            }
+            // the tile's norms are read: the stage may only be refilled after
+            // both the MMA (commit) and this epilogue are done with it
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        if constexpr (MODE == 0) {
+            // merge the two column halves' top-4 lists for each row
+            float* md = sMerge;                 // [128][4]
+            uint32_t* mi = reinterpret_cast<uint32_t*>(sMerge + TC_M * 4);
+            if (half == 1) {
+                for (int j = 0; j < 4; j++) {
+                    md[r * 4 + j] = bd[j];
+                    mi[r * 4 + j] = bi[j];
+                }
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+            if (half == 0 && grow < nx) {
+                float od[4];
+                uint32_t oi[4];
+                int a = 0, c = 0;
+                for (int j = 0; j < 4; j++) {  // merge two sorted lists by (d, idx)
+                    const float xd = bd[a], yd = md[r * 4 + c];
+                    const uint32_t xi = bi[a], yi = mi[r * 4 + c];
+                    const bool takex = (xd < yd) || (xd == yd && xi < yi);
+                    od[j] = takex ? xd : yd;
+                    oi[j] = takex ? xi : yi;
+                    if (takex) a++;
+                    else c++;
+                }
+                for (int j = 0; j < 4; j++) {
+                    top_d[grow * 4 + j] = od[j];
+                    top_idx[grow * 4 + j] = oi[j];
+                }
+            }
+        }
+    }
+    // the producer's last stage refills were not consumed past ntiles; all
+    // MMAs completed (epilogue waited on every tfull)
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+}
+
+// Re-lay centroids [K, D] row-major into the UMMA interleaved K-major tile
+// layout, padding rows to a multiple of 128 (zero rows, +inf norms).
+__global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, uint32_t dim, uint32_t ntiles,
+                                     float* __restrict__ out, float* __restrict__ norm_out) {
+    const uint32_t nchunk = dim / 4;
+    const uint64_t total = (uint64_t)ntiles * TC_N * nchunk;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t row = t / nchunk;
+        const uint32_t c = (uint32_t)(t % nchunk);
+        const uint32_t tile = (uint32_t)(row / TC_N), r = (uint32_t)(row % TC_N);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < k) v = reinterpret_cast<const float4*>(C + row * dim)[c];
+        const uint64_t off = (uint64_t)tile * TC_N * dim + (r >> 3) * (nchunk * 32) + c * 32 + (r & 7) * 4;
+        *reinterpret_cast<float4*>(out + off) = v;
+    }
+    for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < (uint64_t)ntiles * TC_N;
+         row += (uint64_t)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        if (row < k)
+            for (uint32_t d = 0; d < dim; d++) acc = dot_step(acc, C[row * dim + d], C[row * dim + d]);
+        norm_out[row] = row < k ? acc : __int_as_float(0x7f800000);
+    }
+}
+
+}  // namespace dev
+
+size_t coarse_tc_smem(uint32_t dim) {
+    return (size_t)dev::TC_M * dim * 4 + (size_t)dev::TC_STAGES * dev::TC_N * dim * 4 +
+           (size_t)dev::TC_STAGES * dev::TC_N * 4 + 2 * dev::TC_STAGES * 8 + 4 * 8 + 16 + (size_t)dev::TC_M * 8 * 4 +
+           1024;
+}
+
+bool coarse_tc_supported(uint32_t dim) {
+    return dim % 8 == 0 && dim >= 8 && coarse_tc_smem(dim) <= 227 * 1024;
+}
+
+void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* norm_out, cudaStream_t st) {
+    const uint32_t ntiles = (k + dev::TC_N - 1) / dev::TC_N;
+    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, norm_out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cnorm,
+                      uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d, cudaStream_t st) {
+    if (nx == 0) return;
+    const uint32_t ntiles = (k + dev::TC_N - 1) / dev::TC_N;
+    const size_t smem = coarse_tc_smem(dim);
+    const unsigned grid = (unsigned)((nx + dev::TC_M - 1) / dev::TC_M);
+    if (mode == 0) {
+        CUDA_CHECK(cudaFuncSetAttribute(dev::k_coarse_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dev::k_coarse_tc<0><<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cnorm, ntiles, k, out_row, ldo,
+                                                                  top_idx, top_d);
+    } else {
+        CUDA_CHECK(cudaFuncSetAttribute(dev::k_coarse_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dev::k_coarse_tc<1><<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cnorm, ntiles, k, out_row, ldo,
+                                                                  top_idx, top_d);
+    }
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq
