@@ -109,6 +109,8 @@ SearchArgs Engine::search_args() const {
     a.hi = hi_;
     a.lam_absmax = std::max(std::max(std::fabs(lo_), std::fabs(hi_)), 0.0f);
     a.emax = emax_;
+    a.lam_delta = (hi_ - lo_) * (1.0f / 256.0f);
+    a.lam0 = lo_ + 0.5f * a.lam_delta;
     a.centroids = centroids_.p;
     a.nbr = nbr_.p;
     a.elen = elen_.p;

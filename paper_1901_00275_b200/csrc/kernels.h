@@ -21,6 +21,7 @@ struct SearchArgs {
     // index (replicated coarse structures + this shard's posting lists)
     uint32_t dim, k, n, m;
     float lo, hi, lam_absmax, emax;
+    float lam_delta, lam0;  // fast-path dequantization: lam ~= lam0 + b * lam_delta
     const float* centroids;
     const uint32_t* nbr;
     const float* elen;

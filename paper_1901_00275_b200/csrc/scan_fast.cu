@@ -246,21 +246,13 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
         t = lo;
     }
     const float* wsq = a.ws + q * a.k;
-    const float delta = (a.hi - a.lo) * (1.0f / 256.0f);
-    const float lam0 = a.lo + 0.5f * delta;
+    const float delta = a.lam_delta, lam0 = a.lam0;  // dequantization affine map
     uint32_t L = 0, pos0 = 0;
     const uint8_t* codes_c = nullptr;
     const uint8_t* lam_c = nullptr;
     const float* e_c = nullptr;
     float av = 0.f, Bc = 0.f, cv = 0.f;
     uint32_t loaded_t = 0xffffffffu;
-
-    // chunk data double buffer (registers; static indices only)
-    uint32_t cw[U][NW], ncw[U][NW];
-    uint32_t lb[U], nlb[U];
-    float ev[U], nev[U];
-    uint32_t o_cur = 0, L_cur = 0, pos_cur = 0;
-    float av_cur = 0.f, Bc_cur = 0.f, cv_cur = 0.f;
 
     auto locate = [&](uint32_t g) {  // walks t forward to the cell holding chunk g
         while (cpref[t + 1] <= g) t++;
@@ -281,64 +273,55 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
         }
         return (g - cpref[t]) * CH;
     };
-    auto issue = [&](uint32_t (&xcw)[U][NW], uint32_t (&xlb)[U], float (&xev)[U], uint32_t o) {
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const uint32_t idx = o + u * 32 + lane;
-            if (idx < L) {
-                load_code_vec<M>(codes_c + (size_t)idx * M, xcw[u]);
-                xlb[u] = __ldg(lam_c + idx);
-                xev[u] = __ldg(e_c + idx);
-            } else {
-#pragma unroll
-                for (int w = 0; w < NW; w++) xcw[u][w] = 0;
-                xlb[u] = 0;
-                xev[u] = 0.0f;
-            }
-        }
-    };
 
-    uint32_t g = c_lo;        // next chunk to issue
     uint32_t done = 0;        // chunks consumed by this warp
     uint64_t n_seen = 0;      // block-wide entries processed before this round (estimate)
-    if (g < c_hi) {
-        const uint32_t o = locate(g);
-        issue(cw, lb, ev, o);
-        o_cur = o; L_cur = L; pos_cur = pos0; av_cur = av; Bc_cur = Bc; cv_cur = cv;
-        g++;
-    }
     uint32_t rlen = 1;
     const uint32_t my_total = c_hi - c_lo;
     // Rounds: every warp processes up to rlen chunks, then the block meets
     // and flushes the shared buffer if needed.  A warp whose insertions do not
-    // fit the buffer writes nothing for that chunk and retries it next round
-    // (its chunk data is still in registers), so nothing is ever dropped.
+    // fit the buffer writes nothing for that chunk and redoes it next round,
+    // so nothing is ever dropped.
     while (__syncthreads_or(done < my_total)) {
         for (uint32_t r = 0; r < rlen && done < my_total; r++) {
-            // prefetch the next chunk into the other slot
-            uint32_t o_nx = 0, L_nx = 0, pos_nx = 0;
-            float av_nx = 0.f, Bc_nx = 0.f, cv_nx = 0.f;
-            if (g < c_hi) {
-                o_nx = locate(g);
-                issue(ncw, nlb, nev, o_nx);
-                L_nx = L; pos_nx = pos0; av_nx = av; Bc_nx = Bc; cv_nx = cv;
+            const uint32_t o = locate(c_lo + done);
+            uint32_t cw[U][NW];
+            uint32_t lb[U];
+            float ev[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t idx = o + u * 32 + lane;
+                if (idx < L) {
+                    load_code_vec<M>(codes_c + (size_t)idx * M, cw[u]);
+                    lb[u] = __ldg(lam_c + idx);
+                    ev[u] = __ldg(e_c + idx);
+                } else {
+#pragma unroll
+                    for (int w = 0; w < NW; w++) cw[u][w] = 0;
+                    lb[u] = 0;
+                    ev[u] = 0.0f;
+                }
             }
             const uint64_t tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
             uint64_t key[U];
             uint32_t tk = 0;
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const uint32_t idx = o_cur + u * 32 + lane;
-                const float lam = fmaf((float)lb[u], delta, lam0);
-                const float t1 = fmaf(lam, fmaf(lam, cv_cur, Bc_cur), av_cur);
-                const float s5 = lut_sum<M, R>(lut, cw[u], lane);
-                const float dist = fmaf(-2.0f, s5, t1 + ev[u]);
-                uint32_t ub = __float_as_uint(dist);
-                ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
-                key[u] = idx < L_cur ? (((uint64_t)ub << 32) | (pos_cur + idx)) : ~0ull;
+                key[u] = ~0ull;
+                if (o + u * 32 < L) {  // warp-uniform: skip fully empty slots
+                    const uint32_t idx = o + u * 32 + lane;
+                    const float lam = fmaf((float)lb[u], delta, lam0);
+                    const float t1 = fmaf(lam, fmaf(lam, cv, Bc), av);
+                    const float s5 = lut_sum<M, R>(lut, cw[u], lane);
+                    const float dist = fmaf(-2.0f, s5, t1 + ev[u]);
+                    uint32_t ub = __float_as_uint(dist);
+                    ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
+                    if (idx < L) key[u] = ((uint64_t)ub << 32) | (pos0 + idx);
+                }
                 tk |= (key[u] < tau ? 1u : 0u) << u;
             }
-            uint32_t bal[U], wtot = 0;
+            uint32_t wtot = 0;
+            uint32_t bal[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 bal[u] = __ballot_sync(0xffffffffu, (tk >> u) & 1u);
@@ -360,7 +343,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
                     }
                 }
                 base = __shfl_sync(0xffffffffu, base, 0);
-                if (base == 0xffffffffu) break;  // buffer full: retry this chunk after the flush
+                if (base == 0xffffffffu) break;  // buffer full: redo this chunk after the flush
                 const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
                 for (int u = 0; u < U; u++) {
@@ -368,16 +351,6 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
                     base += __popc(bal[u]);
                 }
             }
-            // rotate the double buffer
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-#pragma unroll
-                for (int w = 0; w < NW; w++) cw[u][w] = ncw[u][w];
-                lb[u] = nlb[u];
-                ev[u] = nev[u];
-            }
-            o_cur = o_nx; L_cur = L_nx; pos_cur = pos_nx; av_cur = av_nx; Bc_cur = Bc_nx; cv_cur = cv_nx;
-            if (g < c_hi) g++;
             done++;
         }
         __syncthreads();
@@ -393,7 +366,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
             __syncthreads();
         }
         // next round length: expected insertions ~ keep * (new entries) / n_seen
-        // with a 4x margin; an underestimate only costs a retried chunk
+        // with a 4x margin; an underestimate only costs a redone chunk
         const uint32_t free_slots = cap - s_count;
         const uint64_t per_chunk_round = (uint64_t)nwarps * CH;
         uint64_t rn = (s_tau == ~0ull) ? free_slots / per_chunk_round
@@ -418,7 +391,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
 
 template <int M, int R>
 static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
-    constexpr int U = 2;
+    constexpr int U = 4;
     const uint32_t nwarps = R == 2 ? 16 : 8;
     const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
     const size_t smem = 4 * (size_t)dev::LutPlan<M, R>::words() + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
