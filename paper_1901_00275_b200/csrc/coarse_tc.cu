@@ -109,14 +109,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     k_coarse_tc(const float* __restrict__ X, uint64_t nx, uint32_t dim, const float* __restrict__ cent_tc,
                 const float* __restrict__ cnorm_pad, uint32_t ntiles, uint32_t kvalid, float* __restrict__ out_row,
                 uint64_t ldo, uint32_t* __restrict__ top_idx, float* __restrict__ top_d) {
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t tile_bytes = TC_N * dim * 4;  // one centroid tile
     const uint32_t a_bytes = TC_M * dim * 4;
     unsigned char* sA = smem;
     unsigned char* sB = smem + a_bytes;                                   // STAGES x tile_bytes
-    float* sNorm = reinterpret_cast<float*>(sB + TC_STAGES * tile_bytes);  // STAGES x TC_N
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sNorm + TC_STAGES * TC_N);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + TC_STAGES * tile_bytes);
     uint64_t* full = bars;                   // [STAGES]
     uint64_t* empty = bars + TC_STAGES;      // [STAGES]
     uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]
@@ -161,9 +160,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (uint32_t t = 0; t < ntiles; t++) {
                 const uint32_t s = t % TC_STAGES, ph = (t / TC_STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], tile_bytes + TC_N * 4);
+                mbar_expect_tx(&full[s], tile_bytes);
                 bulk_g2s(sB + s * tile_bytes, cent_tc + (size_t)t * TC_N * dim, tile_bytes, &full[s]);
-                bulk_g2s(sNorm + s * TC_N, cnorm_pad + (size_t)t * TC_N, TC_N * 4, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -200,10 +198,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint32_t bi[4] = {0, 0, 0, 0};
         for (uint32_t t = 0; t < ntiles; t++) {
             const uint32_t b = t & 1u, bph = (t >> 1) & 1u;
-            const uint32_t s = t % TC_STAGES;
             mbar_wait(&tfull[b], bph);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const float* nrm = sNorm + s * TC_N;
+            const float* nrm = cnorm_pad + (size_t)t * TC_N;  // warp-uniform broadcast loads
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 uint32_t acc[32];
@@ -212,7 +209,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     const uint32_t cidx = t * TC_N + col + j;
-                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), nrm[col + j]);
+                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), __ldg(nrm + col + j));
                     if constexpr (MODE == 0) {
                         if (d < bd[3]) {  // sorted insert, ties keep the lower index (earlier)
                             if (d < bd[2]) {
@@ -229,8 +226,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                 }
             }
-            // the tile's norms are read: the stage may only be refilled after
-            // both the MMA (commit) and this epilogue are done with it
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[b]);
@@ -301,9 +296,8 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
 }  // namespace dev
 
 size_t coarse_tc_smem(uint32_t dim) {
-    return (size_t)dev::TC_M * dim * 4 + (size_t)dev::TC_STAGES * dev::TC_N * dim * 4 +
-           (size_t)dev::TC_STAGES * dev::TC_N * 4 + 2 * dev::TC_STAGES * 8 + 4 * 8 + 16 + (size_t)dev::TC_M * 8 * 4 +
-           1024;
+    return (size_t)dev::TC_M * dim * 4 + (size_t)dev::TC_STAGES * dev::TC_N * dim * 4 + 2 * dev::TC_STAGES * 8 +
+           4 * 8 + 16 + (size_t)dev::TC_M * 8 * 4 + 1024;
 }
 
 bool coarse_tc_supported(uint32_t dim) {
@@ -331,6 +325,212 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
         dev::k_coarse_tc<1><<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cnorm, ntiles, k, out_row, ldo,
                                                                   top_idx, top_d);
     }
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq
+
+// ---------------------------------------------------------------------------
+// Exact refinement + certificate of the tensor-core candidates.
+//
+// |approx(x,c) + |x|^2 - sqdist(x,c)| <= eps(x) for every centroid c, with
+//   eps = 2 (2^-9 + D 2^-24) |x| cmax + D 2^-24 ((|x| + cmax)^2 + cmax^2) + 2^-23 (|x| + cmax)^2
+// (TF32 operands truncate to 10 mantissa bits: relative error <= 2^-10 per
+// factor; fp32 accumulation; the fp32 norm and the exact sequential sqdist
+// each add D u |.|), times a 1.5 safety factor.  So every centroid whose
+// exact distance can beat the approximate best lies within 2 eps of it.
+// ---------------------------------------------------------------------------
+namespace vlq {
+namespace dev {
+
+__device__ __forceinline__ float tc_eps(float xnorm2, float cmax, uint32_t dim) {
+    const float xn = sqrtf(xnorm2);
+    const float s = xn + cmax;
+    const float u = 5.9604645e-08f;
+    return 1.5f * (2.0f * (1.953125e-3f + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + 2.0f * u * s * s) +
+           1e-30f;
+}
+
+// Add path: exact argmin among the 4 tensor-core candidates (strict '<' from
+// FLT_MAX, lowest id on ties: index.cpp:96-103) when the candidate set is
+// provably complete; otherwise the point goes to the exact full scan.
+__global__ void k_refine_argmin(const float* __restrict__ X, uint64_t nx, uint32_t dim,
+                                const float* __restrict__ C, const uint32_t* __restrict__ top_idx,
+                                const float* __restrict__ top_d, float cmax, uint32_t* __restrict__ best,
+                                uint32_t* __restrict__ flagged, unsigned int* __restrict__ nflag) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nx; p += (uint64_t)gridDim.x * blockDim.x) {
+        const float* x = X + p * dim;
+        float xn = 0.0f;
+        for (uint32_t d = 0; d < dim; d++) xn = fmaf(x[d], x[d], xn);
+        const float eps = tc_eps(xn, cmax, dim);
+        const float lim = top_d[p * 4] + 2.0f * eps;
+        if (top_d[p * 4 + 3] <= lim) {  // a 5th centroid could also be within the margin
+            flagged[atomicAdd(nflag, 1u)] = (uint32_t)p;
+            continue;
+        }
+        uint64_t bk = ~0ull;
+        for (int j = 0; j < 4; j++) {
+            if (top_d[p * 4 + j] > lim) break;
+            const uint32_t c = top_idx[p * 4 + j];
+            const float* cp = C + (uint64_t)c * dim;
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, x[d], cp[d]);
+            const uint64_t key = (acc < FLT_MAX) ? make_key(acc, c) : ~0ull;
+            bk = key < bk ? key : bk;
+        }
+        best[p] = bk == ~0ull ? 0u : (uint32_t)bk;
+    }
+}
+
+__global__ void k_gather_rows_list(const float* __restrict__ X, uint32_t dim, const uint32_t* __restrict__ rows,
+                                   uint32_t nr, float* __restrict__ out) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (uint64_t)nr * dim;
+         t += (uint64_t)gridDim.x * blockDim.x)
+        out[t] = X[(uint64_t)rows[t / dim] * dim + t % dim];
+}
+
+__global__ void k_scatter_u32(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ rows, uint32_t nr,
+                              uint32_t* __restrict__ out) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += gridDim.x * blockDim.x) out[rows[t]] = vals[t];
+}
+
+// Search path: exact top-w1 among the L approximate candidates of each query
+// (top[q*L..]), written back as ascending ids, exact distances stored into
+// the ws row; certificate: L-th approximate value + |y|^2 - eps > exact
+// w1-th, else the query is listed for an exact full row.
+__global__ void k_refine_first(const float* __restrict__ Y, uint32_t dim, const float* __restrict__ C,
+                               float* __restrict__ ws, uint32_t k, const uint32_t* __restrict__ cand, uint32_t L,
+                               uint32_t w1, float cmax, uint32_t* __restrict__ top, uint32_t* __restrict__ flagged,
+                               unsigned int* __restrict__ nflag) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // npow2
+    float* ys = reinterpret_cast<float*>(smem + 8 * 2048);
+    __shared__ unsigned int s_amax;  // order-preserving bits of the largest candidate approx
+    __shared__ float s_yn;
+    const uint64_t q = blockIdx.x;
+    uint32_t np2 = 1;
+    while (np2 < L) np2 <<= 1;
+    for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
+    if (threadIdx.x == 0) s_amax = 0u;
+    __syncthreads();
+    float* wsq = ws + q * k;
+    const uint32_t* cq = cand + q * L;
+    float amax = -__int_as_float(0x7f800000);
+    for (uint32_t t = threadIdx.x; t < np2; t += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (t < L) {
+            const uint32_t c = cq[t];
+            amax = fmaxf(amax, wsq[c]);  // approximate value (before overwrite)
+            const float* cp = C + (uint64_t)c * dim;
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], cp[d]);
+            key = make_key(acc, c);
+        }
+        keys[t] = key;
+    }
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_amax, ord_float(amax));
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, np2, threadIdx.x, blockDim.x);
+    if (threadIdx.x == 0) {
+        float yn = 0.0f;
+        for (uint32_t d = 0; d < dim; d++) yn = fmaf(ys[d], ys[d], yn);
+        s_yn = yn;
+    }
+    __syncthreads();
+    // certificate (all non-candidates have approx >= the L-th candidate's)
+    if (threadIdx.x == 0) {
+        const float eps = tc_eps(s_yn, cmax, dim);
+        const float exact_w1 = unord_float((uint32_t)(keys[w1 - 1] >> 32));
+        const double lower = (double)unord_float(s_amax) + (double)s_yn - (double)eps;
+        if (!(L < k ? lower > (double)exact_w1 : true)) flagged[atomicAdd(nflag, 1u)] = (uint32_t)q;
+    }
+    // exact values into the ws row (the downstream kernels read them)
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+        const uint64_t key = keys[t];
+        wsq[(uint32_t)key] = unord_float((uint32_t)(key >> 32));
+    }
+    __syncthreads();
+    // the w1 winners, re-sorted by id (second_level_rank's tie order needs ascending ids)
+    for (uint32_t t = threadIdx.x; t < np2; t += blockDim.x)
+        keys[t] = t < w1 ? (uint64_t)(uint32_t)keys[t] : ~0ull;
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, np2, threadIdx.x, blockDim.x);
+    for (uint32_t t = threadIdx.x; t < w1; t += blockDim.x) top[q * w1 + t] = (uint32_t)keys[t];
+}
+
+// Exact full ws rows for the listed queries (certificate failures).
+__global__ void k_exact_rows(const float* __restrict__ Y, uint32_t dim, const float* __restrict__ C, uint32_t k,
+                             float* __restrict__ ws, const uint32_t* __restrict__ qlist,
+                             const unsigned int* __restrict__ count) {
+    extern __shared__ float ysm[];
+    if (blockIdx.x >= *count) return;
+    const uint64_t q = qlist[blockIdx.x];
+    for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ysm[d] = Y[q * dim + d];
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < k; c += blockDim.x) {
+        const float* cp = C + (uint64_t)c * dim;
+        float acc = 0.0f;
+        for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ysm[d], cp[d]);
+        ws[q * k + c] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(512) k_first_level_list(const float* __restrict__ ws, uint32_t k, uint32_t w1,
+                                                          uint32_t* __restrict__ top, const uint32_t* __restrict__ qlist,
+                                                          const unsigned int* __restrict__ count) {
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    if (blockIdx.x >= *count) return;
+    const uint64_t q = qlist[blockIdx.x];
+    block_select_ordered(ws + q * k, k, w1, top + q * w1, hist, scan);
+}
+
+}  // namespace dev
+
+void launch_refine_argmin(const float* X, uint64_t nx, uint32_t dim, const float* C, const uint32_t* top_idx,
+                          const float* top_d, float cmax, uint32_t* best, uint32_t* flagged, unsigned int* nflag,
+                          cudaStream_t st) {
+    if (nx == 0) return;
+    dev::k_refine_argmin<<<(unsigned)dev::umin64((nx + 127) / 128, 4736), 128, 0, st>>>(X, nx, dim, C, top_idx, top_d,
+                                                                                     cmax, best, flagged, nflag);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_gather_rows_list(const float* X, uint32_t dim, const uint32_t* rows, uint32_t nr, float* out,
+                             cudaStream_t st) {
+    if (nr == 0) return;
+    dev::k_gather_rows_list<<<1184, 256, 0, st>>>(X, dim, rows, nr, out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_scatter_u32(const uint32_t* vals, const uint32_t* rows, uint32_t nr, uint32_t* out, cudaStream_t st) {
+    if (nr == 0) return;
+    dev::k_scatter_u32<<<(nr + 255) / 256, 256, 0, st>>>(vals, rows, nr, out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float* C, float* ws, uint32_t k,
+                         const uint32_t* cand, uint32_t L, uint32_t w1, float cmax, uint32_t* top, uint32_t* flagged,
+                         unsigned int* nflag, cudaStream_t st) {
+    if (nq == 0) return;
+    const size_t smem = 8 * 2048 + (size_t)dim * 4;
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_refine_first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_refine_first<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, ws, k, cand, L, w1, cmax, top, flagged, nflag);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,
+                       const uint32_t* qlist, const unsigned int* count, cudaStream_t st) {
+    if (nq == 0) return;
+    dev::k_exact_rows<<<(unsigned)nq, 256, dim * 4, st>>>(Y, dim, C, k, ws, qlist, count);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_first_level_list(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top,
+                             const uint32_t* qlist, const unsigned int* count, cudaStream_t st) {
+    if (nq == 0) return;
+    dev::k_first_level_list<<<(unsigned)nq, 512, 0, st>>>(ws, k, w1, top, qlist, count);
     CUDA_LAUNCH_CHECK();
 }
 

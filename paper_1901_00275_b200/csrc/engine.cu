@@ -4,6 +4,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -59,6 +60,8 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = (uint32_t)std::atoi(v);
     if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
         throw std::runtime_error("engine: invalid shard configuration");
     int ndev = 0;
@@ -173,7 +176,52 @@ void Engine::upload_model() {
     launch_tables(centroids_.p, k_, dim_, pq_.p, m_, t2_.p, t3_.p, stream_);
     if (!model_.t3.empty())
         CUDA_CHECK(cudaMemcpyAsync(t3_.p, model_.t3.data(), model_.t3.size() * 4, cudaMemcpyHostToDevice, stream_));
+    // tensor-core coarse stage: centroids re-laid out for tcgen05 (UMMA
+    // K-major interleaved tiles of 128) + exact norms
+    tc_ = cfg_.use_tc && coarse_tc_supported(dim_) && k_ >= cfg_.tc_min_k;
+    if (tc_) {
+        const uint32_t ntiles = (k_ + 127) / 128;
+        cent_tc_.alloc((size_t)ntiles * 128 * dim_);
+        cnorm_tc_.alloc((size_t)ntiles * 128);
+        launch_relayout_centroids(centroids_.p, k_, dim_, cent_tc_.p, cnorm_tc_.p, stream_);
+        double mx = 0.0;
+        for (uint32_t i = 0; i < k_; i++) {
+            double s = 0.0;
+            for (uint32_t d = 0; d < dim_; d++) s += (double)model_.centroids[(size_t)i * dim_ + d] * model_.centroids[(size_t)i * dim_ + d];
+            mx = std::max(mx, s);
+        }
+        cmax_ = (float)(std::sqrt(mx) * (1.0 + 1e-6)) + 1e-30f;
+    }
     CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+// Exact nearest centroid (assign_point, index.cpp:86-106) for a chunk: the
+// tensor-core GEMM proposes 4 candidates per point, k_refine_argmin settles
+// them exactly when the TF32 bound proves the set complete, and the rest go
+// through the exact CUDA-core full scan.
+void Engine::assign_chunk(const float* X, uint64_t nx, uint32_t* best, cudaStream_t st) {
+    AddArgs a = add_args();
+    if (!tc_) {
+        launch_assign_nearest(a, X, nx, best, st);
+        return;
+    }
+    tc_idx_.alloc(nx * 4);
+    tc_d_.alloc(nx * 4);
+    tc_flag_.alloc(nx);
+    launch_coarse_tc(0, X, nx, dim_, cent_tc_.p, cnorm_tc_.p, k_, nullptr, 0, tc_idx_.p, tc_d_.p, st);
+    CUDA_CHECK(cudaMemsetAsync(err_.p + 5, 0, 4, st));
+    launch_refine_argmin(X, nx, dim_, centroids_.p, tc_idx_.p, tc_d_.p, cmax_, best, tc_flag_.p, err_.p + 5, st);
+    unsigned int nflag = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 5, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (nflag) {
+        stats_.tc_refine_fallbacks += nflag;
+        tc_rows_.alloc((size_t)nflag * dim_);
+        tc_best_.alloc(nflag);
+        launch_gather_rows_list(X, dim_, tc_flag_.p, nflag, tc_rows_.p, st);
+        launch_assign_nearest(a, tc_rows_.p, nflag, tc_best_.p, st);
+        launch_scatter_u32(tc_best_.p, tc_flag_.p, nflag, best, st);
+    }
 }
 
 void Engine::upload_lists(const HostLists& L) {
@@ -244,7 +292,7 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
         for (uint64_t f = 0; f < nb; f += chunk) {
             uint64_t c = std::min(chunk, nb - f);
             src(f, c, X.p, st);
-            launch_assign_nearest(a, X.p, c, best.p, st);
+            assign_chunk(X.p, c, best.p, st);
             launch_encode(a, X.p, c, best.p, 0, nullptr, lam.p, nullptr, nullptr, nullptr, nullptr, st);
             launch_minmax(lam.p, c, reinterpret_cast<float*>(err_.p + 3), st);
         }
@@ -277,7 +325,7 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
         for (uint64_t f = 0; f < nb; f += chunk) {
             uint64_t c = std::min(chunk, nb - f);
             src(f, c, X.p, st);
-            launch_assign_nearest(a, X.p, c, best.p, st);
+            assign_chunk(X.p, c, best.p, st);
             launch_encode(a, X.p, c, best.p, clamp_ ? 1 : 0, cells.p + f, nullptr, codes_pt.p + f * m_, lamb_pt.p + f,
                           eterm_pt.p + f, err_.p + 1, st);
         }
@@ -373,7 +421,7 @@ void Engine::encode_host(const float* x, uint64_t nx, uint32_t* cells, float* la
     CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 8 * sizeof(unsigned int), st));
     CUDA_CHECK(cudaMemcpyAsync(X.p, x, nx * dim_ * 4, cudaMemcpyHostToDevice, st));
     AddArgs a = add_args();
-    launch_assign_nearest(a, X.p, nx, best.p, st);
+    assign_chunk(X.p, nx, best.p, st);
     launch_encode(a, X.p, nx, best.p, clamp_ ? 1 : 0, cl.p, lam.p, cd.p, lb.p, et.p, err_.p + 1, st);
     if (cells) CUDA_CHECK(cudaMemcpyAsync(cells, cl.p, nx * 4, cudaMemcpyDeviceToHost, st));
     if (lambdas) CUDA_CHECK(cudaMemcpyAsync(lambdas, lam.p, nx * 4, cudaMemcpyDeviceToHost, st));
@@ -419,13 +467,14 @@ void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alp
     DeviceGuard g(cfg_.device);
     const uint32_t w2 = w2_of(w1, alpha, n_);
     const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
-    const uint64_t per_q = 4ull * k_ + 4ull * w1 + 4ull * w1 * n_ + 4ull * w2 + 4ull * VLQ_KSUB * m_ + 8ull * keep +
+    const uint64_t per_q = 4ull * k_ + 8ull * w1 + 128 + 4ull * w1 * n_ + 4ull * w2 + 4ull * VLQ_KSUB * m_ + 8ull * keep +
                            sizeof(QueryMeta) + 4;
     uint64_t tile = std::max<uint64_t>(1, cfg_.workspace_bytes / per_q);
     tile = std::min<uint64_t>(tile, cfg_.max_tile);
     tile = std::min<uint64_t>(tile, nq);
     ws_.alloc(tile * k_);
     top_.alloc(tile * w1);
+    cand_top_.alloc(tile * (uint64_t)std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2)));
     dbuf_.alloc(tile * (uint64_t)w1 * n_);
     sel_.alloc(tile * w2);
     t5_.alloc(tile * VLQ_KSUB * m_);
@@ -446,15 +495,36 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
     };
     uint64_t launches = 0;
+    const uint32_t L = std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2));
+    const bool tc = tc_ && L <= 2048 && w1 < k_;
     mark(PH_COARSE);
-    launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
+    if (tc) {
+        // approximate rows on the tensor cores, then top-L on them
+        launch_coarse_tc(1, d_q, nt, dim_, cent_tc_.p, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
+        launches += 1;
+    } else {
+        launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
+        launches += 1;
+    }
     mark(PH_FIRST);
-    launch_first_level(ws_.p, nt, k_, w1, top_.p, st);
+    if (tc) {
+        launch_first_level(ws_.p, nt, k_, L, cand_top_.p, st);
+        CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
+        launch_refine_first(d_q, nt, dim_, centroids_.p, ws_.p, k_, cand_top_.p, L, w1, cmax_, top_.p, qlist_.p,
+                            err_.p + 6, st);
+        launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
+        launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
+        launches += 4;
+        a.Y = d_q;
+    } else {
+        launch_first_level(ws_.p, nt, k_, w1, top_.p, st);
+        launches += 1;
+    }
     mark(PH_SECOND);
     launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
     launch_term5(d_q, pq_.p, dim_, m_, t5_.p, meta_.p, nt, st);
-    launches += 4;
+    launches += 2;
     const uint32_t keep_x = next_pow2(std::max<uint32_t>(32, topk));
     const uint32_t buf_x = 2 * keep_x;
     const uint32_t warps_x = std::min<uint32_t>(8, std::max<uint32_t>(1, 8192 / buf_x));

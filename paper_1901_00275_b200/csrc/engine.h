@@ -26,7 +26,9 @@ struct EngineConfig {
     uint64_t workspace_bytes = 4ull << 30;  // per-query-tile scratch budget
     uint32_t max_tile = 16384;
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
-    int scan_variant = 0;  // 0 auto (replicated LUT), 1 generic warp-buffer scan, 3 single-table LUT
+    int scan_variant = 0;  // 0 default (single-table LUT), 1 generic warp-buffer scan, 2 replicated LUT
+    int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
+    uint32_t tc_min_k = 1024;  // ... and K >= this (env VLQ_TC_MIN_K)
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -76,6 +78,7 @@ enum Phase { PH_COARSE = 0, PH_FIRST, PH_SECOND, PH_TERM5, PH_SCAN, PH_RESCORE, 
 
 struct EngineStats {
     uint64_t launches = 0;      // kernels launched by search calls
+    uint64_t tc_refine_fallbacks = 0;  // coarse/assignment rows that needed the exact full scan
     uint64_t tiles = 0;
     uint64_t flagged = 0;       // queries that took the exact fallback
     double phase_ms[PH_COUNT] = {0};  // CUDA-event time per phase (profiling on)
@@ -150,6 +153,9 @@ private:
     bool profiling_ = false;
     cudaEvent_t ev_[PH_COUNT + 1] = {};
     EngineStats stats_;
+    void assign_chunk(const float* X, uint64_t nx, uint32_t* best, cudaStream_t st);
+    DevBuf<uint32_t> tc_idx_, tc_flag_, tc_best_;
+    DevBuf<float> tc_d_, tc_rows_;
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;
     bool clamp_ = true;
@@ -160,6 +166,9 @@ private:
     HostModel model_;
 
     DevBuf<float> centroids_, elen_, pq_, t2_, t3_;
+    DevBuf<float> cent_tc_, cnorm_tc_;  // UMMA-layout centroids + norms (tensor-core path)
+    bool tc_ = false;
+    float cmax_ = 0.0f;  // max centroid norm (certificate bound)
     DevBuf<uint32_t> nbr_;
     DevBuf<uint64_t> list_off_;
     DevBuf<uint8_t> codes_, lambdas_;
@@ -169,7 +178,7 @@ private:
 
     // search workspace
     DevBuf<float> ws_, dbuf_, t5_;
-    DevBuf<uint32_t> top_, sel_, qlist_;
+    DevBuf<uint32_t> top_, sel_, qlist_, cand_top_;
     DevBuf<uint64_t> cand_;
     DevBuf<QueryMeta> meta_;
 };

@@ -42,6 +42,8 @@ struct SearchArgs {
     uint64_t* cand;   // [T, keep] fast-scan survivors (key = dist | pos)
     QueryMeta* meta;  // [T]
     unsigned int* error_flag;
+    const float* Y;  // non-null: ws holds approximate (tensor-core) rows; second level
+                     // recomputes neighbour distances exactly from the query vectors
 };
 
 // Add-path device views.
@@ -102,4 +104,25 @@ void launch_gt_merge(const float* dist, uint64_t ldd, uint64_t nq, uint32_t k, u
                      const uint32_t* sel_pos, uint64_t base_id, uint64_t* running, cudaStream_t st);
 void launch_select_rows(const float* vals, uint64_t ld, uint64_t nrows, uint32_t len, uint32_t L, uint32_t* out,
                         cudaStream_t st);
+}  // namespace vlq
+
+namespace vlq {
+// tensor-core coarse stage (coarse_tc.cu)
+bool coarse_tc_supported(uint32_t dim);
+void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* norm_out, cudaStream_t st);
+void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cnorm,
+                      uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d, cudaStream_t st);
+void launch_refine_argmin(const float* X, uint64_t nx, uint32_t dim, const float* C, const uint32_t* top_idx,
+                          const float* top_d, float cmax, uint32_t* best, uint32_t* flagged, unsigned int* nflag,
+                          cudaStream_t st);
+void launch_gather_rows_list(const float* X, uint32_t dim, const uint32_t* rows, uint32_t nr, float* out,
+                             cudaStream_t st);
+void launch_scatter_u32(const uint32_t* vals, const uint32_t* rows, uint32_t nr, uint32_t* out, cudaStream_t st);
+void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float* C, float* ws, uint32_t k,
+                         const uint32_t* cand, uint32_t L, uint32_t w1, float cmax, uint32_t* top, uint32_t* flagged,
+                         unsigned int* nflag, cudaStream_t st);
+void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,
+                       const uint32_t* qlist, const unsigned int* count, cudaStream_t st);
+void launch_first_level_list(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top,
+                             const uint32_t* qlist, const unsigned int* count, cudaStream_t st);
 }  // namespace vlq

@@ -110,10 +110,25 @@ __global__ void __launch_bounds__(512) k_second_level(SearchArgs a, uint32_t w1,
         s_scanned = 0;
         s_dmax = 0.0f;
     }
+    extern __shared__ float ys2[];  // query vector (tensor-core mode)
+    if (a.Y) {
+        for (uint32_t d = threadIdx.x; d < a.dim; d += blockDim.x) ys2[d] = a.Y[q * a.dim + d];
+        __syncthreads();
+    }
     for (uint32_t e = threadIdx.x; e < total; e += blockDim.x) {
         uint32_t i = topq[e / n], j = e % n;
         float av = wsq[i];
-        float bv = wsq[a.nbr[(uint64_t)i * n + j]];
+        const uint32_t s = a.nbr[(uint64_t)i * n + j];
+        float bv;
+        if (a.Y) {  // ws[s] may be approximate: recompute exactly and publish it
+            const float* cp = a.centroids + (uint64_t)s * a.dim;
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < a.dim; d++) acc = sq_step(acc, ys2[d], cp[d]);
+            bv = acc;
+            const_cast<float*>(wsq)[s] = acc;
+        } else {
+            bv = wsq[s];
+        }
         float cv = a.elen[(uint64_t)i * n + j];
         if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
         float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
@@ -439,7 +454,7 @@ void launch_first_level(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, u
 }
 
 void launch_second_level(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, cudaStream_t st) {
-    dev::k_second_level<<<(unsigned)nq, 512, 0, st>>>(a, w1, w2);
+    dev::k_second_level<<<(unsigned)nq, 512, a.Y ? a.dim * sizeof(float) : 0, st>>>(a, w1, w2);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -1,0 +1,94 @@
+"""Tensor-core (tcgen05 TF32) coarse stage and add assignment, forced on for
+the small golden models (VLQ_TC_MIN_K=0): results must stay bit-exact with
+the reference -- the TF32 candidates are only proposals, settled by exact
+reference-order distances under a certificate."""
+import numpy as np
+import pytest
+
+from conftest import grid_of, load_golden, regen_base
+
+pytestmark = pytest.mark.gpu
+
+# golden cases whose dim is a multiple of 8 (the tf32 MMA K step)
+TC_CASES = ["smoke", "unclamped", "m16", "n1m8", "accept_small"]
+
+
+@pytest.fixture()
+def vlqadc(monkeypatch):
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    monkeypatch.setenv("VLQ_TC_MIN_K", "0")
+    monkeypatch.setenv("VLQ_TC", "1")
+    from paper_1901_00275_b200 import vlqadc as mod
+    return mod
+
+
+def same_f32(a, b):
+    return np.array_equal(np.asarray(a, np.float32).view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
+
+
+@pytest.mark.parametrize("name", TC_CASES)
+def test_tc_search_matches_reference_golden(vlqadc, name):
+    z, index_path, _ = load_golden(name)
+    idx = vlqadc.Index.load(index_path)
+    for gi, (w1, alpha, k) in enumerate(grid_of(z)):
+        ids, dists, scanned = idx.search(z["queries"], w1=w1, alpha=alpha, k=k, return_scanned=True)
+        assert np.array_equal(ids, z[f"ids_{gi}"]), (name, gi)
+        assert same_f32(dists, z[f"dists_{gi}"]), (name, gi)
+        assert int(scanned.sum()) == int(z[f"scanned_{gi}"]), (name, gi)
+
+
+@pytest.mark.parametrize("name", [c for c in TC_CASES if c != "accept_small"])
+def test_tc_add_matches_reference_file(vlqadc, name, tmp_path):
+    z, index_path, model_path = load_golden(name)
+    base = regen_base(z)
+    idx = vlqadc.Index.load(model_path)
+    idx.add(base)
+    out = str(tmp_path / "tc.vlq")
+    idx.save(out)
+    assert open(out, "rb").read() == open(index_path, "rb").read()
+
+
+def test_tc_per_point_assignment_matches_oracle(vlqadc, oracle_mod):
+    z, index_path, _ = load_golden("accept_small")
+    base = regen_base(z)
+    idx = vlqadc.Index.load(index_path)
+    cells, lams, codes, lb = idx.encode(base)
+    oc, ol, ocd, olb = oracle_mod.OracleIndex.load(index_path).assign(base)
+    assert np.array_equal(cells, oc) and same_f32(lams, ol)
+    assert np.array_equal(codes, ocd) and np.array_equal(lb, olb)
+
+
+def test_tc_random_parameters_match_oracle(vlqadc, oracle_mod):
+    rng = np.random.default_rng(7)
+    for name in TC_CASES:
+        z, index_path, _ = load_golden(name)
+        idx = vlqadc.Index.load(index_path)
+        o = oracle_mod.OracleIndex.load(index_path)
+        for _ in range(4):
+            w1 = int(rng.integers(1, idx.k))
+            alpha = float(np.float32(rng.uniform(0.05, 1.0)))
+            k = int(rng.choice([1, 10, 100]))
+            ids, dists = idx.search(z["queries"], w1=w1, alpha=alpha, k=k)
+            oids, od, _ = o.search(z["queries"], w1, alpha, k)
+            assert np.array_equal(ids, oids) and same_f32(dists, od), (name, w1, alpha, k)
+
+
+def test_tc_larger_codebook_trained_on_gpu(vlqadc, oracle_mod, tmp_path):
+    """K = 2048 GPU-trained model (D = 32): tensor-core add + search vs the
+    oracle on the exported file."""
+    base = vlqadc.gen_synthetic(60000, 32, clusters=300, spread=0.05, seed=5)
+    q = vlqadc.gen_synthetic(200, 32, clusters=300, spread=0.05, seed=6)
+    idx = vlqadc.Index.train(base[:20000], k=2048, n=16, m=8, iters=4, seed=3)
+    idx.add(base)
+    path = str(tmp_path / "k2048.vlq")
+    idx.save(path)
+    o = oracle_mod.OracleIndex.load(path)
+    built = o.build(base)  # the oracle's own add on the same model
+    off, ids, codes, lams = idx.lists()
+    assert np.array_equal(off, built.list_off) and np.array_equal(ids, built.ids)
+    assert np.array_equal(codes, built.codes) and np.array_equal(lams, built.lambdas)
+    for w1, alpha, k in [(64, 0.25, 100), (16, 0.5, 10), (256, 0.1, 50)]:
+        ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
+        oids, od, _ = o.search(q, w1, alpha, k)
+        assert np.array_equal(ids_, oids) and same_f32(d_, od)
