@@ -131,6 +131,10 @@ int vlq_engine_reset_stats(vlq_engine* e);
 /* Index.k / n / m / dim / ntotal (bindings.cpp:222-232). */
 int vlq_engine_info(vlq_engine* e, vlq_info* out);
 
+/* Copies the trained quantizers back to the host (any pointer may be NULL):
+ * centroids[k*dim], neighbor_ids[k*n], edge_sq_len[k*n], pq[m*256*(dim/m)]. */
+int vlq_engine_get_model(vlq_engine* e, float* centroids, uint32_t* neighbor_ids, float* edge_sq_len, float* pq);
+
 /* Copies the (this shard's) posting lists back to the host:
  * list_off[k*n+1], ids[local_entries], codes[local_entries*m], lambdas[...]. */
 int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8_t* codes, uint8_t* lambdas);

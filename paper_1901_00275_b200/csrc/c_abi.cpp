@@ -245,6 +245,18 @@ int vlq_engine_info(vlq_engine* e, vlq_info* out) {
     return VLQ_OK;
 }
 
+int vlq_engine_get_model(vlq_engine* e, float* centroids, uint32_t* neighbor_ids, float* edge_sq_len, float* pq) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!e->impl->has_model()) throw std::runtime_error("get_model: no model loaded");
+        const vlq::HostModel& m = e->impl->model();
+        if (centroids) std::memcpy(centroids, m.centroids.data(), m.centroids.size() * 4);
+        if (neighbor_ids) std::memcpy(neighbor_ids, m.nbr.data(), m.nbr.size() * 4);
+        if (edge_sq_len) std::memcpy(edge_sq_len, m.elen.data(), m.elen.size() * 4);
+        if (pq) std::memcpy(pq, m.pq.data(), m.pq.size() * 4);
+    });
+}
+
 int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8_t* codes, uint8_t* lambdas) {
     ENGINE_OR_FAIL(e);
     return guarded([&] {

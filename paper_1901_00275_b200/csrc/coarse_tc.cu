@@ -459,6 +459,71 @@ __global__ void k_refine_first(const float* __restrict__ Y, uint32_t dim, const 
     for (uint32_t t = threadIdx.x; t < w1; t += blockDim.x) top[q * w1 + t] = (uint32_t)keys[t];
 }
 
+// Exact distances for every centroid the downstream stages read: the top-w1
+// regions and all their neighbours (second_level_rank reads ws[nbr],
+// search.cpp:57).  Needed ids are deduplicated through a shared bitmap,
+// compacted, and processed 32 at a time: the warp stages 32 centroid rows with
+// coalesced float4 loads, then each lane runs one sequential (reference-order)
+// sqdist from shared memory.
+__global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ Y, uint32_t dim,
+                                                      const float* __restrict__ C, uint32_t k, uint32_t n,
+                                                      const uint32_t* __restrict__ nbr, float* __restrict__ ws,
+                                                      const uint32_t* __restrict__ top, uint32_t w1) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t nwords = (k + 31) / 32;
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);            // nwords
+    uint32_t* ids = bitmap + nwords;                                  // up to w1*(n+1)
+    float* ys = reinterpret_cast<float*>(ids + w1 * (n + 1));         // dim
+    float* rows = ys + ((dim + 3) & ~3u);                             // 8 warps x 32 x (dim+1)
+    __shared__ uint32_t s_scan[40];
+    const uint64_t q = blockIdx.x;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) bitmap[i] = 0;
+    for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
+    __syncthreads();
+    const uint32_t* tq = top + q * w1;
+    for (uint32_t e = threadIdx.x; e < w1 * (n + 1); e += blockDim.x) {
+        const uint32_t r = e / (n + 1), j = e % (n + 1);
+        const uint32_t c = j == 0 ? tq[r] : nbr[(uint64_t)tq[r] * n + (j - 1)];
+        atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+    }
+    __syncthreads();
+    // compact set bits (ascending ids)
+    const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
+    uint32_t local = 0;
+    for (uint32_t i = threadIdx.x * per; i < min(nwords, (threadIdx.x + 1) * per); i++) local += __popc(bitmap[i]);
+    uint32_t total;
+    uint32_t run = block_excl_scan_u32(local, s_scan, &total);
+    for (uint32_t i = threadIdx.x * per; i < min(nwords, (threadIdx.x + 1) * per); i++) {
+        uint32_t w = bitmap[i];
+        while (w) {
+            const uint32_t b = __ffs(w) - 1;
+            ids[run++] = i * 32 + b;
+            w &= w - 1;
+        }
+    }
+    __syncthreads();
+    // 32 centroids per warp pass
+    float* wrows = rows + (size_t)warp * 32 * (dim + 1);
+    const uint32_t nwarps = blockDim.x >> 5;
+    float* wsq = ws + q * k;
+    for (uint32_t base = warp * 32; base < total; base += nwarps * 32) {
+        const uint32_t cnt = min(32u, total - base);
+        for (uint32_t r = 0; r < cnt; r++) {
+            const float* cp = C + (uint64_t)ids[base + r] * dim;
+            for (uint32_t d = lane; d < dim; d += 32) wrows[r * (dim + 1) + d] = cp[d];
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            const float* rp = wrows + lane * (dim + 1);
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], rp[d]);
+            wsq[ids[base + lane]] = acc;
+        }
+        __syncwarp();
+    }
+}
+
 // Exact full ws rows for the listed queries (certificate failures).
 __global__ void k_exact_rows(const float* __restrict__ Y, uint32_t dim, const float* __restrict__ C, uint32_t k,
                              float* __restrict__ ws, const uint32_t* __restrict__ qlist,
@@ -518,6 +583,21 @@ void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float*
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_refine_first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dev::k_refine_first<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, ws, k, cand, L, w1, cmax, top, flagged, nflag);
     CUDA_LAUNCH_CHECK();
+}
+
+void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, uint32_t n,
+                         const uint32_t* nbr, float* ws, const uint32_t* top, uint32_t w1, cudaStream_t st) {
+    if (nq == 0) return;
+    const size_t smem = (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4 +
+                        (size_t)8 * 32 * (dim + 1) * 4;
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_exact_needed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_exact_needed<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, k, n, nbr, ws, top, w1);
+    CUDA_LAUNCH_CHECK();
+}
+
+size_t exact_needed_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t dim) {
+    return (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4 +
+           (size_t)8 * 32 * (dim + 1) * 4;
 }
 
 void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,

@@ -496,7 +496,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     };
     uint64_t launches = 0;
     const uint32_t L = std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2));
-    const bool tc = tc_ && L <= 2048 && w1 < k_;
+    const bool tc = tc_ && L <= 2048 && w1 < k_ && exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
     mark(PH_COARSE);
     if (tc) {
         // approximate rows on the tensor cores, then top-L on them
@@ -514,8 +514,8 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
                             err_.p + 6, st);
         launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
         launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
-        launches += 4;
-        a.Y = d_q;
+        launch_exact_needed(d_q, nt, dim_, centroids_.p, k_, n_, nbr_.p, ws_.p, top_.p, w1, st);
+        launches += 5;
     } else {
         launch_first_level(ws_.p, nt, k_, w1, top_.p, st);
         launches += 1;

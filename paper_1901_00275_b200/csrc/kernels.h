@@ -123,6 +123,9 @@ void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float*
                          unsigned int* nflag, cudaStream_t st);
 void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,
                        const uint32_t* qlist, const unsigned int* count, cudaStream_t st);
+void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, uint32_t n,
+                         const uint32_t* nbr, float* ws, const uint32_t* top, uint32_t w1, cudaStream_t st);
+size_t exact_needed_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t dim);
 void launch_first_level_list(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top,
                              const uint32_t* qlist, const unsigned int* count, cudaStream_t st);
 }  // namespace vlq

@@ -211,6 +211,18 @@ class Index:
         _lib.check(_lib.lib().vlq_engine_encode(self._h, _p(a), nx, _p(cells), _p(lams), _p(codes), _p(lb)))
         return cells, lams, codes, lb
 
+    def model(self) -> dict:
+        """The trained quantizers (host copies): centroids, nbr, elen, pq, lambda range, clamp."""
+        info = self._info()
+        k, n, m, dim = int(info.k), int(info.n), int(info.m), int(info.dim)
+        cent = np.empty((k, dim), np.float32)
+        nbr = np.empty((k, n), np.uint32)
+        elen = np.empty((k, n), np.float32)
+        pq = np.empty((m, KSUB, dim // m), np.float32)
+        _lib.check(_lib.lib().vlq_engine_get_model(self._h, _p(cent), _p(nbr), _p(elen), _p(pq)))
+        return dict(dim=dim, k=k, n=n, m=m, clamp=bool(info.clamp_lambda), lo=float(info.lambda_lo),
+                    hi=float(info.lambda_hi), centroids=cent, nbr=nbr, elen=elen, pq=pq)
+
     def lists(self):
         """This engine's posting lists: (list_off u64[k*n+1], ids u32, codes u8[.,m], lambdas u8)."""
         info = self._info()
