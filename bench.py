@@ -53,10 +53,10 @@ WORKLOADS = {
     "deep100m": dict(desc="DEEP100M-shaped synthetic (HBM-resident scan study): 100M x 96, K=4096 x 32 lines, PQ 16 B, "
                           "nq=10k, k=100", n=100_000_000, dim=96, k=4096, edges=32, m=16, clusters=4000,
                      ntrain=200_000),
-    "c3": dict(desc="SIFT100M-shaped synthetic (configs[2]): 100M x 128, K=65536 x 32 lines, PQ 8 B, nq=10k",
-               n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=262_144),
-    "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k",
-               n=1_000_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536, ntrain=262_144),
+    "c3": dict(desc="SIFT100M-shaped synthetic (configs[2]): 100M x 128, K=65536 x 32 lines, PQ 8 B, nq=10k, k=100",
+               n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=524_288, gt_queries=500),
+    "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k, k=100",
+               n=1_000_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536, ntrain=524_288, gt_queries=200),
 }
 SPREAD, BASE_SEED, QUERY_SEED, TRAIN_SEED = 0.05, 42, 43, 1
 
@@ -179,6 +179,29 @@ def time_reference(ref_idx, refmod, queries: np.ndarray, w1, alpha, k, budget_s:
     return ns / dt, ns, dt, ids, dists, warm
 
 
+def time_port(idx, queries: np.ndarray, w1, alpha, k, budget_s: float, warm: int = 100):
+    """The C restatement of the reference search (oracle/, test infrastructure)
+    on host copies of the GPU-built index: for 1e8-1e9-point indexes where a
+    VLQ1 round trip through the reference is tens of GB of file I/O."""
+    from oracle import oracle as orc, vlq1
+    mdl = idx.model()
+    off, ids, codes, lams = idx.lists()
+    ix = vlq1.Vlq1(mdl["dim"], mdl["k"], mdl["n"], mdl["m"], mdl["clamp"], mdl["lo"], mdl["hi"], mdl["centroids"],
+                   mdl["nbr"], mdl["elen"], mdl["pq"], None, off, ids, codes, lams)
+    o = orc.OracleIndex(ix)
+    o.search(queries[:warm], w1, alpha, k)
+    probe = queries[warm:warm + 50]
+    t = time.perf_counter()
+    o.search(probe, w1, alpha, k)
+    rate = len(probe) / max(time.perf_counter() - t, 1e-6)
+    ns = int(min(len(queries) - warm, max(50, rate * budget_s)))
+    sample = queries[warm:warm + ns]
+    t = time.perf_counter()
+    rids, rd, _ = o.search(sample, w1, alpha, k)
+    dt = time.perf_counter() - t
+    return ns / dt, ns, dt, rids, rd, warm
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -190,7 +213,9 @@ def main():
     ap.add_argument("--w1", type=int, default=64)
     ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--k", type=int, default=100)
-    ap.add_argument("--gt-queries", type=int, default=1000)
+    ap.add_argument("--gt-queries", type=int, default=None, help="queries with exact ground truth (default per workload)")
+    ap.add_argument("--cpu-kind", default=None, choices=["reference", "port"],
+                    help="CPU baseline: the reference via a VLQ1 file (default up to 1e8 points) or the C oracle port")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of reference CPU work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -306,7 +331,7 @@ def main():
                 "scan_share_of_step": round(scan_ms / (ms_max / args.steps), 4)}
 
     # recall on the exact ground truth of a query subset
-    ngt = min(args.gt_queries, nq)
+    ngt = min(args.gt_queries or w.get("gt_queries", 1000), nq)
     qh = q.cpu().numpy()
     gt = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], SPREAD, BASE_SEED, qh[:ngt], 1,
                                          device=local)
@@ -331,23 +356,28 @@ def main():
     cpu = None
     parity = None
     if world == 1 and not args.no_cpu_baseline:
+        kind = args.cpu_kind or ("reference" if w["n"] <= 100_000_000 else "port")
         try:
-            refmod = ref_module()
-            with tempfile.TemporaryDirectory() as tmp:
-                path = os.path.join(tmp, "bench.vlq")
-                idx.save(path)
-                ref_idx = refmod.Index.load(path)
-            qps, ns, dt, rids, rd, off = time_reference(ref_idx, refmod, qh, args.w1, np.float32(args.alpha), k,
-                                                        args.cpu_budget)
+            if kind == "reference":
+                refmod = ref_module()
+                with tempfile.TemporaryDirectory() as tmp:
+                    path = os.path.join(tmp, "bench.vlq")
+                    idx.save(path)
+                    ref_idx = refmod.Index.load(path)
+                qps, ns, dt, rids, rd, off = time_reference(ref_idx, refmod, qh, args.w1, np.float32(args.alpha), k,
+                                                            args.cpu_budget)
+                del ref_idx
+                what = "reference Index.search (oracle/_ref) on the same index via VLQ1, set_max_threads(0)"
+            else:
+                qps, ns, dt, rids, rd, off = time_port(idx, qh, args.w1, np.float32(args.alpha), k, args.cpu_budget)
+                what = "C oracle port (oracle/vlq_oracle.c) on host copies of the same index, all host threads"
             parity = bool(np.array_equal(rids, res_ids[off:off + ns]) and
                           np.array_equal(rd.view(np.uint32), res_d[off:off + ns].view(np.uint32)))
-            cpu = {"value": round(qps, 2), "unit": "queries/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"{ns} of the {nq} benchmark queries (after 100 warm-up), same VLQ1 index, "
-                             f"Index.search with set_max_threads(0), {dt:.1f} s",
+            cpu = {"value": round(qps, 2), "unit": "queries/s", "cores": os.cpu_count(), "kind": kind,
+                   "sample": f"{ns} of the {nq} benchmark queries (after 100 warm-up), {what}, {dt:.1f} s",
                    "ids_and_dists_bit_exact_vs_gpu": parity}
-            del ref_idx
         except Exception as e:  # reported, never silently replaced
-            cpu = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
+            cpu = {"value": None, "kind": kind, "unavailable": f"{type(e).__name__}: {e}"}
 
     clk = clocks.summary()
     line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,

@@ -61,7 +61,8 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
-    if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = (uint32_t)std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
         throw std::runtime_error("engine: invalid shard configuration");
     int ndev = 0;
@@ -496,7 +497,8 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     };
     uint64_t launches = 0;
     const uint32_t L = std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2));
-    const bool tc = tc_ && L <= 2048 && w1 < k_ && exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
+    const bool tc = tc_ && k_ >= cfg_.tc_search_min_k && L <= 2048 && w1 < k_ &&
+                    exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
     mark(PH_COARSE);
     if (tc) {
         // approximate rows on the tensor cores, then top-L on them

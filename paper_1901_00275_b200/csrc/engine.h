@@ -28,7 +28,8 @@ struct EngineConfig {
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
     int scan_variant = 0;  // 0 default (single-table LUT), 1 generic warp-buffer scan, 2 replicated LUT
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
-    uint32_t tc_min_k = 1024;  // ... and K >= this (env VLQ_TC_MIN_K)
+    uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
+    uint32_t tc_search_min_k = 16384; // search coarse stage on tensor cores for K >= this (env VLQ_TC_SEARCH_MIN_K)
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).

@@ -39,11 +39,13 @@ def gather_parts(local_ids, local_dists, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    gi = torch.empty((world,) + tuple(local_ids.shape), dtype=local_ids.dtype, device=local_ids.device)
-    gd = torch.empty((world,) + tuple(local_dists.shape), dtype=local_dists.dtype, device=local_dists.device)
+    nq = local_ids.shape[0]
+    # concatenated along dim 0 (the layout every backend accepts), viewed [world, nq, k]
+    gi = torch.empty((world * nq,) + tuple(local_ids.shape[1:]), dtype=local_ids.dtype, device=local_ids.device)
+    gd = torch.empty((world * nq,) + tuple(local_dists.shape[1:]), dtype=local_dists.dtype, device=local_dists.device)
     dist.all_gather_into_tensor(gi, local_ids.contiguous(), group=group)
     dist.all_gather_into_tensor(gd, local_dists.contiguous(), group=group)
-    return gi, gd
+    return gi.view((world,) + tuple(local_ids.shape)), gd.view((world,) + tuple(local_dists.shape))
 
 
 class ShardedIndex:

@@ -1,0 +1,94 @@
+"""CPU test of the multi-GPU path's host logic (gloo, world_size 2).
+
+Each rank holds the regions i % world == rank of the golden index (the
+engine's shard rule, csrc/engine.h Engine::owner), searches its shard, and the
+per-shard top-k blocks are exchanged with paper_1901_00275_b200.dist.gather_parts
+(the same call the NCCL path uses).  The (dist, id) merge of the gathered
+blocks must equal the unsharded search.  The shard search and the merge here
+are the oracle's (no GPU on this box); the GPU merge kernel is covered by
+tests/test_gpu_parity.py::test_sharded_engines_merge_to_the_single_engine_result.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def shard_of(ix, rank, world):
+    from oracle import vlq1
+    keep = np.zeros(ix.k * ix.n, bool)
+    for c in range(ix.k * ix.n):
+        keep[c] = (c // ix.n) % world == rank
+    lens = np.diff(ix.list_off.astype(np.int64))
+    lens = np.where(keep, lens, 0)
+    off = np.zeros(ix.k * ix.n + 1, np.uint64)
+    np.cumsum(lens, out=off[1:])
+    sel = np.concatenate([np.arange(int(ix.list_off[c]), int(ix.list_off[c + 1])) for c in range(ix.k * ix.n)
+                          if keep[c]] or [np.zeros(0, np.int64)]).astype(np.int64)
+    return vlq1.Vlq1(ix.dim, ix.k, ix.n, ix.m, ix.clamp, ix.lo, ix.hi, ix.centroids, ix.nbr, ix.elen, ix.pq, ix.t3, off,
+                     ix.ids[sel], ix.codes[sel], ix.lambdas[sel])
+
+
+def merge_np(ids, dists):
+    """(dist, id) merge of [G, nq, k] blocks, -1/inf padded (the K9 contract)."""
+    G, nq, k = ids.shape
+    out_i = np.full((nq, k), -1, np.int64)
+    out_d = np.full((nq, k), np.inf, np.float32)
+    for q in range(nq):
+        cand = [(float(dists[g, q, j]), int(ids[g, q, j])) for g in range(G) for j in range(k) if ids[g, q, j] >= 0]
+        cand.sort()
+        for j, (d, i) in enumerate(cand[:k]):
+            out_i[q, j], out_d[q, j] = i, d
+    return out_i, out_d
+
+
+def _worker(rank, world, port, name, params, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle, vlq1
+    from paper_1901_00275_b200.dist import gather_parts
+    z, index_path, _ = load_golden(name)
+    ix = vlq1.read(index_path)
+    o = oracle.OracleIndex(shard_of(ix, rank, world))
+    res = []
+    for w1, alpha, k in params:
+        ids, d, _ = o.search(z["queries"], w1, alpha, k)
+        gi, gd = gather_parts(torch.from_numpy(ids), torch.from_numpy(d))
+        res.append((gi.numpy(), gd.numpy()))
+    if rank == 0:
+        import pickle
+        with open(out_path, "wb") as f:
+            pickle.dump([merge_np(*r) for r in res], f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["accept_small", "m16"])
+def test_gloo_sharded_search_merges_to_single_index(name, tmp_path):
+    import torch.multiprocessing as mp
+    from oracle import oracle
+    params = [(16, 0.5, 10), (64, 0.25, 100), (4, 1.0, 7)]
+    out = str(tmp_path / "merged.pkl")
+    mp.start_processes(_worker, args=(2, _free_port(), name, params, out), nprocs=2, join=True, start_method="spawn")
+    import pickle
+    with open(out, "rb") as f:
+        merged = pickle.load(f)
+    z, index_path, _ = load_golden(name)
+    o = oracle.OracleIndex.load(index_path)
+    for (w1, alpha, k), (mi, md) in zip(params, merged):
+        ids, d, _ = o.search(z["queries"], w1, alpha, k)
+        assert np.array_equal(mi, ids)
+        assert np.array_equal(np.asarray(md, np.float32).view(np.uint32), d.view(np.uint32))
