@@ -386,7 +386,8 @@ def main():
             "data": "synthetic", "config": cfg, "recall": recall, "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
-            "fallback_queries_per_step": stats["flagged"] / args.steps}
+            "fallback_queries_per_step": stats["flagged"] / args.steps,
+            "tc_coarse_fallbacks_per_step": stats["tc_fallbacks"] / args.steps}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

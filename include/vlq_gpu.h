@@ -59,6 +59,7 @@ typedef struct {
     uint64_t launches;      /* engine kernels launched by search calls */
     uint64_t tiles;         /* query tiles processed */
     uint64_t flagged;       /* queries whose certificate failed -> exact scan (profiling on) */
+    uint64_t tc_fallbacks;  /* tensor-core coarse rows / add points that needed the exact full scan */
     double phase_ms[8];     /* CUDA-event ms per phase (profiling on): coarse, first-level,
                                second-level, term5, scan, rescore, fallback, output */
 } vlq_stats;

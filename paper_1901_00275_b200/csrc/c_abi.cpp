@@ -220,6 +220,7 @@ int vlq_engine_get_stats(vlq_engine* e, vlq_stats* out) {
     out->launches = s.launches;
     out->tiles = s.tiles;
     out->flagged = s.flagged;
+    out->tc_fallbacks = s.tc_refine_fallbacks;
     for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
     return VLQ_OK;
 }

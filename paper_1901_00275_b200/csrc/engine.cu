@@ -574,6 +574,12 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
             CUDA_CHECK(cudaStreamSynchronize(st));
             stats_.flagged += nflag;
         }
+        if (tc) {
+            unsigned int nflag = 0;
+            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            stats_.tc_refine_fallbacks += nflag;
+        }
     }
 }
 

@@ -18,6 +18,8 @@
 // as C_p interleaved copies (word (j*C_p + c) for copy c); lane l reads copy
 // (l mod C_p), so lane groups hit disjoint bank sets.  C_p = 16 gives exactly
 // 2 wavefronts, 32 gives 1.  The copy budget per M fills <= 160 KB of smem.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "select.cuh"
 
@@ -171,7 +173,7 @@ __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep,
 }
 
 template <int M, int U, int R>
-__global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 : 3)) k_scan_fast(SearchArgs a, uint32_t w2, uint32_t keep,
+__global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 || U > 6 ? 2 : 3)) k_scan_fast(SearchArgs a, uint32_t w2, uint32_t keep,
                                                                       uint32_t cap) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Plan = LutPlan<M, R>;
@@ -389,9 +391,8 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 ? 2 :
 
 }  // namespace dev
 
-template <int M, int R>
-static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
-    constexpr int U = 4;
+template <int M, int R, int U>
+static void launch_fast_u(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
     const uint32_t nwarps = R == 2 ? 16 : 8;
     const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
     const size_t smem = 4 * (size_t)dev::LutPlan<M, R>::words() + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
@@ -399,6 +400,23 @@ static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)nq, nwarps * 32, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
+}
+
+// entry-slots per lane per chunk (4 by default; env VLQ_SCAN_U = 6 / 8 for studies)
+static int scan_u() {
+    static int u = [] {
+        const char* v = std::getenv("VLQ_SCAN_U");
+        const int x = v ? std::atoi(v) : 4;
+        return (x == 6 || x == 8) ? x : 4;
+    }();
+    return u;
+}
+
+template <int M, int R>
+static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
+    if (R == 0 && scan_u() == 6) launch_fast_u<M, R, 6>(a, nq, w2, keep, st);
+    else if (R == 0 && scan_u() == 8) launch_fast_u<M, R, 8>(a, nq, w2, keep, st);
+    else launch_fast_u<M, R, 4>(a, nq, w2, keep, st);
 }
 
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, cudaStream_t st) {
