@@ -30,7 +30,6 @@ namespace dev {
 
 constexpr int TC_M = 128;      // rows of X per CTA (UMMA M)
 constexpr int TC_N = 128;      // centroids per tile (UMMA N)
-constexpr int TC_STAGES = 3;
 constexpr int TC_THREADS = 320;  // 10 warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -105,23 +104,39 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 template <int MODE>  // 0 = ARGMIN (top-4 per row), 1 = STORE (approx row)
+__host__ __device__ constexpr int tc_stages() { return MODE == 0 ? 3 : 2; }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// SPLIT = 3xTF32: x = hi + lo with hi = tf32(x); <x, c> ~= hi.hi + hi.lo + lo.hi
+// (error ~2^-21 relative instead of 2^-9), three MMAs per K step, 64-centroid tiles.
+template <int MODE, bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_coarse_tc(const float* __restrict__ X, uint64_t nx, uint32_t dim, const float* __restrict__ cent_tc,
-                const float* __restrict__ cnorm_pad, uint32_t ntiles, uint32_t kvalid, float* __restrict__ out_row,
-                uint64_t ldo, uint32_t* __restrict__ top_idx, float* __restrict__ top_d) {
+                const float* __restrict__ cent_lo, const float* __restrict__ cnorm_pad, uint32_t ntiles,
+                uint32_t kvalid, float* __restrict__ out_row, uint64_t ldo, uint32_t* __restrict__ top_idx,
+                float* __restrict__ top_d) {
     extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int TN = SPLIT ? 64 : TC_N;  // centroids per tile (UMMA N)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t tile_bytes = TC_N * dim * 4;  // one centroid tile
+    const uint32_t tile_bytes = TN * dim * 4;  // one centroid tile (one precision half)
     const uint32_t a_bytes = TC_M * dim * 4;
     unsigned char* sA = smem;
-    unsigned char* sB = smem + a_bytes;                                   // STAGES x tile_bytes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + TC_STAGES * tile_bytes);
+    unsigned char* sAlo = smem + a_bytes;  // SPLIT only
+    constexpr int TC_STAGES = tc_stages<MODE>();
+    constexpr int NB = SPLIT ? 2 : 1;
+    unsigned char* sB = smem + a_bytes * NB;                              // STAGES x NB x tile_bytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + TC_STAGES * NB * tile_bytes);
     uint64_t* full = bars;                   // [STAGES]
     uint64_t* empty = bars + TC_STAGES;      // [STAGES]
     uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]
     uint64_t* tempty = tfull + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* sMerge = reinterpret_cast<float*>(tmem_slot + 4);  // 128 rows x 4 (d) + 128 x 4 (idx)
+    float* sMerge = reinterpret_cast<float*>(tmem_slot + 4);  // ARGMIN: 128 x 4 d + 128 x 4 idx; STORE: 8 x 32 x 33 transpose
 
     const uint64_t row0 = (uint64_t)blockIdx.x * TC_M;
     // ---- A tile: row-major global -> interleaved K-major smem (all threads)
@@ -131,7 +146,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (row0 + r < nx) v = __ldg(reinterpret_cast<const float4*>(X + (row0 + r) * dim) + c);
         const uint32_t off = (r >> 3) * (nchunk * 128) + c * 128 + (r & 7) * 16;
-        *reinterpret_cast<float4*>(sA + off) = v;
+        if constexpr (SPLIT) {
+            const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+            *reinterpret_cast<float4*>(sA + off) = hi;
+            *reinterpret_cast<float4*>(sAlo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        } else {
+            *reinterpret_cast<float4*>(sA + off) = v;
+        }
     }
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < TC_STAGES; s++) {
@@ -145,7 +166,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // TMEM: two 128-column fp32 accumulators
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));  // >= 2 x TN
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A tile -> async proxy
@@ -160,13 +181,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (uint32_t t = 0; t < ntiles; t++) {
                 const uint32_t s = t % TC_STAGES, ph = (t / TC_STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], tile_bytes);
-                bulk_g2s(sB + s * tile_bytes, cent_tc + (size_t)t * TC_N * dim, tile_bytes, &full[s]);
+                mbar_expect_tx(&full[s], NB * tile_bytes);
+                bulk_g2s(sB + s * NB * tile_bytes, cent_tc + (size_t)t * TN * dim, tile_bytes, &full[s]);
+                if constexpr (SPLIT)
+                    bulk_g2s(sB + (s * NB + 1) * tile_bytes, cent_lo + (size_t)t * TN * dim, tile_bytes, &full[s]);
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) |
                                ((uint32_t)(TC_M >> 4) << 24);
         const uint32_t sbo = nchunk * 128, lbo = 128;
         const uint32_t a_addr = smem_u32(sA);
@@ -177,11 +200,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_wait(&full[s], ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
-                const uint32_t b_addr = smem_u32(sB + s * tile_bytes);
+                const uint32_t b_addr = smem_u32(sB + s * NB * tile_bytes);
                 for (uint32_t k = 0; k < dim / 8; k++) {  // K = 8 tf32 per MMA = two 16-B chunks
                     const uint64_t ad = umma_desc(a_addr + k * 256, lbo, sbo);
                     const uint64_t bd = umma_desc(b_addr + k * 256, lbo, sbo);
-                    umma_tf32(tmem_base + b * TC_N, ad, bd, idesc, k > 0 ? 1u : 0u);
+                    umma_tf32(tmem_base + b * TN, ad, bd, idesc, k > 0 ? 1u : 0u);
+                    if constexpr (SPLIT) {
+                        const uint64_t bl = umma_desc(b_addr + tile_bytes + k * 256, lbo, sbo);
+                        const uint64_t al = umma_desc(smem_u32(sAlo) + k * 256, lbo, sbo);
+                        umma_tf32(tmem_base + b * TN, ad, bl, idesc, 1u);  // hi . lo
+                        umma_tf32(tmem_base + b * TN, al, bd, idesc, 1u);  // lo . hi
+                    }
                 }
                 umma_commit(&empty[s]);
                 umma_commit(&tfull[b]);
@@ -200,15 +229,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t b = t & 1u, bph = (t >> 1) & 1u;
             mbar_wait(&tfull[b], bph);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const float* nrm = cnorm_pad + (size_t)t * TC_N;  // warp-uniform broadcast loads
+            const float* nrm = cnorm_pad + (size_t)t * TN;  // warp-uniform broadcast loads
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
+            for (int h = 0; h < TN / 64; h++) {
                 uint32_t acc[32];
-                const uint32_t col = half * 64 + h * 32;
-                tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TC_N + col, acc);
+                const uint32_t col = half * (TN / 2) + h * 32;
+                tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TN + col, acc);
+                float* tr = sMerge + (warp - 2) * 32 * 33;  // STORE: this warp's transpose tile
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
-                    const uint32_t cidx = t * TC_N + col + j;
+                    const uint32_t cidx = t * TN + col + j;
                     const float d = fmaf(-2.0f, __uint_as_float(acc[j]), __ldg(nrm + col + j));
                     if constexpr (MODE == 0) {
                         if (d < bd[3]) {  // sorted insert, ties keep the lower index (earlier)
@@ -222,8 +252,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             } else { bd[3] = d; bi[3] = cidx; }
                         }
                     } else {
-                        if (grow < nx && cidx < kvalid) out_row[grow * ldo + cidx] = d;
+                        tr[lane * 33 + j] = d;
                     }
+                }
+                if constexpr (MODE == 1) {  // coalesced: one 128-byte row segment per instruction
+                    __syncwarp();
+                    const uint32_t cidx = t * TN + col + lane;
+#pragma unroll 4
+                    for (int rr = 0; rr < 32; rr++) {
+                        const uint64_t orow = row0 + quad * 32 + rr;
+                        if (orow < nx && cidx < kvalid) out_row[orow * ldo + cidx] = tr[rr * 33 + lane];
+                    }
+                    __syncwarp();
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -272,7 +312,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // Re-lay centroids [K, D] row-major into the UMMA interleaved K-major tile
 // layout, padding rows to a multiple of 128 (zero rows, +inf norms).
 __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, uint32_t dim, uint32_t ntiles,
-                                     float* __restrict__ out, float* __restrict__ norm_out) {
+                                     float* __restrict__ out, float* __restrict__ out_lo, float* __restrict__ norm_out) {
     const uint32_t nchunk = dim / 4;
     const uint64_t total = (uint64_t)ntiles * TC_N * nchunk;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
@@ -283,6 +323,11 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
         if (row < k) v = reinterpret_cast<const float4*>(C + row * dim)[c];
         const uint64_t off = (uint64_t)tile * TC_N * dim + (r >> 3) * (nchunk * 32) + c * 32 + (r & 7) * 4;
         *reinterpret_cast<float4*>(out + off) = v;
+        if (out_lo) {  // 3xTF32 split of the centroids (hi stays in `out` unrounded: the MMA truncates)
+            const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+            *reinterpret_cast<float4*>(out + off) = hi;
+            *reinterpret_cast<float4*>(out_lo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        }
     }
     for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < (uint64_t)ntiles * TC_N;
          row += (uint64_t)gridDim.x * blockDim.x) {
@@ -295,36 +340,54 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
 
 }  // namespace dev
 
-size_t coarse_tc_smem(uint32_t dim) {
-    return (size_t)dev::TC_M * dim * 4 + (size_t)dev::TC_STAGES * dev::TC_N * dim * 4 + 2 * dev::TC_STAGES * 8 +
-           4 * 8 + 16 + (size_t)dev::TC_M * 8 * 4 + 1024;
+size_t coarse_tc_smem(uint32_t dim, int mode, bool split) {
+    const int stages = mode == 0 ? dev::tc_stages<0>() : dev::tc_stages<1>();
+    const size_t tail = mode == 0 ? (size_t)dev::TC_M * 8 * 4 : (size_t)8 * 32 * 33 * 4;
+    const size_t tn = split ? 64 : dev::TC_N, nb = split ? 2 : 1;
+    return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * nb * tn * dim * 4 + 2 * stages * 8 + 4 * 8 + 16 +
+           tail + 256;
 }
 
 bool coarse_tc_supported(uint32_t dim) {
-    return dim % 8 == 0 && dim >= 8 && coarse_tc_smem(dim) <= 227 * 1024;
+    return dim % 8 == 0 && dim >= 8 && coarse_tc_smem(dim, 0, false) <= 227 * 1024 &&
+           coarse_tc_smem(dim, 1, false) <= 227 * 1024;
 }
 
-void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* norm_out, cudaStream_t st) {
+bool coarse_tc_split_supported(uint32_t dim) {
+    return dim % 8 == 0 && dim >= 8 && coarse_tc_smem(dim, 1, true) <= 227 * 1024;
+}
+
+void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
+                               cudaStream_t st) {
     const uint32_t ntiles = (k + dev::TC_N - 1) / dev::TC_N;
-    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, norm_out);
+    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, out_lo, norm_out);
     CUDA_LAUNCH_CHECK();
 }
 
-void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cnorm,
-                      uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d, cudaStream_t st) {
+void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
+                      const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,
+                      cudaStream_t st) {
     if (nx == 0) return;
-    const uint32_t ntiles = (k + dev::TC_N - 1) / dev::TC_N;
-    const size_t smem = coarse_tc_smem(dim);
+    const bool split = cent_lo != nullptr;
+    const uint32_t tn = split ? 64 : dev::TC_N;
+    const uint32_t ntiles = (k + tn - 1) / tn;
+    const size_t smem = coarse_tc_smem(dim, mode, split);
     const unsigned grid = (unsigned)((nx + dev::TC_M - 1) / dev::TC_M);
+#define VLQ_TC_LAUNCH(MODE_, SPLIT_)                                                                            \
+    do {                                                                                                        \
+        auto fn = dev::k_coarse_tc<MODE_, SPLIT_>;                                                              \
+        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
+        fn<<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cent_lo, cnorm, ntiles, k, out_row, ldo,   \
+                                                top_idx, top_d);                                                \
+    } while (0)
     if (mode == 0) {
-        CUDA_CHECK(cudaFuncSetAttribute(dev::k_coarse_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dev::k_coarse_tc<0><<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cnorm, ntiles, k, out_row, ldo,
-                                                                  top_idx, top_d);
+        if (split) VLQ_TC_LAUNCH(0, true);
+        else VLQ_TC_LAUNCH(0, false);
     } else {
-        CUDA_CHECK(cudaFuncSetAttribute(dev::k_coarse_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dev::k_coarse_tc<1><<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cnorm, ntiles, k, out_row, ldo,
-                                                                  top_idx, top_d);
+        if (split) VLQ_TC_LAUNCH(1, true);
+        else VLQ_TC_LAUNCH(1, false);
     }
+#undef VLQ_TC_LAUNCH
     CUDA_LAUNCH_CHECK();
 }
 
@@ -343,12 +406,14 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
 namespace vlq {
 namespace dev {
 
-__device__ __forceinline__ float tc_eps(float xnorm2, float cmax, uint32_t dim) {
+__device__ __forceinline__ float tc_eps(float xnorm2, float cmax, uint32_t dim, bool split = false) {
+    // 1xTF32: each operand keeps 10 mantissa bits (<= 2^-10 relative per factor);
+    // 3xTF32: the dropped lo.lo term and the truncated lo parts leave <= 3 * 2^-21
     const float xn = sqrtf(xnorm2);
     const float s = xn + cmax;
     const float u = 5.9604645e-08f;
-    return 1.5f * (2.0f * (1.953125e-3f + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + 2.0f * u * s * s) +
-           1e-30f;
+    const float rel = split ? 1.430511474609375e-06f : 1.953125e-3f;
+    return 1.5f * (2.0f * (rel + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + 2.0f * u * s * s) + 1e-30f;
 }
 
 // Add path: exact argmin among the 4 tensor-core candidates (strict '<' from
@@ -401,7 +466,7 @@ __global__ void k_scatter_u32(const uint32_t* __restrict__ vals, const uint32_t*
 __global__ void k_refine_first(const float* __restrict__ Y, uint32_t dim, const float* __restrict__ C,
                                float* __restrict__ ws, uint32_t k, const uint32_t* __restrict__ cand, uint32_t L,
                                uint32_t w1, float cmax, uint32_t* __restrict__ top, uint32_t* __restrict__ flagged,
-                               unsigned int* __restrict__ nflag) {
+                               unsigned int* __restrict__ nflag, int split) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // npow2
     float* ys = reinterpret_cast<float*>(smem + 8 * 2048);
@@ -440,7 +505,7 @@ __global__ void k_refine_first(const float* __restrict__ Y, uint32_t dim, const 
     __syncthreads();
     // certificate (all non-candidates have approx >= the L-th candidate's)
     if (threadIdx.x == 0) {
-        const float eps = tc_eps(s_yn, cmax, dim);
+        const float eps = tc_eps(s_yn, cmax, dim, split != 0);
         const float exact_w1 = unord_float((uint32_t)(keys[w1 - 1] >> 32));
         const double lower = (double)unord_float(s_amax) + (double)s_yn - (double)eps;
         if (!(L < k ? lower > (double)exact_w1 : true)) flagged[atomicAdd(nflag, 1u)] = (uint32_t)q;
@@ -577,11 +642,12 @@ void launch_scatter_u32(const uint32_t* vals, const uint32_t* rows, uint32_t nr,
 
 void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float* C, float* ws, uint32_t k,
                          const uint32_t* cand, uint32_t L, uint32_t w1, float cmax, uint32_t* top, uint32_t* flagged,
-                         unsigned int* nflag, cudaStream_t st) {
+                         unsigned int* nflag, int split, cudaStream_t st) {
     if (nq == 0) return;
     const size_t smem = 8 * 2048 + (size_t)dim * 4;
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_refine_first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dev::k_refine_first<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, ws, k, cand, L, w1, cmax, top, flagged, nflag);
+    dev::k_refine_first<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, ws, k, cand, L, w1, cmax, top, flagged, nflag,
+                                                         split);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -184,7 +184,14 @@ void Engine::upload_model() {
         const uint32_t ntiles = (k_ + 127) / 128;
         cent_tc_.alloc((size_t)ntiles * 128 * dim_);
         cnorm_tc_.alloc((size_t)ntiles * 128);
-        launch_relayout_centroids(centroids_.p, k_, dim_, cent_tc_.p, cnorm_tc_.p, stream_);
+        launch_relayout_centroids(centroids_.p, k_, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, stream_);
+        // 3xTF32 split copy for the search coarse stage (hi/lo halves)
+        tc_split_ = coarse_tc_split_supported(dim_);
+        if (tc_split_) {
+            cent_hi_.alloc((size_t)ntiles * 128 * dim_);
+            cent_lo_.alloc((size_t)ntiles * 128 * dim_);
+            launch_relayout_centroids(centroids_.p, k_, dim_, cent_hi_.p, cent_lo_.p, cnorm_tc_.p, stream_);
+        }
         double mx = 0.0;
         for (uint32_t i = 0; i < k_; i++) {
             double s = 0.0;
@@ -209,7 +216,7 @@ void Engine::assign_chunk(const float* X, uint64_t nx, uint32_t* best, cudaStrea
     tc_idx_.alloc(nx * 4);
     tc_d_.alloc(nx * 4);
     tc_flag_.alloc(nx);
-    launch_coarse_tc(0, X, nx, dim_, cent_tc_.p, cnorm_tc_.p, k_, nullptr, 0, tc_idx_.p, tc_d_.p, st);
+    launch_coarse_tc(0, X, nx, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, nullptr, 0, tc_idx_.p, tc_d_.p, st);
     CUDA_CHECK(cudaMemsetAsync(err_.p + 5, 0, 4, st));
     launch_refine_argmin(X, nx, dim_, centroids_.p, tc_idx_.p, tc_d_.p, cmax_, best, tc_flag_.p, err_.p + 5, st);
     unsigned int nflag = 0;
@@ -502,7 +509,10 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     mark(PH_COARSE);
     if (tc) {
         // approximate rows on the tensor cores, then top-L on them
-        launch_coarse_tc(1, d_q, nt, dim_, cent_tc_.p, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
+        if (tc_split_)
+            launch_coarse_tc(1, d_q, nt, dim_, cent_hi_.p, cent_lo_.p, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
+        else
+            launch_coarse_tc(1, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
         launches += 1;
     } else {
         launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
@@ -513,7 +523,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         launch_first_level(ws_.p, nt, k_, L, cand_top_.p, st);
         CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
         launch_refine_first(d_q, nt, dim_, centroids_.p, ws_.p, k_, cand_top_.p, L, w1, cmax_, top_.p, qlist_.p,
-                            err_.p + 6, st);
+                            err_.p + 6, tc_split_ ? 1 : 0, st);
         launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
         launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
         launch_exact_needed(d_q, nt, dim_, centroids_.p, k_, n_, nbr_.p, ws_.p, top_.p, w1, st);

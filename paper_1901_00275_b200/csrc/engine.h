@@ -168,7 +168,8 @@ private:
 
     DevBuf<float> centroids_, elen_, pq_, t2_, t3_;
     DevBuf<float> cent_tc_, cnorm_tc_;  // UMMA-layout centroids + norms (tensor-core path)
-    bool tc_ = false;
+    DevBuf<float> cent_hi_, cent_lo_;   // 3xTF32 split halves (search coarse stage)
+    bool tc_ = false, tc_split_ = false;
     float cmax_ = 0.0f;  // max centroid norm (certificate bound)
     DevBuf<uint32_t> nbr_;
     DevBuf<uint64_t> list_off_;

@@ -109,9 +109,12 @@ void launch_select_rows(const float* vals, uint64_t ld, uint64_t nrows, uint32_t
 namespace vlq {
 // tensor-core coarse stage (coarse_tc.cu)
 bool coarse_tc_supported(uint32_t dim);
-void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* norm_out, cudaStream_t st);
-void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cnorm,
-                      uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d, cudaStream_t st);
+bool coarse_tc_split_supported(uint32_t dim);
+void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
+                               cudaStream_t st);
+void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
+                      const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,
+                      cudaStream_t st);
 void launch_refine_argmin(const float* X, uint64_t nx, uint32_t dim, const float* C, const uint32_t* top_idx,
                           const float* top_d, float cmax, uint32_t* best, uint32_t* flagged, unsigned int* nflag,
                           cudaStream_t st);
@@ -120,7 +123,7 @@ void launch_gather_rows_list(const float* X, uint32_t dim, const uint32_t* rows,
 void launch_scatter_u32(const uint32_t* vals, const uint32_t* rows, uint32_t nr, uint32_t* out, cudaStream_t st);
 void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float* C, float* ws, uint32_t k,
                          const uint32_t* cand, uint32_t L, uint32_t w1, float cmax, uint32_t* top, uint32_t* flagged,
-                         unsigned int* nflag, cudaStream_t st);
+                         unsigned int* nflag, int split, cudaStream_t st);
 void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,
                        const uint32_t* qlist, const unsigned int* count, cudaStream_t st);
 void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, uint32_t n,
