@@ -207,7 +207,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nq", type=int, default=10_000)
     ap.add_argument("--w1", type=int, default=64)
@@ -405,11 +405,15 @@ def run_reference_arm(args, w, cfg, rank, world, local):
     refmod = ref_module()
     idx, _ = build_index(vlqadc, w, local)
     qh = make_queries(vlqadc, w, args.nq, local).cpu().numpy()
-    with tempfile.TemporaryDirectory() as tmp:
+    with tempfile.TemporaryDirectory(dir=os.environ.get("VLQ_REF_TMP")) as tmp:
         path = os.path.join(tmp, "bench.vlq")
+        t0 = time.time()
         idx.save(path)
         del idx
+        t1 = time.time()
         ref_idx = refmod.Index.load(path)
+        log(f"[reference] VLQ1 hand-off: save {t1 - t0:.1f}s ({os.path.getsize(path) / 1e9:.1f} GB), "
+            f"reference load {time.time() - t1:.1f}s")
     refmod.set_max_threads(0)
     alpha = np.float32(args.alpha)
     ref_idx.search(qh[:100], w1=args.w1, alpha=alpha, k=args.k)
