@@ -104,7 +104,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 template <int MODE>  // 0 = ARGMIN (top-4 per row), 1 = STORE (approx row)
-__host__ __device__ constexpr int tc_stages() { return MODE == 0 ? 3 : 2; }
+__host__ __device__ constexpr int tc_stages() { return MODE == 1 ? 2 : 3; }
 
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
@@ -114,12 +114,18 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // SPLIT = 3xTF32: x = hi + lo with hi = tf32(x); <x, c> ~= hi.hi + hi.lo + lo.hi
 // (error ~2^-21 relative instead of 2^-9), three MMAs per K step, 64-centroid tiles.
+// MODE 2 = TILEMIN: per row, the min of every 32-centroid column chunk
+//   (out_row[row * ldo + chunk]).  The L-th smallest chunk minimum bounds the
+//   row's L-th smallest value from above (L distinct elements lie below it).
+// MODE 3 = FILTER: per row, append every (approx, centroid) with approx <=
+//   tau[row] to the row's candidate list (top_d/top_idx, capacity cap,
+//   count in cnt[row]).
 template <int MODE, bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_coarse_tc(const float* __restrict__ X, uint64_t nx, uint32_t dim, const float* __restrict__ cent_tc,
                 const float* __restrict__ cent_lo, const float* __restrict__ cnorm_pad, uint32_t ntiles,
                 uint32_t kvalid, float* __restrict__ out_row, uint64_t ldo, uint32_t* __restrict__ top_idx,
-                float* __restrict__ top_d) {
+                float* __restrict__ top_d, const float* __restrict__ tau, uint32_t* __restrict__ cnt, uint32_t cap) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int TN = SPLIT ? 64 : TC_N;  // centroids per tile (UMMA N)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -223,6 +229,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t half = (warp - 2u) >> 2;     // column half 0/1
         const uint32_t r = quad * 32 + lane;        // row within the tile
         const uint64_t grow = row0 + r;
+        const float tau_r = (MODE == 3 && grow < nx) ? tau[grow] : 0.0f;
         float bd[4] = {FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX};
         uint32_t bi[4] = {0, 0, 0, 0};
         for (uint32_t t = 0; t < ntiles; t++) {
@@ -236,6 +243,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const uint32_t col = half * (TN / 2) + h * 32;
                 tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TN + col, acc);
                 float* tr = sMerge + (warp - 2) * 32 * 33;  // STORE: this warp's transpose tile
+                float cmin = __int_as_float(0x7f800000);
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     const uint32_t cidx = t * TN + col + j;
@@ -251,9 +259,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                 } else { bd[2] = d; bi[2] = cidx; }
                             } else { bd[3] = d; bi[3] = cidx; }
                         }
-                    } else {
+                    } else if constexpr (MODE == 1) {
                         tr[lane * 33 + j] = d;
+                    } else if constexpr (MODE == 2) {
+                        cmin = fminf(cmin, d);
+                    } else {
+                        if (d <= tau_r && grow < nx) {
+                            const uint32_t slot = atomicAdd(&cnt[grow], 1u);
+                            if (slot < cap) {
+                                top_d[grow * cap + slot] = d;
+                                top_idx[grow * cap + slot] = cidx;
+                            }
+                        }
                     }
+                }
+                if constexpr (MODE == 2) {
+                    if (grow < nx) out_row[grow * ldo + t * (TN / 32) + col / 32] = cmin;
                 }
                 if constexpr (MODE == 1) {  // coalesced: one 128-byte row segment per instruction
                     __syncwarp();
@@ -341,8 +362,8 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
 }  // namespace dev
 
 size_t coarse_tc_smem(uint32_t dim, int mode, bool split) {
-    const int stages = mode == 0 ? dev::tc_stages<0>() : dev::tc_stages<1>();
-    const size_t tail = mode == 0 ? (size_t)dev::TC_M * 8 * 4 : (size_t)8 * 32 * 33 * 4;
+    const int stages = mode == 1 ? dev::tc_stages<1>() : dev::tc_stages<0>();
+    const size_t tail = mode == 1 ? (size_t)8 * 32 * 33 * 4 : (size_t)dev::TC_M * 8 * 4;
     const size_t tn = split ? 64 : dev::TC_N, nb = split ? 2 : 1;
     return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * nb * tn * dim * 4 + 2 * stages * 8 + 4 * 8 + 16 +
            tail + 256;
@@ -366,7 +387,7 @@ void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* 
 
 void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
                       const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,
-                      cudaStream_t st) {
+                      cudaStream_t st, const float* tau, uint32_t* cnt, uint32_t cap) {
     if (nx == 0) return;
     const bool split = cent_lo != nullptr;
     const uint32_t tn = split ? 64 : dev::TC_N;
@@ -378,14 +399,13 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
         auto fn = dev::k_coarse_tc<MODE_, SPLIT_>;                                                              \
         CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
         fn<<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cent_lo, cnorm, ntiles, k, out_row, ldo,   \
-                                                top_idx, top_d);                                                \
+                                                top_idx, top_d, tau, cnt, cap);                                 \
     } while (0)
-    if (mode == 0) {
-        if (split) VLQ_TC_LAUNCH(0, true);
-        else VLQ_TC_LAUNCH(0, false);
-    } else {
-        if (split) VLQ_TC_LAUNCH(1, true);
-        else VLQ_TC_LAUNCH(1, false);
+    switch (mode) {
+        case 0: if (split) VLQ_TC_LAUNCH(0, true); else VLQ_TC_LAUNCH(0, false); break;
+        case 1: if (split) VLQ_TC_LAUNCH(1, true); else VLQ_TC_LAUNCH(1, false); break;
+        case 2: if (split) VLQ_TC_LAUNCH(2, true); else VLQ_TC_LAUNCH(2, false); break;
+        default: if (split) VLQ_TC_LAUNCH(3, true); else VLQ_TC_LAUNCH(3, false); break;
     }
 #undef VLQ_TC_LAUNCH
     CUDA_LAUNCH_CHECK();
@@ -589,6 +609,81 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
     }
 }
 
+// tau[row] = the L-th smallest chunk minimum (an upper bound on the row's
+// L-th smallest approximate value).
+__global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
+                                                  uint32_t* __restrict__ scratch, float* __restrict__ tau) {
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    __shared__ unsigned int s_max;
+    const uint64_t q = blockIdx.x;
+    const float* row = tmin + q * nchunk;
+    uint32_t* pos = scratch + q * L;
+    block_select_ordered(row, nchunk, L, pos, hist, scan);
+    if (threadIdx.x == 0) s_max = 0u;
+    __syncthreads();
+    float mx = -__int_as_float(0x7f800000);
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) mx = fmaxf(mx, row[pos[t]]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_max, ord_float(mx));
+    __syncthreads();
+    if (threadIdx.x == 0) tau[q] = unord_float(s_max);
+}
+
+// Exact top-w1 from the filtered candidate list: exact reference-order
+// sqdist of every listed centroid, (dist, id) order, certificate
+// tau + |y|^2 - eps > exact_w1 (every unlisted centroid has approx > tau).
+__global__ void k_refine_list(const float* __restrict__ Y, uint32_t dim, const float* __restrict__ C, uint32_t k,
+                              const uint32_t* __restrict__ cand, const uint32_t* __restrict__ cnt, uint32_t cap,
+                              const float* __restrict__ tau, uint32_t w1, float cmax, int split,
+                              uint32_t* __restrict__ top, uint32_t* __restrict__ flagged,
+                              unsigned int* __restrict__ nflag) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // pow2 >= cap
+    float* ys = reinterpret_cast<float*>(smem + 8 * 2048);
+    __shared__ float s_yn;
+    const uint64_t q = blockIdx.x;
+    const uint32_t n = cnt[q];
+    if (n > cap || n < w1) {  // list overflow (or too short): exact full row
+        if (threadIdx.x == 0) flagged[atomicAdd(nflag, 1u)] = (uint32_t)q;
+        return;
+    }
+    uint32_t np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
+    __syncthreads();
+    const uint32_t* cq = cand + q * cap;
+    for (uint32_t t = threadIdx.x; t < np2; t += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (t < n) {
+            const uint32_t c = cq[t];
+            const float* cp = C + (uint64_t)c * dim;
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], cp[d]);
+            key = make_key(acc, c);
+        }
+        keys[t] = key;
+    }
+    if (threadIdx.x == 0) {
+        float yn = 0.0f;
+        for (uint32_t d = 0; d < dim; d++) yn = fmaf(ys[d], ys[d], yn);
+        s_yn = yn;
+    }
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, np2, threadIdx.x, blockDim.x);
+    if (threadIdx.x == 0) {
+        const float eps = tc_eps(s_yn, cmax, dim, split != 0);
+        const float exact_w1 = unord_float((uint32_t)(keys[w1 - 1] >> 32));
+        const double lower = (double)tau[q] + (double)s_yn - (double)eps;
+        if (!(lower > (double)exact_w1)) flagged[atomicAdd(nflag, 1u)] = (uint32_t)q;
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < np2; t += blockDim.x) keys[t] = t < w1 ? (uint64_t)(uint32_t)keys[t] : ~0ull;
+    __syncthreads();
+    bitonic_sort_u64<false>(keys, np2, threadIdx.x, blockDim.x);
+    for (uint32_t t = threadIdx.x; t < w1; t += blockDim.x) top[q * w1 + t] = (uint32_t)keys[t];
+}
+
 // Exact full ws rows for the listed queries (certificate failures).
 __global__ void k_exact_rows(const float* __restrict__ Y, uint32_t dim, const float* __restrict__ C, uint32_t k,
                              float* __restrict__ ws, const uint32_t* __restrict__ qlist,
@@ -664,6 +759,24 @@ void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float*
 size_t exact_needed_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t dim) {
     return (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4 +
            (size_t)8 * 32 * (dim + 1) * 4;
+}
+
+void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
+                     cudaStream_t st) {
+    if (nq == 0) return;
+    dev::k_tau_rows<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, scratch, tau);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, const uint32_t* cand,
+                        const uint32_t* cnt, uint32_t cap, const float* tau, uint32_t w1, float cmax, int split,
+                        uint32_t* top, uint32_t* flagged, unsigned int* nflag, cudaStream_t st) {
+    if (nq == 0) return;
+    const size_t smem = 8 * 2048 + (size_t)dim * 4;
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_refine_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_refine_list<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, k, cand, cnt, cap, tau, w1, cmax, split, top,
+                                                        flagged, nflag);
+    CUDA_LAUNCH_CHECK();
 }
 
 void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,

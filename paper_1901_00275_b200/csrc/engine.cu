@@ -63,6 +63,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC_STORE_ROWS")) cfg_.tc_store_rows = std::atoi(v);
     if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
         throw std::runtime_error("engine: invalid shard configuration");
     int ndev = 0;
@@ -483,6 +484,14 @@ void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alp
     ws_.alloc(tile * k_);
     top_.alloc(tile * w1);
     cand_top_.alloc(tile * (uint64_t)std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2)));
+    if (tc_) {
+        const uint32_t tn = tc_split_ ? 64 : 128;
+        tmin_.alloc(tile * (uint64_t)(((k_ + tn - 1) / tn) * (tn / 32)));
+        tau_.alloc(tile);
+        lcnt_.alloc(tile);
+        lidx_.alloc(tile * (uint64_t)kListCap);
+        ld_.alloc(tile * (uint64_t)kListCap);
+    }
     dbuf_.alloc(tile * (uint64_t)w1 * n_);
     sel_.alloc(tile * w2);
     t5_.alloc(tile * VLQ_KSUB * m_);
@@ -507,12 +516,23 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     const bool tc = tc_ && k_ >= cfg_.tc_search_min_k && L <= 2048 && w1 < k_ &&
                     exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
     mark(PH_COARSE);
-    if (tc) {
+    const float* c_hi = tc_split_ ? cent_hi_.p : cent_tc_.p;
+    const float* c_lo = tc_split_ ? cent_lo_.p : nullptr;
+    const uint32_t tn = tc_split_ ? 64 : 128;
+    const uint32_t nchunk = ((k_ + tn - 1) / tn) * (tn / 32);
+    const bool two_pass = tc && nchunk >= 2 * L && !cfg_.tc_store_rows;
+    if (two_pass) {
+        // pass 1: chunk minima -> tau (upper bound of the L-th smallest);
+        // pass 2: recompute, keep only approx <= tau (no K-wide row in HBM)
+        launch_coarse_tc(2, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr, st);
+        launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st);
+        CUDA_CHECK(cudaMemsetAsync(lcnt_.p, 0, nt * 4, st));
+        launch_coarse_tc(3, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, nullptr, 0, lidx_.p, ld_.p, st, tau_.p,
+                         lcnt_.p, kListCap);
+        launches += 3;
+    } else if (tc) {
         // approximate rows on the tensor cores, then top-L on them
-        if (tc_split_)
-            launch_coarse_tc(1, d_q, nt, dim_, cent_hi_.p, cent_lo_.p, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
-        else
-            launch_coarse_tc(1, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
+        launch_coarse_tc(1, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
         launches += 1;
     } else {
         launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
@@ -520,10 +540,15 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     }
     mark(PH_FIRST);
     if (tc) {
-        launch_first_level(ws_.p, nt, k_, L, cand_top_.p, st);
         CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
-        launch_refine_first(d_q, nt, dim_, centroids_.p, ws_.p, k_, cand_top_.p, L, w1, cmax_, top_.p, qlist_.p,
-                            err_.p + 6, tc_split_ ? 1 : 0, st);
+        if (two_pass) {
+            launch_refine_list(d_q, nt, dim_, centroids_.p, k_, lidx_.p, lcnt_.p, kListCap, tau_.p, w1, cmax_,
+                               tc_split_ ? 1 : 0, top_.p, qlist_.p, err_.p + 6, st);
+        } else {
+            launch_first_level(ws_.p, nt, k_, L, cand_top_.p, st);
+            launch_refine_first(d_q, nt, dim_, centroids_.p, ws_.p, k_, cand_top_.p, L, w1, cmax_, top_.p, qlist_.p,
+                                err_.p + 6, tc_split_ ? 1 : 0, st);
+        }
         launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
         launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
         launch_exact_needed(d_q, nt, dim_, centroids_.p, k_, n_, nbr_.p, ws_.p, top_.p, w1, st);

@@ -30,6 +30,7 @@ struct EngineConfig {
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
     uint32_t tc_search_min_k = 16384; // search coarse stage on tensor cores for K >= this (env VLQ_TC_SEARCH_MIN_K)
+    int tc_store_rows = 0;  // 1: materialise approximate rows + radix select instead of the two-pass filter
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -157,6 +158,9 @@ private:
     void assign_chunk(const float* X, uint64_t nx, uint32_t* best, cudaStream_t st);
     DevBuf<uint32_t> tc_idx_, tc_flag_, tc_best_;
     DevBuf<float> tc_d_, tc_rows_;
+    static constexpr uint32_t kListCap = 1024;  // per-query candidate list of the two-pass coarse filter
+    DevBuf<float> tmin_, tau_, ld_;
+    DevBuf<uint32_t> lcnt_, lidx_;
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;
     bool clamp_ = true;

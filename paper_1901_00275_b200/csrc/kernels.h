@@ -114,7 +114,12 @@ void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* 
                                cudaStream_t st);
 void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
                       const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,
-                      cudaStream_t st);
+                      cudaStream_t st, const float* tau = nullptr, uint32_t* cnt = nullptr, uint32_t cap = 0);
+void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
+                     cudaStream_t st);
+void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, const uint32_t* cand,
+                        const uint32_t* cnt, uint32_t cap, const float* tau, uint32_t w1, float cmax, int split,
+                        uint32_t* top, uint32_t* flagged, unsigned int* nflag, cudaStream_t st);
 void launch_refine_argmin(const float* X, uint64_t nx, uint32_t dim, const float* C, const uint32_t* top_idx,
                           const float* top_d, float cmax, uint32_t* best, uint32_t* flagged, unsigned int* nflag,
                           cudaStream_t st);

@@ -92,3 +92,22 @@ def test_tc_larger_codebook_trained_on_gpu(vlqadc, oracle_mod, tmp_path):
         ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
         oids, od, _ = o.search(q, w1, alpha, k)
         assert np.array_equal(ids_, oids) and same_f32(d_, od)
+
+
+@pytest.mark.parametrize("store_rows", ["0", "1"])
+def test_tc_two_pass_coarse_filter_large_k(vlqadc, oracle_mod, tmp_path, monkeypatch, store_rows):
+    """K = 16384: the two-pass tensor-core coarse stage (chunk minima -> tau ->
+    filtered candidate list, no K-wide rows in HBM) and the store-rows variant
+    both reproduce the oracle exactly."""
+    monkeypatch.setenv("VLQ_TC_STORE_ROWS", store_rows)
+    base = vlqadc.gen_synthetic(120000, 32, clusters=2000, spread=0.05, seed=15)
+    q = vlqadc.gen_synthetic(150, 32, clusters=2000, spread=0.05, seed=16)
+    idx = vlqadc.Index.train(base[:60000], k=16384, n=8, m=8, iters=3, seed=4)
+    idx.add(base)
+    path = str(tmp_path / "k16k.vlq")
+    idx.save(path)
+    o = oracle_mod.OracleIndex.load(path)
+    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100), (200, 0.1, 20)]:
+        ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
+        oids, od, _ = o.search(q, w1, alpha, k)
+        assert np.array_equal(ids_, oids) and same_f32(d_, od), (w1, alpha, k)
