@@ -548,8 +548,8 @@ __global__ void k_refine_first(const float* __restrict__ Y, uint32_t dim, const 
 // regions and all their neighbours (second_level_rank reads ws[nbr],
 // search.cpp:57).  Needed ids are deduplicated through a shared bitmap,
 // compacted, and processed 32 at a time: the warp stages 32 centroid rows with
-// coalesced float4 loads, then each lane runs one sequential (reference-order)
-// sqdist from shared memory.
+// 16-byte loads (one thread per centroid), then the sequential
+// reference-order sqdist.
 __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ Y, uint32_t dim,
                                                       const float* __restrict__ C, uint32_t k, uint32_t n,
                                                       const uint32_t* __restrict__ nbr, float* __restrict__ ws,
@@ -559,10 +559,8 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
     uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);            // nwords
     uint32_t* ids = bitmap + nwords;                                  // up to w1*(n+1)
     float* ys = reinterpret_cast<float*>(ids + w1 * (n + 1));         // dim
-    float* rows = ys + ((dim + 3) & ~3u);                             // 8 warps x 32 x (dim+1)
     __shared__ uint32_t s_scan[40];
     const uint64_t q = blockIdx.x;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) bitmap[i] = 0;
     for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
     __syncthreads();
@@ -588,24 +586,47 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
         }
     }
     __syncthreads();
-    // 32 centroids per warp pass
-    float* wrows = rows + (size_t)warp * 32 * (dim + 1);
-    const uint32_t nwarps = blockDim.x >> 5;
+    // one thread per needed centroid: 16-byte loads straight from L2, then the
+    // sequential reference-order sqdist
     float* wsq = ws + q * k;
-    for (uint32_t base = warp * 32; base < total; base += nwarps * 32) {
-        const uint32_t cnt = min(32u, total - base);
-        for (uint32_t r = 0; r < cnt; r++) {
-            const float* cp = C + (uint64_t)ids[base + r] * dim;
-            for (uint32_t d = lane; d < dim; d += 32) wrows[r * (dim + 1) + d] = cp[d];
-        }
-        __syncwarp();
-        if (lane < cnt) {
-            const float* rp = wrows + lane * (dim + 1);
+    if ((dim & 3u) == 0) {
+        const uint32_t n4 = dim >> 2;
+        for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+            const uint32_t c = ids[t];
+            const float4* cp = reinterpret_cast<const float4*>(C + (uint64_t)c * dim);
             float acc = 0.0f;
-            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], rp[d]);
-            wsq[ids[base + lane]] = acc;
+            uint32_t d4 = 0;
+            for (; d4 + 8 <= n4; d4 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = __ldg(cp + d4 + u);
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const uint32_t d = (d4 + u) * 4;
+                    acc = sq_step(acc, ys[d], v[u].x);
+                    acc = sq_step(acc, ys[d + 1], v[u].y);
+                    acc = sq_step(acc, ys[d + 2], v[u].z);
+                    acc = sq_step(acc, ys[d + 3], v[u].w);
+                }
+            }
+            for (; d4 < n4; d4++) {
+                const float4 v = __ldg(cp + d4);
+                const uint32_t d = d4 * 4;
+                acc = sq_step(acc, ys[d], v.x);
+                acc = sq_step(acc, ys[d + 1], v.y);
+                acc = sq_step(acc, ys[d + 2], v.z);
+                acc = sq_step(acc, ys[d + 3], v.w);
+            }
+            wsq[c] = acc;
         }
-        __syncwarp();
+    } else {
+        for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+            const uint32_t c = ids[t];
+            const float* cp = C + (uint64_t)c * dim;
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], cp[d]);
+            wsq[c] = acc;
+        }
     }
 }
 
@@ -746,20 +767,19 @@ void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float*
     CUDA_LAUNCH_CHECK();
 }
 
+size_t exact_needed_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t dim) {
+    return (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4;
+}
+
 void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, uint32_t n,
                          const uint32_t* nbr, float* ws, const uint32_t* top, uint32_t w1, cudaStream_t st) {
     if (nq == 0) return;
-    const size_t smem = (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4 +
-                        (size_t)8 * 32 * (dim + 1) * 4;
+    const size_t smem = exact_needed_smem(k, n, w1, dim);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_exact_needed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dev::k_exact_needed<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, k, n, nbr, ws, top, w1);
     CUDA_LAUNCH_CHECK();
 }
 
-size_t exact_needed_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t dim) {
-    return (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4 +
-           (size_t)8 * 32 * (dim + 1) * 4;
-}
 
 void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
                      cudaStream_t st) {
