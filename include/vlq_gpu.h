@@ -109,6 +109,19 @@ int vlq_engine_search_device(vlq_engine* e, const float* d_queries, uint64_t nq,
                              uint32_t k, int64_t* d_ids, float* d_dists, uint64_t* d_scanned, void* stream);
 int vlq_engine_sync(vlq_engine* e, void* stream);
 
+/* Index.search split at the first-level boundary, for the query-split
+ * multi-GPU path (each rank runs the coarse stage on a slice of the batch,
+ * the slices are all-gathered, every rank runs the fine stage on its shard):
+ *  - coarse: first_level_scan (proj/src/search.cpp:11-36) -> d_top[nq*w1],
+ *    the exact top-w1 region ids of each query in (dist, id) order;
+ *  - fine: second_level_rank .. select_topk (search.cpp:38-167) from d_top.
+ * coarse followed by fine on the same engine equals vlq_engine_search_device. */
+int vlq_engine_search_coarse_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, uint32_t* d_top,
+                                    void* stream);
+int vlq_engine_search_fine_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                                  uint32_t k, const uint32_t* d_top, int64_t* d_ids, float* d_dists,
+                                  uint64_t* d_scanned, void* stream);
+
 /* Streamed Index.add of the engine's counter-based synthetic generator
  * (the reference's Gaussian-mixture law, dataset.cpp:13-44): rows are
  * generated on the device chunk by chunk, so 1e8-1e9-point bases never touch
@@ -123,6 +136,12 @@ int vlq_gen_synthetic_device(int device, uint64_t first, uint64_t count, uint32_
  * generator (ground truth at scale). */
 int vlq_brute_force_gt_synthetic(int device, uint64_t nb, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
                                  const float* queries, uint64_t nq, uint32_t k, uint32_t* out);
+
+/* Study knobs, not part of the reference surface: "scan_variant" (0 = v6
+ * packed-fp32 fast scan, 2/3/4 = v5 LUT layouts, 1 = generic scan),
+ * "scan_slots" (entry slots per lane: 4/6/8), "tc_search_min_k",
+ * "force_exact".  Results are identical for every setting. */
+int vlq_engine_set_tuning(vlq_engine* e, const char* key, int64_t value);
 
 /* Per-phase CUDA-event timing (recorded on the search stream) and counters. */
 int vlq_engine_set_profiling(vlq_engine* e, int on);

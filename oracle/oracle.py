@@ -119,6 +119,30 @@ class OracleIndex:
                                ctypes.c_int(threads)))
         return ids, dists, scanned
 
+    def first_level(self, queries: np.ndarray, w1: int, threads: int = 0) -> np.ndarray:
+        """Exact top-w1 region ids of every query (first_level_scan,
+        search.cpp:11-36), uint32 [nq, w1] in (dist, id) order."""
+        q = np.ascontiguousarray(queries, np.float32)
+        top = np.empty((q.shape[0], w1), np.uint32)
+        _check(lib().vo_first_level(ctypes.byref(self.s), _p(q), ctypes.c_uint64(q.shape[0]), ctypes.c_uint32(w1),
+                                    _p(top), ctypes.c_int(threads)))
+        return top
+
+    def search_from_top(self, queries: np.ndarray, top: np.ndarray, w1: int, alpha: float, k: int,
+                        threads: int = 0):
+        """search() from given top-w1 lists (search.cpp:38-167)."""
+        q = np.ascontiguousarray(queries, np.float32)
+        top = np.ascontiguousarray(top, np.uint32)
+        assert top.shape == (q.shape[0], w1)
+        nq = q.shape[0]
+        ids = np.empty((nq, k), np.int64)
+        dists = np.empty((nq, k), np.float32)
+        scanned = np.zeros(nq, np.uint64)
+        _check(lib().vo_search_from_top(ctypes.byref(self.s), _p(q), ctypes.c_uint64(nq), ctypes.c_uint32(w1),
+                                        ctypes.c_float(alpha), ctypes.c_uint32(k), _p(top), _p(ids), _p(dists),
+                                        _p(scanned), ctypes.c_int(threads)))
+        return ids, dists, scanned
+
     def assign(self, base: np.ndarray, clamp: bool | None = None, threads: int = 0):
         """Per-point (cell, exact lambda, code, lambda byte) of the add path."""
         x = np.ascontiguousarray(base, np.float32)

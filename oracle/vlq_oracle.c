@@ -217,17 +217,30 @@ typedef struct {
     size_t cand_cap;
 } vo_scratch;
 
+/* top_in (nullable): the query's top-w1 regions from an earlier
+ * first-level pass (the staged / query-split search); top_out (nullable)
+ * receives them; out_ids == NULL stops after the first level. */
 static int search_one(const vo_index* ix, const float* y, uint32_t w1, uint32_t w2, uint32_t topk,
-                      vo_scratch* s, int64_t* out_ids, float* out_d, uint64_t* scanned) {
+                      vo_scratch* s, int64_t* out_ids, float* out_d, uint64_t* scanned,
+                      const uint32_t* top_in, uint32_t* top_out) {
     const uint32_t k = ix->k, n = ix->n, m = ix->m, dim = ix->dim, dsub = dim / m;
     /* first_level_scan (search.cpp:11-36) */
     for (uint32_t i = 0; i < k; i++) {
         s->ws[i] = vo_sqdist(y, ix->centroids + (size_t)i * dim, dim);
         s->keys[i] = fkey(s->ws[i], i);
     }
-    select_smallest(s->keys, k, w1);
     uint32_t* top = (uint32_t*)malloc(sizeof(uint32_t) * w1);
-    for (uint32_t r = 0; r < w1; r++) top[r] = (uint32_t)s->keys[r];
+    if (top_in) {
+        memcpy(top, top_in, sizeof(uint32_t) * w1);
+    } else {
+        select_smallest(s->keys, k, w1);
+        for (uint32_t r = 0; r < w1; r++) top[r] = (uint32_t)s->keys[r];
+    }
+    if (top_out) memcpy(top_out, top, sizeof(uint32_t) * w1);
+    if (!out_ids) {
+        free(top);
+        return 0;
+    }
     /* second_level_rank (search.cpp:38-78) */
     size_t total = (size_t)w1 * n;
     for (uint32_t r = 0; r < w1; r++) {
@@ -357,6 +370,8 @@ typedef struct {
     int64_t* out_ids;
     float* out_dists;
     uint64_t* out_scanned;
+    const uint32_t* top_in;
+    uint32_t* top_out;
 } search_ctx;
 
 static void* search_scratch(void* c) {
@@ -381,8 +396,11 @@ static void search_scratch_free(void* p) {
 static int search_item(void* c, void* scratch, int64_t q) {
     search_ctx* ctx = (search_ctx*)c;
     return search_one(ctx->ix, ctx->queries + (size_t)q * ctx->ix->dim, ctx->w1, ctx->w2, ctx->topk,
-                      (vo_scratch*)scratch, ctx->out_ids + (size_t)q * ctx->topk,
-                      ctx->out_dists + (size_t)q * ctx->topk, ctx->out_scanned + q);
+                      (vo_scratch*)scratch, ctx->out_ids ? ctx->out_ids + (size_t)q * ctx->topk : NULL,
+                      ctx->out_dists ? ctx->out_dists + (size_t)q * ctx->topk : NULL,
+                      ctx->out_scanned ? ctx->out_scanned + q : NULL,
+                      ctx->top_in ? ctx->top_in + (size_t)q * ctx->w1 : NULL,
+                      ctx->top_out ? ctx->top_out + (size_t)q * ctx->w1 : NULL);
 }
 
 /* search_batch (search.cpp:169-191); per-query scanned counts returned
@@ -391,7 +409,26 @@ int vo_search(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1
               uint32_t topk, int64_t* out_ids, float* out_dists, uint64_t* out_scanned,
               int nthreads) {
     if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
-    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned};
+    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, NULL, NULL};
+    return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
+}
+
+/* The same search split at the first-level boundary (the GPU engine's
+ * vlq_engine_search_coarse_device / _fine_device): vo_first_level writes
+ * the exact top-w1 of every query, vo_search_from_top runs
+ * second_level_rank .. select_topk from given top-w1 lists. */
+int vo_first_level(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1, uint32_t* top_out,
+                   int nthreads) {
+    if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
+    search_ctx ctx = {ix, queries, w1, 1, 0, NULL, NULL, NULL, NULL, top_out};
+    return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
+}
+
+int vo_search_from_top(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1, float alpha,
+                       uint32_t topk, const uint32_t* top_in, int64_t* out_ids, float* out_dists,
+                       uint64_t* out_scanned, int nthreads) {
+    if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
+    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, top_in, NULL};
     return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
 }
 

@@ -47,6 +47,9 @@ _SIGS = {
     "vlq_engine_train": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_u32, c_u32, c_u32, c_u64, c_i32]),
     "vlq_engine_search": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp]),
     "vlq_engine_search_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp]),
+    "vlq_engine_set_tuning": (c_i32, [c_vp, ctypes.c_char_p, ctypes.c_int64]),
+    "vlq_engine_search_coarse_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_vp, c_vp]),
+    "vlq_engine_search_fine_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_sync": (c_i32, [c_vp, c_vp]),
     "vlq_engine_info": (c_i32, [c_vp, ctypes.POINTER(VlqInfo)]),
     "vlq_engine_add_synthetic": (c_i32, [c_vp, c_u64, c_u32, c_f32, c_u64]),

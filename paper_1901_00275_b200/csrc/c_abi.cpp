@@ -162,6 +162,30 @@ int vlq_engine_search_device(vlq_engine* e, const float* d_queries, uint64_t nq,
     });
 }
 
+int vlq_engine_search_coarse_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, uint32_t* d_top,
+                                    void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        e->impl->search_coarse_device(d_queries, nq, w1, d_top, stream ? (cudaStream_t)stream : e->impl->stream());
+    });
+}
+
+int vlq_engine_search_fine_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                                  uint32_t k, const uint32_t* d_top, int64_t* d_ids, float* d_dists,
+                                  uint64_t* d_scanned, void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        e->impl->search_fine_device(d_queries, nq, w1, alpha, k, d_top, d_ids, d_dists, d_scanned,
+                                    stream ? (cudaStream_t)stream : e->impl->stream());
+    });
+}
+
+int vlq_engine_set_tuning(vlq_engine* e, const char* key, int64_t value) {
+    ENGINE_OR_FAIL(e);
+    if (!key) return fail(VLQ_ERR_INVALID, "set_tuning: key is NULL");
+    return guarded([&] { e->impl->set_tuning(key, value); });
+}
+
 int vlq_engine_sync(vlq_engine* e, void* stream) {
     ENGINE_OR_FAIL(e);
     return guarded([&] { e->impl->check_device_errors(stream ? (cudaStream_t)stream : e->impl->stream()); });

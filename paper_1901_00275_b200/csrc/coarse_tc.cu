@@ -103,8 +103,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int MODE>  // 0 = ARGMIN (top-4 per row), 1 = STORE (approx row)
-__host__ __device__ constexpr int tc_stages() { return MODE == 1 ? 2 : 3; }
+constexpr int TC_MAX_STAGES = 3;  // centroid-tile ring depth: as many as fit in 227 KB, 2 or 3
+// (a template parameter: a runtime ring depth made nvcc 12.9 drop the high
+// half of the bulk-copy source address in the producer loop)
 
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
@@ -120,7 +121,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // MODE 3 = FILTER: per row, append every (approx, centroid) with approx <=
 //   tau[row] to the row's candidate list (top_d/top_idx, capacity cap,
 //   count in cnt[row]).
-template <int MODE, bool SPLIT>
+template <int MODE, bool SPLIT, int TC_STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_coarse_tc(const float* __restrict__ X, uint64_t nx, uint32_t dim, const float* __restrict__ cent_tc,
                 const float* __restrict__ cent_lo, const float* __restrict__ cnorm_pad, uint32_t ntiles,
@@ -133,7 +134,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t a_bytes = TC_M * dim * 4;
     unsigned char* sA = smem;
     unsigned char* sAlo = smem + a_bytes;  // SPLIT only
-    constexpr int TC_STAGES = tc_stages<MODE>();
     constexpr int NB = SPLIT ? 2 : 1;
     unsigned char* sB = smem + a_bytes * NB;                              // STAGES x NB x tile_bytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + TC_STAGES * NB * tile_bytes);
@@ -361,22 +361,31 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
 
 }  // namespace dev
 
-size_t coarse_tc_smem(uint32_t dim, int mode, bool split) {
-    const int stages = mode == 1 ? dev::tc_stages<1>() : dev::tc_stages<0>();
+static size_t coarse_tc_smem_at(uint32_t dim, int mode, bool split, uint32_t stages) {
     const size_t tail = mode == 1 ? (size_t)8 * 32 * 33 * 4 : (size_t)dev::TC_M * 8 * 4;
     const size_t tn = split ? 64 : dev::TC_N, nb = split ? 2 : 1;
     return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * nb * tn * dim * 4 + 2 * stages * 8 + 4 * 8 + 16 +
            tail + 256;
 }
 
-bool coarse_tc_supported(uint32_t dim) {
-    return dim % 8 == 0 && dim >= 8 && coarse_tc_smem(dim, 0, false) <= 227 * 1024 &&
-           coarse_tc_smem(dim, 1, false) <= 227 * 1024;
+// deepest centroid-tile ring (<= TC_MAX_STAGES) that fits 227 KB; 0 if not even 2
+static uint32_t coarse_tc_stages(uint32_t dim, int mode, bool split) {
+    for (uint32_t s = dev::TC_MAX_STAGES; s >= 2; s--)
+        if (coarse_tc_smem_at(dim, mode, split, s) <= 227 * 1024) return s;
+    return 0;
 }
 
-bool coarse_tc_split_supported(uint32_t dim) {
-    return dim % 8 == 0 && dim >= 8 && coarse_tc_smem(dim, 1, true) <= 227 * 1024;
+// every epilogue mode the engine may launch (add: 0; search: 1, 2, 3)
+static bool coarse_tc_fits(uint32_t dim, bool split) {
+    if (dim % 8 != 0 || dim < 8) return false;
+    for (int mode = 0; mode < 4; mode++)
+        if (coarse_tc_stages(dim, mode, split) == 0) return false;
+    return true;
 }
+
+bool coarse_tc_supported(uint32_t dim) { return coarse_tc_fits(dim, false); }
+
+bool coarse_tc_split_supported(uint32_t dim) { return coarse_tc_fits(dim, true); }
 
 void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
                                cudaStream_t st) {
@@ -392,11 +401,13 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
     const bool split = cent_lo != nullptr;
     const uint32_t tn = split ? 64 : dev::TC_N;
     const uint32_t ntiles = (k + tn - 1) / tn;
-    const size_t smem = coarse_tc_smem(dim, mode, split);
+    const uint32_t stages = coarse_tc_stages(dim, mode, split);
+    if (stages == 0) throw std::runtime_error("coarse_tc: shared-memory ring does not fit for this dim");
+    const size_t smem = coarse_tc_smem_at(dim, mode, split, stages);
     const unsigned grid = (unsigned)((nx + dev::TC_M - 1) / dev::TC_M);
 #define VLQ_TC_LAUNCH(MODE_, SPLIT_)                                                                            \
     do {                                                                                                        \
-        auto fn = dev::k_coarse_tc<MODE_, SPLIT_>;                                                              \
+        auto fn = stages == 3 ? dev::k_coarse_tc<MODE_, SPLIT_, 3> : dev::k_coarse_tc<MODE_, SPLIT_, 2>;         \
         CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
         fn<<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cent_lo, cnorm, ntiles, k, out_row, ldo,   \
                                                 top_idx, top_d, tau, cnt, cap);                                 \
@@ -554,7 +565,7 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
                                                       const float* __restrict__ C, uint32_t k, uint32_t n,
                                                       const uint32_t* __restrict__ nbr, float* __restrict__ ws,
                                                       const uint32_t* __restrict__ top, uint32_t w1) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t nwords = (k + 31) / 32;
     uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);            // nwords
     uint32_t* ids = bitmap + nwords;                                  // up to w1*(n+1)

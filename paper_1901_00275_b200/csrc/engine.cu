@@ -60,6 +60,7 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -469,6 +470,24 @@ void Engine::get_tables(std::vector<float>& t2, std::vector<float>& t3) {
 // ---------------------------------------------------------------------------
 void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
                            float* d_dists, uint64_t* d_scanned, cudaStream_t st) {
+    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, nullptr, nullptr, STAGE_ALL, st);
+}
+
+void Engine::search_coarse_device(const float* d_q, uint64_t nq, uint32_t w1, uint32_t* d_top, cudaStream_t st) {
+    if (!d_top) throw std::runtime_error("search_coarse: top output is NULL");
+    search_staged(d_q, nq, w1, 0.0f, 1, nullptr, nullptr, nullptr, nullptr, d_top, STAGE_COARSE, st);
+}
+
+void Engine::search_fine_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
+                                const uint32_t* d_top, int64_t* d_ids, float* d_dists, uint64_t* d_scanned,
+                                cudaStream_t st) {
+    if (!d_top) throw std::runtime_error("search_fine: top input is NULL");
+    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, d_top, nullptr, STAGE_FINE, st);
+}
+
+void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
+                           float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
+                           Stage stage, cudaStream_t st) {
     if (!model_ok_) throw std::runtime_error("search: no model loaded");
     if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
     if (topk > 1024) throw std::runtime_error("search: k > 1024 is not supported by the GPU engine");
@@ -500,22 +519,74 @@ void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alp
     qlist_.alloc(tile);
     for (uint64_t t0 = 0; t0 < nq; t0 += tile) {
         const uint64_t nt = std::min(tile, nq - t0);
-        search_tile(d_q + t0 * dim_, nt, w1, w2, topk, d_ids + t0 * topk, d_dists + t0 * topk,
-                    d_scanned ? d_scanned + t0 : nullptr, st);
+        search_tile(d_q + t0 * dim_, nt, w1, w2, topk, d_ids ? d_ids + t0 * topk : nullptr,
+                    d_dists ? d_dists + t0 * topk : nullptr, d_scanned ? d_scanned + t0 : nullptr,
+                    d_top_in ? d_top_in + t0 * w1 : nullptr, d_top_out ? d_top_out + t0 * w1 : nullptr, stage, st);
     }
 }
 
 void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
-                         float* d_dists, uint64_t* d_scanned, cudaStream_t st) {
-    SearchArgs a = search_args();
+                         float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
+                         Stage stage, cudaStream_t st) {
     auto mark = [&](int ph) {
         if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
     };
     uint64_t launches = 0;
+    bool tc = false, fast = false;
+    mark(PH_COARSE);
+    if (stage == STAGE_FINE) {
+        // top-w1 from another rank's coarse stage: exact distances of the
+        // regions and neighbours the later stages read (as the TC path does)
+        CUDA_CHECK(cudaMemcpyAsync(top_.p, d_top_in, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
+        mark(PH_FIRST);
+        if (exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024)
+            launch_exact_needed(d_q, nt, dim_, centroids_.p, k_, n_, nbr_.p, ws_.p, top_.p, w1, st);
+        else
+            launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
+        launches += 1;
+    } else {
+        tc = coarse_tile(d_q, nt, w1, launches, st);
+    }
+    if (stage == STAGE_COARSE) {
+        CUDA_CHECK(cudaMemcpyAsync(d_top_out, top_.p, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
+        for (int p = PH_SECOND; p <= PH_COUNT; p++) mark(p);
+    } else {
+        fast = fine_tile(d_q, nt, w1, w2, topk, d_ids, d_dists, d_scanned, launches, st);
+    }
+    stats_.launches += launches;
+    stats_.tiles += 1;
+    if (profiling_) {
+        CUDA_CHECK(cudaEventSynchronize(ev_[PH_COUNT]));
+        for (int p = 0; p < PH_COUNT; p++) {
+            float ms = 0.0f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[p], ev_[p + 1]));
+            stats_.phase_ms[p] += ms;
+        }
+        if (fast) {
+            unsigned int nflag = 0;
+            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            stats_.flagged += nflag;
+        }
+        if (tc) {
+            unsigned int nflag = 0;
+            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            stats_.tc_refine_fallbacks += nflag;
+        }
+    }
+}
+
+// first_level_scan (search.cpp:11-36): exact top-w1 regions into top_ (and,
+// on the tensor-core path, exact ws_ entries for them and their neighbours).
+// Returns whether the tensor-core path ran.
+bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& launches, cudaStream_t st) {
+    auto mark = [&](int ph) {
+        if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
+    };
     const uint32_t L = std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2));
     const bool tc = tc_ && k_ >= cfg_.tc_search_min_k && L <= 2048 && w1 < k_ &&
                     exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
-    mark(PH_COARSE);
     const float* c_hi = tc_split_ ? cent_hi_.p : cent_tc_.p;
     const float* c_lo = tc_split_ ? cent_lo_.p : nullptr;
     const uint32_t tn = tc_split_ ? 64 : 128;
@@ -557,6 +628,17 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         launch_first_level(ws_.p, nt, k_, w1, top_.p, st);
         launches += 1;
     }
+    return tc;
+}
+
+// second_level_rank -> query_term5 -> fused scan + top-k' -> exact re-score
+// (search.cpp:38-167) from top_ / ws_.  Returns whether the fast scan ran.
+bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
+                       float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st) {
+    auto mark = [&](int ph) {
+        if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
+    };
+    SearchArgs a = search_args();
     mark(PH_SECOND);
     launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
@@ -569,7 +651,8 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
         mark(PH_SCAN);
-        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, st)) launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
+        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, cfg_.scan_slots, st))
+            launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
         mark(PH_FALLBACK);
@@ -594,28 +677,15 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         launches += 1;
     }
     mark(PH_COUNT);
-    stats_.launches += launches;
-    stats_.tiles += 1;
-    if (profiling_) {
-        CUDA_CHECK(cudaEventSynchronize(ev_[PH_COUNT]));
-        for (int p = 0; p < PH_COUNT; p++) {
-            float ms = 0.0f;
-            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[p], ev_[p + 1]));
-            stats_.phase_ms[p] += ms;
-        }
-        if (fast) {
-            unsigned int nflag = 0;
-            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaStreamSynchronize(st));
-            stats_.flagged += nflag;
-        }
-        if (tc) {
-            unsigned int nflag = 0;
-            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaStreamSynchronize(st));
-            stats_.tc_refine_fallbacks += nflag;
-        }
-    }
+    return fast;
+}
+
+void Engine::set_tuning(const std::string& key, int64_t value) {
+    if (key == "scan_variant") cfg_.scan_variant = (int)value;
+    else if (key == "scan_slots") cfg_.scan_slots = (int)value;
+    else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;
+    else if (key == "force_exact") cfg_.force_exact = (int)value;
+    else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 
 void Engine::set_profiling(bool on) {
@@ -632,22 +702,34 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     if (nq == 0) return;
     DeviceGuard g(cfg_.device);
     cudaStream_t st = stream_;
-    DevBuf<float> dq, dd;
-    DevBuf<int64_t> di;
-    DevBuf<uint64_t> ds;
-    dq.alloc(nq * dim_);
-    di.alloc(std::max<uint64_t>(nq * topk, 1));
-    dd.alloc(std::max<uint64_t>(nq * topk, 1));
-    ds.alloc(nq);
+    // grow-only device buffers and pinned host staging: no per-call
+    // cudaMalloc/cudaFree (cudaFree synchronises the device) and full-speed
+    // DMA instead of pageable copies
+    const size_t qb = nq * dim_ * 4, ib = nq * topk * 8, db = nq * topk * 4, sb = nq * 8;
+    sq_.alloc(nq * dim_);
+    si_.alloc(std::max<uint64_t>(nq * topk, 1));
+    sd_.alloc(std::max<uint64_t>(nq * topk, 1));
+    ss_.alloc(nq);
+    pin_.alloc(qb + ib + db + sb);
+    unsigned char* pq = pin_.p;
+    unsigned char* pi = pq + qb;
+    unsigned char* pd = pi + ib;
+    unsigned char* ps = pd + db;
+    std::memcpy(pq, q, qb);
     CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
-    CUDA_CHECK(cudaMemcpyAsync(dq.p, q, nq * dim_ * 4, cudaMemcpyHostToDevice, st));
-    search_device(dq.p, nq, w1, alpha, topk, di.p, dd.p, ds.p, st);
+    CUDA_CHECK(cudaMemcpyAsync(sq_.p, pq, qb, cudaMemcpyHostToDevice, st));
+    search_device(sq_.p, nq, w1, alpha, topk, si_.p, sd_.p, ss_.p, st);
     if (topk) {
-        CUDA_CHECK(cudaMemcpyAsync(ids, di.p, nq * topk * 8, cudaMemcpyDeviceToHost, st));
-        CUDA_CHECK(cudaMemcpyAsync(dists, dd.p, nq * topk * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(pi, si_.p, ib, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(pd, sd_.p, db, cudaMemcpyDeviceToHost, st));
     }
-    if (scanned) CUDA_CHECK(cudaMemcpyAsync(scanned, ds.p, nq * 8, cudaMemcpyDeviceToHost, st));
+    if (scanned) CUDA_CHECK(cudaMemcpyAsync(ps, ss_.p, sb, cudaMemcpyDeviceToHost, st));
     check_device_errors(st);
+    if (topk) {
+        std::memcpy(ids, pi, ib);
+        std::memcpy(dists, pd, db);
+    }
+    if (scanned) std::memcpy(scanned, ps, sb);
 }
 
 // ---------------------------------------------------------------------------

@@ -26,7 +26,8 @@ struct EngineConfig {
     uint64_t workspace_bytes = 4ull << 30;  // per-query-tile scratch budget
     uint32_t max_tile = 16384;
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
-    int scan_variant = 0;  // 0 default (single-table LUT), 1 generic warp-buffer scan, 2 replicated LUT
+    int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants
+    int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
     uint32_t tc_search_min_k = 16384; // search coarse stage on tensor cores for K >= this (env VLQ_TC_SEARCH_MIN_K)
@@ -51,6 +52,27 @@ struct HostLists {
     std::vector<uint8_t> codes;
     std::vector<uint8_t> lambdas;
     uint64_t base_count = 0;
+};
+
+// grow-only pinned host buffer (staging for the host-pointer API)
+struct PinnedBuf {
+    unsigned char* p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() { reset(); }
+    void reset() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t bytes) {
+        if (bytes <= n && p) return;
+        reset();
+        CUDA_CHECK(cudaMallocHost(&p, bytes));
+        n = bytes;
+    }
 };
 
 template <typename T>
@@ -116,6 +138,15 @@ public:
     // search (Index.search, bindings.cpp:99-126): device pointers, async on `st`
     void search_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
                        float* d_dists, uint64_t* d_scanned, cudaStream_t st);
+    // Staged search for the query-split multi-GPU path:
+    //   coarse: first_level_scan only (search.cpp:11-36) -> exact top-w1 region
+    //           ids per query, d_top [nq, w1] in (dist, id) order;
+    //   fine:   everything after it (search.cpp:38-167) from a given d_top, on
+    //           this engine's shard.  coarse + fine == search_device.
+    void search_coarse_device(const float* d_q, uint64_t nq, uint32_t w1, uint32_t* d_top, cudaStream_t st);
+    void search_fine_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
+                            const uint32_t* d_top, int64_t* d_ids, float* d_dists, uint64_t* d_scanned,
+                            cudaStream_t st);
     void search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
                      float* dists, uint64_t* scanned);
     void check_device_errors(cudaStream_t st);
@@ -138,6 +169,8 @@ public:
                                       uint64_t nq, uint32_t dim, uint32_t k, uint32_t* out);
 
     void set_profiling(bool on);
+    // study knobs (scan_variant, scan_slots, use_tc_search): take effect on the next search
+    void set_tuning(const std::string& key, int64_t value);
     const EngineStats& stats() const { return stats_; }
     void reset_stats() { stats_ = EngineStats(); }
 
@@ -147,8 +180,16 @@ private:
     void compute_eterm();
     AddArgs add_args() const;
     SearchArgs search_args() const;
+    enum Stage { STAGE_ALL = 0, STAGE_COARSE = 1, STAGE_FINE = 2 };
+    void search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
+                       float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
+                       Stage stage, cudaStream_t st);
+    bool coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& launches, cudaStream_t st);
+    bool fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
+                   float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st);
     void search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
-                     float* d_dists, uint64_t* d_scanned, cudaStream_t st);
+                     float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
+                     Stage stage, cudaStream_t st);
 
     EngineConfig cfg_;
     cudaStream_t stream_ = nullptr;
@@ -181,6 +222,12 @@ private:
     DevBuf<uint32_t> ids_;
     DevBuf<float> eterm_;
     DevBuf<unsigned int> err_;  // [0] error flag, [1] emax bits, [2] flagged count, [3..4] minmax
+
+    // host-pointer search staging (search_host)
+    DevBuf<float> sq_, sd_;
+    DevBuf<int64_t> si_;
+    DevBuf<uint64_t> ss_;
+    PinnedBuf pin_;
 
     // search workspace
     DevBuf<float> ws_, dbuf_, t5_;

@@ -69,7 +69,8 @@ void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, flo
 size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);
 void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,
                  bool fast, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st);
-bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, cudaStream_t st);
+bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int slots,
+                      cudaStream_t st);
 void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
                     cudaStream_t st);
 void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,

@@ -389,6 +389,231 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 || U 
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
 }
 
+// v6: the v5 schedule (balanced chunk ranges, block-shared candidate buffer,
+// adaptive rounds) with the per-entry arithmetic halved by the sm_100
+// packed fp32 pipe.  Entries are taken in pairs (slot u, u+1 of a lane):
+//     lambda, term1, term1 + e, the m-term LUT sum and the final -2 sum5 FFMA
+// run as FFMA2 / FADD2 on (entry u, entry u+1), each element with exactly the
+// rounding of the scalar v5 code (per-entry operation order unchanged, so the
+// certificate of k_rescore holds as is).  Loads are unconditional at a
+// clamped index (no zero-fill moves), and the threshold test is one float
+// compare against the threshold key's distance; the exact 64-bit
+// (dist, position) key is formed only for entries that pass it.
+template <int M>
+__device__ __forceinline__ float lut_at(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], int p) {
+    return *reinterpret_cast<const float*>(lut + 4 * 256 * p + lut_index<0>(w[p >> 2], p & 3, 0u));
+}
+
+__device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an order-preserving key (upper 32 bits)
+    const uint32_t ub = (uint32_t)(key >> 32);
+    return __uint_as_float((ub & 0x80000000u) ? (ub & 0x7fffffffu) : ~ub);
+}
+
+template <int M, int U>
+__global__ void __launch_bounds__(256, 3) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
+    static_assert(U % 2 == 0, "entries are processed in pairs");
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NW = (M + 3) / 4;
+    constexpr uint32_t CH = 32 * U;  // entries per chunk
+    const uint32_t nwarps = blockDim.x >> 5;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t q = blockIdx.x;
+    unsigned char* lut = smem;
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + 4 * 256 * M);  // cap keys
+    uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);         // w2 + 1
+    __shared__ uint32_t hist[256];
+    __shared__ unsigned int s_misc[48];
+    __shared__ unsigned int s_count;
+    __shared__ unsigned long long s_tau;
+
+    // 1. the query's term5 table (one copy per sub-space)
+    const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
+    for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    // 2. chunk prefix over the selected cells (chunks never straddle cells)
+    const uint32_t* selq = a.sel + q * w2;
+    {
+        const uint32_t per = (w2 + blockDim.x - 1) / blockDim.x;
+        uint32_t local = 0;
+        for (uint32_t t = threadIdx.x * per; t < min(w2, (threadIdx.x + 1) * per); t++) {
+            const uint32_t c = selq[t];
+            const uint32_t len = (uint32_t)(a.list_off[c + 1] - a.list_off[c]);
+            cpref[t] = (len + CH - 1) / CH;
+            local += cpref[t];
+        }
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, s_misc + 8, &total);
+        for (uint32_t t = threadIdx.x * per; t < min(w2, (threadIdx.x + 1) * per); t++) {
+            const uint32_t c = cpref[t];
+            cpref[t] = run;
+            run += c;
+        }
+        if (threadIdx.x == 0) {
+            cpref[w2] = total;
+            s_count = 0;
+            s_tau = ~0ull;
+        }
+    }
+    __syncthreads();
+    const uint32_t nchunks = cpref[w2];
+    const uint32_t c_lo = (uint32_t)(((uint64_t)nchunks * warp) / nwarps);
+    const uint32_t c_hi = (uint32_t)(((uint64_t)nchunks * (warp + 1)) / nwarps);
+    uint32_t t = 0;
+    {
+        uint32_t lo = 0, hi = w2;  // largest t with cpref[t] <= c_lo
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cpref[mid] <= c_lo) lo = mid;
+            else hi = mid;
+        }
+        t = lo;
+    }
+    const float* wsq = a.ws + q * a.k;
+    const float2 delta2 = make_float2(a.lam_delta, a.lam_delta), lam02 = make_float2(a.lam0, a.lam0);
+    const float2 m2 = make_float2(-2.0f, -2.0f);
+    uint32_t L = 0, pos0 = 0;
+    const uint8_t* codes_c = nullptr;
+    const uint8_t* lam_c = nullptr;
+    const float* e_c = nullptr;
+    float2 av2 = make_float2(0.f, 0.f), Bc2 = av2, cv2 = av2;
+    uint32_t loaded_t = 0xffffffffu;
+
+    auto locate = [&](uint32_t g) {  // walks t forward to the cell holding chunk g
+        while (cpref[t + 1] <= g) t++;
+        if (t != loaded_t) {
+            loaded_t = t;
+            const uint32_t cell = selq[t];
+            const uint64_t b0 = a.list_off[cell];
+            L = (uint32_t)(a.list_off[cell + 1] - b0);
+            pos0 = (uint32_t)b0;
+            const uint32_t i = cell / a.n;
+            const float av = wsq[i];
+            const float bv = wsq[a.nbr[cell]];
+            const float cv = a.elen[cell];
+            av2 = make_float2(av, av);
+            Bc2 = make_float2((bv - av) - cv, (bv - av) - cv);
+            cv2 = make_float2(cv, cv);
+            codes_c = a.codes + b0 * M;
+            lam_c = a.lambdas + b0;
+            e_c = a.eterm + b0;
+        }
+        return (g - cpref[t]) * CH;
+    };
+
+    uint32_t done = 0;
+    uint64_t n_seen = 0;
+    uint32_t rlen = 1;
+    const uint32_t my_total = c_hi - c_lo;
+    while (__syncthreads_or(done < my_total)) {
+        for (uint32_t r = 0; r < rlen && done < my_total; r++) {
+            const uint32_t o = locate(c_lo + done);
+            uint32_t cw[U][NW];
+            uint32_t lb[U];
+            float ev[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t ic = min(o + u * 32 + lane, L - 1);  // clamped: the tail re-reads entry L-1
+                load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
+                lb[u] = __ldg(lam_c + ic);
+                ev[u] = __ldg(e_c + ic);
+            }
+            const uint64_t tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
+            const float taud = tau == ~0ull ? __int_as_float(0x7f800000) : key_dist(tau);
+            uint32_t tk = 0;
+            float dist[U];
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+                dist[u] = dist[u + 1] = __int_as_float(0x7fffffff);
+                if (o + u * 32 < L) {  // warp-uniform: skip fully empty pairs
+                    const float2 lam = __ffma2_rn(make_float2((float)lb[u], (float)lb[u + 1]), delta2, lam02);
+                    const float2 t1 = __ffma2_rn(lam, __ffma2_rn(lam, cv2, Bc2), av2);
+                    const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
+                    float2 s = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
+#pragma unroll
+                    for (int p = 1; p < M; p++)
+                        s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
+                    const float2 d = __ffma2_rn(m2, s, te);
+                    dist[u] = d.x;
+                    dist[u + 1] = d.y;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t idx = o + u * 32 + lane;
+                if (idx < L && dist[u] <= taud) {  // rare after the first rounds: exact key test
+                    uint32_t ub = __float_as_uint(dist[u]);
+                    ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
+                    const uint64_t key = ((uint64_t)ub << 32) | (pos0 + idx);
+                    if (key < tau) tk |= 1u << u;
+                }
+            }
+            const uint32_t any = __ballot_sync(0xffffffffu, tk != 0);
+            if (any) {
+                uint32_t wtot = 0;
+                uint32_t bal[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    bal[u] = __ballot_sync(0xffffffffu, (tk >> u) & 1u);
+                    wtot += __popc(bal[u]);
+                }
+                uint32_t base = 0;
+                if (lane == 0) {
+                    unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&s_count);
+                    base = 0xffffffffu;
+                    while (cur + wtot <= cap) {
+                        const unsigned int prev = atomicCAS(&s_count, cur, cur + wtot);
+                        if (prev == cur) {
+                            base = cur;
+                            break;
+                        }
+                        cur = prev;
+                    }
+                }
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base == 0xffffffffu) break;  // buffer full: redo this chunk after the flush
+                const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if ((tk >> u) & 1u) {
+                        uint32_t ub = __float_as_uint(dist[u]);
+                        ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;
+                        cbuf[base + __popc(bal[u] & lt)] = ((uint64_t)ub << 32) | (pos0 + o + u * 32 + lane);
+                    }
+                    base += __popc(bal[u]);
+                }
+            }
+            done++;
+        }
+        __syncthreads();
+        n_seen += rlen * nwarps * CH;
+        const uint32_t cnt = s_count;
+        if (cnt > keep && cnt > cap / 2) {  // block-uniform
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_count = keep;
+                s_tau = T + 1;  // insert only keys <= T
+            }
+            __syncthreads();
+        }
+        const uint32_t free_slots = cap - s_count;
+        const uint64_t per_chunk_round = (uint64_t)nwarps * CH;
+        uint64_t rn = (s_tau == ~0ull) ? free_slots / per_chunk_round
+                                       : ((uint64_t)free_slots * n_seen) / (4ull * keep * per_chunk_round);
+        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > 32 ? 32ull : rn));
+    }
+    uint32_t n = s_count;
+    if (n > keep) {
+        block_select_keep(cbuf, n, keep, hist, s_misc);
+        n = keep;
+    }
+    __syncthreads();
+    for (uint32_t i = n + threadIdx.x; i < keep; i += blockDim.x) cbuf[i] = ~0ull;
+    __syncthreads();
+    bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
+    uint64_t* candq = a.cand + q * keep;
+    for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
+}
+
 }  // namespace dev
 
 template <int M, int R, int U>
@@ -402,34 +627,44 @@ static void launch_fast_u(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_
     CUDA_LAUNCH_CHECK();
 }
 
-// entry-slots per lane per chunk (4 by default; env VLQ_SCAN_U = 6 / 8 for studies)
-static int scan_u() {
-    static int u = [] {
-        const char* v = std::getenv("VLQ_SCAN_U");
-        const int x = v ? std::atoi(v) : 6;  // 6: best measured on deep100m
-        return (x == 4 || x == 8) ? x : 6;
-    }();
-    return u;
-}
-
 template <int M, int R>
-static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
-    if (R == 0 && scan_u() == 6) launch_fast_u<M, R, 6>(a, nq, w2, keep, st);
-    else if (R == 0 && scan_u() == 8) launch_fast_u<M, R, 8>(a, nq, w2, keep, st);
+static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
+    if (R == 0 && su == 6) launch_fast_u<M, R, 6>(a, nq, w2, keep, st);
+    else if (R == 0 && su == 8) launch_fast_u<M, R, 8>(a, nq, w2, keep, st);
     else launch_fast_u<M, R, 4>(a, nq, w2, keep, st);
 }
 
-bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, cudaStream_t st) {
-    // variant: 0 = default (single table: more CTAs/SM beat fewer bank
-    // conflicts on B200), 1 = generic warp-buffer scan (not
-    // here), 2 = fully replicated LUT, 3 = four copies, 4 = single table
+template <int M>
+static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
+    const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
+    const size_t smem = 4 * 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
+    auto fn = su == 4 ? dev::k_scan_fast2<M, 4> : (su == 8 ? dev::k_scan_fast2<M, 8> : dev::k_scan_fast2<M, 6>);
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
+    CUDA_LAUNCH_CHECK();
+}
+
+// su: entry-slots per lane per chunk (4 / 6 / 8; 6 default, measured best on deep100m)
+bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int su,
+                      cudaStream_t st) {
+    // variant: 0 = default (v6: packed-fp32 pairs, single-table LUT),
+    // 1 = generic warp-buffer scan (not here), 2 = fully replicated LUT (v5),
+    // 3 = four copies (v5), 4 = single table (v5)
     if (keep > 512 || w2 > 4096 || variant == 1) return false;
+    if (variant == 0) {
+        switch (a.m) {
+            case 16: launch_fast2<16>(a, nq, w2, keep, su, st); return true;
+            case 8: launch_fast2<8>(a, nq, w2, keep, su, st); return true;
+            case 4: launch_fast2<4>(a, nq, w2, keep, su, st); return true;
+            default: break;  // other m: the v5 path below (or the generic scan)
+        }
+    }
     const int r = variant == 2 ? 2 : (variant == 3 ? 1 : 0);  // default: single table (measured best)
 #define VLQ_FAST(MM)                                                  \
     do {                                                              \
-        if (r == 2) launch_fast_t<MM, 2>(a, nq, w2, keep, st);        \
-        else if (r == 1) launch_fast_t<MM, 1>(a, nq, w2, keep, st);   \
-        else launch_fast_t<MM, 0>(a, nq, w2, keep, st);               \
+        if (r == 2) launch_fast_t<MM, 2>(a, nq, w2, keep, su, st);        \
+        else if (r == 1) launch_fast_t<MM, 1>(a, nq, w2, keep, su, st);   \
+        else launch_fast_t<MM, 0>(a, nq, w2, keep, su, st);               \
         return true;                                                  \
     } while (0)
     switch (a.m) {

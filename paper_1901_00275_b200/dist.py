@@ -3,12 +3,21 @@ of one box (one process per GPU), coarse quantizer replicated, per-shard
 top-k merged by (dist, id) (the paper's "split the index into b parts, search
 locally, join").
 
-Each rank's engine holds regions i with i % world_size == rank.  A query batch
-is searched on every rank against its shard; the local exact top-k rows are
-exchanged with one NCCL all-gather and merged by the K9 kernel
-(vlq_merge_topk_device).  Because every shard returns its exact local top-k
-under the reference's total order, the merge is exactly the single-engine
-answer regardless of shard order.
+Each rank's engine holds regions i with i % world_size == rank.  Per batch:
+
+1. query-split coarse stage: rank r runs first_level_scan (the tensor-core
+   GEMM + exact refine, search.cpp:11-36) for its slice of the batch only;
+2. the slices' top-w1 region lists (nq x w1 u32, 2.5 MB at nq = 10k,
+   w1 = 64) are exchanged with one NCCL all-gather;
+3. every rank runs the rest of the search (second level, term5, fused scan,
+   exact re-score) for the whole batch on the cells it owns;
+4. the local exact top-k rows are all-gathered and merged by the K9 kernel
+   (vlq_merge_topk_device).
+
+Because every shard returns its exact local top-k under the reference's total
+order, the merge is exactly the single-engine answer regardless of shard
+order, and the coarse stage (the one step whose cost does not shrink with the
+shard) is divided by the GPU count instead of replicated.
 """
 from __future__ import annotations
 
@@ -48,6 +57,28 @@ def gather_parts(local_ids, local_dists, group=None):
     return gi.view((world,) + tuple(local_ids.shape)), gd.view((world,) + tuple(local_dists.shape))
 
 
+def query_slice(nq: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [lo, hi) of an nq-query batch whose coarse stage rank runs (equal
+    ceil-sized slices; the last ones may be short or empty)."""
+    per = (nq + world - 1) // world
+    lo = min(nq, rank * per)
+    return lo, min(nq, lo + per)
+
+
+def gather_top(local_top, nq: int, w1: int, group=None):
+    """All-gathers every rank's [slice, w1] top-w1 block into the [nq, w1]
+    table (slices padded to the common ceil size for the collective)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    per = (nq + world - 1) // world
+    send = torch.zeros((per, w1), dtype=local_top.dtype, device=local_top.device)
+    send[:local_top.shape[0]] = local_top
+    out = torch.empty((world * per, w1), dtype=local_top.dtype, device=local_top.device)
+    dist.all_gather_into_tensor(out, send, group=group)
+    return out[:nq]
+
+
 class ShardedIndex:
     """One rank's shard of a VLQ1 index plus the collective search."""
 
@@ -73,6 +104,32 @@ class ShardedIndex:
         st = torch.cuda.current_stream(dev).cuda_stream
         self.index.search_device(d_queries.data_ptr(), nq, w1, alpha, k, ids.data_ptr(), dists.data_ptr(),
                                  scanned.data_ptr(), st)
+        gi, gd = gather_parts(ids, dists, self.group)
+        mi, md = merge_topk(gi, gd, st)
+        return mi, md, scanned
+
+    def search_query_split(self, d_queries, w1: int, alpha: float, k: int, out=None):
+        """Query-split coarse stage + sharded fine stage (module docstring).
+        d_queries: the same CUDA float32 [nq, dim] batch on every rank.
+        Returns the merged (ids, dists) and the local scanned counts."""
+        import torch
+        import torch.distributed as dist
+        nq = d_queries.shape[0]
+        dev = d_queries.device
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        lo, hi = query_slice(nq, rank, world)
+        top_local = torch.empty((hi - lo, w1), dtype=torch.int32, device=dev)
+        if hi > lo:
+            self.index.search_coarse_device(d_queries[lo:hi].data_ptr(), hi - lo, w1, top_local.data_ptr(), st)
+        top = gather_top(top_local, nq, w1, self.group).contiguous()
+        if out is None:
+            out = (torch.empty((nq, k), dtype=torch.int64, device=dev),
+                   torch.empty((nq, k), dtype=torch.float32, device=dev),
+                   torch.empty((nq,), dtype=torch.int64, device=dev))
+        ids, dists, scanned = out
+        self.index.search_fine_device(d_queries.data_ptr(), nq, w1, alpha, k, top.data_ptr(), ids.data_ptr(),
+                                      dists.data_ptr(), scanned.data_ptr(), st)
         gi, gd = gather_parts(ids, dists, self.group)
         mi, md = merge_topk(gi, gd, st)
         return mi, md, scanned

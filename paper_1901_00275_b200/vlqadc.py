@@ -181,6 +181,29 @@ class Index:
                                                        ctypes.c_void_p(d_scanned) if d_scanned else None,
                                                        ctypes.c_void_p(stream) if stream else None))
 
+    def search_coarse_device(self, d_queries: int, nq: int, w1: int, d_top: int, stream: int | None = None) -> None:
+        """first_level_scan only (search.cpp:11-36): exact top-w1 region ids
+        (uint32 [nq, w1], (dist, id) order) into d_top.  Asynchronous."""
+        _lib.check(_lib.lib().vlq_engine_search_coarse_device(self._h, ctypes.c_void_p(d_queries), nq, w1,
+                                                              ctypes.c_void_p(d_top),
+                                                              ctypes.c_void_p(stream) if stream else None))
+
+    def search_fine_device(self, d_queries: int, nq: int, w1: int, alpha: float, k: int, d_top: int, d_ids: int,
+                           d_dists: int, d_scanned: int | None = None, stream: int | None = None) -> None:
+        """The rest of the search (search.cpp:38-167) on this shard from given
+        top-w1 lists.  search_coarse_device + search_fine_device ==
+        search_device.  Asynchronous."""
+        _lib.check(_lib.lib().vlq_engine_search_fine_device(self._h, ctypes.c_void_p(d_queries), nq, w1, alpha, k,
+                                                            ctypes.c_void_p(d_top), ctypes.c_void_p(d_ids),
+                                                            ctypes.c_void_p(d_dists),
+                                                            ctypes.c_void_p(d_scanned) if d_scanned else None,
+                                                            ctypes.c_void_p(stream) if stream else None))
+
+    def set_tuning(self, key: str, value: int) -> None:
+        """Study knobs (scan_variant, scan_slots, tc_search_min_k, force_exact);
+        results are identical for every setting."""
+        _lib.check(_lib.lib().vlq_engine_set_tuning(self._h, key.encode(), int(value)))
+
     def sync(self, stream: int | None = None) -> None:
         _lib.check(_lib.lib().vlq_engine_sync(self._h, ctypes.c_void_p(stream) if stream else None))
 

@@ -222,6 +222,48 @@ def test_sharded_engines_merge_to_the_single_engine_result(vlqadc):
         assert same_f32(got_d.cpu().numpy(), want_d)
 
 
+@pytest.mark.parametrize("tc", ["0", "1"])
+def test_query_split_staged_search_matches_single_engine(vlqadc, monkeypatch, tc):
+    """The multi-GPU schedule on one device: the coarse stage
+    (search_coarse_device) runs per query slice, the slices' top-w1 tables
+    are concatenated, every shard engine runs search_fine_device on the whole
+    batch, and the K9 merge equals the unsharded search bit-exactly (with the
+    tensor-core coarse stage forced on and off)."""
+    import torch
+    from paper_1901_00275_b200 import dist as vdist
+    monkeypatch.setenv("VLQ_TC_MIN_K", "0" if tc == "1" else "100000000")
+    z, index_path, _ = load_golden("accept_small")
+    full = vlqadc.Index.load(index_path)
+    G = 3
+    shards = [vlqadc.Index.load(index_path, shard_rank=r, shard_count=G) for r in range(G)]
+    q = torch.from_numpy(z["queries"]).cuda()
+    nq = q.shape[0]
+    st = torch.cuda.current_stream().cuda_stream
+    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100), (5, 1.0, 7)]:
+        want_ids, want_d = full.search(z["queries"], w1=w1, alpha=alpha, k=k)
+        tops = []
+        for r in range(G):
+            lo, hi = vdist.query_slice(nq, r, G)
+            t = torch.empty((hi - lo, w1), dtype=torch.int32, device="cuda")
+            if hi > lo:
+                shards[r].search_coarse_device(q[lo:hi].data_ptr(), hi - lo, w1, t.data_ptr(), st)
+            tops.append(t)
+        top = torch.cat(tops).contiguous()
+        pi, pd = [], []
+        for s in shards:
+            ids = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+            d = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+            s.search_fine_device(q.data_ptr(), nq, w1, alpha, k, top.data_ptr(), ids.data_ptr(), d.data_ptr(),
+                                 None, st)
+            pi.append(ids)
+            pd.append(d)
+        got_i, got_d = vdist.merge_topk(torch.stack(pi), torch.stack(pd))
+        for s in shards:
+            s.sync(st)
+        assert np.array_equal(got_i.cpu().numpy(), want_ids), (w1, alpha, k)
+        assert same_f32(got_d.cpu().numpy(), want_d), (w1, alpha, k)
+
+
 @pytest.mark.slow
 def test_acceptance_c7_trend_kats(vlqadc, tmp_path):
     """acceptance.cpp:330-363 on the reference's 'big' instance, built by the

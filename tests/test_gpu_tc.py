@@ -111,3 +111,21 @@ def test_tc_two_pass_coarse_filter_large_k(vlqadc, oracle_mod, tmp_path, monkeyp
         ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
         oids, od, _ = o.search(q, w1, alpha, k)
         assert np.array_equal(ids_, oids) and same_f32(d_, od), (w1, alpha, k)
+
+
+@pytest.mark.parametrize("dim", [96, 128])
+def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
+    """The C4 (D = 96, 3xTF32: hi + lo tiles) and C3/C5 (D = 128) shapes of
+    the two-pass coarse stage: the shared-memory ring depth is chosen to fit
+    227 KB, and the result stays bit-exact with the oracle."""
+    base = vlqadc.gen_synthetic(40000, dim, clusters=1500, spread=0.05, seed=25)
+    q = vlqadc.gen_synthetic(120, dim, clusters=1500, spread=0.05, seed=26)
+    idx = vlqadc.Index.train(base[:30000], k=4096, n=8, m=8, iters=2, seed=4)
+    idx.add(base)
+    path = str(tmp_path / f"d{dim}.vlq")
+    idx.save(path)
+    o = oracle_mod.OracleIndex.load(path)
+    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100)]:
+        ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
+        oids, od, _ = o.search(q, w1, alpha, k)
+        assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, w1, alpha, k)
