@@ -257,7 +257,10 @@ def main():
     dists = torch.empty((nq, k), dtype=torch.float32, device=q.device)
     scanned = torch.empty((nq,), dtype=torch.int64, device=q.device)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=q.device)
-    stream = torch.cuda.current_stream(q.device)
+    # one dedicated stream for the L2 flush, the events and every engine /
+    # NCCL launch, so the flush is ordered before each timed step
+    stream = torch.cuda.Stream(q.device)
+    torch.cuda.set_stream(stream)
     st = stream.cuda_stream
 
     sharded = ShardedIndex(idx) if world > 1 else None
@@ -274,6 +277,8 @@ def main():
         step()
     idx.sync(st)
     torch.cuda.synchronize()
+    # per-phase CUDA events ride along on the same stream (no host sync until
+    # stats() after the timed region)
     idx.set_profiling(True)
     idx.stats(reset=True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

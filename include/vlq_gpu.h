@@ -156,7 +156,8 @@ int vlq_engine_info(vlq_engine* e, vlq_info* out);
 int vlq_engine_get_model(vlq_engine* e, float* centroids, uint32_t* neighbor_ids, float* edge_sq_len, float* pq);
 
 /* Copies the (this shard's) posting lists back to the host:
- * list_off[k*n+1], ids[local_entries], codes[local_entries*m], lambdas[...]. */
+ * list_off[k*n+1], ids[local_entries], codes[local_entries*m], lambdas[...]; with
+ * ids, codes and lambdas all NULL only the offsets are copied. */
 int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8_t* codes, uint8_t* lambdas);
 
 /* Per-point add-path outputs without mutating the index: assign_point +

@@ -286,7 +286,7 @@ int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8
     ENGINE_OR_FAIL(e);
     return guarded([&] {
         vlq::HostLists L;
-        e->impl->get_lists(L);
+        e->impl->get_lists(L, !ids && !codes && !lambdas);
         if (list_off) std::memcpy(list_off, L.off.data(), L.off.size() * 8);
         if (ids) std::memcpy(ids, L.ids.data(), L.ids.size() * 4);
         if (codes) std::memcpy(codes, L.codes.data(), L.codes.size());

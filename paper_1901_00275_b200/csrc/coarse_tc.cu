@@ -20,7 +20,9 @@
 // the final answer: the refine kernels recompute exact reference-order
 // distances for every candidate within the TF32 error bound of the best and
 // certify that no other centroid can win (else an exact CUDA-core fallback).
+#include <algorithm>
 #include <cfloat>
+#include <stdexcept>
 
 #include "kernels.h"
 #include "select.cuh"
@@ -65,6 +67,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// bulk copy of any size: cp.async.bulk takes < 64 KB per instruction (a 64 KB
+// centroid tile at D = 128 must be split)
+__device__ __forceinline__ void bulk_g2s_any(unsigned char* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    const unsigned char* s = static_cast<const unsigned char*>(src);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+        bulk_g2s(dst + off, s + off, min(32768u, bytes - off), bar);
 }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -121,13 +131,21 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // MODE 3 = FILTER: per row, append every (approx, centroid) with approx <=
 //   tau[row] to the row's candidate list (top_d/top_idx, capacity cap,
 //   count in cnt[row]).
-template <int MODE, bool SPLIT, int TC_STAGES>
+// PERSIST (search modes 1-3): a persistent grid of one CTA per SM walks a
+// balanced contiguous range of (row block, centroid tile) units, so the
+// nq = 10k batch (79 row blocks) keeps all 148 SMs busy.  Rows come
+// pre-laid-out in the UMMA layout (Xtc / Xlo_tc, k_relayout_centroids); the
+// producer bulk-copies a row block's A tile whenever the range enters a new
+// one, after the MMA warp's commit on `aempty` shows the old A is consumed.
+template <int MODE, bool SPLIT, int TC_STAGES, bool PERSIST>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_coarse_tc(const float* __restrict__ X, uint64_t nx, uint32_t dim, const float* __restrict__ cent_tc,
                 const float* __restrict__ cent_lo, const float* __restrict__ cnorm_pad, uint32_t ntiles,
                 uint32_t kvalid, float* __restrict__ out_row, uint64_t ldo, uint32_t* __restrict__ top_idx,
-                float* __restrict__ top_d, const float* __restrict__ tau, uint32_t* __restrict__ cnt, uint32_t cap) {
+                float* __restrict__ top_d, const float* __restrict__ tau, uint32_t* __restrict__ cnt, uint32_t cap,
+                const float* __restrict__ Xtc, const float* __restrict__ Xlo_tc, uint32_t nrb) {
     extern __shared__ __align__(128) unsigned char smem[];
+    static_assert(!PERSIST || MODE != 0, "ARGMIN merges per row block: not persistent");
     constexpr int TN = SPLIT ? 64 : TC_N;  // centroids per tile (UMMA N)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t tile_bytes = TN * dim * 4;  // one centroid tile (one precision half)
@@ -141,23 +159,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t* empty = bars + TC_STAGES;      // [STAGES]
     uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]
     uint64_t* tempty = tfull + 2;            // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* afull = tempty + 2;            // A tile landed (PERSIST)
+    uint64_t* aempty = afull + 1;            // A tile consumed by every MMA (PERSIST)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
     float* sMerge = reinterpret_cast<float*>(tmem_slot + 4);  // ARGMIN: 128 x 4 d + 128 x 4 idx; STORE: 8 x 32 x 33 transpose
 
-    const uint64_t row0 = (uint64_t)blockIdx.x * TC_M;
-    // ---- A tile: row-major global -> interleaved K-major smem (all threads)
+    // unit u = rb * ntiles + t; this CTA's contiguous range [u0, u1)
+    uint64_t u0, u1;
+    if constexpr (PERSIST) {
+        const uint64_t U = (uint64_t)nrb * ntiles;
+        u0 = U * blockIdx.x / gridDim.x;
+        u1 = U * (blockIdx.x + 1) / gridDim.x;
+    } else {
+        u0 = (uint64_t)blockIdx.x * ntiles;
+        u1 = u0 + ntiles;
+    }
     const uint32_t nchunk = dim / 4;  // 16-byte chunks per row
-    for (uint32_t t = threadIdx.x; t < TC_M * nchunk; t += blockDim.x) {
-        const uint32_t r = t / nchunk, c = t % nchunk;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row0 + r < nx) v = __ldg(reinterpret_cast<const float4*>(X + (row0 + r) * dim) + c);
-        const uint32_t off = (r >> 3) * (nchunk * 128) + c * 128 + (r & 7) * 16;
-        if constexpr (SPLIT) {
-            const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
-            *reinterpret_cast<float4*>(sA + off) = hi;
-            *reinterpret_cast<float4*>(sAlo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
-        } else {
-            *reinterpret_cast<float4*>(sA + off) = v;
+    if constexpr (!PERSIST) {
+        // ---- A tile: row-major global -> interleaved K-major smem (all threads)
+        const uint64_t row0 = (uint64_t)blockIdx.x * TC_M;
+        for (uint32_t t = threadIdx.x; t < TC_M * nchunk; t += blockDim.x) {
+            const uint32_t r = t / nchunk, c = t % nchunk;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row0 + r < nx) v = __ldg(reinterpret_cast<const float4*>(X + (row0 + r) * dim) + c);
+            const uint32_t off = (r >> 3) * (nchunk * 128) + c * 128 + (r & 7) * 16;
+            if constexpr (SPLIT) {
+                const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+                *reinterpret_cast<float4*>(sA + off) = hi;
+                *reinterpret_cast<float4*>(sAlo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+            } else {
+                *reinterpret_cast<float4*>(sA + off) = v;
+            }
         }
     }
     if (warp == 0 && lane == 0) {
@@ -169,6 +201,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 8);
         }
+        mbar_init(afull, 1);
+        mbar_init(aempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // TMEM: two 128-column fp32 accumulators
@@ -182,15 +216,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- producer: centroid tiles -> smem ring
+        // ---------------- producer: (A tiles +) centroid tiles -> smem ring
         if (lane == 0) {
-            for (uint32_t t = 0; t < ntiles; t++) {
-                const uint32_t s = t % TC_STAGES, ph = (t / TC_STAGES) & 1u;
+            uint32_t cur_rb = 0xffffffffu, aloads = 0;
+            for (uint64_t u = u0; u < u1; u++) {
+                const uint32_t i = (uint32_t)(u - u0);
+                const uint32_t t = (uint32_t)(u % ntiles);
+                if constexpr (PERSIST) {
+                    const uint32_t rb = (uint32_t)(u / ntiles);
+                    if (rb != cur_rb) {
+                        if (aloads > 0) mbar_wait(aempty, (aloads - 1) & 1u);
+                        mbar_expect_tx(afull, NB * a_bytes);
+                        bulk_g2s_any(sA, Xtc + (size_t)rb * TC_M * dim, a_bytes, afull);
+                        if constexpr (SPLIT) bulk_g2s_any(sAlo, Xlo_tc + (size_t)rb * TC_M * dim, a_bytes, afull);
+                        cur_rb = rb;
+                        aloads++;
+                    }
+                }
+                const uint32_t s = i % TC_STAGES, ph = (i / TC_STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
                 mbar_expect_tx(&full[s], NB * tile_bytes);
-                bulk_g2s(sB + s * NB * tile_bytes, cent_tc + (size_t)t * TN * dim, tile_bytes, &full[s]);
+                bulk_g2s_any(sB + s * NB * tile_bytes, cent_tc + (size_t)t * TN * dim, tile_bytes, &full[s]);
                 if constexpr (SPLIT)
-                    bulk_g2s(sB + (s * NB + 1) * tile_bytes, cent_lo + (size_t)t * TN * dim, tile_bytes, &full[s]);
+                    bulk_g2s_any(sB + (s * NB + 1) * tile_bytes, cent_lo + (size_t)t * TN * dim, tile_bytes, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -199,9 +247,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                ((uint32_t)(TC_M >> 4) << 24);
         const uint32_t sbo = nchunk * 128, lbo = 128;
         const uint32_t a_addr = smem_u32(sA);
-        for (uint32_t t = 0; t < ntiles; t++) {
-            const uint32_t s = t % TC_STAGES, ph = (t / TC_STAGES) & 1u;
-            const uint32_t b = t & 1u, bph = (t >> 1) & 1u;
+        uint32_t cur_rb = 0xffffffffu, aloads = 0;
+        for (uint64_t u = u0; u < u1; u++) {
+            const uint32_t i = (uint32_t)(u - u0);
+            if constexpr (PERSIST) {
+                const uint32_t rb = (uint32_t)(u / ntiles);
+                if (rb != cur_rb) {
+                    if (aloads > 0 && lane == 0) umma_commit(aempty);  // fires when the old A's MMAs are done
+                    __syncwarp();
+                    mbar_wait(afull, aloads & 1u);
+                    cur_rb = rb;
+                    aloads++;
+                }
+            }
+            const uint32_t s = i % TC_STAGES, ph = (i / TC_STAGES) & 1u;
+            const uint32_t b = i & 1u, bph = (i >> 1) & 1u;
             mbar_wait(&tempty[b], bph ^ 1u);
             mbar_wait(&full[s], ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -228,26 +288,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t quad = warp & 3u;            // TMEM lanes 32*quad ..
         const uint32_t half = (warp - 2u) >> 2;     // column half 0/1
         const uint32_t r = quad * 32 + lane;        // row within the tile
-        const uint64_t grow = row0 + r;
-        const float tau_r = (MODE == 3 && grow < nx) ? tau[grow] : 0.0f;
         float bd[4] = {FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX};
         uint32_t bi[4] = {0, 0, 0, 0};
-        for (uint32_t t = 0; t < ntiles; t++) {
-            const uint32_t b = t & 1u, bph = (t >> 1) & 1u;
+        uint32_t cur_rb = 0xffffffffu;
+        uint64_t grow = 0, row0 = 0;
+        float tau_r = 0.0f;
+        for (uint64_t u = u0; u < u1; u++) {
+            const uint32_t i = (uint32_t)(u - u0);
+            const uint32_t t = (uint32_t)(u % ntiles);
+            const uint32_t rb = (uint32_t)(u / ntiles);
+            if (rb != cur_rb) {
+                cur_rb = rb;
+                row0 = (uint64_t)rb * TC_M;
+                grow = row0 + r;
+                tau_r = (MODE == 3 && grow < nx) ? tau[grow] : 0.0f;
+            }
+            const uint32_t b = i & 1u, bph = (i >> 1) & 1u;
             mbar_wait(&tfull[b], bph);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const float* nrm = cnorm_pad + (size_t)t * TN;  // warp-uniform broadcast loads
+            const float* nrm = cnorm_pad + (size_t)t * TN;
 #pragma unroll
             for (int h = 0; h < TN / 64; h++) {
                 uint32_t acc[32];
                 const uint32_t col = half * (TN / 2) + h * 32;
+                const float nv = __ldg(nrm + col + lane);  // one coalesced load, broadcast by shuffles
                 tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TN + col, acc);
                 float* tr = sMerge + (warp - 2) * 32 * 33;  // STORE: this warp's transpose tile
                 float cmin = __int_as_float(0x7f800000);
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     const uint32_t cidx = t * TN + col + j;
-                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), __ldg(nrm + col + j));
+                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), __shfl_sync(0xffffffffu, nv, j));
                     if constexpr (MODE == 0) {
                         if (d < bd[3]) {  // sorted insert, ties keep the lower index (earlier)
                             if (d < bd[2]) {
@@ -322,8 +393,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     }
-    // the producer's last stage refills were not consumed past ntiles; all
-    // MMAs completed (epilogue waited on every tfull)
+    // every MMA completed (the epilogue waited on every tfull); the producer's
+    // copies were all consumed
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -350,12 +421,12 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
             *reinterpret_cast<float4*>(out_lo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
         }
     }
-    for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < (uint64_t)ntiles * TC_N;
+    for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; norm_out && row < (uint64_t)ntiles * TC_N;
          row += (uint64_t)gridDim.x * blockDim.x) {
         float acc = 0.0f;
         if (row < k)
             for (uint32_t d = 0; d < dim; d++) acc = dot_step(acc, C[row * dim + d], C[row * dim + d]);
-        norm_out[row] = row < k ? acc : __int_as_float(0x7f800000);
+        if (norm_out) norm_out[row] = row < k ? acc : __int_as_float(0x7f800000);
     }
 }
 
@@ -364,7 +435,7 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
 static size_t coarse_tc_smem_at(uint32_t dim, int mode, bool split, uint32_t stages) {
     const size_t tail = mode == 1 ? (size_t)8 * 32 * 33 * 4 : (size_t)dev::TC_M * 8 * 4;
     const size_t tn = split ? 64 : dev::TC_N, nb = split ? 2 : 1;
-    return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * nb * tn * dim * 4 + 2 * stages * 8 + 4 * 8 + 16 +
+    return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * nb * tn * dim * 4 + 2 * stages * 8 + 6 * 8 + 16 +
            tail + 256;
 }
 
@@ -396,28 +467,56 @@ void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* 
 
 void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
                       const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,
-                      cudaStream_t st, const float* tau, uint32_t* cnt, uint32_t cap) {
+                      cudaStream_t st, const float* tau, uint32_t* cnt, uint32_t cap, const float* Xtc,
+                      const float* Xlo_tc) {
     if (nx == 0) return;
     const bool split = cent_lo != nullptr;
+    const bool persist = Xtc != nullptr && mode != 0;
     const uint32_t tn = split ? 64 : dev::TC_N;
     const uint32_t ntiles = (k + tn - 1) / tn;
     const uint32_t stages = coarse_tc_stages(dim, mode, split);
     if (stages == 0) throw std::runtime_error("coarse_tc: shared-memory ring does not fit for this dim");
+    if (persist && split && !Xlo_tc) throw std::runtime_error("coarse_tc: split rows need the lo half");
     const size_t smem = coarse_tc_smem_at(dim, mode, split, stages);
-    const unsigned grid = (unsigned)((nx + dev::TC_M - 1) / dev::TC_M);
-#define VLQ_TC_LAUNCH(MODE_, SPLIT_)                                                                            \
-    do {                                                                                                        \
-        auto fn = stages == 3 ? dev::k_coarse_tc<MODE_, SPLIT_, 3> : dev::k_coarse_tc<MODE_, SPLIT_, 2>;         \
-        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
-        fn<<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cent_lo, cnorm, ntiles, k, out_row, ldo,   \
-                                                top_idx, top_d, tau, cnt, cap);                                 \
+    const uint32_t nrb = (uint32_t)((nx + dev::TC_M - 1) / dev::TC_M);
+    unsigned grid = nrb;
+    if (persist) {
+        static int nsm = 0;
+        if (!nsm) {
+            int dev = 0;
+            CUDA_CHECK(cudaGetDevice(&dev));
+            CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        }
+        grid = (unsigned)std::min<uint64_t>((uint64_t)nsm, (uint64_t)nrb * ntiles);
+    }
+#define VLQ_TC_LAUNCH(MODE_, SPLIT_, PERSIST_)                                                                   \
+    do {                                                                                                         \
+        auto fn = stages == 3 ? dev::k_coarse_tc<MODE_, SPLIT_, 3, PERSIST_>                                     \
+                              : dev::k_coarse_tc<MODE_, SPLIT_, 2, PERSIST_>;                                    \
+        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));           \
+        fn<<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cent_lo, cnorm, ntiles, k, out_row, ldo,    \
+                                                top_idx, top_d, tau, cnt, cap, Xtc, Xlo_tc, nrb);                \
+    } while (0)
+#define VLQ_TC_MODE(MODE_)                                                         \
+    do {                                                                           \
+        if (persist) {                                                             \
+            if (split) VLQ_TC_LAUNCH(MODE_, true, true);                           \
+            else VLQ_TC_LAUNCH(MODE_, false, true);                                \
+        } else {                                                                   \
+            if (split) VLQ_TC_LAUNCH(MODE_, true, false);                          \
+            else VLQ_TC_LAUNCH(MODE_, false, false);                               \
+        }                                                                          \
     } while (0)
     switch (mode) {
-        case 0: if (split) VLQ_TC_LAUNCH(0, true); else VLQ_TC_LAUNCH(0, false); break;
-        case 1: if (split) VLQ_TC_LAUNCH(1, true); else VLQ_TC_LAUNCH(1, false); break;
-        case 2: if (split) VLQ_TC_LAUNCH(2, true); else VLQ_TC_LAUNCH(2, false); break;
-        default: if (split) VLQ_TC_LAUNCH(3, true); else VLQ_TC_LAUNCH(3, false); break;
+        case 0:
+            if (split) VLQ_TC_LAUNCH(0, true, false);
+            else VLQ_TC_LAUNCH(0, false, false);
+            break;
+        case 1: VLQ_TC_MODE(1); break;
+        case 2: VLQ_TC_MODE(2); break;
+        default: VLQ_TC_MODE(3); break;
     }
+#undef VLQ_TC_MODE
 #undef VLQ_TC_LAUNCH
     CUDA_LAUNCH_CHECK();
 }

@@ -65,6 +65,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_STORE_ROWS")) cfg_.tc_store_rows = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC_PERSIST")) cfg_.tc_persist = std::atoi(v);
     if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
         throw std::runtime_error("engine: invalid shard configuration");
     int ndev = 0;
@@ -77,8 +78,12 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
 }
 
 Engine::~Engine() {
-    for (auto& e : ev_)
-        if (e) cudaEventDestroy(e);
+    for (auto& sl : prof_) {
+        for (auto& e : sl.ev)
+            if (e) cudaEventDestroy(e);
+        if (sl.done) cudaEventDestroy(sl.done);
+        if (sl.counts) cudaFreeHost(sl.counts);
+    }
     if (stream_) {
         cudaSetDevice(cfg_.device);
         cudaStreamSynchronize(stream_);
@@ -440,15 +445,17 @@ void Engine::encode_host(const float* x, uint64_t nx, uint32_t* cells, float* la
     check_device_errors(st);
 }
 
-void Engine::get_lists(HostLists& out) {
+void Engine::get_lists(HostLists& out, bool offsets_only) {
     DeviceGuard g(cfg_.device);
     out.off.resize((size_t)k_ * n_ + 1);
-    out.ids.resize(nent_);
-    out.codes.resize(nent_ * m_);
-    out.lambdas.resize(nent_);
     out.base_count = base_count_;
     CUDA_CHECK(cudaMemcpyAsync(out.off.data(), list_off_.p, out.off.size() * 8, cudaMemcpyDeviceToHost, stream_));
-    if (nent_) {
+    if (!offsets_only) {
+        out.ids.resize(nent_);
+        out.codes.resize(nent_ * m_);
+        out.lambdas.resize(nent_);
+    }
+    if (nent_ && !offsets_only) {
         CUDA_CHECK(cudaMemcpyAsync(out.ids.data(), ids_.p, nent_ * 4, cudaMemcpyDeviceToHost, stream_));
         CUDA_CHECK(cudaMemcpyAsync(out.codes.data(), codes_.p, nent_ * m_, cudaMemcpyDeviceToHost, stream_));
         CUDA_CHECK(cudaMemcpyAsync(out.lambdas.data(), lambdas_.p, nent_, cudaMemcpyDeviceToHost, stream_));
@@ -528,9 +535,7 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
 void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                          float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
                          Stage stage, cudaStream_t st) {
-    auto mark = [&](int ph) {
-        if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
-    };
+    auto mark = [&](int ph) { mark_phase(ph, st); };
     uint64_t launches = 0;
     bool tc = false, fast = false;
     mark(PH_COARSE);
@@ -556,24 +561,16 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     stats_.launches += launches;
     stats_.tiles += 1;
     if (profiling_) {
-        CUDA_CHECK(cudaEventSynchronize(ev_[PH_COUNT]));
-        for (int p = 0; p < PH_COUNT; p++) {
-            float ms = 0.0f;
-            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[p], ev_[p + 1]));
-            stats_.phase_ms[p] += ms;
-        }
-        if (fast) {
-            unsigned int nflag = 0;
-            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaStreamSynchronize(st));
-            stats_.flagged += nflag;
-        }
-        if (tc) {
-            unsigned int nflag = 0;
-            CUDA_CHECK(cudaMemcpyAsync(&nflag, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaStreamSynchronize(st));
-            stats_.tc_refine_fallbacks += nflag;
-        }
+        // counters travel with the events; everything is read lazily in
+        // collect_profile(), so profiling never blocks the host mid-batch
+        ProfSlot& sl = prof_[prof_used_];
+        sl.fast = fast;
+        sl.tc = tc;
+        unsigned int* hv = sl.counts;
+        if (fast) CUDA_CHECK(cudaMemcpyAsync(hv, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
+        if (tc) CUDA_CHECK(cudaMemcpyAsync(hv + 1, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaEventRecord(sl.done, st));
+        prof_used_++;
     }
 }
 
@@ -581,9 +578,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
 // on the tensor-core path, exact ws_ entries for them and their neighbours).
 // Returns whether the tensor-core path ran.
 bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& launches, cudaStream_t st) {
-    auto mark = [&](int ph) {
-        if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
-    };
+    auto mark = [&](int ph) { mark_phase(ph, st); };
     const uint32_t L = std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2));
     const bool tc = tc_ && k_ >= cfg_.tc_search_min_k && L <= 2048 && w1 < k_ &&
                     exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
@@ -592,18 +587,33 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
     const uint32_t tn = tc_split_ ? 64 : 128;
     const uint32_t nchunk = ((k_ + tn - 1) / tn) * (tn / 32);
     const bool two_pass = tc && nchunk >= 2 * L && !cfg_.tc_store_rows;
+    // persistent coarse kernels (all SMs busy at any batch size): the query
+    // rows re-laid out once per tile in the UMMA layout (hi / lo halves)
+    const float* xtc = nullptr;
+    const float* xlo = nullptr;
+    if (tc && cfg_.tc_persist) {
+        const uint64_t rows = ((nt + 127) / 128) * 128;
+        xtc_.alloc(rows * dim_);
+        if (tc_split_) xlo_.alloc(rows * dim_);
+        launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc_.p, tc_split_ ? xlo_.p : nullptr, nullptr, st);
+        xtc = xtc_.p;
+        xlo = tc_split_ ? xlo_.p : nullptr;
+        launches += 1;
+    }
     if (two_pass) {
         // pass 1: chunk minima -> tau (upper bound of the L-th smallest);
         // pass 2: recompute, keep only approx <= tau (no K-wide row in HBM)
-        launch_coarse_tc(2, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr, st);
+        launch_coarse_tc(2, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr, st,
+                         nullptr, nullptr, 0, xtc, xlo);
         launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st);
         CUDA_CHECK(cudaMemsetAsync(lcnt_.p, 0, nt * 4, st));
         launch_coarse_tc(3, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, nullptr, 0, lidx_.p, ld_.p, st, tau_.p,
-                         lcnt_.p, kListCap);
+                         lcnt_.p, kListCap, xtc, xlo);
         launches += 3;
     } else if (tc) {
         // approximate rows on the tensor cores, then top-L on them
-        launch_coarse_tc(1, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st);
+        launch_coarse_tc(1, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, ws_.p, k_, nullptr, nullptr, st, nullptr,
+                         nullptr, 0, xtc, xlo);
         launches += 1;
     } else {
         launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
@@ -635,9 +645,7 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
 // (search.cpp:38-167) from top_ / ws_.  Returns whether the fast scan ran.
 bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                        float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st) {
-    auto mark = [&](int ph) {
-        if (profiling_) CUDA_CHECK(cudaEventRecord(ev_[ph], st));
-    };
+    auto mark = [&](int ph) { mark_phase(ph, st); };
     SearchArgs a = search_args();
     mark(PH_SECOND);
     launch_second_level(a, nt, w1, w2, st);
@@ -651,7 +659,20 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
         mark(PH_SCAN);
-        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, cfg_.scan_slots, st))
+        if (cfg_.scan_l2_budget_mb > 0 && cfg_.scan_variant == 0) {
+            // L2 retention: the batch's most re-read cells stay (evict_last),
+            // single-visit cells stream through (evict_first)
+            const uint32_t ncell = k_ * n_;
+            visits_.alloc(ncell);
+            vhist_.alloc(256);
+            hot_t_.alloc(1);
+            launch_cell_visits(sel_.p, nt * w2, visits_.p, ncell, list_off_.p, m_ + 5,
+                               (uint64_t)cfg_.scan_l2_budget_mb << 20, vhist_.p, hot_t_.p, st);
+            a.cell_visits = visits_.p;
+            a.hot_threshold = hot_t_.p;
+            launches += 3;
+        }
+        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, cfg_.scan_slots, cfg_.scan_prefetch, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
@@ -683,15 +704,60 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
+    else if (key == "scan_prefetch") cfg_.scan_prefetch = (int)value;
     else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;
     else if (key == "force_exact") cfg_.force_exact = (int)value;
+    else if (key == "tc_persist") cfg_.tc_persist = (int)value;
+    else if (key == "scan_l2_budget_mb") cfg_.scan_l2_budget_mb = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
+}
+
+// Per-tile phase events (profiling on): a pool of event sets, one per tile
+// searched since the last collection; no host synchronisation until
+// collect_profile().
+void Engine::mark_phase(int ph, cudaStream_t st) {
+    if (!profiling_) return;
+    if (prof_used_ == prof_.size()) {
+        prof_.emplace_back();
+        ProfSlot& sl = prof_.back();
+        for (auto& e : sl.ev) CUDA_CHECK(cudaEventCreate(&e));
+        CUDA_CHECK(cudaEventCreate(&sl.done));
+        CUDA_CHECK(cudaMallocHost(&sl.counts, 2 * sizeof(unsigned int)));
+    }
+    CUDA_CHECK(cudaEventRecord(prof_[prof_used_].ev[ph], st));
+}
+
+void Engine::collect_profile() {
+    if (prof_used_ == 0) return;
+    DeviceGuard g(cfg_.device);
+    for (size_t i = 0; i < prof_used_; i++) {
+        ProfSlot& sl = prof_[i];
+        CUDA_CHECK(cudaEventSynchronize(sl.done));
+        for (int p = 0; p < PH_COUNT; p++) {
+            float ms = 0.0f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, sl.ev[p], sl.ev[p + 1]));
+            stats_.phase_ms[p] += ms;
+        }
+        const unsigned int* hv = sl.counts;
+        if (sl.fast) stats_.flagged += hv[0];
+        if (sl.tc) stats_.tc_refine_fallbacks += hv[1];
+    }
+    prof_used_ = 0;
+}
+
+const EngineStats& Engine::stats() {
+    collect_profile();
+    return stats_;
+}
+
+void Engine::reset_stats() {
+    collect_profile();
+    stats_ = EngineStats();
 }
 
 void Engine::set_profiling(bool on) {
     DeviceGuard g(cfg_.device);
-    if (on && !ev_[0])
-        for (auto& e : ev_) CUDA_CHECK(cudaEventCreate(&e));
+    if (!on) collect_profile();
     profiling_ = on;
 }
 

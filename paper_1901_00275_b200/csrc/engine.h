@@ -28,10 +28,13 @@ struct EngineConfig {
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
     int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
+    int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
+    int scan_l2_budget_mb = 0;  // v6 scan: MB of the batch's most re-read cells loaded evict_last (0 = plain loads)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
     uint32_t tc_search_min_k = 16384; // search coarse stage on tensor cores for K >= this (env VLQ_TC_SEARCH_MIN_K)
     int tc_store_rows = 0;  // 1: materialise approximate rows + radix select instead of the two-pass filter
+    int tc_persist = 1;     // search coarse kernels as a persistent grid (one CTA per SM)
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -154,7 +157,7 @@ public:
     // per-point add-path outputs for parity tests (no index mutation)
     void encode_host(const float* x, uint64_t nx, uint32_t* cells, float* lambdas, uint8_t* codes,
                      uint8_t* lam_bytes);
-    void get_lists(HostLists& out);
+    void get_lists(HostLists& out, bool offsets_only = false);
     void get_tables(std::vector<float>& t2, std::vector<float>& t3);
 
     cudaStream_t stream() const { return stream_; }
@@ -171,8 +174,8 @@ public:
     void set_profiling(bool on);
     // study knobs (scan_variant, scan_slots, use_tc_search): take effect on the next search
     void set_tuning(const std::string& key, int64_t value);
-    const EngineStats& stats() const { return stats_; }
-    void reset_stats() { stats_ = EngineStats(); }
+    const EngineStats& stats();  // folds in the pending per-tile profile (syncs on its events)
+    void reset_stats();
 
 private:
     void upload_model();
@@ -194,13 +197,25 @@ private:
     EngineConfig cfg_;
     cudaStream_t stream_ = nullptr;
     bool profiling_ = false;
-    cudaEvent_t ev_[PH_COUNT + 1] = {};
+    struct ProfSlot {
+        cudaEvent_t ev[PH_COUNT + 1] = {};
+        cudaEvent_t done = nullptr;
+        unsigned int* counts = nullptr;  // pinned [2]: fast-scan flagged, tc refine fallbacks
+        bool fast = false, tc = false;
+    };
+    std::vector<ProfSlot> prof_;  // one per tile searched since the last collect_profile()
+    size_t prof_used_ = 0;
+    void mark_phase(int ph, cudaStream_t st);
+    void collect_profile();
     EngineStats stats_;
     void assign_chunk(const float* X, uint64_t nx, uint32_t* best, cudaStream_t st);
     DevBuf<uint32_t> tc_idx_, tc_flag_, tc_best_;
     DevBuf<float> tc_d_, tc_rows_;
     static constexpr uint32_t kListCap = 1024;  // per-query candidate list of the two-pass coarse filter
     DevBuf<float> tmin_, tau_, ld_;
+    DevBuf<float> xtc_, xlo_;  // query rows in the UMMA layout (persistent coarse kernels)
+    DevBuf<uint32_t> visits_, hot_t_;      // per-batch cell visit counts, L2-retention threshold
+    DevBuf<unsigned long long> vhist_;
     DevBuf<uint32_t> lcnt_, lidx_;
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;

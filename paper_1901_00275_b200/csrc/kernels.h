@@ -44,6 +44,11 @@ struct SearchArgs {
     unsigned int* error_flag;
     const float* Y;  // non-null: ws holds approximate (tensor-core) rows; second level
                      // recomputes neighbour distances exactly from the query vectors
+    // L2 retention (v6 scan): per-cell visit counts of the current batch and
+    // the threshold above which a cell's entries are loaded evict_last
+    // (re-read by other queries of the batch); null = plain loads
+    const uint32_t* cell_visits;
+    const uint32_t* hot_threshold;
 };
 
 // Add-path device views.
@@ -69,8 +74,13 @@ void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, flo
 size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);
 void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,
                  bool fast, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st);
+// per-batch cell visit counts and the L2-retention threshold (budget bytes of
+// the most re-read cells' entries kept evict_last)
+void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, uint32_t ncell, const uint64_t* list_off,
+                        uint32_t bytes_per_entry, uint64_t budget, unsigned long long* hist, uint32_t* threshold,
+                        cudaStream_t st);
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int slots,
-                      cudaStream_t st);
+                      int prefetch, cudaStream_t st);
 void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
                     cudaStream_t st);
 void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,
@@ -115,7 +125,8 @@ void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* 
                                cudaStream_t st);
 void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
                       const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,
-                      cudaStream_t st, const float* tau = nullptr, uint32_t* cnt = nullptr, uint32_t cap = 0);
+                      cudaStream_t st, const float* tau = nullptr, uint32_t* cnt = nullptr, uint32_t cap = 0,
+                      const float* Xtc = nullptr, const float* Xlo_tc = nullptr);
 void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
                      cudaStream_t st);
 void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, const uint32_t* cand,

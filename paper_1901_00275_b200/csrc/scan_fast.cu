@@ -389,6 +389,77 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 || U 
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
 }
 
+// L2-policy loads (ld.global.nc with an L2::cache_hint policy register)
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t pol;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <int M>
+__device__ __forceinline__ void load_code_vec_pol(const uint8_t* __restrict__ p, uint32_t (&w)[(M + 3) / 4],
+                                                  uint64_t pol) {
+    if constexpr (M == 16) {
+        asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "l"(p), "l"(pol));
+    } else if constexpr (M == 8) {
+        asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(w[0]), "=r"(w[1]) : "l"(p), "l"(pol));
+    } else if constexpr (M == 4) {
+        asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(w[0]) : "l"(p), "l"(pol));
+    } else {
+        load_code_vec<M>(p, w);
+    }
+}
+
+__device__ __forceinline__ uint32_t ld_u8_pol(const uint8_t* p, uint64_t pol) {
+    uint16_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ float ld_f32_pol(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Batch cell visit counts (how many queries of this batch scan each cell)
+__global__ void k_cell_visits(const uint32_t* __restrict__ sel, uint64_t nsel, uint32_t* __restrict__ visits) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nsel; t += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&visits[sel[t]], 1u);
+}
+
+// bytes of entries by visit count (capped at 255), re-read cells only
+__global__ void k_visit_bytes(const uint32_t* __restrict__ visits, uint32_t ncell, const uint64_t* __restrict__ off,
+                              uint32_t bpe, unsigned long long* __restrict__ hist) {
+    __shared__ unsigned long long h[256];
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        const uint32_t v = visits[c];
+        if (v >= 2) atomicAdd(&h[min(v, 255u)], (unsigned long long)(off[c + 1] - off[c]) * bpe);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// smallest visit count T >= 2 whose cells (visits >= T) fit the budget
+__global__ void k_pick_threshold(const unsigned long long* __restrict__ hist, uint64_t budget,
+                                 uint32_t* __restrict__ threshold) {
+    if (threadIdx.x != 0) return;
+    unsigned long long acc = 0;
+    uint32_t T = 0xffffffffu;
+    for (int v = 255; v >= 2; v--) {
+        acc += hist[v];
+        if (acc > budget) break;
+        T = (uint32_t)v;
+    }
+    *threshold = T;
+}
+
 // v6: the v5 schedule (balanced chunk ranges, block-shared candidate buffer,
 // adaptive rounds) with the per-entry arithmetic halved by the sm_100
 // packed fp32 pipe.  Entries are taken in pairs (slot u, u+1 of a lane):
@@ -409,8 +480,17 @@ __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an ord
     return __uint_as_float((ub & 0x80000000u) ? (ub & 0x7fffffffu) : ~ub);
 }
 
-template <int M, int U>
-__global__ void __launch_bounds__(256, 3) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
+// warp-cooperative L2 prefetch of [p, p + bytes): one 128-byte line per lane
+__device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes, uint32_t lane) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)127;
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(p) + bytes;
+    for (uintptr_t x = a0 + 128u * lane; x < a1; x += 128u * 32u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x));
+}
+
+template <int M, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap,
+                                                          uint32_t pf) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = (M + 3) / 4;
@@ -476,6 +556,10 @@ __global__ void __launch_bounds__(256, 3) k_scan_fast2(SearchArgs a, uint32_t w2
     const float* e_c = nullptr;
     float2 av2 = make_float2(0.f, 0.f), Bc2 = av2, cv2 = av2;
     uint32_t loaded_t = 0xffffffffu;
+    const bool hinted = a.cell_visits != nullptr;
+    const uint32_t hot_t = hinted ? *a.hot_threshold : 0xffffffffu;
+    const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
+    uint64_t pol = pol_stream;
 
     auto locate = [&](uint32_t g) {  // walks t forward to the cell holding chunk g
         while (cpref[t + 1] <= g) t++;
@@ -495,6 +579,7 @@ __global__ void __launch_bounds__(256, 3) k_scan_fast2(SearchArgs a, uint32_t w2
             codes_c = a.codes + b0 * M;
             lam_c = a.lambdas + b0;
             e_c = a.eterm + b0;
+            if (hinted) pol = a.cell_visits[cell] >= hot_t ? pol_keep : pol_stream;
         }
         return (g - cpref[t]) * CH;
     };
@@ -506,15 +591,30 @@ __global__ void __launch_bounds__(256, 3) k_scan_fast2(SearchArgs a, uint32_t w2
     while (__syncthreads_or(done < my_total)) {
         for (uint32_t r = 0; r < rlen && done < my_total; r++) {
             const uint32_t o = locate(c_lo + done);
+            if (pf) {  // L2 prefetch of the chunk pf ahead in this cell (off the critical path)
+                const uint32_t s0 = o + pf * CH;
+                if (s0 < L) {
+                    const uint32_t n0 = min(L - s0, CH);
+                    prefetch_l2_range(codes_c + (size_t)s0 * M, (size_t)n0 * M, lane);
+                    prefetch_l2_range(lam_c + s0, n0, lane);
+                    prefetch_l2_range(e_c + s0, (size_t)n0 * 4, lane);
+                }
+            }
             uint32_t cw[U][NW];
             uint32_t lb[U];
             float ev[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const uint32_t ic = min(o + u * 32 + lane, L - 1);  // clamped: the tail re-reads entry L-1
-                load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
-                lb[u] = __ldg(lam_c + ic);
-                ev[u] = __ldg(e_c + ic);
+                if (hinted) {
+                    load_code_vec_pol<M>(codes_c + (size_t)ic * M, cw[u], pol);
+                    lb[u] = ld_u8_pol(lam_c + ic, pol);
+                    ev[u] = ld_f32_pol(e_c + ic, pol);
+                } else {
+                    load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
+                    lb[u] = __ldg(lam_c + ic);
+                    ev[u] = __ldg(e_c + ic);
+                }
             }
             const uint64_t tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
             const float taud = tau == ~0ull ? __int_as_float(0x7f800000) : key_dist(tau);
@@ -634,18 +734,37 @@ static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_
     else launch_fast_u<M, R, 4>(a, nq, w2, keep, st);
 }
 
+void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, uint32_t ncell, const uint64_t* list_off,
+                        uint32_t bytes_per_entry, uint64_t budget, unsigned long long* hist, uint32_t* threshold,
+                        cudaStream_t st) {
+    CUDA_CHECK(cudaMemsetAsync(visits, 0, (size_t)ncell * 4, st));
+    CUDA_CHECK(cudaMemsetAsync(hist, 0, 256 * 8, st));
+    if (nsel) dev::k_cell_visits<<<(unsigned)dev::umin64((nsel + 255) / 256, 4736), 256, 0, st>>>(sel, nsel, visits);
+    dev::k_visit_bytes<<<(unsigned)dev::umin64(((uint64_t)ncell + 255) / 256, 1184), 256, 0, st>>>(
+        visits, ncell, list_off, bytes_per_entry, hist);
+    dev::k_pick_threshold<<<1, 32, 0, st>>>(hist, budget, threshold);
+    CUDA_LAUNCH_CHECK();
+}
+
 template <int M>
-static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
+static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, int pf,
+                         cudaStream_t st) {
     const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
     const size_t smem = 4 * 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
-    auto fn = su == 4 ? dev::k_scan_fast2<M, 4> : (su == 8 ? dev::k_scan_fast2<M, 8> : dev::k_scan_fast2<M, 6>);
+    // su: slots per lane (4/6/8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
+    auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
+              : su == 8 ? dev::k_scan_fast2<M, 8, 3>
+              : su == 104 ? dev::k_scan_fast2<M, 4, 4>
+              : su == 106 ? dev::k_scan_fast2<M, 6, 4>
+                          : dev::k_scan_fast2<M, 6, 3>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
+    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap, (uint32_t)pf);
     CUDA_LAUNCH_CHECK();
 }
 
 // su: entry-slots per lane per chunk (4 / 6 / 8; 6 default, measured best on deep100m)
-bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int su,
+// pf: L2 prefetch distance of the v6 scan in chunks (0 = off)
+bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int su, int pf,
                       cudaStream_t st) {
     // variant: 0 = default (v6: packed-fp32 pairs, single-table LUT),
     // 1 = generic warp-buffer scan (not here), 2 = fully replicated LUT (v5),
@@ -653,9 +772,9 @@ bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t ke
     if (keep > 512 || w2 > 4096 || variant == 1) return false;
     if (variant == 0) {
         switch (a.m) {
-            case 16: launch_fast2<16>(a, nq, w2, keep, su, st); return true;
-            case 8: launch_fast2<8>(a, nq, w2, keep, su, st); return true;
-            case 4: launch_fast2<4>(a, nq, w2, keep, su, st); return true;
+            case 16: launch_fast2<16>(a, nq, w2, keep, su, pf, st); return true;
+            case 8: launch_fast2<8>(a, nq, w2, keep, su, pf, st); return true;
+            case 4: launch_fast2<4>(a, nq, w2, keep, su, pf, st); return true;
             default: break;  // other m: the v5 path below (or the generic scan)
         }
     }

@@ -40,6 +40,18 @@ def _p(a: np.ndarray | None):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream (torch's default stream)
+
+
+def _stream(stream: int | None):
+    """None -> the engine's own stream; 0 (torch's default stream handle) ->
+    cudaStreamLegacy, so work stays ordered with torch's default stream;
+    anything else -> that cudaStream_t."""
+    if stream is None:
+        return None
+    return ctypes.c_void_p(CUDA_STREAM_LEGACY if stream == 0 else stream)
+
+
 def _to_vecset(arr) -> np.ndarray:
     """to_vecset + VectorSet::validate (bindings.cpp:23-31, vecset.cpp:8-20)."""
     a = np.ascontiguousarray(arr, dtype=np.float32)
@@ -179,14 +191,14 @@ class Index:
         _lib.check(_lib.lib().vlq_engine_search_device(self._h, ctypes.c_void_p(d_queries), nq, w1, alpha, k,
                                                        ctypes.c_void_p(d_ids), ctypes.c_void_p(d_dists),
                                                        ctypes.c_void_p(d_scanned) if d_scanned else None,
-                                                       ctypes.c_void_p(stream) if stream else None))
+                                                       _stream(stream)))
 
     def search_coarse_device(self, d_queries: int, nq: int, w1: int, d_top: int, stream: int | None = None) -> None:
         """first_level_scan only (search.cpp:11-36): exact top-w1 region ids
         (uint32 [nq, w1], (dist, id) order) into d_top.  Asynchronous."""
         _lib.check(_lib.lib().vlq_engine_search_coarse_device(self._h, ctypes.c_void_p(d_queries), nq, w1,
                                                               ctypes.c_void_p(d_top),
-                                                              ctypes.c_void_p(stream) if stream else None))
+                                                              _stream(stream)))
 
     def search_fine_device(self, d_queries: int, nq: int, w1: int, alpha: float, k: int, d_top: int, d_ids: int,
                            d_dists: int, d_scanned: int | None = None, stream: int | None = None) -> None:
@@ -197,7 +209,7 @@ class Index:
                                                             ctypes.c_void_p(d_top), ctypes.c_void_p(d_ids),
                                                             ctypes.c_void_p(d_dists),
                                                             ctypes.c_void_p(d_scanned) if d_scanned else None,
-                                                            ctypes.c_void_p(stream) if stream else None))
+                                                            _stream(stream)))
 
     def set_tuning(self, key: str, value: int) -> None:
         """Study knobs (scan_variant, scan_slots, tc_search_min_k, force_exact);
@@ -205,7 +217,7 @@ class Index:
         _lib.check(_lib.lib().vlq_engine_set_tuning(self._h, key.encode(), int(value)))
 
     def sync(self, stream: int | None = None) -> None:
-        _lib.check(_lib.lib().vlq_engine_sync(self._h, ctypes.c_void_p(stream) if stream else None))
+        _lib.check(_lib.lib().vlq_engine_sync(self._h, _stream(stream)))
 
     def add_synthetic(self, n: int, clusters: int = 200, spread: float = 0.05, seed: int = 42) -> None:
         """Streamed add of n rows of the device synthetic generator."""
@@ -246,6 +258,14 @@ class Index:
         _lib.check(_lib.lib().vlq_engine_get_model(self._h, _p(cent), _p(nbr), _p(elen), _p(pq)))
         return dict(dim=dim, k=k, n=n, m=m, clamp=bool(info.clamp_lambda), lo=float(info.lambda_lo),
                     hi=float(info.lambda_hi), centroids=cent, nbr=nbr, elen=elen, pq=pq)
+
+    def list_offsets(self) -> np.ndarray:
+        """This engine's list offsets u64[k*n+1] only (cell c holds entries
+        [off[c], off[c+1]))."""
+        info = self._info()
+        off = np.empty(info.k * info.n + 1, np.uint64)
+        _lib.check(_lib.lib().vlq_engine_get_lists(self._h, _p(off), None, None, None))
+        return off
 
     def lists(self):
         """This engine's posting lists: (list_off u64[k*n+1], ids u32, codes u8[.,m], lambdas u8)."""
@@ -294,7 +314,7 @@ def gen_synthetic_device(first: int, count: int, dim: int, clusters: int, spread
     """Rows [first, first+count) of the counter-based device generator."""
     _lib.check(_lib.lib().vlq_gen_synthetic_device(_default_device() if device is None else device, first, count,
                                                    dim, clusters, spread, seed, ctypes.c_void_p(d_out),
-                                                   ctypes.c_void_p(stream) if stream else None))
+                                                   _stream(stream)))
 
 
 def brute_force_gt_synthetic(nb: int, dim: int, clusters: int, spread: float, seed: int, queries, k: int, *,

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--configs", nargs="+", default=["scan_variant=0"])
+    ap.add_argument("--hubs", action="store_true", help="region-visit skew: bytes of the hottest regions vs reads")
     args = ap.parse_args()
     import torch
     from paper_1901_00275_b200 import vlqadc
@@ -41,6 +42,23 @@ def main():
     scanned = torch.empty((nq,), dtype=torch.int64, device=q.device)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=q.device)
     st = torch.cuda.current_stream().cuda_stream
+    if args.hubs:
+        top = torch.empty((nq, args.w1), dtype=torch.int32, device=q.device)
+        idx.search_coarse_device(q.data_ptr(), nq, args.w1, top.data_ptr(), st)
+        torch.cuda.synchronize()
+        visits = np.bincount(top.cpu().numpy().ravel().view(np.uint32), minlength=w["k"]).astype(np.float64)
+        off = idx.list_offsets().astype(np.int64)
+        nreg = w["k"]
+        rb = (off[np.arange(1, nreg + 1) * w["edges"]] - off[np.arange(nreg) * w["edges"]]) * (w["m"] + 5)
+        order = np.argsort(-visits, kind="stable")
+        cb = np.cumsum(rb[order])
+        cr = np.cumsum((visits * rb)[order])
+        out = {"regions_visited": int((visits > 0).sum()), "mean_visits": float(visits.mean()),
+               "max_visits": int(visits.max()), "region_reads_gb": float(cr[-1] / 1e9)}
+        for mb in (32, 64, 96, 128, 512, 2048):
+            j = int(np.searchsorted(cb, mb * 1e6))
+            out[f"reads_in_hottest_{mb}MB"] = round(float(cr[min(j, len(cr) - 1)] / cr[-1]), 4)
+        print(json.dumps({"hubs": out}), flush=True)
     ref = None
     for cfg in args.configs:
         for kv in cfg.split(","):

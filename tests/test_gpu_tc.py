@@ -125,7 +125,11 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
     path = str(tmp_path / f"d{dim}.vlq")
     idx.save(path)
     o = oracle_mod.OracleIndex.load(path)
-    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100)]:
-        ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
-        oids, od, _ = o.search(q, w1, alpha, k)
-        assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, w1, alpha, k)
+    # persistent / per-row-block coarse grids; plain vs L2-retention-hinted scan loads
+    for persist, l2mb in [(1, 0), (0, 0), (1, 1)]:
+        idx.set_tuning("tc_persist", persist)
+        idx.set_tuning("scan_l2_budget_mb", l2mb)
+        for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100)]:
+            ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
+            oids, od, _ = o.search(q, w1, alpha, k)
+            assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, persist, l2mb, w1, alpha, k)
