@@ -219,6 +219,8 @@ def main():
                     help="CPU baseline: the reference via a VLQ1 file (default up to 1e8 points) or the C oracle port")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of reference CPU work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ivf", action="store_true",
+                    help="also build and time the IVFADC comparison baseline (ivf_baseline.cpp) on the same model, w = w1")
     ap.add_argument("--profile", action="store_true",
                     help="wrap the timed steps in cudaProfilerStart/Stop (for ncu --profile-from-start off) and exit")
     args = ap.parse_args()
@@ -310,9 +312,13 @@ def main():
     ms_max = float(t_max.item())
     value = nq * args.steps / (ms_max / 1e3)
 
-    # algorithmic bytes of the dominant kernel (the fused list scan): S_q*(m+5)
+    # algorithmic bytes of the dominant kernel (the fused list scan): (m+5) per
+    # evaluated entry.  S_q (the reference's scanned count) minus the entries
+    # in cells the scan proved cannot qualify (cell lower bound, never read).
     local_scanned = int(scanned.sum().item())
-    scan_bytes_per_step = local_scanned * (w["m"] + 5)
+    pruned_per_step = stats["pruned"] / args.steps
+    evaluated = local_scanned - pruned_per_step
+    scan_bytes_per_step = int(evaluated * (w["m"] + 5))
     scan_ms = stats["phase_ms"]["scan"] / args.steps
     res_ids = out_ids.cpu().numpy()
     res_d = out_d.cpu().numpy()
@@ -334,6 +340,10 @@ def main():
                 "frac": round(achieved / hbm, 4) if achieved else None, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
                 "algorithmic_bytes_per_launch": scan_bytes_per_step,
+                "evaluated_entries_per_launch": int(evaluated),
+                "reference_scanned_entries_per_launch": local_scanned,
+                "reference_semantics_bytes_per_launch": local_scanned * (w["m"] + 5),
+                "pruned_fraction": round(pruned_per_step / max(local_scanned, 1), 4),
                 "bytes_per_candidate": w["m"] + 5, "scan_ms_per_launch": round(scan_ms, 4),
                 "phase_ms_per_step": {p: round(v / args.steps, 4) for p, v in stats["phase_ms"].items()},
                 "scan_share_of_step": round(scan_ms / (ms_max / args.steps), 4)}
@@ -387,6 +397,31 @@ def main():
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "kind": kind, "unavailable": f"{type(e).__name__}: {e}"}
 
+    ivf_line = None
+    if args.ivf and world == 1:
+        t0 = time.time()
+        ivf = vlqadc.build_ivf_baseline_synthetic(w["n"], idx, clusters=w["clusters"], spread=SPREAD, seed=BASE_SEED)
+        build_s = time.time() - t0
+        for _ in range(args.warmup):
+            ivf.search_device(q.data_ptr(), nq, args.w1, k, ids.data_ptr(), dists.data_ptr(), scanned.data_ptr(), st)
+        torch.cuda.synchronize()
+        ivf_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ivf.search_device(q.data_ptr(), nq, args.w1, k, ids.data_ptr(), dists.data_ptr(), scanned.data_ptr(), st)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ivf_ms += e0.elapsed_time(e1)
+        iv_ids = ids.cpu().numpy()
+        ivf_line = {"system": "ivfadc (ivf_baseline.cpp, exact GPU port)", "w": args.w1,
+                    "value": round(nq * args.steps / (ivf_ms / 1e3), 1), "unit": "queries/s",
+                    "ms_per_step": round(ivf_ms / args.steps, 3),
+                    "scanned_per_query": round(float(scanned.sum().item()) / nq, 1), "build_s": round(build_s, 1),
+                    "recall": {f"recall@{r}": round(recall_at(iv_ids[:ngt], gt, r), 4) for r in (1, 10, 100)
+                               if r <= k}}
+
     clk = clocks.summary()
     line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
@@ -394,6 +429,7 @@ def main():
             "data": "synthetic", "config": cfg, "recall": recall, "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
             "coarse_stage": "query-split (1/N of the batch per rank)" if world > 1 else "single GPU",
+            "ivfadc": ivf_line,
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
             "fallback_queries_per_step": stats["flagged"] / args.steps,
             "tc_coarse_fallbacks_per_step": stats["tc_fallbacks"] / args.steps}

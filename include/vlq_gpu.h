@@ -62,6 +62,7 @@ typedef struct {
     uint64_t tc_fallbacks;  /* tensor-core coarse rows / add points that needed the exact full scan */
     double phase_ms[8];     /* CUDA-event ms per phase (profiling on): coarse, first-level,
                                second-level, term5, scan, rescore, fallback, output */
+    uint64_t pruned;        /* posting entries the fast scan skipped by the cell lower bound (profiling on) */
 } vlq_stats;
 
 /* Thread-local message of the last failing call on this thread. */
@@ -136,6 +137,24 @@ int vlq_gen_synthetic_device(int device, uint64_t first, uint64_t count, uint32_
  * generator (ground truth at scale). */
 int vlq_brute_force_gt_synthetic(int device, uint64_t nb, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
                                  const float* queries, uint64_t nq, uint32_t k, uint32_t* out);
+
+/* IVFADC comparison baseline (proj/include/vlq/ivf_baseline.hpp), built
+ * with this engine's codebook and PQ as eval.cpp:182 does:
+ *  - build: build_ivf_baseline (proj/src/ivf_baseline.cpp:11-51) -- exact
+ *    assign_nearest, residual x - c, pq_encode, ordered appends; a host base
+ *    array or the device synthetic generator;
+ *  - search: search_ivf_baseline (ivf_baseline.cpp:53-126) -- exact top-w
+ *    regions, per-region residual LUT, exact (dist, id) top-k, -1/+inf
+ *    padded; out_scanned = SearchStats::scanned_candidates per query;
+ *  - get_lists: count of points and the region-major lists
+ *    (list_off[k+1], ids[count], codes[count*m]); any pointer may be NULL. */
+int vlq_engine_ivf_build(vlq_engine* e, const float* base, uint64_t n, uint32_t dim);
+int vlq_engine_ivf_build_synthetic(vlq_engine* e, uint64_t n, uint32_t clusters, float spread, uint64_t seed);
+int vlq_engine_ivf_search(vlq_engine* e, const float* queries, uint64_t nq, uint32_t dim, uint32_t w, uint32_t k,
+                          int64_t* out_ids, float* out_dists, uint64_t* out_scanned);
+int vlq_engine_ivf_search_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w, uint32_t k,
+                                 int64_t* d_ids, float* d_dists, uint64_t* d_scanned, void* stream);
+int vlq_engine_ivf_get_lists(vlq_engine* e, uint64_t* count, uint64_t* list_off, uint32_t* ids, uint8_t* codes);
 
 /* Study knobs, not part of the reference surface: "scan_variant" (0 = v6
  * packed-fp32 fast scan, 2/3/4 = v5 LUT layouts, 1 = generic scan),

@@ -143,6 +143,31 @@ class OracleIndex:
                                         _p(scanned), ctypes.c_int(threads)))
         return ids, dists, scanned
 
+    def ivf_build(self, base: np.ndarray):
+        """build_ivf_baseline (ivf_baseline.cpp:11-51) with this model's
+        codebook and PQ -> (list_off u64[k+1], ids u32[N], codes u8[N, m])."""
+        x = np.ascontiguousarray(base, np.float32)
+        nb = x.shape[0]
+        off = np.zeros(self.ix.k + 1, np.uint64)
+        ids = np.empty(nb, np.uint32)
+        codes = np.empty((nb, self.ix.m), np.uint8)
+        _check(lib().vo_ivf_build(ctypes.byref(self.s), _p(x), ctypes.c_uint64(nb), _p(off), _p(ids), _p(codes)))
+        return off, ids, codes
+
+    def ivf_search(self, lists, queries: np.ndarray, w: int, k: int, threads: int = 0):
+        """search_ivf_baseline (ivf_baseline.cpp:53-126) over `lists` (from
+        ivf_build) -> (ids int64[nq,k], dists float32[nq,k], scanned u64[nq])."""
+        off, ids_, codes = (np.ascontiguousarray(a) for a in lists)
+        q = np.ascontiguousarray(queries, np.float32)
+        nq = q.shape[0]
+        ids = np.empty((nq, k), np.int64)
+        dists = np.empty((nq, k), np.float32)
+        scanned = np.zeros(nq, np.uint64)
+        _check(lib().vo_ivf_search(ctypes.byref(self.s), _p(off), _p(ids_), _p(codes), _p(q), ctypes.c_uint64(nq),
+                                   ctypes.c_uint32(w), ctypes.c_uint32(k), _p(ids), _p(dists), _p(scanned),
+                                   ctypes.c_int(threads)))
+        return ids, dists, scanned
+
     def assign(self, base: np.ndarray, clamp: bool | None = None, threads: int = 0):
         """Per-point (cell, exact lambda, code, lambda byte) of the add path."""
         x = np.ascontiguousarray(base, np.float32)

@@ -23,6 +23,13 @@
 //
 //   ref_tools build <model.vlq> <base.fvecs> <out.vlq>
 //       Index.add replay (proj/python/bindings.cpp:83-97).
+//
+//   ref_tools ivf <model.vlq> <base.fvecs> <queries.fvecs> <w> <k> <out.bin>
+//       The IVFADC comparison baseline (proj/src/ivf_baseline.cpp):
+//       build_ivf_baseline with the model's codebook and PQ (as eval.cpp:182
+//       does), then search_ivf_baseline with SearchStats.  Writes u32 K, u32 m,
+//       per region: u32 len, len x u32 id, len*m code bytes; then the search
+//       results in the `search` format.
 
 #include <cstdio>
 #include <cstdlib>
@@ -35,6 +42,7 @@
 
 #include "vlq/dataset.hpp"
 #include "vlq/index.hpp"
+#include "vlq/ivf_baseline.hpp"
 #include "vlq/line_quant.hpp"
 #include "vlq/search.hpp"
 #include "vlq/vecs_io.hpp"
@@ -174,12 +182,48 @@ int cmd_build(int argc, char** argv) {
     return 0;
 }
 
+int cmd_ivf(int argc, char** argv) {
+    if (argc != 8) throw std::runtime_error("ivf: bad arguments");
+    InvertedIndex model = deserialize_index(argv[2]);
+    VectorSet base = read_vecs(argv[3], VecsKind::F32);
+    VectorSet queries = read_vecs(argv[4], VecsKind::F32);
+    uint32_t w = std::strtoul(argv[5], nullptr, 10);
+    uint32_t k = std::strtoul(argv[6], nullptr, 10);
+    IvfBaselineIndex ivf = build_ivf_baseline(base, model.codebook, model.pq);
+    SearchStats stats;
+    auto results = search_ivf_baseline(ivf, queries, w, k, &stats);
+    std::ofstream out(argv[7], std::ios::binary | std::ios::trunc);
+    uint32_t K = (uint32_t)ivf.ids.size(), m = ivf.pq.m;
+    out.write(reinterpret_cast<const char*>(&K), 4);
+    out.write(reinterpret_cast<const char*>(&m), 4);
+    for (uint32_t c = 0; c < K; c++) {
+        uint32_t len = (uint32_t)ivf.ids[c].size();
+        out.write(reinterpret_cast<const char*>(&len), 4);
+        out.write(reinterpret_cast<const char*>(ivf.ids[c].data()), (std::streamsize)len * 4);
+        out.write(reinterpret_cast<const char*>(ivf.codes[c].data()), (std::streamsize)len * m);
+    }
+    uint64_t nq = results.size();
+    uint64_t scanned = stats.scanned_candidates;
+    out.write(reinterpret_cast<const char*>(&nq), 8);
+    out.write(reinterpret_cast<const char*>(&k), 4);
+    out.write(reinterpret_cast<const char*>(&scanned), 8);
+    for (const auto& r : results) {
+        uint32_t c = (uint32_t)r.ids.size();
+        out.write(reinterpret_cast<const char*>(&c), 4);
+        for (uint32_t i = 0; i < c; i++) {
+            out.write(reinterpret_cast<const char*>(&r.ids[i]), 4);
+            out.write(reinterpret_cast<const char*>(&r.dists[i]), 4);
+        }
+    }
+    return out ? 0 : 2;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
         if (argc < 2) {
-            std::fprintf(stderr, "usage: ref_tools instance|search|scanstats|model|build ...\n");
+            std::fprintf(stderr, "usage: ref_tools instance|search|scanstats|model|build|ivf ...\n");
             return 1;
         }
         std::string cmd = argv[1];
@@ -188,6 +232,7 @@ int main(int argc, char** argv) {
         if (cmd == "scanstats") return cmd_scanstats(argc, argv);
         if (cmd == "model") return cmd_model(argc, argv);
         if (cmd == "build") return cmd_build(argc, argv);
+        if (cmd == "ivf") return cmd_ivf(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 1;
     } catch (const std::exception& e) {

@@ -162,5 +162,38 @@ def read_ref_search(path: str):
     return ids, dists, scanned
 
 
+def read_ref_ivf(path: str):
+    """Parses ref_tools' ivf output -> ((list_off u64[K+1], ids u32[N], codes u8[N, m]),
+    (ids int64[nq,k], dists f32[nq,k], scanned))."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    K, m = struct.unpack_from("<II", buf, 0)
+    pos = 8
+    off = np.zeros(K + 1, np.uint64)
+    ids, codes = [], []
+    for c in range(K):
+        (n,) = struct.unpack_from("<I", buf, pos)
+        pos += 4
+        ids.append(np.frombuffer(buf, "<u4", count=n, offset=pos).copy())
+        pos += 4 * n
+        codes.append(np.frombuffer(buf, np.uint8, count=n * m, offset=pos).reshape(n, m).copy())
+        pos += n * m
+        off[c + 1] = off[c] + n
+    lists = (off, np.concatenate(ids).astype(np.uint32) if K else np.zeros(0, np.uint32),
+             np.concatenate(codes) if K else np.zeros((0, m), np.uint8))
+    nq, k, scanned = struct.unpack_from("<QIQ", buf, pos)
+    pos += 20
+    rid = np.full((nq, k), -1, np.int64)
+    rd = np.full((nq, k), np.inf, np.float32)
+    for q in range(nq):
+        (c,) = struct.unpack_from("<I", buf, pos)
+        pos += 4
+        rec = np.frombuffer(buf, "<u4", count=2 * c, offset=pos).reshape(c, 2) if c else np.zeros((0, 2), "<u4")
+        pos += 8 * c
+        rid[q, :c] = rec[:, 0]
+        rd[q, :c] = rec[:, 1].view("<f4")
+    return lists, (rid, rd, scanned)
+
+
 def file_exists(path: str) -> bool:
     return os.path.isfile(path)

@@ -581,3 +581,156 @@ float vo_line_lambda_raw(float a, float b, float c) {
 }
 float vo_line_sqdist_raw(float a, float b, float c, float l) { return vo_line_sqdist(a, b, c, l); }
 float vo_sqdist_raw(const float* a, const float* b, uint32_t d) { return vo_sqdist(a, b, d); }
+
+/* ==== IVFADC comparison baseline: proj/src/ivf_baseline.cpp ==============
+ * Single-level index: K lists of (id, PQ code of x - c_i) with the VLQ
+ * model's codebook and PQ (eval.cpp:182).  Lists are returned flattened:
+ * list_off[K+1], ids[N] (ascending within a list: point order), codes[N*m]. */
+
+/* build_ivf_baseline (ivf_baseline.cpp:11-51): assign_nearest (strict '<',
+ * kmeans.cpp:21-33), residual x - c (fp32 sub), pq_encode (pq.cpp:52-67),
+ * then ordered appends.  Serial: the output is batch-independent. */
+int vo_ivf_build(const vo_index* ix, const float* base, uint64_t nb, uint64_t* list_off, uint32_t* ids,
+                 uint8_t* codes) {
+    const uint32_t k = ix->k, dim = ix->dim, m = ix->m, dsub = dim / m;
+    uint32_t* assign = (uint32_t*)malloc(sizeof(uint32_t) * (nb ? nb : 1));
+    uint8_t* code = (uint8_t*)malloc((size_t)(nb ? nb : 1) * m);
+    float* r = (float*)malloc(sizeof(float) * dim);
+    for (uint64_t i = 0; i < nb; i++) {
+        const float* x = base + i * dim;
+        uint32_t best = 0;
+        float best_d = FLT_MAX;
+        for (uint32_t c = 0; c < k; c++) {
+            float d = vo_sqdist(x, ix->centroids + (size_t)c * dim, dim);
+            if (d < best_d) {
+                best_d = d;
+                best = c;
+            }
+        }
+        assign[i] = best;
+        const float* ctr = ix->centroids + (size_t)best * dim;
+        for (uint32_t d = 0; d < dim; d++) r[d] = x[d] - ctr[d];
+        for (uint32_t p = 0; p < m; p++) {
+            uint32_t bj = 0;
+            float bd = FLT_MAX;
+            for (uint32_t j = 0; j < KSUB; j++) {
+                float d = vo_sqdist(r + (size_t)p * dsub, ix->pq + ((size_t)p * KSUB + j) * dsub, dsub);
+                if (d < bd) {
+                    bd = d;
+                    bj = j;
+                }
+            }
+            code[i * m + p] = (uint8_t)bj;
+        }
+    }
+    for (uint32_t c = 0; c <= k; c++) list_off[c] = 0;
+    for (uint64_t i = 0; i < nb; i++) list_off[assign[i] + 1]++;
+    for (uint32_t c = 0; c < k; c++) list_off[c + 1] += list_off[c];
+    uint64_t* fill = (uint64_t*)malloc(sizeof(uint64_t) * k);
+    for (uint32_t c = 0; c < k; c++) fill[c] = list_off[c];
+    for (uint64_t i = 0; i < nb; i++) {
+        uint64_t e = fill[assign[i]]++;
+        ids[e] = (uint32_t)i;
+        memcpy(codes + e * m, code + i * m, m);
+    }
+    free(fill);
+    free(r);
+    free(code);
+    free(assign);
+    return 0;
+}
+
+typedef struct {
+    const vo_index* ix;
+    const uint64_t* off;
+    const uint32_t* ids;
+    const uint8_t* codes;
+    const float* queries;
+    uint32_t w, topk;
+    int64_t* out_ids;
+    float* out_dists;
+    uint64_t* out_scanned;
+} ivf_ctx;
+
+typedef struct {
+    uint64_t* keys;  /* k */
+    float* resid;    /* dim */
+    float* lut;      /* m*256 */
+    uint64_t* cand;
+    size_t cand_cap;
+} ivf_scratch;
+
+static void* ivf_scratch_new(void* c) {
+    ivf_ctx* ctx = (ivf_ctx*)c;
+    ivf_scratch* s = (ivf_scratch*)calloc(1, sizeof(ivf_scratch));
+    s->keys = (uint64_t*)malloc(sizeof(uint64_t) * ctx->ix->k);
+    s->resid = (float*)malloc(sizeof(float) * ctx->ix->dim);
+    s->lut = (float*)malloc(sizeof(float) * ctx->ix->m * KSUB);
+    return s;
+}
+
+static void ivf_scratch_free(void* p) {
+    ivf_scratch* s = (ivf_scratch*)p;
+    free(s->keys);
+    free(s->resid);
+    free(s->lut);
+    free(s->cand);
+    free(s);
+}
+
+/* search_ivf_baseline (ivf_baseline.cpp:53-126) for one query */
+static int ivf_item(void* c, void* scratch, int64_t q) {
+    ivf_ctx* ctx = (ivf_ctx*)c;
+    ivf_scratch* s = (ivf_scratch*)scratch;
+    const vo_index* ix = ctx->ix;
+    const uint32_t k = ix->k, dim = ix->dim, m = ix->m, dsub = dim / m;
+    const float* y = ctx->queries + (size_t)q * dim;
+    for (uint32_t i = 0; i < k; i++) s->keys[i] = fkey(vo_sqdist(y, ix->centroids + (size_t)i * dim, dim), i);
+    select_smallest(s->keys, k, ctx->w);
+    size_t nc = 0;
+    for (uint32_t r = 0; r < ctx->w; r++) {
+        uint32_t region = (uint32_t)s->keys[r];
+        uint64_t b0 = ctx->off[region], b1 = ctx->off[region + 1];
+        if (b0 == b1) continue;
+        const float* ctr = ix->centroids + (size_t)region * dim;
+        for (uint32_t d = 0; d < dim; d++) s->resid[d] = y[d] - ctr[d];
+        for (uint32_t p = 0; p < m; p++)
+            for (uint32_t j = 0; j < KSUB; j++)
+                s->lut[(size_t)p * KSUB + j] =
+                    vo_sqdist(s->resid + (size_t)p * dsub, ix->pq + ((size_t)p * KSUB + j) * dsub, dsub);
+        if (nc + (b1 - b0) > s->cand_cap) {
+            size_t cap = s->cand_cap ? s->cand_cap : 1024;
+            while (cap < nc + (b1 - b0)) cap *= 2;
+            s->cand = (uint64_t*)realloc(s->cand, cap * sizeof(uint64_t));
+            s->cand_cap = cap;
+        }
+        for (uint64_t e = b0; e < b1; e++) {
+            float d = 0;
+            const uint8_t* code = ctx->codes + e * m;
+            for (uint32_t p = 0; p < m; p++) d += s->lut[(size_t)p * KSUB + code[p]];
+            s->cand[nc++] = fkey(d, ctx->ids[e]);
+        }
+    }
+    ctx->out_scanned[q] = nc;
+    select_smallest(s->cand, nc, ctx->topk);
+    for (uint32_t r = 0; r < ctx->topk; r++) {
+        int64_t* oi = ctx->out_ids + (size_t)q * ctx->topk;
+        float* od = ctx->out_dists + (size_t)q * ctx->topk;
+        if (r < nc) {
+            oi[r] = (int64_t)(uint32_t)s->cand[r];
+            od[r] = key_float(s->cand[r]);
+        } else {
+            oi[r] = -1;
+            od[r] = INFINITY;
+        }
+    }
+    return 0;
+}
+
+int vo_ivf_search(const vo_index* ix, const uint64_t* list_off, const uint32_t* ids, const uint8_t* codes,
+                  const float* queries, uint64_t nq, uint32_t w, uint32_t topk, int64_t* out_ids, float* out_dists,
+                  uint64_t* out_scanned, int nthreads) {
+    if (w == 0 || w > ix->k) return fail("search_ivf_baseline: need 0 < w <= k");
+    ivf_ctx ctx = {ix, list_off, ids, codes, queries, w, topk, out_ids, out_dists, out_scanned};
+    return par_for((int64_t)nq, 4, nthreads, &ctx, ivf_item, ivf_scratch_new, ivf_scratch_free);
+}

@@ -24,7 +24,7 @@ class VlqConfig(ctypes.Structure):
 
 class VlqStats(ctypes.Structure):
     _fields_ = [("launches", c_u64), ("tiles", c_u64), ("flagged", c_u64), ("tc_fallbacks", c_u64),
-                ("phase_ms", ctypes.c_double * 8)]
+                ("phase_ms", ctypes.c_double * 8), ("pruned", c_u64)]
 
 
 PHASES = ["coarse", "first_level", "second_level", "term5", "scan", "rescore", "fallback", "output"]
@@ -48,6 +48,11 @@ _SIGS = {
     "vlq_engine_search": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp]),
     "vlq_engine_search_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_set_tuning": (c_i32, [c_vp, ctypes.c_char_p, ctypes.c_int64]),
+    "vlq_engine_ivf_build": (c_i32, [c_vp, c_vp, c_u64, c_u32]),
+    "vlq_engine_ivf_build_synthetic": (c_i32, [c_vp, c_u64, c_u32, c_f32, c_u64]),
+    "vlq_engine_ivf_search": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_u32, c_vp, c_vp, c_vp]),
+    "vlq_engine_ivf_search_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp]),
+    "vlq_engine_ivf_get_lists": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_search_coarse_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_vp, c_vp]),
     "vlq_engine_search_fine_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_sync": (c_i32, [c_vp, c_vp]),

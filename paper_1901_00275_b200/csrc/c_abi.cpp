@@ -186,6 +186,58 @@ int vlq_engine_set_tuning(vlq_engine* e, const char* key, int64_t value) {
     return guarded([&] { e->impl->set_tuning(key, value); });
 }
 
+// ---- IVFADC comparison baseline (proj/src/ivf_baseline.cpp) ----------------
+int vlq_engine_ivf_build(vlq_engine* e, const float* base, uint64_t n, uint32_t dim) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!e->impl->has_model()) throw std::runtime_error("build_ivf_baseline: no model loaded");
+        if (dim != e->impl->dim()) throw std::runtime_error("build_ivf_baseline: dimension mismatch");
+        if (n && !base) throw std::runtime_error("build_ivf_baseline: base is NULL");
+        e->impl->ivf_build_host(base, n);
+    });
+}
+
+int vlq_engine_ivf_build_synthetic(vlq_engine* e, uint64_t n, uint32_t clusters, float spread, uint64_t seed) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!e->impl->has_model()) throw std::runtime_error("build_ivf_baseline: no model loaded");
+        if (clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
+        if (!(spread > 0)) throw std::runtime_error("gen_synthetic: spread must be positive");
+        const uint32_t dim = e->impl->dim();
+        const uint64_t chunk = std::max<uint64_t>(1, (512ull << 20) / (4ull * dim));
+        e->impl->ivf_build_stream(n, chunk, [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+            vlq::launch_synth(first, count, dim, clusters, spread, seed, dst, st);
+        });
+    });
+}
+
+int vlq_engine_ivf_search(vlq_engine* e, const float* queries, uint64_t nq, uint32_t dim, uint32_t w, uint32_t k,
+                          int64_t* out_ids, float* out_dists, uint64_t* out_scanned) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (dim != e->impl->dim()) throw std::runtime_error("search_ivf_baseline: dimension mismatch");
+        if (nq && (!queries || (k && (!out_ids || !out_dists)))) throw std::runtime_error("search: NULL buffer");
+        e->impl->ivf_search_host(queries, nq, w, k, out_ids, out_dists, out_scanned);
+    });
+}
+
+int vlq_engine_ivf_search_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w, uint32_t k,
+                                 int64_t* d_ids, float* d_dists, uint64_t* d_scanned, void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        e->impl->ivf_search_device(d_queries, nq, w, k, d_ids, d_dists, d_scanned,
+                                   stream ? (cudaStream_t)stream : e->impl->stream());
+    });
+}
+
+int vlq_engine_ivf_get_lists(vlq_engine* e, uint64_t* count, uint64_t* list_off, uint32_t* ids, uint8_t* codes) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (count) *count = e->impl->ivf_built() ? e->impl->ivf_count() : 0;
+        if (list_off || ids || codes) e->impl->ivf_get_lists(list_off, ids, codes);
+    });
+}
+
 int vlq_engine_sync(vlq_engine* e, void* stream) {
     ENGINE_OR_FAIL(e);
     return guarded([&] { e->impl->check_device_errors(stream ? (cudaStream_t)stream : e->impl->stream()); });
@@ -246,6 +298,7 @@ int vlq_engine_get_stats(vlq_engine* e, vlq_stats* out) {
     out->flagged = s.flagged;
     out->tc_fallbacks = s.tc_refine_fallbacks;
     for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
+    out->pruned = s.pruned;
     return VLQ_OK;
 }
 

@@ -23,18 +23,6 @@ uint32_t next_pow2(uint32_t v) {
     return p;
 }
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        CUDA_CHECK(cudaGetDevice(&prev));
-        if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() {
-        int cur;
-        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
-    }
-};
-
 template <typename T>
 void h2d(DevBuf<T>& dst, const std::vector<T>& src, cudaStream_t st) {
     dst.alloc(std::max<size_t>(src.size(), 1));
@@ -61,6 +49,7 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_SCAN_PRUNE")) cfg_.scan_prune = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -258,6 +247,15 @@ void Engine::compute_eterm() {
     CUDA_CHECK(cudaMemcpyAsync(&bits, err_.p + 1, 4, cudaMemcpyDeviceToHost, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     std::memcpy(&emax_, &bits, 4);
+    compute_cell_emin();
+}
+
+void Engine::compute_cell_emin() {
+    DeviceGuard g(cfg_.device);
+    const uint32_t ncell = k_ * n_;
+    emin_.alloc(std::max<uint32_t>(ncell, 1));
+    launch_cell_emin(list_off_.p, ncell, eterm_.p, emin_.p, stream_);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
 void Engine::check_device_errors(cudaStream_t st) {
@@ -415,6 +413,7 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
     }
     std::memcpy(&emax_, &flags[1], 4);
     nent_ = nloc;
+    compute_cell_emin();
     base_count_ = nb;
 }
 
@@ -567,7 +566,13 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         sl.fast = fast;
         sl.tc = tc;
         unsigned int* hv = sl.counts;
-        if (fast) CUDA_CHECK(cudaMemcpyAsync(hv, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
+        if (fast) {
+            CUDA_CHECK(cudaMemcpyAsync(hv, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
+            prun_acc_.alloc(1);
+            CUDA_CHECK(cudaMemsetAsync(prun_acc_.p, 0, 8, st));
+            launch_sum_pruned(meta_.p, nt, prun_acc_.p, st);
+            CUDA_CHECK(cudaMemcpyAsync(hv + 2, prun_acc_.p, 8, cudaMemcpyDeviceToHost, st));
+        }
         if (tc) CUDA_CHECK(cudaMemcpyAsync(hv + 1, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaEventRecord(sl.done, st));
         prof_used_++;
@@ -659,6 +664,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
         mark(PH_SCAN);
+        if (cfg_.scan_prune && emin_.p) a.cell_emin = emin_.p;
         if (cfg_.scan_l2_budget_mb > 0 && cfg_.scan_variant == 0) {
             // L2 retention: the batch's most re-read cells stay (evict_last),
             // single-visit cells stream through (evict_first)
@@ -709,21 +715,26 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "force_exact") cfg_.force_exact = (int)value;
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;
     else if (key == "scan_l2_budget_mb") cfg_.scan_l2_budget_mb = (int)value;
+    else if (key == "scan_prune") cfg_.scan_prune = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 
 // Per-tile phase events (profiling on): a pool of event sets, one per tile
 // searched since the last collection; no host synchronisation until
 // collect_profile().
-void Engine::mark_phase(int ph, cudaStream_t st) {
-    if (!profiling_) return;
-    if (prof_used_ == prof_.size()) {
+void Engine::grow_profile(size_t slots) {
+    while (prof_.size() < slots) {
         prof_.emplace_back();
         ProfSlot& sl = prof_.back();
         for (auto& e : sl.ev) CUDA_CHECK(cudaEventCreate(&e));
         CUDA_CHECK(cudaEventCreate(&sl.done));
-        CUDA_CHECK(cudaMallocHost(&sl.counts, 2 * sizeof(unsigned int)));
+        CUDA_CHECK(cudaMallocHost(&sl.counts, 4 * sizeof(unsigned int)));
     }
+}
+
+void Engine::mark_phase(int ph, cudaStream_t st) {
+    if (!profiling_) return;
+    if (prof_used_ == prof_.size()) grow_profile(2 * prof_.size() + 16);  // slots are pre-made by set_profiling
     CUDA_CHECK(cudaEventRecord(prof_[prof_used_].ev[ph], st));
 }
 
@@ -739,7 +750,10 @@ void Engine::collect_profile() {
             stats_.phase_ms[p] += ms;
         }
         const unsigned int* hv = sl.counts;
-        if (sl.fast) stats_.flagged += hv[0];
+        if (sl.fast) {
+            stats_.flagged += hv[0];
+            stats_.pruned += (uint64_t)hv[2] | ((uint64_t)hv[3] << 32);
+        }
         if (sl.tc) stats_.tc_refine_fallbacks += hv[1];
     }
     prof_used_ = 0;
@@ -758,6 +772,9 @@ void Engine::reset_stats() {
 void Engine::set_profiling(bool on) {
     DeviceGuard g(cfg_.device);
     if (!on) collect_profile();
+    // event sets and pinned counters are created here, never inside a timed
+    // batch (cudaMallocHost synchronises the device)
+    if (on) grow_profile(64);
     profiling_ = on;
 }
 

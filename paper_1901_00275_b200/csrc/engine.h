@@ -30,6 +30,7 @@ struct EngineConfig {
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
     int scan_l2_budget_mb = 0;  // v6 scan: MB of the batch's most re-read cells loaded evict_last (0 = plain loads)
+    int scan_prune = 1;    // v6 scan: skip cells whose distance lower bound exceeds the block threshold
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
     uint32_t tc_search_min_k = 16384; // search coarse stage on tensor cores for K >= this (env VLQ_TC_SEARCH_MIN_K)
@@ -55,6 +56,19 @@ struct HostLists {
     std::vector<uint8_t> codes;
     std::vector<uint8_t> lambdas;
     uint64_t base_count = 0;
+};
+
+// sets the current device for a scope, restoring the caller's on exit
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CUDA_CHECK(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
 };
 
 // grow-only pinned host buffer (staging for the host-pointer API)
@@ -109,6 +123,7 @@ struct EngineStats {
     uint64_t tiles = 0;
     uint64_t flagged = 0;       // queries that took the exact fallback
     double phase_ms[PH_COUNT] = {0};  // CUDA-event time per phase (profiling on)
+    uint64_t pruned = 0;        // posting entries the fast scan never read (cell lower bound; profiling on)
 };
 
 class Engine {
@@ -171,6 +186,18 @@ public:
     static void brute_force_gt_source(int device, const BaseSource& src, uint64_t nb, const float* queries,
                                       uint64_t nq, uint32_t dim, uint32_t k, uint32_t* out);
 
+    // IVFADC comparison baseline (proj/src/ivf_baseline.cpp, ivf.cu) with this
+    // engine's codebook and PQ: build_ivf_baseline / search_ivf_baseline
+    void ivf_build_host(const float* base, uint64_t nb);
+    void ivf_build_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src);
+    void ivf_search_device(const float* d_q, uint64_t nq, uint32_t w, uint32_t topk, int64_t* d_ids, float* d_dists,
+                           uint64_t* d_scanned, cudaStream_t st);
+    void ivf_search_host(const float* q, uint64_t nq, uint32_t w, uint32_t topk, int64_t* ids, float* dists,
+                         uint64_t* scanned);
+    void ivf_get_lists(uint64_t* off, uint32_t* ids, uint8_t* codes);
+    bool ivf_built() const { return ivf_ok_; }
+    uint64_t ivf_count() const { return ivf_n_; }
+
     void set_profiling(bool on);
     // study knobs (scan_variant, scan_slots, use_tc_search): take effect on the next search
     void set_tuning(const std::string& key, int64_t value);
@@ -181,6 +208,7 @@ private:
     void upload_model();
     void upload_lists(const HostLists& L);
     void compute_eterm();
+    void compute_cell_emin();
     AddArgs add_args() const;
     SearchArgs search_args() const;
     enum Stage { STAGE_ALL = 0, STAGE_COARSE = 1, STAGE_FINE = 2 };
@@ -200,12 +228,13 @@ private:
     struct ProfSlot {
         cudaEvent_t ev[PH_COUNT + 1] = {};
         cudaEvent_t done = nullptr;
-        unsigned int* counts = nullptr;  // pinned [2]: fast-scan flagged, tc refine fallbacks
+        unsigned int* counts = nullptr;  // pinned [4]: fast-scan flagged, tc refine fallbacks, u64 pruned entries
         bool fast = false, tc = false;
     };
     std::vector<ProfSlot> prof_;  // one per tile searched since the last collect_profile()
     size_t prof_used_ = 0;
     void mark_phase(int ph, cudaStream_t st);
+    void grow_profile(size_t slots);
     void collect_profile();
     EngineStats stats_;
     void assign_chunk(const float* X, uint64_t nx, uint32_t* best, cudaStream_t st);
@@ -236,7 +265,16 @@ private:
     DevBuf<uint8_t> codes_, lambdas_;
     DevBuf<uint32_t> ids_;
     DevBuf<float> eterm_;
+    DevBuf<float> emin_;  // per-cell min e-term (cell-level pruning bound)
+    DevBuf<unsigned long long> prun_acc_;  // per-tile pruned-entry total (profiling)
     DevBuf<unsigned int> err_;  // [0] error flag, [1] emax bits, [2] flagged count, [3..4] minmax
+
+    // IVFADC baseline lists (region-major; ids ascending within a list)
+    DevBuf<uint64_t> ivf_off_;
+    DevBuf<uint32_t> ivf_ids_;
+    DevBuf<uint8_t> ivf_codes_;
+    uint64_t ivf_n_ = 0;
+    bool ivf_ok_ = false;
 
     // host-pointer search staging (search_host)
     DevBuf<float> sq_, sd_;

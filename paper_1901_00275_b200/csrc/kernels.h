@@ -13,7 +13,7 @@ struct QueryMeta {
     float dmax;                  // bound on |term1| over the query's selected cells
     float s5max;                 // bound on |sum5|
     uint32_t flag;               // 1: certificate failed -> exact fallback
-    uint32_t pad;
+    uint32_t pruned;             // entries the fast scan skipped by the cell lower bound (never read)
 };
 
 // Device views used by the search kernels (all pointers device-resident).
@@ -49,6 +49,8 @@ struct SearchArgs {
     // (re-read by other queries of the batch); null = plain loads
     const uint32_t* cell_visits;
     const uint32_t* hot_threshold;
+    // cell-level pruning (v6 scan): min e-term of every cell's entries; null = off
+    const float* cell_emin;
 };
 
 // Add-path device views.
@@ -79,6 +81,8 @@ void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t ke
 void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, uint32_t ncell, const uint64_t* list_off,
                         uint32_t bytes_per_entry, uint64_t budget, unsigned long long* hist, uint32_t* threshold,
                         cudaStream_t st);
+// emin[c] = min of eterm over cell c's entries (+inf for an empty cell)
+void launch_cell_emin(const uint64_t* list_off, uint32_t ncell, const float* eterm, float* emin, cudaStream_t st);
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int slots,
                       int prefetch, cudaStream_t st);
 void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
@@ -106,6 +110,7 @@ void launch_histogram(const uint32_t* cells, uint64_t n, unsigned long long* cou
 namespace vlq {
 void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st);
 void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st);
+void launch_sum_pruned(const QueryMeta* meta, uint64_t nq, unsigned long long* out, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 void launch_synth(uint64_t first, uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
                   float* out, cudaStream_t st);

@@ -460,6 +460,20 @@ __global__ void k_pick_threshold(const unsigned long long* __restrict__ hist, ui
     *threshold = T;
 }
 
+// emin[c] = min over cell c's e-terms (warp per cell)
+__global__ void k_cell_emin(const uint64_t* __restrict__ off, uint32_t ncell, const float* __restrict__ eterm,
+                            float* __restrict__ emin) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < ncell;
+         c += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint64_t b0 = off[c], b1 = off[c + 1];
+        float mn = __int_as_float(0x7f800000);
+        for (uint64_t e = b0 + lane; e < b1; e += 32) mn = fminf(mn, eterm[e]);
+        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if (lane == 0) emin[c] = mn;
+    }
+}
+
 // v6: the v5 schedule (balanced chunk ranges, block-shared candidate buffer,
 // adaptive rounds) with the per-entry arithmetic halved by the sm_100
 // packed fp32 pipe.  Entries are taken in pairs (slot u, u+1 of a lane):
@@ -505,6 +519,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     __shared__ unsigned int s_misc[48];
     __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
+    __shared__ unsigned int s_pruned;
 
     // 1. the query's term5 table (one copy per sub-space)
     const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
@@ -531,6 +546,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             cpref[w2] = total;
             s_count = 0;
             s_tau = ~0ull;
+            s_pruned = 0;
         }
     }
     __syncthreads();
@@ -556,6 +572,15 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     const float* e_c = nullptr;
     float2 av2 = make_float2(0.f, 0.f), Bc2 = av2, cv2 = av2;
     uint32_t loaded_t = 0xffffffffu;
+    // Cell-level pruning: every entry of a cell has fast distance >=
+    //   LB = min_lambda term1(lambda) + emin_cell - 2 S5max_q
+    // (term1 is convex in lambda: c > 0; sum5 <= S5max_q = sum_p max_j |t5|);
+    // once the block threshold is below LB minus a rounding margin, no entry
+    // of the cell can enter the top-k' and its bytes are never read.
+    const bool prune = a.cell_emin != nullptr;
+    const float s5max2 = 2.0f * a.meta[q].s5max;
+    const float lam_lo = a.lam0, lam_hi = fmaf(255.0f, a.lam_delta, a.lam0);
+    float cell_lb = -__int_as_float(0x7f800000);
     const bool hinted = a.cell_visits != nullptr;
     const uint32_t hot_t = hinted ? *a.hot_threshold : 0xffffffffu;
     const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
@@ -580,6 +605,17 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             lam_c = a.lambdas + b0;
             e_c = a.eterm + b0;
             if (hinted) pol = a.cell_visits[cell] >= hot_t ? pol_keep : pol_stream;
+            if (prune) {
+                const float Bv = (bv - av) - cv;
+                cell_lb = -__int_as_float(0x7f800000);
+                if (cv > 0.0f) {
+                    const float ls = fminf(fmaxf(-Bv / (2.0f * cv), lam_lo), lam_hi);
+                    const float em = a.cell_emin[cell];
+                    const float t1m = av + ls * (Bv + ls * cv);
+                    const float margin = 1e-3f * (fabsf(av) + fabsf(Bv) + cv + fabsf(em) + s5max2) + 1e-5f;
+                    cell_lb = (t1m + em) - s5max2 - margin;
+                }
+            }
         }
         return (g - cpref[t]) * CH;
     };
@@ -591,6 +627,15 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     while (__syncthreads_or(done < my_total)) {
         for (uint32_t r = 0; r < rlen && done < my_total; r++) {
             const uint32_t o = locate(c_lo + done);
+            if (prune) {
+                const uint64_t tcur = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
+                if (tcur != ~0ull && cell_lb > key_dist(tcur)) {  // nothing in this cell can qualify
+                    const uint32_t end_chunk = min(cpref[t + 1], c_hi);
+                    if (lane == 0) atomicAdd(&s_pruned, min(L, (end_chunk - cpref[t]) * CH) - o);
+                    done = end_chunk - c_lo;
+                    continue;
+                }
+            }
             if (pf) {  // L2 prefetch of the chunk pf ahead in this cell (off the critical path)
                 const uint32_t s0 = o + pf * CH;
                 if (s0 < L) {
@@ -712,6 +757,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
     uint64_t* candq = a.cand + q * keep;
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
+    if (threadIdx.x == 0) a.meta[q].pruned = s_pruned;
 }
 
 }  // namespace dev
@@ -743,6 +789,13 @@ void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, ui
     dev::k_visit_bytes<<<(unsigned)dev::umin64(((uint64_t)ncell + 255) / 256, 1184), 256, 0, st>>>(
         visits, ncell, list_off, bytes_per_entry, hist);
     dev::k_pick_threshold<<<1, 32, 0, st>>>(hist, budget, threshold);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_cell_emin(const uint64_t* list_off, uint32_t ncell, const float* eterm, float* emin, cudaStream_t st) {
+    if (ncell == 0) return;
+    dev::k_cell_emin<<<(unsigned)dev::umin64(((uint64_t)ncell * 32 + 255) / 256, 4736), 256, 0, st>>>(list_off, ncell,
+                                                                                                   eterm, emin);
     CUDA_LAUNCH_CHECK();
 }
 

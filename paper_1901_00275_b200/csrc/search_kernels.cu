@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(512) k_second_level(SearchArgs a, uint32_t w1,
         a.meta[q].scanned = s_scanned;
         a.meta[q].dmax = s_dmax;
         a.meta[q].flag = 0;  // the fast scan may set 2 (candidate overflow)
+        a.meta[q].pruned = 0;
     }
 }
 
@@ -599,6 +600,14 @@ __global__ void k_copy_scanned(const QueryMeta* __restrict__ meta, uint64_t nq, 
         out[q] = meta[q].scanned;
 }
 
+__global__ void k_sum_pruned(const QueryMeta* __restrict__ meta, uint64_t nq, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x)
+        acc += meta[q].pruned;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 __global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         v[i] = (uint32_t)i;
@@ -613,6 +622,11 @@ void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, u
 
 void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st) {
     dev::k_copy_scanned<<<(unsigned)dev::umin64((nq + 255) / 256, 1184), 256, 0, st>>>(meta, nq, out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_sum_pruned(const QueryMeta* meta, uint64_t nq, unsigned long long* out, cudaStream_t st) {
+    dev::k_sum_pruned<<<(unsigned)dev::umin64((nq + 255) / 256, 148), 256, 0, st>>>(meta, nq, out);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -232,7 +232,7 @@ class Index:
         if reset:
             _lib.check(_lib.lib().vlq_engine_reset_stats(self._h))
         return {"launches": int(s.launches), "tiles": int(s.tiles), "flagged": int(s.flagged),
-                "tc_fallbacks": int(s.tc_fallbacks),
+                "tc_fallbacks": int(s.tc_fallbacks), "pruned": int(s.pruned),
                 "phase_ms": dict(zip(_lib.PHASES, [float(x) for x in s.phase_ms]))}
 
     def encode(self, x):
@@ -281,6 +281,72 @@ class Index:
 
 # ---- module functions ---------------------------------------------------------
 _MAX_THREADS = 0
+
+
+class IvfBaselineIndex:
+    """The IVFADC comparison baseline (proj/include/vlq/ivf_baseline.hpp):
+    k posting lists of (id, PQ code of x - c_i), built with an Index's
+    codebook and PQ (as eval.cpp:182 does).  Held by that Index's engine on
+    its device; build with build_ivf_baseline, query with
+    search_ivf_baseline."""
+
+    def __init__(self, index: Index):
+        self.index = index
+
+    @property
+    def base_count(self) -> int:
+        n = ctypes.c_uint64(0)
+        _lib.check(_lib.lib().vlq_engine_ivf_get_lists(self.index._h, ctypes.byref(n), None, None, None))
+        return int(n.value)
+
+    def lists(self):
+        """(list_off u64[k+1], ids u32[N], codes u8[N, m]) -- region-major,
+        ids ascending within a list (the reference's ids[c] / codes[c])."""
+        n = self.base_count
+        off = np.empty(self.index.k + 1, np.uint64)
+        ids = np.empty(n, np.uint32)
+        codes = np.empty((n, self.index.m), np.uint8)
+        _lib.check(_lib.lib().vlq_engine_ivf_get_lists(self.index._h, None, _p(off), _p(ids), _p(codes)))
+        return off, ids, codes
+
+    def search_device(self, d_queries: int, nq: int, w: int, k: int, d_ids: int, d_dists: int,
+                      d_scanned: int | None = None, stream: int | None = None) -> None:
+        _lib.check(_lib.lib().vlq_engine_ivf_search_device(self.index._h, ctypes.c_void_p(d_queries), nq, w, k,
+                                                           ctypes.c_void_p(d_ids), ctypes.c_void_p(d_dists),
+                                                           ctypes.c_void_p(d_scanned) if d_scanned else None,
+                                                           _stream(stream)))
+
+
+def build_ivf_baseline(base, index: Index) -> IvfBaselineIndex:
+    """build_ivf_baseline(base, codebook, pq) (ivf_baseline.cpp:11-51) with
+    index's codebook and PQ."""
+    b = _to_vecset(base)
+    dim = b.shape[1] if b.size else index.dim
+    _lib.check(_lib.lib().vlq_engine_ivf_build(index._h, _p(b), b.shape[0], dim))
+    return IvfBaselineIndex(index)
+
+
+def build_ivf_baseline_synthetic(n: int, index: Index, clusters: int = 200, spread: float = 0.05,
+                                 seed: int = 42) -> IvfBaselineIndex:
+    """The same over rows [0, n) of the device synthetic generator."""
+    _lib.check(_lib.lib().vlq_engine_ivf_build_synthetic(index._h, n, clusters, spread, seed))
+    return IvfBaselineIndex(index)
+
+
+def search_ivf_baseline(ivf: IvfBaselineIndex, queries, w: int, top_k: int, *, return_scanned: bool = False):
+    """search_ivf_baseline(index, queries, w, top_k) (ivf_baseline.cpp:53-126)
+    -> (ids int64[nq, top_k], dists float32[nq, top_k]), -1 / +inf padded."""
+    q = _to_vecset(queries)
+    nq = q.shape[0]
+    ids = np.empty((nq, top_k), np.int64)
+    dists = np.empty((nq, top_k), np.float32)
+    scanned = np.zeros(nq, np.uint64)
+    dim = q.shape[1] if q.size else ivf.index.dim
+    _lib.check(_lib.lib().vlq_engine_ivf_search(ivf.index._h, _p(q), nq, dim, w, top_k, _p(ids), _p(dists),
+                                                _p(scanned)))
+    if return_scanned:
+        return ids, dists, scanned
+    return ids, dists
 
 
 def set_max_threads(threads: int) -> None:

@@ -130,3 +130,48 @@ def test_adc_decomposition_matches_direct_evaluation():
                 got = o.adc_distance(ws, t5, ix.codes[e], int(ix.lambdas[e]), i, j)
                 want = o.direct_adc(y, ix.codes[e], int(ix.lambdas[e]), i, j)
                 assert abs(got - want) <= 1e-4 * max(1e-3, abs(want), ynorm)
+
+
+IVF_CASES = ["smoke", "m16", "n1m8", "m1", "accept_small"]
+
+
+def _ivf_fixture(name):
+    from conftest import GOLDEN
+    z = dict(np.load(os.path.join(GOLDEN, f"ivf_{name}.npz")))
+    model = os.path.join(GOLDEN, f"{name}.model.vlq")
+    if not os.path.exists(model):
+        model = os.path.join(GOLDEN, f"{name}.index.vlq")
+    return z, model
+
+
+@pytest.mark.parametrize("name", IVF_CASES)
+def test_oracle_ivf_baseline_matches_reference_golden(name):
+    """The C restatement of build_ivf_baseline / search_ivf_baseline
+    (ivf_baseline.cpp) reproduces the reference's lists and results
+    bit-exactly (fixtures made by the reference itself,
+    tests/golden/make_golden_ivf.py)."""
+    z, model = _ivf_fixture(name)
+    g, _, _ = load_golden(name)
+    o = oracle.OracleIndex(vlq1.read(model))
+    base = regen_base(g)
+    off, ids, codes = o.ivf_build(base)
+    assert np.array_equal(off, z["list_off"]) and np.array_equal(ids, z["ids"])
+    assert np.array_equal(codes, z["codes"])
+    for gi, (w, k) in enumerate(z["grid"]):
+        rid, rd, sc = o.ivf_search((off, ids, codes), g["queries"], int(w), int(k))
+        assert np.array_equal(rid, z[f"ids_{gi}"]), (name, gi)
+        assert np.array_equal(rd.view(np.uint32), z[f"dists_{gi}"].view(np.uint32)), (name, gi)
+        assert int(sc.sum()) == int(z[f"scanned_{gi}"])
+
+
+def test_oracle_ivf_exhaustive_equals_full_adc():
+    """test_eval.cpp "w=k is exhaustive-ADC-exact": w = K scans every list."""
+    z, model = _ivf_fixture("smoke")
+    g, _, _ = load_golden("smoke")
+    o = oracle.OracleIndex(vlq1.read(model))
+    base = regen_base(g)
+    lists = o.ivf_build(base)
+    rid, rd, sc = o.ivf_search(lists, g["queries"], o.ix.k, 10)
+    assert (sc == len(base)).all()
+    with pytest.raises(RuntimeError, match="search_ivf_baseline: need 0 < w <= k"):
+        o.ivf_search(lists, g["queries"], 0, 10)
