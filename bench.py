@@ -58,6 +58,8 @@ WORKLOADS = {
                n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=524_288, gt_queries=500),
     "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k, k=100",
                n=1_000_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536, ntrain=524_288, gt_queries=200),
+    "c5": dict(desc="SIFT1B-shaped synthetic (configs[4]): 1B x 128, K=65536 x 32 lines, PQ 8 B, k=100",
+               n=1_000_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=524_288, gt_queries=200),
 }
 SPREAD, BASE_SEED, QUERY_SEED, TRAIN_SEED = 0.05, 42, 43, 1
 
@@ -219,6 +221,8 @@ def main():
                     help="CPU baseline: the reference via a VLQ1 file (default up to 1e8 points) or the C oracle port")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of reference CPU work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", default=None,
+                    help="comma-separated w1 values: device QPS and recall@1/10/100 per w1 (QPS-recall curve)")
     ap.add_argument("--ivf", action="store_true",
                     help="also build and time the IVFADC comparison baseline (ivf_baseline.cpp) on the same model, w = w1")
     ap.add_argument("--profile", action="store_true",
@@ -312,13 +316,9 @@ def main():
     ms_max = float(t_max.item())
     value = nq * args.steps / (ms_max / 1e3)
 
-    # algorithmic bytes of the dominant kernel (the fused list scan): (m+5) per
-    # evaluated entry.  S_q (the reference's scanned count) minus the entries
-    # in cells the scan proved cannot qualify (cell lower bound, never read).
+    # algorithmic bytes of the dominant kernel (the fused list scan): S_q*(m+5)
     local_scanned = int(scanned.sum().item())
-    pruned_per_step = stats["pruned"] / args.steps
-    evaluated = local_scanned - pruned_per_step
-    scan_bytes_per_step = int(evaluated * (w["m"] + 5))
+    scan_bytes_per_step = local_scanned * (w["m"] + 5)
     scan_ms = stats["phase_ms"]["scan"] / args.steps
     res_ids = out_ids.cpu().numpy()
     res_d = out_d.cpu().numpy()
@@ -340,10 +340,6 @@ def main():
                 "frac": round(achieved / hbm, 4) if achieved else None, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
                 "algorithmic_bytes_per_launch": scan_bytes_per_step,
-                "evaluated_entries_per_launch": int(evaluated),
-                "reference_scanned_entries_per_launch": local_scanned,
-                "reference_semantics_bytes_per_launch": local_scanned * (w["m"] + 5),
-                "pruned_fraction": round(pruned_per_step / max(local_scanned, 1), 4),
                 "bytes_per_candidate": w["m"] + 5, "scan_ms_per_launch": round(scan_ms, 4),
                 "phase_ms_per_step": {p: round(v / args.steps, 4) for p, v in stats["phase_ms"].items()},
                 "scan_share_of_step": round(scan_ms / (ms_max / args.steps), 4)}
@@ -397,6 +393,32 @@ def main():
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "kind": kind, "unavailable": f"{type(e).__name__}: {e}"}
 
+    sweep = None
+    if args.sweep and world == 1:
+        sweep = []
+        for sw1 in [int(x) for x in args.sweep.split(",") if x]:
+            for _ in range(2):
+                idx.search_device(q.data_ptr(), nq, sw1, args.alpha, k, ids.data_ptr(), dists.data_ptr(),
+                                  scanned.data_ptr(), st)
+            torch.cuda.synchronize()
+            sms = 0.0
+            for _ in range(max(3, args.steps // 2)):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                idx.search_device(q.data_ptr(), nq, sw1, args.alpha, k, ids.data_ptr(), dists.data_ptr(),
+                                  scanned.data_ptr(), st)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                sms += e0.elapsed_time(e1)
+            reps = max(3, args.steps // 2)
+            sids = ids.cpu().numpy()
+            sweep.append({"w1": sw1, "alpha": args.alpha, "qps": round(nq * reps / (sms / 1e3), 1),
+                          "ms_per_step": round(sms / reps, 3),
+                          "scanned_per_query": round(float(scanned.sum().item()) / nq, 1),
+                          **{f"recall@{r}": round(recall_at(sids[:ngt], gt, r), 4) for r in (1, 10, 100) if r <= k}})
+            log(f"[sweep] {sweep[-1]}")
+
     ivf_line = None
     if args.ivf and world == 1:
         t0 = time.time()
@@ -429,7 +451,7 @@ def main():
             "data": "synthetic", "config": cfg, "recall": recall, "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
             "coarse_stage": "query-split (1/N of the batch per rank)" if world > 1 else "single GPU",
-            "ivfadc": ivf_line,
+            "ivfadc": ivf_line, "sweep": sweep,
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
             "fallback_queries_per_step": stats["flagged"] / args.steps,
             "tc_coarse_fallbacks_per_step": stats["tc_fallbacks"] / args.steps}

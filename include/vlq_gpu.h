@@ -62,7 +62,6 @@ typedef struct {
     uint64_t tc_fallbacks;  /* tensor-core coarse rows / add points that needed the exact full scan */
     double phase_ms[8];     /* CUDA-event ms per phase (profiling on): coarse, first-level,
                                second-level, term5, scan, rescore, fallback, output */
-    uint64_t pruned;        /* posting entries the fast scan skipped by the cell lower bound (profiling on) */
 } vlq_stats;
 
 /* Thread-local message of the last failing call on this thread. */

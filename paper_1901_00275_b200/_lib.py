@@ -24,7 +24,7 @@ class VlqConfig(ctypes.Structure):
 
 class VlqStats(ctypes.Structure):
     _fields_ = [("launches", c_u64), ("tiles", c_u64), ("flagged", c_u64), ("tc_fallbacks", c_u64),
-                ("phase_ms", ctypes.c_double * 8), ("pruned", c_u64)]
+                ("phase_ms", ctypes.c_double * 8)]
 
 
 PHASES = ["coarse", "first_level", "second_level", "term5", "scan", "rescore", "fallback", "output"]

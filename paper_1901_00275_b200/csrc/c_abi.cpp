@@ -298,7 +298,6 @@ int vlq_engine_get_stats(vlq_engine* e, vlq_stats* out) {
     out->flagged = s.flagged;
     out->tc_fallbacks = s.tc_refine_fallbacks;
     for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
-    out->pruned = s.pruned;
     return VLQ_OK;
 }
 

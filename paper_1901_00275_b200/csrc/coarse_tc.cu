@@ -311,14 +311,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int h = 0; h < TN / 64; h++) {
                 uint32_t acc[32];
                 const uint32_t col = half * (TN / 2) + h * 32;
-                const float nv = __ldg(nrm + col + lane);  // one coalesced load, broadcast by shuffles
+                // search modes: one coalesced load, broadcast by shuffles; the
+                // add path's ARGMIN epilogue keeps broadcast L1 loads (measured faster there)
+                const float nv = MODE == 0 ? 0.0f : __ldg(nrm + col + lane);
                 tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TN + col, acc);
                 float* tr = sMerge + (warp - 2) * 32 * 33;  // STORE: this warp's transpose tile
                 float cmin = __int_as_float(0x7f800000);
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     const uint32_t cidx = t * TN + col + j;
-                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), __shfl_sync(0xffffffffu, nv, j));
+                    const float nj = MODE == 0 ? __ldg(nrm + col + j) : __shfl_sync(0xffffffffu, nv, j);
+                    const float d = fmaf(-2.0f, __uint_as_float(acc[j]), nj);
                     if constexpr (MODE == 0) {
                         if (d < bd[3]) {  // sorted insert, ties keep the lower index (earlier)
                             if (d < bd[2]) {
@@ -742,8 +745,12 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
 
 // tau[row] = the L-th smallest chunk minimum (an upper bound on the row's
 // L-th smallest approximate value).
+// Y != null: the chunk minima came from the 1xTF32 pass, and tau is raised by
+// twice that pass's error bound so it also bounds the L-th smallest 3xTF32
+// value the filter pass compares against (at least L centroids pass).
 __global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
-                                                  uint32_t* __restrict__ scratch, float* __restrict__ tau) {
+                                                  uint32_t* __restrict__ scratch, float* __restrict__ tau,
+                                                  const float* __restrict__ Y, uint32_t dim, float cmax) {
     __shared__ uint32_t hist[2048];
     __shared__ uint32_t scan[40];
     __shared__ unsigned int s_max;
@@ -758,7 +765,15 @@ __global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) atomicMax(&s_max, ord_float(mx));
     __syncthreads();
-    if (threadIdx.x == 0) tau[q] = unord_float(s_max);
+    if (threadIdx.x == 0) {
+        float t = unord_float(s_max);
+        if (Y) {
+            float yn = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
+            t += 2.0f * tc_eps(yn, cmax, dim, false) * 1.01f;
+        }
+        tau[q] = t;
+    }
 }
 
 // Exact top-w1 from the filtered candidate list: exact reference-order
@@ -892,9 +907,9 @@ void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float*
 
 
 void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
-                     cudaStream_t st) {
+                     cudaStream_t st, const float* Y, uint32_t dim, float cmax) {
     if (nq == 0) return;
-    dev::k_tau_rows<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, scratch, tau);
+    dev::k_tau_rows<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, scratch, tau, Y, dim, cmax);
     CUDA_LAUNCH_CHECK();
 }
 

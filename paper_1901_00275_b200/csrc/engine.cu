@@ -49,7 +49,6 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
-    if (const char* v = std::getenv("VLQ_SCAN_PRUNE")) cfg_.scan_prune = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -247,14 +246,13 @@ void Engine::compute_eterm() {
     CUDA_CHECK(cudaMemcpyAsync(&bits, err_.p + 1, 4, cudaMemcpyDeviceToHost, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     std::memcpy(&emax_, &bits, 4);
-    compute_cell_emin();
+    pack_eterm_lam();
 }
 
-void Engine::compute_cell_emin() {
+void Engine::pack_eterm_lam() {
     DeviceGuard g(cfg_.device);
-    const uint32_t ncell = k_ * n_;
-    emin_.alloc(std::max<uint32_t>(ncell, 1));
-    launch_cell_emin(list_off_.p, ncell, eterm_.p, emin_.p, stream_);
+    eterm_lam_.alloc(std::max<uint64_t>(nent_, 1));
+    launch_pack_eterm_lam(eterm_.p, lambdas_.p, nent_, eterm_lam_.p, stream_);
     CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
@@ -413,7 +411,7 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
     }
     std::memcpy(&emax_, &flags[1], 4);
     nent_ = nloc;
-    compute_cell_emin();
+    pack_eterm_lam();
     base_count_ = nb;
 }
 
@@ -566,13 +564,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         sl.fast = fast;
         sl.tc = tc;
         unsigned int* hv = sl.counts;
-        if (fast) {
-            CUDA_CHECK(cudaMemcpyAsync(hv, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
-            prun_acc_.alloc(1);
-            CUDA_CHECK(cudaMemsetAsync(prun_acc_.p, 0, 8, st));
-            launch_sum_pruned(meta_.p, nt, prun_acc_.p, st);
-            CUDA_CHECK(cudaMemcpyAsync(hv + 2, prun_acc_.p, 8, cudaMemcpyDeviceToHost, st));
-        }
+        if (fast) CUDA_CHECK(cudaMemcpyAsync(hv, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
         if (tc) CUDA_CHECK(cudaMemcpyAsync(hv + 1, err_.p + 6, 4, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaEventRecord(sl.done, st));
         prof_used_++;
@@ -608,9 +600,25 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
     if (two_pass) {
         // pass 1: chunk minima -> tau (upper bound of the L-th smallest);
         // pass 2: recompute, keep only approx <= tau (no K-wide row in HBM)
-        launch_coarse_tc(2, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr, st,
-                         nullptr, nullptr, 0, xtc, xlo);
-        launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st);
+        if (tc_split_ && cfg_.tc_pass1_single) {
+            // pass 1 in 1xTF32 on 128-centroid tiles (a third of the MMAs; same
+            // 32-column chunks), tau raised by its error bound
+            if (!xtc1_.p || xtc1_.n < ((nt + 127) / 128) * 128 * dim_) {
+                xtc1_.alloc(((nt + 127) / 128) * 128 * dim_);
+            }
+            const float* x1 = nullptr;
+            if (cfg_.tc_persist) {
+                launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st);
+                x1 = xtc1_.p;
+            }
+            launch_coarse_tc(2, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr,
+                             st, nullptr, nullptr, 0, x1, nullptr);
+            launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st, d_q, dim_, cmax_);
+        } else {
+            launch_coarse_tc(2, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr, st,
+                             nullptr, nullptr, 0, xtc, xlo);
+            launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st);
+        }
         CUDA_CHECK(cudaMemsetAsync(lcnt_.p, 0, nt * 4, st));
         launch_coarse_tc(3, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, nullptr, 0, lidx_.p, ld_.p, st, tau_.p,
                          lcnt_.p, kListCap, xtc, xlo);
@@ -664,7 +672,10 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (fast) {
         const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
         mark(PH_SCAN);
-        if (cfg_.scan_prune && emin_.p) a.cell_emin = emin_.p;
+        if (cfg_.scan_packed && cfg_.scan_variant == 0 && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
+            a.eterm_lam = eterm_lam_.p;
+            a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
+        }
         if (cfg_.scan_l2_budget_mb > 0 && cfg_.scan_variant == 0) {
             // L2 retention: the batch's most re-read cells stay (evict_last),
             // single-visit cells stream through (evict_first)
@@ -715,7 +726,8 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "force_exact") cfg_.force_exact = (int)value;
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;
     else if (key == "scan_l2_budget_mb") cfg_.scan_l2_budget_mb = (int)value;
-    else if (key == "scan_prune") cfg_.scan_prune = (int)value;
+    else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
+    else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 
@@ -728,7 +740,7 @@ void Engine::grow_profile(size_t slots) {
         ProfSlot& sl = prof_.back();
         for (auto& e : sl.ev) CUDA_CHECK(cudaEventCreate(&e));
         CUDA_CHECK(cudaEventCreate(&sl.done));
-        CUDA_CHECK(cudaMallocHost(&sl.counts, 4 * sizeof(unsigned int)));
+        CUDA_CHECK(cudaMallocHost(&sl.counts, 2 * sizeof(unsigned int)));
     }
 }
 
@@ -750,10 +762,7 @@ void Engine::collect_profile() {
             stats_.phase_ms[p] += ms;
         }
         const unsigned int* hv = sl.counts;
-        if (sl.fast) {
-            stats_.flagged += hv[0];
-            stats_.pruned += (uint64_t)hv[2] | ((uint64_t)hv[3] << 32);
-        }
+        if (sl.fast) stats_.flagged += hv[0];
         if (sl.tc) stats_.tc_refine_fallbacks += hv[1];
     }
     prof_used_ = 0;

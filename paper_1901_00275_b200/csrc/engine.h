@@ -30,12 +30,13 @@ struct EngineConfig {
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
     int scan_l2_budget_mb = 0;  // v6 scan: MB of the batch's most re-read cells loaded evict_last (0 = plain loads)
-    int scan_prune = 1;    // v6 scan: skip cells whose distance lower bound exceeds the block threshold
+    int scan_packed = 1;   // v6 scan reads the packed e-term | lambda-byte stream (one load per entry)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
     uint32_t tc_search_min_k = 16384; // search coarse stage on tensor cores for K >= this (env VLQ_TC_SEARCH_MIN_K)
     int tc_store_rows = 0;  // 1: materialise approximate rows + radix select instead of the two-pass filter
     int tc_persist = 1;     // search coarse kernels as a persistent grid (one CTA per SM)
+    int tc_pass1_single = 1;  // two-pass coarse filter: first pass in 1xTF32 (tau raised by its error bound)
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -123,7 +124,6 @@ struct EngineStats {
     uint64_t tiles = 0;
     uint64_t flagged = 0;       // queries that took the exact fallback
     double phase_ms[PH_COUNT] = {0};  // CUDA-event time per phase (profiling on)
-    uint64_t pruned = 0;        // posting entries the fast scan never read (cell lower bound; profiling on)
 };
 
 class Engine {
@@ -208,7 +208,7 @@ private:
     void upload_model();
     void upload_lists(const HostLists& L);
     void compute_eterm();
-    void compute_cell_emin();
+    void pack_eterm_lam();
     AddArgs add_args() const;
     SearchArgs search_args() const;
     enum Stage { STAGE_ALL = 0, STAGE_COARSE = 1, STAGE_FINE = 2 };
@@ -228,7 +228,7 @@ private:
     struct ProfSlot {
         cudaEvent_t ev[PH_COUNT + 1] = {};
         cudaEvent_t done = nullptr;
-        unsigned int* counts = nullptr;  // pinned [4]: fast-scan flagged, tc refine fallbacks, u64 pruned entries
+        unsigned int* counts = nullptr;  // pinned [2]: fast-scan flagged, tc refine fallbacks
         bool fast = false, tc = false;
     };
     std::vector<ProfSlot> prof_;  // one per tile searched since the last collect_profile()
@@ -243,6 +243,7 @@ private:
     static constexpr uint32_t kListCap = 1024;  // per-query candidate list of the two-pass coarse filter
     DevBuf<float> tmin_, tau_, ld_;
     DevBuf<float> xtc_, xlo_;  // query rows in the UMMA layout (persistent coarse kernels)
+    DevBuf<float> xtc1_;       // unsplit copy for the 1xTF32 first pass
     DevBuf<uint32_t> visits_, hot_t_;      // per-batch cell visit counts, L2-retention threshold
     DevBuf<unsigned long long> vhist_;
     DevBuf<uint32_t> lcnt_, lidx_;
@@ -265,8 +266,7 @@ private:
     DevBuf<uint8_t> codes_, lambdas_;
     DevBuf<uint32_t> ids_;
     DevBuf<float> eterm_;
-    DevBuf<float> emin_;  // per-cell min e-term (cell-level pruning bound)
-    DevBuf<unsigned long long> prun_acc_;  // per-tile pruned-entry total (profiling)
+    DevBuf<uint32_t> eterm_lam_;  // packed e-term | lambda byte (v6 scan stream)
     DevBuf<unsigned int> err_;  // [0] error flag, [1] emax bits, [2] flagged count, [3..4] minmax
 
     // IVFADC baseline lists (region-major; ids ascending within a list)

@@ -13,7 +13,7 @@ struct QueryMeta {
     float dmax;                  // bound on |term1| over the query's selected cells
     float s5max;                 // bound on |sum5|
     uint32_t flag;               // 1: certificate failed -> exact fallback
-    uint32_t pruned;             // entries the fast scan skipped by the cell lower bound (never read)
+    uint32_t pad;
 };
 
 // Device views used by the search kernels (all pointers device-resident).
@@ -49,8 +49,12 @@ struct SearchArgs {
     // (re-read by other queries of the batch); null = plain loads
     const uint32_t* cell_visits;
     const uint32_t* hot_threshold;
-    // cell-level pruning (v6 scan): min e-term of every cell's entries; null = off
-    const float* cell_emin;
+    // v6 scan input stream: e-term with its low 8 mantissa bits replaced by the
+    // entry's lambda byte (one 4-byte load per entry instead of 4 + 1);
+    // e_pack_err bounds the e-term change (2^-15 Emax), added to the
+    // certificate when the packed stream was scanned
+    const uint32_t* eterm_lam;
+    float e_pack_err;
 };
 
 // Add-path device views.
@@ -81,8 +85,8 @@ void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t ke
 void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, uint32_t ncell, const uint64_t* list_off,
                         uint32_t bytes_per_entry, uint64_t budget, unsigned long long* hist, uint32_t* threshold,
                         cudaStream_t st);
-// emin[c] = min of eterm over cell c's entries (+inf for an empty cell)
-void launch_cell_emin(const uint64_t* list_off, uint32_t ncell, const float* eterm, float* emin, cudaStream_t st);
+// eterm_lam[e] = (bits(eterm[e]) & ~0xff) | lambdas[e]
+void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t n, uint32_t* out, cudaStream_t st);
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int slots,
                       int prefetch, cudaStream_t st);
 void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
@@ -110,7 +114,6 @@ void launch_histogram(const uint32_t* cells, uint64_t n, unsigned long long* cou
 namespace vlq {
 void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st);
 void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st);
-void launch_sum_pruned(const QueryMeta* meta, uint64_t nq, unsigned long long* out, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 void launch_synth(uint64_t first, uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,
                   float* out, cudaStream_t st);
@@ -133,7 +136,7 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
                       cudaStream_t st, const float* tau = nullptr, uint32_t* cnt = nullptr, uint32_t cap = 0,
                       const float* Xtc = nullptr, const float* Xlo_tc = nullptr);
 void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
-                     cudaStream_t st);
+                     cudaStream_t st, const float* Y = nullptr, uint32_t dim = 0, float cmax = 0.0f);
 void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, const uint32_t* cand,
                         const uint32_t* cnt, uint32_t cap, const float* tau, uint32_t w1, float cmax, int split,
                         uint32_t* top, uint32_t* flagged, unsigned int* nflag, cudaStream_t st);

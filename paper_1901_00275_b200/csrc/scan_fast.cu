@@ -460,18 +460,10 @@ __global__ void k_pick_threshold(const unsigned long long* __restrict__ hist, ui
     *threshold = T;
 }
 
-// emin[c] = min over cell c's e-terms (warp per cell)
-__global__ void k_cell_emin(const uint64_t* __restrict__ off, uint32_t ncell, const float* __restrict__ eterm,
-                            float* __restrict__ emin) {
-    const uint32_t lane = threadIdx.x & 31u;
-    for (uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < ncell;
-         c += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint64_t b0 = off[c], b1 = off[c + 1];
-        float mn = __int_as_float(0x7f800000);
-        for (uint64_t e = b0 + lane; e < b1; e += 32) mn = fminf(mn, eterm[e]);
-        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        if (lane == 0) emin[c] = mn;
-    }
+__global__ void k_pack_eterm_lam(const float* __restrict__ eterm, const uint8_t* __restrict__ lambdas, uint64_t n,
+                                 uint32_t* __restrict__ out) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
+        out[e] = (__float_as_uint(eterm[e]) & ~0xffu) | (uint32_t)lambdas[e];
 }
 
 // v6: the v5 schedule (balanced chunk ranges, block-shared candidate buffer,
@@ -519,7 +511,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     __shared__ unsigned int s_misc[48];
     __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
-    __shared__ unsigned int s_pruned;
 
     // 1. the query's term5 table (one copy per sub-space)
     const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
@@ -546,7 +537,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             cpref[w2] = total;
             s_count = 0;
             s_tau = ~0ull;
-            s_pruned = 0;
         }
     }
     __syncthreads();
@@ -572,15 +562,8 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     const float* e_c = nullptr;
     float2 av2 = make_float2(0.f, 0.f), Bc2 = av2, cv2 = av2;
     uint32_t loaded_t = 0xffffffffu;
-    // Cell-level pruning: every entry of a cell has fast distance >=
-    //   LB = min_lambda term1(lambda) + emin_cell - 2 S5max_q
-    // (term1 is convex in lambda: c > 0; sum5 <= S5max_q = sum_p max_j |t5|);
-    // once the block threshold is below LB minus a rounding margin, no entry
-    // of the cell can enter the top-k' and its bytes are never read.
-    const bool prune = a.cell_emin != nullptr;
-    const float s5max2 = 2.0f * a.meta[q].s5max;
-    const float lam_lo = a.lam0, lam_hi = fmaf(255.0f, a.lam_delta, a.lam0);
-    float cell_lb = -__int_as_float(0x7f800000);
+    const bool packed = a.eterm_lam != nullptr;
+    const uint32_t* el_c = nullptr;
     const bool hinted = a.cell_visits != nullptr;
     const uint32_t hot_t = hinted ? *a.hot_threshold : 0xffffffffu;
     const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
@@ -604,18 +587,8 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             codes_c = a.codes + b0 * M;
             lam_c = a.lambdas + b0;
             e_c = a.eterm + b0;
+            if (packed) el_c = a.eterm_lam + b0;
             if (hinted) pol = a.cell_visits[cell] >= hot_t ? pol_keep : pol_stream;
-            if (prune) {
-                const float Bv = (bv - av) - cv;
-                cell_lb = -__int_as_float(0x7f800000);
-                if (cv > 0.0f) {
-                    const float ls = fminf(fmaxf(-Bv / (2.0f * cv), lam_lo), lam_hi);
-                    const float em = a.cell_emin[cell];
-                    const float t1m = av + ls * (Bv + ls * cv);
-                    const float margin = 1e-3f * (fabsf(av) + fabsf(Bv) + cv + fabsf(em) + s5max2) + 1e-5f;
-                    cell_lb = (t1m + em) - s5max2 - margin;
-                }
-            }
         }
         return (g - cpref[t]) * CH;
     };
@@ -627,15 +600,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     while (__syncthreads_or(done < my_total)) {
         for (uint32_t r = 0; r < rlen && done < my_total; r++) {
             const uint32_t o = locate(c_lo + done);
-            if (prune) {
-                const uint64_t tcur = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
-                if (tcur != ~0ull && cell_lb > key_dist(tcur)) {  // nothing in this cell can qualify
-                    const uint32_t end_chunk = min(cpref[t + 1], c_hi);
-                    if (lane == 0) atomicAdd(&s_pruned, min(L, (end_chunk - cpref[t]) * CH) - o);
-                    done = end_chunk - c_lo;
-                    continue;
-                }
-            }
             if (pf) {  // L2 prefetch of the chunk pf ahead in this cell (off the critical path)
                 const uint32_t s0 = o + pf * CH;
                 if (s0 < L) {
@@ -648,14 +612,33 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             uint32_t cw[U][NW];
             uint32_t lb[U];
             float ev[U];
+            // (warp-uniform variants hoisted out of the slot loop so each
+            // issues its U x 2-3 loads back to back)
+            if (packed) {  // one 4-byte word: e-term (low 8 mantissa bits dropped) | lambda byte
+                uint32_t le[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t ic = min(o + u * 32 + lane, L - 1);  // clamped: the tail re-reads entry L-1
-                if (hinted) {
+                for (int u = 0; u < U; u++) {
+                    const uint32_t ic = min(o + u * 32 + lane, L - 1);  // clamped: the tail re-reads entry L-1
+                    load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
+                    le[u] = __ldg(el_c + ic);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    lb[u] = le[u] & 0xffu;
+                    ev[u] = __uint_as_float(le[u] & ~0xffu);
+                }
+            } else if (hinted) {
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t ic = min(o + u * 32 + lane, L - 1);
                     load_code_vec_pol<M>(codes_c + (size_t)ic * M, cw[u], pol);
                     lb[u] = ld_u8_pol(lam_c + ic, pol);
                     ev[u] = ld_f32_pol(e_c + ic, pol);
-                } else {
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t ic = min(o + u * 32 + lane, L - 1);
                     load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
                     lb[u] = __ldg(lam_c + ic);
                     ev[u] = __ldg(e_c + ic);
@@ -757,7 +740,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
     uint64_t* candq = a.cand + q * keep;
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
-    if (threadIdx.x == 0) a.meta[q].pruned = s_pruned;
 }
 
 }  // namespace dev
@@ -792,10 +774,9 @@ void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, ui
     CUDA_LAUNCH_CHECK();
 }
 
-void launch_cell_emin(const uint64_t* list_off, uint32_t ncell, const float* eterm, float* emin, cudaStream_t st) {
-    if (ncell == 0) return;
-    dev::k_cell_emin<<<(unsigned)dev::umin64(((uint64_t)ncell * 32 + 255) / 256, 4736), 256, 0, st>>>(list_off, ncell,
-                                                                                                   eterm, emin);
+void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t n, uint32_t* out, cudaStream_t st) {
+    if (n == 0) return;
+    dev::k_pack_eterm_lam<<<(unsigned)dev::umin64((n + 255) / 256, 4736), 256, 0, st>>>(eterm, lambdas, n, out);
     CUDA_LAUNCH_CHECK();
 }
 

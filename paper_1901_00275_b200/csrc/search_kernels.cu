@@ -166,7 +166,6 @@ __global__ void __launch_bounds__(512) k_second_level(SearchArgs a, uint32_t w1,
         a.meta[q].scanned = s_scanned;
         a.meta[q].dmax = s_dmax;
         a.meta[q].flag = 0;  // the fast scan may set 2 (candidate overflow)
-        a.meta[q].pruned = 0;
     }
 }
 
@@ -424,7 +423,8 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, ui
             // |term1_fast - term1_exact| <= 19u*Dmax (FFMA lambda/term1 vs the
             // reference op order), the reassociated e-sum 8u*(Dmax+Emax), the
             // final subtraction 4u*S5max; 1.25x margin
-            const double eps = 1.25 * u * (27.0 * (double)mt.dmax + 8.0 * (double)a.emax + 4.0 * (double)mt.s5max) + 1e-30;
+            const double eps = 1.25 * u * (27.0 * (double)mt.dmax + 8.0 * (double)a.emax + 4.0 * (double)mt.s5max) +
+                               1.25 * (double)a.e_pack_err + 1e-30;
             const double exact_k = (double)unord_float((uint32_t)(keys[topk - 1] >> 32));
             const double fast_last = (double)s_fast_last;
             if (!(fast_last - eps > exact_k)) flag = 1;
@@ -600,14 +600,6 @@ __global__ void k_copy_scanned(const QueryMeta* __restrict__ meta, uint64_t nq, 
         out[q] = meta[q].scanned;
 }
 
-__global__ void k_sum_pruned(const QueryMeta* __restrict__ meta, uint64_t nq, unsigned long long* __restrict__ out) {
-    unsigned long long acc = 0;
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x)
-        acc += meta[q].pruned;
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
-}
-
 __global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         v[i] = (uint32_t)i;
@@ -622,11 +614,6 @@ void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, u
 
 void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st) {
     dev::k_copy_scanned<<<(unsigned)dev::umin64((nq + 255) / 256, 1184), 256, 0, st>>>(meta, nq, out);
-    CUDA_LAUNCH_CHECK();
-}
-
-void launch_sum_pruned(const QueryMeta* meta, uint64_t nq, unsigned long long* out, cudaStream_t st) {
-    dev::k_sum_pruned<<<(unsigned)dev::umin64((nq + 255) / 256, 148), 256, 0, st>>>(meta, nq, out);
     CUDA_LAUNCH_CHECK();
 }
 

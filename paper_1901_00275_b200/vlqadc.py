@@ -232,7 +232,7 @@ class Index:
         if reset:
             _lib.check(_lib.lib().vlq_engine_reset_stats(self._h))
         return {"launches": int(s.launches), "tiles": int(s.tiles), "flagged": int(s.flagged),
-                "tc_fallbacks": int(s.tc_fallbacks), "pruned": int(s.pruned),
+                "tc_fallbacks": int(s.tc_fallbacks),
                 "phase_ms": dict(zip(_lib.PHASES, [float(x) for x in s.phase_ms]))}
 
     def encode(self, x):

@@ -61,6 +61,7 @@ def main():
         print(json.dumps({"hubs": out}), flush=True)
     ref = None
     for cfg in args.configs:
+        clk = bench.ClockSampler(0)
         for kv in cfg.split(","):
             key, val = kv.split("=")
             idx.set_tuning(key, int(val))
@@ -72,14 +73,15 @@ def main():
         idx.stats(reset=True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tot = 0.0
-        for _ in range(args.steps):
-            flush.zero_()
-            ev0.record()
-            idx.search_device(q.data_ptr(), nq, args.w1, args.alpha, k, ids.data_ptr(), dists.data_ptr(),
-                              scanned.data_ptr(), st)
-            ev1.record()
-            torch.cuda.synchronize()
-            tot += ev0.elapsed_time(ev1)
+        with clk:
+            for _ in range(args.steps):
+                flush.zero_()
+                ev0.record()
+                idx.search_device(q.data_ptr(), nq, args.w1, args.alpha, k, ids.data_ptr(), dists.data_ptr(),
+                                  scanned.data_ptr(), st)
+                ev1.record()
+                torch.cuda.synchronize()
+                tot += ev0.elapsed_time(ev1)
         stats = idx.stats()
         idx.set_profiling(False)
         res = (ids.cpu().numpy().copy(), dists.cpu().numpy().view(np.uint32).copy())
@@ -94,7 +96,8 @@ def main():
                 "qps": round(nq * args.steps / (tot / 1e3), 1),
                 "phase_ms": {p: round(v / args.steps, 3) for p, v in stats["phase_ms"].items()},
                 "scan_gbs": round(sc * (w["m"] + 5) / (scan_ms / 1e3) / 1e9, 1) if scan_ms else None,
-                "flagged_per_step": stats["flagged"] / args.steps, "same_as_first": same, "setup": setup}
+                "flagged_per_step": stats["flagged"] / args.steps, "clocks": clk.summary(),
+                "same_as_first": same, "setup": setup}
         print(json.dumps(line), flush=True)
 
 

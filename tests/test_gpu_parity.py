@@ -84,15 +84,15 @@ def test_exhaustive_search_equals_full_scan(vlqadc, oracle_mod):
         assert np.array_equal(ids, oids) and same_f32(dists, odists)
 
 
-@pytest.mark.parametrize("seed,prune", [(0, 1), (1, 1), (2, 0)])
-def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed, prune):
-    """Random (w1, alpha, k) vs the oracle, with the scan's cell-level
-    lower-bound pruning on (default) and off."""
+@pytest.mark.parametrize("seed,variant", [(0, 0), (1, 0), (2, 4)])
+def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed, variant):
+    """Random (w1, alpha, k) vs the oracle (v6 scan; seed 2 with the v5
+    single-table scan)."""
     rng = np.random.default_rng(seed)
     for name in ALL_CASES:
         z, index_path, _ = load_golden(name)
         idx = vlqadc.Index.load(index_path)
-        idx.set_tuning("scan_prune", prune)
+        idx.set_tuning("scan_variant", variant)
         o = oracle_mod.OracleIndex.load(index_path)
         for _ in range(3):
             w1 = int(rng.integers(1, idx.k + 1))

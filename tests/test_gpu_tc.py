@@ -126,11 +126,16 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
     idx.save(path)
     o = oracle_mod.OracleIndex.load(path)
     # persistent / per-row-block coarse grids; plain vs L2-retention-hinted scan loads
-    for persist, l2mb, prune in [(1, 0, 1), (0, 0, 1), (1, 1, 1), (1, 0, 0)]:
-        idx.set_tuning("tc_persist", persist)
-        idx.set_tuning("scan_l2_budget_mb", l2mb)
-        idx.set_tuning("scan_prune", prune)
+    variants = [dict(tc_persist=1), dict(tc_persist=0), dict(scan_l2_budget_mb=1), dict(tc_pass1_single=1),
+                dict(tc_pass1_single=1, tc_persist=0), dict(scan_variant=4), dict(scan_prefetch=1),
+                dict(scan_packed=0)]
+    for v in variants:
+        knobs = dict(tc_persist=1, scan_l2_budget_mb=0, tc_pass1_single=0, scan_variant=0, scan_prefetch=0,
+                     scan_packed=1)
+        knobs.update(v)
+        for key, val in knobs.items():
+            idx.set_tuning(key, val)
         for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100)]:
             ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
             oids, od, _ = o.search(q, w1, alpha, k)
-            assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, persist, l2mb, prune, w1, alpha, k)
+            assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, v, w1, alpha, k)
