@@ -235,9 +235,15 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; VLQ_DIST_BACKEND=gloo (with ranks sharing GPUs
+    # round-robin) is the single-GPU rehearsal of the N > 1 path
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    backend = os.environ.get("VLQ_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     os.environ["VLQ_DEVICE"] = str(local)
     w = WORKLOADS[args.workload]
@@ -310,7 +316,8 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in ev)
     stats = idx.stats()
     idx.set_profiling(False)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=q.device)
+    red_dev = q.device if backend == "nccl" else "cpu"  # gloo reduces host tensors
+    t_max = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
@@ -322,6 +329,33 @@ def main():
     scan_ms = stats["phase_ms"]["scan"] / args.steps
     res_ids = out_ids.cpu().numpy()
     res_d = out_d.cpu().numpy()
+
+    e2e = None
+    if world > 1:
+        # every rank copies the batch in (pinned), runs the query-split search;
+        # rank 0 reads the merged result back; device time, max over ranks
+        qpin = torch.from_numpy(q.cpu().numpy()).pin_memory()
+        qdev = torch.empty_like(q)
+        e_ms = 0.0
+        for s_ in range(args.steps + 1):
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            qdev.copy_(qpin, non_blocking=True)
+            mi, md, _ = sharded.search_query_split(qdev, args.w1, args.alpha, k, out=(ids, dists, scanned))
+            if rank == 0:
+                e_ids = mi.to("cpu", non_blocking=True)
+                e_d = md.to("cpu", non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if s_ > 0:  # the first call is a warm-up
+                e_ms += e0.elapsed_time(e1)
+        t_e = torch.tensor([e_ms], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(nq * args.steps / (float(t_e.item()) / 1e3), 1), "unit": "queries/s",
+               "h2d_bytes_per_step": int(qpin.numel() * 4), "d2h_bytes_per_step": int(nq * k * 12),
+               "api": "ShardedIndex.search_query_split (pinned host queries in, merged ids/dists out on rank 0)",
+               "timing": "CUDA events around H2D + search + D2H, max over ranks"}
 
     if rank != 0:
         dist.barrier()
@@ -352,7 +386,6 @@ def main():
     recall = {f"recall@{r}": round(recall_at(res_ids[:ngt], gt, r), 4) for r in (1, 10, 100) if r <= k}
 
     # e2e: public API with host buffers (H2D queries + D2H results per step)
-    e2e = None
     if world == 1:
         idx.search(qh, w1=args.w1, alpha=args.alpha, k=k)
         per = []

@@ -157,7 +157,9 @@ int vlq_engine_ivf_get_lists(vlq_engine* e, uint64_t* count, uint64_t* list_off,
 
 /* Study knobs, not part of the reference surface: "scan_variant" (0 = v6
  * packed-fp32 fast scan, 2/3/4 = v5 LUT layouts, 1 = generic scan),
- * "scan_slots" (entry slots per lane: 4/6/8), "tc_search_min_k",
+ * "scan_slots" (entry slots per lane: 4/6/8; +100 = 4 CTAs/SM),
+ * "scan_prefetch" (L2 prefetch distance in chunks), "scan_packed" (packed
+ * e-term|lambda stream), "tc_persist", "tc_pass1_single", "tc_search_min_k",
  * "force_exact".  Results are identical for every setting. */
 int vlq_engine_set_tuning(vlq_engine* e, const char* key, int64_t value);
 

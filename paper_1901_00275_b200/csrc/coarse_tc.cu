@@ -671,7 +671,9 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
     const uint32_t nwords = (k + 31) / 32;
     uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);            // nwords
     uint32_t* ids = bitmap + nwords;                                  // up to w1*(n+1)
-    float* ys = reinterpret_cast<float*>(ids + w1 * (n + 1));         // dim
+    const size_t head = ((size_t)(nwords + w1 * (n + 1)) * 4 + 15) & ~(size_t)15;
+    float* ys = reinterpret_cast<float*>(smem + head);                // dim, 16-B aligned
+    float* tiles = ys + ((dim + 3) & ~3u);                             // 8 warps x 16 rows x (dim + 4)
     __shared__ uint32_t s_scan[40];
     const uint64_t q = blockIdx.x;
     for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) bitmap[i] = 0;
@@ -699,38 +701,37 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
         }
     }
     __syncthreads();
-    // one thread per needed centroid: 16-byte loads straight from L2, then the
-    // sequential reference-order sqdist
+    // rows staged through shared memory, 16 per warp at a time: the warp reads
+    // each row with coalesced 16-byte loads (one row per instruction), then
+    // lanes 0..15 each run the sequential reference-order sqdist of one row
+    // (row stride dim + 4 floats: conflict-free 128-bit stores and loads)
     float* wsq = ws + q * k;
-    if ((dim & 3u) == 0) {
-        const uint32_t n4 = dim >> 2;
-        for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-            const uint32_t c = ids[t];
-            const float4* cp = reinterpret_cast<const float4*>(C + (uint64_t)c * dim);
-            float acc = 0.0f;
-            uint32_t d4 = 0;
-            for (; d4 + 8 <= n4; d4 += 8) {
-                float4 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) v[u] = __ldg(cp + d4 + u);
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const uint32_t d = (d4 + u) * 4;
-                    acc = sq_step(acc, ys[d], v[u].x);
-                    acc = sq_step(acc, ys[d + 1], v[u].y);
-                    acc = sq_step(acc, ys[d + 2], v[u].z);
-                    acc = sq_step(acc, ys[d + 3], v[u].w);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+    if ((dim & 3u) == 0 && dim <= 128) {
+        const uint32_t n4 = dim >> 2, stride = dim + 4;
+        float* tile = tiles + (size_t)warp * 16 * stride;
+        for (uint32_t b0 = warp * 16; b0 < total; b0 += nwarps * 16) {
+            const uint32_t nb = min(16u, total - b0);
+            for (uint32_t r = 0; r < nb; r++) {
+                const float4* cp = reinterpret_cast<const float4*>(C + (uint64_t)ids[b0 + r] * dim);
+                for (uint32_t c4 = lane; c4 < n4; c4 += 32)
+                    *reinterpret_cast<float4*>(tile + r * stride + c4 * 4) = __ldg(cp + c4);
+            }
+            __syncwarp();
+            if (lane < nb) {
+                const float* row = tile + lane * stride;
+                float acc = 0.0f;
+                for (uint32_t c4 = 0; c4 < n4; c4++) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+                    const float4 yv = *reinterpret_cast<const float4*>(ys + c4 * 4);
+                    acc = sq_step(acc, yv.x, v.x);
+                    acc = sq_step(acc, yv.y, v.y);
+                    acc = sq_step(acc, yv.z, v.z);
+                    acc = sq_step(acc, yv.w, v.w);
                 }
+                wsq[ids[b0 + lane]] = acc;
             }
-            for (; d4 < n4; d4++) {
-                const float4 v = __ldg(cp + d4);
-                const uint32_t d = d4 * 4;
-                acc = sq_step(acc, ys[d], v.x);
-                acc = sq_step(acc, ys[d + 1], v.y);
-                acc = sq_step(acc, ys[d + 2], v.z);
-                acc = sq_step(acc, ys[d + 3], v.w);
-            }
-            wsq[c] = acc;
+            __syncwarp();
         }
     } else {
         for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
@@ -746,8 +747,8 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
 // tau[row] = the L-th smallest chunk minimum (an upper bound on the row's
 // L-th smallest approximate value).
 // Y != null: the chunk minima came from the 1xTF32 pass, and tau is raised by
-// twice that pass's error bound so it also bounds the L-th smallest 3xTF32
-// value the filter pass compares against (at least L centroids pass).
+// both passes' error bounds so it also bounds the L-th smallest 3xTF32 value
+// the filter pass compares against (at least L centroids pass).
 __global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
                                                   uint32_t* __restrict__ scratch, float* __restrict__ tau,
                                                   const float* __restrict__ Y, uint32_t dim, float cmax) {
@@ -770,7 +771,9 @@ __global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin
         if (Y) {
             float yn = 0.0f;
             for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
-            t += 2.0f * tc_eps(yn, cmax, dim, false) * 1.01f;
+            // approx3 <= approx1 + eps1 + eps3: the L centroids under tau1
+            // (1xTF32) are all under tau1 + eps1 + eps3 (3xTF32)
+            t += (tc_eps(yn, cmax, dim, false) + tc_eps(yn, cmax, dim, true)) * 1.01f;
         }
         tau[q] = t;
     }
@@ -787,6 +790,7 @@ __global__ void k_refine_list(const float* __restrict__ Y, uint32_t dim, const f
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // pow2 >= cap
     float* ys = reinterpret_cast<float*>(smem + 8 * 2048);
+    float* tiles = ys + ((dim + 3) & ~3u);               // 8 warps x 16 rows x (dim + 4)
     __shared__ float s_yn;
     const uint64_t q = blockIdx.x;
     const uint32_t n = cnt[q];
@@ -799,16 +803,48 @@ __global__ void k_refine_list(const float* __restrict__ Y, uint32_t dim, const f
     for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
     __syncthreads();
     const uint32_t* cq = cand + q * cap;
-    for (uint32_t t = threadIdx.x; t < np2; t += blockDim.x) {
-        uint64_t key = ~0ull;
-        if (t < n) {
-            const uint32_t c = cq[t];
-            const float* cp = C + (uint64_t)c * dim;
-            float acc = 0.0f;
-            for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], cp[d]);
-            key = make_key(acc, c);
+    if ((dim & 3u) == 0 && dim <= 128) {
+        // rows staged through shared memory, 16 per warp (coalesced 16-byte
+        // loads), lanes 0..15 run the reference-order sqdist of one row each
+        const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+        const uint32_t n4 = dim >> 2, stride = dim + 4;
+        float* tile = tiles + (size_t)warp * 16 * stride;
+        for (uint32_t t = n + threadIdx.x; t < np2; t += blockDim.x) keys[t] = ~0ull;
+        for (uint32_t b0 = warp * 16; b0 < n; b0 += nwarps * 16) {
+            const uint32_t nb = min(16u, n - b0);
+            for (uint32_t r = 0; r < nb; r++) {
+                const float4* cp = reinterpret_cast<const float4*>(C + (uint64_t)cq[b0 + r] * dim);
+                for (uint32_t c4 = lane; c4 < n4; c4 += 32)
+                    *reinterpret_cast<float4*>(tile + r * stride + c4 * 4) = __ldg(cp + c4);
+            }
+            __syncwarp();
+            if (lane < nb) {
+                const float* row = tile + lane * stride;
+                float acc = 0.0f;
+                for (uint32_t c4 = 0; c4 < n4; c4++) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+                    const float4 yv = *reinterpret_cast<const float4*>(ys + c4 * 4);
+                    acc = sq_step(acc, yv.x, v.x);
+                    acc = sq_step(acc, yv.y, v.y);
+                    acc = sq_step(acc, yv.z, v.z);
+                    acc = sq_step(acc, yv.w, v.w);
+                }
+                keys[b0 + lane] = make_key(acc, cq[b0 + lane]);
+            }
+            __syncwarp();
         }
-        keys[t] = key;
+    } else {
+        for (uint32_t t = threadIdx.x; t < np2; t += blockDim.x) {
+            uint64_t key = ~0ull;
+            if (t < n) {
+                const uint32_t c = cq[t];
+                const float* cp = C + (uint64_t)c * dim;
+                float acc = 0.0f;
+                for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ys[d], cp[d]);
+                key = make_key(acc, c);
+            }
+            keys[t] = key;
+        }
     }
     if (threadIdx.x == 0) {
         float yn = 0.0f;
@@ -893,7 +929,9 @@ void launch_refine_first(const float* Y, uint64_t nq, uint32_t dim, const float*
 }
 
 size_t exact_needed_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t dim) {
-    return (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4 + (size_t)((dim + 3) & ~3u) * 4;
+    const size_t head = (size_t)((k + 31) / 32) * 4 + (size_t)w1 * (n + 1) * 4;
+    const size_t tiles = ((dim & 3u) == 0 && dim <= 128) ? (size_t)8 * 16 * (dim + 4) * 4 : 0;
+    return ((head + 15) & ~(size_t)15) + (size_t)((dim + 3) & ~3u) * 4 + tiles;
 }
 
 void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, uint32_t n,
@@ -917,7 +955,8 @@ void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* 
                         const uint32_t* cnt, uint32_t cap, const float* tau, uint32_t w1, float cmax, int split,
                         uint32_t* top, uint32_t* flagged, unsigned int* nflag, cudaStream_t st) {
     if (nq == 0) return;
-    const size_t smem = 8 * 2048 + (size_t)dim * 4;
+    const size_t tiles = ((dim & 3u) == 0 && dim <= 128) ? (size_t)8 * 16 * (dim + 4) * 4 : 0;
+    const size_t smem = 8 * 2048 + (size_t)((dim + 3) & ~3u) * 4 + tiles;
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_refine_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dev::k_refine_list<<<(unsigned)nq, 256, smem, st>>>(Y, dim, C, k, cand, cnt, cap, tau, w1, cmax, split, top,
                                                         flagged, nflag);

@@ -676,19 +676,6 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             a.eterm_lam = eterm_lam_.p;
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
-        if (cfg_.scan_l2_budget_mb > 0 && cfg_.scan_variant == 0) {
-            // L2 retention: the batch's most re-read cells stay (evict_last),
-            // single-visit cells stream through (evict_first)
-            const uint32_t ncell = k_ * n_;
-            visits_.alloc(ncell);
-            vhist_.alloc(256);
-            hot_t_.alloc(1);
-            launch_cell_visits(sel_.p, nt * w2, visits_.p, ncell, list_off_.p, m_ + 5,
-                               (uint64_t)cfg_.scan_l2_budget_mb << 20, vhist_.p, hot_t_.p, st);
-            a.cell_visits = visits_.p;
-            a.hot_threshold = hot_t_.p;
-            launches += 3;
-        }
         if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, cfg_.scan_slots, cfg_.scan_prefetch, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
@@ -725,7 +712,6 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;
     else if (key == "force_exact") cfg_.force_exact = (int)value;
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;
-    else if (key == "scan_l2_budget_mb") cfg_.scan_l2_budget_mb = (int)value;
     else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);

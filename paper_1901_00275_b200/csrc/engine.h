@@ -29,7 +29,6 @@ struct EngineConfig {
     int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
-    int scan_l2_budget_mb = 0;  // v6 scan: MB of the batch's most re-read cells loaded evict_last (0 = plain loads)
     int scan_packed = 1;   // v6 scan reads the packed e-term | lambda-byte stream (one load per entry)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
@@ -244,8 +243,6 @@ private:
     DevBuf<float> tmin_, tau_, ld_;
     DevBuf<float> xtc_, xlo_;  // query rows in the UMMA layout (persistent coarse kernels)
     DevBuf<float> xtc1_;       // unsplit copy for the 1xTF32 first pass
-    DevBuf<uint32_t> visits_, hot_t_;      // per-batch cell visit counts, L2-retention threshold
-    DevBuf<unsigned long long> vhist_;
     DevBuf<uint32_t> lcnt_, lidx_;
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;

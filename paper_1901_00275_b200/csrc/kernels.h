@@ -44,11 +44,6 @@ struct SearchArgs {
     unsigned int* error_flag;
     const float* Y;  // non-null: ws holds approximate (tensor-core) rows; second level
                      // recomputes neighbour distances exactly from the query vectors
-    // L2 retention (v6 scan): per-cell visit counts of the current batch and
-    // the threshold above which a cell's entries are loaded evict_last
-    // (re-read by other queries of the batch); null = plain loads
-    const uint32_t* cell_visits;
-    const uint32_t* hot_threshold;
     // v6 scan input stream: e-term with its low 8 mantissa bits replaced by the
     // entry's lambda byte (one 4-byte load per entry instead of 4 + 1);
     // e_pack_err bounds the e-term change (2^-15 Emax), added to the
@@ -80,11 +75,6 @@ void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, flo
 size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);
 void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,
                  bool fast, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st);
-// per-batch cell visit counts and the L2-retention threshold (budget bytes of
-// the most re-read cells' entries kept evict_last)
-void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, uint32_t ncell, const uint64_t* list_off,
-                        uint32_t bytes_per_entry, uint64_t budget, unsigned long long* hist, uint32_t* threshold,
-                        cudaStream_t st);
 // eterm_lam[e] = (bits(eterm[e]) & ~0xff) | lambdas[e]
 void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t n, uint32_t* out, cudaStream_t st);
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int slots,

@@ -389,77 +389,6 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 || U 
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
 }
 
-// L2-policy loads (ld.global.nc with an L2::cache_hint policy register)
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-    uint64_t pol;
-    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-template <int M>
-__device__ __forceinline__ void load_code_vec_pol(const uint8_t* __restrict__ p, uint32_t (&w)[(M + 3) / 4],
-                                                  uint64_t pol) {
-    if constexpr (M == 16) {
-        asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-                     : "l"(p), "l"(pol));
-    } else if constexpr (M == 8) {
-        asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(w[0]), "=r"(w[1]) : "l"(p), "l"(pol));
-    } else if constexpr (M == 4) {
-        asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(w[0]) : "l"(p), "l"(pol));
-    } else {
-        load_code_vec<M>(p, w);
-    }
-}
-
-__device__ __forceinline__ uint32_t ld_u8_pol(const uint8_t* p, uint64_t pol) {
-    uint16_t v;
-    asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ float ld_f32_pol(const float* p, uint64_t pol) {
-    float v;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
-// Batch cell visit counts (how many queries of this batch scan each cell)
-__global__ void k_cell_visits(const uint32_t* __restrict__ sel, uint64_t nsel, uint32_t* __restrict__ visits) {
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nsel; t += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(&visits[sel[t]], 1u);
-}
-
-// bytes of entries by visit count (capped at 255), re-read cells only
-__global__ void k_visit_bytes(const uint32_t* __restrict__ visits, uint32_t ncell, const uint64_t* __restrict__ off,
-                              uint32_t bpe, unsigned long long* __restrict__ hist) {
-    __shared__ unsigned long long h[256];
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
-    __syncthreads();
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
-        const uint32_t v = visits[c];
-        if (v >= 2) atomicAdd(&h[min(v, 255u)], (unsigned long long)(off[c + 1] - off[c]) * bpe);
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
-        if (h[i]) atomicAdd(&hist[i], h[i]);
-}
-
-// smallest visit count T >= 2 whose cells (visits >= T) fit the budget
-__global__ void k_pick_threshold(const unsigned long long* __restrict__ hist, uint64_t budget,
-                                 uint32_t* __restrict__ threshold) {
-    if (threadIdx.x != 0) return;
-    unsigned long long acc = 0;
-    uint32_t T = 0xffffffffu;
-    for (int v = 255; v >= 2; v--) {
-        acc += hist[v];
-        if (acc > budget) break;
-        T = (uint32_t)v;
-    }
-    *threshold = T;
-}
-
 __global__ void k_pack_eterm_lam(const float* __restrict__ eterm, const uint8_t* __restrict__ lambdas, uint64_t n,
                                  uint32_t* __restrict__ out) {
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
@@ -564,10 +493,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     uint32_t loaded_t = 0xffffffffu;
     const bool packed = a.eterm_lam != nullptr;
     const uint32_t* el_c = nullptr;
-    const bool hinted = a.cell_visits != nullptr;
-    const uint32_t hot_t = hinted ? *a.hot_threshold : 0xffffffffu;
-    const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
-    uint64_t pol = pol_stream;
 
     auto locate = [&](uint32_t g) {  // walks t forward to the cell holding chunk g
         while (cpref[t + 1] <= g) t++;
@@ -588,7 +513,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             lam_c = a.lambdas + b0;
             e_c = a.eterm + b0;
             if (packed) el_c = a.eterm_lam + b0;
-            if (hinted) pol = a.cell_visits[cell] >= hot_t ? pol_keep : pol_stream;
         }
         return (g - cpref[t]) * CH;
     };
@@ -626,14 +550,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                 for (int u = 0; u < U; u++) {
                     lb[u] = le[u] & 0xffu;
                     ev[u] = __uint_as_float(le[u] & ~0xffu);
-                }
-            } else if (hinted) {
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const uint32_t ic = min(o + u * 32 + lane, L - 1);
-                    load_code_vec_pol<M>(codes_c + (size_t)ic * M, cw[u], pol);
-                    lb[u] = ld_u8_pol(lam_c + ic, pol);
-                    ev[u] = ld_f32_pol(e_c + ic, pol);
                 }
             } else {
 #pragma unroll
@@ -760,18 +676,6 @@ static void launch_fast_t(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_
     if (R == 0 && su == 6) launch_fast_u<M, R, 6>(a, nq, w2, keep, st);
     else if (R == 0 && su == 8) launch_fast_u<M, R, 8>(a, nq, w2, keep, st);
     else launch_fast_u<M, R, 4>(a, nq, w2, keep, st);
-}
-
-void launch_cell_visits(const uint32_t* sel, uint64_t nsel, uint32_t* visits, uint32_t ncell, const uint64_t* list_off,
-                        uint32_t bytes_per_entry, uint64_t budget, unsigned long long* hist, uint32_t* threshold,
-                        cudaStream_t st) {
-    CUDA_CHECK(cudaMemsetAsync(visits, 0, (size_t)ncell * 4, st));
-    CUDA_CHECK(cudaMemsetAsync(hist, 0, 256 * 8, st));
-    if (nsel) dev::k_cell_visits<<<(unsigned)dev::umin64((nsel + 255) / 256, 4736), 256, 0, st>>>(sel, nsel, visits);
-    dev::k_visit_bytes<<<(unsigned)dev::umin64(((uint64_t)ncell + 255) / 256, 1184), 256, 0, st>>>(
-        visits, ncell, list_off, bytes_per_entry, hist);
-    dev::k_pick_threshold<<<1, 32, 0, st>>>(hist, budget, threshold);
-    CUDA_LAUNCH_CHECK();
 }
 
 void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t n, uint32_t* out, cudaStream_t st) {

@@ -43,6 +43,18 @@ def merge_topk(ids, dists, stream: int | None = None):
     return out_i, out_d
 
 
+def _all_gather(out, inp, group=None):
+    """all_gather_into_tensor; CUDA tensors go through host copies when the
+    backend cannot take them (gloo: the single-GPU rehearsal of N > 1)."""
+    import torch.distributed as dist
+    if inp.is_cuda and dist.get_backend(group) != "nccl":
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
 def gather_parts(local_ids, local_dists, group=None):
     """All-gathers every rank's [nq, k] result block into [world, nq, k]."""
     import torch
@@ -52,8 +64,8 @@ def gather_parts(local_ids, local_dists, group=None):
     # concatenated along dim 0 (the layout every backend accepts), viewed [world, nq, k]
     gi = torch.empty((world * nq,) + tuple(local_ids.shape[1:]), dtype=local_ids.dtype, device=local_ids.device)
     gd = torch.empty((world * nq,) + tuple(local_dists.shape[1:]), dtype=local_dists.dtype, device=local_dists.device)
-    dist.all_gather_into_tensor(gi, local_ids.contiguous(), group=group)
-    dist.all_gather_into_tensor(gd, local_dists.contiguous(), group=group)
+    _all_gather(gi, local_ids.contiguous(), group)
+    _all_gather(gd, local_dists.contiguous(), group)
     return gi.view((world,) + tuple(local_ids.shape)), gd.view((world,) + tuple(local_dists.shape))
 
 
@@ -75,7 +87,7 @@ def gather_top(local_top, nq: int, w1: int, group=None):
     send = torch.zeros((per, w1), dtype=local_top.dtype, device=local_top.device)
     send[:local_top.shape[0]] = local_top
     out = torch.empty((world * per, w1), dtype=local_top.dtype, device=local_top.device)
-    dist.all_gather_into_tensor(out, send, group=group)
+    _all_gather(out, send, group)
     return out[:nq]
 
 

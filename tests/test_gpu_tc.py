@@ -125,12 +125,12 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
     path = str(tmp_path / f"d{dim}.vlq")
     idx.save(path)
     o = oracle_mod.OracleIndex.load(path)
-    # persistent / per-row-block coarse grids; plain vs L2-retention-hinted scan loads
-    variants = [dict(tc_persist=1), dict(tc_persist=0), dict(scan_l2_budget_mb=1), dict(tc_pass1_single=1),
+    # persistent / per-row-block coarse grids, 1xTF32 first pass, scan variants
+    variants = [dict(tc_persist=1), dict(tc_persist=0), dict(tc_pass1_single=1),
                 dict(tc_pass1_single=1, tc_persist=0), dict(scan_variant=4), dict(scan_prefetch=1),
                 dict(scan_packed=0)]
     for v in variants:
-        knobs = dict(tc_persist=1, scan_l2_budget_mb=0, tc_pass1_single=0, scan_variant=0, scan_prefetch=0,
+        knobs = dict(tc_persist=1, tc_pass1_single=0, scan_variant=0, scan_prefetch=0,
                      scan_packed=1)
         knobs.update(v)
         for key, val in knobs.items():
