@@ -113,7 +113,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-constexpr int TC_MAX_STAGES = 3;  // centroid-tile ring depth: as many as fit in 227 KB, 2 or 3
+constexpr int TC_MAX_STAGES = 4;  // centroid-tile ring depth: as many as fit in 227 KB, 2 to 4
 // (a template parameter: a runtime ring depth made nvcc 12.9 drop the high
 // half of the bulk-copy source address in the producer loop)
 
@@ -148,13 +148,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     static_assert(!PERSIST || MODE != 0, "ARGMIN merges per row block: not persistent");
     constexpr int TN = SPLIT ? 64 : TC_N;  // centroids per tile (UMMA N)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t tile_bytes = TN * dim * 4;  // one centroid tile (one precision half)
+    const uint32_t tile_bytes = TN * dim * 4;  // one centroid tile (one precision)
     const uint32_t a_bytes = TC_M * dim * 4;
     unsigned char* sA = smem;
     unsigned char* sAlo = smem + a_bytes;  // SPLIT only
     constexpr int NB = SPLIT ? 2 : 1;
-    unsigned char* sB = smem + a_bytes * NB;                              // STAGES x NB x tile_bytes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + TC_STAGES * NB * tile_bytes);
+    // Ring stage = tile_bytes.  1xTF32: one whole centroid tile.  3xTF32: one
+    // K half of a tile, hi and lo halves side by side (the centroids are laid
+    // out as [tile][K half][row/8][k/4][row%8][4], k_relayout_khalf), so twice
+    // as many stages are in flight and D = 128 fits beside its 128 KB A tile.
+    const uint32_t half_bytes = tile_bytes / 2;
+    unsigned char* sB = smem + a_bytes * NB;                              // STAGES x tile_bytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + TC_STAGES * tile_bytes);
     uint64_t* full = bars;                   // [STAGES]
     uint64_t* empty = bars + TC_STAGES;      // [STAGES]
     uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]
@@ -233,12 +238,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         aloads++;
                     }
                 }
-                const uint32_t s = i % TC_STAGES, ph = (i / TC_STAGES) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], NB * tile_bytes);
-                bulk_g2s_any(sB + s * NB * tile_bytes, cent_tc + (size_t)t * TN * dim, tile_bytes, &full[s]);
-                if constexpr (SPLIT)
-                    bulk_g2s_any(sB + (s * NB + 1) * tile_bytes, cent_lo + (size_t)t * TN * dim, tile_bytes, &full[s]);
+                if constexpr (SPLIT) {
+                    for (uint32_t h = 0; h < 2; h++) {
+                        const uint32_t i2 = 2 * i + h;
+                        const uint32_t s = i2 % TC_STAGES, ph = (i2 / TC_STAGES) & 1u;
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        mbar_expect_tx(&full[s], tile_bytes);
+                        const size_t src = ((size_t)t * 2 + h) * (TN * dim / 2);
+                        bulk_g2s_any(sB + s * tile_bytes, cent_tc + src, half_bytes, &full[s]);
+                        bulk_g2s_any(sB + s * tile_bytes + half_bytes, cent_lo + src, half_bytes, &full[s]);
+                    }
+                } else {
+                    const uint32_t s = i % TC_STAGES, ph = (i / TC_STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_expect_tx(&full[s], tile_bytes);
+                    bulk_g2s_any(sB + s * tile_bytes, cent_tc + (size_t)t * TN * dim, tile_bytes, &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -260,28 +275,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     aloads++;
                 }
             }
-            const uint32_t s = i % TC_STAGES, ph = (i / TC_STAGES) & 1u;
             const uint32_t b = i & 1u, bph = (i >> 1) & 1u;
             mbar_wait(&tempty[b], bph ^ 1u);
-            mbar_wait(&full[s], ph);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
-                const uint32_t b_addr = smem_u32(sB + s * NB * tile_bytes);
-                for (uint32_t k = 0; k < dim / 8; k++) {  // K = 8 tf32 per MMA = two 16-B chunks
-                    const uint64_t ad = umma_desc(a_addr + k * 256, lbo, sbo);
-                    const uint64_t bd = umma_desc(b_addr + k * 256, lbo, sbo);
-                    umma_tf32(tmem_base + b * TN, ad, bd, idesc, k > 0 ? 1u : 0u);
-                    if constexpr (SPLIT) {
-                        const uint64_t bl = umma_desc(b_addr + tile_bytes + k * 256, lbo, sbo);
-                        const uint64_t al = umma_desc(smem_u32(sAlo) + k * 256, lbo, sbo);
-                        umma_tf32(tmem_base + b * TN, ad, bl, idesc, 1u);  // hi . lo
-                        umma_tf32(tmem_base + b * TN, al, bd, idesc, 1u);  // lo . hi
+            if constexpr (SPLIT) {
+                const uint32_t sbo_b = (nchunk / 2) * 128;  // row-group stride inside a K half
+                const uint32_t kh = dim / 16;               // MMAs (K = 8) per K half
+                for (uint32_t h = 0; h < 2; h++) {
+                    const uint32_t i2 = 2 * i + h;
+                    const uint32_t s = i2 % TC_STAGES, ph = (i2 / TC_STAGES) & 1u;
+                    mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (lane == 0) {
+                        const uint32_t b_addr = smem_u32(sB + s * tile_bytes);
+                        for (uint32_t kk = 0; kk < kh; kk++) {
+                            const uint32_t k = h * kh + kk;
+                            const uint64_t ad = umma_desc(a_addr + k * 256, lbo, sbo);
+                            const uint64_t al = umma_desc(smem_u32(sAlo) + k * 256, lbo, sbo);
+                            const uint64_t bd = umma_desc(b_addr + kk * 256, lbo, sbo_b);
+                            const uint64_t bl = umma_desc(b_addr + half_bytes + kk * 256, lbo, sbo_b);
+                            umma_tf32(tmem_base + b * TN, ad, bd, idesc, k > 0 ? 1u : 0u);  // hi . hi
+                            umma_tf32(tmem_base + b * TN, ad, bl, idesc, 1u);               // hi . lo
+                            umma_tf32(tmem_base + b * TN, al, bd, idesc, 1u);               // lo . hi
+                        }
+                        umma_commit(&empty[s]);
+                        if (h == 1) umma_commit(&tfull[b]);
                     }
+                    __syncwarp();
                 }
-                umma_commit(&empty[s]);
-                umma_commit(&tfull[b]);
+            } else {
+                const uint32_t s = i % TC_STAGES, ph = (i / TC_STAGES) & 1u;
+                mbar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t b_addr = smem_u32(sB + s * tile_bytes);
+                    for (uint32_t k = 0; k < dim / 8; k++) {  // K = 8 tf32 per MMA = two 16-B chunks
+                        const uint64_t ad = umma_desc(a_addr + k * 256, lbo, sbo);
+                        const uint64_t bd = umma_desc(b_addr + k * 256, lbo, sbo);
+                        umma_tf32(tmem_base + b * TN, ad, bd, idesc, k > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                    umma_commit(&tfull[b]);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else {
         // ---------------- epilogue warps 2..9
@@ -433,13 +469,41 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
     }
 }
 
+// Split (3xTF32) copy of the centroids for the search coarse stage: hi =
+// tf32(x), lo = x - hi, laid out per 64-centroid tile and K half as
+// [tile][h][row/8][k/4 within the half][row%8][4] (one bulk copy per half).
+__global__ void k_relayout_khalf(const float* __restrict__ C, uint32_t k, uint32_t dim, uint32_t ntiles,
+                                 float* __restrict__ out_hi, float* __restrict__ out_lo) {
+    const uint32_t nchunk = dim / 4, hc = nchunk / 2;
+    const uint64_t total = (uint64_t)ntiles * 64 * nchunk;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t row = t / nchunk;
+        const uint32_t c = (uint32_t)(t % nchunk);
+        const uint32_t tile = (uint32_t)(row / 64), r = (uint32_t)(row % 64);
+        const uint32_t h = c / hc, cc = c % hc;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < k) v = reinterpret_cast<const float4*>(C + row * dim)[c];
+        const uint64_t off = ((uint64_t)tile * 2 + h) * (64 * dim / 2) + (r >> 3) * (hc * 32) + cc * 32 + (r & 7) * 4;
+        const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+        *reinterpret_cast<float4*>(out_hi + off) = hi;
+        *reinterpret_cast<float4*>(out_lo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+    }
+}
+
 }  // namespace dev
+
+void launch_relayout_khalf(const float* C, uint32_t k, uint32_t dim, float* out_hi, float* out_lo, cudaStream_t st) {
+    const uint32_t ntiles = (k + 63) / 64;
+    dev::k_relayout_khalf<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out_hi, out_lo);
+    CUDA_LAUNCH_CHECK();
+}
 
 static size_t coarse_tc_smem_at(uint32_t dim, int mode, bool split, uint32_t stages) {
     const size_t tail = mode == 1 ? (size_t)8 * 32 * 33 * 4 : (size_t)dev::TC_M * 8 * 4;
     const size_t tn = split ? 64 : dev::TC_N, nb = split ? 2 : 1;
-    return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * nb * tn * dim * 4 + 2 * stages * 8 + 6 * 8 + 16 +
-           tail + 256;
+    // stage = one tile (1xTF32) or one K half of a tile in hi + lo (3xTF32): tn * dim * 4 either way
+    return (size_t)dev::TC_M * dim * 4 * nb + (size_t)stages * tn * dim * 4 + 2 * stages * 8 + 6 * 8 + 16 + tail +
+           256;
 }
 
 // deepest centroid-tile ring (<= TC_MAX_STAGES) that fits 227 KB; 0 if not even 2
@@ -449,10 +513,10 @@ static uint32_t coarse_tc_stages(uint32_t dim, int mode, bool split) {
     return 0;
 }
 
-// every epilogue mode the engine may launch (add: 0; search: 1, 2, 3)
+// every epilogue mode the engine may launch (add: 0 unsplit; search: 1, 2, 3)
 static bool coarse_tc_fits(uint32_t dim, bool split) {
-    if (dim % 8 != 0 || dim < 8) return false;
-    for (int mode = 0; mode < 4; mode++)
+    if (dim % (split ? 16u : 8u) != 0 || dim < 8) return false;  // K = 8 per MMA; split: two K halves
+    for (int mode = split ? 1 : 0; mode < 4; mode++)
         if (coarse_tc_stages(dim, mode, split) == 0) return false;
     return true;
 }
@@ -494,8 +558,9 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
     }
 #define VLQ_TC_LAUNCH(MODE_, SPLIT_, PERSIST_)                                                                   \
     do {                                                                                                         \
-        auto fn = stages == 3 ? dev::k_coarse_tc<MODE_, SPLIT_, 3, PERSIST_>                                     \
-                              : dev::k_coarse_tc<MODE_, SPLIT_, 2, PERSIST_>;                                    \
+        auto fn = stages == 4   ? dev::k_coarse_tc<MODE_, SPLIT_, 4, PERSIST_>                                   \
+                  : stages == 3 ? dev::k_coarse_tc<MODE_, SPLIT_, 3, PERSIST_>                                   \
+                                : dev::k_coarse_tc<MODE_, SPLIT_, 2, PERSIST_>;                                  \
         CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));           \
         fn<<<grid, dev::TC_THREADS, smem, st>>>(X, nx, dim, cent_tc, cent_lo, cnorm, ntiles, k, out_row, ldo,    \
                                                 top_idx, top_d, tau, cnt, cap, Xtc, Xlo_tc, nrb);                \

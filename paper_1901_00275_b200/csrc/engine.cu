@@ -185,7 +185,7 @@ void Engine::upload_model() {
         if (tc_split_) {
             cent_hi_.alloc((size_t)ntiles * 128 * dim_);
             cent_lo_.alloc((size_t)ntiles * 128 * dim_);
-            launch_relayout_centroids(centroids_.p, k_, dim_, cent_hi_.p, cent_lo_.p, cnorm_tc_.p, stream_);
+            launch_relayout_khalf(centroids_.p, k_, dim_, cent_hi_.p, cent_lo_.p, stream_);
         }
         double mx = 0.0;
         for (uint32_t i = 0; i < k_; i++) {
