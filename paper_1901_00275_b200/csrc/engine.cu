@@ -498,7 +498,7 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
     if (nq == 0) return;
     DeviceGuard g(cfg_.device);
     const uint32_t w2 = w2_of(w1, alpha, n_);
-    const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+    const uint32_t keep = scan_keep(topk);
     const uint64_t per_q = 4ull * k_ + 8ull * w1 + 128 + 4ull * w1 * n_ + 4ull * w2 + 4ull * VLQ_KSUB * m_ + 8ull * keep +
                            sizeof(QueryMeta) + 4;
     uint64_t tile = std::max<uint64_t>(1, cfg_.workspace_bytes / per_q);
@@ -670,9 +670,9 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     const uint32_t warps_x = std::min<uint32_t>(8, std::max<uint32_t>(1, 8192 / buf_x));
     const bool fast = !cfg_.force_exact && topk > 0 && topk <= 768;
     if (fast) {
-        const uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+        const uint32_t keep = scan_keep(topk);
         mark(PH_SCAN);
-        if (cfg_.scan_packed && cfg_.scan_variant == 0 && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
+        if (cfg_.scan_packed && (cfg_.scan_variant == 0 || (cfg_.scan_variant >= 5 && cfg_.scan_variant <= 9)) && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
             a.eterm_lam = eterm_lam_.p;
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
@@ -705,6 +705,14 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     return fast;
 }
 
+// fast-scan survivors per query (k'): the smallest power of two >= k + max(16, k/4),
+// at least scan_keep_min (a study knob), at most 512 (the fast scan's limit)
+uint32_t Engine::scan_keep(uint32_t topk) const {
+    uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+    if (cfg_.scan_keep_min > keep) keep = std::min<uint32_t>(512, next_pow2(cfg_.scan_keep_min));
+    return keep;
+}
+
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
@@ -714,6 +722,7 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;
     else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
+    else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 

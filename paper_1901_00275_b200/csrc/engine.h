@@ -29,6 +29,7 @@ struct EngineConfig {
     int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
+    uint32_t scan_keep_min = 0;  // study knob: lower bound on k' (fast-scan survivors)
     int scan_packed = 1;   // v6 scan reads the packed e-term | lambda-byte stream (one load per entry)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
     uint32_t tc_min_k = 1024;         // add-path assignment on tensor cores for K >= this (env VLQ_TC_MIN_K)
@@ -109,7 +110,9 @@ struct DevBuf {
         if (count <= n && p) return;
         reset();
         if (count == 0) return;
-        CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        // 64 bytes of slack: the staged scan's bulk copies round their sizes up
+        // to 16 bytes and may read up to 15 bytes past the last entry
+        CUDA_CHECK(cudaMalloc(&p, count * sizeof(T) + 64));
         n = count;
     }
     T* get() const { return p; }
@@ -200,6 +203,7 @@ public:
     void set_profiling(bool on);
     // study knobs (scan_variant, scan_slots, use_tc_search): take effect on the next search
     void set_tuning(const std::string& key, int64_t value);
+    uint32_t scan_keep(uint32_t topk) const;
     const EngineStats& stats();  // folds in the pending per-tile profile (syncs on its events)
     void reset_stats();
 

@@ -13,7 +13,7 @@ struct QueryMeta {
     float dmax;                  // bound on |term1| over the query's selected cells
     float s5max;                 // bound on |sum5|
     uint32_t flag;               // 1: certificate failed -> exact fallback
-    uint32_t pad;
+    float qerr;                  // bound on |fast - exact| added by a quantized scan LUT (0 otherwise)
 };
 
 // Device views used by the search kernels (all pointers device-resident).

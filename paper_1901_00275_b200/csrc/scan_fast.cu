@@ -18,7 +18,10 @@
 // as C_p interleaved copies (word (j*C_p + c) for copy c); lane l reads copy
 // (l mod C_p), so lane groups hit disjoint bank sets.  C_p = 16 gives exactly
 // 2 wavefronts, 32 gives 1.  The copy budget per M fills <= 160 KB of smem.
+#include <algorithm>
 #include <cstdlib>
+
+#include "async.cuh"
 
 #include "kernels.h"
 #include "select.cuh"
@@ -405,9 +408,14 @@ __global__ void k_pack_eterm_lam(const float* __restrict__ eterm, const uint8_t*
 // clamped index (no zero-fill moves), and the threshold test is one float
 // compare against the threshold key's distance; the exact 64-bit
 // (dist, position) key is formed only for entries that pass it.
+// LUT[p][code_p]: the byte is extracted with one LOP3 / PRMT / SHF and the
+// shared load scales it (LDS [R.X4 + imm]), so a lookup is 2 instructions
 template <int M>
 __device__ __forceinline__ float lut_at(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], int p) {
-    return *reinterpret_cast<const float*>(lut + 4 * 256 * p + lut_index<0>(w[p >> 2], p & 3, 0u));
+    const uint32_t word = w[p >> 2];
+    const int k = p & 3;
+    const uint32_t b = k == 0 ? (word & 0xffu) : (k == 3 ? (word >> 24) : __byte_perm(word, 0u, 0x4440u + k));
+    return reinterpret_cast<const float*>(lut)[p * 256 + b];
 }
 
 __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an order-preserving key (upper 32 bits)
@@ -423,7 +431,20 @@ __device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes, u
         asm volatile("prefetch.global.L2 [%0];" ::"l"(x));
 }
 
-template <int M, int U, int MINB>
+// Q8: the query's term5 table is quantized to u8 in shared memory (one scale
+// for all sub-spaces, a per-sub-space offset), so a lookup is one PRMT and one
+// LDS.U8, the m-term sum is exact integer arithmetic and the table is 4x
+// smaller (fewer bank conflicts).  The quantization error (at most half a step
+// per term) is written to meta[q].qerr and added to the re-score certificate.
+template <int M>
+__device__ __forceinline__ uint32_t lut8_at(const unsigned char* lq, const uint32_t (&w)[(M + 3) / 4], int p) {
+    const uint32_t word = w[p >> 2];
+    const int k = p & 3;
+    const uint32_t b = k == 0 ? (word & 0xffu) : (k == 3 ? (word >> 24) : __byte_perm(word, 0u, 0x4440u + k));
+    return lq[p * 256 + b];
+}
+
+template <int M, int U, int MINB, bool Q8 = false>
 __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap,
                                                           uint32_t pf) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
@@ -434,16 +455,63 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t q = blockIdx.x;
     unsigned char* lut = smem;
-    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + 4 * 256 * M);  // cap keys
+    constexpr uint32_t LUT_B = (Q8 ? 1 : 4) * 256 * M;
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + LUT_B);        // cap keys
     uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);         // w2 + 1
     __shared__ uint32_t hist[256];
     __shared__ unsigned int s_misc[48];
     __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
+    __shared__ float s_qmin[Q8 ? M : 1], s_qrng[Q8 ? M : 1];
 
     // 1. the query's term5 table (one copy per sub-space)
     const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
-    for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    float2 qs2 = make_float2(0.f, 0.f), qc2 = qs2;  // Q8: dist = qs * isum + (te + qc)
+    if constexpr (!Q8) {
+        for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    } else {
+        const float* t5f = a.t5 + q * M * VLQ_KSUB;
+        for (uint32_t p = warp; p < (uint32_t)M; p += nwarps) {  // per-sub-space range
+            float mn = __int_as_float(0x7f800000), mx = -mn;
+            for (uint32_t j = lane; j < VLQ_KSUB; j += 32) {
+                const float v = __ldg(t5f + p * VLQ_KSUB + j);
+                mn = fminf(mn, v);
+                mx = fmaxf(mx, v);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if (lane == 0) {
+                s_qmin[p] = mn;
+                s_qrng[p] = mx - mn;
+            }
+        }
+        __syncthreads();
+        float rng = 0.0f, smin = 0.0f, sabs = 0.0f;
+#pragma unroll
+        for (int p = 0; p < M; p++) {
+            rng = fmaxf(rng, s_qrng[p]);
+            smin += s_qmin[p];
+            sabs += fabsf(s_qmin[p]);
+        }
+        const float scale = rng > 0.0f ? rng / 255.0f : 1.0f;
+        const float inv = 1.0f / scale;
+        for (uint32_t i = threadIdx.x; i < 256u * M; i += blockDim.x) {
+            const float v = __ldg(t5f + i);
+            const int qv = __float2int_rn((v - s_qmin[i >> 8]) * inv);
+            lut[i] = (unsigned char)min(255, max(0, qv));
+        }
+        qs2 = make_float2(-2.0f * scale, -2.0f * scale);
+        qc2 = make_float2(-2.0f * smin, -2.0f * smin);
+        if (threadIdx.x == 0) {
+            // |sum5_q8 - sum5| <= M * (scale / 2) (+ the rounding of the step
+            // computation); the affine reconstruction adds a few ulps of
+            // |smin| + the largest integer sum: bound both generously
+            const float span = sabs + scale * 255.0f * M;
+            a.meta[q].qerr = 2.0f * (0.5f * M * scale * 1.001f) + 1e-5f * span;
+        }
+    }
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
     {
@@ -571,11 +639,22 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                     const float2 lam = __ffma2_rn(make_float2((float)lb[u], (float)lb[u + 1]), delta2, lam02);
                     const float2 t1 = __ffma2_rn(lam, __ffma2_rn(lam, cv2, Bc2), av2);
                     const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
-                    float2 s = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
+                    float2 d;
+                    if constexpr (Q8) {
+                        uint32_t i0 = 0, i1 = 0;
 #pragma unroll
-                    for (int p = 1; p < M; p++)
-                        s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
-                    const float2 d = __ffma2_rn(m2, s, te);
+                        for (int p = 0; p < M; p++) {
+                            i0 += lut8_at<M>(lut, cw[u], p);
+                            i1 += lut8_at<M>(lut, cw[u + 1], p);
+                        }
+                        d = __ffma2_rn(qs2, make_float2((float)i0, (float)i1), __fadd2_rn(te, qc2));
+                    } else {
+                        float2 s = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
+#pragma unroll
+                        for (int p = 1; p < M; p++)
+                            s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
+                        d = __ffma2_rn(m2, s, te);
+                    }
                     dist[u] = d.x;
                     dist[u + 1] = d.y;
                 }
@@ -658,7 +737,302 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
 }
 
+// v7: the v6 arithmetic and candidate handling, with the entry stream staged
+// into shared memory by the bulk-async copy engine instead of per-lane LDGs.
+// Every warp owns a ring of NS stages (one chunk of 32 U entries each: the
+// codes and the packed e-term | lambda words, both contiguous in HBM since a
+// chunk never straddles a cell).  Lane 0 issues `cp.async.bulk` for chunk
+// g + NS as soon as chunk g is consumed, so each warp keeps NS - 1 chunks in
+// flight while it computes; consumers wait on the stage's mbarrier and read
+// the entries with conflict-free LDS.  The per-cell parameters (list position
+// and length, A = a, B = (b - a) - c, C = c) are computed once per query in the
+// prologue, so the loop issues no dependent global loads at cell changes.
+template <int M>
+__device__ __forceinline__ void load_code_smem(const unsigned char* p, uint32_t (&w)[(M + 3) / 4]) {
+    if constexpr (M == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        w[0] = v.x;
+        w[1] = v.y;
+        w[2] = v.z;
+        w[3] = v.w;
+    } else if constexpr (M == 8) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        w[0] = v.x;
+        w[1] = v.y;
+    } else {
+        static_assert(M == 4, "bulk scan: m in {4, 8, 16}");
+        w[0] = *reinterpret_cast<const uint32_t*>(p);
+    }
+}
+
+template <int M, int U>
+struct BulkPlan {
+    static constexpr uint32_t CH = 32 * U;
+    static constexpr uint32_t CODE_B = CH * M + 16;  // + the 16-byte alignment slack of the source
+    static constexpr uint32_t EL_B = CH * 4 + 16;
+    static constexpr uint32_t STAGE_B = CODE_B + EL_B;
+    static_assert(STAGE_B % 16 == 0, "stages stay 16-byte aligned");
+};
+
+template <int M, int U, int NS>
+__host__ __device__ constexpr size_t bulk_smem_bytes(uint32_t w2, uint32_t cap) {
+    return 4 * 256 * (size_t)M + 8 * (size_t)NS * (BulkPlan<M, U>::STAGE_B + 16 + 8) + (size_t)cap * 8 +
+           (size_t)w2 * 24 + ((size_t)w2 + 1) * 4;
+}
+
+template <int M, int U, int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
+    static_assert(U % 2 == 0, "entries are processed in pairs");
+    using P = BulkPlan<M, U>;
+    constexpr uint32_t CH = P::CH;
+    constexpr int NW = (M + 3) / 4;
+    constexpr uint32_t NWARPS = 8;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t q = blockIdx.x;
+    unsigned char* lut = smem;
+    unsigned char* ring = smem + 4 * 256 * M;                                       // [warp][stage]
+    uint4* smeta = reinterpret_cast<uint4*>(ring + NWARPS * NS * P::STAGE_B);       // [warp][stage]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smeta + NWARPS * NS);              // [warp][stage]
+    uint64_t* cbuf = bars + NWARPS * NS;                                            // cap keys
+    float4* cpar = reinterpret_cast<float4*>(cbuf + cap);                           // [w2] (A, B, C, -)
+    uint2* cpos = reinterpret_cast<uint2*>(cpar + w2);                              // [w2] (position, length)
+    uint32_t* cpref = reinterpret_cast<uint32_t*>(cpos + w2);                       // [w2 + 1] chunk prefix
+    __shared__ uint32_t hist[256];
+    __shared__ unsigned int s_misc[48];
+    __shared__ unsigned int s_count;
+    __shared__ unsigned long long s_tau;
+
+    // 1. the query's term5 table (one copy per sub-space)
+    const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
+    for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    // 2. per-cell parameters and the chunk prefix (chunks never straddle cells)
+    const uint32_t* selq = a.sel + q * w2;
+    const float* wsq = a.ws + q * a.k;
+    {
+        const uint32_t per = (w2 + blockDim.x - 1) / blockDim.x;
+        uint32_t local = 0;
+        for (uint32_t t = threadIdx.x * per; t < min(w2, (threadIdx.x + 1) * per); t++) {
+            const uint32_t c = selq[t];
+            const uint64_t b0 = a.list_off[c];
+            const uint32_t len = (uint32_t)(a.list_off[c + 1] - b0);
+            const float av = wsq[c / a.n];
+            const float bv = wsq[a.nbr[c]];
+            const float cv = a.elen[c];
+            cpar[t] = make_float4(av, (bv - av) - cv, cv, 0.0f);
+            cpos[t] = make_uint2((uint32_t)b0, len);
+            cpref[t] = (len + CH - 1) / CH;
+            local += cpref[t];
+        }
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, s_misc + 8, &total);
+        for (uint32_t t = threadIdx.x * per; t < min(w2, (threadIdx.x + 1) * per); t++) {
+            const uint32_t c = cpref[t];
+            cpref[t] = run;
+            run += c;
+        }
+        if (threadIdx.x == 0) {
+            cpref[w2] = total;
+            s_count = 0;
+            s_tau = ~0ull;
+        }
+        if (lane == 0) {
+            for (int s = 0; s < NS; s++) mbar_init(&bars[warp * NS + s], 1);
+            mbar_fence_init();
+        }
+    }
+    __syncthreads();
+    const uint32_t nchunks = cpref[w2];
+    const uint32_t c_lo = (uint32_t)(((uint64_t)nchunks * warp) / NWARPS);
+    const uint32_t c_hi = (uint32_t)(((uint64_t)nchunks * (warp + 1)) / NWARPS);
+    const uint32_t my_total = c_hi - c_lo;
+    uint32_t tp = 0;  // producer cursor: cell of the next chunk to stage
+    {
+        uint32_t lo = 0, hi = w2;  // largest t with cpref[t] <= c_lo
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cpref[mid] <= c_lo) lo = mid;
+            else hi = mid;
+        }
+        tp = lo;
+    }
+    unsigned char* wring = ring + warp * NS * P::STAGE_B;
+    uint4* wmeta = smeta + warp * NS;
+    uint64_t* wbar = bars + warp * NS;
+    // lane 0: stage chunk (c_lo + d) into slot d % NS
+    auto fill = [&](uint32_t d) {
+        const uint32_t g = c_lo + d, s = d % NS;
+        while (cpref[tp + 1] <= g) tp++;
+        const uint2 cp = cpos[tp];
+        const uint32_t o = (g - cpref[tp]) * CH;
+        const uint32_t n = min(CH, cp.y - o);
+        const uint32_t pos = cp.x + o;
+        const uint64_t cb = (uint64_t)pos * M;                     // code bytes: align the source down to 16
+        const uint32_t csh = (uint32_t)(cb & 15u);
+        const uint32_t cbytes = (csh + n * M + 15u) & ~15u;
+        const uint32_t esh = pos & 3u;                             // packed words: 4 per 16 bytes
+        const uint32_t ebytes = ((esh + n) * 4u + 15u) & ~15u;
+        wmeta[s] = make_uint4(tp, pos, n, (csh / M) | (esh << 8));
+        unsigned char* st = wring + s * P::STAGE_B;
+        mbar_expect_tx(&wbar[s], cbytes + ebytes);
+        bulk_g2s(st, a.codes + (cb - csh), cbytes, &wbar[s]);
+        bulk_g2s(st + P::CODE_B, a.eterm_lam + (pos - esh), ebytes, &wbar[s]);
+    };
+    if (lane == 0)
+        for (uint32_t d = 0; d < (uint32_t)NS && d < my_total; d++) fill(d);
+
+    const float2 delta2 = make_float2(a.lam_delta, a.lam_delta), lam02 = make_float2(a.lam0, a.lam0);
+    const float2 m2 = make_float2(-2.0f, -2.0f);
+    uint32_t done = 0;
+    uint64_t n_seen = 0;
+    uint32_t rlen = 1;
+    while (__syncthreads_or(done < my_total)) {
+        for (uint32_t r = 0; r < rlen && done < my_total; r++) {
+            const uint32_t s = done % NS;
+            mbar_wait(&wbar[s], (done / NS) & 1u);
+            const uint4 mt = wmeta[s];
+            const float4 cp = cpar[mt.x];
+            const uint32_t pos = mt.y, n = mt.z, csh = mt.w & 0xffu, esh = mt.w >> 8;
+            const float2 av2 = make_float2(cp.x, cp.x), Bc2 = make_float2(cp.y, cp.y), cv2 = make_float2(cp.z, cp.z);
+            const unsigned char* st = wring + s * P::STAGE_B;
+            const uint32_t* els = reinterpret_cast<const uint32_t*>(st + P::CODE_B) + esh;
+            uint32_t cw[U][NW];
+            uint32_t lb[U];
+            float ev[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t idx = u * 32 + lane;  // entries >= n hold stale bytes; masked below
+                load_code_smem<M>(st + (csh + idx) * M, cw[u]);
+                const uint32_t le = els[idx];
+                lb[u] = le & 0xffu;
+                ev[u] = __uint_as_float(le & ~0xffu);
+            }
+            const uint64_t tau = *reinterpret_cast<volatile unsigned long long*>(&s_tau);
+            const float taud = tau == ~0ull ? __int_as_float(0x7f800000) : key_dist(tau);
+            uint32_t tk = 0;
+            float dist[U];
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+                dist[u] = dist[u + 1] = __int_as_float(0x7fffffff);
+                if (u * 32 < n) {  // warp-uniform: skip fully empty pairs
+                    const float2 lam = __ffma2_rn(make_float2((float)lb[u], (float)lb[u + 1]), delta2, lam02);
+                    const float2 t1 = __ffma2_rn(lam, __ffma2_rn(lam, cv2, Bc2), av2);
+                    const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
+                    float2 sm = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
+#pragma unroll
+                    for (int p = 1; p < M; p++)
+                        sm = __fadd2_rn(sm, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
+                    const float2 d = __ffma2_rn(m2, sm, te);
+                    dist[u] = d.x;
+                    dist[u + 1] = d.y;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t idx = u * 32 + lane;
+                if (idx < n && dist[u] <= taud) {
+                    uint32_t ub = __float_as_uint(dist[u]);
+                    ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;
+                    const uint64_t key = ((uint64_t)ub << 32) | (pos + idx);
+                    if (key < tau) tk |= 1u << u;
+                }
+            }
+            const uint32_t any = __ballot_sync(0xffffffffu, tk != 0);
+            if (any) {
+                uint32_t wtot = 0;
+                uint32_t bal[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    bal[u] = __ballot_sync(0xffffffffu, (tk >> u) & 1u);
+                    wtot += __popc(bal[u]);
+                }
+                uint32_t base = 0;
+                if (lane == 0) {
+                    unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&s_count);
+                    base = 0xffffffffu;
+                    while (cur + wtot <= cap) {
+                        const unsigned int prev = atomicCAS(&s_count, cur, cur + wtot);
+                        if (prev == cur) {
+                            base = cur;
+                            break;
+                        }
+                        cur = prev;
+                    }
+                }
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base == 0xffffffffu) break;  // buffer full: redo this chunk (still staged) after the flush
+                const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if ((tk >> u) & 1u) {
+                        uint32_t ub = __float_as_uint(dist[u]);
+                        ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;
+                        cbuf[base + __popc(bal[u] & lt)] = ((uint64_t)ub << 32) | (pos + u * 32 + lane);
+                    }
+                    base += __popc(bal[u]);
+                }
+            }
+            __syncwarp();  // every lane has read slot s: refill it
+            if (lane == 0 && done + NS < my_total) fill(done + NS);
+            done++;
+        }
+        __syncthreads();
+        n_seen += rlen * NWARPS * CH;
+        const uint32_t cnt = s_count;
+        if (cnt > keep && cnt > cap / 2) {  // block-uniform
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_count = keep;
+                s_tau = T + 1;
+            }
+            __syncthreads();
+        }
+        const uint32_t free_slots = cap - s_count;
+        const uint64_t per_chunk_round = (uint64_t)NWARPS * CH;
+        uint64_t rn = (s_tau == ~0ull) ? free_slots / per_chunk_round
+                                       : ((uint64_t)free_slots * n_seen) / (4ull * keep * per_chunk_round);
+        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > 64 ? 64ull : rn));
+    }
+    uint32_t n = s_count;
+    if (n > keep) {
+        block_select_keep(cbuf, n, keep, hist, s_misc);
+        n = keep;
+    }
+    __syncthreads();
+    for (uint32_t i = n + threadIdx.x; i < keep; i += blockDim.x) cbuf[i] = ~0ull;
+    __syncthreads();
+    bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
+    uint64_t* candq = a.cand + q * keep;
+    for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
+}
+
 }  // namespace dev
+
+// v7 launcher: su = slots per lane (2 / 4), stages per warp and CTAs per SM
+// chosen so the ring fits the shared-memory budget; false if it cannot fit
+template <int M, int U, int NS, int MINB>
+static bool launch_bulk_cfg(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, uint32_t cap,
+                            cudaStream_t st) {
+    const size_t smem = dev::bulk_smem_bytes<M, U, NS>(w2, cap);
+    if (smem > (size_t)(228 * 1024) / MINB - 2048) return false;
+    auto fn = dev::k_scan_bulk<M, U, NS, MINB>;
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
+    CUDA_LAUNCH_CHECK();
+    return true;
+}
+
+template <int M>
+static bool launch_bulk(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int cfg, cudaStream_t st) {
+    const uint32_t cap = std::max<uint32_t>(1024, 4 * keep);
+    switch (cfg) {
+        case 1: return launch_bulk_cfg<M, 2, 3, 3>(a, nq, w2, keep, cap, st);
+        case 2: return launch_bulk_cfg<M, 4, 2, 2>(a, nq, w2, keep, cap, st);
+        case 3: return launch_bulk_cfg<M, 2, 2, 3>(a, nq, w2, keep, cap, st);
+        default: return launch_bulk_cfg<M, 4, 3, 2>(a, nq, w2, keep, cap, st);
+    }
+}
 
 template <int M, int R, int U>
 static void launch_fast_u(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, cudaStream_t st) {
@@ -686,8 +1060,19 @@ void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t 
 
 template <int M>
 static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, int pf,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool q8 = false) {
     const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
+    if (q8) {  // u8 LUT: su 6 (3 CTAs/SM), 8, 104 / 106 (4 CTAs/SM)
+        const size_t smem = 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
+        auto fn = su == 8 ? dev::k_scan_fast2<M, 8, 3, true>
+                  : su == 104 ? dev::k_scan_fast2<M, 4, 4, true>
+                  : su == 106 ? dev::k_scan_fast2<M, 6, 4, true>
+                              : dev::k_scan_fast2<M, 6, 3, true>;
+        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap, 0u);
+        CUDA_LAUNCH_CHECK();
+        return;
+    }
     const size_t smem = 4 * 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
     // su: slots per lane (4/6/8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
     auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
@@ -708,6 +1093,25 @@ bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t ke
     // 1 = generic warp-buffer scan (not here), 2 = fully replicated LUT (v5),
     // 3 = four copies (v5), 4 = single table (v5)
     if (keep > 512 || w2 > 4096 || variant == 1) return false;
+    if (variant >= 5 && variant <= 8 && a.eterm_lam) {  // v7: bulk-async staged entry stream
+        bool ok = false;
+        switch (a.m) {
+            case 16: ok = launch_bulk<16>(a, nq, w2, keep, variant - 5, st); break;
+            case 8: ok = launch_bulk<8>(a, nq, w2, keep, variant - 5, st); break;
+            case 4: ok = launch_bulk<4>(a, nq, w2, keep, variant - 5, st); break;
+            default: break;
+        }
+        if (ok) return true;
+        variant = 0;  // the ring does not fit (very large w2): v6
+    }
+    if (variant == 9 && a.eterm_lam) {  // v6 with the u8-quantized LUT
+        switch (a.m) {
+            case 16: launch_fast2<16>(a, nq, w2, keep, su, pf, st, true); return true;
+            case 8: launch_fast2<8>(a, nq, w2, keep, su, pf, st, true); return true;
+            case 4: launch_fast2<4>(a, nq, w2, keep, su, pf, st, true); return true;
+            default: variant = 0; break;
+        }
+    }
     if (variant == 0) {
         switch (a.m) {
             case 16: launch_fast2<16>(a, nq, w2, keep, su, pf, st); return true;

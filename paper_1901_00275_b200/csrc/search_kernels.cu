@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(256) k_term5(const float* __restrict__ Y, cons
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) meta[q].s5max = s5;
+    if (threadIdx.x == 0) {
+        meta[q].s5max = s5;
+        meta[q].qerr = 0.0f;  // set by a quantized-LUT scan
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, ui
             // reference op order), the reassociated e-sum 8u*(Dmax+Emax), the
             // final subtraction 4u*S5max; 1.25x margin
             const double eps = 1.25 * u * (27.0 * (double)mt.dmax + 8.0 * (double)a.emax + 4.0 * (double)mt.s5max) +
-                               1.25 * (double)a.e_pack_err + 1e-30;
+                               1.25 * (double)a.e_pack_err + (double)mt.qerr + 1e-30;
             const double exact_k = (double)unord_float((uint32_t)(keys[topk - 1] >> 32));
             const double fast_last = (double)s_fast_last;
             if (!(fast_last - eps > exact_k)) flag = 1;
