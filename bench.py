@@ -141,10 +141,16 @@ def build_index(vlqadc, w, device, rank=0, world=1):
     return idx, {"train_s": round(t1 - t0, 2), "add_s": round(t2 - t1, 2)}
 
 
-def make_queries(vlqadc, w, nq, device):
+def make_queries(vlqadc, w, nq, device, kind="ref"):
+    """kind "ref": the reference's convention (README.md:79-80, acceptance.cpp:113):
+    gen_synthetic with another seed, i.e. another set of cluster centres, so
+    the queries lie outside the base mixture.  kind "heldout": fresh rows
+    n, n+1, ... of the base generator -- the same mixture as the base (how
+    DEEP1B / SIFT1B queries relate to their bases)."""
     import torch
     q = torch.empty((nq, w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
-    vlqadc.gen_synthetic_device(0, nq, w["dim"], w["clusters"], SPREAD, QUERY_SEED, q.data_ptr(), device=device)
+    first, seed = (w["n"], BASE_SEED) if kind == "heldout" else (0, QUERY_SEED)
+    vlqadc.gen_synthetic_device(first, nq, w["dim"], w["clusters"], SPREAD, seed, q.data_ptr(), device=device)
     torch.cuda.synchronize(device)
     return q
 
@@ -384,6 +390,14 @@ def main():
     gt = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], SPREAD, BASE_SEED, qh[:ngt], 1,
                                          device=local)
     recall = {f"recall@{r}": round(recall_at(res_ids[:ngt], gt, r), 4) for r in (1, 10, 100) if r <= k}
+    # the same search on held-out queries of the base mixture (not timed)
+    qho = make_queries(vlqadc, w, ngt, local, kind="heldout").cpu().numpy()
+    gt_ho = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], SPREAD, BASE_SEED, qho, 1, device=local)
+    if world == 1:
+        ho_ids, _ = idx.search(qho, w1=args.w1, alpha=args.alpha, k=k)
+        recall["heldout"] = {f"recall@{r}": round(recall_at(ho_ids, gt_ho, r), 4) for r in (1, 10, 100) if r <= k}
+        recall["heldout"]["queries"] = (f"{ngt} fresh rows of the base generator (same mixture); the main figures "
+                                        f"use the reference's query convention (another seed = other centres)")
 
     # e2e: public API with host buffers (H2D queries + D2H results per step)
     if world == 1:

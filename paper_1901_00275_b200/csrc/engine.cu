@@ -10,6 +10,8 @@
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
+#include <thread>
+#include <vector>
 
 #include "engine.h"
 
@@ -676,6 +678,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             a.eterm_lam = eterm_lam_.p;
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
+        a.scan_cap = cfg_.scan_cap;
         if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, cfg_.scan_slots, cfg_.scan_prefetch, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
@@ -723,6 +726,7 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
+    else if (key == "scan_cap") cfg_.scan_cap = (uint32_t)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 
@@ -782,6 +786,29 @@ void Engine::set_profiling(bool on) {
     profiling_ = on;
 }
 
+// host copy between the caller's (pageable) arrays and the pinned staging:
+// split over a few threads above 1 MiB -- a single thread is bound by the
+// first-touch page faults of freshly allocated numpy outputs (~2 ms for the
+// 12 MB of a 10k x 100 result)
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t kMin = 1u << 20;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = (unsigned)std::min<size_t>(std::min(8u, hw), bytes / kMin);
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt && t * per < bytes; t++)
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + t * per, static_cast<const char*>(src) + t * per,
+                        std::min(per, bytes - t * per));
+        });
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& x : th) x.join();
+}
+
 void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
                          float* dists, uint64_t* scanned) {
     if (!model_ok_) throw std::runtime_error("search: no model loaded");
@@ -802,7 +829,7 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     unsigned char* pi = pq + qb;
     unsigned char* pd = pi + ib;
     unsigned char* ps = pd + db;
-    std::memcpy(pq, q, qb);
+    par_memcpy(pq, q, qb);
     CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
     CUDA_CHECK(cudaMemcpyAsync(sq_.p, pq, qb, cudaMemcpyHostToDevice, st));
     search_device(sq_.p, nq, w1, alpha, topk, si_.p, sd_.p, ss_.p, st);
@@ -813,10 +840,10 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     if (scanned) CUDA_CHECK(cudaMemcpyAsync(ps, ss_.p, sb, cudaMemcpyDeviceToHost, st));
     check_device_errors(st);
     if (topk) {
-        std::memcpy(ids, pi, ib);
-        std::memcpy(dists, pd, db);
+        par_memcpy(ids, pi, ib);
+        par_memcpy(dists, pd, db);
     }
-    if (scanned) std::memcpy(scanned, ps, sb);
+    if (scanned) par_memcpy(scanned, ps, sb);
 }
 
 // ---------------------------------------------------------------------------

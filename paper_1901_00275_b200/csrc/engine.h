@@ -29,6 +29,7 @@ struct EngineConfig {
     int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
+    uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
     uint32_t scan_keep_min = 0;  // study knob: lower bound on k' (fast-scan survivors)
     int scan_packed = 1;   // v6 scan reads the packed e-term | lambda-byte stream (one load per entry)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported

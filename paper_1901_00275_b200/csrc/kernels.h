@@ -50,6 +50,7 @@ struct SearchArgs {
     // certificate when the packed stream was scanned
     const uint32_t* eterm_lam;
     float e_pack_err;
+    uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
 };
 
 // Add-path device views.

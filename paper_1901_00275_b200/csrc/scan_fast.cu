@@ -1061,7 +1061,8 @@ void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t 
 template <int M>
 static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, int pf,
                          cudaStream_t st, bool q8 = false) {
-    const uint32_t cap = 2048;  // block-shared candidate buffer (keys)
+    // block-shared candidate buffer (keys): 2048 unless the scan_cap knob says otherwise
+    const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 2048u, 4 * keep);
     if (q8) {  // u8 LUT: su 6 (3 CTAs/SM), 8, 104 / 106 (4 CTAs/SM)
         const size_t smem = 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
         auto fn = su == 8 ? dev::k_scan_fast2<M, 8, 3, true>

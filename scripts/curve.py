@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--gt", type=int, default=200)
+    ap.add_argument("--queries", default="ref,heldout", help="query sets: ref (reference convention), heldout")
     args = ap.parse_args()
     import torch
     from paper_1901_00275_b200 import vlqadc
@@ -39,14 +40,20 @@ def main():
     idx, setup = bench.build_index(vlqadc, w, 0)
     nqs = [int(x) for x in args.nqs.split(",") if x]
     w1s = [int(x) for x in args.w1s.split(",") if x]
-    qall = bench.make_queries(vlqadc, w, max(nqs), 0)
-    ngt = min(args.gt, min(nqs))
-    gt = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], bench.SPREAD, bench.BASE_SEED,
-                                         qall[:ngt].cpu().numpy(), 1, device=0)
     k = args.k
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=qall.device)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda:0")
     stream = torch.cuda.Stream()
     st = stream.cuda_stream
+    for kind in [x for x in args.queries.split(",") if x]:
+        qall = bench.make_queries(vlqadc, w, max(nqs), 0, kind=kind)
+        ngt = min(args.gt, min(nqs))
+        gt = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], bench.SPREAD, bench.BASE_SEED,
+                                             qall[:ngt].cpu().numpy(), 1, device=0)
+        run(args, idx, qall, nqs, w1s, k, gt, ngt, flush, stream, st, setup, kind)
+
+
+def run(args, idx, qall, nqs, w1s, k, gt, ngt, flush, stream, st, setup, kind):
+    import torch
     for nq in nqs:
         q = qall[:nq].contiguous()
         ids = torch.empty((nq, k), dtype=torch.int64, device=q.device)
@@ -72,7 +79,7 @@ def main():
                         stream.synchronize()
                         tot += e0.elapsed_time(e1)
             res = ids[:ngt].cpu().numpy()
-            line = {"workload": args.workload, "nq": nq, "w1": w1, "alpha": args.alpha, "k": k,
+            line = {"workload": args.workload, "queries": kind, "nq": nq, "w1": w1, "alpha": args.alpha, "k": k,
                     "qps": round(nq * args.steps / (tot / 1e3), 1), "ms_per_step": round(tot / args.steps, 3),
                     "scanned_per_query": round(float(scanned.sum().item()) / nq, 1),
                     **{f"recall@{r}": round(bench.recall_at(res, gt, r), 4) for r in (1, 10, 100) if r <= k},
