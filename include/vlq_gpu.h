@@ -156,11 +156,14 @@ int vlq_engine_ivf_search_device(vlq_engine* e, const float* d_queries, uint64_t
 int vlq_engine_ivf_get_lists(vlq_engine* e, uint64_t* count, uint64_t* list_off, uint32_t* ids, uint8_t* codes);
 
 /* Study knobs, not part of the reference surface: "scan_variant" (0 = v6
- * packed-fp32 fast scan, 2/3/4 = v5 LUT layouts, 1 = generic scan),
+ * packed-fp32 fast scan, 2/3/4 = v5 LUT layouts, 1 = generic scan, 5-8 = v7
+ * bulk-async staged entry ring, 9 = v6 with the u8-quantized LUT),
  * "scan_slots" (entry slots per lane: 4/6/8; +100 = 4 CTAs/SM),
  * "scan_prefetch" (L2 prefetch distance in chunks), "scan_packed" (packed
- * e-term|lambda stream), "tc_persist", "tc_pass1_single", "tc_search_min_k",
- * "force_exact".  Results are identical for every setting. */
+ * e-term|lambda stream), "scan_keep_min" (lower bound on the fast-scan
+ * survivors k'), "scan_cap" (candidate buffer keys per CTA), "tc_persist",
+ * "tc_pass1_single", "tc_search_min_k", "force_exact".  Results are identical
+ * for every setting. */
 int vlq_engine_set_tuning(vlq_engine* e, const char* key, int64_t value);
 
 /* Per-phase CUDA-event timing (recorded on the search stream) and counters. */

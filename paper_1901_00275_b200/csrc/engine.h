@@ -26,7 +26,8 @@ struct EngineConfig {
     uint64_t workspace_bytes = 4ull << 30;  // per-query-tile scratch budget
     uint32_t max_tile = 16384;
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
-    int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants
+    int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants,
+                           // 5-8 v7 bulk-async staged ring (4 ring configs), 9 v6 with the u8-quantized LUT
     int scan_slots = 6;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)

@@ -84,10 +84,12 @@ def test_exhaustive_search_equals_full_scan(vlqadc, oracle_mod):
         assert np.array_equal(ids, oids) and same_f32(dists, odists)
 
 
-@pytest.mark.parametrize("seed,variant", [(0, 0), (1, 0), (2, 4)])
+@pytest.mark.parametrize("seed,variant", [(0, 0), (1, 0), (2, 4), (3, 5), (4, 7), (5, 9)])
 def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed, variant):
     """Random (w1, alpha, k) vs the oracle (v6 scan; seed 2 with the v5
-    single-table scan)."""
+    single-table scan; seeds 3/4 with the bulk-async staged scan v7; seed 5
+    with the u8-quantized LUT, whose widened certificate sends more queries
+    to the exact fallback -- results must not change)."""
     rng = np.random.default_rng(seed)
     for name in ALL_CASES:
         z, index_path, _ = load_golden(name)
