@@ -674,7 +674,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (fast) {
         const uint32_t keep = scan_keep(topk);
         mark(PH_SCAN);
-        if (cfg_.scan_packed && (cfg_.scan_variant == 0 || (cfg_.scan_variant >= 5 && cfg_.scan_variant <= 9)) && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
+        if (cfg_.scan_packed && (cfg_.scan_variant == 0 || (cfg_.scan_variant >= 5 && cfg_.scan_variant <= 12)) && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
             a.eterm_lam = eterm_lam_.p;
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }

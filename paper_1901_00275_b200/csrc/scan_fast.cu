@@ -444,10 +444,81 @@ __device__ __forceinline__ uint32_t lut8_at(const unsigned char* lq, const uint3
     return lq[p * 256 + b];
 }
 
-template <int M, int U, int MINB, bool Q8 = false>
-__global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap,
-                                                          uint32_t pf) {
+// The query's term5 table quantized to u8 (all threads of the CTA): one step
+// `scale` for all sub-spaces (the widest range / 255) and per-sub-space offsets,
+// LUT_q8[p][j] = rint((t5[p][j] - min_p) / scale), so that
+//     sum5 ~= smin + scale * sum_p LUT_q8[p][code_p]        (smin = sum_p min_p)
+// with |error| <= m * scale / 2.  meta->qerr receives the resulting bound on
+// |dist_q8 - dist| (x2 for the -2 sum5 of adc_distance) plus a generous
+// allowance for the fp32 rounding of the reconstruction.  Ends synchronised.
+template <int M>
+__device__ void build_q8_lut(const float* __restrict__ t5f, unsigned char* lq, float* s_qmin, float* s_qrng,
+                             QueryMeta* meta, float& scale, float& smin) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+    for (uint32_t p = warp; p < (uint32_t)M; p += nwarps) {  // per-sub-space range
+        float mn = __int_as_float(0x7f800000), mx = -mn;
+        for (uint32_t j = lane; j < VLQ_KSUB; j += 32) {
+            const float v = __ldg(t5f + p * VLQ_KSUB + j);
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            s_qmin[p] = mn;
+            s_qrng[p] = mx - mn;
+        }
+    }
+    __syncthreads();
+    float rng = 0.0f, sabs = 0.0f;
+    smin = 0.0f;
+#pragma unroll
+    for (int p = 0; p < M; p++) {
+        rng = fmaxf(rng, s_qrng[p]);
+        smin += s_qmin[p];
+        sabs += fabsf(s_qmin[p]);
+    }
+    scale = rng > 0.0f ? rng / 255.0f : 1.0f;
+    const float inv = 1.0f / scale;
+    for (uint32_t i = threadIdx.x; i < 256u * M; i += blockDim.x) {
+        const float v = __ldg(t5f + i);
+        const int qv = __float2int_rn((v - s_qmin[i >> 8]) * inv);
+        lq[i] = (unsigned char)min(255, max(0, qv));
+    }
+    if (threadIdx.x == 0) {
+        const float span = sabs + scale * 255.0f * M;
+        meta->qerr = 2.0f * (0.5f * M * scale * 1.001f) + 1e-5f * span;
+    }
+    __syncthreads();
+}
+
+// LM = 2 (q8x32): the u8 table replicated once per lane so that every lane
+// reads its own bank -- conflict-free LUT loads (one wavefront per warp
+// lookup) at the price of 32x the table (64 KB per 8 sub-spaces, one CTA of
+// 16 warps per SM).  Row (g, j) is 256 bytes: [half h][lane l][byte b] holds
+// LUT[8g + 4h + b][j], so the address of LUT[p][j] for lane l is
+//     (j << 8 | l << 2) + 65536 (p / 8) + 128 ((p / 4) % 2) + p % 4,
+// where the first term is ONE PRMT of the code word with the lane's base and
+// the rest is the LDS immediate; bank = l for every p and j.
+template <int M>
+__device__ __forceinline__ uint32_t lut8x32_at(const unsigned char* lq, const uint32_t (&w)[(M + 3) / 4], int p,
+                                               uint32_t lane4) {
+    const uint32_t a = __byte_perm(w[p >> 2], lane4, 0x7604u | ((uint32_t)(p & 3) << 4));
+    return lq[a + 65536u * (p >> 3) + 128u * ((p >> 2) & 1) + (p & 3)];
+}
+
+template <int M>
+__host__ __device__ constexpr uint32_t lut_bytes(int lm) {
+    return lm == 0 ? 4 * 256 * M : (lm == 1 ? 256 * M : 65536u * ((M + 7) / 8));
+}
+
+template <int M, int U, int MINB, int LM = 0, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap,
+                                                         uint32_t pf) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
+    constexpr bool Q8 = LM != 0;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = (M + 3) / 4;
     constexpr uint32_t CH = 32 * U;  // entries per chunk
@@ -455,7 +526,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t q = blockIdx.x;
     unsigned char* lut = smem;
-    constexpr uint32_t LUT_B = (Q8 ? 1 : 4) * 256 * M;
+    constexpr uint32_t LUT_B = lut_bytes<M>(LM);
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + LUT_B);        // cap keys
     uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);         // w2 + 1
     __shared__ uint32_t hist[256];
@@ -471,46 +542,32 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
         for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
     } else {
         const float* t5f = a.t5 + q * M * VLQ_KSUB;
-        for (uint32_t p = warp; p < (uint32_t)M; p += nwarps) {  // per-sub-space range
-            float mn = __int_as_float(0x7f800000), mx = -mn;
-            for (uint32_t j = lane; j < VLQ_KSUB; j += 32) {
-                const float v = __ldg(t5f + p * VLQ_KSUB + j);
-                mn = fminf(mn, v);
-                mx = fmaxf(mx, v);
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            }
-            if (lane == 0) {
-                s_qmin[p] = mn;
-                s_qrng[p] = mx - mn;
-            }
-        }
-        __syncthreads();
-        float rng = 0.0f, smin = 0.0f, sabs = 0.0f;
+        float scale, smin;
+        // LM = 2: quantize into the (not yet used) candidate buffer, then replicate
+        unsigned char* lq = LM == 2 ? reinterpret_cast<unsigned char*>(cbuf) : lut;
+        build_q8_lut<M>(t5f, lq, s_qmin, s_qrng, a.meta + q, scale, smin);
+        if constexpr (LM == 2) {
+            __syncthreads();
+            for (uint32_t r = threadIdx.x; r < 256u * ((M + 7) / 8); r += blockDim.x) {
+                const uint32_t g = r >> 8, j = r & 255u;
+                uint32_t hw[2];
 #pragma unroll
-        for (int p = 0; p < M; p++) {
-            rng = fmaxf(rng, s_qrng[p]);
-            smin += s_qmin[p];
-            sabs += fabsf(s_qmin[p]);
-        }
-        const float scale = rng > 0.0f ? rng / 255.0f : 1.0f;
-        const float inv = 1.0f / scale;
-        for (uint32_t i = threadIdx.x; i < 256u * M; i += blockDim.x) {
-            const float v = __ldg(t5f + i);
-            const int qv = __float2int_rn((v - s_qmin[i >> 8]) * inv);
-            lut[i] = (unsigned char)min(255, max(0, qv));
+                for (int h = 0; h < 2; h++) {
+                    hw[h] = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        const uint32_t p = 8 * g + 4 * h + b;
+                        if (p < (uint32_t)M) hw[h] |= (uint32_t)lq[p * 256 + j] << (8 * b);
+                    }
+                }
+                uint4* row = reinterpret_cast<uint4*>(lut + 65536u * g + 256u * j);
+#pragma unroll
+                for (int i = 0; i < 16; i++) row[i] = make_uint4(hw[i >> 3], hw[i >> 3], hw[i >> 3], hw[i >> 3]);
+            }
+            __syncthreads();  // the staging bytes in cbuf are dead from here on
         }
         qs2 = make_float2(-2.0f * scale, -2.0f * scale);
         qc2 = make_float2(-2.0f * smin, -2.0f * smin);
-        if (threadIdx.x == 0) {
-            // |sum5_q8 - sum5| <= M * (scale / 2) (+ the rounding of the step
-            // computation); the affine reconstruction adds a few ulps of
-            // |smin| + the largest integer sum: bound both generously
-            const float span = sabs + scale * 255.0f * M;
-            a.meta[q].qerr = 2.0f * (0.5f * M * scale * 1.001f) + 1e-5f * span;
-        }
     }
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
@@ -644,8 +701,13 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                         uint32_t i0 = 0, i1 = 0;
 #pragma unroll
                         for (int p = 0; p < M; p++) {
-                            i0 += lut8_at<M>(lut, cw[u], p);
-                            i1 += lut8_at<M>(lut, cw[u + 1], p);
+                            if constexpr (LM == 2) {
+                                i0 += lut8x32_at<M>(lut, cw[u], p, lane << 2);
+                                i1 += lut8x32_at<M>(lut, cw[u + 1], p, lane << 2);
+                            } else {
+                                i0 += lut8_at<M>(lut, cw[u], p);
+                                i1 += lut8_at<M>(lut, cw[u + 1], p);
+                            }
                         }
                         d = __ffma2_rn(qs2, make_float2((float)i0, (float)i1), __fadd2_rn(te, qc2));
                     } else {
@@ -774,15 +836,18 @@ struct BulkPlan {
     static_assert(STAGE_B % 16 == 0, "stages stay 16-byte aligned");
 };
 
-template <int M, int U, int NS>
+template <int M, int U, int NS, int LM>
 __host__ __device__ constexpr size_t bulk_smem_bytes(uint32_t w2, uint32_t cap) {
-    return 4 * 256 * (size_t)M + 8 * (size_t)NS * (BulkPlan<M, U>::STAGE_B + 16 + 8) + (size_t)cap * 8 +
+    return (size_t)lut_bytes<M>(LM) + 8 * (size_t)NS * (BulkPlan<M, U>::STAGE_B + 16 + 8) + (size_t)cap * 8 +
            (size_t)w2 * 24 + ((size_t)w2 + 1) * 4;
 }
 
-template <int M, int U, int NS, int MINB>
+// LM = 1: the u8-quantized LUT of k_scan_fast2<.., 1> (4x smaller table, so
+// the ring fits at 3 CTAs per SM)
+template <int M, int U, int NS, int MINB, int LM = 0>
 __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
+    static_assert(LM == 0 || LM == 1, "bulk scan: fp32 or u8 LUT");
     using P = BulkPlan<M, U>;
     constexpr uint32_t CH = P::CH;
     constexpr int NW = (M + 3) / 4;
@@ -791,7 +856,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t q = blockIdx.x;
     unsigned char* lut = smem;
-    unsigned char* ring = smem + 4 * 256 * M;                                       // [warp][stage]
+    unsigned char* ring = smem + lut_bytes<M>(LM);                                 // [warp][stage]
     uint4* smeta = reinterpret_cast<uint4*>(ring + NWARPS * NS * P::STAGE_B);       // [warp][stage]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smeta + NWARPS * NS);              // [warp][stage]
     uint64_t* cbuf = bars + NWARPS * NS;                                            // cap keys
@@ -803,9 +868,19 @@ __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t 
     __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
 
+    __shared__ float s_qmin[LM ? M : 1], s_qrng[LM ? M : 1];
+
     // 1. the query's term5 table (one copy per sub-space)
-    const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
-    for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    float2 qs2 = make_float2(0.f, 0.f), qc2 = qs2;  // LM = 1: dist = qs * isum + (te + qc)
+    if constexpr (LM == 0) {
+        const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
+        for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    } else {
+        float scale, smin;
+        build_q8_lut<M>(a.t5 + q * M * VLQ_KSUB, lut, s_qmin, s_qrng, a.meta + q, scale, smin);
+        qs2 = make_float2(-2.0f * scale, -2.0f * scale);
+        qc2 = make_float2(-2.0f * smin, -2.0f * smin);
+    }
     // 2. per-cell parameters and the chunk prefix (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
     const float* wsq = a.ws + q * a.k;
@@ -918,11 +993,22 @@ __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t 
                     const float2 lam = __ffma2_rn(make_float2((float)lb[u], (float)lb[u + 1]), delta2, lam02);
                     const float2 t1 = __ffma2_rn(lam, __ffma2_rn(lam, cv2, Bc2), av2);
                     const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
-                    float2 sm = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
+                    float2 d;
+                    if constexpr (LM == 1) {
+                        uint32_t i0 = 0, i1 = 0;
 #pragma unroll
-                    for (int p = 1; p < M; p++)
-                        sm = __fadd2_rn(sm, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
-                    const float2 d = __ffma2_rn(m2, sm, te);
+                        for (int p = 0; p < M; p++) {
+                            i0 += lut8_at<M>(lut, cw[u], p);
+                            i1 += lut8_at<M>(lut, cw[u + 1], p);
+                        }
+                        d = __ffma2_rn(qs2, make_float2((float)i0, (float)i1), __fadd2_rn(te, qc2));
+                    } else {
+                        float2 sm = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
+#pragma unroll
+                        for (int p = 1; p < M; p++)
+                            sm = __fadd2_rn(sm, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
+                        d = __ffma2_rn(m2, sm, te);
+                    }
                     dist[u] = d.x;
                     dist[u + 1] = d.y;
                 }
@@ -1011,12 +1097,12 @@ __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t 
 
 // v7 launcher: su = slots per lane (2 / 4), stages per warp and CTAs per SM
 // chosen so the ring fits the shared-memory budget; false if it cannot fit
-template <int M, int U, int NS, int MINB>
+template <int M, int U, int NS, int MINB, int LM = 0>
 static bool launch_bulk_cfg(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, uint32_t cap,
                             cudaStream_t st) {
-    const size_t smem = dev::bulk_smem_bytes<M, U, NS>(w2, cap);
+    const size_t smem = dev::bulk_smem_bytes<M, U, NS, LM>(w2, cap);
     if (smem > (size_t)(228 * 1024) / MINB - 2048) return false;
-    auto fn = dev::k_scan_bulk<M, U, NS, MINB>;
+    auto fn = dev::k_scan_bulk<M, U, NS, MINB, LM>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
@@ -1025,8 +1111,10 @@ static bool launch_bulk_cfg(const SearchArgs& a, uint64_t nq, uint32_t w2, uint3
 
 template <int M>
 static bool launch_bulk(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int cfg, cudaStream_t st) {
-    const uint32_t cap = std::max<uint32_t>(1024, 4 * keep);
+    const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 1024u, 2 * keep + 512);
     switch (cfg) {
+        case 4: return launch_bulk_cfg<M, 4, 2, 3, 1>(a, nq, w2, keep, cap, st);  // u8 LUT, 3 CTAs/SM
+        case 5: return launch_bulk_cfg<M, 4, 3, 2, 1>(a, nq, w2, keep, cap, st);  // u8 LUT, 2 CTAs/SM
         case 1: return launch_bulk_cfg<M, 2, 3, 3>(a, nq, w2, keep, cap, st);
         case 2: return launch_bulk_cfg<M, 4, 2, 2>(a, nq, w2, keep, cap, st);
         case 3: return launch_bulk_cfg<M, 2, 2, 3>(a, nq, w2, keep, cap, st);
@@ -1060,15 +1148,25 @@ void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t 
 
 template <int M>
 static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, int pf,
-                         cudaStream_t st, bool q8 = false) {
+                         cudaStream_t st, int q8 = 0) {
     // block-shared candidate buffer (keys): 2048 unless the scan_cap knob says otherwise
     const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 2048u, 4 * keep);
+    if (q8 == 2) {  // lane-replicated u8 LUT: one CTA of 16 warps (su 6) or 8 warps (su 106) per SM
+        const size_t smem = dev::lut_bytes<M>(2) + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
+        if (smem > 220 * 1024) throw std::runtime_error("scan q8x32: shared memory does not fit");
+        const unsigned nt = su == 106 ? 256 : 512;
+        auto fn = su == 106 ? dev::k_scan_fast2<M, 6, 1, 2, 256> : dev::k_scan_fast2<M, 6, 1, 2, 512>;
+        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        fn<<<(unsigned)nq, nt, smem, st>>>(a, w2, keep, cap, 0u);
+        CUDA_LAUNCH_CHECK();
+        return;
+    }
     if (q8) {  // u8 LUT: su 6 (3 CTAs/SM), 8, 104 / 106 (4 CTAs/SM)
         const size_t smem = 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
-        auto fn = su == 8 ? dev::k_scan_fast2<M, 8, 3, true>
-                  : su == 104 ? dev::k_scan_fast2<M, 4, 4, true>
-                  : su == 106 ? dev::k_scan_fast2<M, 6, 4, true>
-                              : dev::k_scan_fast2<M, 6, 3, true>;
+        auto fn = su == 8 ? dev::k_scan_fast2<M, 8, 3, 1>
+                  : su == 104 ? dev::k_scan_fast2<M, 4, 4, 1>
+                  : su == 106 ? dev::k_scan_fast2<M, 6, 4, 1>
+                              : dev::k_scan_fast2<M, 6, 3, 1>;
         CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap, 0u);
         CUDA_LAUNCH_CHECK();
@@ -1094,7 +1192,9 @@ bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t ke
     // 1 = generic warp-buffer scan (not here), 2 = fully replicated LUT (v5),
     // 3 = four copies (v5), 4 = single table (v5)
     if (keep > 512 || w2 > 4096 || variant == 1) return false;
-    if (variant >= 5 && variant <= 8 && a.eterm_lam) {  // v7: bulk-async staged entry stream
+    if (((variant >= 5 && variant <= 8) || variant == 11 || variant == 12) && a.eterm_lam) {
+        // v7: bulk-async staged entry stream (11 / 12: with the u8 LUT)
+        if (variant >= 11) variant -= 2;
         bool ok = false;
         switch (a.m) {
             case 16: ok = launch_bulk<16>(a, nq, w2, keep, variant - 5, st); break;
@@ -1105,11 +1205,12 @@ bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t ke
         if (ok) return true;
         variant = 0;  // the ring does not fit (very large w2): v6
     }
-    if (variant == 9 && a.eterm_lam) {  // v6 with the u8-quantized LUT
+    if ((variant == 9 || variant == 10) && a.eterm_lam) {  // v6 with the u8-quantized LUT (10: lane-replicated)
+        const int lm = variant == 9 ? 1 : 2;
         switch (a.m) {
-            case 16: launch_fast2<16>(a, nq, w2, keep, su, pf, st, true); return true;
-            case 8: launch_fast2<8>(a, nq, w2, keep, su, pf, st, true); return true;
-            case 4: launch_fast2<4>(a, nq, w2, keep, su, pf, st, true); return true;
+            case 16: launch_fast2<16>(a, nq, w2, keep, su, pf, st, lm); return true;
+            case 8: launch_fast2<8>(a, nq, w2, keep, su, pf, st, lm); return true;
+            case 4: launch_fast2<4>(a, nq, w2, keep, su, pf, st, lm); return true;
             default: variant = 0; break;
         }
     }
