@@ -284,8 +284,8 @@ def main():
     sharded = ShardedIndex(idx) if world > 1 else None
 
     def step():
-        if sharded is not None:  # query-split coarse stage + sharded scan + K9 merge
-            mi, md, _ = sharded.search_query_split(q, args.w1, args.alpha, k, out=(ids, dists, scanned))
+        if sharded is not None:  # query-split coarse stage + selection, sharded scan, K9 merge
+            mi, md, _ = sharded.search_select_split(q, args.w1, args.alpha, k, out=(ids, dists, scanned))
             return mi, md
         idx.search_device(q.data_ptr(), nq, args.w1, args.alpha, k, ids.data_ptr(), dists.data_ptr(),
                           scanned.data_ptr(), st)
@@ -348,7 +348,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             qdev.copy_(qpin, non_blocking=True)
-            mi, md, _ = sharded.search_query_split(qdev, args.w1, args.alpha, k, out=(ids, dists, scanned))
+            mi, md, _ = sharded.search_select_split(qdev, args.w1, args.alpha, k, out=(ids, dists, scanned))
             if rank == 0:
                 e_ids = mi.to("cpu", non_blocking=True)
                 e_d = md.to("cpu", non_blocking=True)
@@ -360,7 +360,7 @@ def main():
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e2e = {"value": round(nq * args.steps / (float(t_e.item()) / 1e3), 1), "unit": "queries/s",
                "h2d_bytes_per_step": int(qpin.numel() * 4), "d2h_bytes_per_step": int(nq * k * 12),
-               "api": "ShardedIndex.search_query_split (pinned host queries in, merged ids/dists out on rank 0)",
+               "api": "ShardedIndex.search_select_split (pinned host queries in, merged ids/dists out on rank 0)",
                "timing": "CUDA events around H2D + search + D2H, max over ranks"}
 
     if rank != 0:
@@ -497,7 +497,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 (exact reference order) + u8 codes",
             "data": "synthetic", "config": cfg, "recall": recall, "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
-            "coarse_stage": "query-split (1/N of the batch per rank)" if world > 1 else "single GPU",
+            "coarse_stage": ("query-split first level + cell selection (1/N of the batch per rank), "
+                             "selections all-gathered") if world > 1 else "single GPU",
             "ivfadc": ivf_line, "sweep": sweep,
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
             "fallback_queries_per_step": stats["flagged"] / args.steps,

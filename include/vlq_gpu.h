@@ -122,6 +122,25 @@ int vlq_engine_search_fine_device(vlq_engine* e, const float* d_queries, uint64_
                                   uint32_t k, const uint32_t* d_top, int64_t* d_ids, float* d_dists,
                                   uint64_t* d_scanned, void* stream);
 
+/* Index.search split after second_level_rank, for the select-split multi-GPU
+ * path (each rank runs the coarse stage AND the cell selection for a slice of
+ * the batch; the selections are all-gathered; every rank runs the scan stage
+ * on its shard):
+ *  - select: first_level_scan + second_level_rank (search.cpp:11-78) ->
+ *    d_sel[nq*w2] selected cell ids (i*n + j, the reference's order) and
+ *    d_ab[nq*w2*2] their exact (a, b) = (|y - c_i|^2, |y - c_nbr|^2);
+ *  - fine_sel: query_term5 .. select_topk (search.cpp:80-167) on this shard
+ *    from a gathered selection (w2 = the same alpha-derived count).
+ * select followed by fine_sel on the same engine equals vlq_engine_search_device. */
+int vlq_engine_search_select_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                                    uint32_t* d_sel, float* d_ab, void* stream);
+int vlq_engine_search_fine_sel_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                                      uint32_t k, const uint32_t* d_sel, const float* d_ab, int64_t* d_ids,
+                                      float* d_dists, uint64_t* d_scanned, void* stream);
+/* w2 = max(1, floor(alpha * w1 * n)) clamped to w1 * n (search.hpp:16-20): the
+ * row length of the select-split buffers. */
+uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n);
+
 /* Streamed Index.add of the engine's counter-based synthetic generator
  * (the reference's Gaussian-mixture law, dataset.cpp:13-44): rows are
  * generated on the device chunk by chunk, so 1e8-1e9-point bases never touch

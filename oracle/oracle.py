@@ -143,6 +143,32 @@ class OracleIndex:
                                         _p(scanned), ctypes.c_int(threads)))
         return ids, dists, scanned
 
+    def select(self, queries: np.ndarray, w1: int, alpha: float, threads: int = 0):
+        """first_level_scan + second_level_rank: (sel uint32 [nq, w2], ab
+        float32 [nq, w2, 2]) -- the select-split hand-off."""
+        q = np.ascontiguousarray(queries, np.float32)
+        w2 = int(lib().vo_w2(w1, np.float32(alpha), self.ix.n))
+        sel = np.empty((q.shape[0], w2), np.uint32)
+        ab = np.empty((q.shape[0], w2, 2), np.float32)
+        _check(lib().vo_select(ctypes.byref(self.s), _p(q), ctypes.c_uint64(q.shape[0]), ctypes.c_uint32(w1),
+                               ctypes.c_float(alpha), _p(sel), _p(ab), ctypes.c_int(threads)))
+        return sel, ab
+
+    def search_from_sel(self, queries: np.ndarray, sel: np.ndarray, ab: np.ndarray, w1: int, alpha: float, k: int,
+                        threads: int = 0):
+        """query_term5 .. select_topk from a select() hand-off (on this index's lists)."""
+        q = np.ascontiguousarray(queries, np.float32)
+        nq = q.shape[0]
+        sel = np.ascontiguousarray(sel, np.uint32)
+        ab = np.ascontiguousarray(ab, np.float32)
+        ids = np.empty((nq, k), np.int64)
+        d = np.empty((nq, k), np.float32)
+        sc = np.empty(nq, np.uint64)
+        _check(lib().vo_search_from_sel(ctypes.byref(self.s), _p(q), ctypes.c_uint64(nq), ctypes.c_uint32(w1),
+                                        ctypes.c_float(alpha), ctypes.c_uint32(k), _p(sel), _p(ab), _p(ids), _p(d),
+                                        _p(sc), ctypes.c_int(threads)))
+        return ids, d, sc
+
     def ivf_build(self, base: np.ndarray):
         """build_ivf_baseline (ivf_baseline.cpp:11-51) with this model's
         codebook and PQ -> (list_off u64[k+1], ids u32[N], codes u8[N, m])."""

@@ -219,11 +219,28 @@ typedef struct {
 
 /* top_in (nullable): the query's top-w1 regions from an earlier
  * first-level pass (the staged / query-split search); top_out (nullable)
- * receives them; out_ids == NULL stops after the first level. */
+ * receives them; out_ids == NULL stops after the first level.
+ * sel_out / ab_out (nullable): the w2 selected cells of second_level_rank
+ * and their (a, b) = (ws[i], ws[nbr]) (the select-split hand-off; with
+ * out_ids == NULL the search stops there).  sel_in / ab_in (nullable): start
+ * from such a selection -- first_level_scan and second_level_rank are
+ * skipped and ws holds ONLY the handed-over a and b values, which proves the
+ * hand-off carries everything the later stages read. */
 static int search_one(const vo_index* ix, const float* y, uint32_t w1, uint32_t w2, uint32_t topk,
                       vo_scratch* s, int64_t* out_ids, float* out_d, uint64_t* scanned,
-                      const uint32_t* top_in, uint32_t* top_out) {
+                      const uint32_t* top_in, uint32_t* top_out, const uint32_t* sel_in, const float* ab_in,
+                      uint32_t* sel_out, float* ab_out) {
     const uint32_t k = ix->k, n = ix->n, m = ix->m, dim = ix->dim, dsub = dim / m;
+    if (sel_in) {
+        for (uint32_t i = 0; i < k; i++) s->ws[i] = NAN;
+        for (uint32_t r = 0; r < w2; r++) {
+            const uint32_t cell = sel_in[r];
+            s->keys[r] = cell;
+            s->ws[cell / n] = ab_in[2 * (size_t)r];
+            s->ws[ix->nbr[cell]] = ab_in[2 * (size_t)r + 1];
+        }
+        goto term5;
+    }
     /* first_level_scan (search.cpp:11-36) */
     for (uint32_t i = 0; i < k; i++) {
         s->ws[i] = vo_sqdist(y, ix->centroids + (size_t)i * dim, dim);
@@ -237,7 +254,7 @@ static int search_one(const vo_index* ix, const float* y, uint32_t w1, uint32_t 
         for (uint32_t r = 0; r < w1; r++) top[r] = (uint32_t)s->keys[r];
     }
     if (top_out) memcpy(top_out, top, sizeof(uint32_t) * w1);
-    if (!out_ids) {
+    if (!out_ids && !sel_out) {
         free(top);
         return 0;
     }
@@ -260,6 +277,16 @@ static int search_one(const vo_index* ix, const float* y, uint32_t w1, uint32_t 
     }
     free(top);
     select_smallest(s->keys, total, w2);
+    if (sel_out) {
+        for (uint32_t r = 0; r < w2; r++) {
+            const uint32_t cell = (uint32_t)s->keys[r];
+            sel_out[r] = cell;
+            ab_out[2 * (size_t)r] = s->ws[cell / n];
+            ab_out[2 * (size_t)r + 1] = s->ws[ix->nbr[cell]];
+        }
+        if (!out_ids) return 0;
+    }
+term5:
     /* query_term5 (search.cpp:80-90) */
     for (uint32_t p = 0; p < m; p++)
         for (uint32_t j = 0; j < KSUB; j++)
@@ -372,6 +399,10 @@ typedef struct {
     uint64_t* out_scanned;
     const uint32_t* top_in;
     uint32_t* top_out;
+    const uint32_t* sel_in; /* select-split hand-off: [nq, w2] cells + [nq, w2, 2] (a, b) */
+    const float* ab_in;
+    uint32_t* sel_out;
+    float* ab_out;
 } search_ctx;
 
 static void* search_scratch(void* c) {
@@ -400,7 +431,11 @@ static int search_item(void* c, void* scratch, int64_t q) {
                       ctx->out_dists ? ctx->out_dists + (size_t)q * ctx->topk : NULL,
                       ctx->out_scanned ? ctx->out_scanned + q : NULL,
                       ctx->top_in ? ctx->top_in + (size_t)q * ctx->w1 : NULL,
-                      ctx->top_out ? ctx->top_out + (size_t)q * ctx->w1 : NULL);
+                      ctx->top_out ? ctx->top_out + (size_t)q * ctx->w1 : NULL,
+                      ctx->sel_in ? ctx->sel_in + (size_t)q * ctx->w2 : NULL,
+                      ctx->ab_in ? ctx->ab_in + (size_t)q * ctx->w2 * 2 : NULL,
+                      ctx->sel_out ? ctx->sel_out + (size_t)q * ctx->w2 : NULL,
+                      ctx->ab_out ? ctx->ab_out + (size_t)q * ctx->w2 * 2 : NULL);
 }
 
 /* search_batch (search.cpp:169-191); per-query scanned counts returned
@@ -409,7 +444,8 @@ int vo_search(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1
               uint32_t topk, int64_t* out_ids, float* out_dists, uint64_t* out_scanned,
               int nthreads) {
     if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
-    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, NULL, NULL};
+    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, NULL, NULL,
+                      NULL, NULL, NULL, NULL};
     return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
 }
 
@@ -420,7 +456,7 @@ int vo_search(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1
 int vo_first_level(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1, uint32_t* top_out,
                    int nthreads) {
     if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
-    search_ctx ctx = {ix, queries, w1, 1, 0, NULL, NULL, NULL, NULL, top_out};
+    search_ctx ctx = {ix, queries, w1, 1, 0, NULL, NULL, NULL, NULL, top_out, NULL, NULL, NULL, NULL};
     return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
 }
 
@@ -428,7 +464,29 @@ int vo_search_from_top(const vo_index* ix, const float* queries, uint64_t nq, ui
                        uint32_t topk, const uint32_t* top_in, int64_t* out_ids, float* out_dists,
                        uint64_t* out_scanned, int nthreads) {
     if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
-    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, top_in, NULL};
+    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, top_in, NULL,
+                      NULL, NULL, NULL, NULL};
+    return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
+}
+
+/* The search split after second_level_rank (the GPU engine's
+ * vlq_engine_search_select_device / _fine_sel_device): vo_select writes the
+ * w2 selected cells and their (a, b) of every query, vo_search_from_sel runs
+ * query_term5 .. select_topk from such a selection. */
+int vo_select(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1, float alpha, uint32_t* sel_out,
+              float* ab_out, int nthreads) {
+    if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
+    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), 0, NULL, NULL, NULL, NULL, NULL,
+                      NULL, NULL, sel_out, ab_out};
+    return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
+}
+
+int vo_search_from_sel(const vo_index* ix, const float* queries, uint64_t nq, uint32_t w1, float alpha,
+                       uint32_t topk, const uint32_t* sel_in, const float* ab_in, int64_t* out_ids, float* out_dists,
+                       uint64_t* out_scanned, int nthreads) {
+    if (w1 == 0 || w1 > ix->k) return fail("first_level_scan: need 0 < w1 <= k");
+    search_ctx ctx = {ix, queries, w1, vo_w2(w1, alpha, ix->n), topk, out_ids, out_dists, out_scanned, NULL, NULL,
+                      sel_in, ab_in, NULL, NULL};
     return par_for((int64_t)nq, 4, nthreads, &ctx, search_item, search_scratch, search_scratch_free);
 }
 

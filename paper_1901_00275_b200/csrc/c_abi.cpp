@@ -180,6 +180,25 @@ int vlq_engine_search_fine_device(vlq_engine* e, const float* d_queries, uint64_
     });
 }
 
+int vlq_engine_search_select_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                                    uint32_t* d_sel, float* d_ab, void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        e->impl->search_select_device(d_queries, nq, w1, alpha, d_sel, d_ab,
+                                      stream ? (cudaStream_t)stream : e->impl->stream());
+    });
+}
+
+int vlq_engine_search_fine_sel_device(vlq_engine* e, const float* d_queries, uint64_t nq, uint32_t w1, float alpha,
+                                      uint32_t k, const uint32_t* d_sel, const float* d_ab, int64_t* d_ids,
+                                      float* d_dists, uint64_t* d_scanned, void* stream) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        e->impl->search_fine_sel_device(d_queries, nq, w1, alpha, k, d_sel, d_ab, d_ids, d_dists, d_scanned,
+                                        stream ? (cudaStream_t)stream : e->impl->stream());
+    });
+}
+
 int vlq_engine_set_tuning(vlq_engine* e, const char* key, int64_t value) {
     ENGINE_OR_FAIL(e);
     if (!key) return fail(VLQ_ERR_INVALID, "set_tuning: key is NULL");
@@ -397,5 +416,7 @@ int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spr
         }
     });
 }
+
+uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n) { return vlq::w2_of(w1, alpha, n); }
 
 }  // extern "C"

@@ -474,26 +474,57 @@ void Engine::get_tables(std::vector<float>& t2, std::vector<float>& t3) {
 // ---------------------------------------------------------------------------
 // search: search_batch (search.cpp:169-191), tiled over queries
 // ---------------------------------------------------------------------------
+Engine::StageIO Engine::StageIO::at(uint64_t t0, uint32_t w1, uint32_t w2) const {
+    StageIO o;
+    o.top_in = top_in ? top_in + t0 * w1 : nullptr;
+    o.top_out = top_out ? top_out + t0 * w1 : nullptr;
+    o.sel_in = sel_in ? sel_in + t0 * w2 : nullptr;
+    o.ab_in = ab_in ? ab_in + t0 * w2 * 2 : nullptr;
+    o.sel_out = sel_out ? sel_out + t0 * w2 : nullptr;
+    o.ab_out = ab_out ? ab_out + t0 * w2 * 2 : nullptr;
+    return o;
+}
+
 void Engine::search_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
                            float* d_dists, uint64_t* d_scanned, cudaStream_t st) {
-    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, nullptr, nullptr, STAGE_ALL, st);
+    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, StageIO{}, STAGE_ALL, st);
 }
 
 void Engine::search_coarse_device(const float* d_q, uint64_t nq, uint32_t w1, uint32_t* d_top, cudaStream_t st) {
     if (!d_top) throw std::runtime_error("search_coarse: top output is NULL");
-    search_staged(d_q, nq, w1, 0.0f, 1, nullptr, nullptr, nullptr, nullptr, d_top, STAGE_COARSE, st);
+    StageIO io;
+    io.top_out = d_top;
+    search_staged(d_q, nq, w1, 0.0f, 1, nullptr, nullptr, nullptr, io, STAGE_COARSE, st);
 }
 
 void Engine::search_fine_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
                                 const uint32_t* d_top, int64_t* d_ids, float* d_dists, uint64_t* d_scanned,
                                 cudaStream_t st) {
     if (!d_top) throw std::runtime_error("search_fine: top input is NULL");
-    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, d_top, nullptr, STAGE_FINE, st);
+    StageIO io;
+    io.top_in = d_top;
+    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, io, STAGE_FINE, st);
+}
+void Engine::search_select_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t* d_sel,
+                                  float* d_ab, cudaStream_t st) {
+    if (!d_sel || !d_ab) throw std::runtime_error("search_select: selection output is NULL");
+    StageIO io;
+    io.sel_out = d_sel;
+    io.ab_out = d_ab;
+    search_staged(d_q, nq, w1, alpha, 1, nullptr, nullptr, nullptr, io, STAGE_SELECT, st);
+}
+void Engine::search_fine_sel_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
+                                    const uint32_t* d_sel, const float* d_ab, int64_t* d_ids, float* d_dists,
+                                    uint64_t* d_scanned, cudaStream_t st) {
+    if (!d_sel || !d_ab) throw std::runtime_error("search_fine_sel: selection input is NULL");
+    StageIO io;
+    io.sel_in = d_sel;
+    io.ab_in = d_ab;
+    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, io, STAGE_FINE_SEL, st);
 }
 
 void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
-                           float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
-                           Stage stage, cudaStream_t st) {
+                           float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st) {
     if (!model_ok_) throw std::runtime_error("search: no model loaded");
     if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
     if (topk > 1024) throw std::runtime_error("search: k > 1024 is not supported by the GPU engine");
@@ -527,13 +558,12 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
         const uint64_t nt = std::min(tile, nq - t0);
         search_tile(d_q + t0 * dim_, nt, w1, w2, topk, d_ids ? d_ids + t0 * topk : nullptr,
                     d_dists ? d_dists + t0 * topk : nullptr, d_scanned ? d_scanned + t0 : nullptr,
-                    d_top_in ? d_top_in + t0 * w1 : nullptr, d_top_out ? d_top_out + t0 * w1 : nullptr, stage, st);
+                    io.at(t0, w1, w2), stage, st);
     }
 }
 
 void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
-                         float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
-                         Stage stage, cudaStream_t st) {
+                         float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st) {
     auto mark = [&](int ph) { mark_phase(ph, st); };
     uint64_t launches = 0;
     bool tc = false, fast = false;
@@ -541,21 +571,31 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     if (stage == STAGE_FINE) {
         // top-w1 from another rank's coarse stage: exact distances of the
         // regions and neighbours the later stages read (as the TC path does)
-        CUDA_CHECK(cudaMemcpyAsync(top_.p, d_top_in, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
+        CUDA_CHECK(cudaMemcpyAsync(top_.p, io.top_in, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
         mark(PH_FIRST);
         if (exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024)
             launch_exact_needed(d_q, nt, dim_, centroids_.p, k_, n_, nbr_.p, ws_.p, top_.p, w1, st);
         else
             launch_sqdist_matrix(d_q, nt, centroids_.p, k_, dim_, ws_.p, k_, st);
         launches += 1;
+    } else if (stage == STAGE_FINE_SEL) {
+        mark(PH_FIRST);  // the selection (and its coarse values) comes from another rank
     } else {
         tc = coarse_tile(d_q, nt, w1, launches, st);
     }
     if (stage == STAGE_COARSE) {
-        CUDA_CHECK(cudaMemcpyAsync(d_top_out, top_.p, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
+        CUDA_CHECK(cudaMemcpyAsync(io.top_out, top_.p, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
         for (int p = PH_SECOND; p <= PH_COUNT; p++) mark(p);
+    } else if (stage == STAGE_SELECT) {
+        SearchArgs a = search_args();
+        mark(PH_SECOND);
+        launch_second_level(a, nt, w1, w2, st);
+        launch_pack_selection(a, nt, w2, io.sel_out, io.ab_out, st);
+        launches += 2;
+        for (int p = PH_TERM5; p <= PH_COUNT; p++) mark(p);
     } else {
-        fast = fine_tile(d_q, nt, w1, w2, topk, d_ids, d_dists, d_scanned, launches, st);
+        fast = fine_tile(d_q, nt, w1, w2, topk, d_ids, d_dists, d_scanned, launches, st,
+                         stage == STAGE_FINE_SEL ? &io : nullptr);
     }
     stats_.launches += launches;
     stats_.tiles += 1;
@@ -659,11 +699,13 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
 // second_level_rank -> query_term5 -> fused scan + top-k' -> exact re-score
 // (search.cpp:38-167) from top_ / ws_.  Returns whether the fast scan ran.
 bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
-                       float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st) {
+                       float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st,
+                       const StageIO* sel) {
     auto mark = [&](int ph) { mark_phase(ph, st); };
     SearchArgs a = search_args();
     mark(PH_SECOND);
-    launch_second_level(a, nt, w1, w2, st);
+    if (sel) launch_apply_selection(a, nt, w2, sel->sel_in, sel->ab_in, st);
+    else launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
     launch_term5(d_q, pq_.p, dim_, m_, t5_.p, meta_.p, nt, st);
     launches += 2;

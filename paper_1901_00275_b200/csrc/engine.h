@@ -169,6 +169,16 @@ public:
     void search_fine_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
                             const uint32_t* d_top, int64_t* d_ids, float* d_dists, uint64_t* d_scanned,
                             cudaStream_t st);
+    // Select-split schedule (dist.py): select = first_level_scan + second_level_rank
+    // for a query slice, publishing the selected cells [nq, w2] and their
+    // (a, b) pairs [nq, w2, 2]; fine_sel = everything after second_level_rank
+    // from a gathered selection, on this engine's shard.  select + fine_sel ==
+    // search_device.
+    void search_select_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t* d_sel, float* d_ab,
+                              cudaStream_t st);
+    void search_fine_sel_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
+                                const uint32_t* d_sel, const float* d_ab, int64_t* d_ids, float* d_dists,
+                                uint64_t* d_scanned, cudaStream_t st);
     void search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
                      float* dists, uint64_t* scanned);
     void check_device_errors(cudaStream_t st);
@@ -216,16 +226,25 @@ private:
     void pack_eterm_lam();
     AddArgs add_args() const;
     SearchArgs search_args() const;
-    enum Stage { STAGE_ALL = 0, STAGE_COARSE = 1, STAGE_FINE = 2 };
+    enum Stage { STAGE_ALL = 0, STAGE_COARSE = 1, STAGE_FINE = 2, STAGE_SELECT = 3, STAGE_FINE_SEL = 4 };
+    // stage inputs / outputs of the multi-GPU schedules (batch-level pointers)
+    struct StageIO {
+        const uint32_t* top_in = nullptr;  // STAGE_FINE: [nq, w1]
+        uint32_t* top_out = nullptr;       // STAGE_COARSE
+        const uint32_t* sel_in = nullptr;  // STAGE_FINE_SEL: [nq, w2] cells
+        const float* ab_in = nullptr;      //                 [nq, w2, 2]
+        uint32_t* sel_out = nullptr;       // STAGE_SELECT
+        float* ab_out = nullptr;
+        StageIO at(uint64_t t0, uint32_t w1, uint32_t w2) const;
+    };
     void search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
-                       float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
-                       Stage stage, cudaStream_t st);
+                       float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st);
     bool coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& launches, cudaStream_t st);
     bool fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
-                   float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st);
+                   float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st,
+                   const StageIO* sel = nullptr);
     void search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
-                     float* d_dists, uint64_t* d_scanned, const uint32_t* d_top_in, uint32_t* d_top_out,
-                     Stage stage, cudaStream_t st);
+                     float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st);
 
     EngineConfig cfg_;
     cudaStream_t stream_ = nullptr;

@@ -71,6 +71,12 @@ void launch_sqdist_matrix(const float* Y, uint64_t ny, const float* C, uint64_t 
                           uint64_t ldo, cudaStream_t st);
 void launch_first_level(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top, cudaStream_t st);
 void launch_second_level(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, cudaStream_t st);
+// select-split multi-GPU schedule: publish / apply a query's selected cells
+// with their (a, b) = (ws[i], ws[nbr]) pairs ([nq, w2] u32 / [nq, w2, 2] f32)
+void launch_pack_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t* sel_out, float* ab,
+                           cudaStream_t st);
+void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const uint32_t* sel_in, const float* ab,
+                            cudaStream_t st);
 void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
                   uint64_t nq, cudaStream_t st);
 size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);

@@ -170,6 +170,67 @@ __global__ void __launch_bounds__(512) k_second_level(SearchArgs a, uint32_t w1,
 }
 
 // ---------------------------------------------------------------------------
+// Select-split multi-GPU schedule (dist.py): the rank that ran
+// first_level_scan + second_level_rank for a query slice publishes, per
+// selected cell, (a, b) = (ws[i], ws[nbr(cell)]) -- the only coarse values the
+// later stages read -- and every shard engine applies the gathered selection:
+// the cells into sel, a and b back into its ws rows, and the LOCAL scanned
+// count and |term1| bound (exactly k_second_level's formulas) into meta.
+// ---------------------------------------------------------------------------
+__global__ void k_pack_selection(SearchArgs a, uint32_t w2, uint32_t* __restrict__ sel_out, float* __restrict__ ab) {
+    const uint64_t q = blockIdx.x;
+    const float* wsq = a.ws + q * a.k;
+    for (uint32_t t = threadIdx.x; t < w2; t += blockDim.x) {
+        const uint32_t cell = a.sel[q * w2 + t];
+        sel_out[q * w2 + t] = cell;
+        ab[(q * w2 + t) * 2] = wsq[cell / a.n];
+        ab[(q * w2 + t) * 2 + 1] = wsq[a.nbr[cell]];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t w2, const uint32_t* __restrict__ sel_in,
+                                                         const float* __restrict__ ab) {
+    __shared__ unsigned long long s_scanned;
+    __shared__ float s_dmax;
+    const uint64_t q = blockIdx.x;
+    float* wsq = a.ws + q * a.k;
+    if (threadIdx.x == 0) {
+        s_scanned = 0;
+        s_dmax = 0.0f;
+    }
+    __syncthreads();
+    const float lmax = a.lam_absmax;
+    unsigned long long cnt = 0;
+    float dmax = 0.0f;
+    for (uint32_t t = threadIdx.x; t < w2; t += blockDim.x) {
+        const uint32_t cell = sel_in[q * w2 + t];
+        a.sel[q * w2 + t] = cell;
+        const float av = ab[(q * w2 + t) * 2], bv = ab[(q * w2 + t) * 2 + 1], cv = a.elen[cell];
+        // equal values from every writer: both are the exact reference-order
+        // distance to that centroid
+        wsq[cell / a.n] = av;
+        wsq[a.nbr[cell]] = bv;
+        cnt += a.list_off[cell + 1] - a.list_off[cell];
+        const float bound = (1.0f + lmax) * fabsf(av) + (lmax * lmax + lmax) * fabsf(cv) + lmax * fabsf(bv);
+        dmax = fmaxf(dmax, bound);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_scanned, cnt);
+        atomicMax(reinterpret_cast<unsigned int*>(&s_dmax), __float_as_uint(dmax));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.meta[q].scanned = s_scanned;
+        a.meta[q].dmax = s_dmax;
+        a.meta[q].flag = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // term5 table (query_term5): t5[q][p][j] = dot(y_p, PQ[p][j]) in order; also
 // S5max = sum_p max_j |t5| for the certificate.
 // ---------------------------------------------------------------------------
@@ -459,6 +520,18 @@ void launch_first_level(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, u
 
 void launch_second_level(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, cudaStream_t st) {
     dev::k_second_level<<<(unsigned)nq, 512, a.Y ? a.dim * sizeof(float) : 0, st>>>(a, w1, w2);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_pack_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t* sel_out, float* ab,
+                           cudaStream_t st) {
+    dev::k_pack_selection<<<(unsigned)nq, 256, 0, st>>>(a, w2, sel_out, ab);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const uint32_t* sel_in, const float* ab,
+                            cudaStream_t st) {
+    dev::k_apply_selection<<<(unsigned)nq, 256, 0, st>>>(a, w2, sel_in, ab);
     CUDA_LAUNCH_CHECK();
 }
 

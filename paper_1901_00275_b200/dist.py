@@ -3,21 +3,30 @@ of one box (one process per GPU), coarse quantizer replicated, per-shard
 top-k merged by (dist, id) (the paper's "split the index into b parts, search
 locally, join").
 
-Each rank's engine holds regions i with i % world_size == rank.  Per batch:
+Each rank's engine holds regions i with i % world_size == rank.  Per batch
+(`ShardedIndex.search_select_split`, the default schedule):
 
-1. query-split coarse stage: rank r runs first_level_scan (the tensor-core
-   GEMM + exact refine, search.cpp:11-36) for its slice of the batch only;
-2. the slices' top-w1 region lists (nq x w1 u32, 2.5 MB at nq = 10k,
-   w1 = 64) are exchanged with one NCCL all-gather;
-3. every rank runs the rest of the search (second level, term5, fused scan,
-   exact re-score) for the whole batch on the cells it owns;
+1. query-split selection: rank r runs first_level_scan (the tensor-core GEMM
+   + exact refine, search.cpp:11-36) AND second_level_rank (search.cpp:38-78)
+   for its slice of the batch only -- everything whose cost does not shrink
+   with the shard;
+2. the slices' selections are exchanged with two NCCL all-gathers: the
+   selected cells (nq x w2 u32, 20 MB at nq = 10k, w2 = 512) and their exact
+   (a, b) = (|y - c_i|^2, |y - c_nbr|^2) pairs (41 MB), the only coarse values
+   the later stages read;
+3. every rank applies the gathered selection (its own scanned counts and
+   certificate bound) and runs term5, the fused scan and the exact re-score
+   for the whole batch on the cells it owns;
 4. the local exact top-k rows are all-gathered and merged by the K9 kernel
    (vlq_merge_topk_device).
 
+`search_query_split` is the earlier schedule: only first_level_scan is split
+(top-w1 tables, 2.5 MB, all-gathered) and every rank repeats the exact
+neighbour distances and second_level_rank for the whole batch.
+
 Because every shard returns its exact local top-k under the reference's total
 order, the merge is exactly the single-engine answer regardless of shard
-order, and the coarse stage (the one step whose cost does not shrink with the
-shard) is divided by the GPU count instead of replicated.
+order (both schedules).
 """
 from __future__ import annotations
 
@@ -91,6 +100,21 @@ def gather_top(local_top, nq: int, w1: int, group=None):
     return out[:nq]
 
 
+def gather_rows(local, nq: int, group=None):
+    """All-gathers every rank's [slice, ...] block (query_slice rows) into the
+    [nq, ...] batch table (slices padded to the common ceil size)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    per = (nq + world - 1) // world
+    tail = tuple(local.shape[1:])
+    send = torch.zeros((per,) + tail, dtype=local.dtype, device=local.device)
+    send[:local.shape[0]] = local
+    out = torch.empty((world * per,) + tail, dtype=local.dtype, device=local.device)
+    _all_gather(out, send, group)
+    return out[:nq]
+
+
 class ShardedIndex:
     """One rank's shard of a VLQ1 index plus the collective search."""
 
@@ -142,6 +166,37 @@ class ShardedIndex:
         ids, dists, scanned = out
         self.index.search_fine_device(d_queries.data_ptr(), nq, w1, alpha, k, top.data_ptr(), ids.data_ptr(),
                                       dists.data_ptr(), scanned.data_ptr(), st)
+        gi, gd = gather_parts(ids, dists, self.group)
+        mi, md = merge_topk(gi, gd, st)
+        return mi, md, scanned
+
+    def search_select_split(self, d_queries, w1: int, alpha: float, k: int, out=None):
+        """Query-split coarse stage and cell selection + sharded scan stage
+        (module docstring).  d_queries: the same CUDA float32 [nq, dim] batch
+        on every rank.  Returns the merged (ids, dists) and the local scanned
+        counts."""
+        import torch
+        import torch.distributed as dist
+        nq = d_queries.shape[0]
+        dev = d_queries.device
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        w2 = self.index.w2(w1, alpha)
+        lo, hi = query_slice(nq, rank, world)
+        sel_local = torch.empty((hi - lo, w2), dtype=torch.int32, device=dev)
+        ab_local = torch.empty((hi - lo, w2, 2), dtype=torch.float32, device=dev)
+        if hi > lo:
+            self.index.search_select_device(d_queries[lo:hi].data_ptr(), hi - lo, w1, alpha, sel_local.data_ptr(),
+                                            ab_local.data_ptr(), st)
+        sel = gather_rows(sel_local, nq, self.group).contiguous()
+        ab = gather_rows(ab_local, nq, self.group).contiguous()
+        if out is None:
+            out = (torch.empty((nq, k), dtype=torch.int64, device=dev),
+                   torch.empty((nq, k), dtype=torch.float32, device=dev),
+                   torch.empty((nq,), dtype=torch.int64, device=dev))
+        ids, dists, scanned = out
+        self.index.search_fine_sel_device(d_queries.data_ptr(), nq, w1, alpha, k, sel.data_ptr(), ab.data_ptr(),
+                                          ids.data_ptr(), dists.data_ptr(), scanned.data_ptr(), st)
         gi, gd = gather_parts(ids, dists, self.group)
         mi, md = merge_topk(gi, gd, st)
         return mi, md, scanned

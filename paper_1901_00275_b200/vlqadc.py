@@ -211,6 +211,31 @@ class Index:
                                                             ctypes.c_void_p(d_scanned) if d_scanned else None,
                                                             _stream(stream)))
 
+    def search_select_device(self, d_queries: int, nq: int, w1: int, alpha: float, d_sel: int, d_ab: int,
+                             stream: int | None = None) -> None:
+        """first_level_scan + second_level_rank (search.cpp:11-78): the selected
+        cells (uint32 [nq, w2]) and their exact (a, b) distances (float32
+        [nq, w2, 2]) into d_sel / d_ab.  Asynchronous."""
+        _lib.check(_lib.lib().vlq_engine_search_select_device(self._h, ctypes.c_void_p(d_queries), nq, w1, alpha,
+                                                              ctypes.c_void_p(d_sel), ctypes.c_void_p(d_ab),
+                                                              _stream(stream)))
+
+    def search_fine_sel_device(self, d_queries: int, nq: int, w1: int, alpha: float, k: int, d_sel: int, d_ab: int,
+                               d_ids: int, d_dists: int, d_scanned: int | None = None,
+                               stream: int | None = None) -> None:
+        """query_term5 .. select_topk (search.cpp:80-167) on this shard from a
+        given selection.  search_select_device + search_fine_sel_device ==
+        search_device.  Asynchronous."""
+        _lib.check(_lib.lib().vlq_engine_search_fine_sel_device(self._h, ctypes.c_void_p(d_queries), nq, w1, alpha,
+                                                                k, ctypes.c_void_p(d_sel), ctypes.c_void_p(d_ab),
+                                                                ctypes.c_void_p(d_ids), ctypes.c_void_p(d_dists),
+                                                                ctypes.c_void_p(d_scanned) if d_scanned else None,
+                                                                _stream(stream)))
+
+    def w2(self, w1: int, alpha: float) -> int:
+        """Cells scanned per query (QueryParams::w2, search.hpp:16-20)."""
+        return int(_lib.lib().vlq_w2(w1, alpha, self.n))
+
     def set_tuning(self, key: str, value: int) -> None:
         """Study knobs (scan_variant, scan_slots, tc_search_min_k, force_exact);
         results are identical for every setting."""

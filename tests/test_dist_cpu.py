@@ -148,6 +148,79 @@ def test_gloo_query_split_coarse_stage_merges_to_single_index(world, tmp_path):
         assert np.array_equal(np.asarray(md, np.float32).view(np.uint32), d.view(np.uint32))
 
 
+def _worker_select_split(rank, world, port, name, params, out_path):
+    """The select-split schedule of ShardedIndex.search_select_split with the
+    oracle standing in for the engine: first level + cell selection on this
+    rank's query slice only, all-gather of the selected cells and their
+    (a, b) pairs (dist.gather_rows), scan stage for the whole batch on this
+    rank's shard starting from the hand-off alone, all-gather of the top-k
+    blocks."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle, vlq1
+    from paper_1901_00275_b200.dist import gather_parts, gather_rows, query_slice
+    z, index_path, _ = load_golden(name)
+    ix = vlq1.read(index_path)
+    full = oracle.OracleIndex(ix)                      # the replicated coarse quantizer
+    shard = oracle.OracleIndex(shard_of(ix, rank, world))
+    q = z["queries"]
+    res = []
+    for w1, alpha, k in params:
+        lo, hi = query_slice(q.shape[0], rank, world)
+        sel_l, ab_l = full.select(q[lo:hi], w1, alpha)
+        sel = gather_rows(torch.from_numpy(sel_l.view(np.int32)), q.shape[0]).numpy().view(np.uint32)
+        ab = gather_rows(torch.from_numpy(ab_l), q.shape[0]).numpy()
+        ids, d, _ = shard.search_from_sel(q, sel, ab, w1, alpha, k)
+        gi, gd = gather_parts(torch.from_numpy(ids), torch.from_numpy(d))
+        res.append((gi.numpy(), gd.numpy()))
+    if rank == 0:
+        import pickle
+        with open(out_path, "wb") as f:
+            pickle.dump([merge_np(*r) for r in res], f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_select_split_merges_to_single_index(world, tmp_path):
+    import torch.multiprocessing as mp
+    from oracle import oracle
+    name = "accept_small"
+    params = [(16, 0.5, 10), (64, 0.25, 100), (3, 1.0, 5)]
+    out = str(tmp_path / "merged.pkl")
+    mp.start_processes(_worker_select_split, args=(world, _free_port(), name, params, out), nprocs=world, join=True,
+                       start_method="spawn")
+    import pickle
+    with open(out, "rb") as f:
+        merged = pickle.load(f)
+    z, index_path, _ = load_golden(name)
+    o = oracle.OracleIndex.load(index_path)
+    for (w1, alpha, k), (mi, md) in zip(params, merged):
+        ids, d, _ = o.search(z["queries"], w1, alpha, k)
+        assert np.array_equal(mi, ids)
+        assert np.array_equal(np.asarray(md, np.float32).view(np.uint32), d.view(np.uint32))
+
+
+def test_oracle_select_split_equals_search():
+    """select() + search_from_sel() (the hand-off alone: the scan stage sees
+    only the selected cells and their a, b) equals search()."""
+    from oracle import oracle
+    for name in ("m16", "accept_small"):
+        z, index_path, _ = load_golden(name)
+        o = oracle.OracleIndex.load(index_path)
+        q = z["queries"]
+        for w1, alpha, k in [(8, 0.5, 10), (32, 0.25, 100), (o.ix.k, 1.0, 7)]:
+            sel, ab = o.select(q, w1, alpha)
+            a = o.search(q, w1, alpha, k)
+            b = o.search_from_sel(q, sel, ab, w1, alpha, k)
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y)
+
+
 def test_query_slices_cover_the_batch():
     from paper_1901_00275_b200.dist import query_slice
     for nq in (0, 1, 7, 100, 10_000):

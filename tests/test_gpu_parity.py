@@ -269,6 +269,62 @@ def test_query_split_staged_search_matches_single_engine(vlqadc, monkeypatch, tc
         assert same_f32(got_d.cpu().numpy(), want_d), (w1, alpha, k)
 
 
+@pytest.mark.parametrize("tc", ["0", "1"])
+def test_select_split_staged_search_matches_single_engine(vlqadc, oracle_mod, monkeypatch, tc):
+    """The select-split multi-GPU schedule on one device: first level + cell
+    selection (search_select_device) per query slice, the slices' cells and
+    (a, b) pairs concatenated, every shard engine runs search_fine_sel_device
+    on the whole batch, and the K9 merge equals the unsharded search
+    bit-exactly; the hand-off equals the oracle's (select())."""
+    import torch
+    from paper_1901_00275_b200 import dist as vdist
+    monkeypatch.setenv("VLQ_TC_MIN_K", "0" if tc == "1" else "100000000")
+    z, index_path, _ = load_golden("accept_small")
+    full = vlqadc.Index.load(index_path)
+    o = oracle_mod.OracleIndex.load(index_path)
+    G = 3
+    shards = [vlqadc.Index.load(index_path, shard_rank=r, shard_count=G) for r in range(G)]
+    q = torch.from_numpy(z["queries"]).cuda()
+    nq = q.shape[0]
+    st = torch.cuda.current_stream().cuda_stream
+    for w1, alpha, k in [(16, 0.5, 10), (64, 0.25, 100), (5, 1.0, 7)]:
+        want_ids, want_d = full.search(z["queries"], w1=w1, alpha=alpha, k=k)
+        w2 = full.w2(w1, alpha)
+        sels, abs_ = [], []
+        for r in range(G):
+            lo, hi = vdist.query_slice(nq, r, G)
+            sl = torch.empty((hi - lo, w2), dtype=torch.int32, device="cuda")
+            ab = torch.empty((hi - lo, w2, 2), dtype=torch.float32, device="cuda")
+            if hi > lo:
+                shards[r].search_select_device(q[lo:hi].data_ptr(), hi - lo, w1, alpha, sl.data_ptr(), ab.data_ptr(),
+                                               st)
+            sels.append(sl)
+            abs_.append(ab)
+        sel = torch.cat(sels).contiguous()
+        ab = torch.cat(abs_).contiguous()
+        osel, oab = o.select(z["queries"], w1, alpha)
+        torch.cuda.synchronize()
+        # the same cell SET per query (the engine lists it by edge position,
+        # the oracle by distance), with the same (a, b) for each cell
+        gsel, gab = sel.cpu().numpy().view(np.uint32), ab.cpu().numpy()
+        gi_, oi_ = np.argsort(gsel, axis=1), np.argsort(osel, axis=1)
+        assert np.array_equal(np.take_along_axis(gsel, gi_, 1), np.take_along_axis(osel, oi_, 1))
+        assert same_f32(np.take_along_axis(gab, gi_[:, :, None], 1), np.take_along_axis(oab, oi_[:, :, None], 1))
+        pi, pd = [], []
+        for s in shards:
+            ids = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+            d = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+            s.search_fine_sel_device(q.data_ptr(), nq, w1, alpha, k, sel.data_ptr(), ab.data_ptr(), ids.data_ptr(),
+                                     d.data_ptr(), None, st)
+            pi.append(ids)
+            pd.append(d)
+        got_i, got_d = vdist.merge_topk(torch.stack(pi), torch.stack(pd))
+        for s in shards:
+            s.sync(st)
+        assert np.array_equal(got_i.cpu().numpy(), want_ids), (w1, alpha, k)
+        assert same_f32(got_d.cpu().numpy(), want_d), (w1, alpha, k)
+
+
 @pytest.mark.slow
 def test_acceptance_c7_trend_kats(vlqadc, tmp_path):
     """acceptance.cpp:330-363 on the reference's 'big' instance, built by the
