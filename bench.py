@@ -10,11 +10,13 @@ GPU ground truth for a query subset.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
 
-Under torchrun (N > 1) each rank holds the regions i % N == rank of the same
-index; each rank runs the coarse stage for 1/N of the batch, the top-w1 tables
-are all-gathered (NCCL), every rank scans its shard for the whole batch, and
-the per-shard exact top-k are all-gathered and merged by (dist, id) --
-scaling "strong" (the index and batch are fixed, the lists are split).
+Under torchrun (N > 1) each rank holds the posting lists c with
+shard_of_cell(c, N) == rank of the same index; each rank runs the first level
+and the cell selection for 1/N of the batch, the selections (cells + exact
+(a, b) pairs) are all-gathered (NCCL), every rank scans its shard for the
+whole batch, and the per-shard exact top-k are all-gathered and merged by
+(dist, id) (dist.ShardedIndex.search_select_split) -- scaling "strong" (the
+index and batch are fixed, the lists are split).
 
 `value` is device-timed (CUDA events, queries resident in HBM, L2 flushed
 between steps, max over ranks).  `e2e` is the same metric through the public

@@ -40,7 +40,8 @@ typedef struct vlq_engine vlq_engine;
 
 typedef struct {
     int device;                /* CUDA ordinal */
-    int shard_rank;            /* regions i with i % shard_count == shard_rank live here */
+    int shard_rank;            /* posting lists c with ((c * 0x9E3779B97F4A7C15) >> 40) % shard_count
+                                  == shard_rank live here (64-bit product) */
     int shard_count;           /* 1 = whole index on this device */
     uint64_t workspace_bytes;  /* per-query-tile scratch budget (0 = 4 GiB) */
     uint32_t max_tile;         /* max queries per tile (0 = 16384) */
@@ -210,7 +211,9 @@ int vlq_engine_encode(vlq_engine* e, const float* x, uint64_t n, uint32_t* cells
 
 /* Merges nparts per-shard top-k result blocks [nparts][nq][k] (device
  * pointers) into the global (dist, id) top-k (the paper's multi-GPU join,
- * PAPER.md:498-499). */
+ * PAPER.md:498-499).  Every row must be ascending by (dist, id) with -1/+inf
+ * padding at the end -- as every search output is -- and an id may appear in
+ * one part only (each base point lives in one shard). */
 int vlq_merge_topk_device(int device, const int64_t* d_in_ids, const float* d_in_dists, uint32_t nparts, uint64_t nq,
                           uint32_t k, int64_t* d_out_ids, float* d_out_dists, void* stream);
 

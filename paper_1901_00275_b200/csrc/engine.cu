@@ -31,12 +31,9 @@ void h2d(DevBuf<T>& dst, const std::vector<T>& src, cudaStream_t st) {
     if (!src.empty()) CUDA_CHECK(cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
 }
 
-__global__ void k_mask_cells(uint32_t* cells, uint64_t n, uint32_t nedges, uint32_t shards, uint32_t rank,
-                             uint32_t sentinel) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t region = cells[i] / nedges;
-        if (region % shards != rank) cells[i] = sentinel;
-    }
+__global__ void k_mask_cells(uint32_t* cells, uint64_t n, uint32_t shards, uint32_t rank, uint32_t sentinel) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if (shard_of_cell(cells[i], shards) != rank) cells[i] = sentinel;
 }
 
 }  // namespace
@@ -350,7 +347,7 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
     const uint32_t ncell = k_ * n_;
     const uint32_t sentinel = ncell;
     if (cfg_.shard_count > 1) {
-        k_mask_cells<<<1184, 256, 0, st>>>(cells.p, nb, n_, (uint32_t)cfg_.shard_count, (uint32_t)cfg_.shard_rank,
+        k_mask_cells<<<1184, 256, 0, st>>>(cells.p, nb, (uint32_t)cfg_.shard_count, (uint32_t)cfg_.shard_rank,
                                            sentinel);
         CUDA_LAUNCH_CHECK();
     }
@@ -1032,7 +1029,7 @@ void Engine::load_vlq1(const std::string& path) {
             else seen[id] = 1;
         }
         total += len;
-        const bool own = owner((uint32_t)(c / m.n)) == cfg_.shard_rank;
+        const bool own = owner((uint32_t)c) == cfg_.shard_rank;
         if (own) {
             L.ids.insert(L.ids.end(), ids.begin(), ids.end());
             L.codes.insert(L.codes.end(), codes.begin(), codes.begin() + (size_t)len * m.m);

@@ -607,6 +607,58 @@ __global__ void k_emit_exact(SearchArgs a, const uint32_t* __restrict__ qlist, c
 
 // Merges nparts per-shard top-k rows (each ascending by (dist, id), padded
 // with -1/+inf) into the global top-k under the same total order.
+// K9 on sorted parts (every search output row is ascending by (dist, id),
+// padded with -1 / +inf): the merged position of a part's r-th key is r plus
+// the number of smaller keys in every other part (a binary search each;
+// keys are unique since every id lives in exactly one shard).  No sort, two
+// block barriers.
+__global__ void __launch_bounds__(256) k_merge_sorted(const int64_t* __restrict__ in_ids, const float* __restrict__ in_d,
+                                                      uint32_t nparts, uint64_t nq, uint32_t topk,
+                                                      int64_t* __restrict__ out_ids, float* __restrict__ out_d) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [nparts][topk]
+    uint64_t* res = keys + (size_t)nparts * topk;         // [topk]
+    const uint64_t q = blockIdx.x;
+    const uint32_t total = nparts * topk;
+    for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint32_t part = t / topk, r = t % topk;
+        const uint64_t src = ((uint64_t)part * nq + q) * topk + r;
+        const int64_t id = in_ids[src];
+        keys[t] = id >= 0 ? make_key(in_d[src], (uint32_t)id) : ~0ull;
+    }
+    for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) res[t] = ~0ull;
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint64_t key = keys[t];
+        if (key == ~0ull) continue;
+        const uint32_t part = t / topk;
+        uint32_t pos = t % topk;
+        for (uint32_t g = 0; g < nparts && pos < topk; g++) {
+            if (g == part) continue;
+            const uint64_t* row = keys + (size_t)g * topk;
+            uint32_t lo = 0, hi = topk;  // count of keys < key in row g
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (row[mid] < key) lo = mid + 1;
+                else hi = mid;
+            }
+            pos += lo;
+        }
+        if (pos < topk) res[pos] = key;
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) {
+        const uint64_t key = res[t];
+        if (key != ~0ull) {
+            out_ids[q * topk + t] = (int64_t)(uint32_t)key;
+            out_d[q * topk + t] = unord_float((uint32_t)(key >> 32));
+        } else {
+            out_ids[q * topk + t] = -1;
+            out_d[q * topk + t] = __int_as_float(0x7f800000);
+        }
+    }
+}
+
 __global__ void k_merge_topk(const int64_t* __restrict__ in_ids, const float* __restrict__ in_d, uint32_t nparts,
                              uint64_t nq, uint32_t topk, uint32_t npow2, int64_t* __restrict__ out_ids,
                              float* __restrict__ out_d) {
@@ -649,6 +701,14 @@ void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigne
 void launch_merge_topk(const int64_t* in_ids, const float* in_d, uint32_t nparts, uint64_t nq, uint32_t topk,
                        int64_t* out_ids, float* out_d, cudaStream_t st) {
     if (nq == 0 || topk == 0) return;
+    const size_t smem_sorted = ((size_t)nparts + 1) * topk * 8;
+    if (smem_sorted <= 200 * 1024) {
+        CUDA_CHECK(cudaFuncSetAttribute(dev::k_merge_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem_sorted));
+        dev::k_merge_sorted<<<(unsigned)nq, 256, smem_sorted, st>>>(in_ids, in_d, nparts, nq, topk, out_ids, out_d);
+        CUDA_LAUNCH_CHECK();
+        return;
+    }
     uint32_t n = 1;
     while (n < nparts * topk) n <<= 1;
     size_t smem = (size_t)n * 8;

@@ -3,7 +3,10 @@ of one box (one process per GPU), coarse quantizer replicated, per-shard
 top-k merged by (dist, id) (the paper's "split the index into b parts, search
 locally, join").
 
-Each rank's engine holds regions i with i % world_size == rank.  Per batch
+Each rank's engine holds the posting lists (cells) c with
+((c * 0x9E3779B97F4A7C15) mod 2^64 >> 40) % world_size == rank (csrc/engine.h
+shard_of_cell: a hash, so every region's n lists and every hub region spread
+over all ranks).  Per batch
 (`ShardedIndex.search_select_split`, the default schedule):
 
 1. query-split selection: rank r runs first_level_scan (the tensor-core GEMM

@@ -1,7 +1,7 @@
 """CPU test of the multi-GPU path's host logic (gloo, world_size 2).
 
-Each rank holds the regions i % world == rank of the golden index (the
-engine's shard rule, csrc/engine.h Engine::owner), searches its shard, and the
+Each rank holds the posting lists c with shard_of_cell(c, world) == rank of the
+golden index (the engine's shard rule, csrc/engine.h), searches its shard, and the
 per-shard top-k blocks are exchanged with paper_1901_00275_b200.dist.gather_parts
 (the same call the NCCL path uses).  The (dist, id) merge of the gathered
 blocks must equal the unsharded search.  The shard search and the merge here
@@ -23,11 +23,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def shard_of_cell(c, shards):
+    """The engine's list ownership (csrc/engine.h shard_of_cell)."""
+    return (((c * 0x9E3779B97F4A7C15) & ((1 << 64) - 1)) >> 40) % shards
+
+
 def shard_of(ix, rank, world):
     from oracle import vlq1
     keep = np.zeros(ix.k * ix.n, bool)
     for c in range(ix.k * ix.n):
-        keep[c] = (c // ix.n) % world == rank
+        keep[c] = shard_of_cell(c, world) == rank
     lens = np.diff(ix.list_off.astype(np.int64))
     lens = np.where(keep, lens, 0)
     off = np.zeros(ix.k * ix.n + 1, np.uint64)

@@ -351,3 +351,35 @@ def test_acceptance_c7_trend_kats(vlqadc, tmp_path):
     for alpha, total in want_scan.items():
         _, _, sc = idx.search(q, w1=64, alpha=alpha, k=10, return_scanned=True)
         assert int(sc.sum()) == total, (alpha, int(sc.sum()))
+
+
+@pytest.mark.parametrize("G,k", [(2, 10), (8, 100), (3, 1), (5, 37)])
+def test_merge_of_sorted_parts_random(vlqadc, G, k):
+    """K9 on random sorted parts (ragged: each part holds a random number of
+    real rows, -1/+inf padded; equal distances across parts broken by id)
+    equals a host (dist, id) merge."""
+    import torch
+    from paper_1901_00275_b200 import dist as vdist
+    rng = np.random.default_rng(G * 100 + k)
+    nq = 64
+    ids = np.full((G, nq, k), -1, np.int64)
+    d = np.full((G, nq, k), np.inf, np.float32)
+    perm = rng.permutation(G * nq * k)  # unique ids across parts
+    for g in range(G):
+        for q in range(nq):
+            n = int(rng.integers(0, k + 1))
+            dd = np.round(rng.uniform(0, 4, n), 1).astype(np.float32)  # many ties
+            ii = perm[(g * nq + q) * k:(g * nq + q) * k + n].astype(np.int64)
+            o = np.lexsort((ii, dd))
+            ids[g, q, :n], d[g, q, :n] = ii[o], dd[o]
+    got_i, got_d = vdist.merge_topk(torch.from_numpy(ids).cuda(), torch.from_numpy(d).cuda())
+    got_i, got_d = got_i.cpu().numpy(), got_d.cpu().numpy()
+    for q in range(nq):
+        m = ids[:, q, :] >= 0
+        ci, cd = ids[:, q, :][m], d[:, q, :][m]
+        o = np.lexsort((ci, cd))[:k]
+        want_i = np.full(k, -1, np.int64)
+        want_d = np.full(k, np.inf, np.float32)
+        want_i[:len(o)], want_d[:len(o)] = ci[o], cd[o]
+        assert np.array_equal(got_i[q], want_i), q
+        assert same_f32(got_d[q], want_d)
