@@ -718,7 +718,9 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
         a.scan_cap = cfg_.scan_cap;
-        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, cfg_.scan_slots, cfg_.scan_prefetch, st))
+        a.sel_agg = cfg_.scan_sel_agg != 0;
+        const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
+        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, slots, cfg_.scan_prefetch, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
@@ -766,6 +768,7 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
     else if (key == "scan_cap") cfg_.scan_cap = (uint32_t)value;
+    else if (key == "scan_sel_agg") cfg_.scan_sel_agg = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 

@@ -51,6 +51,7 @@ struct SearchArgs {
     const uint32_t* eterm_lam;
     float e_pack_err;
     uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
+    bool sel_agg;       // fast-scan flush: warp-aggregated (match_any) histogram atomics
 };
 
 // Add-path device views.

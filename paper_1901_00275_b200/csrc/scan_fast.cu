@@ -112,19 +112,60 @@ __device__ __forceinline__ void bitonic_merge_warp(uint64_t* a, uint32_t n, uint
 // Block-wide radix select over the block-shared candidate buffer: keeps
 // exactly the `keep` smallest u64 keys (compacted, unordered) and returns the
 // largest kept key.  Keys are unique (dist bits | entry position).  Digits of
-// 8 bits from the top; stops early once the selected bin is taken whole.
+// 8 bits from the first byte in which the keys differ (an AND / OR reduction
+// skips the common leading bytes -- the sign/exponent byte every distance of
+// a query shares, whose histogram was one fully contended bin); histogram
+// atomics are aggregated per warp (__match_any_sync); stops early once the
+// selected bin is taken whole; compaction reserves output slots per warp.
+// `hist` >= 256 words, `s_misc` >= 48 words of shared scratch.
 __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep, uint32_t* hist,
-                                      unsigned int* s_misc) {
-    const uint32_t tid = threadIdx.x, nt = blockDim.x;
-    uint64_t prefix = 0, pmask = 0;
+                                      unsigned int* s_misc, bool agg = false) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u, warp = tid >> 5, nwarps = nt >> 5;
+    // 0. common leading bits of all keys
+    uint64_t kand = ~0ull, kor = 0;
+    for (uint32_t i = tid; i < n; i += nt) {
+        const uint64_t k = cbuf[i];
+        kand &= k;
+        kor |= k;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+    }
+    if (lane == 0) {  // hist as scratch: 4 words per warp (hist is only 4-byte aligned)
+        hist[4 * warp] = (uint32_t)kand;
+        hist[4 * warp + 1] = (uint32_t)(kand >> 32);
+        hist[4 * warp + 2] = (uint32_t)kor;
+        hist[4 * warp + 3] = (uint32_t)(kor >> 32);
+    }
+    __syncthreads();
+    kand = ~0ull;
+    kor = 0;
+    for (uint32_t w = 0; w < nwarps; w++) {
+        kand &= ((uint64_t)hist[4 * w + 1] << 32) | hist[4 * w];
+        kor |= ((uint64_t)hist[4 * w + 3] << 32) | hist[4 * w + 2];
+    }
+    __syncthreads();  // hist is reused below
+    const uint64_t diff = kand ^ kor;
+    int sh = diff ? ((63 - __clzll((long long)diff)) & ~7) : 0;
+    uint64_t pmask = sh >= 56 ? 0ull : ~((1ull << (sh + 8)) - 1ull);
+    uint64_t prefix = kand & pmask;
     uint32_t remaining = keep;
-    int sh = 56;
+    const uint32_t n_all = ((n + nt - 1) / nt) * nt;  // every lane runs the same trip count (match_any)
     for (; sh >= 0; sh -= 8) {
         for (uint32_t b = tid; b < 256; b += nt) hist[b] = 0;
         __syncthreads();
-        for (uint32_t i = tid; i < n; i += nt) {
-            const uint64_t k = cbuf[i];
-            if ((k & pmask) == prefix) atomicAdd(&hist[(uint32_t)(k >> sh) & 255u], 1u);
+        for (uint32_t i = tid; i < n_all; i += nt) {
+            const uint64_t k = i < n ? cbuf[i] : 0ull;
+            const bool valid = i < n && (k & pmask) == prefix;
+            const uint32_t d = valid ? ((uint32_t)(k >> sh) & 255u) : (256u + lane);  // invalid: no peers
+            if (agg) {
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                if (valid && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+            } else if (valid) {
+                atomicAdd(&hist[d], 1u);
+            }
         }
         __syncthreads();
         if (tid < 32) {  // warp 0: scan 256 bins (8 per lane), find the crossing bin
@@ -160,16 +201,30 @@ __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep,
         if (inbin == remaining) break;  // the whole bin is kept
     }
     const uint64_t T = sh > 0 ? (prefix | ((1ull << sh) - 1ull)) : prefix;  // keep keys <= T
-    // in-place ordered compaction, one block-sized chunk at a time
-    uint32_t written = 0;
-    for (uint32_t base = 0; base < n; base += nt) {
-        const uint32_t i = base + tid;
-        const uint64_t k = i < n ? cbuf[i] : ~0ull;
-        const uint32_t take = (i < n && k <= T) ? 1u : 0u;
-        uint32_t total;
-        const uint32_t ex = block_excl_scan_u32(take, s_misc + 8, &total);
-        if (take) cbuf[written + ex] = k;
-        written += total;
+    // in-place compaction in chunks of 8 keys per thread: the chunk is read
+    // into registers before any slot is written, and every written slot lies
+    // below the chunk's end, so no unread key is overwritten
+    constexpr uint32_t R = 8;
+    if (tid == 0) s_misc[3] = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += R * nt) {
+        uint64_t k[R];
+        uint32_t take = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < R; r++) {
+            const uint32_t i = base + r * nt + tid;
+            k[r] = i < n ? cbuf[i] : ~0ull;
+            take |= (i < n && k[r] <= T ? 1u : 0u) << r;
+        }
+        __syncthreads();
+#pragma unroll
+        for (uint32_t r = 0; r < R; r++) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (take >> r) & 1u);
+            uint32_t slot = 0;
+            if (lane == 0 && bal) slot = atomicAdd(&s_misc[3], (uint32_t)__popc(bal));
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if ((take >> r) & 1u) cbuf[slot + __popc(bal & ((1u << lane) - 1u))] = k[r];
+        }
         __syncthreads();
     }
     return T;
@@ -362,7 +417,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 || U 
         n_seen += rlen * nwarps * CH;
         const uint32_t cnt = s_count;
         if (cnt > keep && cnt > cap / 2) {  // block-uniform
-            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc, a.sel_agg);
             __syncthreads();
             if (threadIdx.x == 0) {
                 s_count = keep;
@@ -381,7 +436,7 @@ __global__ void __launch_bounds__(R == 2 ? 512 : 256, R == 2 ? 1 : (R == 1 || U 
     // final: exactly min(count, keep) smallest keys, sorted, padded with +inf
     uint32_t n = s_count;
     if (n > keep) {
-        block_select_keep(cbuf, n, keep, hist, s_misc);
+        block_select_keep(cbuf, n, keep, hist, s_misc, a.sel_agg);
         n = keep;
     }
     __syncthreads();
@@ -772,7 +827,7 @@ __global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t 
         n_seen += rlen * nwarps * CH;
         const uint32_t cnt = s_count;
         if (cnt > keep && cnt > cap / 2) {  // block-uniform
-            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc, a.sel_agg);
             __syncthreads();
             if (threadIdx.x == 0) {
                 s_count = keep;
@@ -788,7 +843,7 @@ __global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t 
     }
     uint32_t n = s_count;
     if (n > keep) {
-        block_select_keep(cbuf, n, keep, hist, s_misc);
+        block_select_keep(cbuf, n, keep, hist, s_misc, a.sel_agg);
         n = keep;
     }
     __syncthreads();
@@ -1066,7 +1121,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t 
         n_seen += rlen * NWARPS * CH;
         const uint32_t cnt = s_count;
         if (cnt > keep && cnt > cap / 2) {  // block-uniform
-            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc);
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc, a.sel_agg);
             __syncthreads();
             if (threadIdx.x == 0) {
                 s_count = keep;
@@ -1082,7 +1137,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_bulk(SearchArgs a, uint32_t 
     }
     uint32_t n = s_count;
     if (n > keep) {
-        block_select_keep(cbuf, n, keep, hist, s_misc);
+        block_select_keep(cbuf, n, keep, hist, s_misc, a.sel_agg);
         n = keep;
     }
     __syncthreads();
