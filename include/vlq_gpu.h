@@ -96,6 +96,14 @@ int vlq_engine_train(vlq_engine* e, const float* train, uint64_t nt, uint32_t di
  * observe_lambda_range for unclamped models (bindings.cpp:83-97). */
 int vlq_engine_add(vlq_engine* e, const float* base, uint64_t n, uint32_t dim);
 
+/* Index.add of a vector file without loading it into host memory: the
+ * reference's read_vecs (vecs_io.cpp:29-86: .bvecs -> bytes, .ivecs -> int32,
+ * otherwise float32; every record's dimension checked; same error texts)
+ * followed by build_index, streamed through double-buffered pinned staging
+ * (chunk_rows rows per chunk, 0 = 128 MiB of floats).  Ids are the record
+ * numbers.  Equivalent to vlq_engine_add(read_vecs(path)). */
+int vlq_engine_add_vecs(vlq_engine* e, const char* path, uint64_t chunk_rows);
+
 /* Index.search: search_batch (proj/src/search.cpp:169-191) with the
  * binding's padding (bindings.cpp:111-125): out_ids/out_dists are nq*k,
  * rows ascending by (dist, id), unfilled slots -1/+inf.  out_scanned

@@ -142,6 +142,14 @@ int vlq_engine_add(vlq_engine* e, const float* base, uint64_t n, uint32_t dim) {
     });
 }
 
+int vlq_engine_add_vecs(vlq_engine* e, const char* path, uint64_t chunk_rows) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (!path) throw std::runtime_error("add_vecs: path is NULL");
+        e->impl->add_vecs(path, chunk_rows);
+    });
+}
+
 int vlq_engine_search(vlq_engine* e, const float* queries, uint64_t nq, uint32_t dim, uint32_t w1, float alpha,
                       uint32_t k, int64_t* out_ids, float* out_dists, uint64_t* out_scanned) {
     ENGINE_OR_FAIL(e);

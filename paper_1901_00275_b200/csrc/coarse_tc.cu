@@ -782,7 +782,8 @@ __global__ void __launch_bounds__(256) k_exact_needed(const float* __restrict__ 
 // the filter pass compares against (at least L centroids pass).
 __global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
                                                   uint32_t* __restrict__ scratch, float* __restrict__ tau,
-                                                  const float* __restrict__ Y, uint32_t dim, float cmax) {
+                                                  const float* __restrict__ Y, uint32_t dim, float cmax,
+                                                  int pass2_split) {
     __shared__ uint32_t hist[2048];
     __shared__ uint32_t scan[40];
     __shared__ unsigned int s_max;
@@ -802,9 +803,10 @@ __global__ void __launch_bounds__(512) k_tau_rows(const float* __restrict__ tmin
         if (Y) {
             float yn = 0.0f;
             for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
-            // approx3 <= approx1 + eps1 + eps3: the L centroids under tau1
-            // (1xTF32) are all under tau1 + eps1 + eps3 (3xTF32)
-            t += (tc_eps(yn, cmax, dim, false) + tc_eps(yn, cmax, dim, true)) * 1.01f;
+            // approx2 <= approx1 + eps1 + eps2: the L centroids under tau1
+            // (1xTF32) are all under tau1 + eps1 + eps2, eps2 the bound of the
+            // filter pass (3xTF32, or 1xTF32 again when pass2_split == 0)
+            t += (tc_eps(yn, cmax, dim, false) + tc_eps(yn, cmax, dim, pass2_split != 0)) * 1.01f;
         }
         tau[q] = t;
     }
@@ -976,9 +978,9 @@ void launch_exact_needed(const float* Y, uint64_t nq, uint32_t dim, const float*
 
 
 void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
-                     cudaStream_t st, const float* Y, uint32_t dim, float cmax) {
+                     cudaStream_t st, const float* Y, uint32_t dim, float cmax, int pass2_split) {
     if (nq == 0) return;
-    dev::k_tau_rows<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, scratch, tau, Y, dim, cmax);
+    dev::k_tau_rows<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, scratch, tau, Y, dim, cmax, pass2_split);
     CUDA_LAUNCH_CHECK();
 }
 

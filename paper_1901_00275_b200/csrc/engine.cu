@@ -279,6 +279,87 @@ void Engine::add_host(const float* base, uint64_t nb) {
     });
 }
 
+void Engine::add_vecs(const std::string& path, uint64_t chunk_rows) {
+    if (!model_ok_) throw std::runtime_error("add: no model loaded");
+    if (base_count_ != 0) throw std::runtime_error("index already holds a base set");
+    auto ends_with = [&](const char* suf) {  // vecs_kind_from_path (vecs_io.cpp:11-23)
+        const size_t n = std::strlen(suf);
+        return path.size() >= n && path.compare(path.size() - n, n, suf) == 0;
+    };
+    const int kind = ends_with(".bvecs") ? 1 : (ends_with(".ivecs") ? 2 : 0);  // 0 f32, 1 u8, 2 i32
+    const uint64_t vsz = kind == 1 ? 1 : 4;
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("read_vecs: cannot open " + path);
+    struct Closer {
+        std::FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    int32_t d0 = 0;
+    const size_t got = std::fread(&d0, 1, 4, f);
+    if (got == 0) throw std::runtime_error("read_vecs: no records in " + path);
+    if (got != 4) throw std::runtime_error("read_vecs: truncated record header in " + path);
+    if (d0 <= 0) throw std::runtime_error("read_vecs: non-positive dimension in " + path);
+    if (std::fseek(f, 0, SEEK_END) != 0) throw std::runtime_error("read_vecs: cannot seek " + path);
+    const uint64_t fsize = (uint64_t)std::ftell(f);
+    const uint64_t rowb = 4 + (uint64_t)d0 * vsz;
+    const uint64_t nb = fsize / rowb;
+    if (nb * rowb != fsize) {  // the reference reads record by record and fails on the partial last one
+        const uint64_t tail = fsize - nb * rowb;
+        throw std::runtime_error(tail < 4 ? "read_vecs: truncated record header in " + path
+                                          : "read_vecs: truncated record payload in " + path);
+    }
+    if ((uint32_t)d0 != dim_) throw std::runtime_error("build_index: dimension mismatch");
+    const uint64_t chunk = chunk_rows ? chunk_rows : std::max<uint64_t>(1, (128ull << 20) / (4ull * dim_));
+    const uint64_t crows = std::min(chunk, nb);
+    PinnedBuf raw, fl[2];
+    raw.alloc(crows * rowb);
+    fl[0].alloc(crows * dim_ * 4);
+    fl[1].alloc(crows * dim_ * 4);
+    cudaEvent_t ev[2];
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } evg{ev};
+    bool used[2] = {false, false};
+    int cur = 0;
+    add_stream(nb, chunk, [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+        if (std::fseek(f, (long)(first * rowb), SEEK_SET) != 0 || std::fread(raw.p, 1, count * rowb, f) != count * rowb)
+            throw std::runtime_error("read_vecs: truncated record payload in " + path);
+        if (used[cur]) CUDA_CHECK(cudaEventSynchronize(ev[cur]));  // the H2D that last read this buffer
+        float* out = reinterpret_cast<float*>(fl[cur].p);
+        for (uint64_t r = 0; r < count; r++) {
+            const unsigned char* rec = raw.p + r * rowb;
+            int32_t d;
+            std::memcpy(&d, rec, 4);
+            if (d <= 0) throw std::runtime_error("read_vecs: non-positive dimension in " + path);
+            if ((uint32_t)d != dim_) throw std::runtime_error("read_vecs: mismatched record dimension in " + path);
+            float* o = out + r * dim_;
+            if (kind == 0) {
+                std::memcpy(o, rec + 4, 4ull * dim_);
+            } else if (kind == 1) {
+                for (uint32_t t = 0; t < dim_; t++) o[t] = (float)rec[4 + t];
+            } else {
+                for (uint32_t t = 0; t < dim_; t++) {
+                    int32_t v;
+                    std::memcpy(&v, rec + 4 + 4ull * t, 4);
+                    o[t] = (float)v;
+                }
+            }
+            for (uint32_t t = 0; t < dim_; t++)
+                if (!std::isfinite(o[t])) throw std::runtime_error("VectorSet: non-finite value");
+        }
+        CUDA_CHECK(cudaMemcpyAsync(dst, out, count * dim_ * 4, cudaMemcpyHostToDevice, st));
+        CUDA_CHECK(cudaEventRecord(ev[cur], st));
+        used[cur] = true;
+        cur ^= 1;
+    });
+}
+
 void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
     if (!model_ok_) throw std::runtime_error("add: no model loaded");
     if (base_count_ != 0) throw std::runtime_error("index already holds a base set");
@@ -636,31 +717,37 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
         xlo = tc_split_ ? xlo_.p : nullptr;
         launches += 1;
     }
+    // filter pass in 1xTF32 as well (study knob): tau raised by two 1x bounds
+    const bool p2single = two_pass && tc_split_ && cfg_.tc_pass1_single && cfg_.tc_pass2_single;
     if (two_pass) {
         // pass 1: chunk minima -> tau (upper bound of the L-th smallest);
         // pass 2: recompute, keep only approx <= tau (no K-wide row in HBM)
+        const float* x1 = nullptr;
         if (tc_split_ && cfg_.tc_pass1_single) {
             // pass 1 in 1xTF32 on 128-centroid tiles (a third of the MMAs; same
             // 32-column chunks), tau raised by its error bound
             if (!xtc1_.p || xtc1_.n < ((nt + 127) / 128) * 128 * dim_) {
                 xtc1_.alloc(((nt + 127) / 128) * 128 * dim_);
             }
-            const float* x1 = nullptr;
             if (cfg_.tc_persist) {
                 launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st);
                 x1 = xtc1_.p;
             }
             launch_coarse_tc(2, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr,
                              st, nullptr, nullptr, 0, x1, nullptr);
-            launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st, d_q, dim_, cmax_);
+            launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st, d_q, dim_, cmax_, p2single ? 0 : 1);
         } else {
             launch_coarse_tc(2, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, tmin_.p, nchunk, nullptr, nullptr, st,
                              nullptr, nullptr, 0, xtc, xlo);
             launch_tau_rows(tmin_.p, nt, nchunk, L, cand_top_.p, tau_.p, st);
         }
         CUDA_CHECK(cudaMemsetAsync(lcnt_.p, 0, nt * 4, st));
-        launch_coarse_tc(3, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, nullptr, 0, lidx_.p, ld_.p, st, tau_.p,
-                         lcnt_.p, kListCap, xtc, xlo);
+        if (p2single)
+            launch_coarse_tc(3, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, nullptr, 0, lidx_.p, ld_.p, st,
+                             tau_.p, lcnt_.p, kListCap, x1, nullptr);
+        else
+            launch_coarse_tc(3, d_q, nt, dim_, c_hi, c_lo, cnorm_tc_.p, k_, nullptr, 0, lidx_.p, ld_.p, st, tau_.p,
+                             lcnt_.p, kListCap, xtc, xlo);
         launches += 3;
     } else if (tc) {
         // approximate rows on the tensor cores, then top-L on them
@@ -676,7 +763,7 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
         CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
         if (two_pass) {
             launch_refine_list(d_q, nt, dim_, centroids_.p, k_, lidx_.p, lcnt_.p, kListCap, tau_.p, w1, cmax_,
-                               tc_split_ ? 1 : 0, top_.p, qlist_.p, err_.p + 6, st);
+                               (tc_split_ && !p2single) ? 1 : 0, top_.p, qlist_.p, err_.p + 6, st);
         } else {
             launch_first_level(ws_.p, nt, k_, L, cand_top_.p, st);
             launch_refine_first(d_q, nt, dim_, centroids_.p, ws_.p, k_, cand_top_.p, L, w1, cmax_, top_.p, qlist_.p,
@@ -765,6 +852,7 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "force_exact") cfg_.force_exact = (int)value;
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;
     else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
+    else if (key == "tc_pass2_single") cfg_.tc_pass2_single = (int)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
     else if (key == "scan_cap") cfg_.scan_cap = (uint32_t)value;

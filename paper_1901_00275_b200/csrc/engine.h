@@ -48,6 +48,7 @@ struct EngineConfig {
     int tc_store_rows = 0;  // 1: materialise approximate rows + radix select instead of the two-pass filter
     int tc_persist = 1;     // search coarse kernels as a persistent grid (one CTA per SM)
     int tc_pass1_single = 1;  // two-pass coarse filter: first pass in 1xTF32 (tau raised by its error bound)
+    int tc_pass2_single = 0;  // ... and the filter pass in 1xTF32 too (tau raised by both bounds; more candidates)
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -166,6 +167,11 @@ public:
 
     // add (Index.add, proj/python/bindings.cpp:83-97)
     void add_host(const float* base, uint64_t nb);
+    // streamed add of a .fvecs / .bvecs / .ivecs file (the reference CLI's
+    // `build` input, read_vecs vecs_io.cpp:29-86 semantics and error texts)
+    // through double-buffered pinned staging: the base never has to fit in
+    // host memory
+    void add_vecs(const std::string& path, uint64_t chunk_rows = 0);
     // streamed add: the source writes points [first, first+count) to a device buffer
     using ChunkSource = std::function<void(uint64_t first, uint64_t count, float* dst, cudaStream_t st)>;
     void add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src);

@@ -135,7 +135,8 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
                       cudaStream_t st, const float* tau = nullptr, uint32_t* cnt = nullptr, uint32_t cap = 0,
                       const float* Xtc = nullptr, const float* Xlo_tc = nullptr);
 void launch_tau_rows(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, uint32_t* scratch, float* tau,
-                     cudaStream_t st, const float* Y = nullptr, uint32_t dim = 0, float cmax = 0.0f);
+                     cudaStream_t st, const float* Y = nullptr, uint32_t dim = 0, float cmax = 0.0f,
+                     int pass2_split = 1);
 void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, const uint32_t* cand,
                         const uint32_t* cnt, uint32_t cap, const float* tau, uint32_t w1, float cmax, int split,
                         uint32_t* top, uint32_t* flagged, unsigned int* nflag, cudaStream_t st);

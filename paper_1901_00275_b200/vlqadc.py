@@ -126,6 +126,11 @@ class Index:
         b = _to_vecset(base)
         _lib.check(_lib.lib().vlq_engine_add(self._h, _p(b), b.shape[0], b.shape[1] if b.shape[0] else self.dim))
 
+    def add_vecs(self, path: str, chunk_rows: int = 0) -> None:
+        """add(read_vecs(path)) streamed from the file (.fvecs / .bvecs /
+        .ivecs) without holding the base in host memory (extension)."""
+        _lib.check(_lib.lib().vlq_engine_add_vecs(self._h, str(path).encode(), chunk_rows))
+
     def search(self, queries, w1: int = 64, alpha: float = 0.25, k: int = 10, *, return_scanned: bool = False):
         """Index.search (bindings.cpp:99-126) -> (ids int64[nq,k], dists float32[nq,k])."""
         q = _to_vecset(queries)

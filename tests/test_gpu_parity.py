@@ -383,3 +383,55 @@ def test_merge_of_sorted_parts_random(vlqadc, G, k):
         want_i[:len(o)], want_d[:len(o)] = ci[o], cd[o]
         assert np.array_equal(got_i[q], want_i), q
         assert same_f32(got_d[q], want_d)
+
+
+@pytest.mark.parametrize("name,suffix,chunk", [("smoke", ".fvecs", 0), ("unclamped", ".fvecs", 777),
+                                                ("m16", ".bvecs", 1000), ("n1m8", ".ivecs", 0)])
+def test_add_vecs_streamed_file_equals_reference_build(vlqadc, name, suffix, chunk, tmp_path):
+    """Index.add_vecs(path) (streamed from the file, any chunking; unclamped
+    models take two passes over the file) == add(read_vecs(path)); for the
+    float file the result is the reference-built index byte for byte."""
+    z, index_path, model_path = load_golden(name)
+    base = regen_base(z)
+    if suffix != ".fvecs":  # byte / int payloads: integer-valued data of the same shape
+        base = np.clip(np.rint(base * 255.0), 0, 255).astype(np.float32)
+    path = str(tmp_path / f"base{suffix}")
+    vlqadc.write_vecs(base, path)
+    want = vlqadc.Index.load(model_path)
+    want.add(vlqadc.read_vecs(path))
+    got = vlqadc.Index.load(model_path)
+    got.add_vecs(path, chunk_rows=chunk)
+    assert got.ntotal == len(base)
+    a, b = str(tmp_path / "want.vlq"), str(tmp_path / "got.vlq")
+    want.save(a)
+    got.save(b)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    if suffix == ".fvecs":
+        assert open(b, "rb").read() == open(index_path, "rb").read()
+
+
+def test_add_vecs_errors_mirror_read_vecs(vlqadc, tmp_path):
+    z, _, model_path = load_golden("smoke")
+    base = regen_base(z)[:100]
+    path = str(tmp_path / "b.fvecs")
+    vlqadc.write_vecs(base, path)
+    raw = open(path, "rb").read()
+    cases = {"missing.fvecs": None, "empty.fvecs": b"", "trunc.fvecs": raw[:-3], "hdr.fvecs": raw + b"\x01\x00"}
+    msgs = {"missing.fvecs": "cannot open", "empty.fvecs": "no records", "trunc.fvecs": "truncated record payload",
+            "hdr.fvecs": "truncated record header"}
+    for fname, data in cases.items():
+        p = str(tmp_path / fname)
+        if data is not None:
+            open(p, "wb").write(data)
+        idx = vlqadc.Index.load(model_path)
+        with pytest.raises(RuntimeError, match=msgs[fname]):
+            idx.add_vecs(p)
+        assert idx.ntotal == 0
+    other = str(tmp_path / "d.fvecs")
+    vlqadc.write_vecs(np.zeros((4, base.shape[1] + 1), np.float32), other)
+    with pytest.raises(RuntimeError, match="dimension mismatch"):
+        vlqadc.Index.load(model_path).add_vecs(other)
+    idx = vlqadc.Index.load(model_path)
+    idx.add_vecs(path)
+    with pytest.raises(RuntimeError, match="index already holds a base set"):
+        idx.add_vecs(path)
