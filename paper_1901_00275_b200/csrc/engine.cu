@@ -10,6 +10,9 @@
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -917,26 +920,91 @@ void Engine::set_profiling(bool on) {
 }
 
 // host copy between the caller's (pageable) arrays and the pinned staging:
-// split over a few threads above 1 MiB -- a single thread is bound by the
-// first-touch page faults of freshly allocated numpy outputs (~2 ms for the
-// 12 MB of a 10k x 100 result)
+// split over a small persistent worker pool above 1 MiB -- a single thread is
+// bound by the first-touch page faults of freshly allocated numpy outputs
+// (~1 ms for the 12 MB of a 10k x 100 result), and spawning threads per call
+// costs about as much as it saves
+namespace {
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    unsigned workers() const { return (unsigned)th_.size(); }
+    // runs fn(0..n-1): parts 1..n-1 on the workers, part 0 on the caller
+    void run(unsigned n, const std::function<void(unsigned)>& fn) {
+        std::unique_lock<std::mutex> lk(call_mu_);  // one batch at a time
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            fn_ = &fn;
+            next_ = 1;
+            total_ = n;
+            pending_ = n - 1;
+            gen_++;
+        }
+        cv_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+            gen_++;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+private:
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (unsigned i = 0; i + 1 < std::min(8u, hw); i++) th_.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> g(mu_);
+        for (;;) {
+            cv_.wait(g, [&] { return stop_ || (gen_ != seen && next_ < total_); });
+            if (stop_) return;
+            seen = gen_;
+            while (next_ < total_) {
+                const unsigned part = next_++;
+                const std::function<void(unsigned)>* fn = fn_;
+                g.unlock();
+                (*fn)(part);
+                g.lock();
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(unsigned)>* fn_ = nullptr;
+    unsigned next_ = 0, total_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+}  // namespace
+
 static void par_memcpy(void* dst, const void* src, size_t bytes) {
     const size_t kMin = 1u << 20;
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned nt = (unsigned)std::min<size_t>(std::min(8u, hw), bytes / kMin);
+    CopyPool& pool = CopyPool::get();
+    const unsigned nt = (unsigned)std::min<size_t>(pool.workers() + 1, bytes / kMin);
     if (nt <= 1) {
         std::memcpy(dst, src, bytes);
         return;
     }
     const size_t per = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
-    std::vector<std::thread> th;
-    for (unsigned t = 1; t < nt && t * per < bytes; t++)
-        th.emplace_back([=] {
+    pool.run(nt, [&](unsigned t) {
+        if (t * per < bytes)
             std::memcpy(static_cast<char*>(dst) + t * per, static_cast<const char*>(src) + t * per,
                         std::min(per, bytes - t * per));
-        });
-    std::memcpy(dst, src, std::min(per, bytes));
-    for (auto& x : th) x.join();
+    });
 }
 
 void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
@@ -1142,7 +1210,7 @@ void Engine::save_vlq1(const std::string& path, bool store_t3) {
     if (!model_ok_) throw std::runtime_error("save: no model loaded");
     if (cfg_.shard_count != 1) throw std::runtime_error("save: a sharded engine cannot write a complete VLQ1 index");
     HostLists L;
-    get_lists(L);
+    get_lists(L, /*offsets_only=*/true);  // the lists themselves are streamed below
     std::vector<float> t2, t3;
     if (store_t3) get_tables(t2, t3);
     Writer w(path);
@@ -1161,13 +1229,58 @@ void Engine::save_vlq1(const std::string& path, bool store_t3) {
     w.bytes(model_.elen.data(), model_.elen.size() * 4);
     w.bytes(model_.pq.data(), model_.pq.size() * 4);
     if (store_t3) w.bytes(t3.data(), t3.size() * 4);
+    // posting lists (index_io.cpp:63-98 record order), streamed: batches of
+    // whole cells (<= 8M entries unless one cell is larger) are copied to
+    // double-buffered pinned memory while the previous batch is written, so
+    // a 1B-entry index never needs a host copy of its ~21 GB of lists
     const size_t ncell = (size_t)k_ * n_;
-    for (size_t c = 0; c < ncell; c++) {
-        const uint64_t b0 = L.off[c], b1 = L.off[c + 1];
-        w.u32((uint32_t)(b1 - b0));
-        w.bytes(L.ids.data() + b0, (b1 - b0) * 4);
-        w.bytes(L.codes.data() + b0 * m_, (b1 - b0) * m_);
-        w.bytes(L.lambdas.data() + b0, b1 - b0);
+    const uint64_t kBatch = 8ull << 20;
+    std::vector<std::pair<size_t, size_t>> batches;
+    uint64_t maxb = 1;
+    for (size_t c0 = 0; c0 < ncell;) {
+        size_t c1 = c0 + 1;
+        while (c1 < ncell && L.off[c1 + 1] - L.off[c0] <= kBatch) c1++;
+        batches.emplace_back(c0, c1);
+        maxb = std::max<uint64_t>(maxb, L.off[c1] - L.off[c0]);
+        c0 = c1;
+    }
+    DeviceGuard g(cfg_.device);
+    PinnedBuf pb[2];
+    cudaEvent_t ev[2];
+    for (int b = 0; b < 2; b++) {
+        pb[b].alloc(maxb * (4 + m_ + 1));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } evg{ev};
+    auto fetch = [&](size_t bi) {  // D2H of batch bi into buffer bi % 2
+        const uint64_t e0 = L.off[batches[bi].first], ne = L.off[batches[bi].second] - e0;
+        unsigned char* p = pb[bi & 1].p;
+        if (ne) {
+            CUDA_CHECK(cudaMemcpyAsync(p, ids_.p + e0, ne * 4, cudaMemcpyDeviceToHost, stream_));
+            CUDA_CHECK(cudaMemcpyAsync(p + ne * 4, codes_.p + e0 * m_, ne * m_, cudaMemcpyDeviceToHost, stream_));
+            CUDA_CHECK(cudaMemcpyAsync(p + ne * (4 + m_), lambdas_.p + e0, ne, cudaMemcpyDeviceToHost, stream_));
+        }
+        CUDA_CHECK(cudaEventRecord(ev[bi & 1], stream_));
+    };
+    if (!batches.empty()) fetch(0);
+    for (size_t bi = 0; bi < batches.size(); bi++) {
+        if (bi + 1 < batches.size()) fetch(bi + 1);  // its buffer's previous batch (bi - 1) is fully written
+        CUDA_CHECK(cudaEventSynchronize(ev[bi & 1]));
+        const uint64_t e0 = L.off[batches[bi].first], ne = L.off[batches[bi].second] - e0;
+        const unsigned char* p = pb[bi & 1].p;
+        for (size_t c = batches[bi].first; c < batches[bi].second; c++) {
+            const uint64_t b0 = L.off[c] - e0, len = L.off[c + 1] - L.off[c];
+            w.u32((uint32_t)len);
+            w.bytes(p + b0 * 4, len * 4);
+            w.bytes(p + ne * 4 + b0 * m_, len * m_);
+            w.bytes(p + ne * (4 + m_) + b0, len);
+        }
     }
     if (!w.out) throw std::runtime_error("serialize_index: write failed for " + path);
 }
