@@ -10,6 +10,7 @@
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
+#include <atomic>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -991,27 +992,45 @@ private:
 };
 }  // namespace
 
-static void par_memcpy(void* dst, const void* src, size_t bytes) {
+// every float of [p, p + n) finite (VectorSet::validate, vecset.cpp:14-18):
+// an exponent-field test the compiler vectorises
+static bool all_finite(const float* p, size_t n) {
+    uint32_t bad = 0;
+    for (size_t i = 0; i < n; i++) {
+        uint32_t u;
+        std::memcpy(&u, p + i, 4);
+        bad |= (uint32_t)((u & 0x7f800000u) == 0x7f800000u);
+    }
+    return bad == 0;
+}
+
+// copies `bytes` and, when check_f32, returns whether every copied float is
+// finite (the check runs on the freshly written, cache-hot destination)
+static bool par_memcpy(void* dst, const void* src, size_t bytes, bool check_f32 = false) {
     const size_t kMin = 1u << 20;
     CopyPool& pool = CopyPool::get();
     const unsigned nt = (unsigned)std::min<size_t>(pool.workers() + 1, bytes / kMin);
     if (nt <= 1) {
         std::memcpy(dst, src, bytes);
-        return;
+        return !check_f32 || all_finite(static_cast<const float*>(dst), bytes / 4);
     }
     const size_t per = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
+    std::atomic<bool> ok{true};
     pool.run(nt, [&](unsigned t) {
-        if (t * per < bytes)
-            std::memcpy(static_cast<char*>(dst) + t * per, static_cast<const char*>(src) + t * per,
-                        std::min(per, bytes - t * per));
+        if (t * per < bytes) {
+            const size_t nb = std::min(per, bytes - t * per);
+            char* d = static_cast<char*>(dst) + t * per;
+            std::memcpy(d, static_cast<const char*>(src) + t * per, nb);
+            if (check_f32 && !all_finite(reinterpret_cast<const float*>(d), nb / 4)) ok = false;
+        }
     });
+    return ok;
 }
 
 void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
                          float* dists, uint64_t* scanned) {
     if (!model_ok_) throw std::runtime_error("search: no model loaded");
-    if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
-    if (nq == 0) return;
+    if (nq == 0) return;  // search_batch runs no query, so first_level_scan never checks w1 (search.cpp:169-191)
     DeviceGuard g(cfg_.device);
     cudaStream_t st = stream_;
     // grow-only device buffers and pinned host staging: no per-call
@@ -1027,7 +1046,10 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     unsigned char* pi = pq + qb;
     unsigned char* pd = pi + ib;
     unsigned char* ps = pd + db;
-    par_memcpy(pq, q, qb);
+    // the query copy validates it too (to_vecset's VectorSet::validate,
+    // bindings.cpp:23-31): the Python mirror skips its own numpy pass
+    if (!par_memcpy(pq, q, qb, /*check_f32=*/true)) throw std::runtime_error("VectorSet: non-finite value");
+    if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
     CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
     CUDA_CHECK(cudaMemcpyAsync(sq_.p, pq, qb, cudaMemcpyHostToDevice, st));
     search_device(sq_.p, nq, w1, alpha, topk, si_.p, sd_.p, ss_.p, st);

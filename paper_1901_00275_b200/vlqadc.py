@@ -52,12 +52,14 @@ def _stream(stream: int | None):
     return ctypes.c_void_p(CUDA_STREAM_LEGACY if stream == 0 else stream)
 
 
-def _to_vecset(arr) -> np.ndarray:
-    """to_vecset + VectorSet::validate (bindings.cpp:23-31, vecset.cpp:8-20)."""
+def _to_vecset(arr, validate: bool = True) -> np.ndarray:
+    """to_vecset + VectorSet::validate (bindings.cpp:23-31, vecset.cpp:8-20).
+    validate=False leaves the finiteness check to the engine (the host search
+    checks while staging the queries, with the same message)."""
     a = np.ascontiguousarray(arr, dtype=np.float32)
     if a.ndim != 2:
         raise RuntimeError("expected a 2-D float array")
-    if a.size and not np.isfinite(a).all():
+    if validate and a.size and not np.isfinite(a).all():
         raise RuntimeError("VectorSet: non-finite value")
     return a
 
@@ -133,13 +135,14 @@ class Index:
 
     def search(self, queries, w1: int = 64, alpha: float = 0.25, k: int = 10, *, return_scanned: bool = False):
         """Index.search (bindings.cpp:99-126) -> (ids int64[nq,k], dists float32[nq,k])."""
-        q = _to_vecset(queries)
+        q = _to_vecset(queries, validate=False)  # vlq_engine_search validates while staging
         nq = q.shape[0]
         ids = np.empty((nq, k), np.int64)
         dists = np.empty((nq, k), np.float32)
         scanned = np.zeros(nq, np.uint64)
         dim = q.shape[1] if q.size else self.dim
         if q.shape[1] != self.dim:
+            _to_vecset(q)  # the reference validates (non-finite) before the dimension check
             raise RuntimeError("search_batch: dimension mismatch")
         _lib.check(_lib.lib().vlq_engine_search(self._h, _p(q), nq, dim, w1, alpha, k, _p(ids), _p(dists),
                                                 _p(scanned)))

@@ -56,6 +56,30 @@ def main():
         idx.search(qh, w1=64, alpha=0.25, k=k)
         t.append(time.perf_counter() - t0)
     out["host_api_ms"] = round(1e3 * float(np.median(t)), 3)
+    # the bare C call on preallocated outputs (no Python-side allocation)
+    import ctypes
+    from paper_1901_00275_b200 import _lib
+    oi = np.empty((nq, k), np.int64)
+    od = np.empty((nq, k), np.float32)
+    osc = np.empty(nq, np.uint64)
+    t = []
+    for _ in range(args.reps):
+        t0 = time.perf_counter()
+        _lib.check(_lib.lib().vlq_engine_search(idx._h, qh.ctypes.data_as(ctypes.c_void_p), nq, qh.shape[1], 64,
+                                                0.25, k, oi.ctypes.data_as(ctypes.c_void_p),
+                                                od.ctypes.data_as(ctypes.c_void_p),
+                                                osc.ctypes.data_as(ctypes.c_void_p)))
+        t.append(time.perf_counter() - t0)
+    out["c_call_prealloc_ms"] = round(1e3 * float(np.median(t)), 3)
+    # device search + its own host-side enqueue cost, timed on the host
+    t = []
+    for _ in range(args.reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        idx.search_device(q.data_ptr(), nq, 64, 0.25, k, ids.data_ptr(), dists.data_ptr(), None, st)
+        torch.cuda.synchronize()
+        t.append(time.perf_counter() - t0)
+    out["device_search_wall_ms"] = round(1e3 * float(np.median(t)), 3)
     # traffic of one call alone
     pin_q = torch.empty((nq, w["dim"]), dtype=torch.float32).pin_memory()
     pin_i = torch.empty((nq, k), dtype=torch.int64).pin_memory()
