@@ -4,6 +4,10 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -69,6 +73,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
 }
 
 Engine::~Engine() {
+    if (flusher_.joinable()) flusher_.join();
     for (auto& sl : prof_) {
         for (auto& e : sl.ev)
             if (e) cudaEventDestroy(e);
@@ -1004,13 +1009,41 @@ static bool all_finite(const float* p, size_t n) {
     return bad == 0;
 }
 
+// Evicts [p, p + n) from every CPU cache.  Pinned staging lines left dirty
+// or shared in several cores' caches by the worker threads make the next DMA
+// snoop them: measured on the GPU box (scripts/cuda/copy_probe.cu), a 3.84 MB
+// H2D fell from 45 to 6.4 GB/s and a 12 MB D2H from 55 to 15 GB/s after an
+// 8-thread copy, and recovered fully with this flush.
+#if defined(__x86_64__)
+__attribute__((target("clflushopt"))) static void flush_lines_opt(const void* p, size_t n) {
+    const char* c = static_cast<const char*>(p);
+    for (size_t i = 0; i < n; i += 64) _mm_clflushopt(const_cast<char*>(c + i));
+    _mm_sfence();
+}
+static void flush_lines(const void* p, size_t n) {
+    static const bool opt = __builtin_cpu_supports("clflushopt");
+    if (opt) {
+        flush_lines_opt(p, n);
+        return;
+    }
+    const char* c = static_cast<const char*>(p);
+    for (size_t i = 0; i < n; i += 64) _mm_clflush(c + i);
+    _mm_mfence();
+}
+#else
+static void flush_lines(const void*, size_t) {}
+#endif
+
+enum class Pinned { Dst, Src, NoFlush };  // the side of a staging copy to flush (the pinned DMA buffer)
+
 // copies `bytes` and, when check_f32, returns whether every copied float is
-// finite (the check runs on the freshly written, cache-hot destination)
-static bool par_memcpy(void* dst, const void* src, size_t bytes, bool check_f32 = false) {
+// finite (checked on the cache-hot destination); the pinned side's lines are
+// flushed afterwards by the thread that touched them
+static bool par_memcpy(void* dst, const void* src, size_t bytes, Pinned pinned, bool check_f32 = false) {
     const size_t kMin = 1u << 20;
     CopyPool& pool = CopyPool::get();
     const unsigned nt = (unsigned)std::min<size_t>(pool.workers() + 1, bytes / kMin);
-    if (nt <= 1) {
+    if (nt <= 1) {  // one thread's cache: the DMA snoops it cheaply (measured), no flush
         std::memcpy(dst, src, bytes);
         return !check_f32 || all_finite(static_cast<const float*>(dst), bytes / 4);
     }
@@ -1020,8 +1053,11 @@ static bool par_memcpy(void* dst, const void* src, size_t bytes, bool check_f32 
         if (t * per < bytes) {
             const size_t nb = std::min(per, bytes - t * per);
             char* d = static_cast<char*>(dst) + t * per;
-            std::memcpy(d, static_cast<const char*>(src) + t * per, nb);
+            const char* sp = static_cast<const char*>(src) + t * per;
+            std::memcpy(d, sp, nb);
             if (check_f32 && !all_finite(reinterpret_cast<const float*>(d), nb / 4)) ok = false;
+            if (pinned != Pinned::NoFlush)
+                flush_lines(pinned == Pinned::Dst ? static_cast<const void*>(d) : static_cast<const void*>(sp), nb);
         }
     });
     return ok;
@@ -1033,6 +1069,12 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     if (nq == 0) return;  // search_batch runs no query, so first_level_scan never checks w1 (search.cpp:169-191)
     DeviceGuard g(cfg_.device);
     cudaStream_t st = stream_;
+    static const bool timing = std::getenv("VLQ_HOST_TIMING") != nullptr;  // diagnostics: phase wall times
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t0 = now();
     // grow-only device buffers and pinned host staging: no per-call
     // cudaMalloc/cudaFree (cudaFree synchronises the device) and full-speed
     // DMA instead of pageable copies
@@ -1041,6 +1083,7 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     si_.alloc(std::max<uint64_t>(nq * topk, 1));
     sd_.alloc(std::max<uint64_t>(nq * topk, 1));
     ss_.alloc(nq);
+    if (qb + ib + db + sb > pin_.n && flusher_.joinable()) flusher_.join();  // never free a buffer being flushed
     pin_.alloc(qb + ib + db + sb);
     unsigned char* pq = pin_.p;
     unsigned char* pi = pq + qb;
@@ -1048,22 +1091,48 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     unsigned char* ps = pd + db;
     // the query copy validates it too (to_vecset's VectorSet::validate,
     // bindings.cpp:23-31): the Python mirror skips its own numpy pass
-    if (!par_memcpy(pq, q, qb, /*check_f32=*/true)) throw std::runtime_error("VectorSet: non-finite value");
+    if (!par_memcpy(pq, q, qb, Pinned::Dst, /*check_f32=*/true))
+        throw std::runtime_error("VectorSet: non-finite value");
     if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
+    const auto t1 = now();
+    cudaEvent_t tev[4] = {};
+    if (timing)
+        for (auto& e : tev) CUDA_CHECK(cudaEventCreate(&e));
+    if (timing) CUDA_CHECK(cudaEventRecord(tev[0], st));
     CUDA_CHECK(cudaMemsetAsync(err_.p, 0, 4, st));
     CUDA_CHECK(cudaMemcpyAsync(sq_.p, pq, qb, cudaMemcpyHostToDevice, st));
+    if (timing) CUDA_CHECK(cudaEventRecord(tev[1], st));
     search_device(sq_.p, nq, w1, alpha, topk, si_.p, sd_.p, ss_.p, st);
+    if (timing) CUDA_CHECK(cudaEventRecord(tev[2], st));
+    // the previous call's output lines must be out of the CPU caches before
+    // this call's D2H lands on them (flushed in the background meanwhile)
+    if (flusher_.joinable()) flusher_.join();
+    const auto t2 = now();
     if (topk) {
         CUDA_CHECK(cudaMemcpyAsync(pi, si_.p, ib, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaMemcpyAsync(pd, sd_.p, db, cudaMemcpyDeviceToHost, st));
     }
     if (scanned) CUDA_CHECK(cudaMemcpyAsync(ps, ss_.p, sb, cudaMemcpyDeviceToHost, st));
+    if (timing) CUDA_CHECK(cudaEventRecord(tev[3], st));
     check_device_errors(st);
+    const auto t3 = now();
     if (topk) {
-        par_memcpy(ids, pi, ib);
-        par_memcpy(dists, pd, db);
+        par_memcpy(ids, pi, ib, Pinned::NoFlush);
+        par_memcpy(dists, pd, db, Pinned::NoFlush);
     }
-    if (scanned) par_memcpy(scanned, ps, sb);
+    if (scanned) par_memcpy(scanned, ps, sb, Pinned::NoFlush);
+    // evict the output staging lines the copy threads just read, off the
+    // caller's critical path (joined before the next D2H into them)
+    flusher_ = std::thread([pi, n = ib + db + sb] { flush_lines(pi, n); });
+    if (timing) {
+        float g[3];
+        for (int e = 0; e < 3; e++) CUDA_CHECK(cudaEventElapsedTime(&g[e], tev[e], tev[e + 1]));
+        for (auto& e : tev) cudaEventDestroy(e);
+        std::fprintf(stderr,
+                     "[search_host] stage+check %.3f ms, enqueue %.3f ms, wait %.3f ms, copy-out %.3f ms | "
+                     "GPU: h2d %.3f, search %.3f, d2h %.3f ms\n",
+                     ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, now()), g[0], g[1], g[2]);
+    }
 }
 
 // ---------------------------------------------------------------------------

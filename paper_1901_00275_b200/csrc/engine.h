@@ -13,6 +13,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.h"
@@ -322,6 +323,7 @@ private:
     DevBuf<int64_t> si_;
     DevBuf<uint64_t> ss_;
     PinnedBuf pin_;
+    std::thread flusher_;  // background cache flush of the host-search output staging
 
     // search workspace
     DevBuf<float> ws_, dbuf_, t5_;

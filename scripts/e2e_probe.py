@@ -80,6 +80,17 @@ def main():
         torch.cuda.synchronize()
         t.append(time.perf_counter() - t0)
     out["device_search_wall_ms"] = round(1e3 * float(np.median(t)), 3)
+    # the same on the engine's private stream (stream NULL at the C ABI)
+    t = []
+    for _ in range(args.reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(_lib.lib().vlq_engine_search_device(idx._h, ctypes.c_void_p(q.data_ptr()), nq, 64, 0.25, k,
+                                                       ctypes.c_void_p(ids.data_ptr()),
+                                                       ctypes.c_void_p(dists.data_ptr()), None, None))
+        idx.sync(None)
+        t.append(time.perf_counter() - t0)
+    out["device_search_engine_stream_wall_ms"] = round(1e3 * float(np.median(t)), 3)
     # traffic of one call alone
     pin_q = torch.empty((nq, w["dim"]), dtype=torch.float32).pin_memory()
     pin_i = torch.empty((nq, k), dtype=torch.int64).pin_memory()
