@@ -618,6 +618,14 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
     if (nq == 0) return;
     DeviceGuard g(cfg_.device);
     const uint32_t w2 = w2_of(w1, alpha, n_);
+    if (cfg_.scan_adapt_keep) {
+        if (!flag_seen_.p) {
+            flag_seen_.alloc(64);
+            std::memset(flag_seen_.p, 0, 64);
+        }
+        const uint32_t f = *reinterpret_cast<volatile uint32_t*>(flag_seen_.p);
+        if (flag_seen_nq_ && (uint64_t)f * 50 > flag_seen_nq_ && keep_boost_ < 4) keep_boost_ *= 2;
+    }
     const uint32_t keep = scan_keep(topk);
     const uint64_t per_q = 4ull * k_ + 8ull * w1 + 128 + 4ull * w1 * n_ + 4ull * w2 + 4ull * VLQ_KSUB * m_ + 8ull * keep +
                            sizeof(QueryMeta) + 4;
@@ -639,6 +647,9 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
     sel_.alloc(tile * w2);
     t5_.alloc(tile * VLQ_KSUB * m_);
     cand_.alloc(tile * keep);
+    if (cfg_.scan_retry) cand2_.alloc(tile * (uint64_t)std::min<uint32_t>(512, 4 * keep));
+    qlist2_.alloc(tile);
+    cnt2_.alloc(1);
     meta_.alloc(tile);
     qlist_.alloc(tile);
     for (uint64_t t0 = 0; t0 < nq; t0 += tile) {
@@ -816,6 +827,9 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         a.scan_cap = cfg_.scan_cap;
         a.sel_agg = cfg_.scan_sel_agg != 0;
         const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
+        // fast_kind: the v6 / q8 scan ran (the only kernels with the retry indirection)
+        const bool fast_kind = (cfg_.scan_variant == 0 || cfg_.scan_variant == 9) && a.eterm_lam &&
+                               (m_ == 16 || m_ == 8 || m_ == 4) && w2 <= 4096;
         if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, slots, cfg_.scan_prefetch, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
@@ -823,9 +837,32 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         mark(PH_FALLBACK);
         CUDA_CHECK(cudaMemsetAsync(err_.p + 2, 0, 4, st));
         launch_compact_flags(meta_.p, nt, qlist_.p, err_.p + 2, st);
-        launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, qlist_.p, err_.p + 2, st);
-        launch_emit_exact(a, qlist_.p, err_.p + 2, nt, keep_x, topk, d_ids, d_dists, st);
-        launches += 5;
+        if (cfg_.scan_adapt_keep && flag_seen_.p) {
+            CUDA_CHECK(cudaMemcpyAsync(flag_seen_.p, err_.p + 2, 4, cudaMemcpyDeviceToHost, st));
+            flag_seen_nq_ = nt;
+        }
+        const uint32_t keep2 = std::min<uint32_t>(512, 4 * keep);
+        if (cfg_.scan_retry && keep2 > keep && fast_kind) {
+            // certificate failures (near-ties at the k'-th fast distance): the
+            // fast scan again with 4x the survivors, for the listed queries only
+            // (blocks past the device-side count exit at once), then re-score;
+            // what still fails takes the exact scan
+            SearchArgs r = a;
+            r.cand = cand2_.p;
+            r.qlist = qlist_.p;
+            r.qcount = err_.p + 2;
+            launch_scan_fast(r, nt, w2, keep2, cfg_.scan_variant, slots, cfg_.scan_prefetch, st);
+            launch_rescore(r, nt, keep2, topk, d_ids, d_dists, st);
+            CUDA_CHECK(cudaMemsetAsync(cnt2_.p, 0, 4, st));
+            launch_compact_flags(meta_.p, nt, qlist2_.p, cnt2_.p, st);
+            launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, qlist2_.p, cnt2_.p, st);
+            launch_emit_exact(a, qlist2_.p, cnt2_.p, nt, keep_x, topk, d_ids, d_dists, st);
+            launches += 7;
+        } else {
+            launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, qlist_.p, err_.p + 2, st);
+            launch_emit_exact(a, qlist_.p, err_.p + 2, nt, keep_x, topk, d_ids, d_dists, st);
+            launches += 5;
+        }
     } else {
         mark(PH_SCAN);
         mark(PH_RESCORE);
@@ -849,6 +886,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
 // at least scan_keep_min (a study knob), at most 512 (the fast scan's limit)
 uint32_t Engine::scan_keep(uint32_t topk) const {
     uint32_t keep = next_pow2(std::max<uint32_t>(32, topk + std::max<uint32_t>(16, topk / 4)));
+    if (keep_boost_ > 1 && keep < 512) keep = std::min<uint32_t>(512, keep * keep_boost_);
     if (cfg_.scan_keep_min > keep) keep = std::min<uint32_t>(512, next_pow2(cfg_.scan_keep_min));
     return keep;
 }
@@ -865,6 +903,12 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
     else if (key == "scan_cap") cfg_.scan_cap = (uint32_t)value;
+    else if (key == "scan_retry") cfg_.scan_retry = (int)value;
+    else if (key == "scan_adapt_keep") {
+        cfg_.scan_adapt_keep = (int)value;
+        keep_boost_ = 1;
+        flag_seen_nq_ = 0;
+    }
     else if (key == "scan_sel_agg") cfg_.scan_sel_agg = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }

@@ -41,6 +41,8 @@ struct EngineConfig {
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
+    int scan_retry = 1;          // certificate failures: fast scan again with 4x k' before the exact scan
+    int scan_adapt_keep = 1;     // raise k' (x2, up to x4) after a batch whose certificate failed for > 2% of queries
     uint32_t scan_keep_min = 0;  // study knob: lower bound on k' (fast-scan survivors)
     int scan_packed = 1;   // v6 scan reads the packed e-term | lambda-byte stream (one load per entry)
     int use_tc = 1;         // tensor-core (tcgen05 TF32) coarse stage + add assignment when supported
@@ -324,11 +326,19 @@ private:
     DevBuf<uint64_t> ss_;
     PinnedBuf pin_;
     std::thread flusher_;  // background cache flush of the host-search output staging
+    // adaptive k': the previous fine stage's certificate-failure count lands
+    // here asynchronously (read one call later; a stale value only delays
+    // the adaptation), and k' doubles while more than 2% of a batch fails
+    PinnedBuf flag_seen_;
+    uint64_t flag_seen_nq_ = 0;
+    uint32_t keep_boost_ = 1;
 
     // search workspace
     DevBuf<float> ws_, dbuf_, t5_;
     DevBuf<uint32_t> top_, sel_, qlist_, cand_top_;
-    DevBuf<uint64_t> cand_;
+    DevBuf<uint64_t> cand_, cand2_;  // fast-scan survivors (k') / of the retry pass (4 k')
+    DevBuf<uint32_t> qlist2_;
+    DevBuf<unsigned int> cnt2_;
     DevBuf<QueryMeta> meta_;
 };
 

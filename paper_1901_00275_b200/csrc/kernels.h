@@ -52,6 +52,10 @@ struct SearchArgs {
     float e_pack_err;
     uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
     bool sel_agg;       // fast-scan flush: warp-aggregated (match_any) histogram atomics
+    // retry pass (certificate failures): the kernel's block b handles query
+    // qlist[b] (blocks >= *qcount exit) and its cand row is b, not q
+    const uint32_t* qlist;
+    const unsigned int* qcount;
 };
 
 // Add-path device views.

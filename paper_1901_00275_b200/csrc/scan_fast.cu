@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t 
     constexpr uint32_t CH = 32 * U;  // entries per chunk
     const uint32_t nwarps = blockDim.x >> 5;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint64_t q = blockIdx.x;
+    if (a.qlist && blockIdx.x >= *a.qcount) return;
+    const uint64_t q = a.qlist ? a.qlist[blockIdx.x] : blockIdx.x;
     unsigned char* lut = smem;
     constexpr uint32_t LUT_B = lut_bytes<M>(LM);
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + LUT_B);        // cap keys
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t 
     for (uint32_t i = n + threadIdx.x; i < keep; i += blockDim.x) cbuf[i] = ~0ull;
     __syncthreads();
     bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
-    uint64_t* candq = a.cand + q * keep;
+    uint64_t* candq = a.cand + (a.qlist ? (uint64_t)blockIdx.x : q) * keep;
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
 }
 

@@ -429,9 +429,10 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, ui
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // keep (power of two)
     __shared__ float s_fast_last;
-    const uint64_t q = blockIdx.x;
+    if (a.qlist && blockIdx.x >= *a.qcount) return;
+    const uint64_t q = a.qlist ? a.qlist[blockIdx.x] : blockIdx.x;
     const uint32_t m = a.m;
-    const uint64_t* candq = a.cand + q * keep;
+    const uint64_t* candq = a.cand + (a.qlist ? (uint64_t)blockIdx.x : q) * keep;
     const float* wsq = a.ws + q * a.k;
     const float* t5q = a.t5 + q * m * VLQ_KSUB;
     const uint64_t scanned = a.meta[q].scanned;

@@ -435,3 +435,23 @@ def test_add_vecs_errors_mirror_read_vecs(vlqadc, tmp_path):
     idx.add_vecs(path)
     with pytest.raises(RuntimeError, match="index already holds a base set"):
         idx.add_vecs(path)
+
+
+@pytest.mark.parametrize("retry", [0, 1])
+def test_certificate_retry_and_exact_fallback_match_oracle(vlqadc, oracle_mod, retry):
+    """The u8-LUT scan's widened certificate fails for most queries at
+    k' = 128, so the retry pass (fast scan again with k' = 512 for the
+    listed queries, re-score) and the exact scan for what still fails both
+    run; with the retry on or off the results equal the oracle's."""
+    for name in ALL_CASES:
+        z, index_path, _ = load_golden(name)
+        idx = vlqadc.Index.load(index_path)
+        idx.set_tuning("scan_variant", 9)
+        idx.set_tuning("scan_retry", retry)
+        o = oracle_mod.OracleIndex.load(index_path)
+        for w1, alpha, k in [(min(idx.k, 16), 0.5, 10), (min(idx.k, 64), 0.25, 100), (min(idx.k, 8), 1.0, 3)]:
+            ids, dists, sc = idx.search(z["queries"], w1=w1, alpha=alpha, k=k, return_scanned=True)
+            oids, od, osc = o.search(z["queries"], w1, alpha, k)
+            assert np.array_equal(ids, oids), (name, w1, alpha, k)
+            assert same_f32(dists, od)
+            assert np.array_equal(sc, osc)

@@ -130,10 +130,11 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
                 dict(tc_pass1_single=1, tc_persist=0), dict(scan_variant=4), dict(scan_prefetch=1),
                 dict(scan_packed=0), dict(scan_variant=5), dict(scan_variant=6), dict(scan_variant=9),
                 dict(scan_variant=9, scan_keep_min=512, scan_cap=4096),
-                dict(tc_pass1_single=1, tc_pass2_single=1), dict(tc_pass1_single=1, tc_pass2_single=1, tc_persist=0)]
+                dict(tc_pass1_single=1, tc_pass2_single=1), dict(tc_pass1_single=1, tc_pass2_single=1, tc_persist=0),
+                dict(scan_variant=9, scan_retry=0)]
     for v in variants:
         knobs = dict(tc_persist=1, tc_pass1_single=0, scan_variant=0, scan_prefetch=0,
-                     scan_packed=1, scan_keep_min=0, scan_cap=0, tc_pass2_single=0)
+                     scan_packed=1, scan_keep_min=0, scan_cap=0, tc_pass2_single=0, scan_retry=1)
         knobs.update(v)
         for key, val in knobs.items():
             idx.set_tuning(key, val)
