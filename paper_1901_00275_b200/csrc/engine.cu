@@ -173,6 +173,16 @@ void Engine::upload_model() {
     h2d(nbr_, model_.nbr, stream_);
     h2d(elen_, model_.elen, stream_);
     h2d(pq_, model_.pq, stream_);
+    {  // [p][j][t] -> [p][t][j]: coalesced term5 loads
+        const uint32_t dsub = dim_ / m_;
+        std::vector<float> pqT(model_.pq.size());
+        for (uint32_t p = 0; p < m_; p++)
+            for (uint32_t j = 0; j < VLQ_KSUB; j++)
+                for (uint32_t t = 0; t < dsub; t++)
+                    pqT[((size_t)p * dsub + t) * VLQ_KSUB + j] = model_.pq[((size_t)p * VLQ_KSUB + j) * dsub + t];
+        h2d(pqT_, pqT, stream_);
+        CUDA_CHECK(cudaStreamSynchronize(stream_));  // pqT (host) is freed at scope exit
+    }
     t2_.alloc((size_t)m_ * VLQ_KSUB);
     t3_.alloc(std::max<size_t>((size_t)k_ * m_ * VLQ_KSUB, 1));
     // t2 (pq.cpp:11-18, recomputed on load: index_io.cpp:140) and t3
@@ -811,7 +821,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (sel) launch_apply_selection(a, nt, w2, sel->sel_in, sel->ab_in, st);
     else launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
-    launch_term5(d_q, pq_.p, dim_, m_, t5_.p, meta_.p, nt, st);
+    launch_term5(d_q, pqT_.p, dim_, m_, t5_.p, meta_.p, nt, st);
     launches += 2;
     const uint32_t keep_x = next_pow2(std::max<uint32_t>(32, topk));
     const uint32_t buf_x = 2 * keep_x;

@@ -300,7 +300,7 @@ private:
     float emax_ = 0.0f;
     HostModel model_;
 
-    DevBuf<float> centroids_, elen_, pq_, t2_, t3_;
+    DevBuf<float> centroids_, elen_, pq_, pqT_, t2_, t3_;  // pqT_: [p][t][j] copy for term5
     DevBuf<float> cent_tc_, cnorm_tc_;  // UMMA-layout centroids + norms (tensor-core path)
     DevBuf<float> cent_hi_, cent_lo_;   // 3xTF32 split halves (search coarse stage)
     bool tc_ = false, tc_split_ = false;

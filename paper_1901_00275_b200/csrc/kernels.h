@@ -82,7 +82,8 @@ void launch_pack_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32
                            cudaStream_t st);
 void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const uint32_t* sel_in, const float* ab,
                             cudaStream_t st);
-void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
+// pqT: the PQ codebook transposed to [p][t][j] (j = codeword, fastest)
+void launch_term5(const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
                   uint64_t nq, cudaStream_t st);
 size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);
 void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,

@@ -234,32 +234,51 @@ __global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t 
 // term5 table (query_term5): t5[q][p][j] = dot(y_p, PQ[p][j]) in order; also
 // S5max = sum_p max_j |t5| for the certificate.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_term5(const float* __restrict__ Y, const float* __restrict__ pq,
+__global__ void __launch_bounds__(256) k_term5(const float* __restrict__ Y, const float* __restrict__ pqT,
                                                uint32_t dim, uint32_t m, float* __restrict__ t5,
                                                QueryMeta* __restrict__ meta) {
+    // thread j computes t5[p][j] for every sub-space p (sequential fp32 dot,
+    // search.cpp:80-90 / vecset.cpp:39-45), reading the PQ codebook from its
+    // transposed copy pqT[(p*dsub + t)*256 + j], so every load and every t5
+    // store is warp-coalesced; S5max = sum_p max_j |t5[p][j]| for the
+    // certificate.  blockDim.x == 256 (one thread per codeword).
     extern __shared__ float ys[];
-    __shared__ float s_max[32];
+    __shared__ float s_max[8 * 16];
     const uint64_t q = blockIdx.x;
-    const uint32_t dsub = dim / m;
+    const uint32_t dsub = dim / m, j = threadIdx.x, lane = j & 31u, warp = j >> 5;
     for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
     __syncthreads();
-    float s5 = 0.0f;
-    for (uint32_t p = 0; p < m; p++) {
-        float mx = 0.0f;
-        for (uint32_t j = threadIdx.x; j < VLQ_KSUB; j += blockDim.x) {
-            const float* c = pq + ((uint64_t)p * VLQ_KSUB + j) * dsub;
-            float acc = 0.0f;
-            for (uint32_t t = 0; t < dsub; t++) acc = dot_step(acc, ys[p * dsub + t], c[t]);
-            t5[(q * m + p) * VLQ_KSUB + j] = acc;
-            mx = fmaxf(mx, fabsf(acc));
+    float s5 = 0.0f;  // thread 0's running S5max
+    for (uint32_t p0 = 0; p0 < m; p0 += 16) {  // sub-spaces in groups of 16 (register maxima)
+        float mx[16];
+#pragma unroll
+        for (int pp = 0; pp < 16; pp++) {
+            mx[pp] = 0.0f;
+            const uint32_t p = p0 + pp;
+            if (p < m) {
+                const float* c = pqT + (uint64_t)p * dsub * VLQ_KSUB + j;
+                const float* y = ys + p * dsub;
+                float acc = 0.0f;
+                for (uint32_t t = 0; t < dsub; t++) acc = dot_step(acc, y[t], c[(uint64_t)t * VLQ_KSUB]);
+                t5[(q * m + p) * VLQ_KSUB + j] = acc;
+                mx[pp] = fabsf(acc);
+            }
         }
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+#pragma unroll
+        for (int pp = 0; pp < 16; pp++) {
+            if (p0 + pp < m) {
+                float v = mx[pp];
+                for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (lane == 0) s_max[warp * 16 + pp] = v;
+            }
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            float v = 0.0f;
-            for (uint32_t w = 0; w < (blockDim.x + 31) / 32; w++) v = fmaxf(v, s_max[w]);
-            s5 += v;
+            for (uint32_t pp = 0; pp < 16 && p0 + pp < m; pp++) {
+                float v = 0.0f;
+                for (uint32_t w = 0; w < 8; w++) v = fmaxf(v, s_max[w * 16 + pp]);
+                s5 += v;
+            }
         }
         __syncthreads();
     }
@@ -536,9 +555,9 @@ void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const
     CUDA_LAUNCH_CHECK();
 }
 
-void launch_term5(const float* Y, const float* pq, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
+void launch_term5(const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
                   uint64_t nq, cudaStream_t st) {
-    dev::k_term5<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(Y, pq, dim, m, t5, meta);
+    dev::k_term5<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(Y, pqT, dim, m, t5, meta);
     CUDA_LAUNCH_CHECK();
 }
 
