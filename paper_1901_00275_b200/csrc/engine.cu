@@ -836,6 +836,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         }
         a.scan_cap = cfg_.scan_cap;
         a.sel_agg = cfg_.scan_sel_agg != 0;
+        a.flush_exact = cfg_.scan_flush_exact != 0;
         const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
         // fast_kind: the v6 / q8 scan ran (the only kernels with the retry indirection)
         const bool fast_kind = (cfg_.scan_variant == 0 || cfg_.scan_variant == 9) && a.eterm_lam &&
@@ -920,6 +921,7 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
         flag_seen_nq_ = 0;
     }
     else if (key == "scan_sel_agg") cfg_.scan_sel_agg = (int)value;
+    else if (key == "scan_flush_exact") cfg_.scan_flush_exact = (int)value;
     else throw std::runtime_error("set_tuning: unknown key " + key);
 }
 

@@ -40,6 +40,7 @@ struct EngineConfig {
                            // entries per query: measured 3% faster at 8 shards, neutral unsharded)
     int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
+    int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
     int scan_retry = 1;          // certificate failures: fast scan again with 4x k' before the exact scan
     int scan_adapt_keep = 1;     // raise k' (x2, up to x4) after a batch whose certificate failed for > 2% of queries

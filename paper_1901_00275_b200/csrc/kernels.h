@@ -52,6 +52,7 @@ struct SearchArgs {
     float e_pack_err;
     uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
     bool sel_agg;       // fast-scan flush: warp-aggregated (match_any) histogram atomics
+    bool flush_exact;   // fast-scan intermediate flushes: exact k' selection (else one-pass approximate)
     // retry pass (certificate failures): the kernel's block b handles query
     // qlist[b] (blocks >= *qcount exit) and its cand row is b, not q
     const uint32_t* qlist;

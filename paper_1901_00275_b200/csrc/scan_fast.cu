@@ -118,8 +118,13 @@ __device__ __forceinline__ void bitonic_merge_warp(uint64_t* a, uint32_t n, uint
 // atomics are aggregated per warp (__match_any_sync); stops early once the
 // selected bin is taken whole; compaction reserves output slots per warp.
 // `hist` >= 256 words, `s_misc` >= 48 words of shared scratch.
+// max_keep > 0 (intermediate flushes): stop after the first digit pass when
+// the keys up to and including the crossing bin number <= max_keep, and keep
+// them all (>= keep keys: the threshold stays a valid bound, one pass instead
+// of several); *kept receives the number of keys kept.
 __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep, uint32_t* hist,
-                                      unsigned int* s_misc, bool agg = false) {
+                                      unsigned int* s_misc, bool agg = false, uint32_t max_keep = 0,
+                                      uint32_t* kept = nullptr) {
     const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u, warp = tid >> 5, nwarps = nt >> 5;
     // 0. common leading bits of all keys
     uint64_t kand = ~0ull, kor = 0;
@@ -199,6 +204,7 @@ __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep,
         pmask |= 0xFFull << sh;
         remaining -= before;
         if (inbin == remaining) break;  // the whole bin is kept
+        if (max_keep && keep - remaining + inbin <= max_keep) break;  // approximate: keep the whole bin
     }
     const uint64_t T = sh > 0 ? (prefix | ((1ull << sh) - 1ull)) : prefix;  // keep keys <= T
     // in-place compaction in chunks of 8 keys per thread: the chunk is read
@@ -227,6 +233,7 @@ __device__ uint64_t block_select_keep(uint64_t* cbuf, uint32_t n, uint32_t keep,
         }
         __syncthreads();
     }
+    if (kept) *kept = s_misc[3];
     return T;
 }
 
@@ -828,11 +835,13 @@ __global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t 
         n_seen += rlen * nwarps * CH;
         const uint32_t cnt = s_count;
         if (cnt > keep && cnt > cap / 2) {  // block-uniform
-            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc, a.sel_agg);
+            uint32_t kept = keep;
+            const uint64_t T = block_select_keep(cbuf, cnt, keep, hist, s_misc, a.sel_agg,
+                                                 a.flush_exact ? 0u : cap / 4, &kept);
             __syncthreads();
             if (threadIdx.x == 0) {
-                s_count = keep;
-                s_tau = T + 1;  // insert only keys <= T
+                s_count = kept;  // >= keep after an approximate flush
+                s_tau = T + 1;   // insert only keys <= T
             }
             __syncthreads();
         }
