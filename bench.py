@@ -257,7 +257,7 @@ def main():
     w = WORKLOADS[args.workload]
     cfg = {"workload": w["desc"], "n_base": w["n"], "dim": w["dim"], "K": w["k"], "n_edges": w["edges"],
            "m_bytes": w["m"], "nq": args.nq, "w1": args.w1, "alpha": args.alpha, "k": args.k,
-           "parallelism": f"region-sharded x{world}" if world > 1 else "single GPU",
+           "parallelism": f"list-sharded x{world} (hashed cells)" if world > 1 else "single GPU",
            "l2": "flushed between steps (512 MiB write)", "data": "synthetic Gaussian mixture (sigma 0.05)"}
 
     if args.impl == "reference":
