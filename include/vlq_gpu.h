@@ -149,6 +149,10 @@ int vlq_engine_search_fine_sel_device(vlq_engine* e, const float* d_queries, uin
 /* w2 = max(1, floor(alpha * w1 * n)) clamped to w1 * n (search.hpp:16-20): the
  * row length of the select-split buffers. */
 uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n);
+/* The multi-GPU owner of posting list `cell` among `shards` engines
+ * (vlq_config.shard_rank / shard_count): ((cell * 0x9E3779B97F4A7C15) mod 2^64
+ * >> 40) mod shards.  Host-only, no device needed. */
+uint32_t vlq_shard_of_cell(uint32_t cell, uint32_t shards);
 
 /* Streamed Index.add of the engine's counter-based synthetic generator
  * (the reference's Gaussian-mixture law, dataset.cpp:13-44): rows are

@@ -60,6 +60,7 @@ _SIGS = {
     "vlq_engine_search_fine_sel_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                                   c_vp]),
     "vlq_w2": (c_u32, [c_u32, c_f32, c_u32]),
+    "vlq_shard_of_cell": (c_u32, [c_u32, c_u32]),
     "vlq_engine_sync": (c_i32, [c_vp, c_vp]),
     "vlq_engine_info": (c_i32, [c_vp, ctypes.POINTER(VlqInfo)]),
     "vlq_engine_add_synthetic": (c_i32, [c_vp, c_u64, c_u32, c_f32, c_u64]),

@@ -427,4 +427,6 @@ int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spr
 
 uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n) { return vlq::w2_of(w1, alpha, n); }
 
+uint32_t vlq_shard_of_cell(uint32_t cell, uint32_t shards) { return shards ? vlq::shard_of_cell(cell, shards) : 0u; }
+
 }  // extern "C"

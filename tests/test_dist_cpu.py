@@ -249,3 +249,21 @@ def test_oracle_staged_search_equals_search():
         b = o.search_from_top(q, top, w1, alpha, k)
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+def test_shard_of_cell_matches_the_engine():
+    """The Python restatement used by these tests == the engine's ownership
+    function (exported by libvlqgpu.so; host-only, no GPU needed), and the
+    hash spreads a region's n lists and the lists overall evenly."""
+    from paper_1901_00275_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(7)
+    cells = np.concatenate([np.arange(4096), rng.integers(0, 2**31, 4096)])
+    for shards in (1, 2, 3, 4, 8):
+        got = np.array([L.vlq_shard_of_cell(int(c), shards) for c in cells])
+        want = np.array([shard_of_cell(int(c), shards) for c in cells])
+        assert np.array_equal(got, want)
+    counts = np.bincount([shard_of_cell(c, 8) for c in range(65536 * 32)], minlength=8)
+    assert counts.min() > 0.99 * counts.mean() and counts.max() < 1.01 * counts.mean()
+    region = [shard_of_cell(17 * 32 + j, 8) for j in range(32)]
+    assert len(set(region)) >= 6  # one region's lists land on most ranks
