@@ -18,8 +18,13 @@
  *    "first_level_scan: need 0 < w1 <= k", "deserialize_index: bad magic
  *    in <path>", "index already holds a base set").
  *  - One engine per index (or per shard of an index).  Calls on one engine
- *    must be serialised by the caller, as with the reference's non-const
- *    methods.
+ *    are serialised internally by a per-engine mutex, so any number of host
+ *    threads may call vlq_engine_search on the same engine concurrently (the
+ *    reference's search is const and runs with the GIL released,
+ *    proj/python/bindings.cpp:99-126); each call sees the engine as left by
+ *    the previous one.  The "_device" variants only enqueue work: the mutex
+ *    orders the enqueues, and the caller orders its own streams.
+ *    vlq_engine_destroy waits for a call in flight on another thread.
  *  - There is no CPU fallback: without a CUDA device vlq_engine_create fails.
  */
 #ifndef VLQ_GPU_H
@@ -86,11 +91,23 @@ int vlq_engine_set_model(vlq_engine* e, uint32_t dim, uint32_t k, uint32_t n, ui
                          float lambda_lo, float lambda_hi, const float* centroids, const uint32_t* neighbor_ids,
                          const float* edge_sq_len, const float* pq_sub_centroids, const float* t3_or_null);
 
-/* Index.train (bindings.cpp:44-81) on the device: k-means codebook, exact
- * n-NN centroid graph, anchor displacements, per-subspace PQ; installs the
- * model into `e` (an index with zero points). */
+/* Index.train (bindings.cpp:44-81) on the device: k-means codebook
+ * (vlq_train_kmeans), exact n-NN centroid graph, anchor displacements,
+ * per-subspace PQ k-means; installs the model into `e` (an index with zero
+ * points). */
 int vlq_engine_train(vlq_engine* e, const float* train, uint64_t nt, uint32_t dim, uint32_t k, uint32_t n, uint32_t m,
                      uint32_t iters, uint64_t seed, int clamp_lambda);
+
+/* train_kmeans (proj/include/vlq/kmeans.hpp, proj/src/kmeans.cpp:104-185) on
+ * the device: k-means++ seeding (D^2 sampling, kmeans.cpp:54-102), Lloyd
+ * iterations with exact strict-'<' assignment and in-order double centroid
+ * sums, the reference's empty-cluster repair (kmeans.cpp:157-181).  x is
+ * n*dim host floats, out_centroids k*dim.  With init_or_null (k*dim host
+ * floats) the seeding is skipped and the result equals the reference's
+ * Lloyd loop from those centroids bit for bit; the seeding's random stream
+ * is the engine's own (a counter-based hash, not mt19937_64). */
+int vlq_train_kmeans(int device, const float* x, uint64_t n, uint32_t dim, uint32_t k, uint32_t iters, uint64_t seed,
+                     const float* init_or_null, float* out_centroids);
 
 /* Index.add: build_index (proj/src/index.cpp:134-203) + once-only rule and
  * observe_lambda_range for unclamped models (bindings.cpp:83-97). */

@@ -274,3 +274,67 @@ def line_lambda(a: float, b: float, c: float) -> float:
 
 def line_sqdist(a: float, b: float, c: float, lam: float) -> float:
     return float(lib().vo_line_sqdist_raw(a, b, c, lam))
+
+
+# ---- k-means restatement (oracle/train_oracle.cpp, kmeans.cpp) ---------------
+_TLIB = None
+
+
+def train_lib():
+    global _TLIB
+    if _TLIB is None:
+        path = os.path.join(HERE, "liboracle_train.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"oracle not built: {path} (run make -C oracle)")
+        L = ctypes.CDLL(path)
+        L.vo_train_last_error.restype = ctypes.c_char_p
+        for f in ("vo_train_kmeans", "vo_kmeans_seed", "vo_kmeans_lloyd"):
+            getattr(L, f).restype = ctypes.c_int
+        L.vo_train_kmeans.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
+        L.vo_kmeans_seed.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                     ctypes.c_uint64, ctypes.c_void_p]
+        L.vo_kmeans_lloyd.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]
+        L.vo_quantization_error.restype = ctypes.c_double
+        L.vo_quantization_error.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p,
+                                            ctypes.c_uint32]
+        _TLIB = L
+    return _TLIB
+
+
+def _tcheck(rc: int):
+    if rc != 0:
+        raise RuntimeError(train_lib().vo_train_last_error().decode())
+
+
+def train_kmeans(x: np.ndarray, k: int, iters: int, seed: int) -> np.ndarray:
+    """train_kmeans (kmeans.cpp:104-185), the reference's random stream included."""
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.empty((k, x.shape[1]), np.float32)
+    _tcheck(train_lib().vo_train_kmeans(_p(x), x.shape[0], x.shape[1], k, iters, seed, _p(out)))
+    return out
+
+
+def kmeans_seed(x: np.ndarray, k: int, seed: int) -> np.ndarray:
+    """seed_centroids (kmeans.cpp:54-102): the reference's k-means++ seeds."""
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.empty((k, x.shape[1]), np.float32)
+    _tcheck(train_lib().vo_kmeans_seed(_p(x), x.shape[0], x.shape[1], k, seed, _p(out)))
+    return out
+
+
+def kmeans_lloyd(x: np.ndarray, init: np.ndarray, iters: int) -> np.ndarray:
+    """The Lloyd + empty-cluster repair loop (kmeans.cpp:117-183) from init."""
+    x = np.ascontiguousarray(x, np.float32)
+    init = np.ascontiguousarray(init, np.float32)
+    out = np.empty_like(init)
+    _tcheck(train_lib().vo_kmeans_lloyd(_p(x), x.shape[0], x.shape[1], init.shape[0], iters, _p(init), _p(out)))
+    return out
+
+
+def quantization_error(x: np.ndarray, centroids: np.ndarray) -> float:
+    """quantization_error (kmeans.cpp:35-51)."""
+    x = np.ascontiguousarray(x, np.float32)
+    c = np.ascontiguousarray(centroids, np.float32)
+    return float(train_lib().vo_quantization_error(_p(x), x.shape[0], x.shape[1], _p(c), c.shape[0]))

@@ -46,6 +46,7 @@ _SIGS = {
     "vlq_engine_add": (c_i32, [c_vp, c_vp, c_u64, c_u32]),
     "vlq_engine_add_vecs": (c_i32, [c_vp, ctypes.c_char_p, c_u64]),
     "vlq_engine_train": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_u32, c_u32, c_u32, c_u64, c_i32]),
+    "vlq_train_kmeans": (c_i32, [c_i32, c_vp, c_u64, c_u32, c_u32, c_u32, c_u64, c_vp, c_vp]),
     "vlq_engine_search": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp]),
     "vlq_engine_search_device": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_set_tuning": (c_i32, [c_vp, ctypes.c_char_p, ctypes.c_int64]),

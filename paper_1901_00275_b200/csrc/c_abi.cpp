@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <random>
 #include <string>
@@ -10,8 +11,14 @@
 #include "../../include/vlq_gpu.h"
 #include "engine.h"
 
+// One engine per index.  Every call on an engine takes its mutex, so calls
+// from several host threads are serialised here: the reference's search is
+// const and may be called concurrently with the GIL released
+// (proj/python/bindings.cpp:99-126, :107), while this engine's staging and
+// workspace buffers are per-engine state.
 struct vlq_engine {
     vlq::Engine* impl;
+    std::mutex mu;
 };
 
 namespace {
@@ -75,12 +82,17 @@ int vlq_engine_create(const vlq_config* cfg, vlq_engine** out) {
 
 void vlq_engine_destroy(vlq_engine* e) {
     if (!e) return;
-    delete e->impl;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);  // waits for a call still running on another thread
+        delete e->impl;
+        e->impl = nullptr;
+    }
     delete e;
 }
 
-#define ENGINE_OR_FAIL(e) \
-    if (!(e) || !(e)->impl) return fail(VLQ_ERR_INVALID, "engine handle is NULL")
+#define ENGINE_OR_FAIL(e)                                                        \
+    if (!(e) || !(e)->impl) return fail(VLQ_ERR_INVALID, "engine handle is NULL"); \
+    std::lock_guard<std::mutex> engine_lock_((e)->mu)
 
 int vlq_engine_load_vlq1(vlq_engine* e, const char* path) {
     ENGINE_OR_FAIL(e);
@@ -128,6 +140,14 @@ int vlq_engine_train(vlq_engine* e, const float* train, uint64_t nt, uint32_t di
         vlq::HostModel hm =
             vlq::train_model_device(e->impl->device(), train, nt, dim, k, n, m, iters, seed, clamp_lambda != 0);
         e->impl->set_model(hm);
+    });
+}
+
+int vlq_train_kmeans(int device, const float* x, uint64_t n, uint32_t dim, uint32_t k, uint32_t iters, uint64_t seed,
+                     const float* init_or_null, float* out_centroids) {
+    return guarded([&] {
+        if ((n && !x) || !out_centroids) throw std::runtime_error("train_kmeans: NULL array");
+        vlq::train_kmeans_host(device, x, n, dim, k, iters, seed, init_or_null, out_centroids);
     });
 }
 
@@ -290,11 +310,8 @@ int vlq_gen_synthetic_device(int device, uint64_t first, uint64_t count, uint32_
     return guarded([&] {
         if (dim == 0 || clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
         if (!(spread > 0)) throw std::runtime_error("gen_synthetic: spread must be positive");
-        int prev = 0;
-        vlq::cuda_check(cudaGetDevice(&prev), "cudaGetDevice", __FILE__, __LINE__);
-        vlq::cuda_check(cudaSetDevice(device), "cudaSetDevice", __FILE__, __LINE__);
+        vlq::DeviceGuard g(device);
         vlq::launch_synth(first, count, dim, clusters, spread, seed, d_out, (cudaStream_t)stream);
-        cudaSetDevice(prev);
     });
 }
 
@@ -319,19 +336,19 @@ int vlq_engine_set_profiling(vlq_engine* e, int on) {
 int vlq_engine_get_stats(vlq_engine* e, vlq_stats* out) {
     ENGINE_OR_FAIL(e);
     if (!out) return fail(VLQ_ERR_INVALID, "stats: out is NULL");
-    const vlq::EngineStats& s = e->impl->stats();
-    out->launches = s.launches;
-    out->tiles = s.tiles;
-    out->flagged = s.flagged;
-    out->tc_fallbacks = s.tc_refine_fallbacks;
-    for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
-    return VLQ_OK;
+    return guarded([&] {  // folding in the profile syncs on CUDA events and may throw
+        const vlq::EngineStats& s = e->impl->stats();
+        out->launches = s.launches;
+        out->tiles = s.tiles;
+        out->flagged = s.flagged;
+        out->tc_fallbacks = s.tc_refine_fallbacks;
+        for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
+    });
 }
 
 int vlq_engine_reset_stats(vlq_engine* e) {
     ENGINE_OR_FAIL(e);
-    e->impl->reset_stats();
-    return VLQ_OK;
+    return guarded([&] { e->impl->reset_stats(); });
 }
 
 int vlq_engine_info(vlq_engine* e, vlq_info* out) {
@@ -386,11 +403,8 @@ int vlq_merge_topk_device(int device, const int64_t* d_in_ids, const float* d_in
                           uint32_t k, int64_t* d_out_ids, float* d_out_dists, void* stream) {
     return guarded([&] {
         if (nparts == 0 || nparts * (uint64_t)k > 8192) throw std::runtime_error("merge_topk: nparts*k must be in [1, 8192]");
-        int prev = 0;
-        vlq::cuda_check(cudaGetDevice(&prev), "cudaGetDevice", __FILE__, __LINE__);
-        vlq::cuda_check(cudaSetDevice(device), "cudaSetDevice", __FILE__, __LINE__);
+        vlq::DeviceGuard g(device);
         vlq::launch_merge_topk(d_in_ids, d_in_dists, nparts, nq, k, d_out_ids, d_out_dists, (cudaStream_t)stream);
-        cudaSetDevice(prev);
     });
 }
 

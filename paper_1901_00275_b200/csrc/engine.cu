@@ -80,8 +80,12 @@ Engine::~Engine() {
         if (sl.done) cudaEventDestroy(sl.done);
         if (sl.counts) cudaFreeHost(sl.counts);
     }
+    // the device buffers (members) are freed after this body on the engine's
+    // device; restore_ (declared first, destroyed last) then restores the
+    // caller's device
+    if (cudaGetDevice(&restore_.prev) != cudaSuccess) restore_.prev = -1;
+    cudaSetDevice(cfg_.device);
     if (stream_) {
-        cudaSetDevice(cfg_.device);
         cudaStreamSynchronize(stream_);
         cudaStreamDestroy(stream_);
     }
@@ -386,6 +390,19 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
     if (nb > 0xffffffffull) throw std::runtime_error("add: more than 2^32-1 points (VLQ1 ids are u32)");
     DeviceGuard g(cfg_.device);
     cudaStream_t st = stream_;
+    // the reference assigns the index only after build_index succeeds
+    // (bindings.cpp:89-96): a failed add must leave the lambda range of an
+    // unclamped model unchanged
+    struct RangeRollback {
+        Engine* e;
+        float lo, hi;
+        bool armed = true;
+        ~RangeRollback() {
+            if (!armed) return;
+            e->lo_ = e->model_.lo = lo;
+            e->hi_ = e->model_.hi = hi;
+        }
+    } rollback{this, lo_, hi_};
     chunk = std::max<uint64_t>(1, std::min(chunk, nb));
     DevBuf<float> X;
     DevBuf<uint32_t> best;
@@ -512,6 +529,7 @@ void Engine::add_stream(uint64_t nb, uint64_t chunk, const ChunkSource& src) {
     nent_ = nloc;
     pack_eterm_lam();
     base_count_ = nb;
+    rollback.armed = false;
 }
 
 void Engine::encode_host(const float* x, uint64_t nx, uint32_t* cells, float* lambdas, uint8_t* codes,

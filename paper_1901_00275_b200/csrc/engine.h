@@ -269,6 +269,14 @@ private:
     void search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                      float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st);
 
+    // first member, so destroyed last: puts the caller's CUDA device back
+    // after ~Engine and every member buffer has released its memory
+    struct DeviceRestore {
+        int prev = -1;
+        ~DeviceRestore() {
+            if (prev >= 0) cudaSetDevice(prev);
+        }
+    } restore_;
     EngineConfig cfg_;
     cudaStream_t stream_ = nullptr;
     bool profiling_ = false;
@@ -346,6 +354,8 @@ private:
 uint32_t w2_of(uint32_t w1, float alpha, uint32_t n);
 
 // Index.train on the device (train.cu); t3 is left empty (computed on upload).
+void train_kmeans_host(int device, const float* X, uint64_t n, uint32_t dim, uint32_t k, uint32_t iters,
+                       uint64_t seed, const float* init, float* out);
 HostModel train_model_device(int device, const float* train, uint64_t nt, uint32_t dim, uint32_t k, uint32_t n,
                              uint32_t m, uint32_t iters, uint64_t seed, bool clamp);
 

@@ -91,8 +91,10 @@ class Index:
     def train(train, k: int = 1024, n: int = 16, m: int = 8, iters: int = 10, seed: int = 42,
               clamp_lambda: bool = True, **engine_kw) -> "Index":
         """Index.train (bindings.cpp:44-81), on the GPU (csrc/train.cu).  Same
-        pipeline and error texts as the reference; the codebooks are not
-        bit-identical to the reference's (different k-means seeding)."""
+        pipeline (k-means++ seeding, Lloyd, empty-cluster repair, n-NN graph,
+        PQ) and error texts as the reference; the codebooks equal the
+        reference's in distribution, not bit for bit (the seeding's random
+        stream differs)."""
         t = _to_vecset(train)
         if m == 0 or t.shape[1] % m != 0:
             raise RuntimeError("m must divide the vector dimension")
@@ -126,7 +128,7 @@ class Index:
     def add(self, base) -> None:
         """Index.add (bindings.cpp:83-97): ids are the row numbers."""
         b = _to_vecset(base)
-        _lib.check(_lib.lib().vlq_engine_add(self._h, _p(b), b.shape[0], b.shape[1] if b.shape[0] else self.dim))
+        _lib.check(_lib.lib().vlq_engine_add(self._h, _p(b), b.shape[0], b.shape[1]))
 
     def add_vecs(self, path: str, chunk_rows: int = 0) -> None:
         """add(read_vecs(path)) streamed from the file (.fvecs / .bvecs /
@@ -354,8 +356,7 @@ def build_ivf_baseline(base, index: Index) -> IvfBaselineIndex:
     """build_ivf_baseline(base, codebook, pq) (ivf_baseline.cpp:11-51) with
     index's codebook and PQ."""
     b = _to_vecset(base)
-    dim = b.shape[1] if b.size else index.dim
-    _lib.check(_lib.lib().vlq_engine_ivf_build(index._h, _p(b), b.shape[0], dim))
+    _lib.check(_lib.lib().vlq_engine_ivf_build(index._h, _p(b), b.shape[0], b.shape[1]))
     return IvfBaselineIndex(index)
 
 
@@ -380,6 +381,24 @@ def search_ivf_baseline(ivf: IvfBaselineIndex, queries, w: int, top_k: int, *, r
     if return_scanned:
         return ids, dists, scanned
     return ids, dists
+
+
+def train_kmeans(train, k: int, iters: int = 10, seed: int = 42, *, init=None,
+                 device: int | None = None) -> np.ndarray:
+    """train_kmeans (kmeans.cpp:104-185) on the GPU -> float32 [k, dim]:
+    k-means++ seeding, Lloyd iterations, the reference's empty-cluster
+    repair.  With ``init`` the seeding is skipped (the Lloyd loop then equals
+    the reference's bit for bit)."""
+    t = _to_vecset(train)
+    out = np.empty((k, t.shape[1]), np.float32)
+    ini = None
+    if init is not None:
+        ini = np.ascontiguousarray(init, np.float32)
+        if ini.shape != (k, t.shape[1]):
+            raise RuntimeError("train_kmeans: init must be [k, dim]")
+    _lib.check(_lib.lib().vlq_train_kmeans(_default_device() if device is None else device, _p(t), t.shape[0],
+                                           t.shape[1], k, iters, seed, _p(ini), _p(out)))
+    return out
 
 
 def set_max_threads(threads: int) -> None:

@@ -144,3 +144,62 @@ def test_streamed_synthetic_add_equals_host_add(vlqadc, data):
     la, lb = a.lists(), b.lists()
     for u, v in zip(la, lb):
         assert np.array_equal(u, v)
+
+
+def test_concurrent_search_on_one_index(vlqadc, data, index):
+    """Index.search is const in the reference and runs with the GIL released
+    (bindings.cpp:99-126, :107): several host threads may search one index at
+    once.  The engine serialises the calls (per-engine mutex in the C ABI);
+    every thread's result must equal the sequential one bit for bit."""
+    import threading
+
+    base, queries = data
+    rng = np.random.default_rng(7)
+    batches = [np.ascontiguousarray(base[rng.integers(0, len(base), 300 + 37 * t)]) for t in range(4)]
+    params = [(16, 0.5, 10), (8, 0.25, 5), (32, 1.0, 20), (4, 0.5, 1)]
+    expect = [index.search(b, w1=w1, alpha=a, k=k) for b, (w1, a, k) in zip(batches, params)]
+    got = [[] for _ in range(4)]
+    errors = []
+
+    def worker(t):
+        try:
+            w1, a, k = params[t]
+            for _ in range(12):
+                got[t].append(index.search(batches[t], w1=w1, alpha=a, k=k))
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for t in range(4):
+        assert len(got[t]) == 12
+        for ids, d in got[t]:
+            assert np.array_equal(ids, expect[t][0])
+            assert np.array_equal(d.view(np.uint32), expect[t][1].view(np.uint32))
+
+
+def test_failed_add_leaves_lambda_range_unchanged(vlqadc, data):
+    """A failing add must not alter the index (the reference assigns the
+    index only after build_index succeeds, bindings.cpp:89-96)."""
+    base, _ = data
+    idx = vlqadc.Index.train(base, k=32, n=8, m=4, iters=4, seed=3, clamp_lambda=False)
+    before = idx.lambda_range
+    with pytest.raises(RuntimeError, match="dimension mismatch"):
+        idx.add(np.zeros((0, 5), np.float32))
+    assert idx.lambda_range == before and idx.ntotal == 0
+    # a degenerate edge (c == 0) fails the encode pass AFTER the unclamped
+    # model's observe_lambda_range pre-pass has run
+    mdl = idx.model()
+    elen = mdl["elen"].copy()
+    elen[:, :] = 0.0
+    bad = vlqadc.Index.from_model(mdl["dim"], mdl["k"], mdl["n"], mdl["m"], False, 0.25, 0.75, mdl["centroids"],
+                                  mdl["nbr"], elen, mdl["pq"])
+    with pytest.raises(RuntimeError, match="degenerate edge"):
+        bad.add(base)
+    assert bad.lambda_range == (0.25, 0.75) and bad.ntotal == 0
+    idx.add(base)
+    assert idx.ntotal == len(base)

@@ -142,3 +142,33 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
             ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
             oids, od, _ = o.search(q, w1, alpha, k)
             assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, v, w1, alpha, k)
+
+
+@pytest.mark.parametrize("dim,m", [(96, 16), (128, 8)])
+def test_tc_add_lists_and_search_at_baseline_shapes(vlqadc, oracle_mod, tmp_path, dim, m):
+    """BASELINE shapes (C4: D = 96, m = 16; C3/C5: D = 128, m = 8) with
+    n = 32 edges and K = 16384, tensor cores forced: the GPU add (TF32
+    ARGMIN proposals + certificate-checked exact refine) builds the same
+    lists as the oracle's build_index, point for point, and the 3xTF32 coarse
+    search returns the oracle's ids and distances."""
+    base = vlqadc.gen_synthetic(40000, dim, clusters=4000, spread=0.05, seed=35)
+    q = vlqadc.gen_synthetic(64, dim, clusters=4000, spread=0.05, seed=36)
+    idx = vlqadc.Index.train(base, k=16384, n=32, m=m, iters=2, seed=6)
+    idx.add(base)
+    path = str(tmp_path / f"bl{dim}.vlq")
+    idx.save(path)
+    o = oracle_mod.OracleIndex.load(path)
+    built = o.build(base)
+    off, ids, codes, lams = idx.lists()
+    assert np.array_equal(off, built.list_off) and np.array_equal(ids, built.ids)
+    assert np.array_equal(codes, built.codes) and np.array_equal(lams, built.lambdas)
+    # the add path's per-point outputs on held-out points (the certificate at D = 96 / 128)
+    extra = vlqadc.gen_synthetic(3000, dim, clusters=4000, spread=0.05, seed=37)
+    cells, lam, cd, lb = idx.encode(extra)
+    oc, ol, ocd, olb = o.assign(extra)
+    assert np.array_equal(cells, oc) and same_f32(lam, ol)
+    assert np.array_equal(cd, ocd) and np.array_equal(lb, olb)
+    for w1, alpha, k in [(64, 0.25, 100), (16, 1.0, 10)]:
+        ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
+        oids, od, _ = o.search(q, w1, alpha, k)
+        assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, w1, alpha, k)

@@ -175,3 +175,27 @@ def test_oracle_ivf_exhaustive_equals_full_adc():
     assert (sc == len(base)).all()
     with pytest.raises(RuntimeError, match="search_ivf_baseline: need 0 < w <= k"):
         o.ivf_search(lists, g["queries"], 0, 10)
+
+
+# Index.train arguments of the golden models (tests/golden/make_golden.py PY_CASES)
+TRAIN_PARAMS = {"smoke": dict(k=32, iters=8, seed=1), "unclamped": dict(k=16, iters=6, seed=3),
+                "m16": dict(k=64, iters=5, seed=5), "n1m8": dict(k=20, iters=5, seed=9),
+                "m1": dict(k=8, iters=5, seed=2)}
+
+
+@pytest.mark.parametrize("name", PY_CASES)
+def test_oracle_train_kmeans_equals_reference_codebook(name, oracle_mod):
+    """The k-means restatement (oracle/train_oracle.cpp) reproduces the
+    reference's trained first-level codebook bit for bit: the golden models
+    were written by the reference's Index.train, whose codebook is
+    train_kmeans(train, k, iters, seed) (bindings.cpp:57)."""
+    tp = TRAIN_PARAMS[name]
+    z, _, model_path = load_golden(name)
+    base = regen_base(z)
+    mdl = vlq1.read(model_path)
+    got = oracle_mod.train_kmeans(base, tp["k"], tp["iters"], tp["seed"])
+    assert np.array_equal(got.view(np.uint32), mdl.centroids.view(np.uint32))
+    # seeding + Lloyd from the seeds is the same computation
+    seeds = oracle_mod.kmeans_seed(base, tp["k"], tp["seed"])
+    again = oracle_mod.kmeans_lloyd(base, seeds, tp["iters"])
+    assert np.array_equal(again.view(np.uint32), mdl.centroids.view(np.uint32))
