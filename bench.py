@@ -40,6 +40,13 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+
+
+def w2_of(w1: int, alpha: float, n: int) -> int:
+    """QueryParams::w2 (search.hpp:16-20)."""
+    full = w1 * n
+    w = int(float(np.float32(alpha)) * full)
+    return min(max(w, 1), full)
 sys.path.insert(0, ROOT)
 
 METRIC = "QPS at fixed recall@100, 1B×96 synthetic, 1/2/4/8 B200 vs CPU ref"
@@ -57,11 +64,11 @@ WORKLOADS = {
                           "nq=10k, k=100", n=100_000_000, dim=96, k=4096, edges=32, m=16, clusters=4000,
                      ntrain=200_000),
     "c3": dict(desc="SIFT100M-shaped synthetic (configs[2]): 100M x 128, K=65536 x 32 lines, PQ 8 B, nq=10k, k=100",
-               n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=524_288, gt_queries=500),
+               n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=2_000_000, gt_queries=1000),
     "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k, k=100",
-               n=1_000_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536, ntrain=524_288, gt_queries=200),
+               n=1_000_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536, ntrain=2_000_000, gt_queries=1000),
     "c5": dict(desc="SIFT1B-shaped synthetic (configs[4]): 1B x 128, K=65536 x 32 lines, PQ 8 B, k=100",
-               n=1_000_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=524_288, gt_queries=200),
+               n=1_000_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=2_000_000, gt_queries=1000),
 }
 SPREAD, BASE_SEED, QUERY_SEED, TRAIN_SEED = 0.05, 42, 43, 1
 
@@ -126,21 +133,50 @@ class ClockSampler:
 
 
 def build_index(vlqadc, w, device, rank=0, world=1):
-    """Untimed setup: GPU training on a prefix sample, streamed GPU add."""
+    """Untimed setup: GPU training on a prefix sample (rank 0; the model is
+    broadcast to the other ranks), streamed GPU add of each rank's shard."""
     import torch
     t0 = time.time()
-    sample = torch.empty((w["ntrain"], w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
-    vlqadc.gen_synthetic_device(0, w["ntrain"], w["dim"], w["clusters"], SPREAD, BASE_SEED, sample.data_ptr(),
-                                device=device)
-    torch.cuda.synchronize(device)
-    idx = vlqadc.Index.train(sample.cpu().numpy(), k=w["k"], n=w["edges"], m=w["m"], iters=10, seed=TRAIN_SEED,
-                             device=device, shard_rank=rank, shard_count=world)
+    model = None
+    if rank == 0:
+        sample = torch.empty((w["ntrain"], w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
+        vlqadc.gen_synthetic_device(0, w["ntrain"], w["dim"], w["clusters"], SPREAD, BASE_SEED, sample.data_ptr(),
+                                    device=device)
+        torch.cuda.synchronize(device)
+        trained = vlqadc.Index.train(sample.cpu().numpy(), k=w["k"], n=w["edges"], m=w["m"], iters=10,
+                                     seed=TRAIN_SEED, device=device)
+        model = trained.model()
+        del trained, sample
+    if world > 1:
+        import torch.distributed as dist
+        box = [model]
+        dist.broadcast_object_list(box, src=0)
+        model = box[0]
+    digest = model_digest(model)
+    if world > 1:
+        import torch.distributed as dist
+        digests = [None] * world
+        dist.all_gather_object(digests, digest)
+        assert len(set(digests)) == 1, f"ranks hold different models: {digests}"
+    idx = vlqadc.Index.from_model(model["dim"], model["k"], model["n"], model["m"], model["clamp"], model["lo"],
+                                  model["hi"], model["centroids"], model["nbr"], model["elen"], model["pq"],
+                                  device=device, shard_rank=rank, shard_count=world)
     t1 = time.time()
     idx.add_synthetic(w["n"], clusters=w["clusters"], spread=SPREAD, seed=BASE_SEED)
     t2 = time.time()
     log(f"[setup] rank {rank}: train {t1 - t0:.1f}s, add {w['n']} points {t2 - t1:.1f}s, "
-        f"local entries {idx.local_entries}")
-    return idx, {"train_s": round(t1 - t0, 2), "add_s": round(t2 - t1, 2)}
+        f"local entries {idx.local_entries}, model {digest}")
+    return idx, {"train_s": round(t1 - t0, 2), "add_s": round(t2 - t1, 2), "train_points": w["ntrain"],
+                 "model_sha256_16": digest}
+
+
+def model_digest(model) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for key in ("centroids", "nbr", "elen", "pq"):
+        h.update(np.ascontiguousarray(model[key]).tobytes())
+    h.update(np.array([model["lo"], model["hi"]], np.float32).tobytes())
+    return h.hexdigest()[:16]
 
 
 def make_queries(vlqadc, w, nq, device, kind="ref"):
@@ -213,6 +249,27 @@ def time_port(idx, queries: np.ndarray, w1, alpha, k, budget_s: float, warm: int
     return ns / dt, ns, dt, rids, rd, warm
 
 
+def config_of(args, w, world):
+    return {"workload": w["desc"], "n_base": w["n"], "dim": w["dim"], "K": w["k"], "n_edges": w["edges"],
+            "m_bytes": w["m"], "nq": args.nq, "w1": args.w1, "alpha": args.alpha, "k": args.k,
+            "train_points": w["ntrain"],
+            "parallelism": f"list-sharded x{world} (hashed cells)" if world > 1 else "single GPU",
+            "l2": "flushed between steps (512 MiB write)", "data": "synthetic Gaussian mixture (sigma 0.05)"}
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: one process per GPU under
+    torch.distributed.run on 127.0.0.1 (the driver's own launch line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log(f"[launch] {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -235,14 +292,29 @@ def main():
                     help="also build and time the IVFADC comparison baseline (ivf_baseline.cpp) on the same model, w = w1")
     ap.add_argument("--profile", action="store_true",
                     help="wrap the timed steps in cudaProfilerStart/Stop (for ncu --profile-from-start off) and exit")
+    ap.add_argument("--replay-points", type=int, default=100_000,
+                    help="sampled base rows whose add-path outputs are replayed against the oracle")
+    ap.add_argument("--ref-setup", default=None, help=argparse.SUPPRESS)  # internal: reference-arm index builder
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        sys.exit(self_launch(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.ref_setup:
+        ref_setup(args)
+        return
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
 
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     # one process per GPU; VLQ_DIST_BACKEND=gloo (with ranks sharing GPUs
     # round-robin) is the single-GPU rehearsal of the N > 1 path
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
@@ -255,17 +327,7 @@ def main():
     torch.cuda.set_device(local)
     os.environ["VLQ_DEVICE"] = str(local)
     w = WORKLOADS[args.workload]
-    cfg = {"workload": w["desc"], "n_base": w["n"], "dim": w["dim"], "K": w["k"], "n_edges": w["edges"],
-           "m_bytes": w["m"], "nq": args.nq, "w1": args.w1, "alpha": args.alpha, "k": args.k,
-           "parallelism": f"list-sharded x{world} (hashed cells)" if world > 1 else "single GPU",
-           "l2": "flushed between steps (512 MiB write)", "data": "synthetic Gaussian mixture (sigma 0.05)"}
-
-    if args.impl == "reference":
-        run_reference_arm(args, w, cfg, rank, world, local)
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+    cfg = config_of(args, w, world)
 
     from paper_1901_00275_b200 import vlqadc
     from paper_1901_00275_b200.dist import ShardedIndex
@@ -372,6 +434,37 @@ def main():
 
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
+    # workload shape: scanned entries per query (S_q) and list lengths
+    sq = scanned.cpu().numpy().astype(np.float64)
+    lens = np.diff(idx.list_offsets().astype(np.int64))
+    reg = lens.reshape(w["k"], w["edges"]).sum(axis=1)
+    shape = {"scanned_per_query": {"mean": round(float(sq.mean()), 1), "p50": float(np.percentile(sq, 50)),
+                                   "p99": float(np.percentile(sq, 99)), "max": float(sq.max())},
+             "uniform_model_scanned_per_query": round(w2_of(args.w1, args.alpha, w["edges"]) * w["n"] /
+                                                      (w["k"] * w["edges"]), 1),
+             "list_len": {"mean": round(float(lens.mean()), 2), "p99": float(np.percentile(lens, 99)),
+                          "max": int(lens.max()), "empty_frac": round(float((lens == 0).mean()), 4)},
+             "region_len": {"mean": round(float(reg.mean()), 2), "p99": float(np.percentile(reg, 99)),
+                            "max": int(reg.max())}}
+    # the coarse contraction (first_level_scan's nq x K x D distances) on the
+    # tensor cores: logical 2 nq K D FLOP against the dense TF32 rate
+    coarse_ms = stats["phase_ms"]["coarse"] / args.steps
+    gemm_flop = 2.0 * nq * w["k"] * w["dim"]
+    bf16 = peaks.get("bf16_tflops")
+    tf32_peak = float(bf16) / 2.0 if bf16 else 1100.0
+    gemm = {"bound": "tensor", "kernel": "k_coarse_tc (tcgen05.mma kind::tf32: 1xTF32 tile-minimum pass + "
+                                         "3xTF32 filter pass)",
+            "flop_per_launch": gemm_flop, "coarse_ms_per_step": round(coarse_ms, 4),
+            "achieved": round(gemm_flop / (coarse_ms / 1e3) / 1e12, 1) if coarse_ms > 0 else None,
+            "issued_flop_per_launch": 4 * gemm_flop,
+            "achieved_issued": round(4 * gemm_flop / (coarse_ms / 1e3) / 1e12, 1) if coarse_ms > 0 else None,
+            "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (the dense TF32 rate is half the bf16 rate)"
+                            if bf16 else "fallback: 1.1 PFLOP/s dense TF32 (datasheet)"),
+            "tc_used": bool(w["k"] >= 16384 and w["dim"] % 8 == 0)}
+    if coarse_ms > 0:
+        gemm["frac"] = round(gemm["achieved"] / tf32_peak, 4)
+        gemm["frac_issued"] = round(gemm["achieved_issued"] / tf32_peak, 4)
     achieved = scan_bytes_per_step / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"scan_traffic_{args.workload}.json")
@@ -384,7 +477,7 @@ def main():
                 "algorithmic_bytes_per_launch": scan_bytes_per_step,
                 "bytes_per_candidate": w["m"] + 5, "scan_ms_per_launch": round(scan_ms, 4),
                 "phase_ms_per_step": {p: round(v / args.steps, 4) for p, v in stats["phase_ms"].items()},
-                "scan_share_of_step": round(scan_ms / (ms_max / args.steps), 4)}
+                "scan_share_of_step": round(scan_ms / (ms_max / args.steps), 4), "gemm": gemm}
 
     # recall on the exact ground truth of a query subset
     ngt = min(args.gt_queries or w.get("gt_queries", 1000), nq)

@@ -496,13 +496,37 @@ int vo_search_from_sel(const vo_index* ix, const float* queries, uint64_t nq, ui
  * (pq.cpp:52-67) -> quantize_lambda (index.cpp:12-17).  Outputs the cell,
  * the exact lambda, the PQ code and the lambda byte of every point; the
  * caller buckets by cell in point order (index.cpp:189-200). */
+/* row[i] = sqdist(x, c_i) for a group of points: each centroid row is read
+ * once for the whole group (the distances themselves keep the reference's
+ * sequential order over d); test-infrastructure speed only. */
+static void dist_rows(const vo_index* ix, const float* xs, uint32_t np, float* rows) {
+    const uint32_t k = ix->k, dim = ix->dim;
+    float* xt = (float*)malloc(sizeof(float) * dim * 16); /* [d][p] */
+    for (uint32_t d = 0; d < dim; d++)
+        for (uint32_t p = 0; p < 16; p++) xt[d * 16 + p] = p < np ? xs[(size_t)p * dim + d] : 0.0f;
+    for (uint32_t i = 0; i < k; i++) {
+        const float* c = ix->centroids + (size_t)i * dim;
+        float acc[16] = {0};
+        for (uint32_t d = 0; d < dim; d++) {
+            const float cd = c[d];
+            const float* xd = xt + d * 16;
+            for (uint32_t p = 0; p < 16; p++) { /* 16 independent sequential chains */
+                const float t = xd[p] - cd;
+                acc[p] = acc[p] + t * t;
+            }
+        }
+        for (uint32_t p = 0; p < np; p++) rows[(size_t)p * k + i] = acc[p];
+    }
+    free(xt);
+}
+
 static int assign_one(const vo_index* ix, const float* x, float* row, float* r, uint32_t* cell,
-                      float* lam_out, uint8_t* code, int clamp) {
+                      float* lam_out, uint8_t* code, int clamp, int row_ready) {
     const uint32_t k = ix->k, n = ix->n, dim = ix->dim, m = ix->m, dsub = dim / m;
     uint32_t best = 0;
     float best_d = FLT_MAX;
     for (uint32_t i = 0; i < k; i++) {
-        float d = vo_sqdist(x, ix->centroids + (size_t)i * dim, dim);
+        float d = row_ready ? row[i] : vo_sqdist(x, ix->centroids + (size_t)i * dim, dim);
         row[i] = d;
         if (d < best_d) {
             best_d = d;
@@ -557,6 +581,7 @@ typedef struct {
     float* lambdas;
     uint8_t* codes;
     uint8_t* lam_bytes;
+    int64_t nb;
 } assign_ctx;
 
 typedef struct {
@@ -564,10 +589,12 @@ typedef struct {
     float* r;
 } assign_scratch_t;
 
+#define ASSIGN_GROUP 16
+
 static void* assign_scratch(void* c) {
     assign_ctx* ctx = (assign_ctx*)c;
     assign_scratch_t* s = (assign_scratch_t*)malloc(sizeof *s);
-    s->row = (float*)malloc(sizeof(float) * ctx->ix->k);
+    s->row = (float*)malloc(sizeof(float) * ctx->ix->k * ASSIGN_GROUP);
     s->r = (float*)malloc(sizeof(float) * ctx->ix->dim);
     return s;
 }
@@ -579,14 +606,21 @@ static void assign_scratch_free(void* p) {
     free(s);
 }
 
-static int assign_item(void* c, void* scratch, int64_t p) {
+/* item g = points [g*ASSIGN_GROUP, ...) */
+static int assign_item(void* c, void* scratch, int64_t g) {
     assign_ctx* ctx = (assign_ctx*)c;
     assign_scratch_t* s = (assign_scratch_t*)scratch;
     const vo_index* ix = ctx->ix;
-    if (assign_one(ix, ctx->base + (size_t)p * ix->dim, s->row, s->r, ctx->cells + p, ctx->lambdas + p,
-                   ctx->codes ? ctx->codes + (size_t)p * ix->m : NULL, ctx->clamp))
-        return -1;
-    if (ctx->lam_bytes) ctx->lam_bytes[p] = vo_quantize_lambda(ctx->lambdas[p], ix->lo, ix->hi);
+    const int64_t p0 = g * ASSIGN_GROUP;
+    const uint32_t np = (uint32_t)((ctx->nb - p0) < ASSIGN_GROUP ? (ctx->nb - p0) : ASSIGN_GROUP);
+    dist_rows(ix, ctx->base + (size_t)p0 * ix->dim, np, s->row);
+    for (uint32_t q = 0; q < np; q++) {
+        const int64_t p = p0 + q;
+        if (assign_one(ix, ctx->base + (size_t)p * ix->dim, s->row + (size_t)q * ix->k, s->r, ctx->cells + p,
+                       ctx->lambdas + p, ctx->codes ? ctx->codes + (size_t)p * ix->m : NULL, ctx->clamp, 1))
+            return -1;
+        if (ctx->lam_bytes) ctx->lam_bytes[p] = vo_quantize_lambda(ctx->lambdas[p], ix->lo, ix->hi);
+    }
     return 0;
 }
 
@@ -595,8 +629,9 @@ static int assign_item(void* c, void* scratch, int64_t p) {
  * index.cpp:110-132, which runs assign_point with clamp = false). */
 int vo_assign(const vo_index* ix, const float* base, uint64_t nb, int clamp, uint32_t* cells,
               float* lambdas, uint8_t* codes, uint8_t* lam_bytes, int nthreads) {
-    assign_ctx ctx = {ix, base, clamp, cells, lambdas, codes, lam_bytes};
-    return par_for((int64_t)nb, 256, nthreads, &ctx, assign_item, assign_scratch, assign_scratch_free);
+    assign_ctx ctx = {ix, base, clamp, cells, lambdas, codes, lam_bytes, (int64_t)nb};
+    return par_for(((int64_t)nb + ASSIGN_GROUP - 1) / ASSIGN_GROUP, 4, nthreads, &ctx, assign_item, assign_scratch,
+                   assign_scratch_free);
 }
 
 /* Direct (non-decomposed) ADC: |y - anchor(lambda) - pq_decode(code)|^2, the
