@@ -249,6 +249,75 @@ def time_port(idx, queries: np.ndarray, w1, alpha, k, budget_s: float, warm: int
     return ns / dt, ns, dt, rids, rd, warm
 
 
+def add_replay(vlqadc, idx, w, npoints: int, device: int, seed: int = 7, full_cells: int = 24) -> dict:
+    """Sampled add-path parity of a built index (proj/tests/test_index.cpp:161-189
+    pattern) without copying the index to the host.  The base generator is
+    counter-based, so any row i is regenerated on the device.
+      1. `npoints` rows (blocks of 1000 consecutive ids at seeded random
+         starts): the GPU encode (Index.encode) and the oracle's assign on host
+         copies of the model give the same (cell, exact lambda, code, lambda
+         byte) bit for bit;
+      2. each sampled id is present in the STORED list of its oracle cell with
+         that code and lambda byte, and every fetched list is ascending by id;
+      3. `full_cells` whole stored lists: every entry's row, regenerated and
+         assigned by the oracle, maps to that cell with the stored code and
+         lambda byte (no foreign entries)."""
+    import torch
+    from oracle import oracle as orc, vlq1  # the checker
+    t0 = time.time()
+    mdl = idx.model()
+    o = orc.OracleIndex(vlq1.Vlq1(mdl["dim"], mdl["k"], mdl["n"], mdl["m"], mdl["clamp"], mdl["lo"], mdl["hi"],
+                                  mdl["centroids"], mdl["nbr"], mdl["elen"], mdl["pq"]))
+    rng = np.random.default_rng(seed)
+    blk = 1000
+    nblk = max(1, npoints // blk)
+    starts = np.sort(rng.choice(max(1, (w["n"] - blk) // blk), size=nblk, replace=False)) * blk
+    buf = torch.empty((nblk * blk, w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
+    for b, s0 in enumerate(starts):
+        vlqadc.gen_synthetic_device(int(s0), blk, w["dim"], w["clusters"], SPREAD, BASE_SEED,
+                                    buf[b * blk].data_ptr(), device=device)
+    torch.cuda.synchronize(device)
+    x = buf.cpu().numpy()
+    rows = (starts[:, None] + np.arange(blk)[None, :]).ravel().astype(np.int64)
+    gc, gl, gcd, glb = idx.encode(x)
+    oc, ol, ocd, olb = o.assign(x)
+    encode_ok = bool(np.array_equal(gc, oc) and np.array_equal(gl.view(np.uint32), ol.view(np.uint32)) and
+                     np.array_equal(gcd, ocd) and np.array_equal(glb, olb))
+    # 2. presence in the stored lists
+    ucells, inv = np.unique(oc, return_inverse=True)
+    counts, ids, codes, lams = idx.cells(ucells)
+    seg = np.zeros(len(ucells) + 1, np.int64)
+    np.cumsum(counts.astype(np.int64), out=seg[1:])
+    sorted_ok = all(bool(np.all(np.diff(ids[seg[i]:seg[i + 1]].astype(np.int64)) > 0)) for i in range(len(ucells)))
+    present = 0
+    for p_ in range(len(rows)):
+        a, b = seg[inv[p_]], seg[inv[p_] + 1]
+        j = a + int(np.searchsorted(ids[a:b], rows[p_]))
+        if j < b and ids[j] == rows[p_] and np.array_equal(codes[j], ocd[p_]) and lams[j] == olb[p_]:
+            present += 1
+    # 3. whole lists: no foreign entries
+    nonempty = np.flatnonzero(counts > 0)
+    pick = rng.choice(nonempty, size=min(full_cells, len(nonempty)), replace=False)
+    ent_ids = np.concatenate([ids[seg[i]:seg[i + 1]] for i in pick])
+    ent_cell = np.concatenate([np.full(int(counts[i]), ucells[i], np.uint32) for i in pick])
+    ent_codes = np.concatenate([codes[seg[i]:seg[i + 1]] for i in pick])
+    ent_lams = np.concatenate([lams[seg[i]:seg[i + 1]] for i in pick])
+    xr = torch.empty((len(ent_ids), w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
+    for r, i in enumerate(ent_ids):
+        vlqadc.gen_synthetic_device(int(i), 1, w["dim"], w["clusters"], SPREAD, BASE_SEED, xr[r].data_ptr(),
+                                    device=device)
+    torch.cuda.synchronize(device)
+    fc, _, fcd, flb = o.assign(xr.cpu().numpy())
+    lists_ok = bool(np.array_equal(fc, ent_cell) and np.array_equal(fcd, ent_codes) and np.array_equal(flb, ent_lams))
+    return {"add_replay_bit_exact": bool(encode_ok and present == len(rows) and sorted_ok and lists_ok),
+            "points": int(len(rows)), "encode_bit_exact_vs_oracle": encode_ok,
+            "present_in_stored_list": int(present), "lists_ascending": bool(sorted_ok),
+            "whole_lists_checked": int(len(pick)), "whole_list_entries": int(len(ent_ids)),
+            "whole_lists_bit_exact": lists_ok, "seconds": round(time.time() - t0, 1),
+            "method": "rows regenerated by the counter-based generator; oracle assign (oracle/vlq_oracle.c) on "
+                      "host copies of the model vs Index.encode and vs the stored posting lists (vlq_engine_get_cells)"}
+
+
 def config_of(args, w, world):
     return {"workload": w["desc"], "n_base": w["n"], "dim": w["dim"], "K": w["k"], "n_edges": w["edges"],
             "m_bytes": w["m"], "nq": args.nq, "w1": args.w1, "alpha": args.alpha, "k": args.k,
@@ -535,6 +604,14 @@ def main():
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "kind": kind, "unavailable": f"{type(e).__name__}: {e}"}
 
+    replay = None
+    if world == 1 and args.replay_points > 0:
+        try:
+            replay = add_replay(vlqadc, idx, w, args.replay_points, local)
+        except Exception as e:  # reported, never silently replaced
+            replay = {"add_replay_bit_exact": None, "unavailable": f"{type(e).__name__}: {e}"}
+        log(f"[replay] {replay}")
+
     sweep = None
     if args.sweep and world == 1:
         sweep = []
@@ -594,7 +671,7 @@ def main():
             "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
             "coarse_stage": ("query-split first level + cell selection (1/N of the batch per rank), "
                              "selections all-gathered") if world > 1 else "single GPU",
-            "ivfadc": ivf_line, "sweep": sweep,
+            "ivfadc": ivf_line, "sweep": sweep, "add_replay": replay,
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
             "fallback_queries_per_step": stats["flagged"] / args.steps,
             "tc_coarse_fallbacks_per_step": stats["tc_fallbacks"] / args.steps}
@@ -604,48 +681,118 @@ def main():
         dist.destroy_process_group()
 
 
-def run_reference_arm(args, w, cfg, rank, world, local):
-    """--impl reference: the reference's own CPU search (oracle/_ref) on the
-    same workload.  The index is built once on the GPU (the reference needs
-    hours to train/add at these sizes) and handed to the reference
-    as a VLQ1 file; the timed path is the unmodified reference Index.search."""
+def ref_setup(args):
+    """Child process of the reference arm: builds the workload's index on the
+    GPU (the reference needs hours to train / add at these sizes),
+    exports it as VLQ1 and writes the queries plus the GPU's own results, so
+    the timed reference process never maps libvlqgpu.so."""
+    import torch
+    from paper_1901_00275_b200 import vlqadc
+    out = args.ref_setup
+    w = WORKLOADS[args.workload]
+    idx, setup = build_index(vlqadc, w, 0)
+    q = make_queries(vlqadc, w, args.nq, 0)
+    ids = torch.empty((args.nq, args.k), dtype=torch.int64, device=q.device)
+    dists = torch.empty((args.nq, args.k), dtype=torch.float32, device=q.device)
+    scanned = torch.empty((args.nq,), dtype=torch.int64, device=q.device)
+    idx.search_device(q.data_ptr(), args.nq, args.w1, args.alpha, args.k, ids.data_ptr(), dists.data_ptr(),
+                      scanned.data_ptr(), 0)
+    idx.sync(0)
+    np.save(os.path.join(out, "queries.npy"), q.cpu().numpy())
+    np.save(os.path.join(out, "gpu_ids.npy"), ids.cpu().numpy())
+    np.save(os.path.join(out, "gpu_dists.npy"), dists.cpu().numpy())
+    t0 = time.time()
+    idx.save(os.path.join(out, "bench.vlq"))
+    setup["vlq1_save_s"] = round(time.time() - t0, 1)
+    json.dump(setup, open(os.path.join(out, "setup.json"), "w"))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU search (oracle/_ref, its
+    unmodified sources compiled by oracle/Makefile) on the same workload, on
+    the box's host cores.  The index is built on the GPU in a child process
+    (ref_setup) and handed over as a VLQ1 file; this process loads only the
+    reference module.  Timed: Index.search on bounded query slices with
+    set_max_threads(0) (hardware_concurrency, parallel.cpp:17-24), plus a
+    set_max_threads(1) sample; every searched slice is checked bit-exact
+    against the GPU's results for the same queries.  Under torchrun only rank
+    0 runs."""
     if rank != 0:
         return
-    from paper_1901_00275_b200 import vlqadc
+    w = WORKLOADS[args.workload]
+    cfg = config_of(args, w, 1)
     refmod = ref_module()
-    idx, _ = build_index(vlqadc, w, local)
-    qh = make_queries(vlqadc, w, args.nq, local).cpu().numpy()
     with tempfile.TemporaryDirectory(dir=os.environ.get("VLQ_REF_TMP")) as tmp:
-        path = os.path.join(tmp, "bench.vlq")
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT",
+                            "GROUP_RANK", "ROLE_RANK", "TORCHELASTIC_RUN_ID")}
         t0 = time.time()
-        idx.save(path)
-        del idx
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-setup", tmp, "--workload", args.workload,
+                        "--nq", str(args.nq), "--w1", str(args.w1), "--alpha", str(args.alpha), "--k", str(args.k)],
+                       env=env, check=True)
         t1 = time.time()
+        path = os.path.join(tmp, "bench.vlq")
+        gb = os.path.getsize(path) / 1e9
         ref_idx = refmod.Index.load(path)
-        log(f"[reference] VLQ1 hand-off: save {t1 - t0:.1f}s ({os.path.getsize(path) / 1e9:.1f} GB), "
-            f"reference load {time.time() - t1:.1f}s")
-    refmod.set_max_threads(0)
+        log(f"[reference] GPU build + VLQ1 export {t1 - t0:.1f}s ({gb:.1f} GB), reference load {time.time() - t1:.1f}s")
+        qh = np.load(os.path.join(tmp, "queries.npy"))
+        gids = np.load(os.path.join(tmp, "gpu_ids.npy"))
+        gd = np.load(os.path.join(tmp, "gpu_dists.npy"))
+        setup = json.load(open(os.path.join(tmp, "setup.json")))
     alpha = np.float32(args.alpha)
-    ref_idx.search(qh[:100], w1=args.w1, alpha=alpha, k=args.k)
+    parity = {"queries_checked": 0, "mismatched_queries": 0}
+
+    def search(lo, hi):
+        ids, d = ref_idx.search(qh[lo:hi], w1=args.w1, alpha=alpha, k=args.k)
+        bad = ~((ids == gids[lo:hi]).all(axis=1) & (d.view(np.uint32) == gd[lo:hi].view(np.uint32)).all(axis=1))
+        parity["queries_checked"] += hi - lo
+        parity["mismatched_queries"] += int(bad.sum())
+
+    refmod.set_max_threads(0)
+    search(0, 100)  # warm-up excluded (eval.cpp:91)
     t = time.perf_counter()
-    ref_idx.search(qh[100:300], w1=args.w1, alpha=alpha, k=args.k)
+    search(100, 300)
     rate = 200 / max(time.perf_counter() - t, 1e-6)
-    per_step = int(max(50, min(args.nq, rate * 6.0)))
+    per_step = int(max(50, min(args.nq - 300, rate * 6.0)))
     times = []
     for s in range(args.warmup + args.steps):
-        lo = (s * per_step) % max(1, args.nq - per_step)
+        lo = 300 + (s * per_step) % max(1, args.nq - 300 - per_step)
         t = time.perf_counter()
-        ref_idx.search(qh[lo:lo + per_step], w1=args.w1, alpha=alpha, k=args.k)
+        search(lo, lo + per_step)
         if s >= args.warmup:
             times.append(time.perf_counter() - t)
     value = per_step * len(times) / sum(times)
+    # one host thread (set_max_threads(1)): a bounded sample of ~10 s
+    refmod.set_max_threads(1)
+    n1 = max(5, min(200, int(10.0 * rate / max(1, os.cpu_count() or 1))))
+    t = time.perf_counter()
+    search(0, n1)
+    one_thread = n1 / (time.perf_counter() - t)
+    refmod.set_max_threads(0)
+    cores = os.cpu_count()
+    sample = (f"{per_step} of the {args.nq} benchmark queries per step (slices after 300 warm-up/probe queries), "
+              f"reference Index.search (oracle/_ref, unmodified sources), set_max_threads(0) = {cores} threads")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(cfg, reference_sample=f"{per_step} queries per step"),
-            "cpu_baseline": {"value": round(value, 2), "unit": "queries/s", "cores": os.cpu_count(),
-                             "kind": "reference",
-                             "sample": f"{per_step} queries per step, reference Index.search, set_max_threads(0)"},
+            "cpu_baseline": {"value": round(value, 2), "unit": "queries/s", "cores": cores, "kind": "reference",
+                             "cpu_model": cpu_model(), "sample": sample,
+                             "one_thread": {"value": round(one_thread, 3), "unit": "queries/s", "queries": n1,
+                                            "threads": 1}},
+            "parity_vs_gpu": dict(parity, bit_exact=parity["mismatched_queries"] == 0,
+                                  what="reference ids and distances vs the GPU engine's for the same queries"),
+            "setup": setup,
             "e2e": {"value": round(value, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

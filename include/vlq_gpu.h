@@ -232,6 +232,14 @@ int vlq_engine_get_model(vlq_engine* e, float* centroids, uint32_t* neighbor_ids
  * ids, codes and lambdas all NULL only the offsets are copied. */
 int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8_t* codes, uint8_t* lambdas);
 
+/* The posting lists of the given cells only (index.hpp:26-34 PostingList),
+ * concatenated in request order: counts[i] = length of list cells[i]; ids,
+ * codes (x m) and lambdas hold sum(counts) entries.  ids, codes and lambdas
+ * may all be NULL (counts only).  For sampled checks of 1e9-entry indexes
+ * without copying the whole index to the host. */
+int vlq_engine_get_cells(vlq_engine* e, const uint32_t* cells, uint32_t ncells, uint64_t* counts, uint32_t* ids,
+                         uint8_t* codes, uint8_t* lambdas);
+
 /* Per-point add-path outputs without mutating the index: assign_point +
  * assign_edge + residual + pq_encode + quantize_lambda (index.cpp:86-106,
  * 167-188).  Any output pointer may be NULL. */

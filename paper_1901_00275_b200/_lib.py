@@ -71,6 +71,7 @@ _SIGS = {
     "vlq_engine_get_stats": (c_i32, [c_vp, ctypes.POINTER(VlqStats)]),
     "vlq_engine_reset_stats": (c_i32, [c_vp]),
     "vlq_engine_get_lists": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "vlq_engine_get_cells": (c_i32, [c_vp, c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_get_model": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_encode": (c_i32, [c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "vlq_merge_topk_device": (c_i32, [c_i32, c_vp, c_vp, c_u32, c_u64, c_u32, c_vp, c_vp, c_vp]),

@@ -390,6 +390,15 @@ int vlq_engine_get_lists(vlq_engine* e, uint64_t* list_off, uint32_t* ids, uint8
     });
 }
 
+int vlq_engine_get_cells(vlq_engine* e, const uint32_t* cells, uint32_t ncells, uint64_t* counts, uint32_t* ids,
+                         uint8_t* codes, uint8_t* lambdas) {
+    ENGINE_OR_FAIL(e);
+    return guarded([&] {
+        if (ncells && !cells) throw std::runtime_error("get_cells: cells is NULL");
+        e->impl->get_cells(cells, ncells, counts, ids, codes, lambdas);
+    });
+}
+
 int vlq_engine_encode(vlq_engine* e, const float* x, uint64_t n, uint32_t* cells, float* lambdas, uint8_t* codes,
                       uint8_t* lambda_bytes) {
     ENGINE_OR_FAIL(e);

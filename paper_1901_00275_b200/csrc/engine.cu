@@ -577,6 +577,59 @@ void Engine::get_lists(HostLists& out, bool offsets_only) {
     CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
+// one CTA per requested cell: copy its entries to their slot of the
+// request-ordered output (sampled add replay of 1e9-entry indexes without
+// copying the whole index to the host)
+__global__ void k_gather_cells(const uint32_t* __restrict__ cells, const uint64_t* __restrict__ dst_off,
+                               const uint64_t* __restrict__ list_off, const uint32_t* __restrict__ ids,
+                               const uint8_t* __restrict__ codes, const uint8_t* __restrict__ lambdas, uint32_t m,
+                               uint32_t* __restrict__ o_ids, uint8_t* __restrict__ o_codes,
+                               uint8_t* __restrict__ o_lam) {
+    const uint32_t c = cells[blockIdx.x];
+    const uint64_t src = list_off[c], len = list_off[c + 1] - src, dst = dst_off[blockIdx.x];
+    for (uint64_t e = threadIdx.x; e < len; e += blockDim.x) {
+        o_ids[dst + e] = ids[src + e];
+        o_lam[dst + e] = lambdas[src + e];
+    }
+    for (uint64_t b = threadIdx.x; b < len * m; b += blockDim.x) o_codes[dst * m + b] = codes[src * m + b];
+}
+
+void Engine::get_cells(const uint32_t* cells, uint32_t ncells, uint64_t* counts, uint32_t* ids, uint8_t* codes,
+                       uint8_t* lambdas) {
+    DeviceGuard g(cfg_.device);
+    const uint64_t ncell_total = (uint64_t)k_ * n_;
+    for (uint32_t i = 0; i < ncells; ++i)
+        if (cells[i] >= ncell_total) throw std::runtime_error("get_cells: cell id out of range");
+    std::vector<uint64_t> off(ncell_total + 1);
+    CUDA_CHECK(cudaMemcpyAsync(off.data(), list_off_.p, off.size() * 8, cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    std::vector<uint64_t> dst(ncells + 1, 0);
+    for (uint32_t i = 0; i < ncells; ++i) {
+        const uint64_t len = off[cells[i] + 1] - off[cells[i]];
+        if (counts) counts[i] = len;
+        dst[i + 1] = dst[i] + len;
+    }
+    const uint64_t total = dst[ncells];
+    if ((!ids && !codes && !lambdas) || total == 0 || ncells == 0) return;
+    DevBuf<uint32_t> d_cells, o_ids;
+    DevBuf<uint64_t> d_dst;
+    DevBuf<uint8_t> o_codes, o_lam;
+    d_cells.alloc(ncells);
+    d_dst.alloc(ncells + 1);
+    o_ids.alloc(total);
+    o_codes.alloc(total * m_);
+    o_lam.alloc(total);
+    CUDA_CHECK(cudaMemcpyAsync(d_cells.p, cells, ncells * 4ull, cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaMemcpyAsync(d_dst.p, dst.data(), (ncells + 1) * 8ull, cudaMemcpyHostToDevice, stream_));
+    k_gather_cells<<<ncells, 256, 0, stream_>>>(d_cells.p, d_dst.p, list_off_.p, ids_.p, codes_.p, lambdas_.p, m_,
+                                                 o_ids.p, o_codes.p, o_lam.p);
+    CUDA_CHECK(cudaGetLastError());
+    if (ids) CUDA_CHECK(cudaMemcpyAsync(ids, o_ids.p, total * 4, cudaMemcpyDeviceToHost, stream_));
+    if (codes) CUDA_CHECK(cudaMemcpyAsync(codes, o_codes.p, total * m_, cudaMemcpyDeviceToHost, stream_));
+    if (lambdas) CUDA_CHECK(cudaMemcpyAsync(lambdas, o_lam.p, total, cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
 void Engine::get_tables(std::vector<float>& t2, std::vector<float>& t3) {
     DeviceGuard g(cfg_.device);
     t2.resize((size_t)m_ * VLQ_KSUB);

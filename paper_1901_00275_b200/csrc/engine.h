@@ -210,6 +210,10 @@ public:
     void encode_host(const float* x, uint64_t nx, uint32_t* cells, float* lambdas, uint8_t* codes,
                      uint8_t* lam_bytes);
     void get_lists(HostLists& out, bool offsets_only = false);
+    // the posting lists of the given cells only, concatenated in request order
+    // (counts[i] = length of cells[i]); ids/codes/lambdas may be null (counts only)
+    void get_cells(const uint32_t* cells, uint32_t ncells, uint64_t* counts, uint32_t* ids, uint8_t* codes,
+                   uint8_t* lambdas);
     void get_tables(std::vector<float>& t2, std::vector<float>& t3);
 
     cudaStream_t stream() const { return stream_; }

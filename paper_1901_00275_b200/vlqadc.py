@@ -314,6 +314,21 @@ class Index:
         return off, ids, codes, lams
 
 
+    def cells(self, cells):
+        """The posting lists of the given cells, concatenated in request order:
+        (counts u64[len(cells)], ids u32, codes u8[., m], lambdas u8)."""
+        c = np.ascontiguousarray(cells, np.uint32).ravel()
+        counts = np.empty(c.shape[0], np.uint64)
+        _lib.check(_lib.lib().vlq_engine_get_cells(self._h, _p(c), c.shape[0], _p(counts), None, None, None))
+        tot = int(counts.sum())
+        ids = np.empty(tot, np.uint32)
+        codes = np.empty((tot, self.m), np.uint8)
+        lams = np.empty(tot, np.uint8)
+        if tot:
+            _lib.check(_lib.lib().vlq_engine_get_cells(self._h, _p(c), c.shape[0], _p(counts), _p(ids), _p(codes),
+                                                       _p(lams)))
+        return counts, ids, codes, lams
+
 # ---- module functions ---------------------------------------------------------
 _MAX_THREADS = 0
 

@@ -1,7 +1,7 @@
 #!/bin/bash
-# One GPU-box session: parity tests, bench lines, ncu launch list + full
-# capture of the scan kernel.  Everything lands in gpurun_out/.
-# usage: scripts/gpu_round.sh [workload] [what...]   what in {tests,bench,ref,ncu}
+# One GPU-box session: parity tests, smoke, bench lines, ncu launch list +
+# full capture of the scan kernel.  Everything lands in gpurun_out/.
+# usage: scripts/gpu_round.sh [workload] [what...]   what in {tests,smoke,bench,ref,ncu}
 W=${1:-c2}; shift
 WHAT=${@:-tests bench ref ncu}
 OUT=gpurun_out
@@ -11,13 +11,13 @@ nproc > $OUT/host_cores.txt; lscpu | grep "Model name" >> $OUT/host_cores.txt
 for w in $WHAT; do
   case $w in
     tests)
-      timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log ;;
+      timeout 1200 python -m pytest tests -q -m gpu -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log ;;
     smoke)
-      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1 ;;
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "rc=$?" >> $OUT/smoke.log ;;
     bench)
-      timeout 900 python bench.py --workload $W --steps 10 --warmup 3 > $OUT/bench_$W.json 2> $OUT/bench_$W.log ;;
+      timeout 1500 python bench.py --workload $W --steps 10 --warmup 3 ${EXTRA} > $OUT/bench_$W.json 2> $OUT/bench_$W.log ;;
     ref)
-      timeout 900 python bench.py --workload $W --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_$W.json 2> $OUT/bench_ref_$W.log ;;
+      timeout 1500 python bench.py --workload $W --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_$W.json 2> $OUT/bench_ref_$W.log ;;
     ncu)
       timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $OUT/launches_$W.csv python bench.py --workload $W --steps 2 --warmup 3 --profile > $OUT/ncu_list_$W.log 2>&1

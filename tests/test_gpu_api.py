@@ -203,3 +203,24 @@ def test_failed_add_leaves_lambda_range_unchanged(vlqadc, data):
     assert bad.lambda_range == (0.25, 0.75) and bad.ntotal == 0
     idx.add(base)
     assert idx.ntotal == len(base)
+
+
+def test_get_cells_equals_slices_of_the_full_lists(index):
+    """vlq_engine_get_cells (sampled add replay at 1e9 entries) returns exactly
+    the requested slices of vlq_engine_get_lists, in request order."""
+    off, ids, codes, lams = index.lists()
+    rng = np.random.default_rng(3)
+    req = rng.integers(0, index.k * index.n, size=40).astype(np.uint32)
+    req[5] = req[6]  # duplicates are allowed
+    counts, cids, ccodes, clams = index.cells(req)
+    pos = 0
+    for i, c in enumerate(req):
+        a, b = int(off[c]), int(off[c + 1])
+        assert counts[i] == b - a
+        assert np.array_equal(cids[pos:pos + b - a], ids[a:b])
+        assert np.array_equal(ccodes[pos:pos + b - a], codes[a:b])
+        assert np.array_equal(clams[pos:pos + b - a], lams[a:b])
+        pos += b - a
+    assert pos == len(cids)
+    with pytest.raises(RuntimeError, match="out of range"):
+        index.cells([index.k * index.n])
