@@ -94,6 +94,8 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // MODE 2 = TILEMIN: per row, the min of every 32-centroid column chunk
 //   (out_row[row * ldo + chunk]).  The L-th smallest chunk minimum bounds the
 //   row's L-th smallest value from above (L distinct elements lie below it).
+// MODE 4 = TILEMIN8: per row, the min of every 8-centroid column chunk
+//   (out_row[row * ldo + centroid / 8]); the chunk-select search path.
 // MODE 3 = FILTER: per row, append every (approx, centroid) with approx <=
 //   tau[row] to the row's candidate list (top_d/top_idx, capacity cap,
 //   count in cnt[row]).
@@ -319,6 +321,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tmem_ld32(tmem_base + ((quad * 32) << 16) + b * TN + col, acc);
                 float* tr = sMerge + (warp - 2) * 32 * 33;  // STORE: this warp's transpose tile
                 float cmin = __int_as_float(0x7f800000);
+                float c8[4] = {cmin, cmin, cmin, cmin};  // MODE 4: minima of 8-column chunks
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     const uint32_t cidx = t * TN + col + j;
@@ -339,6 +342,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         tr[lane * 33 + j] = d;
                     } else if constexpr (MODE == 2) {
                         cmin = fminf(cmin, d);
+                    } else if constexpr (MODE == 4) {
+                        c8[j >> 3] = fminf(c8[j >> 3], d);
                     } else {
                         if (d <= tau_r && grow < nx) {
                             const uint32_t slot = atomicAdd(&cnt[grow], 1u);
@@ -351,6 +356,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 if constexpr (MODE == 2) {
                     if (grow < nx) out_row[grow * ldo + t * (TN / 32) + col / 32] = cmin;
+                }
+                if constexpr (MODE == 4) {
+                    if (grow < nx)
+                        *reinterpret_cast<float4*>(out_row + grow * ldo + (t * TN + col) / 8) =
+                            make_float4(c8[0], c8[1], c8[2], c8[3]);
                 }
                 if constexpr (MODE == 1) {  // coalesced: one 128-byte row segment per instruction
                     __syncwarp();
@@ -548,6 +558,11 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
             break;
         case 1: VLQ_TC_MODE(1); break;
         case 2: VLQ_TC_MODE(2); break;
+        case 4:  // chunk-select path: 1xTF32 only
+            if (split) throw std::runtime_error("coarse_tc: TILEMIN8 is a 1xTF32 mode");
+            if (persist) VLQ_TC_LAUNCH(4, false, true);
+            else VLQ_TC_LAUNCH(4, false, false);
+            break;
         default: VLQ_TC_MODE(3); break;
     }
 #undef VLQ_TC_MODE
@@ -570,15 +585,6 @@ void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const
 namespace vlq {
 namespace dev {
 
-__device__ __forceinline__ float tc_eps(float xnorm2, float cmax, uint32_t dim, bool split = false) {
-    // 1xTF32: each operand keeps 10 mantissa bits (<= 2^-10 relative per factor);
-    // 3xTF32: the dropped lo.lo term and the truncated lo parts leave <= 3 * 2^-21
-    const float xn = sqrtf(xnorm2);
-    const float s = xn + cmax;
-    const float u = 5.9604645e-08f;
-    const float rel = split ? 1.430511474609375e-06f : 1.953125e-3f;
-    return 1.5f * (2.0f * (rel + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + 2.0f * u * s * s) + 1e-30f;
-}
 
 // Add path: exact argmin among the 4 tensor-core candidates (strict '<' from
 // FLT_MAX, lowest id on ties: index.cpp:96-103) when the candidate set is

@@ -96,6 +96,22 @@ __device__ __forceinline__ uint64_t make_key(float f, uint32_t idx) {
     return ((uint64_t)ord_float(f) << 32) | idx;
 }
 
+// |approx(x, c) + |x|^2 - sqdist(x, c)| <= tc_eps for every centroid c of the
+// tensor-core coarse stage (approx = |c|^2 - 2 <x, c> on TF32 operands, fp32
+// accumulation; sqdist the exact sequential reference sum): TF32 operands keep
+// 10 mantissa bits (<= 2^-10 relative per factor); 3xTF32 (split) leaves
+// <= 3 * 2^-21 from the dropped lo.lo term and truncated lo parts; the fp32
+// norm and the sequential sqdist each add D u |.|; x 1.5 safety factor.
+__device__ __forceinline__ float tc_eps(float xnorm2, float cmax, uint32_t dim, bool split = false) {
+    // 1xTF32: each operand keeps 10 mantissa bits (<= 2^-10 relative per factor);
+    // 3xTF32: the dropped lo.lo term and the truncated lo parts leave <= 3 * 2^-21
+    const float xn = sqrtf(xnorm2);
+    const float s = xn + cmax;
+    const float u = 5.9604645e-08f;
+    const float rel = split ? 1.430511474609375e-06f : 1.953125e-3f;
+    return 1.5f * (2.0f * (rel + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + 2.0f * u * s * s) + 1e-30f;
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }

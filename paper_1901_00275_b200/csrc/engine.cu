@@ -61,6 +61,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_STORE_ROWS")) cfg_.tc_store_rows = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_PERSIST")) cfg_.tc_persist = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_TC_CHUNK_SELECT")) cfg_.tc_chunk_select = std::atoi(v);
     if (cfg_.shard_count < 1 || cfg_.shard_rank < 0 || cfg_.shard_rank >= cfg_.shard_count)
         throw std::runtime_error("engine: invalid shard configuration");
     int ndev = 0;
@@ -723,6 +724,12 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
         lcnt_.alloc(tile);
         lidx_.alloc(tile * (uint64_t)kListCap);
         ld_.alloc(tile * (uint64_t)kListCap);
+        if (cfg_.tc_chunk_select) {
+            tmin8_.alloc(tile * (uint64_t)(((k_ + 127) / 128) * 16));
+            tch_.alloc(tile);
+            ccnt_.alloc(tile);
+            clist_.alloc(tile * (uint64_t)cfg_.tc_chunk_cap);
+        }
     }
     dbuf_.alloc(tile * (uint64_t)w1 * n_);
     sel_.alloc(tile * w2);
@@ -745,7 +752,7 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
                          float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st) {
     auto mark = [&](int ph) { mark_phase(ph, st); };
     uint64_t launches = 0;
-    bool tc = false, fast = false;
+    bool tc = false, fast = false, fused = false;
     mark(PH_COARSE);
     if (stage == STAGE_FINE) {
         // top-w1 from another rank's coarse stage: exact distances of the
@@ -760,7 +767,8 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     } else if (stage == STAGE_FINE_SEL) {
         mark(PH_FIRST);  // the selection (and its coarse values) comes from another rank
     } else {
-        tc = coarse_tile(d_q, nt, w1, launches, st);
+        tc = coarse_tile(d_q, nt, w1, w2, launches, st, &fused, stage == STAGE_SELECT ? io.sel_out : nullptr,
+                         stage == STAGE_SELECT ? io.ab_out : nullptr);
     }
     if (stage == STAGE_COARSE) {
         CUDA_CHECK(cudaMemcpyAsync(io.top_out, top_.p, nt * w1 * 4, cudaMemcpyDeviceToDevice, st));
@@ -768,13 +776,15 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     } else if (stage == STAGE_SELECT) {
         SearchArgs a = search_args();
         mark(PH_SECOND);
-        launch_second_level(a, nt, w1, w2, st);
-        launch_pack_selection(a, nt, w2, io.sel_out, io.ab_out, st);
-        launches += 2;
+        if (!fused) {
+            launch_second_level(a, nt, w1, w2, st);
+            launch_pack_selection(a, nt, w2, io.sel_out, io.ab_out, st);
+            launches += 2;
+        }
         for (int p = PH_TERM5; p <= PH_COUNT; p++) mark(p);
     } else {
         fast = fine_tile(d_q, nt, w1, w2, topk, d_ids, d_dists, d_scanned, launches, st,
-                         stage == STAGE_FINE_SEL ? &io : nullptr);
+                         stage == STAGE_FINE_SEL ? &io : nullptr, fused);
     }
     stats_.launches += launches;
     stats_.tiles += 1;
@@ -795,8 +805,43 @@ void Engine::search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
 // first_level_scan (search.cpp:11-36): exact top-w1 regions into top_ (and,
 // on the tensor-core path, exact ws_ entries for them and their neighbours).
 // Returns whether the tensor-core path ran.
-bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& launches, cudaStream_t st) {
+bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint64_t& launches, cudaStream_t st,
+                         bool* fused, uint32_t* sel_out, float* ab_out) {
     auto mark = [&](int ph) { mark_phase(ph, st); };
+    *fused = false;
+    // chunk-select path (select_fused.cu): one 1xTF32 pass of 8-centroid chunk
+    // minima, the chunks within the TF32 bound of the w1-th smallest, exact
+    // evaluation + first and second level fused per query
+    if (w2 > 0 && tc_ && cfg_.tc_chunk_select && k_ >= cfg_.tc_search_min_k && w1 < k_ && (k_ + 7) / 8 >= 2 * w1 &&
+        select_fused_supported(k_, n_, w1, w2, dim_) && tmin8_.p) {
+        const uint32_t nchunk8 = ((k_ + 127) / 128) * 16;
+        const float* x1 = nullptr;
+        if (cfg_.tc_persist) {
+            const uint64_t rows = ((nt + 127) / 128) * 128;
+            if (!xtc1_.p || xtc1_.n < rows * dim_) xtc1_.alloc(rows * dim_);
+            launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st);
+            x1 = xtc1_.p;
+            launches += 1;
+        }
+        launch_coarse_tc(4, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, tmin8_.p, nchunk8, nullptr, nullptr,
+                         st, nullptr, nullptr, 0, x1, nullptr);
+        launch_chunk_select(tmin8_.p, nt, nchunk8, w1, d_q, dim_, cmax_, cfg_.tc_chunk_cap, clist_.p, ccnt_.p,
+                            tch_.p, st);
+        mark(PH_FIRST);
+        SearchArgs a = search_args();
+        CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
+        launch_select_fused(a, nt, d_q, w1, w2, 8, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmax_, nullptr,
+                            nullptr, qlist_.p, err_.p + 6, sel_out, ab_out, st);
+        // certificate failures / chunk-list overflows: exact full rows, exact
+        // top-w1, then the fused kernel again from that top-w1
+        launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
+        launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
+        launch_select_fused(a, nt, d_q, w1, w2, 8, nullptr, nullptr, 0, nullptr, cmax_, qlist_.p, err_.p + 6, nullptr,
+                            nullptr, sel_out, ab_out, st);
+        launches += 6;
+        *fused = true;
+        return true;
+    }
     const uint32_t L = std::min<uint32_t>(k_, w1 + std::max<uint32_t>(32, w1 / 2));
     const bool tc = tc_ && k_ >= cfg_.tc_search_min_k && L <= 2048 && w1 < k_ &&
                     exact_needed_smem(k_, n_, w1, dim_) <= 200 * 1024;
@@ -885,12 +930,12 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& l
 // (search.cpp:38-167) from top_ / ws_.  Returns whether the fast scan ran.
 bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                        float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st,
-                       const StageIO* sel) {
+                       const StageIO* sel, bool second_done) {
     auto mark = [&](int ph) { mark_phase(ph, st); };
     SearchArgs a = search_args();
     mark(PH_SECOND);
     if (sel) launch_apply_selection(a, nt, w2, sel->sel_in, sel->ab_in, st);
-    else launch_second_level(a, nt, w1, w2, st);
+    else if (!second_done) launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
     launch_term5(d_q, pqT_.p, dim_, m_, t5_.p, meta_.p, nt, st);
     launches += 2;
@@ -982,6 +1027,8 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;
     else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
     else if (key == "tc_pass2_single") cfg_.tc_pass2_single = (int)value;
+    else if (key == "tc_chunk_select") cfg_.tc_chunk_select = (int)value;
+    else if (key == "tc_chunk_cap") cfg_.tc_chunk_cap = (uint32_t)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
     else if (key == "scan_cap") cfg_.scan_cap = (uint32_t)value;

@@ -53,6 +53,9 @@ struct EngineConfig {
     int tc_persist = 1;     // search coarse kernels as a persistent grid (one CTA per SM)
     int tc_pass1_single = 1;  // two-pass coarse filter: first pass in 1xTF32 (tau raised by its error bound)
     int tc_pass2_single = 0;  // ... and the filter pass in 1xTF32 too (tau raised by both bounds; more candidates)
+    int tc_chunk_select = 1;  // chunk-select coarse stage (one 1xTF32 pass of 8-centroid chunk minima, exact
+                              // evaluation of the selected chunks, fused first + second level; select_fused.cu)
+    uint32_t tc_chunk_cap = 256;  // selected chunks per query before the exact full-row fallback (study knob)
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -266,10 +269,14 @@ private:
     };
     void search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,
                        float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st);
-    bool coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint64_t& launches, cudaStream_t st);
+    // returns whether the tensor-core path ran; *fused: the chunk-select path
+    // also ran second_level_rank (sel_, ws_ a/b entries, meta_ written; and
+    // the select-split hand-off into sel_out / ab_out when given)
+    bool coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint64_t& launches, cudaStream_t st,
+                     bool* fused, uint32_t* sel_out = nullptr, float* ab_out = nullptr);
     bool fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                    float* d_dists, uint64_t* d_scanned, uint64_t& launches, cudaStream_t st,
-                   const StageIO* sel = nullptr);
+                   const StageIO* sel = nullptr, bool second_done = false);
     void search_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, uint32_t topk, int64_t* d_ids,
                      float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st);
 
@@ -304,6 +311,8 @@ private:
     DevBuf<float> xtc_, xlo_;  // query rows in the UMMA layout (persistent coarse kernels)
     DevBuf<float> xtc1_;       // unsplit copy for the 1xTF32 first pass
     DevBuf<uint32_t> lcnt_, lidx_;
+    DevBuf<float> tmin8_, tch_;          // chunk-select path: 8-centroid chunk minima, threshold T per query
+    DevBuf<uint32_t> clist_, ccnt_;      // selected chunks per query
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;
     bool clamp_ = true;

@@ -381,7 +381,8 @@ void Engine::ivf_search_device(const float* d_q, uint64_t nq, uint32_t w, uint32
         const uint64_t nt = std::min(tile, nq - t0);
         const float* q = d_q + t0 * dim_;
         uint64_t launches = 0;
-        coarse_tile(q, nt, w, launches, st);
+        bool fused = false;
+        coarse_tile(q, nt, w, /*w2=*/0, launches, st, &fused);  // first level only
 #define VLQ_IVF(MM)                                                                                               \
     do {                                                                                                          \
         auto fn = dev::k_ivf_scan<MM>;                                                                            \

@@ -38,20 +38,13 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* ws
     return excl;
 }
 
-// Selects the L smallest of vals[0..len) under the order (value, position)
-// -- the reference's (dist, id) comparator when position == id
-// (proj/src/search.cpp:28-33) -- and writes their positions to out[0..L) in
-// ASCENDING position order.  Radix select on the order-preserving u32 key in
-// three digit passes (11/11/10 bits), then one ordered collection pass that
-// keeps every key < T and the first r keys == T in position order.
-// Shared scratch: hist[2048] + scan[40].  All threads of the block call.
-__device__ __noinline__ static void block_select_ordered(const float* __restrict__ vals, uint32_t len, uint32_t L,
-                                     uint32_t* __restrict__ out, uint32_t* hist, uint32_t* scan) {
+// Order-preserving key (ord_float) of the L-th smallest of vals[0..len)
+// (1 <= L <= len): radix select in three digit passes (11/11/10 bits).
+// *rank_in_key receives how many keys equal to the result belong to the L
+// smallest.  Shared scratch: hist[2048] + scan[40].  All threads call.
+__device__ __noinline__ static uint32_t block_kth_ord(const float* __restrict__ vals, uint32_t len, uint32_t L,
+                                                      uint32_t* hist, uint32_t* scan, uint32_t* rank_in_key) {
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
-    if (L >= len) {
-        for (uint32_t i = tid; i < len; i += nt) out[i] = i;
-        return;
-    }
     uint32_t prefix = 0, pmask = 0, remaining = L;  // remaining: 1-based rank inside the prefix group
     const int shifts[3] = {21, 10, 0};
     const int widths[3] = {11, 11, 10};
@@ -87,6 +80,26 @@ __device__ __noinline__ static void block_select_ordered(const float* __restrict
         pmask |= dmask << sh;
         __syncthreads();
     }
+    *rank_in_key = remaining;
+    return prefix;
+}
+
+// Selects the L smallest of vals[0..len) under the order (value, position)
+// -- the reference's (dist, id) comparator when position == id
+// (proj/src/search.cpp:28-33) -- and writes their positions to out[0..L) in
+// ASCENDING position order: the L-th smallest key T (block_kth_ord), then one
+// ordered collection pass that keeps every key < T and the first r keys == T
+// in position order.  Shared scratch: hist[2048] + scan[40].  All threads of
+// the block call.
+__device__ __noinline__ static void block_select_ordered(const float* __restrict__ vals, uint32_t len, uint32_t L,
+                                     uint32_t* __restrict__ out, uint32_t* hist, uint32_t* scan) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    if (L >= len) {
+        for (uint32_t i = tid; i < len; i += nt) out[i] = i;
+        return;
+    }
+    uint32_t remaining;
+    const uint32_t prefix = block_kth_ord(vals, len, L, hist, scan, &remaining);
     const uint32_t T = prefix;  // exact key of the L-th smallest value
     const uint32_t r = remaining;  // how many keys == T to take (in position order)
     uint32_t lt_run = 0, eq_run = 0;

@@ -1,0 +1,402 @@
+// Chunk-select coarse stage: first_level_scan + second_level_rank
+// (proj/src/search.cpp:11-78) from ONE 1xTF32 tensor-core pass.
+//
+//   k_coarse_tc<4> (TILEMIN8)  approx(y, c) = |c|^2 - 2 <y, c> on TF32 operands;
+//                              per query the minimum of every 8-centroid chunk
+//                              (tmin [nq, K/8]); no K-wide row in HBM
+//   k_chunk_select             tau = the w1-th smallest chunk minimum,
+//                              T = tau + 2.02 eps (eps = tc_eps, the TF32 bound);
+//                              compacts the chunks with minimum <= T
+//   k_select_fused             exact reference-order sqdist of every centroid in
+//                              those chunks -> exact top-w1 by (dist, id) with a
+//                              certificate; exact distances of the w1 regions'
+//                              neighbours (bitmap-deduplicated, kept in shared
+//                              memory); second_level_rank over the w1 n edges ->
+//                              the selected cells, their (a, b) pairs, the
+//                              scanned count and the |term1| bound
+//
+// Why the chunk set is complete (the certificate, checked per query): the w1
+// chunks whose minimum is <= tau each hold a centroid with approx <= tau, i.e.
+// exact <= tau + |y|^2 + eps, so the exact w1-th smallest over the evaluated
+// centroids is <= tau + |y|^2 + eps.  Every centroid outside the selected
+// chunks has approx > T, i.e. exact > T + |y|^2 - eps = tau + |y|^2 + 1.02 eps.
+// The kernel checks T + |y|^2 - eps > exact_w1 explicitly (in double); a query
+// that fails it (or whose chunk list overflows) is listed and takes the exact
+// full-row path (k_exact_rows + k_first_level_list), then this kernel again
+// in "top" mode from its exact top-w1.
+//
+// Versus the two-pass filter (1xTF32 chunk minima + 3xTF32 filter pass +
+// exact refine + k_exact_needed writing ~2k exact distances into a K-wide ws
+// row per query): one tensor-core pass instead of two (the 3xTF32 pass issued
+// 3x the MMAs), and the needed exact distances live in shared memory only.
+#include "kernels.h"
+#include "select.cuh"
+
+namespace vlq {
+namespace dev {
+
+constexpr uint32_t FS_THREADS = 256;
+constexpr uint32_t FS_ROWS = 16;       // centroid rows staged per warp
+constexpr uint32_t FS_MAX_KEYS = 2048; // exactly evaluated chunk centroids per query
+
+// tau / T per query and the compacted list of selected chunks.
+__global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
+                                                      const float* __restrict__ Y, uint32_t dim, float cmax,
+                                                      uint32_t capc, uint32_t* __restrict__ clist,
+                                                      uint32_t* __restrict__ ccnt, float* __restrict__ Tout) {
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    __shared__ float s_T;
+    __shared__ unsigned int s_cnt;
+    const uint64_t q = blockIdx.x;
+    const float* row = tmin + q * nchunk;
+    uint32_t r;
+    const uint32_t key = block_kth_ord(row, nchunk, min(L, nchunk), hist, scan, &r);
+    if (threadIdx.x == 0) {
+        float yn = 0.0f;
+        for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
+        s_T = unord_float(key) + 2.02f * tc_eps(yn, cmax, dim, false);
+        s_cnt = 0;
+    }
+    __syncthreads();
+    const float T = s_T;
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t base = 0; base < nchunk; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const bool take = i < nchunk && row[i] <= T;
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        uint32_t slot0 = 0;
+        if (lane == 0 && bal) slot0 = atomicAdd(&s_cnt, (unsigned)__popc(bal));
+        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+        if (take) {
+            const uint32_t slot = slot0 + __popc(bal & ((1u << lane) - 1u));
+            if (slot < capc) clist[q * capc + slot] = i;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ccnt[q] = s_cnt;
+        Tout[q] = T;
+    }
+}
+
+// Exact reference-order sqdist of rows ids[0..cnt) (centroid ids; id >= k
+// gives +inf) into out[0..cnt).  Rows are staged FS_ROWS per warp through
+// shared memory with coalesced 16-byte loads; lanes 0..FS_ROWS-1 then run the
+// sequential sqdist of one row each (vecset.cpp:22-29 order).
+template <typename Out>
+__device__ __forceinline__ void exact_rows_staged(const float* __restrict__ C, uint32_t k, uint32_t dim,
+                                                  const float* ys, float* tiles, uint32_t cnt, Out&& id_of,
+                                                  float* __restrict__ out) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+    const uint32_t n4 = dim >> 2, stride = dim + 4;
+    float* tile = tiles + (size_t)warp * FS_ROWS * stride;
+    for (uint32_t b0 = warp * FS_ROWS; b0 < cnt; b0 += nwarps * FS_ROWS) {
+        const uint32_t nb = min(FS_ROWS, cnt - b0);
+        for (uint32_t r = 0; r < nb; r++) {
+            const uint32_t c = id_of(b0 + r);
+            if (c < k) {
+                const float4* cp = reinterpret_cast<const float4*>(C + (uint64_t)c * dim);
+                for (uint32_t c4 = lane; c4 < n4; c4 += 32)
+                    *reinterpret_cast<float4*>(tile + r * stride + c4 * 4) = __ldg(cp + c4);
+            }
+        }
+        __syncwarp();
+        if (lane < nb) {
+            const uint32_t c = id_of(b0 + lane);
+            float acc = __int_as_float(0x7f800000);
+            if (c < k) {
+                const float* row = tile + lane * stride;
+                acc = 0.0f;
+                for (uint32_t c4 = 0; c4 < n4; c4++) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+                    const float4 yv = *reinterpret_cast<const float4*>(ys + c4 * 4);
+                    acc = sq_step(acc, yv.x, v.x);
+                    acc = sq_step(acc, yv.y, v.y);
+                    acc = sq_step(acc, yv.z, v.z);
+                    acc = sq_step(acc, yv.w, v.w);
+                }
+            }
+            out[b0 + lane] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+struct FusedArgs {
+    const float* Y;
+    uint32_t w1, w2, cs;      // regions, cells, centroids per chunk
+    const uint32_t* clist;    // [nq, capc] selected chunks (chunk mode)
+    const uint32_t* ccnt;     // [nq]
+    uint32_t capc;
+    const float* T;           // [nq] chunk threshold (approx units, without |y|^2)
+    float cmax;
+    const uint32_t* qlist;    // top mode: block b handles query qlist[b] (b < *qcount) from a.top
+    const unsigned int* qcount;
+    uint32_t* flagged;        // chunk mode: queries whose certificate failed / list overflowed
+    unsigned int* nflag;
+    uint32_t* sel_out;        // optional select-split hand-off: cells [nq, w2]
+    float* ab_out;            //                                 (a, b) [nq, w2, 2]
+};
+
+__host__ __device__ inline uint32_t fs_nwords(uint32_t k) { return (k + 31) / 32; }
+
+// dynamic shared memory layout (bytes), shared by host and device
+struct FusedLayout {
+    uint32_t ys, topS, u, tiles, total;
+    __host__ __device__ FusedLayout(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim) {
+        const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1);
+        const uint32_t dimp = (dim + 3) & ~3u;
+        ys = 0;
+        topS = ys + dimp * 4;
+        u = (topS + w1 * 4 + 15) & ~15u;
+        // phase 1: keys (u64) ; phase 2: bitmap, word prefix, needed ids, values, edge distances, positions
+        const uint32_t p1 = FS_MAX_KEYS * 8;
+        const uint32_t p2 = (2 * nw + 2 * nn + w1 * n + w2) * 4;
+        tiles = (u + (p1 > p2 ? p1 : p2) + 15) & ~15u;
+        total = tiles + (FS_THREADS / 32) * FS_ROWS * (dim + 4) * 4;
+    }
+};
+
+__global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, FusedArgs f) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t scan[40];
+    __shared__ float s_yn;
+    __shared__ int s_fail;
+    __shared__ unsigned long long s_scanned;
+    __shared__ float s_dmax;
+    const bool top_mode = f.qlist != nullptr;
+    if (top_mode && blockIdx.x >= *f.qcount) return;
+    const uint64_t q = top_mode ? f.qlist[blockIdx.x] : blockIdx.x;
+    const uint32_t k = a.k, n = a.n, dim = a.dim, w1 = f.w1, w2 = f.w2;
+    const FusedLayout lay(k, n, w1, w2, dim);
+    float* ys = reinterpret_cast<float*>(smem + lay.ys);
+    uint32_t* topS = reinterpret_cast<uint32_t*>(smem + lay.topS);
+    float* tiles = reinterpret_cast<float*>(smem + lay.tiles);
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    for (uint32_t d = tid; d < ((dim + 3) & ~3u); d += nt) ys[d] = d < dim ? f.Y[q * dim + d] : 0.0f;
+    if (tid == 0) {
+        s_fail = 0;
+        s_scanned = 0;
+        s_dmax = 0.0f;
+    }
+    __syncthreads();
+
+    if (!top_mode) {
+        // ---- phase 1: exact distances of the selected chunks' centroids
+        uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.u);
+        const uint32_t nc = f.ccnt[q];
+        const uint32_t ncent = nc * f.cs;
+        if (nc > f.capc || ncent > FS_MAX_KEYS || nc < w1) {
+            if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
+            return;
+        }
+        uint32_t np2 = 1;
+        while (np2 < ncent) np2 <<= 1;
+        const uint32_t* cl = f.clist + q * f.capc;
+        const uint32_t cs = f.cs;
+        // rows staged FS_ROWS per warp (coalesced 16-byte loads), lanes
+        // 0..FS_ROWS-1 run the sequential sqdist of one row each
+        {
+            const uint32_t warp = tid >> 5, lane = tid & 31u, nwarps = nt >> 5;
+            const uint32_t n4 = dim >> 2, stride = dim + 4;
+            float* tile = tiles + (size_t)warp * FS_ROWS * stride;
+            for (uint32_t b0 = warp * FS_ROWS; b0 < ncent; b0 += nwarps * FS_ROWS) {
+                const uint32_t nb = min(FS_ROWS, ncent - b0);
+                for (uint32_t r = 0; r < nb; r++) {
+                    const uint32_t t = b0 + r;
+                    const uint32_t c = cl[t / cs] * cs + t % cs;
+                    if (c < k) {
+                        const float4* cp = reinterpret_cast<const float4*>(a.centroids + (uint64_t)c * dim);
+                        for (uint32_t c4 = lane; c4 < n4; c4 += 32)
+                            *reinterpret_cast<float4*>(tile + r * stride + c4 * 4) = __ldg(cp + c4);
+                    }
+                }
+                __syncwarp();
+                if (lane < nb) {
+                    const uint32_t t = b0 + lane;
+                    const uint32_t c = cl[t / cs] * cs + t % cs;
+                    uint64_t key = ~0ull;
+                    if (c < k) {
+                        const float* row = tile + lane * stride;
+                        float acc = 0.0f;
+                        for (uint32_t c4 = 0; c4 < n4; c4++) {
+                            const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+                            const float4 yv = *reinterpret_cast<const float4*>(ys + c4 * 4);
+                            acc = sq_step(acc, yv.x, v.x);
+                            acc = sq_step(acc, yv.y, v.y);
+                            acc = sq_step(acc, yv.z, v.z);
+                            acc = sq_step(acc, yv.w, v.w);
+                        }
+                        key = make_key(acc, c);
+                    }
+                    keys[t] = key;
+                }
+                __syncwarp();
+            }
+        }
+        for (uint32_t t = ncent + tid; t < np2; t += nt) keys[t] = ~0ull;
+        if (tid == 0) {
+            float yn = 0.0f;
+            for (uint32_t d = 0; d < dim; d++) yn = fmaf(ys[d], ys[d], yn);
+            s_yn = yn;
+        }
+        __syncthreads();
+        bitonic_sort_u64<false>(keys, np2, tid, nt);
+        if (tid == 0) {
+            const uint64_t kw = keys[w1 - 1];
+            const float exact_w1 = unord_float((uint32_t)(kw >> 32));
+            const float eps = tc_eps(s_yn, f.cmax, dim, false);
+            const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
+            if (kw == ~0ull || !(lower > (double)exact_w1)) {
+                s_fail = 1;
+                f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
+            }
+        }
+        __syncthreads();
+        if (s_fail) return;
+        // the w1 winners by ascending id (second_level_rank's edge order)
+        for (uint32_t t = tid; t < w1; t += nt) topS[t] = (uint32_t)keys[t];
+        __syncthreads();
+        uint32_t np2w = 1;
+        while (np2w < w1) np2w <<= 1;
+        for (uint32_t t = tid; t < np2w; t += nt) keys[t] = t < w1 ? (uint64_t)topS[t] : ~0ull;
+        __syncthreads();
+        bitonic_sort_u64<false>(keys, np2w, tid, nt);
+        for (uint32_t t = tid; t < w1; t += nt) {
+            topS[t] = (uint32_t)keys[t];
+            a.top[q * w1 + t] = (uint32_t)keys[t];
+        }
+        __syncthreads();
+    } else {
+        for (uint32_t t = tid; t < w1; t += nt) topS[t] = a.top[q * w1 + t];
+        __syncthreads();
+    }
+
+    // ---- phase 2: exact distances of the regions and their neighbours
+    const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1), total = w1 * n;
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + lay.u);
+    uint32_t* wpref = bitmap + nw;
+    uint32_t* nid = wpref + nw;
+    float* nval = reinterpret_cast<float*>(nid + nn);
+    float* dq = nval + nn;
+    uint32_t* selpos = reinterpret_cast<uint32_t*>(dq + total);
+    for (uint32_t i = tid; i < nw; i += nt) bitmap[i] = 0;
+    __syncthreads();
+    for (uint32_t e = tid; e < nn; e += nt) {
+        const uint32_t r = e / (n + 1), j = e % (n + 1);
+        const uint32_t c = j == 0 ? topS[r] : a.nbr[(uint64_t)topS[r] * n + (j - 1)];
+        atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+    }
+    __syncthreads();
+    uint32_t nneed;
+    {
+        const uint32_t per = (nw + nt - 1) / nt;
+        uint32_t local = 0;
+        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) local += __popc(bitmap[i]);
+        uint32_t run = block_excl_scan_u32(local, scan, &nneed);
+        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) {
+            wpref[i] = run;
+            uint32_t w = bitmap[i];
+            while (w) {
+                const uint32_t b = __ffs(w) - 1;
+                nid[run++] = i * 32 + b;
+                w &= w - 1;
+            }
+        }
+    }
+    __syncthreads();
+    exact_rows_staged(a.centroids, k, dim, ys, tiles, nneed, [&](uint32_t t) { return nid[t]; }, nval);
+    __syncthreads();
+    auto val_of = [&](uint32_t c) -> float {
+        const uint32_t w = c >> 5;
+        return nval[wpref[w] + __popc(bitmap[w] & ((1u << (c & 31)) - 1u))];
+    };
+    // second_level_rank (search.cpp:38-78): line-subregion distances of the
+    // w1 n edges, top-w2 by (dist, centroid id, edge rank) = edge position
+    for (uint32_t e = tid; e < total; e += nt) {
+        const uint32_t i = topS[e / n], j = e % n;
+        const float av = val_of(i);
+        const uint32_t s = a.nbr[(uint64_t)i * n + j];
+        const float bv = val_of(s);
+        const float cv = a.elen[(uint64_t)i * n + j];
+        if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
+        const float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
+        dq[e] = line_sqdist(av, bv, cv, lam);
+    }
+    __syncthreads();
+    block_select_ordered(dq, total, w2, selpos, hist, scan);
+    __syncthreads();
+    // selected cells (ascending id), their (a, b) into the ws row (read by the
+    // scan and the exact re-score), the scanned count and the |term1| bound
+    // (k_second_level / k_apply_selection formulas)
+    float* wsq = a.ws + q * a.k;
+    const float lmax = a.lam_absmax;
+    unsigned long long cnt = 0;
+    float dmax = 0.0f;
+    for (uint32_t t = tid; t < w2; t += nt) {
+        const uint32_t e = selpos[t];
+        const uint32_t i = topS[e / n], j = e % n;
+        const uint32_t cell = i * n + j;
+        const uint32_t s = a.nbr[cell];
+        const float av = val_of(i), bv = val_of(s), cv = a.elen[cell];
+        a.sel[q * w2 + t] = cell;
+        wsq[i] = av;
+        wsq[s] = bv;
+        if (f.sel_out) {
+            f.sel_out[q * w2 + t] = cell;
+            f.ab_out[(q * w2 + t) * 2] = av;
+            f.ab_out[(q * w2 + t) * 2 + 1] = bv;
+        }
+        cnt += a.list_off[cell + 1] - a.list_off[cell];
+        const float bound = (1.0f + lmax) * fabsf(av) + (lmax * lmax + lmax) * fabsf(cv) + lmax * fabsf(bv);
+        dmax = fmaxf(dmax, bound);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(&s_scanned, cnt);
+        atomicMax(reinterpret_cast<unsigned int*>(&s_dmax), __float_as_uint(dmax));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.meta[q].scanned = s_scanned;
+        a.meta[q].dmax = s_dmax;
+        a.meta[q].flag = 0;
+    }
+}
+
+}  // namespace dev
+
+size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim) {
+    return dev::FusedLayout(k, n, w1, w2, dim).total;
+}
+
+bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim) {
+    return dim % 4 == 0 && dim <= 128 && w1 <= 256 && w2 <= w1 * n && (uint64_t)w1 * (n + 1) <= 8192 &&
+           select_fused_smem(k, n, w1, w2, dim) <= 200 * 1024;
+}
+
+void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
+                         float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st) {
+    if (nq == 0) return;
+    dev::k_chunk_select<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2, uint32_t cs,
+                         const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
+                         const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
+                         uint32_t* sel_out, float* ab_out, cudaStream_t st) {
+    if (nblocks == 0) return;
+    dev::FusedArgs f{Y, w1, w2, cs, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, sel_out, ab_out};
+    const size_t smem = select_fused_smem(a.k, a.n, w1, w2, a.dim);
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_select_fused<<<(unsigned)nblocks, dev::FS_THREADS, smem, st>>>(a, f);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace vlq

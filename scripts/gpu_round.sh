@@ -23,6 +23,14 @@ for w in $WHAT; do
         --log-file $OUT/launches_$W.csv python bench.py --workload $W --steps 2 --warmup 3 --profile > $OUT/ncu_list_$W.log 2>&1
       timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_scan -c 1 \
         -f -o $OUT/scan_$W python bench.py --workload $W --steps 1 --warmup 3 --profile > $OUT/ncu_full_$W.log 2>&1 ;;
+    ncu_tc)
+      # tensor-pipe utilisation of the tcgen05 coarse GEMM passes (not part of --set full on B200)
+      timeout 900 ncu --profile-from-start off --clock-control none -k regex:k_coarse_tc -c 4 \
+        --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_hmma.sum,sm__inst_executed_pipe_tmem.sum,sm__warps_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_pipe_tc_wavefronts_mem_shared.sum \
+        --csv --log-file $OUT/coarse_tc_$W.csv python bench.py --workload $W --steps 1 --warmup 3 --profile > $OUT/ncu_tc_$W.log 2>&1 ;;
+    ncu_coarse)
+      timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_coarse_tc|k_exact_needed|k_refine" -c 6 \
+        -f -o $OUT/coarse_$W python bench.py --workload $W --steps 1 --warmup 3 --profile > $OUT/ncu_coarse_$W.log 2>&1 ;;
   esac
 done
 ls -la $OUT

@@ -172,3 +172,54 @@ def test_tc_add_lists_and_search_at_baseline_shapes(vlqadc, oracle_mod, tmp_path
         ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
         oids, od, _ = o.search(q, w1, alpha, k)
         assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, w1, alpha, k)
+
+
+@pytest.mark.parametrize("dim", [96, 128])
+def test_chunk_select_coarse_stage_paths_match_oracle(vlqadc, oracle_mod, tmp_path, dim):
+    """The chunk-select coarse stage (select_fused.cu: one 1xTF32 pass of
+    8-centroid chunk minima, exact evaluation of the chunks within the TF32
+    bound, fused first + second level) at K = 16384, n = 32: bit-exact with the
+    oracle through its normal path, through the exact full-row fallback
+    (chunk list capped below w1, so every query overflows), and equal to the
+    two-pass filter path it replaces; the select-split hand-off (cells + exact
+    (a, b)) of the fused kernel feeds a second engine's fine stage."""
+    base = vlqadc.gen_synthetic(40000, dim, clusters=3000, spread=0.05, seed=45)
+    q = vlqadc.gen_synthetic(96, dim, clusters=3000, spread=0.05, seed=46)
+    idx = vlqadc.Index.train(base, k=16384, n=32, m=8, iters=2, seed=7)
+    idx.add(base)
+    path = str(tmp_path / f"cs{dim}.vlq")
+    idx.save(path)
+    o = oracle_mod.OracleIndex.load(path)
+    grid = [(64, 0.25, 100), (16, 0.5, 10), (200, 0.1, 20), (1, 1.0, 5)]
+    ref = {g: o.search(q, g[0], g[1], g[2])[:2] for g in grid}
+    for knobs in [dict(tc_chunk_select=1, tc_chunk_cap=256), dict(tc_chunk_select=1, tc_chunk_cap=4),
+                  dict(tc_chunk_select=0)]:
+        for key, val in knobs.items():
+            idx.set_tuning(key, val)
+        for g in grid:
+            ids_, d_ = idx.search(q, w1=g[0], alpha=g[1], k=g[2])
+            oids, od = ref[g]
+            assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, knobs, g)
+        st = idx.stats(reset=True)
+        if knobs.get("tc_chunk_cap") == 4:
+            assert st["tc_fallbacks"] > 0  # the fallback path really ran
+    idx.set_tuning("tc_chunk_select", 1)
+    idx.set_tuning("tc_chunk_cap", 256)
+    # select-split: this engine selects, a second engine on the same model scans
+    import torch
+    dq = torch.from_numpy(q).cuda()
+    w1, alpha, k = 64, 0.25, 100
+    w2 = idx.w2(w1, alpha)
+    sel = torch.empty((len(q), w2), dtype=torch.int32, device="cuda")
+    ab = torch.empty((len(q), w2, 2), dtype=torch.float32, device="cuda")
+    idx.search_select_device(dq.data_ptr(), len(q), w1, alpha, sel.data_ptr(), ab.data_ptr(), stream=0)
+    other = vlqadc.Index.load(path)
+    other.set_tuning("tc_chunk_select", 0)
+    ids = torch.empty((len(q), k), dtype=torch.int64, device="cuda")
+    dd = torch.empty((len(q), k), dtype=torch.float32, device="cuda")
+    sc = torch.empty((len(q),), dtype=torch.int64, device="cuda")
+    other.search_fine_sel_device(dq.data_ptr(), len(q), w1, alpha, k, sel.data_ptr(), ab.data_ptr(), ids.data_ptr(),
+                                 dd.data_ptr(), sc.data_ptr(), stream=0)
+    torch.cuda.synchronize()
+    oids, od = ref[(w1, alpha, k)]
+    assert np.array_equal(ids.cpu().numpy(), oids) and same_f32(dd.cpu().numpy(), od)
