@@ -213,12 +213,14 @@ def time_reference(ref_idx, refmod, queries: np.ndarray, w1, alpha, k, budget_s:
     """Reference Index.search on a bounded sample with all host threads
     (set_max_threads(0) = hardware_concurrency, parallel.cpp:17-24)."""
     refmod.set_max_threads(0)
+    cores = os.cpu_count() or 1
     ref_idx.search(queries[:warm], w1=w1, alpha=alpha, k=k)  # warm-up excluded (eval.cpp:91)
     probe = queries[warm:warm + 200]
     t = time.perf_counter()
     ref_idx.search(probe, w1=w1, alpha=alpha, k=k)
-    rate = len(probe) / max(time.perf_counter() - t, 1e-6)
-    ns = int(min(len(queries) - warm, max(200, rate * budget_s)))
+    rate1 = len(probe) / max(time.perf_counter() - t, 1e-6)  # serial: parallel_for runs < 1024 queries on one thread
+    # >= 256 queries per host thread so parallel_for (parallel.cpp:27-40) occupies every core
+    ns = int(min(len(queries) - warm, max(256 * cores, rate1 * cores * budget_s)))
     sample = queries[warm:warm + ns]
     t = time.perf_counter()
     ids, dists = ref_idx.search(sample, w1=w1, alpha=alpha, k=k)
@@ -759,11 +761,15 @@ def run_reference_arm(args, rank, world):
         parity["mismatched_queries"] += int(bad.sum())
 
     refmod.set_max_threads(0)
+    cores = os.cpu_count() or 1
     search(0, 100)  # warm-up excluded (eval.cpp:91)
     t = time.perf_counter()
     search(100, 300)
-    rate = 200 / max(time.perf_counter() - t, 1e-6)
-    per_step = int(max(50, min(args.nq - 300, rate * 6.0)))
+    rate1 = 200 / max(time.perf_counter() - t, 1e-6)  # < 1024 queries: parallel_for runs them serially
+    # parallel_for (parallel.cpp:27-40) runs batches under 1024 queries on ONE
+    # thread and cuts larger ones into chunks of >= 256 queries: a step needs
+    # >= 256 x threads queries to occupy every host core
+    per_step = int(min(args.nq - 300, max(256 * cores, rate1 * cores * 3.0)))
     times = []
     for s in range(args.warmup + args.steps):
         lo = 300 + (s * per_step) % max(1, args.nq - 300 - per_step)
@@ -774,12 +780,11 @@ def run_reference_arm(args, rank, world):
     value = per_step * len(times) / sum(times)
     # one host thread (set_max_threads(1)): a bounded sample of ~10 s
     refmod.set_max_threads(1)
-    n1 = max(5, min(200, int(10.0 * rate / max(1, os.cpu_count() or 1))))
+    n1 = int(max(5, min(2000, 10.0 * rate1)))
     t = time.perf_counter()
     search(0, n1)
     one_thread = n1 / (time.perf_counter() - t)
     refmod.set_max_threads(0)
-    cores = os.cpu_count()
     sample = (f"{per_step} of the {args.nq} benchmark queries per step (slices after 300 warm-up/probe queries), "
               f"reference Index.search (oracle/_ref, unmodified sources), set_max_threads(0) = {cores} threads")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world,

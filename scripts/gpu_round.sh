@@ -25,8 +25,8 @@ for w in $WHAT; do
         -f -o $OUT/scan_$W python bench.py --workload $W --steps 1 --warmup 3 --profile > $OUT/ncu_full_$W.log 2>&1 ;;
     ncu_tc)
       # tensor-pipe utilisation of the tcgen05 coarse GEMM passes (not part of --set full on B200)
-      timeout 900 ncu --profile-from-start off --clock-control none -k regex:k_coarse_tc -c 4 \
-        --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_hmma.sum,sm__inst_executed_pipe_tmem.sum,sm__warps_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_pipe_tc_wavefronts_mem_shared.sum \
+      timeout 900 ncu --profile-from-start off --clock-control none -k regex:k_coarse_tc -c 2 \
+        --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32.sum,sm__inst_executed_pipe_tensor_subpipe_hmma.sum,sm__inst_executed_pipe_tmem.sum,sm__warps_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_pipe_tc_wavefronts_mem_shared.sum \
         --csv --log-file $OUT/coarse_tc_$W.csv python bench.py --workload $W --steps 1 --warmup 3 --profile > $OUT/ncu_tc_$W.log 2>&1 ;;
     ncu_coarse)
       timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_coarse_tc|k_exact_needed|k_refine" -c 6 \
