@@ -63,6 +63,9 @@ WORKLOADS = {
     "deep100m": dict(desc="DEEP100M-shaped synthetic (HBM-resident scan study): 100M x 96, K=4096 x 32 lines, PQ 16 B, "
                           "nq=10k, k=100", n=100_000_000, dim=96, k=4096, edges=32, m=16, clusters=4000,
                      ntrain=200_000),
+    "c4s": dict(desc="C4 coarse-stage study: 50M x 96, K=65536 x 32 lines, PQ 16 B, nq=10k, k=100 (C4's model "
+                     "shape on a 1/20 base)", n=50_000_000, dim=96, k=65536, edges=32, m=16, clusters=65536,
+                ntrain=2_000_000, gt_queries=1000),
     "c3": dict(desc="SIFT100M-shaped synthetic (configs[2]): 100M x 128, K=65536 x 32 lines, PQ 8 B, nq=10k, k=100",
                n=100_000_000, dim=128, k=65536, edges=32, m=8, clusters=65536, ntrain=2_000_000, gt_queries=1000),
     "c4": dict(desc="DEEP1B-shaped synthetic (configs[3]): 1B x 96, K=65536 x 32 lines, PQ 16 B, nq=10k, k=100",

@@ -133,8 +133,8 @@ namespace vlq {
 // tensor-core coarse stage (coarse_tc.cu)
 bool coarse_tc_supported(uint32_t dim);
 // chunk-select coarse stage (select_fused.cu)
-size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim);
-bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim);
+size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc);
+bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc);
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
                          float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st);
 void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2, uint32_t cs,

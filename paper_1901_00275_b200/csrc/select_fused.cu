@@ -29,6 +29,7 @@
 // exact refine + k_exact_needed writing ~2k exact distances into a K-wide ws
 // row per query): one tensor-core pass instead of two (the 3xTF32 pass issued
 // 3x the MMAs), and the needed exact distances live in shared memory only.
+#include "async.cuh"
 #include "kernels.h"
 #include "select.cuh"
 
@@ -36,7 +37,9 @@ namespace vlq {
 namespace dev {
 
 constexpr uint32_t FS_THREADS = 256;
-constexpr uint32_t FS_ROWS = 16;       // centroid rows staged per warp
+constexpr uint32_t FS_PW = 16;         // dimensions per staged row piece
+constexpr uint32_t FS_NBUF = 2;        // row-piece buffers per warp (cp.async pipeline depth)
+constexpr uint32_t FS_BUF_FLOATS = 32 * (FS_PW + 4);  // one piece of 32 rows (stride PW + 4: conflict-free LDS.128)
 constexpr uint32_t FS_MAX_KEYS = 2048; // exactly evaluated chunk centroids per query
 
 // tau / T per query and the compacted list of selected chunks.
@@ -80,47 +83,80 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
     }
 }
 
-// Exact reference-order sqdist of rows ids[0..cnt) (centroid ids; id >= k
-// gives +inf) into out[0..cnt).  Rows are staged FS_ROWS per warp through
-// shared memory with coalesced 16-byte loads; lanes 0..FS_ROWS-1 then run the
-// sequential sqdist of one row each (vecset.cpp:22-29 order).
-template <typename Out>
-__device__ __forceinline__ void exact_rows_staged(const float* __restrict__ C, uint32_t k, uint32_t dim,
-                                                  const float* ys, float* tiles, uint32_t cnt, Out&& id_of,
-                                                  float* __restrict__ out) {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Exact reference-order sqdist (vecset.cpp:22-29: acc += (y - c)^2 in order)
+// of the rows id_of(0 .. cnt) (centroid ids; id >= k gives +inf), out(t, d).
+// Each warp takes batches of 32 rows, lane l owning row l of the batch; the
+// rows stream through shared memory in FS_PW-dimension pieces (coalesced
+// 16-byte cp.async, zero-filled for invalid rows) with FS_NBUF pieces in
+// flight per warp, so the L2 latency of the gathered centroid rows overlaps
+// the sequential sums.  Warp-synchronous; `wbuf` is this warp's
+// FS_NBUF * FS_BUF_FLOATS floats.
+template <typename IdFn, typename OutFn>
+__device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uint32_t k, uint32_t dim,
+                                                const float* ys, float* wbuf, uint32_t cnt, IdFn&& id_of,
+                                                OutFn&& out) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
-    const uint32_t n4 = dim >> 2, stride = dim + 4;
-    float* tile = tiles + (size_t)warp * FS_ROWS * stride;
-    for (uint32_t b0 = warp * FS_ROWS; b0 < cnt; b0 += nwarps * FS_ROWS) {
-        const uint32_t nb = min(FS_ROWS, cnt - b0);
-        for (uint32_t r = 0; r < nb; r++) {
-            const uint32_t c = id_of(b0 + r);
-            if (c < k) {
-                const float4* cp = reinterpret_cast<const float4*>(C + (uint64_t)c * dim);
-                for (uint32_t c4 = lane; c4 < n4; c4 += 32)
-                    *reinterpret_cast<float4*>(tile + r * stride + c4 * 4) = __ldg(cp + c4);
-            }
+    const uint32_t npiece = (dim + FS_PW - 1) / FS_PW;
+    const uint32_t nbatch = cnt > warp * 32 ? (cnt - warp * 32 + nwarps * 32 - 1) / (nwarps * 32) : 0;
+    const uint32_t nu = nbatch * npiece;
+    auto issue = [&](uint32_t u) {
+        const uint32_t bi = u / npiece, p = u - bi * npiece;
+        const uint32_t r0 = (warp + bi * nwarps) * 32;
+        const uint32_t my_id = r0 + lane < cnt ? id_of(r0 + lane) : 0xffffffffu;
+        float* buf = wbuf + (u % FS_NBUF) * FS_BUF_FLOATS;
+#pragma unroll
+        for (uint32_t i = 0; i < FS_PW / 4; i++) {  // 32 rows x FS_PW / 4 chunks of 16 B
+            const uint32_t x = lane + 32 * i;
+            const uint32_t j = x / (FS_PW / 4), c = x % (FS_PW / 4);
+            const uint32_t id = __shfl_sync(0xffffffffu, my_id, j);
+            const uint32_t d0 = p * FS_PW + c * 4;
+            const bool valid = id < k && d0 < dim;
+            const float* src = valid ? C + (uint64_t)id * dim + d0 : C;
+            cp_async16(buf + j * (FS_PW + 4) + c * 4, src, valid);
         }
-        __syncwarp();
-        if (lane < nb) {
-            const uint32_t c = id_of(b0 + lane);
-            float acc = __int_as_float(0x7f800000);
-            if (c < k) {
-                const float* row = tile + lane * stride;
-                acc = 0.0f;
-                for (uint32_t c4 = 0; c4 < n4; c4++) {
-                    const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
-                    const float4 yv = *reinterpret_cast<const float4*>(ys + c4 * 4);
-                    acc = sq_step(acc, yv.x, v.x);
-                    acc = sq_step(acc, yv.y, v.y);
-                    acc = sq_step(acc, yv.z, v.z);
-                    acc = sq_step(acc, yv.w, v.w);
-                }
-            }
-            out[b0 + lane] = acc;
-        }
-        __syncwarp();
+        cp_async_commit();
+    };
+#pragma unroll
+    for (uint32_t u = 0; u < FS_NBUF - 1; u++) {
+        if (u < nu) issue(u);
+        else cp_async_commit();
     }
+    float acc = 0.0f;
+    for (uint32_t u = 0; u < nu; u++) {
+        if (u + FS_NBUF - 1 < nu) issue(u + FS_NBUF - 1);
+        else cp_async_commit();
+        cp_async_wait<FS_NBUF - 1>();
+        __syncwarp();
+        const uint32_t bi = u / npiece, p = u - bi * npiece;
+        const float* row = wbuf + (u % FS_NBUF) * FS_BUF_FLOATS + lane * (FS_PW + 4);
+        const uint32_t dn = min(FS_PW, dim - p * FS_PW);
+        for (uint32_t c4 = 0; c4 < dn / 4; c4++) {
+            const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+            const float4 yv = *reinterpret_cast<const float4*>(ys + p * FS_PW + c4 * 4);
+            acc = sq_step(acc, yv.x, v.x);
+            acc = sq_step(acc, yv.y, v.y);
+            acc = sq_step(acc, yv.z, v.z);
+            acc = sq_step(acc, yv.w, v.w);
+        }
+        __syncwarp();
+        if (p == npiece - 1) {
+            const uint32_t t = (warp + bi * nwarps) * 32 + lane;
+            if (t < cnt) out(t, id_of(t) < k ? acc : __int_as_float(0x7f800000));
+            acc = 0.0f;
+        }
+    }
+    cp_async_wait<0>();
 }
 
 struct FusedArgs {
@@ -140,21 +176,27 @@ struct FusedArgs {
 };
 
 __host__ __device__ inline uint32_t fs_nwords(uint32_t k) { return (k + 31) / 32; }
+__host__ __device__ inline uint32_t fs_pow2(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
 
 // dynamic shared memory layout (bytes), shared by host and device
 struct FusedLayout {
-    uint32_t ys, topS, u, tiles, total;
-    __host__ __device__ FusedLayout(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim) {
+    uint32_t ys, topS, u, bufs, total;
+    __host__ __device__ FusedLayout(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
         const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1);
-        const uint32_t dimp = (dim + 3) & ~3u;
+        const uint32_t dimp = (dim + FS_PW - 1) / FS_PW * FS_PW;
         ys = 0;
         topS = ys + dimp * 4;
         u = (topS + w1 * 4 + 15) & ~15u;
-        // phase 1: keys (u64) ; phase 2: bitmap, word prefix, needed ids, values, edge distances, positions
-        const uint32_t p1 = FS_MAX_KEYS * 8;
+        // phase 1: sorted chunk list (u64, pow2) + chunk-centroid distances + top positions;
+        // phase 2: bitmap, word prefix, needed ids, values, edge distances, positions
+        const uint32_t p1 = fs_pow2(capc) * 8 + FS_MAX_KEYS * 4 + w1 * 4;
         const uint32_t p2 = (2 * nw + 2 * nn + w1 * n + w2) * 4;
-        tiles = (u + (p1 > p2 ? p1 : p2) + 15) & ~15u;
-        total = tiles + (FS_THREADS / 32) * FS_ROWS * (dim + 4) * 4;
+        bufs = (u + (p1 > p2 ? p1 : p2) + 15) & ~15u;
+        total = bufs + (FS_THREADS / 32) * FS_NBUF * FS_BUF_FLOATS * 4;
     }
 };
 
@@ -163,21 +205,22 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
     __shared__ uint32_t hist[2048];
     __shared__ uint32_t scan[40];
     __shared__ float s_yn;
-    __shared__ int s_fail;
+    __shared__ unsigned int s_w1max;
     __shared__ unsigned long long s_scanned;
     __shared__ float s_dmax;
     const bool top_mode = f.qlist != nullptr;
     if (top_mode && blockIdx.x >= *f.qcount) return;
     const uint64_t q = top_mode ? f.qlist[blockIdx.x] : blockIdx.x;
     const uint32_t k = a.k, n = a.n, dim = a.dim, w1 = f.w1, w2 = f.w2;
-    const FusedLayout lay(k, n, w1, w2, dim);
+    const FusedLayout lay(k, n, w1, w2, dim, f.capc);
     float* ys = reinterpret_cast<float*>(smem + lay.ys);
     uint32_t* topS = reinterpret_cast<uint32_t*>(smem + lay.topS);
-    float* tiles = reinterpret_cast<float*>(smem + lay.tiles);
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
-    for (uint32_t d = tid; d < ((dim + 3) & ~3u); d += nt) ys[d] = d < dim ? f.Y[q * dim + d] : 0.0f;
+    float* wbuf = reinterpret_cast<float*>(smem + lay.bufs) + (tid >> 5) * FS_NBUF * FS_BUF_FLOATS;
+    const uint32_t dimp = (dim + FS_PW - 1) / FS_PW * FS_PW;
+    for (uint32_t d = tid; d < dimp; d += nt) ys[d] = d < dim ? f.Y[q * dim + d] : 0.0f;
     if (tid == 0) {
-        s_fail = 0;
+        s_w1max = 0u;
         s_scanned = 0;
         s_dmax = 0.0f;
     }
@@ -185,89 +228,49 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
 
     if (!top_mode) {
         // ---- phase 1: exact distances of the selected chunks' centroids
-        uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.u);
         const uint32_t nc = f.ccnt[q];
-        const uint32_t ncent = nc * f.cs;
+        const uint32_t cs = f.cs, ncent = nc * cs;
         if (nc > f.capc || ncent > FS_MAX_KEYS || nc < w1) {
             if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
             return;
         }
-        uint32_t np2 = 1;
-        while (np2 < ncent) np2 <<= 1;
-        const uint32_t* cl = f.clist + q * f.capc;
-        const uint32_t cs = f.cs;
-        // rows staged FS_ROWS per warp (coalesced 16-byte loads), lanes
-        // 0..FS_ROWS-1 run the sequential sqdist of one row each
-        {
-            const uint32_t warp = tid >> 5, lane = tid & 31u, nwarps = nt >> 5;
-            const uint32_t n4 = dim >> 2, stride = dim + 4;
-            float* tile = tiles + (size_t)warp * FS_ROWS * stride;
-            for (uint32_t b0 = warp * FS_ROWS; b0 < ncent; b0 += nwarps * FS_ROWS) {
-                const uint32_t nb = min(FS_ROWS, ncent - b0);
-                for (uint32_t r = 0; r < nb; r++) {
-                    const uint32_t t = b0 + r;
-                    const uint32_t c = cl[t / cs] * cs + t % cs;
-                    if (c < k) {
-                        const float4* cp = reinterpret_cast<const float4*>(a.centroids + (uint64_t)c * dim);
-                        for (uint32_t c4 = lane; c4 < n4; c4 += 32)
-                            *reinterpret_cast<float4*>(tile + r * stride + c4 * 4) = __ldg(cp + c4);
-                    }
-                }
-                __syncwarp();
-                if (lane < nb) {
-                    const uint32_t t = b0 + lane;
-                    const uint32_t c = cl[t / cs] * cs + t % cs;
-                    uint64_t key = ~0ull;
-                    if (c < k) {
-                        const float* row = tile + lane * stride;
-                        float acc = 0.0f;
-                        for (uint32_t c4 = 0; c4 < n4; c4++) {
-                            const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
-                            const float4 yv = *reinterpret_cast<const float4*>(ys + c4 * 4);
-                            acc = sq_step(acc, yv.x, v.x);
-                            acc = sq_step(acc, yv.y, v.y);
-                            acc = sq_step(acc, yv.z, v.z);
-                            acc = sq_step(acc, yv.w, v.w);
-                        }
-                        key = make_key(acc, c);
-                    }
-                    keys[t] = key;
-                }
-                __syncwarp();
-            }
-        }
-        for (uint32_t t = ncent + tid; t < np2; t += nt) keys[t] = ~0ull;
+        // chunk list sorted ascending, so position order == centroid id order
+        uint64_t* cls = reinterpret_cast<uint64_t*>(smem + lay.u);
+        const uint32_t npc = fs_pow2(nc);
+        float* vals = reinterpret_cast<float*>(cls + fs_pow2(f.capc));
+        uint32_t* topPos = reinterpret_cast<uint32_t*>(vals + FS_MAX_KEYS);
+        for (uint32_t t = tid; t < npc; t += nt) cls[t] = t < nc ? (uint64_t)f.clist[q * f.capc + t] : ~0ull;
+        __syncthreads();
+        bitonic_sort_u64<false>(cls, npc, tid, nt);
+        exact_rows_pipe(a.centroids, k, dim, ys, wbuf, ncent,
+                        [&](uint32_t t) { return (uint32_t)cls[t / cs] * cs + t % cs; },
+                        [&](uint32_t t, float v) { vals[t] = v; });
         if (tid == 0) {
             float yn = 0.0f;
             for (uint32_t d = 0; d < dim; d++) yn = fmaf(ys[d], ys[d], yn);
             s_yn = yn;
         }
         __syncthreads();
-        bitonic_sort_u64<false>(keys, np2, tid, nt);
-        if (tid == 0) {
-            const uint64_t kw = keys[w1 - 1];
-            const float exact_w1 = unord_float((uint32_t)(kw >> 32));
-            const float eps = tc_eps(s_yn, f.cmax, dim, false);
-            const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
-            if (kw == ~0ull || !(lower > (double)exact_w1)) {
-                s_fail = 1;
-                f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
-            }
+        // exact top-w1 by (dist, id): positions ascending == ids ascending
+        block_select_ordered(vals, ncent, w1, topPos, hist, scan);
+        __syncthreads();
+        float mx = 0.0f;
+        for (uint32_t r = tid; r < w1; r += nt) {
+            const uint32_t pos = topPos[r];
+            topS[r] = (uint32_t)cls[pos / cs] * cs + pos % cs;
+            mx = fmaxf(mx, vals[pos]);  // +inf (a padded id) fails the certificate below
         }
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((tid & 31) == 0) atomicMax(&s_w1max, __float_as_uint(mx));  // distances >= 0
         __syncthreads();
-        if (s_fail) return;
-        // the w1 winners by ascending id (second_level_rank's edge order)
-        for (uint32_t t = tid; t < w1; t += nt) topS[t] = (uint32_t)keys[t];
-        __syncthreads();
-        uint32_t np2w = 1;
-        while (np2w < w1) np2w <<= 1;
-        for (uint32_t t = tid; t < np2w; t += nt) keys[t] = t < w1 ? (uint64_t)topS[t] : ~0ull;
-        __syncthreads();
-        bitonic_sort_u64<false>(keys, np2w, tid, nt);
-        for (uint32_t t = tid; t < w1; t += nt) {
-            topS[t] = (uint32_t)keys[t];
-            a.top[q * w1 + t] = (uint32_t)keys[t];
+        const float exact_w1 = __uint_as_float(s_w1max);
+        const float eps = tc_eps(s_yn, f.cmax, dim, false);
+        const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
+        if (!(lower > (double)exact_w1)) {
+            if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
+            return;
         }
+        for (uint32_t r = tid; r < w1; r += nt) a.top[q * w1 + r] = topS[r];
         __syncthreads();
     } else {
         for (uint32_t t = tid; t < w1; t += nt) topS[t] = a.top[q * w1 + t];
@@ -307,7 +310,8 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         }
     }
     __syncthreads();
-    exact_rows_staged(a.centroids, k, dim, ys, tiles, nneed, [&](uint32_t t) { return nid[t]; }, nval);
+    exact_rows_pipe(a.centroids, k, dim, ys, wbuf, nneed, [&](uint32_t t) { return nid[t]; },
+                    [&](uint32_t t, float v) { nval[t] = v; });
     __syncthreads();
     auto val_of = [&](uint32_t c) -> float {
         const uint32_t w = c >> 5;
@@ -371,13 +375,13 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
 
 }  // namespace dev
 
-size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim) {
-    return dev::FusedLayout(k, n, w1, w2, dim).total;
+size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
+    return dev::FusedLayout(k, n, w1, w2, dim, capc).total;
 }
 
-bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim) {
-    return dim % 4 == 0 && dim <= 128 && w1 <= 256 && w2 <= w1 * n && (uint64_t)w1 * (n + 1) <= 8192 &&
-           select_fused_smem(k, n, w1, w2, dim) <= 200 * 1024;
+bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
+    return dim % 4 == 0 && dim <= 256 && w1 <= 256 && w2 <= w1 * n && (uint64_t)w1 * (n + 1) <= 8192 &&
+           capc <= 1024 && select_fused_smem(k, n, w1, w2, dim, capc) <= 200 * 1024;
 }
 
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
@@ -393,7 +397,7 @@ void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, 
                          uint32_t* sel_out, float* ab_out, cudaStream_t st) {
     if (nblocks == 0) return;
     dev::FusedArgs f{Y, w1, w2, cs, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, sel_out, ab_out};
-    const size_t smem = select_fused_smem(a.k, a.n, w1, w2, a.dim);
+    const size_t smem = select_fused_smem(a.k, a.n, w1, w2, a.dim, capc);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dev::k_select_fused<<<(unsigned)nblocks, dev::FS_THREADS, smem, st>>>(a, f);
     CUDA_LAUNCH_CHECK();

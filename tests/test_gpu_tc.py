@@ -192,6 +192,7 @@ def test_chunk_select_coarse_stage_paths_match_oracle(vlqadc, oracle_mod, tmp_pa
     o = oracle_mod.OracleIndex.load(path)
     grid = [(64, 0.25, 100), (16, 0.5, 10), (200, 0.1, 20), (1, 1.0, 5)]
     ref = {g: o.search(q, g[0], g[1], g[2])[:2] for g in grid}
+    idx.set_profiling(True)
     for knobs in [dict(tc_chunk_select=1, tc_chunk_cap=256), dict(tc_chunk_select=1, tc_chunk_cap=4),
                   dict(tc_chunk_select=0)]:
         for key, val in knobs.items():
