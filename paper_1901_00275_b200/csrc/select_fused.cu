@@ -37,10 +37,11 @@ namespace vlq {
 namespace dev {
 
 constexpr uint32_t FS_THREADS = 256;
-constexpr uint32_t FS_PW = 16;         // dimensions per staged row piece
-constexpr uint32_t FS_NBUF = 2;        // row-piece buffers per warp (cp.async pipeline depth)
-constexpr uint32_t FS_BUF_FLOATS = 32 * (FS_PW + 4);  // one piece of 32 rows (stride PW + 4: conflict-free LDS.128)
+constexpr uint32_t FS_PW = 32;         // dimensions per staged row piece (one 128-byte line per row)
+constexpr uint32_t FS_RS = FS_PW + 4;  // staged row stride in floats (conflict-free LDS.128)
+constexpr uint32_t FS_BUF_FLOATS = 32 * FS_RS;  // one piece of 32 rows
 constexpr uint32_t FS_MAX_KEYS = 2048; // exactly evaluated chunk centroids per query
+constexpr uint32_t FS_CS = 8;          // centroids per chunk (TILEMIN8)
 
 // tau / T per query and the compacted list of selected chunks.
 __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
@@ -97,11 +98,12 @@ __device__ __forceinline__ void cp_async_wait() {
 // Exact reference-order sqdist (vecset.cpp:22-29: acc += (y - c)^2 in order)
 // of the rows id_of(0 .. cnt) (centroid ids; id >= k gives +inf), out(t, d).
 // Each warp takes batches of 32 rows, lane l owning row l of the batch; the
-// rows stream through shared memory in FS_PW-dimension pieces (coalesced
-// 16-byte cp.async, zero-filled for invalid rows) with FS_NBUF pieces in
-// flight per warp, so the L2 latency of the gathered centroid rows overlaps
+// rows stream through shared memory in 32-dimension pieces (one 128-byte line
+// per row; coalesced 16-byte cp.async, zero-filled for invalid rows), double-
+// buffered per warp, so the L2 latency of the gathered centroid rows overlaps
 // the sequential sums.  Warp-synchronous; `wbuf` is this warp's
-// FS_NBUF * FS_BUF_FLOATS floats.
+// 2 * FS_BUF_FLOATS floats.  The loop keeps (batch, piece) counters instead of
+// dividing, and the 8 row bases a lane copies for are computed once per batch.
 template <typename IdFn, typename OutFn>
 __device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uint32_t k, uint32_t dim,
                                                 const float* ys, float* wbuf, uint32_t cnt, IdFn&& id_of,
@@ -109,51 +111,75 @@ __device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uin
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
     const uint32_t npiece = (dim + FS_PW - 1) / FS_PW;
     const uint32_t nbatch = cnt > warp * 32 ? (cnt - warp * 32 + nwarps * 32 - 1) / (nwarps * 32) : 0;
+    if (nbatch == 0) return;
     const uint32_t nu = nbatch * npiece;
-    auto issue = [&](uint32_t u) {
-        const uint32_t bi = u / npiece, p = u - bi * npiece;
-        const uint32_t r0 = (warp + bi * nwarps) * 32;
-        const uint32_t my_id = r0 + lane < cnt ? id_of(r0 + lane) : 0xffffffffu;
-        float* buf = wbuf + (u % FS_NBUF) * FS_BUF_FLOATS;
+    const uint32_t sub = lane & 7u, rsub = lane >> 3;  // copy role: 16-byte chunk `sub` of rows 4 i + rsub
+    const float* rb[8];
+    uint32_t rvalid = 0;
+    uint32_t ib = 0, ip = 0, islot = 0;  // next unit to issue
+    auto issue = [&]() {
+        if (ip == 0) {
+            const uint32_t r0 = (warp + ib * nwarps) * 32;
+            const uint32_t my_id = r0 + lane < cnt ? id_of(r0 + lane) : 0xffffffffu;
+            rvalid = 0;
 #pragma unroll
-        for (uint32_t i = 0; i < FS_PW / 4; i++) {  // 32 rows x FS_PW / 4 chunks of 16 B
-            const uint32_t x = lane + 32 * i;
-            const uint32_t j = x / (FS_PW / 4), c = x % (FS_PW / 4);
-            const uint32_t id = __shfl_sync(0xffffffffu, my_id, j);
-            const uint32_t d0 = p * FS_PW + c * 4;
-            const bool valid = id < k && d0 < dim;
-            const float* src = valid ? C + (uint64_t)id * dim + d0 : C;
-            cp_async16(buf + j * (FS_PW + 4) + c * 4, src, valid);
+            for (int i = 0; i < 8; i++) {
+                const uint32_t id = __shfl_sync(0xffffffffu, my_id, 4 * i + rsub);
+                const bool v = id < k;
+                rvalid |= (v ? 1u : 0u) << i;
+                rb[i] = C + (v ? (uint64_t)id * dim : 0ull) + sub * 4;
+            }
         }
+        float* buf = wbuf + islot * FS_BUF_FLOATS + rsub * FS_RS + sub * 4;
+        const bool dval = ip * FS_PW + sub * 4 < dim;
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            cp_async16(buf + 4 * i * FS_RS, rb[i] + ip * FS_PW, dval && ((rvalid >> i) & 1u));
         cp_async_commit();
+        islot ^= 1u;
+        if (++ip == npiece) {
+            ip = 0;
+            ib++;
+        }
     };
-#pragma unroll
-    for (uint32_t u = 0; u < FS_NBUF - 1; u++) {
-        if (u < nu) issue(u);
-        else cp_async_commit();
-    }
+    issue();
     float acc = 0.0f;
+    uint32_t cb = 0, cp = 0, cslot = 0;  // unit being computed
     for (uint32_t u = 0; u < nu; u++) {
-        if (u + FS_NBUF - 1 < nu) issue(u + FS_NBUF - 1);
+        if (u + 1 < nu) issue();
         else cp_async_commit();
-        cp_async_wait<FS_NBUF - 1>();
+        cp_async_wait<1>();
         __syncwarp();
-        const uint32_t bi = u / npiece, p = u - bi * npiece;
-        const float* row = wbuf + (u % FS_NBUF) * FS_BUF_FLOATS + lane * (FS_PW + 4);
-        const uint32_t dn = min(FS_PW, dim - p * FS_PW);
-        for (uint32_t c4 = 0; c4 < dn / 4; c4++) {
-            const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
-            const float4 yv = *reinterpret_cast<const float4*>(ys + p * FS_PW + c4 * 4);
-            acc = sq_step(acc, yv.x, v.x);
-            acc = sq_step(acc, yv.y, v.y);
-            acc = sq_step(acc, yv.z, v.z);
-            acc = sq_step(acc, yv.w, v.w);
+        const float* row = wbuf + cslot * FS_BUF_FLOATS + lane * FS_RS;
+        const float* yp = ys + cp * FS_PW;
+        if (cp * FS_PW + FS_PW <= dim) {
+#pragma unroll
+            for (uint32_t c4 = 0; c4 < FS_PW / 4; c4++) {
+                const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+                const float4 yv = *reinterpret_cast<const float4*>(yp + c4 * 4);
+                acc = sq_step(acc, yv.x, v.x);
+                acc = sq_step(acc, yv.y, v.y);
+                acc = sq_step(acc, yv.z, v.z);
+                acc = sq_step(acc, yv.w, v.w);
+            }
+        } else {
+            for (uint32_t c4 = 0; c4 < (dim - cp * FS_PW) / 4; c4++) {
+                const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
+                const float4 yv = *reinterpret_cast<const float4*>(yp + c4 * 4);
+                acc = sq_step(acc, yv.x, v.x);
+                acc = sq_step(acc, yv.y, v.y);
+                acc = sq_step(acc, yv.z, v.z);
+                acc = sq_step(acc, yv.w, v.w);
+            }
         }
         __syncwarp();
-        if (p == npiece - 1) {
-            const uint32_t t = (warp + bi * nwarps) * 32 + lane;
+        cslot ^= 1u;
+        if (++cp == npiece) {
+            const uint32_t t = (warp + cb * nwarps) * 32 + lane;
             if (t < cnt) out(t, id_of(t) < k ? acc : __int_as_float(0x7f800000));
             acc = 0.0f;
+            cp = 0;
+            cb++;
         }
     }
     cp_async_wait<0>();
@@ -186,24 +212,26 @@ __host__ __device__ inline uint32_t fs_pow2(uint32_t x) {
 struct FusedLayout {
     uint32_t ys, topS, u, bufs, total;
     __host__ __device__ FusedLayout(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
-        const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1);
+        const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1), ne = w1 * n;
         const uint32_t dimp = (dim + FS_PW - 1) / FS_PW * FS_PW;
         ys = 0;
         topS = ys + dimp * 4;
         u = (topS + w1 * 4 + 15) & ~15u;
         // phase 1: sorted chunk list (u64, pow2) + chunk-centroid distances + top positions;
-        // phase 2: bitmap, word prefix, needed ids, values, edge distances, positions
+        // phase 2: bitmap (u32), word prefix (u16), needed values, needed ids / edge distances, positions
         const uint32_t p1 = fs_pow2(capc) * 8 + FS_MAX_KEYS * 4 + w1 * 4;
-        const uint32_t p2 = (2 * nw + 2 * nn + w1 * n + w2) * 4;
+        const uint32_t p2 = nw * 4 + ((nw * 2 + 3) & ~3u) + nn * 4 + (nn > ne ? nn : ne) * 4 + w2 * 4;
         bufs = (u + (p1 > p2 ? p1 : p2) + 15) & ~15u;
-        total = bufs + (FS_THREADS / 32) * FS_NBUF * FS_BUF_FLOATS * 4;
+        // per-warp row-piece double buffers; the selects' histogram (2048 + 40
+        // words) reuses this region outside the row evaluations
+        uint32_t b = (FS_THREADS / 32) * 2 * FS_BUF_FLOATS * 4;
+        if (b < 2088 * 4) b = 2088 * 4;
+        total = bufs + b;
     }
 };
 
 __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, FusedArgs f) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t hist[2048];
-    __shared__ uint32_t scan[40];
     __shared__ float s_yn;
     __shared__ unsigned int s_w1max;
     __shared__ unsigned long long s_scanned;
@@ -216,7 +244,9 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
     float* ys = reinterpret_cast<float*>(smem + lay.ys);
     uint32_t* topS = reinterpret_cast<uint32_t*>(smem + lay.topS);
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
-    float* wbuf = reinterpret_cast<float*>(smem + lay.bufs) + (tid >> 5) * FS_NBUF * FS_BUF_FLOATS;
+    float* wbuf = reinterpret_cast<float*>(smem + lay.bufs) + (tid >> 5) * 2 * FS_BUF_FLOATS;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + lay.bufs);  // aliases the row buffers (used apart)
+    uint32_t* scan = hist + 2048;
     const uint32_t dimp = (dim + FS_PW - 1) / FS_PW * FS_PW;
     for (uint32_t d = tid; d < dimp; d += nt) ys[d] = d < dim ? f.Y[q * dim + d] : 0.0f;
     if (tid == 0) {
@@ -229,7 +259,8 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
     if (!top_mode) {
         // ---- phase 1: exact distances of the selected chunks' centroids
         const uint32_t nc = f.ccnt[q];
-        const uint32_t cs = f.cs, ncent = nc * cs;
+        constexpr uint32_t cs = FS_CS;
+        const uint32_t ncent = nc * cs;
         if (nc > f.capc || ncent > FS_MAX_KEYS || nc < w1) {
             if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
             return;
@@ -243,7 +274,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         __syncthreads();
         bitonic_sort_u64<false>(cls, npc, tid, nt);
         exact_rows_pipe(a.centroids, k, dim, ys, wbuf, ncent,
-                        [&](uint32_t t) { return (uint32_t)cls[t / cs] * cs + t % cs; },
+                        [&](uint32_t t) { return (uint32_t)cls[t / cs] * cs + (t & (cs - 1)); },
                         [&](uint32_t t, float v) { vals[t] = v; });
         if (tid == 0) {
             float yn = 0.0f;
@@ -257,7 +288,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         float mx = 0.0f;
         for (uint32_t r = tid; r < w1; r += nt) {
             const uint32_t pos = topPos[r];
-            topS[r] = (uint32_t)cls[pos / cs] * cs + pos % cs;
+            topS[r] = (uint32_t)cls[pos / cs] * cs + (pos & (cs - 1));
             mx = fmaxf(mx, vals[pos]);  // +inf (a padded id) fails the certificate below
         }
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -280,11 +311,11 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
     // ---- phase 2: exact distances of the regions and their neighbours
     const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1), total = w1 * n;
     uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + lay.u);
-    uint32_t* wpref = bitmap + nw;
-    uint32_t* nid = wpref + nw;
-    float* nval = reinterpret_cast<float*>(nid + nn);
-    float* dq = nval + nn;
-    uint32_t* selpos = reinterpret_cast<uint32_t*>(dq + total);
+    uint16_t* wpref = reinterpret_cast<uint16_t*>(bitmap + nw);
+    float* nval = reinterpret_cast<float*>(bitmap + nw + (nw + 1) / 2);
+    uint32_t* nid = reinterpret_cast<uint32_t*>(nval + nn);
+    float* dq = reinterpret_cast<float*>(nid);  // the needed ids are dead once their values are in nval
+    uint32_t* selpos = nid + (nn > total ? nn : total);
     for (uint32_t i = tid; i < nw; i += nt) bitmap[i] = 0;
     __syncthreads();
     for (uint32_t e = tid; e < nn; e += nt) {
@@ -300,7 +331,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) local += __popc(bitmap[i]);
         uint32_t run = block_excl_scan_u32(local, scan, &nneed);
         for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) {
-            wpref[i] = run;
+            wpref[i] = (uint16_t)run;
             uint32_t w = bitmap[i];
             while (w) {
                 const uint32_t b = __ffs(w) - 1;
