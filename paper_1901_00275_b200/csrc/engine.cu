@@ -56,6 +56,7 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_SCAN_EA")) cfg_.scan_ea = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -937,7 +938,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (sel) launch_apply_selection(a, nt, w2, sel->sel_in, sel->ab_in, st);
     else if (!second_done) launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
-    launch_term5(d_q, pqT_.p, dim_, m_, t5_.p, meta_.p, nt, st);
+    launch_term5(cfg_.cert_slack, d_q, pqT_.p, dim_, m_, t5_.p, meta_.p, nt, st);
     launches += 2;
     const uint32_t keep_x = next_pow2(std::max<uint32_t>(32, topk));
     const uint32_t buf_x = 2 * keep_x;
@@ -946,7 +947,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     if (fast) {
         const uint32_t keep = scan_keep(topk);
         mark(PH_SCAN);
-        if (cfg_.scan_packed && (cfg_.scan_variant == 0 || (cfg_.scan_variant >= 5 && cfg_.scan_variant <= 12)) && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
+        if (cfg_.scan_packed && cfg_.scan_variant == 0 && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
             a.eterm_lam = eterm_lam_.p;
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
@@ -954,10 +955,10 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         a.sel_agg = cfg_.scan_sel_agg != 0;
         a.flush_exact = cfg_.scan_flush_exact != 0;
         const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
-        // fast_kind: the v6 / q8 scan ran (the only kernels with the retry indirection)
-        const bool fast_kind = (cfg_.scan_variant == 0 || cfg_.scan_variant == 9) && a.eterm_lam &&
-                               (m_ == 16 || m_ == 8 || m_ == 4) && w2 <= 4096;
-        if (!launch_scan_fast(a, nt, w2, keep, cfg_.scan_variant, slots, cfg_.scan_prefetch, st))
+        // fast_kind: the fused fast scan ran (the only kernel with the retry indirection)
+        const bool fast_kind = cfg_.scan_variant == 0 && (m_ == 16 || m_ == 8 || m_ == 4) && w2 <= 4096 &&
+                               keep <= 512;
+        if (!fast_kind || !launch_scan_fast(a, nt, w2, keep, slots, cfg_.scan_ea != 0, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
@@ -978,7 +979,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             r.cand = cand2_.p;
             r.qlist = qlist_.p;
             r.qcount = err_.p + 2;
-            launch_scan_fast(r, nt, w2, keep2, cfg_.scan_variant, slots, cfg_.scan_prefetch, st);
+            launch_scan_fast(r, nt, w2, keep2, slots, cfg_.scan_ea != 0, st);
             launch_rescore(r, nt, keep2, topk, d_ids, d_dists, st);
             CUDA_CHECK(cudaMemsetAsync(cnt2_.p, 0, 4, st));
             launch_compact_flags(meta_.p, nt, qlist2_.p, cnt2_.p, st);
@@ -1021,7 +1022,8 @@ uint32_t Engine::scan_keep(uint32_t topk) const {
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
-    else if (key == "scan_prefetch") cfg_.scan_prefetch = (int)value;
+    else if (key == "scan_ea") cfg_.scan_ea = (int)value;
+    else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;
     else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;
     else if (key == "force_exact") cfg_.force_exact = (int)value;
     else if (key == "tc_persist") cfg_.tc_persist = (int)value;

@@ -33,12 +33,12 @@ struct EngineConfig {
     uint64_t workspace_bytes = 4ull << 30;  // per-query-tile scratch budget
     uint32_t max_tile = 16384;
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
-    int scan_variant = 0;  // 0 default (v6 packed-fp32 scan), 1 generic warp-buffer scan, 2/3/4 v5 LUT variants,
-                           // 5-8 v7 bulk-async staged ring (4 ring configs), 9 v6 with the u8-quantized LUT
+    int scan_variant = 0;  // 0 default (fused fast scan + exact re-score), 1 generic warp-buffer scan
     int scan_slots = 0;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8; +100 = 4 CTAs/SM);
                            // 0 = auto: 6 (3 CTAs/SM), or 104 on shards of >= 4 (1/4 or less of the
                            // entries per query: measured 3% faster at 8 shards, neutral unsharded)
-    int scan_prefetch = 0; // v6 scan: L2 prefetch distance in chunks (0 = off)
+    float cert_slack = 0.0f;  // test knob (cert_slack_milli): widens the re-score certificate -> retry / exact paths
+    int scan_ea = 0;       // fast scan: early abandon of the second half of the LUT lookups (exact; scan_fast.cu)
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)

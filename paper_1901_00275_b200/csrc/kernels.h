@@ -13,7 +13,7 @@ struct QueryMeta {
     float dmax;                  // bound on |term1| over the query's selected cells
     float s5max;                 // bound on |sum5|
     uint32_t flag;               // 1: certificate failed -> exact fallback
-    float qerr;                  // bound on |fast - exact| added by a quantized scan LUT (0 otherwise)
+    float qerr;                  // extra bound on |fast - exact| (0: every scan LUT is exact fp32)
 };
 
 // Device views used by the search kernels (all pointers device-resident).
@@ -84,15 +84,17 @@ void launch_pack_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32
 void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const uint32_t* sel_in, const float* ab,
                             cudaStream_t st);
 // pqT: the PQ codebook transposed to [p][t][j] (j = codeword, fastest)
-void launch_term5(const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
+// cert_slack: added to the re-score certificate's error bound (0 in production;
+// tests widen it to force the retry and exact-fallback paths)
+void launch_term5(float cert_slack, const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
                   uint64_t nq, cudaStream_t st);
 size_t scan_smem_bytes(uint32_t m, uint32_t nwarps, uint32_t buf);
 void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t keep, uint32_t buf, uint32_t nwarps,
                  bool fast, const uint32_t* qlist, const unsigned int* qcount, cudaStream_t st);
 // eterm_lam[e] = (bits(eterm[e]) & ~0xff) | lambdas[e]
 void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t n, uint32_t* out, cudaStream_t st);
-bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int variant, int slots,
-                      int prefetch, cudaStream_t st);
+bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int slots, bool early_abandon,
+                      cudaStream_t st);
 void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
                     cudaStream_t st);
 void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,

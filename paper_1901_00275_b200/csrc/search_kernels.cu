@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t 
 // term5 table (query_term5): t5[q][p][j] = dot(y_p, PQ[p][j]) in order; also
 // S5max = sum_p max_j |t5| for the certificate.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_term5(const float* __restrict__ Y, const float* __restrict__ pqT,
+__global__ void __launch_bounds__(256) k_term5(float cert_slack, const float* __restrict__ Y, const float* __restrict__ pqT,
                                                uint32_t dim, uint32_t m, float* __restrict__ t5,
                                                QueryMeta* __restrict__ meta) {
     // thread j computes t5[p][j] for every sub-space p (sequential fp32 dot,
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) k_term5(const float* __restrict__ Y, cons
     }
     if (threadIdx.x == 0) {
         meta[q].s5max = s5;
-        meta[q].qerr = 0.0f;  // set by a quantized-LUT scan
+        meta[q].qerr = cert_slack;  // 0 unless a test widens the certificate (engine knob cert_slack)
     }
 }
 
@@ -555,9 +555,9 @@ void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const
     CUDA_LAUNCH_CHECK();
 }
 
-void launch_term5(const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
+void launch_term5(float cert_slack, const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
                   uint64_t nq, cudaStream_t st) {
-    dev::k_term5<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(Y, pqT, dim, m, t5, meta);
+    dev::k_term5<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(cert_slack, Y, pqT, dim, m, t5, meta);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -84,17 +84,20 @@ def test_exhaustive_search_equals_full_scan(vlqadc, oracle_mod):
         assert np.array_equal(ids, oids) and same_f32(dists, odists)
 
 
-@pytest.mark.parametrize("seed,variant", [(0, 0), (1, 0), (2, 4), (3, 5), (4, 7), (5, 9)])
-def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed, variant):
-    """Random (w1, alpha, k) vs the oracle (v6 scan; seed 2 with the v5
-    single-table scan; seeds 3/4 with the bulk-async staged scan v7; seed 5
-    with the u8-quantized LUT, whose widened certificate sends more queries
-    to the exact fallback -- results must not change)."""
+@pytest.mark.parametrize("seed,knobs", [(0, {}), (1, {}), (2, {"scan_ea": 1}), (3, {"scan_variant": 1}),
+                                        (4, {"scan_ea": 1, "scan_slots": 104}), (5, {"cert_slack_milli": 10**6})])
+def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed, knobs):
+    """Random (w1, alpha, k) vs the oracle: the fused fast scan, with early
+    abandon (skipping the second half of the LUT lookups below the
+    threshold), the generic warp-buffer scan, 4 CTAs/SM slots, and a widened
+    certificate that sends every query through the retry pass and the exact
+    scan -- results must not change."""
     rng = np.random.default_rng(seed)
     for name in ALL_CASES:
         z, index_path, _ = load_golden(name)
         idx = vlqadc.Index.load(index_path)
-        idx.set_tuning("scan_variant", variant)
+        for key, val in knobs.items():
+            idx.set_tuning(key, val)
         o = oracle_mod.OracleIndex.load(index_path)
         for _ in range(3):
             w1 = int(rng.integers(1, idx.k + 1))
@@ -439,14 +442,14 @@ def test_add_vecs_errors_mirror_read_vecs(vlqadc, tmp_path):
 
 @pytest.mark.parametrize("retry", [0, 1])
 def test_certificate_retry_and_exact_fallback_match_oracle(vlqadc, oracle_mod, retry):
-    """The u8-LUT scan's widened certificate fails for most queries at
-    k' = 128, so the retry pass (fast scan again with k' = 512 for the
-    listed queries, re-score) and the exact scan for what still fails both
-    run; with the retry on or off the results equal the oracle's."""
+    """A widened certificate (test knob cert_slack) fails for every query,
+    so the retry pass (fast scan again with 4 k' for the listed queries,
+    re-score) and the exact scan for what still fails both run; with the
+    retry on or off the results equal the oracle's."""
     for name in ALL_CASES:
         z, index_path, _ = load_golden(name)
         idx = vlqadc.Index.load(index_path)
-        idx.set_tuning("scan_variant", 9)
+        idx.set_tuning("cert_slack_milli", 10**6)
         idx.set_tuning("scan_retry", retry)
         o = oracle_mod.OracleIndex.load(index_path)
         for w1, alpha, k in [(min(idx.k, 16), 0.5, 10), (min(idx.k, 64), 0.25, 100), (min(idx.k, 8), 1.0, 3)]:
