@@ -56,7 +56,6 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
-    if (const char* v = std::getenv("VLQ_SCAN_EA")) cfg_.scan_ea = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -826,9 +825,9 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         }
         launch_coarse_tc(4, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, tmin8_.p, nchunk8, nullptr, nullptr,
                          st, nullptr, nullptr, 0, x1, nullptr);
+        mark(PH_FIRST);  // the coarse phase is the tensor-core GEMM alone (its roofline in bench.py)
         launch_chunk_select(tmin8_.p, nt, nchunk8, w1, d_q, dim_, cmax_, cfg_.tc_chunk_cap, clist_.p, ccnt_.p,
                             tch_.p, st);
-        mark(PH_FIRST);
         SearchArgs a = search_args();
         CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
         launch_select_fused(a, nt, d_q, w1, w2, 8, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmax_, nullptr,
@@ -958,7 +957,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         // fast_kind: the fused fast scan ran (the only kernel with the retry indirection)
         const bool fast_kind = cfg_.scan_variant == 0 && (m_ == 16 || m_ == 8 || m_ == 4) && w2 <= 4096 &&
                                keep <= 512;
-        if (!fast_kind || !launch_scan_fast(a, nt, w2, keep, slots, cfg_.scan_ea != 0, st))
+        if (!fast_kind || !launch_scan_fast(a, nt, w2, keep, slots, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
         launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
@@ -979,7 +978,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             r.cand = cand2_.p;
             r.qlist = qlist_.p;
             r.qcount = err_.p + 2;
-            launch_scan_fast(r, nt, w2, keep2, slots, cfg_.scan_ea != 0, st);
+            launch_scan_fast(r, nt, w2, keep2, slots, st);
             launch_rescore(r, nt, keep2, topk, d_ids, d_dists, st);
             CUDA_CHECK(cudaMemsetAsync(cnt2_.p, 0, 4, st));
             launch_compact_flags(meta_.p, nt, qlist2_.p, cnt2_.p, st);
@@ -1022,7 +1021,6 @@ uint32_t Engine::scan_keep(uint32_t topk) const {
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
-    else if (key == "scan_ea") cfg_.scan_ea = (int)value;
     else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;
     else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;
     else if (key == "force_exact") cfg_.force_exact = (int)value;

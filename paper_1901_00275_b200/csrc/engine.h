@@ -38,7 +38,6 @@ struct EngineConfig {
                            // 0 = auto: 6 (3 CTAs/SM), or 104 on shards of >= 4 (1/4 or less of the
                            // entries per query: measured 3% faster at 8 shards, neutral unsharded)
     float cert_slack = 0.0f;  // test knob (cert_slack_milli): widens the re-score certificate -> retry / exact paths
-    int scan_ea = 0;       // fast scan: early abandon of the second half of the LUT lookups (exact; scan_fast.cu)
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)

@@ -15,13 +15,7 @@
 // candidate buffer; at round boundaries the buffer is cut to the k' smallest
 // keys by a block radix select and the threshold tightens.  No candidate list
 // reaches HBM; ids are read only for the k' survivors (k_rescore).
-//
-// EA (early abandon): after the first M/2 lookups the distance is bounded
-// below by (term1 + e) - 2 (s_half + sum of the remaining sub-spaces' table
-// maxima) minus a relative rounding slack; when every lane's pair is above
-// the threshold the second half of the lookups is skipped -- those entries
-// would be rejected by the threshold test anyway, so the survivors (and the
-// result) are unchanged while the LUT wavefronts, the scan's limiter, shrink.
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -199,7 +193,7 @@ __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an ord
     return __uint_as_float((ub & 0x80000000u) ? (ub & 0x7fffffffu) : ~ub);
 }
 
-template <int M, int U, int MINB, bool EA>
+template <int M, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -217,33 +211,10 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     __shared__ unsigned int s_misc[48];
     __shared__ unsigned int s_count;
     __shared__ unsigned long long s_tau;
-    __shared__ float s_pmax[M];
 
     // 1. the query's term5 table (one copy per sub-space)
     const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
     for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
-    // early abandon: per sub-space maxima of the table, so that after the
-    // first M/2 lookups  sum5 <= s_half + sum_{p >= M/2} max_j LUT[p][j]
-    float2 rest2 = make_float2(0.f, 0.f), slack2 = rest2;
-    if constexpr (EA) {
-        __syncthreads();
-        for (uint32_t p = warp; p < (uint32_t)M; p += nwarps) {
-            const float* t = reinterpret_cast<const float*>(lut) + p * 256;
-            float mx = -__int_as_float(0x7f800000);
-            for (uint32_t j = lane; j < 256; j += 32) mx = fmaxf(mx, t[j]);
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            if (lane == 0) s_pmax[p] = mx;
-        }
-        __syncthreads();
-        float rest = 0.0f, rabs = 0.0f;
-#pragma unroll
-        for (int p = M / 2; p < M; p++) {
-            rest += s_pmax[p];
-            rabs += fabsf(s_pmax[p]);
-        }
-        rest2 = make_float2(rest, rest);
-        slack2 = make_float2(rabs, rabs);
-    }
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
     {
@@ -364,25 +335,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                     const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
                     float2 s = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
 #pragma unroll
-                    for (int p = 1; p < M / 2; p++)
-                        s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
-                    if constexpr (EA) {
-                        // lower bound of the final distance from the first half:
-                        // fl is monotone, so sum5 <= s + rest (+ rounding, inside
-                        // the relative slack); skip the second half of the
-                        // lookups when the whole warp's pairs are above the threshold
-                        const float2 ub = __fadd2_rn(s, rest2);
-                        const float2 lb = __ffma2_rn(m2, ub, te);
-                        const float2 mag = __ffma2_rn(make_float2(2.f, 2.f), __fadd2_rn(make_float2(fabsf(s.x), fabsf(s.y)), slack2),
-                                                      make_float2(fabsf(te.x), fabsf(te.y)));
-                        const bool above = lb.x - 1e-5f * mag.x > taud && lb.y - 1e-5f * mag.y > taud;
-                        if (__all_sync(0xffffffffu, above)) {
-                            dist[u] = dist[u + 1] = __int_as_float(0x7f800000);
-                            continue;
-                        }
-                    }
-#pragma unroll
-                    for (int p = M / 2; p < M; p++)
+                    for (int p = 1; p < M; p++)
                         s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
                     const float2 d = __ffma2_rn(m2, s, te);
                     dist[u] = d.x;
@@ -479,18 +432,16 @@ void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t 
 }
 
 template <int M>
-static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, bool ea,
-                         cudaStream_t st) {
+static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
     // block-shared candidate buffer (keys): 2048 unless the scan_cap knob says otherwise
     const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 2048u, 4 * keep);
     const size_t smem = 4 * 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
     // su: slots per lane (4 / 6 / 8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
-    auto fn = ea ? (su == 104 ? dev::k_scan_fast2<M, 4, 4, true> : dev::k_scan_fast2<M, 6, 3, true>)
-                 : (su == 4 ? dev::k_scan_fast2<M, 4, 3, false>
-                    : su == 8 ? dev::k_scan_fast2<M, 8, 3, false>
-                    : su == 104 ? dev::k_scan_fast2<M, 4, 4, false>
-                    : su == 106 ? dev::k_scan_fast2<M, 6, 4, false>
-                                : dev::k_scan_fast2<M, 6, 3, false>);
+    auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
+              : su == 8 ? dev::k_scan_fast2<M, 8, 3>
+              : su == 104 ? dev::k_scan_fast2<M, 4, 4>
+              : su == 106 ? dev::k_scan_fast2<M, 6, 4>
+                          : dev::k_scan_fast2<M, 6, 3>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
@@ -499,13 +450,12 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
 // The fused fast scan for m in {4, 8, 16} on the packed e-term | lambda stream
 // (or the separate arrays); false when it does not apply (other m, w2 > 4096,
 // k' > 512): the engine then runs the generic warp-buffer scan.
-bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int slots, bool early_abandon,
-                      cudaStream_t st) {
+bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int slots, cudaStream_t st) {
     if (keep > 512 || w2 > 4096) return false;
     switch (a.m) {
-        case 16: launch_fast2<16>(a, nq, w2, keep, slots, early_abandon, st); return true;
-        case 8: launch_fast2<8>(a, nq, w2, keep, slots, early_abandon, st); return true;
-        case 4: launch_fast2<4>(a, nq, w2, keep, slots, early_abandon, st); return true;
+        case 16: launch_fast2<16>(a, nq, w2, keep, slots, st); return true;
+        case 8: launch_fast2<8>(a, nq, w2, keep, slots, st); return true;
+        case 4: launch_fast2<4>(a, nq, w2, keep, slots, st); return true;
         default: return false;
     }
 }

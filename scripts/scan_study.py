@@ -5,7 +5,7 @@ Builds the workload's index once (as bench.py does), then for every
 configuration times `--steps` batched searches with per-phase CUDA events and
 checks that the results equal the first configuration's bit for bit.
 
-  python scripts/scan_study.py --workload c4 --configs "scan_ea=0" "scan_ea=1,scan_slots=104"
+  python scripts/scan_study.py --workload c4 --configs "scan_slots=6" "scan_slots=104"
 """
 import argparse
 import json
@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--w1", type=int, default=64)
     ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--k", type=int, default=100)
-    ap.add_argument("--configs", nargs="+", default=["scan_ea=0"])
+    ap.add_argument("--configs", nargs="+", default=["scan_slots=0"])
     ap.add_argument("--hubs", action="store_true", help="region-visit skew: bytes of the hottest regions vs reads")
     args = ap.parse_args()
     import torch

@@ -128,12 +128,12 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
     # persistent / per-row-block coarse grids, 1xTF32 first pass, scan variants
     variants = [dict(tc_persist=1), dict(tc_persist=0), dict(tc_pass1_single=1),
                 dict(tc_pass1_single=1, tc_persist=0), dict(tc_chunk_select=0), dict(tc_chunk_select=0, tc_persist=0),
-                dict(scan_packed=0), dict(scan_ea=1), dict(scan_ea=1, scan_slots=104), dict(scan_slots=8),
+                dict(scan_packed=0), dict(scan_slots=104), dict(scan_slots=4), dict(scan_slots=8),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1, tc_persist=0),
                 dict(cert_slack_milli=10**6, scan_retry=0), dict(cert_slack_milli=10**6)]
     for v in variants:
-        knobs = dict(tc_persist=1, tc_pass1_single=0, tc_chunk_select=1, scan_slots=0, scan_packed=1, scan_ea=0,
+        knobs = dict(tc_persist=1, tc_pass1_single=0, tc_chunk_select=1, scan_slots=0, scan_packed=1,
                      tc_pass2_single=0, scan_retry=1, cert_slack_milli=0)
         knobs.update(v)
         for key, val in knobs.items():
