@@ -4,7 +4,7 @@
 //   k_coarse_tc<4> (TILEMIN8)  approx(y, c) = |c|^2 - 2 <y, c> on TF32 operands;
 //                              per query the minimum of every 8-centroid chunk
 //                              (tmin [nq, K/8]); no K-wide row in HBM
-//   k_chunk_select             tau = the w1-th smallest chunk minimum,
+//   k_chunk_select             tau >= the w1-th smallest chunk minimum (histogram),
 //                              T = tau + 2.02 eps (eps = tc_eps, the TF32 bound);
 //                              compacts the chunks with minimum <= T
 //   k_select_fused             exact reference-order sqdist of every centroid in
@@ -43,30 +43,89 @@ constexpr uint32_t FS_BUF_FLOATS = 32 * FS_RS;  // one piece of 32 rows
 constexpr uint32_t FS_MAX_KEYS = 2048; // exactly evaluated chunk centroids per query
 constexpr uint32_t FS_CS = 8;          // centroids per chunk (TILEMIN8)
 
-// tau / T per query and the compacted list of selected chunks.
+// tau / T per query and the compacted list of selected chunks.  tau is an
+// upper bound on the L-th smallest chunk minimum, found with ONE histogram
+// pass over the row's value range: 2048 equal-width bins between the row's
+// minimum and maximum (a monotone binning), the bin b where the cumulative
+// count reaches L, and tau = the largest value in bin b -- at least the L-th
+// smallest value, and within one bin width (~range / 2048) of it.  (A radix
+// select on the float bits put every value of a row into a handful of
+// first-pass bins -- same exponent -- and serialised on their atomics.)
 __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
                                                       const float* __restrict__ Y, uint32_t dim, float cmax,
                                                       uint32_t capc, uint32_t* __restrict__ clist,
                                                       uint32_t* __restrict__ ccnt, float* __restrict__ Tout) {
-    __shared__ uint32_t hist[2048];
+    constexpr uint32_t NB = 2048;
+    __shared__ uint32_t hist[NB];
     __shared__ uint32_t scan[40];
     __shared__ float s_T;
-    __shared__ unsigned int s_cnt;
+    __shared__ unsigned int s_mn, s_mx, s_cnt, s_bin, s_tau;
     const uint64_t q = blockIdx.x;
     const float* row = tmin + q * nchunk;
-    uint32_t r;
-    const uint32_t key = block_kth_ord(row, nchunk, min(L, nchunk), hist, scan, &r);
-    if (threadIdx.x == 0) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u;
+    for (uint32_t b = tid; b < NB; b += nt) hist[b] = 0;
+    // row min / max over the finite values (padded centroids give +inf)
+    float mn = __int_as_float(0x7f800000), mx = -mn;
+    for (uint32_t i = tid; i < nchunk; i += nt) {
+        const float v = row[i];
+        mn = fminf(mn, v);
+        if (v < __int_as_float(0x7f800000)) mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (tid == 0) {
+        s_mn = 0xffffffffu;  // order-preserving keys (approx values are |c|^2 - 2 <y, c>: often negative)
+        s_mx = 0u;
+        s_cnt = 0;
+        s_tau = 0u;
+    }
+    __syncthreads();
+    if (lane == 0) {
+        atomicMin(&s_mn, ord_float(mn));
+        atomicMax(&s_mx, ord_float(mx));
+    }
+    __syncthreads();
+    const float lo = unord_float(s_mn), hi = fmaxf(unord_float(s_mx), lo);
+    const float inv = hi > lo ? (float)(NB - 1) / (hi - lo) : 0.0f;
+    auto bin_of = [&](float v) -> uint32_t {
+        const float x = (fmaxf(v, lo) - lo) * inv;  // monotone in v; +inf -> the last bin (NaN-free: inv finite)
+        return x < (float)(NB - 1) ? (uint32_t)x : NB - 1;  // NaN (inf * 0) -> the last bin
+    };
+    for (uint32_t i = tid; i < nchunk; i += nt) atomicAdd(&hist[bin_of(row[i])], 1u);
+    __syncthreads();
+    {
+        const uint32_t per = (NB + nt - 1) / nt;
+        uint32_t local = 0;
+        for (uint32_t b = tid * per; b < min(NB, (tid + 1) * per); b++) local += hist[b];
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, scan, &total);
+        const uint32_t Lc = min(L, nchunk);
+        for (uint32_t b = tid * per; b < min(NB, (tid + 1) * per); b++) {
+            if (run < Lc && Lc <= run + hist[b]) s_bin = b;
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+    const uint32_t bsel = s_bin;
+    uint32_t tmax = 0u;  // the largest value in the crossing bin (>= the L-th smallest), order-preserving
+    for (uint32_t i = tid; i < nchunk; i += nt) {
+        const float v = row[i];
+        if (bin_of(v) == bsel) tmax = max(tmax, ord_float(v));
+    }
+    for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    if (lane == 0) atomicMax(&s_tau, tmax);
+    __syncthreads();
+    if (tid == 0) {
         float yn = 0.0f;
         for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
-        s_T = unord_float(key) + 2.02f * tc_eps(yn, cmax, dim, false);
-        s_cnt = 0;
+        s_T = unord_float(s_tau) + 2.02f * tc_eps(yn, cmax, dim, false);
     }
     __syncthreads();
     const float T = s_T;
-    const uint32_t lane = threadIdx.x & 31u;
-    for (uint32_t base = 0; base < nchunk; base += blockDim.x) {
-        const uint32_t i = base + threadIdx.x;
+    for (uint32_t base = 0; base < nchunk; base += nt) {
+        const uint32_t i = base + tid;
         const bool take = i < nchunk && row[i] <= T;
         const uint32_t bal = __ballot_sync(0xffffffffu, take);
         uint32_t slot0 = 0;
@@ -78,7 +137,7 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         ccnt[q] = s_cnt;
         Tout[q] = T;
     }
