@@ -160,6 +160,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
                 *reinterpret_cast<float4*>(sA + off) = hi;
                 *reinterpret_cast<float4*>(sAlo + off) = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+            } else if constexpr (MODE == 4) {  // the chunk-select bound assumes TF32-exact (RNA) operands
+                *reinterpret_cast<float4*>(sA + off) =
+                    make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
             } else {
                 *reinterpret_cast<float4*>(sA + off) = v;
             }
@@ -418,8 +421,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // Re-lay centroids [K, D] row-major into the UMMA interleaved K-major tile
 // layout, padding rows to a multiple of 128 (zero rows, +inf norms).
+// rna: store tf32_rna(x) (round to nearest; the MMA then sees exact TF32
+// operands, <= 2^-11 relative each, instead of truncating them, <= 2^-10)
 __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, uint32_t dim, uint32_t ntiles,
-                                     float* __restrict__ out, float* __restrict__ out_lo, float* __restrict__ norm_out) {
+                                     float* __restrict__ out, float* __restrict__ out_lo, float* __restrict__ norm_out,
+                                     int rna) {
     const uint32_t nchunk = dim / 4;
     const uint64_t total = (uint64_t)ntiles * TC_N * nchunk;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
@@ -429,7 +435,8 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (row < k) v = reinterpret_cast<const float4*>(C + row * dim)[c];
         const uint64_t off = (uint64_t)tile * TC_N * dim + (r >> 3) * (nchunk * 32) + c * 32 + (r & 7) * 4;
-        *reinterpret_cast<float4*>(out + off) = v;
+        *reinterpret_cast<float4*>(out + off) =
+            rna ? make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w)) : v;
         if (out_lo) {  // 3xTF32 split of the centroids (hi stays in `out` unrounded: the MMA truncates)
             const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
             *reinterpret_cast<float4*>(out + off) = hi;
@@ -502,9 +509,9 @@ bool coarse_tc_supported(uint32_t dim) { return coarse_tc_fits(dim, false); }
 bool coarse_tc_split_supported(uint32_t dim) { return coarse_tc_fits(dim, true); }
 
 void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
-                               cudaStream_t st) {
+                               cudaStream_t st, int rna) {
     const uint32_t ntiles = (k + dev::TC_N - 1) / dev::TC_N;
-    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, out_lo, norm_out);
+    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, out_lo, norm_out, rna);
     CUDA_LAUNCH_CHECK();
 }
 

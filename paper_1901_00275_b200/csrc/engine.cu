@@ -202,7 +202,9 @@ void Engine::upload_model() {
         const uint32_t ntiles = (k_ + 127) / 128;
         cent_tc_.alloc((size_t)ntiles * 128 * dim_);
         cnorm_tc_.alloc((size_t)ntiles * 128);
-        launch_relayout_centroids(centroids_.p, k_, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, stream_);
+        // TF32-rounded (RNA) centroids: exact MMA operands (the chunk-select bound
+        // relies on it; the add path's truncation bound covers them as well)
+        launch_relayout_centroids(centroids_.p, k_, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, stream_, /*rna=*/1);
         // 3xTF32 split copy for the search coarse stage (hi/lo halves)
         tc_split_ = coarse_tc_split_supported(dim_);
         if (tc_split_) {
@@ -819,7 +821,7 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         if (cfg_.tc_persist) {
             const uint64_t rows = ((nt + 127) / 128) * 128;
             if (!xtc1_.p || xtc1_.n < rows * dim_) xtc1_.alloc(rows * dim_);
-            launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st);
+            launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st, /*rna=*/1);
             x1 = xtc1_.p;
             launches += 1;
         }

@@ -144,7 +144,7 @@ void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, 
                          uint32_t* sel_out, float* ab_out, cudaStream_t st);
 bool coarse_tc_split_supported(uint32_t dim);
 void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
-                               cudaStream_t st);
+                               cudaStream_t st, int rna = 0);
 void launch_relayout_khalf(const float* C, uint32_t k, uint32_t dim, float* out_hi, float* out_lo, cudaStream_t st);
 void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
                       const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,

@@ -50,7 +50,8 @@ constexpr uint32_t FS_CS = 8;          // centroids per chunk (TILEMIN8)
 // count reaches L, and tau = the largest value in bin b -- at least the L-th
 // smallest value, and within one bin width (~range / 2048) of it.  (A radix
 // select on the float bits put every value of a row into a handful of
-// first-pass bins -- same exponent -- and serialised on their atomics.)
+// first-pass bins -- same exponent -- and serialised on their atomics.)  The
+// list is compacted in ascending chunk order.
 __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
                                                       const float* __restrict__ Y, uint32_t dim, float cmax,
                                                       uint32_t capc, uint32_t* __restrict__ clist,
@@ -120,22 +121,20 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
     if (tid == 0) {
         float yn = 0.0f;
         for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
-        s_T = unord_float(s_tau) + 2.02f * tc_eps(yn, cmax, dim, false);
+        s_T = unord_float(s_tau) + 2.02f * tc_eps(yn, cmax, dim, false, /*rna=*/true);
     }
     __syncthreads();
     const float T = s_T;
-    for (uint32_t base = 0; base < nchunk; base += nt) {
-        const uint32_t i = base + tid;
-        const bool take = i < nchunk && row[i] <= T;
-        const uint32_t bal = __ballot_sync(0xffffffffu, take);
-        uint32_t slot0 = 0;
-        if (lane == 0 && bal) slot0 = atomicAdd(&s_cnt, (unsigned)__popc(bal));
-        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-        if (take) {
-            const uint32_t slot = slot0 + __popc(bal & ((1u << lane) - 1u));
-            if (slot < capc) clist[q * capc + slot] = i;
-        }
-    }
+    // ordered compaction (ascending chunk ids): contiguous ranges per thread
+    const uint32_t per = (nchunk + nt - 1) / nt;
+    const uint32_t b0 = min(nchunk, tid * per), b1 = min(nchunk, b0 + per);
+    uint32_t mine = 0;
+    for (uint32_t i = b0; i < b1; i++) mine += row[i] <= T ? 1u : 0u;
+    uint32_t total;
+    uint32_t slot = block_excl_scan_u32(mine, scan, &total);
+    for (uint32_t i = b0; i < b1 && slot < capc; i++)
+        if (row[i] <= T) clist[q * capc + slot++] = i;
+    if (tid == 0) s_cnt = total;
     __syncthreads();
     if (tid == 0) {
         ccnt[q] = s_cnt;
@@ -276,9 +275,9 @@ struct FusedLayout {
         ys = 0;
         topS = ys + dimp * 4;
         u = (topS + w1 * 4 + 15) & ~15u;
-        // phase 1: sorted chunk list (u64, pow2) + chunk-centroid distances + top positions;
+        // phase 1: chunk list + chunk-centroid distances + top positions;
         // phase 2: bitmap (u32), word prefix (u16), needed values, needed ids / edge distances, positions
-        const uint32_t p1 = fs_pow2(capc) * 8 + FS_MAX_KEYS * 4 + w1 * 4;
+        const uint32_t p1 = capc * 4 + FS_MAX_KEYS * 4 + w1 * 4;
         const uint32_t p2 = nw * 4 + ((nw * 2 + 3) & ~3u) + nn * 4 + (nn > ne ? nn : ne) * 4 + w2 * 4;
         bufs = (u + (p1 > p2 ? p1 : p2) + 15) & ~15u;
         // per-warp row-piece double buffers; the selects' histogram (2048 + 40
@@ -324,16 +323,14 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
             if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
             return;
         }
-        // chunk list sorted ascending, so position order == centroid id order
-        uint64_t* cls = reinterpret_cast<uint64_t*>(smem + lay.u);
-        const uint32_t npc = fs_pow2(nc);
-        float* vals = reinterpret_cast<float*>(cls + fs_pow2(f.capc));
+        // the chunk list is ascending, so position order == centroid id order
+        uint32_t* cls = reinterpret_cast<uint32_t*>(smem + lay.u);
+        float* vals = reinterpret_cast<float*>(cls + f.capc);
         uint32_t* topPos = reinterpret_cast<uint32_t*>(vals + FS_MAX_KEYS);
-        for (uint32_t t = tid; t < npc; t += nt) cls[t] = t < nc ? (uint64_t)f.clist[q * f.capc + t] : ~0ull;
+        for (uint32_t t = tid; t < nc; t += nt) cls[t] = f.clist[q * f.capc + t];
         __syncthreads();
-        bitonic_sort_u64<false>(cls, npc, tid, nt);
         exact_rows_pipe(a.centroids, k, dim, ys, wbuf, ncent,
-                        [&](uint32_t t) { return (uint32_t)cls[t / cs] * cs + (t & (cs - 1)); },
+                        [&](uint32_t t) { return cls[t / cs] * cs + (t & (cs - 1)); },
                         [&](uint32_t t, float v) { vals[t] = v; });
         if (tid == 0) {
             float yn = 0.0f;
@@ -347,14 +344,14 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         float mx = 0.0f;
         for (uint32_t r = tid; r < w1; r += nt) {
             const uint32_t pos = topPos[r];
-            topS[r] = (uint32_t)cls[pos / cs] * cs + (pos & (cs - 1));
+            topS[r] = cls[pos / cs] * cs + (pos & (cs - 1));
             mx = fmaxf(mx, vals[pos]);  // +inf (a padded id) fails the certificate below
         }
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if ((tid & 31) == 0) atomicMax(&s_w1max, __float_as_uint(mx));  // distances >= 0
         __syncthreads();
         const float exact_w1 = __uint_as_float(s_w1max);
-        const float eps = tc_eps(s_yn, f.cmax, dim, false);
+        const float eps = tc_eps(s_yn, f.cmax, dim, false, /*rna=*/true);
         const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
         if (!(lower > (double)exact_w1)) {
             if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
