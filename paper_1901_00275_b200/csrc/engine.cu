@@ -814,7 +814,8 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     // chunk-select path (select_fused.cu): one 1xTF32 pass of 8-centroid chunk
     // minima, the chunks within the TF32 bound of the w1-th smallest, exact
     // evaluation + first and second level fused per query
-    if (w2 > 0 && tc_ && cfg_.tc_chunk_select && k_ >= cfg_.tc_search_min_k && w1 < k_ && (k_ + 7) / 8 >= 2 * w1 &&
+    if (w2 > 0 && tc_ && cfg_.tc_chunk_select && k_ >= cfg_.tc_search_min_k && k_ <= 262144 && w1 < k_ &&
+        (k_ + 7) / 8 >= 2 * w1 &&
         select_fused_supported(k_, n_, w1, w2, dim_, cfg_.tc_chunk_cap) && tmin8_.p) {
         const uint32_t nchunk8 = ((k_ + 127) / 128) * 16;
         const float* x1 = nullptr;

@@ -29,6 +29,8 @@
 // exact refine + k_exact_needed writing ~2k exact distances into a K-wide ws
 // row per query): one tensor-core pass instead of two (the 3xTF32 pass issued
 // 3x the MMAs), and the needed exact distances live in shared memory only.
+#include <stdexcept>
+
 #include "async.cuh"
 #include "kernels.h"
 #include "select.cuh"
@@ -51,26 +53,37 @@ constexpr uint32_t FS_CS = 8;          // centroids per chunk (TILEMIN8)
 // smallest value, and within one bin width (~range / 2048) of it.  (A radix
 // select on the float bits put every value of a row into a handful of
 // first-pass bins -- same exponent -- and serialised on their atomics.)  The
-// list is compacted in ascending chunk order.
-__global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
-                                                      const float* __restrict__ Y, uint32_t dim, float cmax,
-                                                      uint32_t capc, uint32_t* __restrict__ clist,
-                                                      uint32_t* __restrict__ ccnt, float* __restrict__ Tout) {
-    constexpr uint32_t NB = 2048;
+// row lives in registers (VPT values per thread, coalesced); the list is
+// compacted in ascending chunk order (ballots per (slot, warp) segment + one
+// block scan over the segment counts).
+template <int VPT, int NT>
+__global__ void __launch_bounds__(NT) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
+                                                     const float* __restrict__ Y, uint32_t dim, float cmax,
+                                                     uint32_t capc, uint32_t* __restrict__ clist,
+                                                     uint32_t* __restrict__ ccnt, float* __restrict__ Tout) {
+    constexpr uint32_t NB = 2048, NWARP = NT / 32;
     __shared__ uint32_t hist[NB];
     __shared__ uint32_t scan[40];
+    __shared__ uint32_t segc[VPT * NWARP];
     __shared__ float s_T;
-    __shared__ unsigned int s_mn, s_mx, s_cnt, s_bin, s_tau;
+    __shared__ unsigned int s_mn, s_mx, s_bin, s_tau;
     const uint64_t q = blockIdx.x;
     const float* row = tmin + q * nchunk;
-    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u;
-    for (uint32_t b = tid; b < NB; b += nt) hist[b] = 0;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const float INF = __int_as_float(0x7f800000);
+    float v[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; j++) {
+        const uint32_t i = j * NT + tid;
+        v[j] = i < nchunk ? row[i] : INF;
+    }
+    for (uint32_t b = tid; b < NB; b += NT) hist[b] = 0;
     // row min / max over the finite values (padded centroids give +inf)
-    float mn = __int_as_float(0x7f800000), mx = -mn;
-    for (uint32_t i = tid; i < nchunk; i += nt) {
-        const float v = row[i];
-        mn = fminf(mn, v);
-        if (v < __int_as_float(0x7f800000)) mx = fmaxf(mx, v);
+    float mn = INF, mx = -INF;
+#pragma unroll
+    for (int j = 0; j < VPT; j++) {
+        mn = fminf(mn, v[j]);
+        if (v[j] < INF) mx = fmaxf(mx, v[j]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -79,7 +92,6 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
     if (tid == 0) {
         s_mn = 0xffffffffu;  // order-preserving keys (approx values are |c|^2 - 2 <y, c>: often negative)
         s_mx = 0u;
-        s_cnt = 0;
         s_tau = 0u;
     }
     __syncthreads();
@@ -90,14 +102,16 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
     __syncthreads();
     const float lo = unord_float(s_mn), hi = fmaxf(unord_float(s_mx), lo);
     const float inv = hi > lo ? (float)(NB - 1) / (hi - lo) : 0.0f;
-    auto bin_of = [&](float v) -> uint32_t {
-        const float x = (fmaxf(v, lo) - lo) * inv;  // monotone in v; +inf -> the last bin (NaN-free: inv finite)
-        return x < (float)(NB - 1) ? (uint32_t)x : NB - 1;  // NaN (inf * 0) -> the last bin
+    auto bin_of = [&](float x) -> uint32_t {
+        const float t = (fmaxf(x, lo) - lo) * inv;  // monotone in x; +inf -> the last bin
+        return t < (float)(NB - 1) ? (uint32_t)t : NB - 1;  // NaN (inf * 0) -> the last bin
     };
-    for (uint32_t i = tid; i < nchunk; i += nt) atomicAdd(&hist[bin_of(row[i])], 1u);
+#pragma unroll
+    for (int j = 0; j < VPT; j++)
+        if (v[j] < INF) atomicAdd(&hist[bin_of(v[j])], 1u);
     __syncthreads();
     {
-        const uint32_t per = (NB + nt - 1) / nt;
+        constexpr uint32_t per = (NB + NT - 1) / NT;
         uint32_t local = 0;
         for (uint32_t b = tid * per; b < min(NB, (tid + 1) * per); b++) local += hist[b];
         uint32_t total;
@@ -111,10 +125,9 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
     __syncthreads();
     const uint32_t bsel = s_bin;
     uint32_t tmax = 0u;  // the largest value in the crossing bin (>= the L-th smallest), order-preserving
-    for (uint32_t i = tid; i < nchunk; i += nt) {
-        const float v = row[i];
-        if (bin_of(v) == bsel) tmax = max(tmax, ord_float(v));
-    }
+#pragma unroll
+    for (int j = 0; j < VPT; j++)
+        if (v[j] < INF && bin_of(v[j]) == bsel) tmax = max(tmax, ord_float(v[j]));
     for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
     if (lane == 0) atomicMax(&s_tau, tmax);
     __syncthreads();
@@ -125,19 +138,28 @@ __global__ void __launch_bounds__(512) k_chunk_select(const float* __restrict__ 
     }
     __syncthreads();
     const float T = s_T;
-    // ordered compaction (ascending chunk ids): contiguous ranges per thread
-    const uint32_t per = (nchunk + nt - 1) / nt;
-    const uint32_t b0 = min(nchunk, tid * per), b1 = min(nchunk, b0 + per);
-    uint32_t mine = 0;
-    for (uint32_t i = b0; i < b1; i++) mine += row[i] <= T ? 1u : 0u;
-    uint32_t total;
-    uint32_t slot = block_excl_scan_u32(mine, scan, &total);
-    for (uint32_t i = b0; i < b1 && slot < capc; i++)
-        if (row[i] <= T) clist[q * capc + slot++] = i;
-    if (tid == 0) s_cnt = total;
+    // ordered compaction: element j * NT + warp * 32 + lane; segment (j, warp)
+    uint32_t bal[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; j++) {
+        bal[j] = __ballot_sync(0xffffffffu, v[j] <= T);
+        if (lane == 0) segc[j * NWARP + warp] = __popc(bal[j]);
+    }
     __syncthreads();
+    uint32_t total;
+    const uint32_t mine = tid < VPT * NWARP ? segc[tid] : 0u;
+    const uint32_t ex = block_excl_scan_u32(mine, scan, &total);
+    if (tid < VPT * NWARP) segc[tid] = ex;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < VPT; j++) {
+        if ((bal[j] >> lane) & 1u) {
+            const uint32_t slot = segc[j * NWARP + warp] + __popc(bal[j] & ((1u << lane) - 1u));
+            if (slot < capc) clist[q * capc + slot] = j * NT + warp * 32 + lane;
+        }
+    }
     if (tid == 0) {
-        ccnt[q] = s_cnt;
+        ccnt[q] = total;
         Tout[q] = T;
     }
 }
@@ -474,7 +496,13 @@ bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, ui
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
                          float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st) {
     if (nq == 0) return;
-    dev::k_chunk_select<<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T);
+    if (nchunk <= 16 * 512)
+        dev::k_chunk_select<16, 512><<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T);
+    else if (nchunk <= 32 * 1024)
+        dev::k_chunk_select<32, 1024><<<(unsigned)nq, 1024, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt,
+                                                                      T);
+    else
+        throw std::runtime_error("chunk_select: K above 262144");
     CUDA_LAUNCH_CHECK();
 }
 
