@@ -118,6 +118,115 @@ __device__ __noinline__ static void block_select_ordered(const float* __restrict
     }
 }
 
+// The same selection (L smallest of vals[0..len) by (value, position), output
+// positions ascending) with far fewer block barriers, for the fused coarse
+// stage's small selections (~10^3 values): min / max, ONE histogram of 1024
+// equal-width bins over [min, max] (a monotone binning, so every value in a
+// lower bin is strictly smaller), the crossing bin b, then the members of bin
+// b ranked exactly by (value, position) (counting, at most 256 of them) and
+// one ordered compaction.  Falls back to block_select_ordered when bin b
+// holds more than 256 values (e.g. massive ties).  Scratch: hist >= 1024 +
+// 256 words, scan[40].  All threads of the block call.
+__device__ __noinline__ static void block_select_ordered_range(const float* __restrict__ vals, uint32_t len,
+                                                               uint32_t L, uint32_t* __restrict__ out,
+                                                               uint32_t* hist, uint32_t* scan) {
+    constexpr uint32_t NB = 1024, MAXB = 256;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u;
+    if (L >= len) {
+        for (uint32_t i = tid; i < len; i += nt) out[i] = i;
+        return;
+    }
+    uint32_t* memb = hist + NB;  // crossing-bin members (positions), then their ranks
+    const float INF = __int_as_float(0x7f800000);
+    float mn = INF, mx = -INF;
+    for (uint32_t i = tid; i < len; i += nt) {
+        const float v = vals[i];
+        mn = fminf(mn, v);
+        if (v < INF) mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    for (uint32_t b = tid; b < NB; b += nt) hist[b] = 0;
+    if (tid == 0) {
+        scan[36] = 0xffffffffu;
+        scan[37] = 0u;
+        scan[38] = 0u;
+    }
+    __syncthreads();
+    if (lane == 0) {
+        atomicMin(&scan[36], ord_float(mn));
+        atomicMax(&scan[37], ord_float(mx));
+    }
+    __syncthreads();
+    const float lo = unord_float(scan[36]), hi = fmaxf(unord_float(scan[37]), lo);
+    const float inv = hi > lo ? (float)(NB - 1) / (hi - lo) : 0.0f;
+    auto bin_of = [&](float x) -> uint32_t {
+        const float t = (fmaxf(x, lo) - lo) * inv;  // monotone in x
+        return t < (float)(NB - 1) ? (uint32_t)t : NB - 1;  // +inf / NaN -> the last bin
+    };
+    for (uint32_t i = tid; i < len; i += nt) atomicAdd(&hist[bin_of(vals[i])], 1u);
+    __syncthreads();
+    const uint32_t per = (NB + nt - 1) / nt;
+    {
+        uint32_t local = 0;
+        for (uint32_t b = tid * per; b < min(NB, (tid + 1) * per); b++) local += hist[b];
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, scan, &total);
+        for (uint32_t b = tid * per; b < min(NB, (tid + 1) * per); b++) {
+            if (run < L && L <= run + hist[b]) {
+                scan[34] = b;
+                scan[35] = run;
+            }
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+    const uint32_t bsel = scan[34], before = scan[35], hb = hist[bsel];
+    if (hb > min(MAXB, nt)) {  // block-uniform
+        __syncthreads();
+        block_select_ordered(vals, len, L, out, hist, scan);
+        return;
+    }
+    const uint32_t r = L - before;  // members of bin b to take, by (value, position)
+    for (uint32_t i = tid; i < len; i += nt)
+        if (bin_of(vals[i]) == bsel) memb[atomicAdd(&scan[38], 1u)] = i;
+    __syncthreads();
+    // rank of member t among the members by (value, position); taken iff rank < r
+    uint32_t take_pos = 0xffffffffu;
+    if (tid < hb) {
+        const uint32_t pi = memb[tid];
+        const uint32_t ki = ord_float(vals[pi]);
+        uint32_t rank = 0;
+        for (uint32_t u = 0; u < hb; u++) {
+            const uint32_t pu = memb[u];
+            const uint32_t ku = ord_float(vals[pu]);
+            rank += (ku < ki || (ku == ki && pu < pi)) ? 1u : 0u;
+        }
+        if (rank < r) take_pos = pi;
+    }
+    __syncthreads();
+    if (tid < hb) memb[tid] = take_pos;  // the taken members' positions (others: ~0)
+    __syncthreads();
+    // ordered compaction: contiguous position ranges per thread
+    const uint32_t pp = (len + nt - 1) / nt;
+    const uint32_t i0 = min(len, tid * pp), i1 = min(len, i0 + pp);
+    auto taken = [&](uint32_t i) -> bool {
+        const uint32_t b = bin_of(vals[i]);
+        if (b != bsel) return b < bsel;
+        for (uint32_t u = 0; u < hb; u++)
+            if (memb[u] == i) return true;
+        return false;
+    };
+    uint32_t mine = 0;
+    for (uint32_t i = i0; i < i1; i++) mine += taken(i) ? 1u : 0u;
+    uint32_t total;
+    uint32_t slot = block_excl_scan_u32(mine, scan, &total);
+    for (uint32_t i = i0; i < i1; i++)
+        if (taken(i)) out[slot++] = i;
+}
+
 // In-shared-memory bitonic sort (ascending) of n = power of two u64 keys by
 // the calling threads [t0, t0+nthreads).  `sync` is either a warp or block
 // barrier supplied by the caller through the template parameter.

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         }
         __syncthreads();
         // exact top-w1 by (dist, id): positions ascending == ids ascending
-        block_select_ordered(vals, ncent, w1, topPos, hist, scan);
+        block_select_ordered_range(vals, ncent, w1, topPos, hist, scan);
         __syncthreads();
         float mx = 0.0f;
         for (uint32_t r = tid; r < w1; r += nt) {
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         dq[e] = line_sqdist(av, bv, cv, lam);
     }
     __syncthreads();
-    block_select_ordered(dq, total, w2, selpos, hist, scan);
+    block_select_ordered_range(dq, total, w2, selpos, hist, scan);
     __syncthreads();
     // selected cells (ascending id), their (a, b) into the ws row (read by the
     // scan and the exact re-score), the scanned count and the |term1| bound
