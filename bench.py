@@ -372,18 +372,22 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    multi = os.environ.get("VLQ_MULTI", "group")  # group: one process drives N GPUs; procs: one process per GPU
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (multi == "procs" or args.impl == "reference"):
         # one process per GPU: re-launch this command under torch.distributed.run
         sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world != args.gpus:
+    if world > 1 and world != args.gpus:
         raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.ref_setup:
         ref_setup(args)
         return
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+        return
+    if args.gpus > 1 and multi == "group":
+        run_group(args, rank, world)
         return
 
     import torch
@@ -678,6 +682,121 @@ def main():
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
             "fallback_queries_per_step": stats["flagged"] / args.steps,
             "tc_coarse_fallbacks_per_step": stats["tc_fallbacks"] / args.steps}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_group(args, rank, world):
+    """N > 1: the index sharded over N GPUs of this box behind ONE process
+    (vlqadc.IndexGroup = the C-ABI vlq_group, csrc/group.cu): engine g on GPU g
+    holds the lists c with shard_of_cell(c, N) == g; each step runs the
+    query-split selection, the sharded scan reading the selections over NVLink
+    peer memory and the per-slice merge of the shards' top-k from peer memory.
+    Under torchrun (the driver's launch) rank 0 drives all N GPUs and the other
+    ranks only wait; the step time is the device time of the batch, max over
+    the GPUs (CUDA events on every GPU's stream)."""
+    import torch
+    import torch.distributed as dist
+    N = args.gpus
+    if world > 1:
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()  # rank 0 has finished
+            dist.destroy_process_group()
+            return
+    # VLQ_GROUP_DEVICES="0,0": the single-GPU rehearsal (N shard engines on one GPU)
+    devices = [int(x) for x in os.environ.get("VLQ_GROUP_DEVICES", ",".join(map(str, range(N)))).split(",")]
+    if len(devices) != N:
+        raise SystemExit(f"bench: --gpus {N} but VLQ_GROUP_DEVICES lists {len(devices)} devices")
+    if torch.cuda.device_count() <= max(devices):
+        raise SystemExit(f"bench: --gpus {N} but {torch.cuda.device_count()} visible GPUs")
+    udev = sorted(set(devices))
+    from paper_1901_00275_b200 import vlqadc
+    w = WORKLOADS[args.workload]
+    cfg = config_of(args, w, N)
+    cfg["parallelism"] = f"list-sharded x{N} (hashed cells), one process driving {N} GPUs (vlq_group, NVLink P2P)"
+    if os.environ.get("VLQ_GROUP_DEVICES"):
+        cfg["parallelism"] += f"; rehearsal on devices {os.environ['VLQ_GROUP_DEVICES']}"
+    t0 = time.time()
+    sample = torch.empty((w["ntrain"], w["dim"]), dtype=torch.float32, device="cuda:0")
+    vlqadc.gen_synthetic_device(0, w["ntrain"], w["dim"], w["clusters"], SPREAD, BASE_SEED, sample.data_ptr(), device=0)
+    torch.cuda.synchronize(0)
+    trained = vlqadc.Index.train(sample.cpu().numpy(), k=w["k"], n=w["edges"], m=w["m"], iters=10, seed=TRAIN_SEED,
+                                 device=0)
+    model = trained.model()
+    del trained, sample
+    t1 = time.time()
+    grp = vlqadc.IndexGroup.from_model(model, devices)
+    grp.add_synthetic(w["n"], clusters=w["clusters"], spread=SPREAD, seed=BASE_SEED)
+    t2 = time.time()
+    local = grp.local_entries()
+    log(f"[setup] group of {N}: train {t1 - t0:.1f}s, add {w['n']} points {t2 - t1:.1f}s, shards {local}")
+    setup = {"train_s": round(t1 - t0, 2), "add_s": round(t2 - t1, 2), "train_points": w["ntrain"],
+             "model_sha256_16": model_digest(model), "shard_entries": local}
+    qh = make_queries(vlqadc, w, args.nq, 0).cpu().numpy()
+    nq, k = args.nq, args.k
+    flush = [torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{g}") for g in udev]
+    grp.set_queries(qh)
+    for _ in range(args.warmup):
+        grp.search_resident(args.w1, args.alpha, k)
+    grp.set_profiling(True)
+    for g in range(N):
+        grp.stats(g, reset=True)
+    ms_steps = []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            for f in flush:
+                f.zero_()
+            for g in udev:
+                torch.cuda.synchronize(g)
+            ms_steps.append(grp.search_resident(args.w1, args.alpha, k))
+    stats = [grp.stats(g) for g in range(N)]
+    grp.set_profiling(False)
+    ms = sum(ms_steps)
+    value = nq * args.steps / (ms / 1e3)
+    res_ids, res_d, scanned = grp.results()
+    # e2e through the public API: host queries in, merged host results out
+    grp.search(qh, w1=args.w1, alpha=args.alpha, k=k)
+    per = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        e_ids, e_d = grp.search(qh, w1=args.w1, alpha=args.alpha, k=k)
+        per.append(time.perf_counter() - t)
+    assert np.array_equal(e_ids, res_ids)
+    e2e = {"value": round(nq * args.steps / sum(per), 1), "unit": "queries/s", "h2d_bytes_per_step": int(qh.nbytes * N),
+           "d2h_bytes_per_step": int(nq * k * 12), "api": "paper_1901_00275_b200.vlqadc.IndexGroup.search (numpy in/out)",
+           "ms_per_call": [round(1e3 * x, 2) for x in per]}
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    scan_bytes = int(scanned.sum()) * (w["m"] + 5)
+    scan_ms = [st["phase_ms"]["scan"] / args.steps for st in stats]
+    # per GPU: its share of the algorithmic bytes over its own scan time; the
+    # line reports the slowest GPU's rate (the one that sets the step)
+    shard_bytes = [scan_bytes * local[g] / max(1, sum(local)) for g in range(N)]
+    rates = [shard_bytes[g] / (scan_ms[g] / 1e3) / 1e9 if scan_ms[g] > 0 else 0.0 for g in range(N)]
+    gslow = int(np.argmax(scan_ms))
+    roofline = {"bound": "hbm", "kernel": "k_scan_fast2 (fused list scan + top-k'), per GPU",
+                "achieved": round(rates[gslow], 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(rates[gslow] / hbm, 4) if rates[gslow] else None, "traffic": None,
+                "per_gpu_achieved": [round(r, 1) for r in rates],
+                "per_gpu_scan_ms": [round(x, 4) for x in scan_ms],
+                "algorithmic_bytes_per_step": scan_bytes,
+                "note": "shard bytes estimated as the batch's algorithmic bytes x the shard's share of the entries",
+                "phase_ms_per_step_gpu0": {p: round(v / args.steps, 4) for p, v in stats[0]["phase_ms"].items()},
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650"}
+    ngt = min(args.gt_queries or w.get("gt_queries", 1000), nq)
+    gt = vlqadc.brute_force_gt_synthetic(w["n"], w["dim"], w["clusters"], SPREAD, BASE_SEED, qh[:ngt], 1, device=0)
+    recall = {f"recall@{r}": round(recall_at(res_ids[:ngt], gt, r), 4) for r in (1, 10, 100) if r <= k}
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (exact reference order) + u8 codes",
+            "data": "synthetic", "config": cfg, "recall": recall, "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": None, "gpu_launches": sum(st["launches"] for st in stats) + 2 * N * args.steps,
+            "timing": "CUDA events on every GPU's stream around each batch, max over the GPUs; L2 flushed on every GPU",
+            "clocks": clocks.summary(), "setup": setup, "scanned_per_query": round(float(scanned.sum()) / nq, 1),
+            "fallback_queries_per_step": sum(st["flagged"] for st in stats) / args.steps}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

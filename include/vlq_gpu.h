@@ -42,6 +42,7 @@ extern "C" {
 #define VLQ_ERR_IO -3        /* file error (open / truncated / bad magic) */
 
 typedef struct vlq_engine vlq_engine;
+typedef struct vlq_group vlq_group;
 
 typedef struct {
     int device;                /* CUDA ordinal */
@@ -260,6 +261,46 @@ int vlq_brute_force_gt(int device, const float* base, uint64_t nb, const float* 
 
 /* gen_synthetic (proj/src/dataset.cpp:13-44): identical stream. */
 int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed, float* out);
+
+/* ---- Multi-GPU group: one process, one engine per device ------------------
+ * The paper's multi-GPU search (split the index into b parts, search locally,
+ * join: PAPER.md:498-499) behind one handle: engine g on
+ * devices[g] holds the posting lists c with vlq_shard_of_cell(c, n) == g; the
+ * coarse quantizer is replicated.  Per batch: query-split selection (device g
+ * runs first_level_scan + second_level_rank, search.cpp:11-78, for its slice
+ * of the batch), every device scans its shard for the whole batch reading the
+ * selections from their owners over NVLink peer memory, and device g merges
+ * its slice of the per-shard top-k by (dist, id) from every device's block
+ * (peer loads) -- results equal the single-engine search_batch bit for bit.
+ * Needs peer access between every pair of distinct devices; a device may be
+ * listed more than once.  Calls on one group are serialised internally. */
+int vlq_group_create(const int* devices, uint32_t ndevices, const vlq_config* cfg_or_null, vlq_group** out);
+void vlq_group_destroy(vlq_group* g);
+uint32_t vlq_group_size(vlq_group* g);
+/* Index.load / the model half of Index.train / Index.add for every member */
+int vlq_group_load_vlq1(vlq_group* g, const char* path);
+int vlq_group_set_model(vlq_group* g, uint32_t dim, uint32_t k, uint32_t n, uint32_t m, int clamp_lambda,
+                        float lambda_lo, float lambda_hi, const float* centroids, const uint32_t* neighbor_ids,
+                        const float* edge_sq_len, const float* pq_sub_centroids, const float* t3_or_null);
+int vlq_group_add(vlq_group* g, const float* base, uint64_t n, uint32_t dim);
+int vlq_group_add_synthetic(vlq_group* g, uint64_t n, uint32_t clusters, float spread, uint64_t seed);
+/* Index.search (search_batch, proj/src/search.cpp:169-191) over the group:
+ * host queries in, merged host results out (vlq_engine_search conventions;
+ * out_scanned = the sum over the shards, i.e. the reference's count). */
+int vlq_group_search(vlq_group* g, const float* queries, uint64_t nq, uint32_t dim, uint32_t w1, float alpha,
+                     uint32_t k, int64_t* out_ids, float* out_dists, uint64_t* out_scanned);
+/* Device-resident batch: copy the queries to every device once, run timed
+ * searches (out_ms = device time of the batch, max over the devices), read
+ * the last result. */
+int vlq_group_set_queries(vlq_group* g, const float* queries, uint64_t nq, uint32_t dim);
+int vlq_group_search_resident(vlq_group* g, uint32_t w1, float alpha, uint32_t k, float* out_ms);
+int vlq_group_results(vlq_group* g, int64_t* out_ids, float* out_dists, uint64_t* out_scanned);
+/* Per-phase CUDA-event profile of member `member` (vlq_engine_get_stats
+ * conventions; reset != 0 clears it afterwards). */
+int vlq_group_set_profiling(vlq_group* g, int on);
+int vlq_group_get_stats(vlq_group* g, uint32_t member, vlq_stats* out, int reset);
+/* The info record of member `member` (local_entries: its shard). */
+int vlq_group_info(vlq_group* g, uint32_t member, vlq_info* out);
 
 #ifdef __cplusplus
 }

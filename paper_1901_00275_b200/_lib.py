@@ -72,6 +72,21 @@ _SIGS = {
     "vlq_engine_reset_stats": (c_i32, [c_vp]),
     "vlq_engine_get_lists": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_get_cells": (c_i32, [c_vp, c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
+    "vlq_group_create": (c_i32, [c_vp, c_u32, c_vp, ctypes.POINTER(c_vp)]),
+    "vlq_group_destroy": (None, [c_vp]),
+    "vlq_group_size": (c_u32, [c_vp]),
+    "vlq_group_load_vlq1": (c_i32, [c_vp, ctypes.c_char_p]),
+    "vlq_group_set_model": (c_i32, [c_vp, c_u32, c_u32, c_u32, c_u32, c_i32, c_f32, c_f32, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp]),
+    "vlq_group_add": (c_i32, [c_vp, c_vp, c_u64, c_u32]),
+    "vlq_group_add_synthetic": (c_i32, [c_vp, c_u64, c_u32, c_f32, c_u64]),
+    "vlq_group_search": (c_i32, [c_vp, c_vp, c_u64, c_u32, c_u32, c_f32, c_u32, c_vp, c_vp, c_vp]),
+    "vlq_group_set_queries": (c_i32, [c_vp, c_vp, c_u64, c_u32]),
+    "vlq_group_search_resident": (c_i32, [c_vp, c_u32, c_f32, c_u32, ctypes.POINTER(c_f32)]),
+    "vlq_group_results": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "vlq_group_info": (c_i32, [c_vp, c_u32, ctypes.POINTER(VlqInfo)]),
+    "vlq_group_set_profiling": (c_i32, [c_vp, c_i32]),
+    "vlq_group_get_stats": (c_i32, [c_vp, c_u32, ctypes.POINTER(VlqStats), c_i32]),
     "vlq_engine_get_model": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_encode": (c_i32, [c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "vlq_merge_topk_device": (c_i32, [c_i32, c_vp, c_vp, c_u32, c_u64, c_u32, c_vp, c_vp, c_vp]),

@@ -10,6 +10,7 @@
 
 #include "../../include/vlq_gpu.h"
 #include "engine.h"
+#include "group.h"
 
 // One engine per index.  Every call on an engine takes its mutex, so calls
 // from several host threads are serialised here: the reference's search is
@@ -18,6 +19,12 @@
 // workspace buffers are per-engine state.
 struct vlq_engine {
     vlq::Engine* impl;
+    std::mutex mu;
+};
+
+// A multi-GPU group (group.cu); calls serialised by its own mutex.
+struct vlq_group {
+    vlq::Group* impl;
     std::mutex mu;
 };
 
@@ -451,5 +458,180 @@ int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spr
 uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n) { return vlq::w2_of(w1, alpha, n); }
 
 uint32_t vlq_shard_of_cell(uint32_t cell, uint32_t shards) { return shards ? vlq::shard_of_cell(cell, shards) : 0u; }
+
+
+// ---- multi-GPU group --------------------------------------------------------
+
+int vlq_group_create(const int* devices, uint32_t ndevices, const vlq_config* cfg, vlq_group** out) {
+    if (!out) return fail(VLQ_ERR_INVALID, "vlq_group_create: out is NULL");
+    *out = nullptr;
+    return guarded([&] {
+        if (!devices || ndevices == 0) throw std::runtime_error("vlq_group_create: no devices");
+        vlq::EngineConfig c;
+        if (cfg) {
+            if (cfg->workspace_bytes) c.workspace_bytes = cfg->workspace_bytes;
+            if (cfg->max_tile) c.max_tile = cfg->max_tile;
+            c.force_exact = cfg->force_exact;
+        }
+        std::vector<int> devs(devices, devices + ndevices);
+        auto* g = new vlq_group{nullptr};
+        try {
+            g->impl = new vlq::Group(devs, c);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+void vlq_group_destroy(vlq_group* g) {
+    if (!g) return;
+    try {
+        delete g->impl;
+    } catch (...) {
+    }
+    delete g;
+}
+
+#define GROUP_OR_FAIL(g)                                                        \
+    if (!(g) || !(g)->impl) return fail(VLQ_ERR_INVALID, "group handle is NULL"); \
+    std::lock_guard<std::mutex> lock_((g)->mu)
+
+int vlq_group_load_vlq1(vlq_group* g, const char* path) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        if (!path) throw std::runtime_error("load: path is NULL");
+        g->impl->load_vlq1(path);
+    });
+}
+
+int vlq_group_set_model(vlq_group* g, uint32_t dim, uint32_t k, uint32_t n, uint32_t m, int clamp_lambda,
+                        float lambda_lo, float lambda_hi, const float* centroids, const uint32_t* neighbor_ids,
+                        const float* edge_sq_len, const float* pq_sub_centroids, const float* t3_or_null) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        if (dim == 0 || k == 0 || n == 0 || n >= k || m == 0 || dim % m != 0)
+            throw std::runtime_error("set_model: invalid model header");
+        if (!centroids || !neighbor_ids || !edge_sq_len || !pq_sub_centroids)
+            throw std::runtime_error("set_model: NULL array");
+        vlq::HostModel hm;
+        hm.dim = dim;
+        hm.k = k;
+        hm.n = n;
+        hm.m = m;
+        hm.clamp = clamp_lambda != 0;
+        hm.lo = lambda_lo;
+        hm.hi = lambda_hi;
+        hm.centroids.assign(centroids, centroids + (size_t)k * dim);
+        hm.nbr.assign(neighbor_ids, neighbor_ids + (size_t)k * n);
+        hm.elen.assign(edge_sq_len, edge_sq_len + (size_t)k * n);
+        hm.pq.assign(pq_sub_centroids, pq_sub_centroids + (size_t)m * 256 * (dim / m));
+        if (t3_or_null) hm.t3.assign(t3_or_null, t3_or_null + (size_t)k * m * 256);
+        g->impl->set_model(hm);
+    });
+}
+
+int vlq_group_add(vlq_group* g, const float* base, uint64_t n, uint32_t dim) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        vlq::Engine& e0 = g->impl->engine(0);
+        if (!e0.has_model()) throw std::runtime_error("add: no model loaded");
+        if (dim != e0.dim()) throw std::runtime_error("build_index: dimension mismatch");
+        if (e0.ntotal() != 0) throw std::runtime_error("index already holds a base set");
+        if (n == 0) throw std::runtime_error("build_index: empty base set");
+        if (!base) throw std::runtime_error("add: base is NULL");
+        g->impl->add_host(base, n);
+    });
+}
+
+int vlq_group_add_synthetic(vlq_group* g, uint64_t n, uint32_t clusters, float spread, uint64_t seed) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        vlq::Engine& e0 = g->impl->engine(0);
+        if (!e0.has_model()) throw std::runtime_error("add: no model loaded");
+        if (e0.ntotal() != 0) throw std::runtime_error("index already holds a base set");
+        if (clusters == 0) throw std::runtime_error("gen_synthetic: dim and clusters must be positive");
+        if (!(spread > 0)) throw std::runtime_error("gen_synthetic: spread must be positive");
+        const uint32_t dim = e0.dim();
+        const uint64_t chunk = std::max<uint64_t>(1, (512ull << 20) / (4ull * dim));
+        g->impl->add_stream(n, chunk, [&](uint64_t first, uint64_t count, float* dst, cudaStream_t st) {
+            vlq::launch_synth(first, count, dim, clusters, spread, seed, dst, st);
+        });
+    });
+}
+
+int vlq_group_search(vlq_group* g, const float* queries, uint64_t nq, uint32_t dim, uint32_t w1, float alpha,
+                     uint32_t k, int64_t* out_ids, float* out_dists, uint64_t* out_scanned) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        if (nq && (!queries || !out_ids || !out_dists)) throw std::runtime_error("search: NULL buffer");
+        g->impl->search_host(queries, nq, dim, w1, alpha, k, out_ids, out_dists, out_scanned);
+    });
+}
+
+int vlq_group_set_queries(vlq_group* g, const float* queries, uint64_t nq, uint32_t dim) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        if (nq && !queries) throw std::runtime_error("set_queries: NULL buffer");
+        g->impl->upload_queries(queries, nq, dim);
+    });
+}
+
+int vlq_group_search_resident(vlq_group* g, uint32_t w1, float alpha, uint32_t k, float* out_ms) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        const float ms = g->impl->search_resident(w1, alpha, k);
+        if (out_ms) *out_ms = ms;
+    });
+}
+
+int vlq_group_results(vlq_group* g, int64_t* out_ids, float* out_dists, uint64_t* out_scanned) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] { g->impl->results(out_ids, out_dists, out_scanned); });
+}
+
+int vlq_group_info(vlq_group* g, uint32_t member, vlq_info* out) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        if (!out) throw std::runtime_error("info: out is NULL");
+        if (member >= g->impl->size()) throw std::runtime_error("info: member out of range");
+        vlq::Engine& e = g->impl->engine(member);
+        out->dim = e.dim();
+        out->k = e.k();
+        out->n = e.n();
+        out->m = e.m();
+        out->clamp_lambda = e.clamp() ? 1 : 0;
+        out->lambda_lo = e.lo();
+        out->lambda_hi = e.hi();
+        out->ntotal = e.ntotal();
+        out->local_entries = e.local_entries();
+    });
+}
+
+int vlq_group_set_profiling(vlq_group* g, int on) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        for (uint32_t i = 0; i < g->impl->size(); i++) g->impl->engine(i).set_profiling(on != 0);
+    });
+}
+
+int vlq_group_get_stats(vlq_group* g, uint32_t member, vlq_stats* out, int reset) {
+    GROUP_OR_FAIL(g);
+    return guarded([&] {
+        if (!out) throw std::runtime_error("stats: out is NULL");
+        if (member >= g->impl->size()) throw std::runtime_error("stats: member out of range");
+        vlq::Engine& e = g->impl->engine(member);
+        const vlq::EngineStats& s = e.stats();
+        out->launches = s.launches;
+        out->tiles = s.tiles;
+        out->flagged = s.flagged;
+        out->tc_fallbacks = s.tc_refine_fallbacks;
+        for (int p = 0; p < 8; p++) out->phase_ms[p] = s.phase_ms[p];
+        if (reset) e.reset_stats();
+    });
+}
+
+uint32_t vlq_group_size(vlq_group* g) { return (g && g->impl) ? g->impl->size() : 0u; }
 
 }  // extern "C"

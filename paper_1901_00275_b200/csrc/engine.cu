@@ -653,6 +653,8 @@ Engine::StageIO Engine::StageIO::at(uint64_t t0, uint32_t w1, uint32_t w2) const
     o.ab_in = ab_in ? ab_in + t0 * w2 * 2 : nullptr;
     o.sel_out = sel_out ? sel_out + t0 * w2 : nullptr;
     o.ab_out = ab_out ? ab_out + t0 * w2 * 2 : nullptr;
+    o.parts = parts;
+    o.q0 = q0 + t0;
     return o;
 }
 
@@ -691,6 +693,15 @@ void Engine::search_fine_sel_device(const float* d_q, uint64_t nq, uint32_t w1, 
     StageIO io;
     io.sel_in = d_sel;
     io.ab_in = d_ab;
+    search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, io, STAGE_FINE_SEL, st);
+}
+
+void Engine::search_fine_sel_parts(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
+                                   const SelParts& parts, int64_t* d_ids, float* d_dists, uint64_t* d_scanned,
+                                   cudaStream_t st) {
+    if (parts.nparts == 0 || parts.nparts > VLQ_MAX_PARTS) throw std::runtime_error("search_fine_sel: bad parts");
+    StageIO io;
+    io.parts = &parts;
     search_staged(d_q, nq, w1, alpha, topk, d_ids, d_dists, d_scanned, io, STAGE_FINE_SEL, st);
 }
 
@@ -937,7 +948,8 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
     auto mark = [&](int ph) { mark_phase(ph, st); };
     SearchArgs a = search_args();
     mark(PH_SECOND);
-    if (sel) launch_apply_selection(a, nt, w2, sel->sel_in, sel->ab_in, st);
+    if (sel && sel->parts) launch_apply_selection_parts(a, nt, w2, *sel->parts, sel->q0, st);
+    else if (sel) launch_apply_selection(a, nt, w2, sel->sel_in, sel->ab_in, st);
     else if (!second_done) launch_second_level(a, nt, w1, w2, st);
     mark(PH_TERM5);
     launch_term5(cfg_.cert_slack, d_q, pqT_.p, dim_, m_, t5_.p, meta_.p, nt, st);

@@ -204,6 +204,11 @@ public:
     void search_fine_sel_device(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
                                 const uint32_t* d_sel, const float* d_ab, int64_t* d_ids, float* d_dists,
                                 uint64_t* d_scanned, cudaStream_t st);
+    // fine_sel from a selection split in parts over several GPUs (group.cu): query q's
+    // cells / (a, b) are row q % per of part q / per, read over NVLink peer memory
+    void search_fine_sel_parts(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk,
+                               const SelParts& parts, int64_t* d_ids, float* d_dists, uint64_t* d_scanned,
+                               cudaStream_t st);
     void search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
                      float* dists, uint64_t* scanned);
     void check_device_errors(cudaStream_t st);
@@ -264,6 +269,8 @@ private:
         const float* ab_in = nullptr;      //                 [nq, w2, 2]
         uint32_t* sel_out = nullptr;       // STAGE_SELECT
         float* ab_out = nullptr;
+        const SelParts* parts = nullptr;   // STAGE_FINE_SEL from a selection in parts (multi-GPU group)
+        uint64_t q0 = 0;                   //   batch row of this tile's first query
         StageIO at(uint64_t t0, uint32_t w1, uint32_t w2) const;
     };
     void search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* d_ids,

@@ -1,0 +1,306 @@
+// Multi-GPU search group: one process drives G GPUs of one box (SURVEY.md
+// §2.3, §8e; the paper's "split the index into b parts, search locally,
+// join").
+//
+// Engine g (device dev[g]) holds the posting lists c with
+// shard_of_cell(c, G) == g; the coarse quantizer, graph, PQ and t3 are
+// replicated.  Per batch, on per-device streams, with cross-device event
+// waits (no host round trip):
+//
+//   1. select   device g runs first_level_scan + second_level_rank for its
+//               query slice [g per, (g + 1) per): the selected cells and their
+//               exact (a, b) pairs stay in ITS memory;
+//   2. fine     every device runs apply-selection + term5 + the fused scan +
+//               the exact re-score for the whole batch on its shard; the
+//               apply kernel reads query q's selection row directly from the
+//               device that selected it (k_apply_selection over NVLink peer
+//               memory: the all-gather is fused into the consumer);
+//   3. merge    device g merges the G per-shard exact top-k rows of ITS query
+//               slice, reading the other devices' blocks over NVLink
+//               (k_merge_sorted with peer pointers: gather + merge in one
+//               kernel), and returns that slice to the host.
+//
+// Every shard returns its exact local top-k under the reference's (dist, id)
+// order, so the merged rows equal the single-engine result bit for bit.  The
+// collectives are P2P loads by the consuming kernels (cudaDeviceEnablePeerAccess
+// between every pair of devices; NVSwitch gives every pair full bandwidth), so
+// the step needs no NCCL call and no PyTorch.  A group may list the same device
+// several times (parity tests on one GPU): peer pointers are then plain local
+// pointers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "engine.h"
+#include "group.h"
+
+namespace vlq {
+
+namespace {
+uint64_t slice_per(uint64_t nq, uint32_t G) { return (nq + G - 1) / G; }
+}  // namespace
+
+Group::Group(const std::vector<int>& devices, const EngineConfig& base) : dev_(devices) {
+    const uint32_t G = (uint32_t)dev_.size();
+    if (G == 0 || G > VLQ_MAX_PARTS) throw std::runtime_error("group: need 1..16 devices");
+    int ndev = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    for (int d : dev_)
+        if (d < 0 || d >= ndev) throw std::runtime_error("group: device index out of range");
+    // NVLink peer access between every pair of distinct devices (the fused
+    // exchange kernels load peer memory directly)
+    for (uint32_t a = 0; a < G; a++)
+        for (uint32_t b = 0; b < G; b++) {
+            if (dev_[a] == dev_[b]) continue;
+            int ok = 0;
+            CUDA_CHECK(cudaDeviceCanAccessPeer(&ok, dev_[a], dev_[b]));
+            if (!ok) throw std::runtime_error("group: devices " + std::to_string(dev_[a]) + " and " +
+                                              std::to_string(dev_[b]) + " have no peer access");
+            DeviceGuard g(dev_[a]);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(dev_[b], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+            else CUDA_CHECK(e);
+        }
+    for (uint32_t g = 0; g < G; g++) per_.emplace_back();
+    for (uint32_t g = 0; g < G; g++) {
+        EngineConfig c = base;
+        c.device = dev_[g];
+        c.shard_rank = (int)g;
+        c.shard_count = (int)G;
+        eng_.emplace_back(new Engine(c));
+        DeviceGuard dg(dev_[g]);
+        PerDevice& p = per_[g];
+        CUDA_CHECK(cudaStreamCreateWithFlags(&p.st, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&p.ev_sel, &p.ev_fine, &p.ev_done})
+            CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreate(&p.ev_t0));
+        CUDA_CHECK(cudaEventCreate(&p.ev_t1));
+    }
+}
+
+Group::~Group() {
+    for (uint32_t g = 0; g < per_.size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        PerDevice& p = per_[g];
+        if (p.st) cudaStreamSynchronize(p.st);
+        for (cudaEvent_t e : {p.ev_sel, p.ev_fine, p.ev_done, p.ev_t0, p.ev_t1})
+            if (e) cudaEventDestroy(e);
+        p.q.reset();
+        p.sel.reset();
+        p.ab.reset();
+        p.lids.reset();
+        p.ld.reset();
+        p.lsc.reset();
+        p.oids.reset();
+        p.od.reset();
+        if (p.st) cudaStreamDestroy(p.st);
+    }
+    if (pin_) cudaFreeHost(pin_);
+    eng_.clear();
+}
+
+void Group::for_each_device(const std::function<void(uint32_t)>& fn) {
+    // one host thread per engine (set-up work: loads, adds); errors re-thrown
+    const uint32_t G = size();
+    std::vector<std::string> err(G);
+    std::vector<std::thread> th;
+    for (uint32_t g = 0; g < G; g++)
+        th.emplace_back([&, g] {
+            try {
+                fn(g);
+            } catch (const std::exception& e) {
+                err[g] = e.what();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (!e.empty()) throw std::runtime_error(e);
+}
+
+void Group::load_vlq1(const std::string& path) {
+    for_each_device([&](uint32_t g) { eng_[g]->load_vlq1(path); });
+}
+
+void Group::set_model(const HostModel& m) {
+    for_each_device([&](uint32_t g) { eng_[g]->set_model(m); });
+}
+
+void Group::add_host(const float* base, uint64_t nb) {
+    for_each_device([&](uint32_t g) { eng_[g]->add_host(base, nb); });
+}
+
+void Group::add_stream(uint64_t nb, uint64_t chunk, const Engine::ChunkSource& src) {
+    for_each_device([&](uint32_t g) { eng_[g]->add_stream(nb, chunk, src); });
+}
+
+void Group::reserve(uint64_t nq, uint32_t w2, uint32_t k) {
+    const uint32_t G = size();
+    const uint64_t per = slice_per(nq, G);
+    const uint32_t dim = eng_[0]->dim();
+    for (uint32_t g = 0; g < G; g++) {
+        DeviceGuard dg(dev_[g]);
+        PerDevice& p = per_[g];
+        p.q.alloc(std::max<uint64_t>(1, nq * dim));
+        p.sel.alloc(std::max<uint64_t>(1, per * w2));
+        p.ab.alloc(std::max<uint64_t>(1, per * w2 * 2));
+        p.lids.alloc(std::max<uint64_t>(1, nq * k));
+        p.ld.alloc(std::max<uint64_t>(1, nq * k));
+        p.lsc.alloc(std::max<uint64_t>(1, nq));
+        p.oids.alloc(std::max<uint64_t>(1, per * k));
+        p.od.alloc(std::max<uint64_t>(1, per * k));
+    }
+}
+
+void Group::upload_queries(const float* q, uint64_t nq, uint32_t dim) {
+    if (dim != eng_[0]->dim()) throw std::runtime_error("search_batch: dimension mismatch");
+    const uint64_t bytes = nq * dim * 4;
+    if (pin_bytes_ < bytes) {
+        if (pin_) CUDA_CHECK(cudaFreeHost(pin_));
+        pin_ = nullptr;
+        CUDA_CHECK(cudaMallocHost(&pin_, bytes));
+        pin_bytes_ = bytes;
+    }
+    std::memcpy(pin_, q, bytes);
+    for (uint32_t g = 0; g < size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        per_[g].q.alloc(std::max<uint64_t>(1, nq * dim));
+        CUDA_CHECK(cudaMemcpyAsync(per_[g].q.p, pin_, bytes, cudaMemcpyHostToDevice, per_[g].st));
+    }
+    nq_q_ = nq;
+}
+
+void Group::enqueue_search(uint64_t nq, uint32_t w1, float alpha, uint32_t k) {
+    const uint32_t G = size();
+    const uint64_t per = slice_per(nq, G);
+    const uint32_t dim = eng_[0]->dim();
+    // 1. query-split selection
+    for (uint32_t g = 0; g < G; g++) {
+        PerDevice& p = per_[g];
+        DeviceGuard dg(dev_[g]);
+        const uint64_t lo = std::min(nq, g * per), hi = std::min(nq, lo + per);
+        if (hi > lo)
+            eng_[g]->search_select_device(p.q.p + lo * dim, hi - lo, w1, alpha, p.sel.p, p.ab.p, p.st);
+        CUDA_CHECK(cudaEventRecord(p.ev_sel, p.st));
+    }
+    // 2. sharded fine stage, the selection read from its owners over NVLink
+    SelParts sp{};
+    for (uint32_t g = 0; g < G; g++) {
+        sp.sel[g] = per_[g].sel.p;
+        sp.ab[g] = per_[g].ab.p;
+    }
+    sp.nparts = G;
+    sp.per = per;
+    for (uint32_t g = 0; g < G; g++) {
+        PerDevice& p = per_[g];
+        DeviceGuard dg(dev_[g]);
+        for (uint32_t h = 0; h < G; h++)
+            if (h != g) CUDA_CHECK(cudaStreamWaitEvent(p.st, per_[h].ev_sel, 0));
+        eng_[g]->search_fine_sel_parts(p.q.p, nq, w1, alpha, k, sp, p.lids.p, p.ld.p, p.lsc.p, p.st);
+        CUDA_CHECK(cudaEventRecord(p.ev_fine, p.st));
+    }
+    // 3. each device merges its query slice from every shard's block (peer loads)
+    TopkParts tp{};
+    for (uint32_t g = 0; g < G; g++) {
+        tp.ids[g] = per_[g].lids.p;
+        tp.d[g] = per_[g].ld.p;
+    }
+    tp.nparts = G;
+    for (uint32_t g = 0; g < G; g++) {
+        PerDevice& p = per_[g];
+        DeviceGuard dg(dev_[g]);
+        for (uint32_t h = 0; h < G; h++)
+            if (h != g) CUDA_CHECK(cudaStreamWaitEvent(p.st, per_[h].ev_fine, 0));
+        const uint64_t lo = std::min(nq, g * per), hi = std::min(nq, lo + per);
+        launch_merge_topk_parts(tp, lo, hi - lo, k, p.oids.p, p.od.p, p.st);
+        CUDA_CHECK(cudaEventRecord(p.ev_done, p.st));
+    }
+    // no device may reuse its selection / result buffers (next batch) before
+    // every peer finished reading them
+    for (uint32_t g = 0; g < G; g++) {
+        DeviceGuard dg(dev_[g]);
+        for (uint32_t h = 0; h < G; h++)
+            if (h != g) CUDA_CHECK(cudaStreamWaitEvent(per_[g].st, per_[h].ev_done, 0));
+    }
+}
+
+void Group::check_errors() {
+    for (uint32_t g = 0; g < size(); g++) eng_[g]->check_device_errors(per_[g].st);
+}
+
+float Group::search_resident(uint32_t w1, float alpha, uint32_t k) {
+    const uint64_t nq = nq_q_;
+    if (nq == 0) return 0.0f;
+    if (w1 == 0 || w1 > eng_[0]->k()) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
+    reserve(nq, w2_of(w1, alpha, eng_[0]->n()), k);
+    for (uint32_t g = 0; g < size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        CUDA_CHECK(cudaStreamSynchronize(per_[g].st));
+    }
+    for (uint32_t g = 0; g < size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        CUDA_CHECK(cudaEventRecord(per_[g].ev_t0, per_[g].st));
+    }
+    enqueue_search(nq, w1, alpha, k);
+    for (uint32_t g = 0; g < size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        CUDA_CHECK(cudaEventRecord(per_[g].ev_t1, per_[g].st));
+    }
+    float ms = 0.0f;
+    for (uint32_t g = 0; g < size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        CUDA_CHECK(cudaEventSynchronize(per_[g].ev_t1));
+        float t = 0.0f;
+        CUDA_CHECK(cudaEventElapsedTime(&t, per_[g].ev_t0, per_[g].ev_t1));
+        ms = std::max(ms, t);  // the job's time: max over the devices
+    }
+    check_errors();
+    last_k_ = k;
+    return ms;
+}
+
+void Group::results(int64_t* ids, float* dists, uint64_t* scanned) {
+    const uint64_t nq = nq_q_;
+    const uint32_t G = size(), k = last_k_;
+    const uint64_t per = slice_per(nq, G);
+    std::vector<uint64_t> sc(scanned ? nq : 0);
+    for (uint32_t g = 0; g < G; g++) {
+        DeviceGuard dg(dev_[g]);
+        PerDevice& p = per_[g];
+        const uint64_t lo = std::min(nq, g * per), hi = std::min(nq, lo + per);
+        if (hi > lo) {
+            if (ids) CUDA_CHECK(cudaMemcpyAsync(ids + lo * k, p.oids.p, (hi - lo) * k * 8, cudaMemcpyDeviceToHost, p.st));
+            if (dists)
+                CUDA_CHECK(cudaMemcpyAsync(dists + lo * k, p.od.p, (hi - lo) * k * 4, cudaMemcpyDeviceToHost, p.st));
+        }
+        CUDA_CHECK(cudaStreamSynchronize(p.st));
+        if (scanned) {  // reference-semantics scanned count = the sum over the shards
+            CUDA_CHECK(cudaMemcpy(sc.data(), p.lsc.p, nq * 8, cudaMemcpyDeviceToHost));
+            for (uint64_t q = 0; q < nq; q++) scanned[q] = (g == 0 ? 0 : scanned[q]) + sc[q];
+        }
+    }
+}
+
+void Group::search_host(const float* q, uint64_t nq, uint32_t dim, uint32_t w1, float alpha, uint32_t k,
+                        int64_t* ids, float* dists, uint64_t* scanned) {
+    if (dim != eng_[0]->dim()) throw std::runtime_error("search_batch: dimension mismatch");
+    if (w1 == 0 || w1 > eng_[0]->k()) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
+    for (uint64_t i = 0; i < nq * dim; i++)
+        if (!std::isfinite(q[i])) throw std::runtime_error("VectorSet: non-finite value");
+    if (nq == 0) return;
+    upload_queries(q, nq, dim);
+    reserve(nq, w2_of(w1, alpha, eng_[0]->n()), k);
+    enqueue_search(nq, w1, alpha, k);
+    check_errors();
+    last_k_ = k;
+    results(ids, dists, scanned);
+}
+
+uint64_t Group::local_entries(uint32_t g) const { return eng_[g]->local_entries(); }
+
+}  // namespace vlq

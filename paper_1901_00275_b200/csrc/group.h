@@ -1,0 +1,72 @@
+// Multi-GPU search group (group.cu): one process, G engines on G devices,
+// list-sharded index, query-split selection, fused P2P exchange + merge.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <deque>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+namespace vlq {
+
+class Group {
+public:
+    Group(const std::vector<int>& devices, const EngineConfig& base);
+    ~Group();
+    Group(const Group&) = delete;
+    Group& operator=(const Group&) = delete;
+
+    uint32_t size() const { return (uint32_t)eng_.size(); }
+    Engine& engine(uint32_t g) { return *eng_[g]; }
+    int device(uint32_t g) const { return dev_[g]; }
+    uint64_t local_entries(uint32_t g) const;
+
+    // set-up, one host thread per engine
+    void load_vlq1(const std::string& path);
+    void set_model(const HostModel& m);
+    void add_host(const float* base, uint64_t nb);
+    void add_stream(uint64_t nb, uint64_t chunk, const Engine::ChunkSource& src);
+
+    // Index.search over the group: host queries in, merged host results out
+    void search_host(const float* q, uint64_t nq, uint32_t dim, uint32_t w1, float alpha, uint32_t k, int64_t* ids,
+                     float* dists, uint64_t* scanned);
+    // device-resident batch (bench): upload once, then timed searches
+    // (device ms, max over the devices), then results()
+    void upload_queries(const float* q, uint64_t nq, uint32_t dim);
+    float search_resident(uint32_t w1, float alpha, uint32_t k);
+    void results(int64_t* ids, float* dists, uint64_t* scanned);
+
+private:
+    struct PerDevice {
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev_sel = nullptr, ev_fine = nullptr, ev_done = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+        DevBuf<float> q;         // the whole batch [nq, dim]
+        DevBuf<uint32_t> sel;    // this device's query slice: selected cells [per, w2]
+        DevBuf<float> ab;        //                             exact (a, b) [per, w2, 2]
+        DevBuf<int64_t> lids;    // this shard's exact top-k, whole batch [nq, k]
+        DevBuf<float> ld;
+        DevBuf<uint64_t> lsc;    // this shard's scanned counts [nq]
+        DevBuf<int64_t> oids;    // merged top-k of this device's query slice [per, k]
+        DevBuf<float> od;
+    };
+    void for_each_device(const std::function<void(uint32_t)>& fn);
+    void reserve(uint64_t nq, uint32_t w2, uint32_t k);
+    void enqueue_search(uint64_t nq, uint32_t w1, float alpha, uint32_t k);
+    void check_errors();
+
+    std::vector<int> dev_;
+    std::vector<std::unique_ptr<Engine>> eng_;
+    std::deque<PerDevice> per_;  // deque: PerDevice (DevBuf) is neither copyable nor movable
+    void* pin_ = nullptr;
+    uint64_t pin_bytes_ = 0;
+    uint64_t nq_q_ = 0;
+    uint32_t last_k_ = 0;
+};
+
+}  // namespace vlq

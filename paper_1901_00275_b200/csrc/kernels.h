@@ -83,6 +83,29 @@ void launch_pack_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32
                            cudaStream_t st);
 void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const uint32_t* sel_in, const float* ab,
                             cudaStream_t st);
+
+// Multi-GPU group (group.cu): per-device buffers addressed directly by the
+// kernels over NVLink peer memory (P2P loads), at most VLQ_MAX_PARTS devices.
+constexpr uint32_t VLQ_MAX_PARTS = 16;
+// the batch's selection in parts: query q's row is row q % per of part q / per
+struct SelParts {
+    const uint32_t* sel[VLQ_MAX_PARTS];  // [per, w2] cells
+    const float* ab[VLQ_MAX_PARTS];      // [per, w2, 2] exact (a, b)
+    uint32_t nparts;
+    uint64_t per;
+};
+// per-shard top-k blocks: row r of part g at ids[g] + r * topk
+struct TopkParts {
+    const int64_t* ids[VLQ_MAX_PARTS];
+    const float* d[VLQ_MAX_PARTS];
+    uint32_t nparts;
+};
+// k_apply_selection reading each query's row from its part (q = q0 + block)
+void launch_apply_selection_parts(const SearchArgs& a, uint64_t nq, uint32_t w2, const SelParts& p, uint64_t q0,
+                                  cudaStream_t st);
+// (dist, id) merge of rows [row0, row0 + nrows) of every part into out[0 .. nrows)
+void launch_merge_topk_parts(const TopkParts& p, uint64_t row0, uint64_t nrows, uint32_t topk, int64_t* out_ids,
+                             float* out_d, cudaStream_t st);
 // pqT: the PQ codebook transposed to [p][t][j] (j = codeword, fastest)
 // cert_slack: added to the re-score certificate's error bound (0 in production;
 // tests widen it to force the retry and exact-fallback paths)

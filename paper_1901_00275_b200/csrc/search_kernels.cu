@@ -188,12 +188,18 @@ __global__ void k_pack_selection(SearchArgs a, uint32_t w2, uint32_t* __restrict
     }
 }
 
-__global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t w2, const uint32_t* __restrict__ sel_in,
-                                                         const float* __restrict__ ab) {
+__global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t w2, SelParts parts, uint64_t q0) {
     __shared__ unsigned long long s_scanned;
     __shared__ float s_dmax;
     const uint64_t q = blockIdx.x;
     float* wsq = a.ws + q * a.k;
+    // this query's row of the gathered selection: part (q0 + q) / per, possibly
+    // on a peer GPU (read over NVLink)
+    const uint64_t gq = q0 + q;
+    const uint32_t part = parts.per ? (uint32_t)(gq / parts.per) : 0u;
+    const uint64_t row = parts.per ? gq % parts.per : gq;
+    const uint32_t* sel_in = parts.sel[part] + row * w2;
+    const float* ab = parts.ab[part] + row * w2 * 2;
     if (threadIdx.x == 0) {
         s_scanned = 0;
         s_dmax = 0.0f;
@@ -203,9 +209,9 @@ __global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t 
     unsigned long long cnt = 0;
     float dmax = 0.0f;
     for (uint32_t t = threadIdx.x; t < w2; t += blockDim.x) {
-        const uint32_t cell = sel_in[q * w2 + t];
+        const uint32_t cell = sel_in[t];
         a.sel[q * w2 + t] = cell;
-        const float av = ab[(q * w2 + t) * 2], bv = ab[(q * w2 + t) * 2 + 1], cv = a.elen[cell];
+        const float av = ab[t * 2], bv = ab[t * 2 + 1], cv = a.elen[cell];
         // equal values from every writer: both are the exact reference-order
         // distance to that centroid
         wsq[cell / a.n] = av;
@@ -551,7 +557,18 @@ void launch_pack_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32
 
 void launch_apply_selection(const SearchArgs& a, uint64_t nq, uint32_t w2, const uint32_t* sel_in, const float* ab,
                             cudaStream_t st) {
-    dev::k_apply_selection<<<(unsigned)nq, 256, 0, st>>>(a, w2, sel_in, ab);
+    SelParts p{};
+    p.sel[0] = sel_in;
+    p.ab[0] = ab;
+    p.nparts = 1;
+    p.per = 0;  // one part holding every row
+    launch_apply_selection_parts(a, nq, w2, p, 0, st);
+}
+
+void launch_apply_selection_parts(const SearchArgs& a, uint64_t nq, uint32_t w2, const SelParts& p, uint64_t q0,
+                                  cudaStream_t st) {
+    if (nq == 0) return;
+    dev::k_apply_selection<<<(unsigned)nq, 256, 0, st>>>(a, w2, p, q0);
     CUDA_LAUNCH_CHECK();
 }
 
@@ -632,19 +649,19 @@ __global__ void k_emit_exact(SearchArgs a, const uint32_t* __restrict__ qlist, c
 // the number of smaller keys in every other part (a binary search each;
 // keys are unique since every id lives in exactly one shard).  No sort, two
 // block barriers.
-__global__ void __launch_bounds__(256) k_merge_sorted(const int64_t* __restrict__ in_ids, const float* __restrict__ in_d,
-                                                      uint32_t nparts, uint64_t nq, uint32_t topk,
+__global__ void __launch_bounds__(256) k_merge_sorted(TopkParts parts, uint64_t row0, uint32_t topk,
                                                       int64_t* __restrict__ out_ids, float* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t nparts = parts.nparts;
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [nparts][topk]
     uint64_t* res = keys + (size_t)nparts * topk;         // [topk]
     const uint64_t q = blockIdx.x;
     const uint32_t total = nparts * topk;
-    for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+    for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {  // parts may live on peer GPUs (P2P loads)
         const uint32_t part = t / topk, r = t % topk;
-        const uint64_t src = ((uint64_t)part * nq + q) * topk + r;
-        const int64_t id = in_ids[src];
-        keys[t] = id >= 0 ? make_key(in_d[src], (uint32_t)id) : ~0ull;
+        const uint64_t src = (row0 + q) * topk + r;
+        const int64_t id = parts.ids[part][src];
+        keys[t] = id >= 0 ? make_key(parts.d[part][src], (uint32_t)id) : ~0ull;
     }
     for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) res[t] = ~0ull;
     __syncthreads();
@@ -718,15 +735,28 @@ void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigne
     CUDA_LAUNCH_CHECK();
 }
 
+void launch_merge_topk_parts(const TopkParts& p, uint64_t row0, uint64_t nrows, uint32_t topk, int64_t* out_ids,
+                             float* out_d, cudaStream_t st) {
+    if (nrows == 0 || topk == 0) return;
+    const size_t smem = ((size_t)p.nparts + 1) * topk * 8;
+    if (smem > 200 * 1024) throw std::runtime_error("merge_topk: nparts * k too large");
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_merge_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_merge_sorted<<<(unsigned)nrows, 256, smem, st>>>(p, row0, topk, out_ids, out_d);
+    CUDA_LAUNCH_CHECK();
+}
+
 void launch_merge_topk(const int64_t* in_ids, const float* in_d, uint32_t nparts, uint64_t nq, uint32_t topk,
                        int64_t* out_ids, float* out_d, cudaStream_t st) {
     if (nq == 0 || topk == 0) return;
     const size_t smem_sorted = ((size_t)nparts + 1) * topk * 8;
-    if (smem_sorted <= 200 * 1024) {
-        CUDA_CHECK(cudaFuncSetAttribute(dev::k_merge_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem_sorted));
-        dev::k_merge_sorted<<<(unsigned)nq, 256, smem_sorted, st>>>(in_ids, in_d, nparts, nq, topk, out_ids, out_d);
-        CUDA_LAUNCH_CHECK();
+    if (smem_sorted <= 200 * 1024 && nparts <= VLQ_MAX_PARTS) {
+        TopkParts p{};
+        for (uint32_t g = 0; g < nparts; g++) {
+            p.ids[g] = in_ids + (uint64_t)g * nq * topk;
+            p.d[g] = in_d + (uint64_t)g * nq * topk;
+        }
+        p.nparts = nparts;
+        launch_merge_topk_parts(p, 0, nq, topk, out_ids, out_d, st);
         return;
     }
     uint32_t n = 1;

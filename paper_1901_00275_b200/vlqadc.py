@@ -333,6 +333,118 @@ class Index:
 _MAX_THREADS = 0
 
 
+class IndexGroup:
+    """The index sharded over several GPUs of one box, driven by ONE process
+    (include/vlq_gpu.h vlq_group_*; csrc/group.cu): engine g on devices[g]
+    holds the posting lists c with shard_of_cell(c, G) == g, the coarse
+    quantizer is replicated; search runs the query-split selection, the
+    sharded scan reading the selections over NVLink peer memory, and the
+    per-slice (dist, id) merge of the shards' top-k from peer memory.
+    Results equal Index.search on the unsharded index bit for bit."""
+
+    def __init__(self, devices, *, workspace_bytes: int = 0, max_tile: int = 0, force_exact: bool = False):
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        cfg = _lib.VlqConfig(0, 0, 1, workspace_bytes, max_tile, int(force_exact))
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().vlq_group_create(devs, len(devices), ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self.devices = [int(d) for d in devices]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().vlq_group_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @staticmethod
+    def load(path: str, devices, **kw) -> "IndexGroup":
+        g = IndexGroup(devices, **kw)
+        _lib.check(_lib.lib().vlq_group_load_vlq1(g._h, os.fsencode(str(path))))
+        return g
+
+    @staticmethod
+    def from_model(model: dict, devices, **kw) -> "IndexGroup":
+        """An empty group over trained quantizers (Index.model() dict)."""
+        g = IndexGroup(devices, **kw)
+        cent = np.ascontiguousarray(model["centroids"], np.float32)
+        nb = np.ascontiguousarray(model["nbr"], np.uint32)
+        el = np.ascontiguousarray(model["elen"], np.float32)
+        pqa = np.ascontiguousarray(model["pq"], np.float32)
+        _lib.check(_lib.lib().vlq_group_set_model(g._h, model["dim"], model["k"], model["n"], model["m"],
+                                                  int(model["clamp"]), model["lo"], model["hi"], _p(cent), _p(nb),
+                                                  _p(el), _p(pqa), None))
+        return g
+
+    def add(self, base) -> None:
+        b = _to_vecset(base)
+        _lib.check(_lib.lib().vlq_group_add(self._h, _p(b), b.shape[0], b.shape[1]))
+
+    def add_synthetic(self, n: int, clusters: int = 200, spread: float = 0.05, seed: int = 42) -> None:
+        _lib.check(_lib.lib().vlq_group_add_synthetic(self._h, n, clusters, spread, seed))
+
+    def search(self, queries, w1: int = 64, alpha: float = 0.25, k: int = 10, *, return_scanned: bool = False):
+        """Index.search over the group (same outputs)."""
+        q = _to_vecset(queries)
+        nq = q.shape[0]
+        ids = np.empty((nq, k), np.int64)
+        dists = np.empty((nq, k), np.float32)
+        scanned = np.empty(nq, np.uint64) if return_scanned else None
+        _lib.check(_lib.lib().vlq_group_search(self._h, _p(q), nq, q.shape[1], w1, alpha, k, _p(ids), _p(dists),
+                                               _p(scanned)))
+        if return_scanned:
+            return ids, dists, scanned.astype(np.int64)
+        return ids, dists
+
+    def set_queries(self, queries) -> None:
+        q = _to_vecset(queries)
+        _lib.check(_lib.lib().vlq_group_set_queries(self._h, _p(q), q.shape[0], q.shape[1]))
+        self._nq = q.shape[0]
+
+    def search_resident(self, w1: int, alpha: float, k: int) -> float:
+        """Searches the batch of set_queries(); returns its device time in ms
+        (max over the devices)."""
+        ms = ctypes.c_float()
+        _lib.check(_lib.lib().vlq_group_search_resident(self._h, w1, alpha, k, ctypes.byref(ms)))
+        self._k = k
+        return float(ms.value)
+
+    def results(self):
+        nq, k = self._nq, self._k
+        ids = np.empty((nq, k), np.int64)
+        dists = np.empty((nq, k), np.float32)
+        scanned = np.empty(nq, np.uint64)
+        _lib.check(_lib.lib().vlq_group_results(self._h, _p(ids), _p(dists), _p(scanned)))
+        return ids, dists, scanned.astype(np.int64)
+
+    def set_profiling(self, on: bool = True) -> None:
+        _lib.check(_lib.lib().vlq_group_set_profiling(self._h, int(on)))
+
+    def stats(self, member: int, reset: bool = False) -> dict:
+        s = _lib.VlqStats()
+        _lib.check(_lib.lib().vlq_group_get_stats(self._h, member, ctypes.byref(s), int(reset)))
+        return {"launches": int(s.launches), "tiles": int(s.tiles), "flagged": int(s.flagged),
+                "tc_fallbacks": int(s.tc_fallbacks),
+                "phase_ms": dict(zip(_lib.PHASES, [float(x) for x in s.phase_ms]))}
+
+    def __len__(self) -> int:
+        return int(_lib.lib().vlq_group_size(self._h))
+
+    def info(self, member: int = 0) -> _lib.VlqInfo:
+        out = _lib.VlqInfo()
+        _lib.check(_lib.lib().vlq_group_info(self._h, member, ctypes.byref(out)))
+        return out
+
+    @property
+    def ntotal(self) -> int:
+        return int(self.info(0).ntotal)
+
+    def local_entries(self) -> list[int]:
+        return [int(self.info(g).local_entries) for g in range(len(self))]
+
+
 class IvfBaselineIndex:
     """The IVFADC comparison baseline (proj/include/vlq/ivf_baseline.hpp):
     k posting lists of (id, PQ code of x - c_i), built with an Index's
