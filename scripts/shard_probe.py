@@ -10,7 +10,8 @@ with CUDA events on the GPU:
                 slice (nq / G queries): search_select_device;
   * fine_sel -- term5 + fused scan + exact re-score for the WHOLE batch on the
                 shard from the gathered selection: search_fine_sel_device;
-  * merge    -- the K9 (dist, id) merge of G top-k blocks;
+  * merge    -- the K9 (dist, id) merge of the rank's query slice from G top-k
+                blocks (vlq_group: each GPU merges its own slice);
 
 and reports t_rank = select + fine_sel + merge.  The two all-gathers (cells +
 (a, b) pairs: nq*w2*12 B; the top-k blocks: G*nq*k*12 B) are NOT measured
@@ -101,8 +102,9 @@ def main():
                                                          scanned.data_ptr(), st))
             same = bool((ids.cpu().numpy() == ref[0]).all() and (dists.cpu().numpy() == ref[1]).all())
             variants[cfg] = {"fine_sel_ms": round(t, 3), "same_results": same}
-        gi = ids.unsqueeze(0).expand(G, nq, k).contiguous()
-        gd = dists.unsqueeze(0).expand(G, nq, k).contiguous()
+        # the group merges only its own query slice (rows [lo, hi)) from the G blocks
+        gi = ids[lo:hi].unsqueeze(0).expand(G, hi - lo, k).contiguous()
+        gd = dists[lo:hi].unsqueeze(0).expand(G, hi - lo, k).contiguous()
         t_merge = timed(lambda: vdist.merge_topk(gi, gd, st))
         # the earlier schedule for comparison: query-split first level only,
         # every rank repeats exact neighbours + second level for the batch
