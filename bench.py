@@ -139,9 +139,12 @@ def build_index(vlqadc, w, device, rank=0, world=1):
     """Untimed setup: GPU training on a prefix sample (rank 0; the model is
     broadcast to the other ranks), streamed GPU add of each rank's shard."""
     import torch
+    import torch.distributed as dist
+    # scripts/shard_probe.py builds one rank's shard alone (no process group): it trains itself
+    collective = world > 1 and dist.is_initialized()
     t0 = time.time()
     model = None
-    if rank == 0:
+    if rank == 0 or not collective:
         sample = torch.empty((w["ntrain"], w["dim"]), dtype=torch.float32, device=f"cuda:{device}")
         vlqadc.gen_synthetic_device(0, w["ntrain"], w["dim"], w["clusters"], SPREAD, BASE_SEED, sample.data_ptr(),
                                     device=device)
@@ -150,14 +153,12 @@ def build_index(vlqadc, w, device, rank=0, world=1):
                                      seed=TRAIN_SEED, device=device)
         model = trained.model()
         del trained, sample
-    if world > 1:
-        import torch.distributed as dist
+    if collective:
         box = [model]
         dist.broadcast_object_list(box, src=0)
         model = box[0]
     digest = model_digest(model)
-    if world > 1:
-        import torch.distributed as dist
+    if collective:
         digests = [None] * world
         dist.all_gather_object(digests, digest)
         assert len(set(digests)) == 1, f"ranks hold different models: {digests}"

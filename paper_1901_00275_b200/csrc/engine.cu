@@ -709,7 +709,6 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
                            float* d_dists, uint64_t* d_scanned, const StageIO& io, Stage stage, cudaStream_t st) {
     if (!model_ok_) throw std::runtime_error("search: no model loaded");
     if (w1 == 0 || w1 > k_) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
-    if (topk > 1024) throw std::runtime_error("search: k > 1024 is not supported by the GPU engine");
     if (nq == 0) return;
     DeviceGuard g(cfg_.device);
     const uint32_t w2 = w2_of(w1, alpha, n_);
@@ -1009,7 +1008,18 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         mark(PH_SCAN);
         mark(PH_RESCORE);
         mark(PH_FALLBACK);
-        if (topk > 0) {
+        if (topk > 1024) {
+            // k beyond the exact scan's block buffers: every scanned entry's exact
+            // key, sorted per query (large_k.cu); the scanned counts size the groups
+            std::vector<uint64_t> h_sc(nt);
+            DevBuf<uint64_t> d_sc;
+            d_sc.alloc(nt);
+            launch_copy_scanned(meta_.p, nt, d_sc.p, st);
+            CUDA_CHECK(cudaMemcpyAsync(h_sc.data(), d_sc.p, nt * 8, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            launch_topk_large(a, nt, w2, topk, h_sc.data(), 64ull << 20, d_ids, d_dists, st);
+            launches += 4;
+        } else if (topk > 0) {
             launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, nullptr, nullptr, st);
             launch_emit_exact(a, nullptr, nullptr, nt, keep_x, topk, d_ids, d_dists, st);
             launches += 2;

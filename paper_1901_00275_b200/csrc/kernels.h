@@ -121,6 +121,11 @@ void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t to
                     cudaStream_t st);
 void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,
                        uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d, cudaStream_t st);
+// select_topk for k > 1024 (large_k.cu): exact keys of every scanned entry,
+// sorted per query in groups of at most budget_keys keys; h_scanned = the
+// per-query scanned counts (host)
+void launch_topk_large(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t topk, const uint64_t* h_scanned,
+                       uint64_t budget_keys, int64_t* out_ids, float* out_d, cudaStream_t st);
 void launch_merge_topk(const int64_t* in_ids, const float* in_d, uint32_t nparts, uint64_t nq, uint32_t topk,
                        int64_t* out_ids, float* out_d, cudaStream_t st);
 

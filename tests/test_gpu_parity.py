@@ -457,3 +457,20 @@ def test_certificate_retry_and_exact_fallback_match_oracle(vlqadc, oracle_mod, r
             assert np.array_equal(ids, oids), (name, w1, alpha, k)
             assert same_f32(dists, od)
             assert np.array_equal(sc, osc)
+
+
+@pytest.mark.parametrize("k", [1500, 3000])
+def test_large_k_matches_oracle(vlqadc, oracle_mod, k):
+    """select_topk has no cap on k (search.cpp:122-140): k > 1024 takes the
+    exact all-candidates path (large_k.cu: exact keys of every scanned entry,
+    segmented sort per query), padded with -1 / +inf when fewer were scanned."""
+    for name in ["accept_small", "m16", "smoke"]:
+        z, index_path, _ = load_golden(name)
+        idx = vlqadc.Index.load(index_path)
+        o = oracle_mod.OracleIndex.load(index_path)
+        for w1, alpha in [(min(idx.k, 16), 0.5), (idx.k, 1.0)]:
+            ids, dists, sc = idx.search(z["queries"][:40], w1=w1, alpha=alpha, k=k, return_scanned=True)
+            oids, od, osc = o.search(z["queries"][:40], w1, alpha, k)
+            assert np.array_equal(ids, oids), (name, w1, alpha, k)
+            assert same_f32(dists, od)
+            assert np.array_equal(sc, osc)
