@@ -714,10 +714,15 @@ def run_group(args, rank, world):
     if torch.cuda.device_count() <= max(devices):
         raise SystemExit(f"bench: --gpus {N} but {torch.cuda.device_count()} visible GPUs")
     udev = sorted(set(devices))
+    # S-way list sharding x N/S replicas (each replica searches 1/(N/S) of the
+    # batch): pure sharding up to 2 GPUs, 2 replicas of an N/2-way sharding
+    # from 4 (the per-GPU work that does not shrink with the shard halves)
+    S = int(os.environ.get("VLQ_GROUP_SHARDS", str(N if N <= 2 else N // 2)))
     from paper_1901_00275_b200 import vlqadc
     w = WORKLOADS[args.workload]
     cfg = config_of(args, w, N)
-    cfg["parallelism"] = f"list-sharded x{N} (hashed cells), one process driving {N} GPUs (vlq_group, NVLink P2P)"
+    cfg["parallelism"] = (f"list-sharded x{S} (hashed cells) x {N // S} replica(s), one process driving {N} GPUs "
+                          f"(vlq_group, NVLink P2P)")
     if os.environ.get("VLQ_GROUP_DEVICES"):
         cfg["parallelism"] += f"; rehearsal on devices {os.environ['VLQ_GROUP_DEVICES']}"
     t0 = time.time()
@@ -729,7 +734,7 @@ def run_group(args, rank, world):
     model = trained.model()
     del trained, sample
     t1 = time.time()
-    grp = vlqadc.IndexGroup.from_model(model, devices)
+    grp = vlqadc.IndexGroup.from_model(model, devices, shards=S)
     grp.add_synthetic(w["n"], clusters=w["clusters"], spread=SPREAD, seed=BASE_SEED)
     t2 = time.time()
     local = grp.local_entries()
@@ -775,6 +780,7 @@ def run_group(args, rank, world):
     scan_ms = [st["phase_ms"]["scan"] / args.steps for st in stats]
     # per GPU: its share of the algorithmic bytes over its own scan time; the
     # line reports the slowest GPU's rate (the one that sets the step)
+    # member g: shard g % S of replica g / S, which searches 1/R of the batch
     shard_bytes = [scan_bytes * local[g] / max(1, sum(local)) for g in range(N)]
     rates = [shard_bytes[g] / (scan_ms[g] / 1e3) / 1e9 if scan_ms[g] > 0 else 0.0 for g in range(N)]
     gslow = int(np.argmax(scan_ms))

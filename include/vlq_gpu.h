@@ -274,7 +274,12 @@ int vlq_gen_synthetic(uint64_t count, uint32_t dim, uint32_t clusters, float spr
  * (peer loads) -- results equal the single-engine search_batch bit for bit.
  * Needs peer access between every pair of distinct devices; a device may be
  * listed more than once.  Calls on one group are serialised internally. */
-int vlq_group_create(const int* devices, uint32_t ndevices, const vlq_config* cfg_or_null, vlq_group** out);
+/* shards (S) must divide ndevices (G): G / S replicas of an S-way list
+ * sharding, each replica searching its own 1/(G/S) of every batch (0: S = G,
+ * pure list sharding).  Replicas cut the per-GPU work that does not shrink
+ * with the shard (per-query tables, re-score, selection hand-off). */
+int vlq_group_create(const int* devices, uint32_t ndevices, uint32_t shards, const vlq_config* cfg_or_null,
+                     vlq_group** out);
 void vlq_group_destroy(vlq_group* g);
 uint32_t vlq_group_size(vlq_group* g);
 /* Index.load / the model half of Index.train / Index.add for every member */

@@ -72,7 +72,7 @@ _SIGS = {
     "vlq_engine_reset_stats": (c_i32, [c_vp]),
     "vlq_engine_get_lists": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "vlq_engine_get_cells": (c_i32, [c_vp, c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
-    "vlq_group_create": (c_i32, [c_vp, c_u32, c_vp, ctypes.POINTER(c_vp)]),
+    "vlq_group_create": (c_i32, [c_vp, c_u32, c_u32, c_vp, ctypes.POINTER(c_vp)]),
     "vlq_group_destroy": (None, [c_vp]),
     "vlq_group_size": (c_u32, [c_vp]),
     "vlq_group_load_vlq1": (c_i32, [c_vp, ctypes.c_char_p]),

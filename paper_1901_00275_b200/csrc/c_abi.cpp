@@ -462,7 +462,7 @@ uint32_t vlq_shard_of_cell(uint32_t cell, uint32_t shards) { return shards ? vlq
 
 // ---- multi-GPU group --------------------------------------------------------
 
-int vlq_group_create(const int* devices, uint32_t ndevices, const vlq_config* cfg, vlq_group** out) {
+int vlq_group_create(const int* devices, uint32_t ndevices, uint32_t shards, const vlq_config* cfg, vlq_group** out) {
     if (!out) return fail(VLQ_ERR_INVALID, "vlq_group_create: out is NULL");
     *out = nullptr;
     return guarded([&] {
@@ -476,7 +476,7 @@ int vlq_group_create(const int* devices, uint32_t ndevices, const vlq_config* cf
         std::vector<int> devs(devices, devices + ndevices);
         auto* g = new vlq_group{nullptr};
         try {
-            g->impl = new vlq::Group(devs, c);
+            g->impl = new vlq::Group(devs, shards, c);
         } catch (...) {
             delete g;
             throw;

@@ -46,9 +46,11 @@ namespace {
 uint64_t slice_per(uint64_t nq, uint32_t G) { return (nq + G - 1) / G; }
 }  // namespace
 
-Group::Group(const std::vector<int>& devices, const EngineConfig& base) : dev_(devices) {
+Group::Group(const std::vector<int>& devices, uint32_t shards, const EngineConfig& base) : dev_(devices) {
     const uint32_t G = (uint32_t)dev_.size();
     if (G == 0 || G > VLQ_MAX_PARTS) throw std::runtime_error("group: need 1..16 devices");
+    shards_ = shards ? shards : G;
+    if (G % shards_ != 0) throw std::runtime_error("group: shards must divide the number of devices");
     int ndev = 0;
     CUDA_CHECK(cudaGetDeviceCount(&ndev));
     for (int d : dev_)
@@ -71,8 +73,8 @@ Group::Group(const std::vector<int>& devices, const EngineConfig& base) : dev_(d
     for (uint32_t g = 0; g < G; g++) {
         EngineConfig c = base;
         c.device = dev_[g];
-        c.shard_rank = (int)g;
-        c.shard_count = (int)G;
+        c.shard_rank = (int)(g % shards_);
+        c.shard_count = (int)shards_;
         eng_.emplace_back(new Engine(c));
         DeviceGuard dg(dev_[g]);
         PerDevice& p = per_[g];
@@ -139,9 +141,16 @@ void Group::add_stream(uint64_t nb, uint64_t chunk, const Engine::ChunkSource& s
     for_each_device([&](uint32_t g) { eng_[g]->add_stream(nb, chunk, src); });
 }
 
+void Group::sub_batch(uint64_t nq, uint32_t r, uint64_t& r0, uint64_t& r1) const {
+    const uint64_t nqr = slice_per(nq, replicas());
+    r0 = std::min(nq, r * nqr);
+    r1 = std::min(nq, r0 + nqr);
+}
+
 void Group::reserve(uint64_t nq, uint32_t w2, uint32_t k) {
     const uint32_t G = size();
-    const uint64_t per = slice_per(nq, G);
+    const uint64_t nqr = slice_per(nq, replicas());
+    const uint64_t per = slice_per(nqr, shards_);
     const uint32_t dim = eng_[0]->dim();
     for (uint32_t g = 0; g < G; g++) {
         DeviceGuard dg(dev_[g]);
@@ -149,9 +158,9 @@ void Group::reserve(uint64_t nq, uint32_t w2, uint32_t k) {
         p.q.alloc(std::max<uint64_t>(1, nq * dim));
         p.sel.alloc(std::max<uint64_t>(1, per * w2));
         p.ab.alloc(std::max<uint64_t>(1, per * w2 * 2));
-        p.lids.alloc(std::max<uint64_t>(1, nq * k));
-        p.ld.alloc(std::max<uint64_t>(1, nq * k));
-        p.lsc.alloc(std::max<uint64_t>(1, nq));
+        p.lids.alloc(std::max<uint64_t>(1, nqr * k));
+        p.ld.alloc(std::max<uint64_t>(1, nqr * k));
+        p.lsc.alloc(std::max<uint64_t>(1, nqr));
         p.oids.alloc(std::max<uint64_t>(1, per * k));
         p.od.alloc(std::max<uint64_t>(1, per * k));
     }
@@ -176,56 +185,64 @@ void Group::upload_queries(const float* q, uint64_t nq, uint32_t dim) {
 }
 
 void Group::enqueue_search(uint64_t nq, uint32_t w1, float alpha, uint32_t k) {
-    const uint32_t G = size();
-    const uint64_t per = slice_per(nq, G);
+    const uint32_t S = shards_, R = replicas();
     const uint32_t dim = eng_[0]->dim();
-    // 1. query-split selection
-    for (uint32_t g = 0; g < G; g++) {
-        PerDevice& p = per_[g];
-        DeviceGuard dg(dev_[g]);
-        const uint64_t lo = std::min(nq, g * per), hi = std::min(nq, lo + per);
-        if (hi > lo)
-            eng_[g]->search_select_device(p.q.p + lo * dim, hi - lo, w1, alpha, p.sel.p, p.ab.p, p.st);
-        CUDA_CHECK(cudaEventRecord(p.ev_sel, p.st));
-    }
-    // 2. sharded fine stage, the selection read from its owners over NVLink
-    SelParts sp{};
-    for (uint32_t g = 0; g < G; g++) {
-        sp.sel[g] = per_[g].sel.p;
-        sp.ab[g] = per_[g].ab.p;
-    }
-    sp.nparts = G;
-    sp.per = per;
-    for (uint32_t g = 0; g < G; g++) {
-        PerDevice& p = per_[g];
-        DeviceGuard dg(dev_[g]);
-        for (uint32_t h = 0; h < G; h++)
-            if (h != g) CUDA_CHECK(cudaStreamWaitEvent(p.st, per_[h].ev_sel, 0));
-        eng_[g]->search_fine_sel_parts(p.q.p, nq, w1, alpha, k, sp, p.lids.p, p.ld.p, p.lsc.p, p.st);
-        CUDA_CHECK(cudaEventRecord(p.ev_fine, p.st));
-    }
-    // 3. each device merges its query slice from every shard's block (peer loads)
-    TopkParts tp{};
-    for (uint32_t g = 0; g < G; g++) {
-        tp.ids[g] = per_[g].lids.p;
-        tp.d[g] = per_[g].ld.p;
-    }
-    tp.nparts = G;
-    for (uint32_t g = 0; g < G; g++) {
-        PerDevice& p = per_[g];
-        DeviceGuard dg(dev_[g]);
-        for (uint32_t h = 0; h < G; h++)
-            if (h != g) CUDA_CHECK(cudaStreamWaitEvent(p.st, per_[h].ev_fine, 0));
-        const uint64_t lo = std::min(nq, g * per), hi = std::min(nq, lo + per);
-        launch_merge_topk_parts(tp, lo, hi - lo, k, p.oids.p, p.od.p, p.st);
-        CUDA_CHECK(cudaEventRecord(p.ev_done, p.st));
-    }
-    // no device may reuse its selection / result buffers (next batch) before
-    // every peer finished reading them
-    for (uint32_t g = 0; g < G; g++) {
-        DeviceGuard dg(dev_[g]);
-        for (uint32_t h = 0; h < G; h++)
-            if (h != g) CUDA_CHECK(cudaStreamWaitEvent(per_[g].st, per_[h].ev_done, 0));
+    for (uint32_t r = 0; r < R; r++) {  // replicas work on disjoint query sub-batches, independently
+        uint64_t r0, r1;
+        sub_batch(nq, r, r0, r1);
+        const uint64_t nqr = r1 - r0, per = slice_per(nqr, S);
+        auto mem = [&](uint32_t s) { return r * S + s; };
+        // 1. query-split selection inside the replica
+        for (uint32_t s = 0; s < S; s++) {
+            PerDevice& p = per_[mem(s)];
+            DeviceGuard dg(dev_[mem(s)]);
+            const uint64_t lo = std::min(nqr, s * per), hi = std::min(nqr, lo + per);
+            if (hi > lo)
+                eng_[mem(s)]->search_select_device(p.q.p + (r0 + lo) * dim, hi - lo, w1, alpha, p.sel.p, p.ab.p,
+                                                   p.st);
+            CUDA_CHECK(cudaEventRecord(p.ev_sel, p.st));
+        }
+        // 2. sharded fine stage, the selection read from its owners over NVLink
+        SelParts sp{};
+        for (uint32_t s = 0; s < S; s++) {
+            sp.sel[s] = per_[mem(s)].sel.p;
+            sp.ab[s] = per_[mem(s)].ab.p;
+        }
+        sp.nparts = S;
+        sp.per = per;
+        for (uint32_t s = 0; s < S; s++) {
+            PerDevice& p = per_[mem(s)];
+            DeviceGuard dg(dev_[mem(s)]);
+            for (uint32_t h = 0; h < S; h++)
+                if (h != s) CUDA_CHECK(cudaStreamWaitEvent(p.st, per_[mem(h)].ev_sel, 0));
+            if (nqr > 0)
+                eng_[mem(s)]->search_fine_sel_parts(p.q.p + r0 * dim, nqr, w1, alpha, k, sp, p.lids.p, p.ld.p,
+                                                    p.lsc.p, p.st);
+            CUDA_CHECK(cudaEventRecord(p.ev_fine, p.st));
+        }
+        // 3. each device merges its query slice from every shard's block (peer loads)
+        TopkParts tp{};
+        for (uint32_t s = 0; s < S; s++) {
+            tp.ids[s] = per_[mem(s)].lids.p;
+            tp.d[s] = per_[mem(s)].ld.p;
+        }
+        tp.nparts = S;
+        for (uint32_t s = 0; s < S; s++) {
+            PerDevice& p = per_[mem(s)];
+            DeviceGuard dg(dev_[mem(s)]);
+            for (uint32_t h = 0; h < S; h++)
+                if (h != s) CUDA_CHECK(cudaStreamWaitEvent(p.st, per_[mem(h)].ev_fine, 0));
+            const uint64_t lo = std::min(nqr, s * per), hi = std::min(nqr, lo + per);
+            launch_merge_topk_parts(tp, lo, hi - lo, k, p.oids.p, p.od.p, p.st);
+            CUDA_CHECK(cudaEventRecord(p.ev_done, p.st));
+        }
+        // no device may reuse its selection / result buffers (next batch) before
+        // every peer of its replica finished reading them
+        for (uint32_t s = 0; s < S; s++) {
+            DeviceGuard dg(dev_[mem(s)]);
+            for (uint32_t h = 0; h < S; h++)
+                if (h != s) CUDA_CHECK(cudaStreamWaitEvent(per_[mem(s)].st, per_[mem(h)].ev_done, 0));
+        }
     }
 }
 
@@ -266,22 +283,29 @@ float Group::search_resident(uint32_t w1, float alpha, uint32_t k) {
 
 void Group::results(int64_t* ids, float* dists, uint64_t* scanned) {
     const uint64_t nq = nq_q_;
-    const uint32_t G = size(), k = last_k_;
-    const uint64_t per = slice_per(nq, G);
-    std::vector<uint64_t> sc(scanned ? nq : 0);
-    for (uint32_t g = 0; g < G; g++) {
+    const uint32_t S = shards_, k = last_k_;
+    std::vector<uint64_t> sc;
+    for (uint32_t g = 0; g < size(); g++) {
+        const uint32_t r = g / S, s = g % S;
+        uint64_t r0, r1;
+        sub_batch(nq, r, r0, r1);
+        const uint64_t nqr = r1 - r0, per = slice_per(nqr, S);
         DeviceGuard dg(dev_[g]);
         PerDevice& p = per_[g];
-        const uint64_t lo = std::min(nq, g * per), hi = std::min(nq, lo + per);
+        const uint64_t lo = std::min(nqr, s * per), hi = std::min(nqr, lo + per);
         if (hi > lo) {
-            if (ids) CUDA_CHECK(cudaMemcpyAsync(ids + lo * k, p.oids.p, (hi - lo) * k * 8, cudaMemcpyDeviceToHost, p.st));
+            if (ids)
+                CUDA_CHECK(cudaMemcpyAsync(ids + (r0 + lo) * k, p.oids.p, (hi - lo) * k * 8, cudaMemcpyDeviceToHost,
+                                           p.st));
             if (dists)
-                CUDA_CHECK(cudaMemcpyAsync(dists + lo * k, p.od.p, (hi - lo) * k * 4, cudaMemcpyDeviceToHost, p.st));
+                CUDA_CHECK(cudaMemcpyAsync(dists + (r0 + lo) * k, p.od.p, (hi - lo) * k * 4,
+                                           cudaMemcpyDeviceToHost, p.st));
         }
         CUDA_CHECK(cudaStreamSynchronize(p.st));
-        if (scanned) {  // reference-semantics scanned count = the sum over the shards
-            CUDA_CHECK(cudaMemcpy(sc.data(), p.lsc.p, nq * 8, cudaMemcpyDeviceToHost));
-            for (uint64_t q = 0; q < nq; q++) scanned[q] = (g == 0 ? 0 : scanned[q]) + sc[q];
+        if (scanned && nqr > 0) {  // reference-semantics scanned count = the sum over the replica's shards
+            sc.resize(nqr);
+            CUDA_CHECK(cudaMemcpy(sc.data(), p.lsc.p, nqr * 8, cudaMemcpyDeviceToHost));
+            for (uint64_t q = 0; q < nqr; q++) scanned[r0 + q] = (s == 0 ? 0 : scanned[r0 + q]) + sc[q];
         }
     }
 }

@@ -17,12 +17,16 @@ namespace vlq {
 
 class Group {
 public:
-    Group(const std::vector<int>& devices, const EngineConfig& base);
+    // shards S divides G = devices.size(): G / S replicas of an S-way list
+    // sharding; member g is shard g % S of replica g / S (0: S = G)
+    Group(const std::vector<int>& devices, uint32_t shards, const EngineConfig& base);
     ~Group();
     Group(const Group&) = delete;
     Group& operator=(const Group&) = delete;
 
     uint32_t size() const { return (uint32_t)eng_.size(); }
+    uint32_t shards() const { return shards_; }
+    uint32_t replicas() const { return size() / shards_; }
     Engine& engine(uint32_t g) { return *eng_[g]; }
     int device(uint32_t g) const { return dev_[g]; }
     uint64_t local_entries(uint32_t g) const;
@@ -49,9 +53,9 @@ private:
         DevBuf<float> q;         // the whole batch [nq, dim]
         DevBuf<uint32_t> sel;    // this device's query slice: selected cells [per, w2]
         DevBuf<float> ab;        //                             exact (a, b) [per, w2, 2]
-        DevBuf<int64_t> lids;    // this shard's exact top-k, whole batch [nq, k]
+        DevBuf<int64_t> lids;    // this shard's exact top-k, its replica's sub-batch [nq_r, k]
         DevBuf<float> ld;
-        DevBuf<uint64_t> lsc;    // this shard's scanned counts [nq]
+        DevBuf<uint64_t> lsc;    // this shard's scanned counts [nq_r]
         DevBuf<int64_t> oids;    // merged top-k of this device's query slice [per, k]
         DevBuf<float> od;
     };
@@ -60,7 +64,10 @@ private:
     void enqueue_search(uint64_t nq, uint32_t w1, float alpha, uint32_t k);
     void check_errors();
 
+    // replica r's query sub-batch [r0, r1) of an nq batch; shard slices inside it
+    void sub_batch(uint64_t nq, uint32_t r, uint64_t& r0, uint64_t& r1) const;
     std::vector<int> dev_;
+    uint32_t shards_ = 1;
     std::vector<std::unique_ptr<Engine>> eng_;
     std::deque<PerDevice> per_;  // deque: PerDevice (DevBuf) is neither copyable nor movable
     void* pin_ = nullptr;

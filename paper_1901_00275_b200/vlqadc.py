@@ -342,13 +342,17 @@ class IndexGroup:
     per-slice (dist, id) merge of the shards' top-k from peer memory.
     Results equal Index.search on the unsharded index bit for bit."""
 
-    def __init__(self, devices, *, workspace_bytes: int = 0, max_tile: int = 0, force_exact: bool = False):
+    def __init__(self, devices, *, shards: int = 0, workspace_bytes: int = 0, max_tile: int = 0,
+                 force_exact: bool = False):
+        """shards S divides len(devices) = G: G / S replicas of an S-way list
+        sharding (0: S = G)."""
         devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
         cfg = _lib.VlqConfig(0, 0, 1, workspace_bytes, max_tile, int(force_exact))
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().vlq_group_create(devs, len(devices), ctypes.byref(cfg), ctypes.byref(h)))
+        _lib.check(_lib.lib().vlq_group_create(devs, len(devices), shards, ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
         self.devices = [int(d) for d in devices]
+        self.shards = shards or len(devices)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -360,7 +364,7 @@ class IndexGroup:
             self._h = None
 
     @staticmethod
-    def load(path: str, devices, **kw) -> "IndexGroup":
+    def load(path: str, devices, **kw) -> "IndexGroup":  # kw: shards, workspace_bytes, ...
         g = IndexGroup(devices, **kw)
         _lib.check(_lib.lib().vlq_group_load_vlq1(g._h, os.fsencode(str(path))))
         return g
@@ -443,6 +447,10 @@ class IndexGroup:
 
     def local_entries(self) -> list[int]:
         return [int(self.info(g).local_entries) for g in range(len(self))]
+
+    @property
+    def replicas(self) -> int:
+        return len(self) // self.shards
 
 
 class IvfBaselineIndex:

@@ -24,13 +24,16 @@ def same_f32(a, b):
     return np.array_equal(np.asarray(a, np.float32).view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
 
 
-@pytest.mark.parametrize("G", [1, 2, 3, 5])
+@pytest.mark.parametrize("G,S", [(1, 0), (2, 0), (3, 0), (5, 0), (4, 2), (6, 3), (4, 1)])
 @pytest.mark.parametrize("name", ["accept_small", "m16", "unclamped"])
-def test_group_search_matches_reference_golden(vlqadc, name, G):
+def test_group_search_matches_reference_golden(vlqadc, name, G, S):
+    """G members as G / S replicas of an S-way list sharding (S = 0: G)."""
     z, index_path, _ = load_golden(name)
-    grp = vlqadc.IndexGroup.load(index_path, [0] * G)
-    assert len(grp) == G
-    assert sum(grp.local_entries()) == grp.ntotal
+    grp = vlqadc.IndexGroup.load(index_path, [0] * G, shards=S)
+    assert len(grp) == G and grp.replicas * grp.shards == G
+    ent = grp.local_entries()
+    for r in range(grp.replicas):  # every replica holds the whole index, split into its shards
+        assert sum(ent[r * grp.shards:(r + 1) * grp.shards]) == grp.ntotal
     for gi, (w1, alpha, k) in enumerate(grid_of(z)):
         ids, dists, scanned = grp.search(z["queries"], w1=w1, alpha=alpha, k=k, return_scanned=True)
         assert np.array_equal(ids, z[f"ids_{gi}"]), (name, G, gi)
@@ -44,7 +47,7 @@ def test_group_add_and_resident_search_match_single_engine(vlqadc, oracle_mod):
     single = vlqadc.Index.load(model_path)
     single.add(base)
     model = single.model()
-    grp = vlqadc.IndexGroup.from_model(model, [0, 0, 0, 0])
+    grp = vlqadc.IndexGroup.from_model(model, [0, 0, 0, 0, 0, 0], shards=3)
     grp.add(base)
     assert grp.ntotal == single.ntotal
     o = oracle_mod.OracleIndex.load(index_path)
@@ -77,7 +80,7 @@ def test_group_tensor_core_chunk_select_path(vlqadc, oracle_mod, tmp_path, monke
     path = str(tmp_path / "g16k.vlq")
     idx.save(path)
     o = oracle_mod.OracleIndex.load(path)
-    grp = vlqadc.IndexGroup.load(path, [0, 0, 0])
+    grp = vlqadc.IndexGroup.load(path, [0, 0, 0, 0], shards=2)
     for w1, alpha, k in [(64, 0.25, 100), (16, 0.5, 10), (200, 0.1, 20)]:
         ids, d = grp.search(q, w1=w1, alpha=alpha, k=k)
         oids, od, _ = o.search(q, w1, alpha, k)
@@ -93,5 +96,7 @@ def test_group_errors(vlqadc):
         grp.search(np.zeros((3, grp.info().dim + 1), np.float32), w1=4, alpha=0.5, k=10)
     with pytest.raises(RuntimeError, match="device index out of range"):
         vlqadc.IndexGroup([0, 99])
+    with pytest.raises(RuntimeError, match="shards must divide"):
+        vlqadc.IndexGroup([0, 0, 0], shards=2)
     with pytest.raises(RuntimeError, match="index already holds a base set"):
         grp.add(regen_base(z))
