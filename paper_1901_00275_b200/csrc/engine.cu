@@ -75,7 +75,6 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
 
 Engine::~Engine() {
     if (flusher_.joinable()) flusher_.join();
-    if (t5tex_) cudaDestroyTextureObject(t5tex_);
     for (auto& sl : prof_) {
         for (auto& e : sl.ev)
             if (e) cudaEventDestroy(e);
@@ -966,27 +965,6 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
         a.scan_cap = cfg_.scan_cap;
-        a.lut_split = cfg_.scan_lut_split;
-        if (a.lut_split && m_ == 16) {  // study knob: a texture object over this tile's term5 tables
-            const size_t bytes = (size_t)nt * m_ * VLQ_KSUB * 4;
-            if (t5tex_ && (t5tex_ptr_ != t5_.p || t5tex_bytes_ < bytes)) {
-                CUDA_CHECK(cudaDestroyTextureObject(t5tex_));
-                t5tex_ = 0;
-            }
-            if (!t5tex_) {
-                cudaResourceDesc rd{};
-                rd.resType = cudaResourceTypeLinear;
-                rd.res.linear.devPtr = t5_.p;
-                rd.res.linear.desc = cudaCreateChannelDesc<float>();
-                rd.res.linear.sizeInBytes = t5_.n * 4;
-                cudaTextureDesc td{};
-                td.readMode = cudaReadModeElementType;
-                CUDA_CHECK(cudaCreateTextureObject(&t5tex_, &rd, &td, nullptr));
-                t5tex_ptr_ = t5_.p;
-                t5tex_bytes_ = t5_.n * 4;
-            }
-            a.t5tex = t5tex_;
-        }
         a.sel_agg = cfg_.scan_sel_agg != 0;
         a.flush_exact = cfg_.scan_flush_exact != 0;
         const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
@@ -1068,7 +1046,6 @@ uint32_t Engine::scan_keep(uint32_t topk) const {
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
-    else if (key == "scan_lut_split") cfg_.scan_lut_split = (int)value;
     else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;
     else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;
     else if (key == "force_exact") cfg_.force_exact = (int)value;

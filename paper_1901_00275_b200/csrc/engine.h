@@ -37,7 +37,6 @@ struct EngineConfig {
     int scan_slots = 0;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8; +100 = 4 CTAs/SM);
                            // 0 = auto: 6 (3 CTAs/SM), or 104 on shards of >= 4 (1/4 or less of the
                            // entries per query: measured 3% faster at 8 shards, neutral unsharded)
-    int scan_lut_split = 0;   // study knob: LUT lookups partly via __ldg / texture fetches (scan_fast.cu)
     float cert_slack = 0.0f;  // test knob (cert_slack_milli): widens the re-score certificate -> retry / exact paths
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
@@ -364,9 +363,6 @@ private:
 
     // search workspace
     DevBuf<float> ws_, dbuf_, t5_;
-    cudaTextureObject_t t5tex_ = 0;  // scan_lut_split study
-    const float* t5tex_ptr_ = nullptr;
-    size_t t5tex_bytes_ = 0;
     DevBuf<uint32_t> top_, sel_, qlist_, cand_top_;
     DevBuf<uint64_t> cand_, cand2_;  // fast-scan survivors (k') / of the retry pass (4 k')
     DevBuf<uint32_t> qlist2_;

@@ -57,9 +57,6 @@ struct SearchArgs {
     // qlist[b] (blocks >= *qcount exit) and its cand row is b, not q
     const uint32_t* qlist;
     const unsigned int* qcount;
-    // study: LUT lookups partly through global (__ldg) / texture loads (scan_fast.cu)
-    int lut_split = 0;
-    unsigned long long t5tex = 0;  // cudaTextureObject_t over t5
 };
 
 // Add-path device views.

@@ -181,14 +181,6 @@ __global__ void k_pack_eterm_lam(const float* __restrict__ eterm, const uint8_t*
 // LUT[p][code_p]: the byte is extracted with one LOP3 / PRMT / SHF and the
 // shared load scales it (LDS [R.X4 + imm]), so a lookup is 2 instructions
 template <int M>
-__device__ __forceinline__ uint32_t code_byte_t(const uint32_t (&w)[(M + 3) / 4], int p) {
-    const uint32_t word = w[p >> 2];
-    const int k = p & 3;
-    return k == 0 ? (word & 0xffu) : (k == 3 ? (word >> 24) : __byte_perm(word, 0u, 0x4440u + k));
-}
-#define code_byte(w, p) code_byte_t<M>(w, p)
-
-template <int M>
 __device__ __forceinline__ float lut_at(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], int p) {
     const uint32_t word = w[p >> 2];
     const int k = p & 3;
@@ -201,10 +193,7 @@ __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an ord
     return __uint_as_float((ub & 0x80000000u) ? (ub & 0x7fffffffu) : ~ub);
 }
 
-// NG / NT (study): the last NT sub-spaces' lookups go through the texture
-// path (tex1Dfetch on the query's t5 row), the NG before them through
-// non-coherent global loads (__ldg, L1-resident), instead of shared memory
-template <int M, int U, int MINB, int NG = 0, int NT = 0>
+template <int M, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -225,10 +214,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
 
     // 1. the query's term5 table (one copy per sub-space)
     const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
-    const float* t5f = a.t5 + q * M * VLQ_KSUB;
-    const uint32_t t5off = (uint32_t)(q * M * VLQ_KSUB);
-    (void)t5f;
-    (void)t5off;
     for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
@@ -350,21 +335,8 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                     const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
                     float2 s = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
 #pragma unroll
-                    for (int p = 1; p < M; p++) {
-                        float2 v;
-                        if (p < M - NG - NT) {
-                            v = make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p));
-                        } else {
-                            const uint32_t b0 = code_byte(cw[u], p), b1 = code_byte(cw[u + 1], p);
-                            if (p < M - NT) {
-                                v = make_float2(__ldg(t5f + p * 256 + b0), __ldg(t5f + p * 256 + b1));
-                            } else {
-                                v = make_float2(tex1Dfetch<float>(a.t5tex, (int)(t5off + p * 256 + b0)),
-                                                tex1Dfetch<float>(a.t5tex, (int)(t5off + p * 256 + b1)));
-                            }
-                        }
-                        s = __fadd2_rn(s, v);
-                    }
+                    for (int p = 1; p < M; p++)
+                        s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
                     const float2 d = __ffma2_rn(m2, s, te);
                     dist[u] = d.x;
                     dist[u + 1] = d.y;
@@ -470,13 +442,6 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
               : su == 104 ? dev::k_scan_fast2<M, 4, 4>
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
                           : dev::k_scan_fast2<M, 6, 3>;
-    if constexpr (M == 16) {  // study: part of the LUT lookups off the shared-memory pipe
-        if (a.lut_split == 1) fn = dev::k_scan_fast2<M, 6, 3, 4, 0>;
-        else if (a.lut_split == 2) fn = dev::k_scan_fast2<M, 6, 3, 0, 4>;
-        else if (a.lut_split == 3) fn = dev::k_scan_fast2<M, 6, 3, 0, 2>;
-        else if (a.lut_split == 4) fn = dev::k_scan_fast2<M, 6, 3, 2, 2>;
-        else if (a.lut_split == 5) fn = dev::k_scan_fast2<M, 6, 3, 0, 6>;
-    }
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
