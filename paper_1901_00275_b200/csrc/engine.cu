@@ -974,7 +974,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         if (!fast_kind || !launch_scan_fast(a, nt, w2, keep, slots, st))
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         mark(PH_RESCORE);
-        launch_rescore(a, nt, keep, topk, d_ids, d_dists, st);
+        launch_rescore(a, nt, w2, keep, topk, d_ids, d_dists, st);
         mark(PH_FALLBACK);
         CUDA_CHECK(cudaMemsetAsync(err_.p + 2, 0, 4, st));
         launch_compact_flags(meta_.p, nt, qlist_.p, err_.p + 2, st);
@@ -993,7 +993,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             r.qlist = qlist_.p;
             r.qcount = err_.p + 2;
             launch_scan_fast(r, nt, w2, keep2, slots, st);
-            launch_rescore(r, nt, keep2, topk, d_ids, d_dists, st);
+            launch_rescore(r, nt, w2, keep2, topk, d_ids, d_dists, st);
             CUDA_CHECK(cudaMemsetAsync(cnt2_.p, 0, 4, st));
             launch_compact_flags(meta_.p, nt, qlist2_.p, cnt2_.p, st);
             launch_scan(a, nt, w2, keep_x, buf_x, warps_x, false, qlist2_.p, cnt2_.p, st);

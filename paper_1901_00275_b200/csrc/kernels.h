@@ -117,8 +117,8 @@ void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t ke
 // eterm_lam[e] = (bits(eterm[e]) & ~0xff) | lambdas[e]
 void launch_pack_eterm_lam(const float* eterm, const uint8_t* lambdas, uint64_t n, uint32_t* out, cudaStream_t st);
 bool launch_scan_fast(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int slots, cudaStream_t st);
-void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
-                    cudaStream_t st);
+void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, uint32_t topk, int64_t* out_ids,
+                    float* out_d, cudaStream_t st);
 void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,
                        uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d, cudaStream_t st);
 // select_topk for k > 1024 (large_k.cu): exact keys of every scanned entry,

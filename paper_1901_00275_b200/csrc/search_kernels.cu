@@ -437,52 +437,85 @@ __global__ void __launch_bounds__(256) k_scan(SearchArgs a, uint32_t w2, uint32_
 // certificate: with eps bounding |fast - exact| for every scanned entry,
 // fast_k' - eps > exact_k proves that no dropped entry can enter the top-k.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t find_cell(const uint64_t* __restrict__ off, uint32_t ncell,
-                                              uint64_t pos) {
-    // largest c with off[c] <= pos (and off[c+1] > pos)
-    uint32_t lo = 0, hi = ncell;  // invariant: off[lo] <= pos < off[hi]
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (off[mid] <= pos) lo = mid;
-        else hi = mid;
-    }
-    return lo;
-}
 
-__global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t keep, uint32_t topk,
+// Exact re-score of the k' fast-scan survivors.  The survivor's cell is found
+// by a binary search over the query's OWN selected cells' list starts (staged
+// in shared memory: ~9 steps) instead of all K n list offsets in global memory
+// (~21 dependent loads), and for m in {4, 8, 16} the 4 m table gathers of a
+// survivor are unrolled so they are all in flight at once; the sums keep the
+// reference's sequential order (adc_distance, search.cpp:92-120).
+template <int M>
+__global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t topk,
                                                  int64_t* __restrict__ out_ids, float* __restrict__ out_d) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // keep (power of two)
+    uint64_t* cstart = keys + keep;                        // w2: list start of selected cell t
+    uint32_t* ccell = reinterpret_cast<uint32_t*>(cstart + w2);
     __shared__ float s_fast_last;
     if (a.qlist && blockIdx.x >= *a.qcount) return;
     const uint64_t q = a.qlist ? a.qlist[blockIdx.x] : blockIdx.x;
-    const uint32_t m = a.m;
+    const uint32_t m = M > 0 ? (uint32_t)M : a.m;
     const uint64_t* candq = a.cand + (a.qlist ? (uint64_t)blockIdx.x : q) * keep;
     const float* wsq = a.ws + q * a.k;
     const float* t5q = a.t5 + q * m * VLQ_KSUB;
     const uint64_t scanned = a.meta[q].scanned;
     const uint32_t have = (uint32_t)dev::umin64(scanned, keep);
-    const uint32_t ncell = a.k * a.n;
+    const uint32_t* selq = a.sel + q * w2;
+    for (uint32_t t = threadIdx.x; t < w2; t += blockDim.x) {
+        const uint32_t c = selq[t];  // ascending cell ids, so ascending list starts
+        ccell[t] = c;
+        cstart[t] = a.list_off[c];
+    }
+    __syncthreads();
     for (uint32_t t = threadIdx.x; t < keep; t += blockDim.x) {
         uint64_t key = ~0ull;
         if (t < have) {
             const uint64_t ck = candq[t];
             const uint64_t pos = (uint32_t)ck;
-            const uint32_t cell = find_cell(a.list_off, ncell, pos);
+            uint32_t lo = 0, hi = w2;  // the last selected cell whose list starts at or before pos
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (cstart[mid] <= pos) lo = mid;
+                else hi = mid;
+            }
+            const uint32_t cell = ccell[lo];
             const uint32_t i = cell / a.n;
             const uint32_t s = a.nbr[cell];
             const float lam = dequantize_lambda(a.lambdas[pos], a.lo, a.hi);
             const float d = line_sqdist(wsq[i], wsq[s], a.elen[cell], lam);
-            const uint8_t* code = a.codes + pos * m;
             const float* t3i = a.t3 + (uint64_t)i * m * VLQ_KSUB;
             const float* t3s = a.t3 + (uint64_t)s * m * VLQ_KSUB;
             float s2 = 0.0f, s3 = 0.0f, s4 = 0.0f, s5 = 0.0f;
-            for (uint32_t p = 0; p < m; p++) {
-                const uint32_t c = code[p];
-                s2 = __fadd_rn(s2, a.t2[p * VLQ_KSUB + c]);
-                s3 = __fadd_rn(s3, t3i[p * VLQ_KSUB + c]);
-                s4 = __fadd_rn(s4, t3s[p * VLQ_KSUB + c]);
-                s5 = __fadd_rn(s5, t5q[p * VLQ_KSUB + c]);
+            if constexpr (M > 0) {
+                uint8_t code[M];
+                if constexpr (M == 16) *reinterpret_cast<uint4*>(code) = __ldg(reinterpret_cast<const uint4*>(a.codes + pos * 16));
+                else if constexpr (M == 8) *reinterpret_cast<uint2*>(code) = __ldg(reinterpret_cast<const uint2*>(a.codes + pos * 8));
+                else *reinterpret_cast<uint32_t*>(code) = __ldg(reinterpret_cast<const uint32_t*>(a.codes + pos * 4));
+                float v2[M], v3[M], v4[M], v5[M];
+#pragma unroll
+                for (int p = 0; p < M; p++) {  // every gather in flight at once
+                    const uint32_t c = code[p];
+                    v2[p] = __ldg(a.t2 + p * VLQ_KSUB + c);
+                    v3[p] = __ldg(t3i + p * VLQ_KSUB + c);
+                    v4[p] = __ldg(t3s + p * VLQ_KSUB + c);
+                    v5[p] = t5q[p * VLQ_KSUB + c];
+                }
+#pragma unroll
+                for (int p = 0; p < M; p++) {
+                    s2 = __fadd_rn(s2, v2[p]);
+                    s3 = __fadd_rn(s3, v3[p]);
+                    s4 = __fadd_rn(s4, v4[p]);
+                    s5 = __fadd_rn(s5, v5[p]);
+                }
+            } else {
+                const uint8_t* code = a.codes + pos * m;
+                for (uint32_t p = 0; p < m; p++) {
+                    const uint32_t c = code[p];
+                    s2 = __fadd_rn(s2, a.t2[p * VLQ_KSUB + c]);
+                    s3 = __fadd_rn(s3, t3i[p * VLQ_KSUB + c]);
+                    s4 = __fadd_rn(s4, t3s[p * VLQ_KSUB + c]);
+                    s5 = __fadd_rn(s5, t5q[p * VLQ_KSUB + c]);
+                }
             }
             float r = __fadd_rn(d, s2);
             r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, __fsub_rn(1.0f, lam)), s3));
@@ -611,9 +644,13 @@ void launch_scan(const SearchArgs& a, uint64_t nblocks, uint32_t w2, uint32_t ke
     }
 }
 
-void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d,
-                    cudaStream_t st) {
-    dev::k_rescore<<<(unsigned)nq, 256, keep * sizeof(uint64_t), st>>>(a, keep, topk, out_ids, out_d);
+void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, uint32_t topk, int64_t* out_ids,
+                    float* out_d, cudaStream_t st) {
+    const size_t smem = keep * sizeof(uint64_t) + (size_t)w2 * 12;
+    auto fn = a.m == 16 ? dev::k_rescore<16> : a.m == 8 ? dev::k_rescore<8> : a.m == 4 ? dev::k_rescore<4>
+                                                                                          : dev::k_rescore<0>;
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
     CUDA_LAUNCH_CHECK();
 }
 
