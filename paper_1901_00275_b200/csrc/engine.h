@@ -41,6 +41,7 @@ struct EngineConfig {
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
+    uint32_t scan_round_cap = 0; // study knob: most chunks per warp between the fast scan's block barriers (0 = 32)
     int scan_retry = 1;          // certificate failures: fast scan again with 4x k' before the exact scan
     int scan_adapt_keep = 1;     // raise k' (x2, up to x4) after a batch whose certificate failed for > 2% of queries
     uint32_t scan_keep_min = 0;  // study knob: lower bound on k' (fast-scan survivors)

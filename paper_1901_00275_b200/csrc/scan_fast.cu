@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
         const uint64_t per_chunk_round = (uint64_t)nwarps * CH;
         uint64_t rn = (s_tau == ~0ull) ? free_slots / per_chunk_round
                                        : ((uint64_t)free_slots * n_seen) / (4ull * keep * per_chunk_round);
-        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > 32 ? 32ull : rn));
+        const uint64_t rcap = a.round_cap ? a.round_cap : 32u;
+        rlen = (uint32_t)(rn < 1 ? 1ull : (rn > rcap ? rcap : rn));
     }
     uint32_t n = s_count;
     if (n > keep) {
