@@ -679,7 +679,7 @@ def main():
             "cpu_baseline": cpu, "gpu_launches": stats["launches"] + (args.steps if world > 1 else 0),
             "coarse_stage": ("query-split first level + cell selection (1/N of the batch per rank), "
                              "selections all-gathered") if world > 1 else "single GPU",
-            "ivfadc": ivf_line, "sweep": sweep, "add_replay": replay,
+            "ivfadc": ivf_line, "sweep": sweep, "add_replay": replay, "workload_shape": shape,
             "clocks": clk, "setup": setup, "scanned_per_query": round(local_scanned / nq, 1) if world == 1 else None,
             "fallback_queries_per_step": stats["flagged"] / args.steps,
             "tc_coarse_fallbacks_per_step": stats["tc_fallbacks"] / args.steps}
