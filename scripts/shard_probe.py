@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--w1", type=int, default=64)
     ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--replicas", type=int, default=1,
+                    help="R: the member's replica searches nq/R queries (vlq_group with N = R x S GPUs)")
     ap.add_argument("--configs", nargs="*", default=[""],
                     help="set_tuning key=value lists to time fine_sel under (first = the reported one)")
     args = ap.parse_args()
@@ -69,6 +71,8 @@ def main():
             tot += e0.elapsed_time(e1)
         return tot / args.steps
 
+    nq_all = nq
+    nq = (nq_all + args.replicas - 1) // args.replicas  # this member's replica's part of the batch
     for spec in args.shards.split(","):
         G, rank = (int(x) for x in spec.split(":"))
         idx, setup = bench.build_index(vlqadc, w, 0, rank, G)
@@ -115,7 +119,8 @@ def main():
         t_fine_top = timed(lambda: idx.search_fine_device(q.data_ptr(), nq, w1, alpha, k, top.data_ptr(),
                                                           ids.data_ptr(), dists.data_ptr(), scanned.data_ptr(), st))
         steps = args.steps + 2  # timed() runs 2 warm-up calls inside the profiled window
-        line = {"workload": args.workload, "G": G, "rank": rank, "nq": nq, "w1": w1, "alpha": alpha, "k": k,
+        line = {"workload": args.workload, "G": G, "rank": rank, "replicas": args.replicas, "nq_batch": nq_all,
+                "nq": nq, "w1": w1, "alpha": alpha, "k": k,
                 "local_entries": idx.local_entries,
                 "scanned_local_per_query": round(float(scanned.sum().item()) / nq, 1),
                 "select_split_ms": {"select_slice": round(t_sel, 3), "fine_sel": round(t_fine, 3),
