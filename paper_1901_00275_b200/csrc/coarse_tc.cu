@@ -917,8 +917,10 @@ __global__ void k_exact_rows(const float* __restrict__ Y, uint32_t dim, const fl
                              float* __restrict__ ws, const uint32_t* __restrict__ qlist,
                              const unsigned int* __restrict__ count) {
     extern __shared__ float ysm[];
-    if (blockIdx.x >= *count) return;
-    const uint64_t q = qlist[blockIdx.x];
+
+    const uint32_t _nb = *count;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+    const uint64_t q = qlist[_b];
     for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ysm[d] = Y[q * dim + d];
     __syncthreads();
     for (uint32_t c = threadIdx.x; c < k; c += blockDim.x) {
@@ -927,6 +929,8 @@ __global__ void k_exact_rows(const float* __restrict__ Y, uint32_t dim, const fl
         for (uint32_t d = 0; d < dim; d++) acc = sq_step(acc, ysm[d], cp[d]);
         ws[q * k + c] = acc;
     }
+    __syncthreads();  // shared memory is reused by the next query
+    }
 }
 
 __global__ void __launch_bounds__(512) k_first_level_list(const float* __restrict__ ws, uint32_t k, uint32_t w1,
@@ -934,9 +938,13 @@ __global__ void __launch_bounds__(512) k_first_level_list(const float* __restric
                                                           const unsigned int* __restrict__ count) {
     __shared__ uint32_t hist[2048];
     __shared__ uint32_t scan[40];
-    if (blockIdx.x >= *count) return;
-    const uint64_t q = qlist[blockIdx.x];
+
+    const uint32_t _nb = *count;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+    const uint64_t q = qlist[_b];
     block_select_ordered(ws + q * k, k, w1, top + q * w1, hist, scan);
+    __syncthreads();  // shared memory is reused by the next query
+    }
 }
 
 }  // namespace dev
@@ -1012,14 +1020,14 @@ void launch_refine_list(const float* Y, uint64_t nq, uint32_t dim, const float* 
 void launch_exact_rows(const float* Y, uint64_t nq, uint32_t dim, const float* C, uint32_t k, float* ws,
                        const uint32_t* qlist, const unsigned int* count, cudaStream_t st) {
     if (nq == 0) return;
-    dev::k_exact_rows<<<(unsigned)nq, 256, dim * 4, st>>>(Y, dim, C, k, ws, qlist, count);
+    dev::k_exact_rows<<<list_grid(nq, true), 256, dim * 4, st>>>(Y, dim, C, k, ws, qlist, count);
     CUDA_LAUNCH_CHECK();
 }
 
 void launch_first_level_list(const float* ws, uint64_t nq, uint32_t k, uint32_t w1, uint32_t* top,
                              const uint32_t* qlist, const unsigned int* count, cudaStream_t st) {
     if (nq == 0) return;
-    dev::k_first_level_list<<<(unsigned)nq, 512, 0, st>>>(ws, k, w1, top, qlist, count);
+    dev::k_first_level_list<<<list_grid(nq, true), 512, 0, st>>>(ws, k, w1, top, qlist, count);
     CUDA_LAUNCH_CHECK();
 }
 

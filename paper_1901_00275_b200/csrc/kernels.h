@@ -8,6 +8,14 @@
 
 namespace vlq {
 
+// grid of the kernels launched over a device-side query list (certificate
+// failures, overflow rows): a small grid strides over the list, so an empty
+// list costs one short launch instead of one block per query of the tile
+constexpr uint32_t VLQ_LIST_GRID = 592;
+inline unsigned list_grid(uint64_t nblocks, bool is_list) {
+    return (unsigned)(is_list && nblocks > VLQ_LIST_GRID ? VLQ_LIST_GRID : nblocks);
+}
+
 struct QueryMeta {
     unsigned long long scanned;  // reference-semantics scanned candidates (search.cpp:163-165)
     float dmax;                  // bound on |term1| over the query's selected cells

@@ -201,8 +201,10 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     constexpr uint32_t CH = 32 * U;  // entries per chunk
     const uint32_t nwarps = blockDim.x >> 5;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    if (a.qlist && blockIdx.x >= *a.qcount) return;
-    const uint64_t q = a.qlist ? a.qlist[blockIdx.x] : blockIdx.x;
+
+    const uint32_t _nb = a.qlist ? *a.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+    const uint64_t q = a.qlist ? a.qlist[_b] : _b;
     unsigned char* lut = smem;
     constexpr uint32_t LUT_B = 4 * 256 * M;
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + LUT_B);        // cap keys
@@ -419,8 +421,10 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     for (uint32_t i = n + threadIdx.x; i < keep; i += blockDim.x) cbuf[i] = ~0ull;
     __syncthreads();
     bitonic_sort_u64<false>(cbuf, keep, threadIdx.x, blockDim.x);
-    uint64_t* candq = a.cand + (a.qlist ? (uint64_t)blockIdx.x : q) * keep;
+    uint64_t* candq = a.cand + (a.qlist ? (uint64_t)_b : q) * keep;
     for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) candq[i] = cbuf[i];
+    __syncthreads();  // shared memory is reused by the next query
+    }
 }
 
 
@@ -444,7 +448,7 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
                           : dev::k_scan_fast2<M, 6, 3>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, cap);
+    fn<<<list_grid(nq, a.qlist != nullptr), 256, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
 }
 

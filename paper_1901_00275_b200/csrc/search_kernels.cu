@@ -332,11 +332,13 @@ __global__ void __launch_bounds__(256) k_scan(SearchArgs a, uint32_t w2, uint32_
                                               const uint32_t* __restrict__ qlist,
                                               const unsigned int* __restrict__ qcount) {
     extern __shared__ __align__(16) unsigned char smem[];
-    if (qcount && blockIdx.x >= *qcount) return;
+
+    const uint32_t _nb = qcount ? *qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
     const uint32_t m = (M > 0) ? (uint32_t)M : a.m;
     const uint32_t nwarps = blockDim.x >> 5;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint64_t q = qlist ? qlist[blockIdx.x] : blockIdx.x;
+    const uint64_t q = qlist ? qlist[_b] : _b;
     float* lut = reinterpret_cast<float*>(smem);                        // m*256
     uint64_t* bufs = reinterpret_cast<uint64_t*>(smem + (size_t)m * VLQ_KSUB * 4);  // nwarps*buf
     __shared__ unsigned long long s_tau;
@@ -429,6 +431,8 @@ __global__ void __launch_bounds__(256) k_scan(SearchArgs a, uint32_t w2, uint32_
     bitonic_sort_u64<false>(bufs, total, threadIdx.x, blockDim.x);
     uint64_t* candq = a.cand + q * keep;
     for (uint32_t t = threadIdx.x; t < keep; t += blockDim.x) candq[t] = bufs[t];
+    __syncthreads();  // shared memory is reused by the next query
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -452,10 +456,12 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
     uint64_t* cstart = keys + keep;                        // w2: list start of selected cell t
     uint32_t* ccell = reinterpret_cast<uint32_t*>(cstart + w2);
     __shared__ float s_fast_last;
-    if (a.qlist && blockIdx.x >= *a.qcount) return;
-    const uint64_t q = a.qlist ? a.qlist[blockIdx.x] : blockIdx.x;
+
+    const uint32_t _nb = a.qlist ? *a.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+    const uint64_t q = a.qlist ? a.qlist[_b] : _b;
     const uint32_t m = M > 0 ? (uint32_t)M : a.m;
-    const uint64_t* candq = a.cand + (a.qlist ? (uint64_t)blockIdx.x : q) * keep;
+    const uint64_t* candq = a.cand + (a.qlist ? (uint64_t)_b : q) * keep;
     const float* wsq = a.ws + q * a.k;
     const float* t5q = a.t5 + q * m * VLQ_KSUB;
     const uint64_t scanned = a.meta[q].scanned;
@@ -554,6 +560,8 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
         }
         a.meta[q].flag = flag;
     }
+    __syncthreads();  // shared memory is reused by the next query
+    }
 }
 
 }  // namespace dev
@@ -621,7 +629,7 @@ static void launch_scan_t(const SearchArgs& a, uint64_t nblocks, uint32_t w2, ui
     size_t smem = scan_smem_bytes(a.m, nwarps, buf);
     auto fn = dev::k_scan<M, kFast>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)nblocks, nwarps * 32, smem, st>>>(a, w2, keep, buf, qlist, qcount);
+    fn<<<list_grid(nblocks, qcount != nullptr), nwarps * 32, smem, st>>>(a, w2, keep, buf, qlist, qcount);
     CUDA_LAUNCH_CHECK();
 }
 
@@ -650,7 +658,7 @@ void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep
     auto fn = a.m == 16 ? dev::k_rescore<16> : a.m == 8 ? dev::k_rescore<8> : a.m == 4 ? dev::k_rescore<4>
                                                                                           : dev::k_rescore<0>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)nq, 256, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
+    fn<<<list_grid(nq, a.qlist != nullptr), 256, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
     CUDA_LAUNCH_CHECK();
 }
 
@@ -664,8 +672,10 @@ namespace dev {
 
 __global__ void k_emit_exact(SearchArgs a, const uint32_t* __restrict__ qlist, const unsigned int* __restrict__ qcount,
                              uint32_t keep, uint32_t topk, int64_t* __restrict__ out_ids, float* __restrict__ out_d) {
-    if (qcount && blockIdx.x >= *qcount) return;
-    const uint64_t q = qlist ? qlist[blockIdx.x] : blockIdx.x;
+
+    const uint32_t _nb = qcount ? *qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+    const uint64_t q = qlist ? qlist[_b] : _b;
     const uint64_t have = dev::umin64(a.meta[q].scanned, keep);
     const uint64_t* candq = a.cand + q * keep;
     for (uint32_t t = threadIdx.x; t < topk; t += blockDim.x) {
@@ -676,6 +686,8 @@ __global__ void k_emit_exact(SearchArgs a, const uint32_t* __restrict__ qlist, c
             out_ids[q * topk + t] = -1;
             out_d[q * topk + t] = __int_as_float(0x7f800000);
         }
+    }
+    __syncthreads();  // shared memory is reused by the next query
     }
 }
 
@@ -768,7 +780,8 @@ __global__ void k_merge_topk(const int64_t* __restrict__ in_ids, const float* __
 void launch_emit_exact(const SearchArgs& a, const uint32_t* qlist, const unsigned int* qcount, uint64_t nblocks,
                        uint32_t keep, uint32_t topk, int64_t* out_ids, float* out_d, cudaStream_t st) {
     if (nblocks == 0) return;
-    dev::k_emit_exact<<<(unsigned)nblocks, 128, 0, st>>>(a, qlist, qcount, keep, topk, out_ids, out_d);
+    dev::k_emit_exact<<<list_grid(nblocks, qcount != nullptr), 128, 0, st>>>(a, qlist, qcount, keep, topk, out_ids,
+                                                                         out_d);
     CUDA_LAUNCH_CHECK();
 }
 

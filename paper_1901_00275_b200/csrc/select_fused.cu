@@ -317,8 +317,10 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
     __shared__ unsigned long long s_scanned;
     __shared__ float s_dmax;
     const bool top_mode = f.qlist != nullptr;
-    if (top_mode && blockIdx.x >= *f.qcount) return;
-    const uint64_t q = top_mode ? f.qlist[blockIdx.x] : blockIdx.x;
+
+    const uint32_t _nb = top_mode ? *f.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+    const uint64_t q = top_mode ? f.qlist[_b] : _b;
     const uint32_t k = a.k, n = a.n, dim = a.dim, w1 = f.w1, w2 = f.w2;
     const FusedLayout lay(k, n, w1, w2, dim, f.capc);
     float* ys = reinterpret_cast<float*>(smem + lay.ys);
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         const uint32_t ncent = nc * cs;
         if (nc > f.capc || ncent > FS_MAX_KEYS || nc < w1) {
             if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
-            return;
+            continue;
         }
         // the chunk list is ascending, so position order == centroid id order
         uint32_t* cls = reinterpret_cast<uint32_t*>(smem + lay.u);
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
         if (!(lower > (double)exact_w1)) {
             if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
-            return;
+            continue;
         }
         for (uint32_t r = tid; r < w1; r += nt) a.top[q * w1 + r] = topS[r];
         __syncthreads();
@@ -480,6 +482,8 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
         a.meta[q].dmax = s_dmax;
         a.meta[q].flag = 0;
     }
+    __syncthreads();  // shared memory is reused by the next query
+    }
 }
 
 }  // namespace dev
@@ -514,7 +518,7 @@ void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, 
     dev::FusedArgs f{Y, w1, w2, cs, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, sel_out, ab_out};
     const size_t smem = select_fused_smem(a.k, a.n, w1, w2, a.dim, capc);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dev::k_select_fused<<<(unsigned)nblocks, dev::FS_THREADS, smem, st>>>(a, f);
+    dev::k_select_fused<<<list_grid(nblocks, qlist != nullptr), dev::FS_THREADS, smem, st>>>(a, f);
     CUDA_LAUNCH_CHECK();
 }
 
