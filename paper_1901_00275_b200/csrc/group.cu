@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -45,6 +46,22 @@ namespace vlq {
 namespace {
 uint64_t slice_per(uint64_t nq, uint32_t G) { return (nq + G - 1) / G; }
 }  // namespace
+
+namespace {
+// fn(lo, hi) over [0, n) on up to 8 host threads (host staging copies)
+template <typename F>
+void par_for(uint64_t n, F&& fn) {
+    const uint64_t T = std::min<uint64_t>(8, std::max<uint64_t>(1, n >> 18));
+    if (T <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (uint64_t t = 0; t < T; t++) th.emplace_back([&, t] { fn(n * t / T, n * (t + 1) / T); });
+    for (auto& x : th) x.join();
+}
+}  // namespace
+
 
 Group::Group(const std::vector<int>& devices, uint32_t shards, const EngineConfig& base) : dev_(devices) {
     const uint32_t G = (uint32_t)dev_.size();
@@ -104,6 +121,7 @@ Group::~Group() {
         if (p.st) cudaStreamDestroy(p.st);
     }
     if (pin_) cudaFreeHost(pin_);
+    if (out_pin_) cudaFreeHost(out_pin_);
     eng_.clear();
 }
 
@@ -166,7 +184,7 @@ void Group::reserve(uint64_t nq, uint32_t w2, uint32_t k) {
     }
 }
 
-void Group::upload_queries(const float* q, uint64_t nq, uint32_t dim) {
+void Group::upload_queries(const float* q, uint64_t nq, uint32_t dim, bool validate) {
     if (dim != eng_[0]->dim()) throw std::runtime_error("search_batch: dimension mismatch");
     const uint64_t bytes = nq * dim * 4;
     if (pin_bytes_ < bytes) {
@@ -175,7 +193,16 @@ void Group::upload_queries(const float* q, uint64_t nq, uint32_t dim) {
         CUDA_CHECK(cudaMallocHost(&pin_, bytes));
         pin_bytes_ = bytes;
     }
-    std::memcpy(pin_, q, bytes);
+    // staged copy (and VectorSet::validate, vecset.cpp:14-18) on host threads
+    std::atomic<bool> finite{true};
+    float* dst = static_cast<float*>(pin_);
+    par_for(nq * dim, [&](uint64_t a, uint64_t b) {
+        std::memcpy(dst + a, q + a, (b - a) * 4);
+        if (validate)
+            for (uint64_t i = a; i < b; i++)
+                if (!std::isfinite(dst[i])) finite = false;
+    });
+    if (!finite) throw std::runtime_error("VectorSet: non-finite value");
     for (uint32_t g = 0; g < size(); g++) {
         DeviceGuard dg(dev_[g]);
         per_[g].q.alloc(std::max<uint64_t>(1, nq * dim));
@@ -284,7 +311,20 @@ float Group::search_resident(uint32_t w1, float alpha, uint32_t k) {
 void Group::results(int64_t* ids, float* dists, uint64_t* scanned) {
     const uint64_t nq = nq_q_;
     const uint32_t S = shards_, k = last_k_;
-    std::vector<uint64_t> sc;
+    // every device's merged slice (and scanned counts) into pinned staging at
+    // once, then one parallel copy into the caller's buffers
+    const uint64_t ib = nq * k * 8, db = nq * k * 4;
+    const uint64_t nqr_max = slice_per(nq, replicas());
+    const uint64_t sb = scanned ? (uint64_t)size() * nqr_max * 8 : 0;
+    if (out_pin_bytes_ < ib + db + sb) {
+        if (out_pin_) CUDA_CHECK(cudaFreeHost(out_pin_));
+        out_pin_ = nullptr;
+        CUDA_CHECK(cudaMallocHost(&out_pin_, ib + db + sb));
+        out_pin_bytes_ = ib + db + sb;
+    }
+    int64_t* pi = reinterpret_cast<int64_t*>(out_pin_);
+    float* pd = reinterpret_cast<float*>(static_cast<unsigned char*>(out_pin_) + ib);
+    uint64_t* ps = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(out_pin_) + ib + db);
     for (uint32_t g = 0; g < size(); g++) {
         const uint32_t r = g / S, s = g % S;
         uint64_t r0, r1;
@@ -294,18 +334,29 @@ void Group::results(int64_t* ids, float* dists, uint64_t* scanned) {
         PerDevice& p = per_[g];
         const uint64_t lo = std::min(nqr, s * per), hi = std::min(nqr, lo + per);
         if (hi > lo) {
-            if (ids)
-                CUDA_CHECK(cudaMemcpyAsync(ids + (r0 + lo) * k, p.oids.p, (hi - lo) * k * 8, cudaMemcpyDeviceToHost,
-                                           p.st));
-            if (dists)
-                CUDA_CHECK(cudaMemcpyAsync(dists + (r0 + lo) * k, p.od.p, (hi - lo) * k * 4,
-                                           cudaMemcpyDeviceToHost, p.st));
+            CUDA_CHECK(cudaMemcpyAsync(pi + (r0 + lo) * k, p.oids.p, (hi - lo) * k * 8, cudaMemcpyDeviceToHost, p.st));
+            CUDA_CHECK(cudaMemcpyAsync(pd + (r0 + lo) * k, p.od.p, (hi - lo) * k * 4, cudaMemcpyDeviceToHost, p.st));
         }
-        CUDA_CHECK(cudaStreamSynchronize(p.st));
-        if (scanned && nqr > 0) {  // reference-semantics scanned count = the sum over the replica's shards
-            sc.resize(nqr);
-            CUDA_CHECK(cudaMemcpy(sc.data(), p.lsc.p, nqr * 8, cudaMemcpyDeviceToHost));
-            for (uint64_t q = 0; q < nqr; q++) scanned[r0 + q] = (s == 0 ? 0 : scanned[r0 + q]) + sc[q];
+        if (scanned && nqr > 0)
+            CUDA_CHECK(cudaMemcpyAsync(ps + (uint64_t)g * nqr_max, p.lsc.p, nqr * 8, cudaMemcpyDeviceToHost, p.st));
+    }
+    for (uint32_t g = 0; g < size(); g++) {
+        DeviceGuard dg(dev_[g]);
+        CUDA_CHECK(cudaStreamSynchronize(per_[g].st));
+    }
+    par_for(nq, [&](uint64_t a, uint64_t b) {
+        if (ids) std::memcpy(ids + a * k, pi + a * k, (b - a) * k * 8);
+        if (dists) std::memcpy(dists + a * k, pd + a * k, (b - a) * k * 4);
+    });
+    if (scanned) {  // reference-semantics scanned count = the sum over the replica's shards
+        for (uint32_t r = 0; r < replicas(); r++) {
+            uint64_t r0, r1;
+            sub_batch(nq, r, r0, r1);
+            for (uint64_t q = r0; q < r1; q++) {
+                uint64_t t = 0;
+                for (uint32_t s = 0; s < S; s++) t += ps[(uint64_t)(r * S + s) * nqr_max + (q - r0)];
+                scanned[q] = t;
+            }
         }
     }
 }
@@ -314,10 +365,8 @@ void Group::search_host(const float* q, uint64_t nq, uint32_t dim, uint32_t w1, 
                         int64_t* ids, float* dists, uint64_t* scanned) {
     if (dim != eng_[0]->dim()) throw std::runtime_error("search_batch: dimension mismatch");
     if (w1 == 0 || w1 > eng_[0]->k()) throw std::runtime_error("first_level_scan: need 0 < w1 <= k");
-    for (uint64_t i = 0; i < nq * dim; i++)
-        if (!std::isfinite(q[i])) throw std::runtime_error("VectorSet: non-finite value");
     if (nq == 0) return;
-    upload_queries(q, nq, dim);
+    upload_queries(q, nq, dim, /*validate=*/true);
     reserve(nq, w2_of(w1, alpha, eng_[0]->n()), k);
     enqueue_search(nq, w1, alpha, k);
     check_errors();

@@ -42,7 +42,7 @@ public:
                      float* dists, uint64_t* scanned);
     // device-resident batch (bench): upload once, then timed searches
     // (device ms, max over the devices), then results()
-    void upload_queries(const float* q, uint64_t nq, uint32_t dim);
+    void upload_queries(const float* q, uint64_t nq, uint32_t dim, bool validate = true);
     float search_resident(uint32_t w1, float alpha, uint32_t k);
     void results(int64_t* ids, float* dists, uint64_t* scanned);
 
@@ -70,8 +70,10 @@ private:
     uint32_t shards_ = 1;
     std::vector<std::unique_ptr<Engine>> eng_;
     std::deque<PerDevice> per_;  // deque: PerDevice (DevBuf) is neither copyable nor movable
-    void* pin_ = nullptr;
+    void* pin_ = nullptr;  // query staging
     uint64_t pin_bytes_ = 0;
+    void* out_pin_ = nullptr;  // result staging
+    uint64_t out_pin_bytes_ = 0;
     uint64_t nq_q_ = 0;
     uint32_t last_k_ = 0;
 };
