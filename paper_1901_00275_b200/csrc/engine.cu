@@ -752,6 +752,8 @@ void Engine::search_staged(const float* d_q, uint64_t nq, uint32_t w1, float alp
     cnt2_.alloc(1);
     meta_.alloc(tile);
     qlist_.alloc(tile);
+    lpt_.alloc(tile);
+    lpt_cnt_.alloc(1);
     for (uint64_t t0 = 0; t0 < nq; t0 += tile) {
         const uint64_t nt = std::min(tile, nq - t0);
         search_tile(d_q + t0 * dim_, nt, w1, w2, topk, d_ids ? d_ids + t0 * topk : nullptr,
@@ -972,10 +974,21 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         // fast_kind: the fused fast scan ran (the only kernel with the retry indirection)
         const bool fast_kind = cfg_.scan_variant == 0 && (m_ == 16 || m_ == 8 || m_ == 4) && w2 <= 4096 &&
                                keep <= 512;
-        if (!fast_kind || !launch_scan_fast(a, nt, w2, keep, slots, st))
+        // the fast scan (and its re-score) visit the queries longest first
+        SearchArgs sa = a;
+        if (fast_kind && cfg_.scan_lpt && nt > 1) {
+            launch_lpt_order(meta_.p, nt, lpt_.p, lpt_cnt_.p, st);
+            sa.qlist = lpt_.p;
+            sa.qcount = lpt_cnt_.p;
+            sa.qorder = true;
+            launches += 1;
+        }
+        if (!fast_kind || !launch_scan_fast(sa, nt, w2, keep, slots, st)) {
+            sa = a;
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
+        }
         mark(PH_RESCORE);
-        launch_rescore(a, nt, w2, keep, topk, d_ids, d_dists, st);
+        launch_rescore(sa, nt, w2, keep, topk, d_ids, d_dists, st);
         mark(PH_FALLBACK);
         CUDA_CHECK(cudaMemsetAsync(err_.p + 2, 0, 4, st));
         launch_compact_flags(meta_.p, nt, qlist_.p, err_.p + 2, st);
@@ -1047,6 +1060,7 @@ uint32_t Engine::scan_keep(uint32_t topk) const {
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
+    else if (key == "scan_lpt") cfg_.scan_lpt = (int)value;
     else if (key == "scan_round_cap") cfg_.scan_round_cap = (uint32_t)value;
     else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;
     else if (key == "tc_search_min_k") cfg_.tc_search_min_k = (uint32_t)value;

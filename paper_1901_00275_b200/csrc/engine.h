@@ -41,6 +41,7 @@ struct EngineConfig {
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
+    int scan_lpt = 1;            // fast scan + re-score visit a tile's queries longest first (by scanned count)
     uint32_t scan_round_cap = 0; // study knob: most chunks per warp between the fast scan's block barriers (0 = 32)
     int scan_retry = 1;          // certificate failures: fast scan again with 4x k' before the exact scan
     int scan_adapt_keep = 1;     // raise k' (x2, up to x4) after a batch whose certificate failed for > 2% of queries
@@ -367,6 +368,8 @@ private:
     DevBuf<uint32_t> top_, sel_, qlist_, cand_top_;
     DevBuf<uint64_t> cand_, cand2_;  // fast-scan survivors (k') / of the retry pass (4 k')
     DevBuf<uint32_t> qlist2_;
+    DevBuf<uint32_t> lpt_;           // longest-first query order of the fast scan
+    DevBuf<unsigned int> lpt_cnt_;
     DevBuf<unsigned int> cnt2_;
     DevBuf<QueryMeta> meta_;
 };

@@ -66,6 +66,7 @@ struct SearchArgs {
     // qlist[b] (blocks >= *qcount exit) and its cand row is b, not q
     const uint32_t* qlist;
     const unsigned int* qcount;
+    bool qorder = false;  // qlist is a full permutation of the tile (one block per entry, no striding)
 };
 
 // Add-path device views.
@@ -155,6 +156,8 @@ void launch_histogram(const uint32_t* cells, uint64_t n, unsigned long long* cou
 
 namespace vlq {
 void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st);
+// longest-first order of a tile's queries for the fast scan (count := nq)
+void launch_lpt_order(const QueryMeta* meta, uint64_t nq, uint32_t* order, unsigned int* count, cudaStream_t st);
 void launch_copy_scanned(const QueryMeta* meta, uint64_t nq, uint64_t* out, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 void launch_synth(uint64_t first, uint64_t count, uint32_t dim, uint32_t clusters, float spread, uint64_t seed,

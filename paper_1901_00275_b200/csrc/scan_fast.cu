@@ -448,7 +448,7 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
                           : dev::k_scan_fast2<M, 6, 3>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<list_grid(nq, a.qlist != nullptr), 256, smem, st>>>(a, w2, keep, cap);
+    fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), 256, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
 }
 

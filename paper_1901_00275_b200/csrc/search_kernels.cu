@@ -658,7 +658,7 @@ void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep
     auto fn = a.m == 16 ? dev::k_rescore<16> : a.m == 8 ? dev::k_rescore<8> : a.m == 4 ? dev::k_rescore<4>
                                                                                           : dev::k_rescore<0>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<list_grid(nq, a.qlist != nullptr), 256, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
+    fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), 256, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
     CUDA_LAUNCH_CHECK();
 }
 
@@ -831,6 +831,38 @@ __global__ void k_compact_flags(const QueryMeta* __restrict__ meta, uint64_t nq,
         if (meta[q].flag) qlist[atomicAdd(count, 1u)] = (uint32_t)q;
 }
 
+// Longest-processing-time-first order of the tile's queries for the fast
+// scan (one CTA per query, dispatched in block order as SM slots free up):
+// queries bucketed by their scanned-entry count, largest first, so the batch
+// does not end on a few long queries.  One block.
+__global__ void __launch_bounds__(1024) k_lpt_order(const QueryMeta* __restrict__ meta, uint32_t nq,
+                                                    uint32_t* __restrict__ order, unsigned int* __restrict__ count) {
+    constexpr uint32_t NB = 256;
+    __shared__ unsigned long long s_max;
+    __shared__ uint32_t hist[NB], offs[NB];
+    if (threadIdx.x == 0) s_max = 0;
+    for (uint32_t b = threadIdx.x; b < NB; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    unsigned long long mx = 0;
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) mx = max(mx, meta[q].scanned);
+    atomicMax(&s_max, mx);
+    __syncthreads();
+    const unsigned long long m1 = s_max + 1;
+    auto bucket = [&](uint32_t q) { return NB - 1 - (uint32_t)((meta[q].scanned * NB) / m1); };
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) atomicAdd(&hist[bucket(q)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t b = 0; b < NB; b++) {
+            offs[b] = run;
+            run += hist[b];
+        }
+        *count = nq;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) order[atomicAdd(&offs[bucket(q)], 1u)] = q;
+}
+
 __global__ void k_copy_scanned(const QueryMeta* __restrict__ meta, uint64_t nq, uint64_t* __restrict__ out) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x)
         out[q] = meta[q].scanned;
@@ -845,6 +877,12 @@ __global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
 
 void launch_compact_flags(const QueryMeta* meta, uint64_t nq, uint32_t* qlist, unsigned int* count, cudaStream_t st) {
     dev::k_compact_flags<<<(unsigned)dev::umin64((nq + 255) / 256, 1184), 256, 0, st>>>(meta, nq, qlist, count);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_lpt_order(const QueryMeta* meta, uint64_t nq, uint32_t* order, unsigned int* count, cudaStream_t st) {
+    if (nq == 0) return;
+    dev::k_lpt_order<<<1, 1024, 0, st>>>(meta, (uint32_t)nq, order, count);
     CUDA_LAUNCH_CHECK();
 }
 
