@@ -72,7 +72,7 @@ def test_select_topk_equal_distances_order_by_ascending_id(vlqadc, force_exact):
     base = (rng.random((12, 8), dtype=np.float32) * 4.0).astype(np.float32)
     base[7] = base[3]
     base[9] = base[3]
-    idx = vlqadc.Index.train(np.vstack([base, rng.random((200, 8), dtype=np.float32) * 4.0]), k=16, n=4, m=2,
+    idx = vlqadc.Index.train(np.vstack([base, rng.random((400, 8), dtype=np.float32) * 4.0]), k=16, n=4, m=2,
                              iters=4, seed=5, force_exact=force_exact)
     idx.add(base)
     ids, dists = idx.search(base[3:4], w1=16, alpha=1.0, k=2)
