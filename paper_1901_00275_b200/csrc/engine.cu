@@ -968,7 +968,6 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         }
         a.scan_cap = cfg_.scan_cap;
         a.round_cap = cfg_.scan_round_cap;
-        a.lut_copies = cfg_.scan_lut_copies;
         a.sel_agg = cfg_.scan_sel_agg != 0;
         a.flush_exact = cfg_.scan_flush_exact != 0;
         const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
@@ -1061,7 +1060,6 @@ uint32_t Engine::scan_keep(uint32_t topk) const {
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
-    else if (key == "scan_lut_copies") cfg_.scan_lut_copies = (int)value;
     else if (key == "scan_lpt") cfg_.scan_lpt = (int)value;
     else if (key == "scan_round_cap") cfg_.scan_round_cap = (uint32_t)value;
     else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;

@@ -41,7 +41,6 @@ struct EngineConfig {
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select
     int scan_flush_exact = 0;    // study knob: exact (multi-pass) intermediate flushes in the fast scan
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
-    int scan_lut_copies = 1;     // study knob: 2 = one interleaved LUT copy per half-warp (fewer bank conflicts)
     int scan_lpt = 1;            // fast scan + re-score visit a tile's queries longest first (by scanned count)
     uint32_t scan_round_cap = 0; // study knob: most chunks per warp between the fast scan's block barriers (0 = 32)
     int scan_retry = 1;          // certificate failures: fast scan again with 4x k' before the exact scan

@@ -59,8 +59,7 @@ struct SearchArgs {
     const uint32_t* eterm_lam;
     float e_pack_err;
     uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
-    uint32_t round_cap = 0;
-    int lut_copies = 1;      // study: 2 = interleaved LUT copy per half-warp  // fast scan: most chunks per warp between block barriers (0 = 32)
+    uint32_t round_cap = 0;  // fast scan: most chunks per warp between block barriers (0 = 32)
     bool sel_agg;       // fast-scan flush: warp-aggregated (match_any) histogram atomics
     bool flush_exact;   // fast-scan intermediate flushes: exact k' selection (else one-pass approximate)
     // retry pass (certificate failures): the kernel's block b handles query

@@ -180,12 +180,12 @@ __global__ void k_pack_eterm_lam(const float* __restrict__ eterm, const uint8_t*
 
 // LUT[p][code_p]: the byte is extracted with one LOP3 / PRMT / SHF and the
 // shared load scales it (LDS [R.X4 + imm]), so a lookup is 2 instructions
-template <int M, int LC = 1>
+template <int M>
 __device__ __forceinline__ float lut_at(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], int p) {
     const uint32_t word = w[p >> 2];
     const int k = p & 3;
     const uint32_t b = k == 0 ? (word & 0xffu) : (k == 3 ? (word >> 24) : __byte_perm(word, 0u, 0x4440u + k));
-    return reinterpret_cast<const float*>(lut)[(p * 256 + b) * LC];
+    return reinterpret_cast<const float*>(lut)[p * 256 + b];
 }
 
 __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an order-preserving key (upper 32 bits)
@@ -193,10 +193,7 @@ __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an ord
     return __uint_as_float((ub & 0x80000000u) ? (ub & 0x7fffffffu) : ~ub);
 }
 
-// LC = 2 (study): two interleaved copies of the LUT, lanes 0-15 reading the
-// even banks and lanes 16-31 the odd ones, so the half-warps never conflict
-// with each other
-template <int M, int U, int MINB, int LC = 1>
+template <int M, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -209,8 +206,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
     const uint64_t q = a.qlist ? a.qlist[_b] : _b;
     unsigned char* lut = smem;
-    constexpr uint32_t LUT_B = 4 * 256 * M * LC;
-    const unsigned char* lutl = lut + (LC == 2 ? 4u * (lane >> 4) : 0u);  // this lane's copy
+    constexpr uint32_t LUT_B = 4 * 256 * M;
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + LUT_B);        // cap keys
     uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);         // w2 + 1
     __shared__ uint32_t hist[256];
@@ -220,15 +216,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
 
     // 1. the query's term5 table (one copy per sub-space)
     const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
-    if constexpr (LC == 1) {
-        for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
-    } else {
-        for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) {
-            const float4 v = __ldg(t5q + i);
-            reinterpret_cast<float4*>(lut)[2 * i] = make_float4(v.x, v.x, v.y, v.y);
-            reinterpret_cast<float4*>(lut)[2 * i + 1] = make_float4(v.z, v.z, v.w, v.w);
-        }
-    }
+    for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
     {
@@ -347,10 +335,10 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                     const float2 lam = __ffma2_rn(make_float2((float)lb[u], (float)lb[u + 1]), delta2, lam02);
                     const float2 t1 = __ffma2_rn(lam, __ffma2_rn(lam, cv2, Bc2), av2);
                     const float2 te = __fadd2_rn(t1, make_float2(ev[u], ev[u + 1]));
-                    float2 s = make_float2(lut_at<M, LC>(lutl, cw[u], 0), lut_at<M, LC>(lutl, cw[u + 1], 0));
+                    float2 s = make_float2(lut_at<M>(lut, cw[u], 0), lut_at<M>(lut, cw[u + 1], 0));
 #pragma unroll
                     for (int p = 1; p < M; p++)
-                        s = __fadd2_rn(s, make_float2(lut_at<M, LC>(lutl, cw[u], p), lut_at<M, LC>(lutl, cw[u + 1], p)));
+                        s = __fadd2_rn(s, make_float2(lut_at<M>(lut, cw[u], p), lut_at<M>(lut, cw[u + 1], p)));
                     const float2 d = __ffma2_rn(m2, s, te);
                     dist[u] = d.x;
                     dist[u + 1] = d.y;
@@ -452,15 +440,13 @@ template <int M>
 static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
     // block-shared candidate buffer (keys): 2048 unless the scan_cap knob says otherwise
     const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 2048u, 4 * keep);
-    const int lc = a.lut_copies == 2 ? 2 : 1;
-    const size_t smem = 4 * 256 * (size_t)M * lc + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
+    const size_t smem = 4 * 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
     // su: slots per lane (4 / 6 / 8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
     auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
               : su == 8 ? dev::k_scan_fast2<M, 8, 3>
               : su == 104 ? dev::k_scan_fast2<M, 4, 4>
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
                           : dev::k_scan_fast2<M, 6, 3>;
-    if (lc == 2) fn = su == 104 ? dev::k_scan_fast2<M, 4, 4, 2> : dev::k_scan_fast2<M, 6, 3, 2>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), 256, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
