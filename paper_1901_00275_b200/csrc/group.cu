@@ -190,7 +190,7 @@ void Group::upload_queries(const float* q, uint64_t nq, uint32_t dim, bool valid
     if (pin_bytes_ < bytes) {
         if (pin_) CUDA_CHECK(cudaFreeHost(pin_));
         pin_ = nullptr;
-        CUDA_CHECK(cudaMallocHost(&pin_, bytes));
+        CUDA_CHECK(cudaHostAlloc(&pin_, bytes, cudaHostAllocPortable));  // pinned for every device's DMA
         pin_bytes_ = bytes;
     }
     // staged copy (and VectorSet::validate, vecset.cpp:14-18) on host threads
@@ -319,7 +319,7 @@ void Group::results(int64_t* ids, float* dists, uint64_t* scanned) {
     if (out_pin_bytes_ < ib + db + sb) {
         if (out_pin_) CUDA_CHECK(cudaFreeHost(out_pin_));
         out_pin_ = nullptr;
-        CUDA_CHECK(cudaMallocHost(&out_pin_, ib + db + sb));
+        CUDA_CHECK(cudaHostAlloc(&out_pin_, ib + db + sb, cudaHostAllocPortable));
         out_pin_bytes_ = ib + db + sb;
     }
     int64_t* pi = reinterpret_cast<int64_t*>(out_pin_);
