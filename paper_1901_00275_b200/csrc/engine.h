@@ -56,6 +56,7 @@ struct EngineConfig {
     int tc_pass2_single = 0;  // ... and the filter pass in 1xTF32 too (tau raised by both bounds; more candidates)
     int tc_chunk_select = 1;  // chunk-select coarse stage (one 1xTF32 pass of 8-centroid chunk minima, exact
                               // evaluation of the selected chunks, fused first + second level; select_fused.cu)
+    int tc_select_split = 1;  // chunk-select stage in split form (row kernels + selection kernels) vs one fused kernel
     uint32_t tc_chunk_cap = 256;  // selected chunks per query before the exact full-row fallback (study knob)
 };
 
@@ -321,6 +322,8 @@ private:
     DevBuf<uint32_t> lcnt_, lidx_;
     DevBuf<float> tmin8_, tch_;          // chunk-select path: 8-centroid chunk minima, threshold T per query
     DevBuf<uint32_t> clist_, ccnt_;      // selected chunks per query
+    DevBuf<float> svals_, snval_;        // split form: chunk-centroid / needed-id exact distances
+    DevBuf<uint32_t> snid_, snneed_;     // split form: needed ids per query (ascending) and their count
     bool model_ok_ = false;
     uint32_t dim_ = 0, k_ = 0, n_ = 0, m_ = 0;
     bool clamp_ = true;

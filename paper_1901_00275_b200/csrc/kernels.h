@@ -178,6 +178,21 @@ size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint3
 bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc);
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
                          float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st);
+// split form of the fused kernel (select_fused.cu): row kernels + light
+// per-query selection kernels; ldn = select_need_capacity(n, w1)
+uint32_t select_need_capacity(uint32_t n, uint32_t w1);
+uint32_t select_chunk_keys();  // exactly evaluated chunk centroids per query (row stride of the values)
+bool select_split_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc);
+void launch_rows(const float* C, const float* Y, uint32_t k, uint32_t dim, int chunks, const uint32_t* list,
+                 const uint32_t* cnt, uint32_t ld, uint32_t capc, float* out, uint32_t ldo, uint64_t nq,
+                 cudaStream_t st);
+void launch_top_need(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2,
+                     const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
+                     const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
+                     const float* vals, uint32_t* nid, uint32_t* nneed, uint32_t ldn, cudaStream_t st);
+void launch_second_sel(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, const uint32_t* nid,
+                       const float* nval, const uint32_t* nneed, uint32_t ldn, uint32_t* sel_out, float* ab_out,
+                       cudaStream_t st);
 void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2, uint32_t cs,
                          const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
                          const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,

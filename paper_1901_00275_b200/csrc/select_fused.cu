@@ -178,23 +178,25 @@ __device__ __forceinline__ void cp_async_wait() {
 // Exact reference-order sqdist (vecset.cpp:22-29: acc += (y - c)^2 in order)
 // of the rows id_of(0 .. cnt) (centroid ids; id >= k gives +inf), out(t, d).
 // Each warp takes batches of 32 rows, lane l owning row l of the batch; the
-// rows stream through shared memory in 32-dimension pieces (one 128-byte line
-// per row; coalesced 16-byte cp.async, zero-filled for invalid rows), double-
-// buffered per warp, so the L2 latency of the gathered centroid rows overlaps
-// the sequential sums.  Warp-synchronous; `wbuf` is this warp's
-// 2 * FS_BUF_FLOATS floats.  The loop keeps (batch, piece) counters instead of
-// dividing, and the 8 row bases a lane copies for are computed once per batch.
-template <typename IdFn, typename OutFn>
-__device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uint32_t k, uint32_t dim,
-                                                const float* ys, float* wbuf, uint32_t cnt, IdFn&& id_of,
-                                                OutFn&& out) {
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
-    const uint32_t npiece = (dim + FS_PW - 1) / FS_PW;
+// rows stream through shared memory in PW-dimension pieces (coalesced 16-byte
+// cp.async, zero-filled for invalid rows), NB pieces per warp in flight, so
+// the L2 latency of the gathered centroid rows overlaps the sequential sums.
+// Warp-synchronous; `wbuf` is this warp's NB * 32 * (PW + 4) floats (row
+// stride PW + 4: conflict-free LDS.128).  The loop keeps (batch, piece)
+// counters instead of dividing; a lane's row bases are computed once per batch.
+template <uint32_t PW, uint32_t NB, typename IdFn, typename OutFn>
+__device__ __forceinline__ void exact_rows_pipe_t(const float* __restrict__ C, uint32_t k, uint32_t dim,
+                                                  const float* ys, float* wbuf, uint32_t cnt, uint32_t warp,
+                                                  uint32_t nwarps, IdFn&& id_of, OutFn&& out) {
+    constexpr uint32_t RS = PW + 4, BUF = 32 * RS;
+    constexpr uint32_t CPR = PW / 4, RPI = 32 / CPR, NI = CPR;  // chunks per row piece, rows per copy instr
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t npiece = (dim + PW - 1) / PW;
     const uint32_t nbatch = cnt > warp * 32 ? (cnt - warp * 32 + nwarps * 32 - 1) / (nwarps * 32) : 0;
     if (nbatch == 0) return;
     const uint32_t nu = nbatch * npiece;
-    const uint32_t sub = lane & 7u, rsub = lane >> 3;  // copy role: 16-byte chunk `sub` of rows 4 i + rsub
-    const float* rb[8];
+    const uint32_t sub = lane % CPR, rsub = lane / CPR;  // copy role: chunk `sub` of rows RPI i + rsub
+    const float* rb[NI];
     uint32_t rvalid = 0;
     uint32_t ib = 0, ip = 0, islot = 0;  // next unit to issue
     auto issue = [&]() {
@@ -203,38 +205,42 @@ __device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uin
             const uint32_t my_id = r0 + lane < cnt ? id_of(r0 + lane) : 0xffffffffu;
             rvalid = 0;
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const uint32_t id = __shfl_sync(0xffffffffu, my_id, 4 * i + rsub);
+            for (uint32_t i = 0; i < NI; i++) {
+                const uint32_t id = __shfl_sync(0xffffffffu, my_id, RPI * i + rsub);
                 const bool v = id < k;
                 rvalid |= (v ? 1u : 0u) << i;
                 rb[i] = C + (v ? (uint64_t)id * dim : 0ull) + sub * 4;
             }
         }
-        float* buf = wbuf + islot * FS_BUF_FLOATS + rsub * FS_RS + sub * 4;
-        const bool dval = ip * FS_PW + sub * 4 < dim;
+        float* buf = wbuf + islot * BUF + rsub * RS + sub * 4;
+        const bool dval = ip * PW + sub * 4 < dim;
 #pragma unroll
-        for (int i = 0; i < 8; i++)
-            cp_async16(buf + 4 * i * FS_RS, rb[i] + ip * FS_PW, dval && ((rvalid >> i) & 1u));
+        for (uint32_t i = 0; i < NI; i++)
+            cp_async16(buf + RPI * i * RS, rb[i] + ip * PW, dval && ((rvalid >> i) & 1u));
         cp_async_commit();
-        islot ^= 1u;
+        islot = islot + 1 == NB ? 0 : islot + 1;
         if (++ip == npiece) {
             ip = 0;
             ib++;
         }
     };
-    issue();
+#pragma unroll
+    for (uint32_t u = 0; u + 1 < NB; u++) {
+        if (u < nu) issue();
+        else cp_async_commit();
+    }
     float acc = 0.0f;
     uint32_t cb = 0, cp = 0, cslot = 0;  // unit being computed
     for (uint32_t u = 0; u < nu; u++) {
-        if (u + 1 < nu) issue();
+        if (u + NB - 1 < nu) issue();
         else cp_async_commit();
-        cp_async_wait<1>();
+        cp_async_wait<NB - 1>();
         __syncwarp();
-        const float* row = wbuf + cslot * FS_BUF_FLOATS + lane * FS_RS;
-        const float* yp = ys + cp * FS_PW;
-        if (cp * FS_PW + FS_PW <= dim) {
+        const float* row = wbuf + cslot * BUF + lane * RS;
+        const float* yp = ys + cp * PW;
+        if (cp * PW + PW <= dim) {
 #pragma unroll
-            for (uint32_t c4 = 0; c4 < FS_PW / 4; c4++) {
+            for (uint32_t c4 = 0; c4 < PW / 4; c4++) {
                 const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
                 const float4 yv = *reinterpret_cast<const float4*>(yp + c4 * 4);
                 acc = sq_step(acc, yv.x, v.x);
@@ -243,7 +249,7 @@ __device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uin
                 acc = sq_step(acc, yv.w, v.w);
             }
         } else {
-            for (uint32_t c4 = 0; c4 < (dim - cp * FS_PW) / 4; c4++) {
+            for (uint32_t c4 = 0; c4 < (dim - cp * PW) / 4; c4++) {
                 const float4 v = *reinterpret_cast<const float4*>(row + c4 * 4);
                 const float4 yv = *reinterpret_cast<const float4*>(yp + c4 * 4);
                 acc = sq_step(acc, yv.x, v.x);
@@ -253,7 +259,7 @@ __device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uin
             }
         }
         __syncwarp();
-        cslot ^= 1u;
+        cslot = cslot + 1 == NB ? 0 : cslot + 1;
         if (++cp == npiece) {
             const uint32_t t = (warp + cb * nwarps) * 32 + lane;
             if (t < cnt) out(t, id_of(t) < k ? acc : __int_as_float(0x7f800000));
@@ -263,6 +269,13 @@ __device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uin
         }
     }
     cp_async_wait<0>();
+}
+
+template <typename IdFn, typename OutFn>
+__device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uint32_t k, uint32_t dim,
+                                                const float* ys, float* wbuf, uint32_t cnt, IdFn&& id_of,
+                                                OutFn&& out) {
+    exact_rows_pipe_t<FS_PW, 2>(C, k, dim, ys, wbuf, cnt, threadIdx.x >> 5, blockDim.x >> 5, id_of, out);
 }
 
 struct FusedArgs {
@@ -486,6 +499,258 @@ __global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, Fused
     }
 }
 
+// ---------------------------------------------------------------------------
+// Split form of k_select_fused (the default): the exact centroid rows run in
+// kernels that do nothing else -- no block barriers, several CTAs per SM with
+// NB row pieces in flight per warp, so the gathered rows stream at L2 speed --
+// and the selections run in light per-query kernels:
+//   k_rows (chunks)  exact distances of the kept chunks' centroids -> vals [q][t]
+//   k_top_need       exact top-w1 + certificate (chunk mode) or the exact
+//                    top-w1 of the fallback (top mode); the needed ids (regions
+//                    and their neighbours, deduplicated, ascending) -> nid [q][t]
+//   k_rows (list)    exact distances of the needed ids -> nval [q][t]
+//   k_second_sel     second_level_rank from nid / nval -> selection, (a, b),
+//                    scanned count, |term1| bound
+// ---------------------------------------------------------------------------
+constexpr uint32_t RW_WARPS = 4;   // warps per query CTA of the row kernels
+constexpr uint32_t RW_PW = 16, RW_NB = 4;
+
+struct RowsArgs {
+    const float* C;
+    const float* Y;
+    uint32_t k, dim;
+    int chunks;               // 1: ids = list[q][t / 8] * 8 + t % 8 for t < 8 cnt[q] (cnt[q] <= capc); 0: ids = list[q][t]
+    const uint32_t* list;
+    const uint32_t* cnt;
+    uint32_t ld;              // row stride of list (capc, or the needed-id capacity)
+    uint32_t capc;
+    float* out;
+    uint32_t ldo;
+};
+
+__global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowsArgs r) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint64_t q = blockIdx.x;
+    const uint32_t dim = r.dim, dimp = (dim + RW_PW - 1) / RW_PW * RW_PW;
+    float* ys = reinterpret_cast<float*>(smem);
+    float* wbuf = ys + dimp + (threadIdx.x >> 5) * RW_NB * 32 * (RW_PW + 4);
+    for (uint32_t d = threadIdx.x; d < dimp; d += blockDim.x) ys[d] = d < dim ? r.Y[q * dim + d] : 0.0f;
+    uint32_t cnt = r.cnt[q];
+    if (r.chunks) cnt = (cnt > r.capc || cnt * FS_CS > FS_MAX_KEYS) ? 0u : cnt * FS_CS;  // overflow: k_top_need flags it
+    __syncthreads();
+    const uint32_t* lq = r.list + q * r.ld;
+    float* oq = r.out + q * r.ldo;
+    if (r.chunks)
+        exact_rows_pipe_t<RW_PW, RW_NB>(
+            r.C, r.k, dim, ys, wbuf, cnt, threadIdx.x >> 5, RW_WARPS,
+            [&](uint32_t t) { return __ldg(lq + t / FS_CS) * FS_CS + (t & (FS_CS - 1)); },
+            [&](uint32_t t, float v) { oq[t] = v; });
+    else
+        exact_rows_pipe_t<RW_PW, RW_NB>(
+            r.C, r.k, dim, ys, wbuf, cnt, threadIdx.x >> 5, RW_WARPS, [&](uint32_t t) { return __ldg(lq + t); },
+            [&](uint32_t t, float v) { oq[t] = v; });
+}
+
+struct NeedArgs {
+    const float* vals;   // [nq][FS_MAX_KEYS] chunk-centroid distances (chunk mode)
+    uint32_t* nid;       // [nq][ldn] needed ids, ascending
+    uint32_t* nneed;     // [nq]
+    uint32_t ldn;
+};
+
+__global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs f, NeedArgs na) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ float s_yn;
+    __shared__ unsigned int s_w1max;
+    const bool top_mode = f.qlist != nullptr;
+    const uint32_t k = a.k, n = a.n, dim = a.dim, w1 = f.w1, nw = fs_nwords(k);
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint32_t* topS = reinterpret_cast<uint32_t*>(smem);                 // w1
+    uint32_t* bitmap = topS + ((w1 + 3) & ~3u);                           // nw
+    float* vals = reinterpret_cast<float*>(bitmap + nw);                  // FS_MAX_KEYS (chunk mode)
+    uint32_t* topPos = reinterpret_cast<uint32_t*>(vals + FS_MAX_KEYS);  // w1
+    uint32_t* hist = topPos + ((w1 + 3) & ~3u);                           // 1024 + 256 + 40 (range select)
+    uint32_t* scan = hist + 2048;
+    const uint32_t _nb = top_mode ? *f.qcount : gridDim.x;
+    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
+        const uint64_t q = top_mode ? f.qlist[_b] : _b;
+        if (!top_mode) {
+            const uint32_t nc = f.ccnt[q];
+            const uint32_t ncent = nc * FS_CS;
+            if (nc > f.capc || ncent > FS_MAX_KEYS || nc < w1) {
+                if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
+                continue;
+            }
+            const float* vq = na.vals + q * FS_MAX_KEYS;
+            for (uint32_t t = tid; t < ncent; t += nt) vals[t] = vq[t];
+            if (tid == 0) {
+                float yn = 0.0f;
+                for (uint32_t d = 0; d < dim; d++) yn = fmaf(f.Y[q * dim + d], f.Y[q * dim + d], yn);
+                s_yn = yn;
+                s_w1max = 0u;
+            }
+            __syncthreads();
+            // exact top-w1 by (dist, id): the chunk list is ascending, so position order == id order
+            block_select_ordered_range(vals, ncent, w1, topPos, hist, scan);
+            __syncthreads();
+            const uint32_t* cl = f.clist + q * f.capc;
+            float mx = 0.0f;
+            for (uint32_t r = tid; r < w1; r += nt) {
+                const uint32_t pos = topPos[r];
+                topS[r] = cl[pos / FS_CS] * FS_CS + (pos & (FS_CS - 1));
+                mx = fmaxf(mx, vals[pos]);  // +inf (a padded id) fails the certificate below
+            }
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if ((tid & 31) == 0) atomicMax(&s_w1max, __float_as_uint(mx));  // distances >= 0
+            __syncthreads();
+            const float exact_w1 = __uint_as_float(s_w1max);
+            const float eps = tc_eps(s_yn, f.cmax, dim, false, /*rna=*/true);
+            const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
+            if (!(lower > (double)exact_w1)) {
+                if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
+                __syncthreads();
+                continue;
+            }
+            for (uint32_t r = tid; r < w1; r += nt) a.top[q * w1 + r] = topS[r];
+        } else {
+            for (uint32_t t = tid; t < w1; t += nt) topS[t] = a.top[q * w1 + t];
+        }
+        // the regions and their neighbours, deduplicated through a bitmap,
+        // compacted in ascending id order
+        for (uint32_t i = tid; i < nw; i += nt) bitmap[i] = 0;
+        __syncthreads();
+        const uint32_t nn = w1 * (n + 1);
+        for (uint32_t e = tid; e < nn; e += nt) {
+            const uint32_t r = e / (n + 1), j = e % (n + 1);
+            const uint32_t c = j == 0 ? topS[r] : a.nbr[(uint64_t)topS[r] * n + (j - 1)];
+            atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+        }
+        __syncthreads();
+        const uint32_t per = (nw + nt - 1) / nt;
+        uint32_t local = 0;
+        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) local += __popc(bitmap[i]);
+        uint32_t total;
+        uint32_t run = block_excl_scan_u32(local, scan, &total);
+        uint32_t* nq_out = na.nid + q * na.ldn;
+        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) {
+            uint32_t w = bitmap[i];
+            while (w) {
+                const uint32_t b = __ffs(w) - 1;
+                nq_out[run++] = i * 32 + b;
+                w &= w - 1;
+            }
+        }
+        if (tid == 0) na.nneed[q] = total;
+        __syncthreads();
+    }
+}
+
+struct SecondArgs {
+    const uint32_t* nid;
+    const float* nval;
+    const uint32_t* nneed;
+    uint32_t ldn;
+};
+
+__global__ void __launch_bounds__(FS_THREADS) k_second_sel(SearchArgs a, FusedArgs f, SecondArgs sa) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long s_scanned;
+    __shared__ float s_dmax;
+    const uint32_t k = a.k, n = a.n, w1 = f.w1, w2 = f.w2, nw = fs_nwords(k), total = w1 * n;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    const uint64_t q = blockIdx.x;
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);          // nw
+    uint16_t* wpref = reinterpret_cast<uint16_t*>(bitmap + nw);     // nw
+    float* nval = reinterpret_cast<float*>(bitmap + nw + (nw + 1) / 2);  // ldn
+    float* dq = nval + sa.ldn;                                      // w1 n
+    uint32_t* selpos = reinterpret_cast<uint32_t*>(dq + total);     // w2
+    uint32_t* topS = selpos + w2;                                   // w1
+    uint32_t* hist = topS + w1;                                     // range select scratch
+    uint32_t* scan = hist + 2048;
+    for (uint32_t i = tid; i < nw; i += nt) bitmap[i] = 0;
+    if (tid == 0) {
+        s_scanned = 0;
+        s_dmax = 0.0f;
+    }
+    const uint32_t cnt = sa.nneed[q];
+    const uint32_t* idq = sa.nid + q * sa.ldn;
+    const float* vq = sa.nval + q * sa.ldn;
+    for (uint32_t r = tid; r < w1; r += nt) topS[r] = a.top[q * w1 + r];
+    __syncthreads();
+    for (uint32_t t = tid; t < cnt; t += nt) {
+        const uint32_t c = idq[t];
+        atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+        nval[t] = vq[t];  // ids are ascending: rank(c) = t
+    }
+    __syncthreads();
+    {
+        const uint32_t per = (nw + nt - 1) / nt;
+        uint32_t local = 0;
+        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) local += __popc(bitmap[i]);
+        uint32_t tot;
+        uint32_t run = block_excl_scan_u32(local, scan, &tot);
+        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) {
+            wpref[i] = (uint16_t)run;
+            run += __popc(bitmap[i]);
+        }
+    }
+    __syncthreads();
+    auto val_of = [&](uint32_t c) -> float {
+        const uint32_t w = c >> 5;
+        return nval[wpref[w] + __popc(bitmap[w] & ((1u << (c & 31)) - 1u))];
+    };
+    // second_level_rank (search.cpp:38-78)
+    for (uint32_t e = tid; e < total; e += nt) {
+        const uint32_t i = topS[e / n], j = e % n;
+        const float av = val_of(i);
+        const uint32_t s = a.nbr[(uint64_t)i * n + j];
+        const float bv = val_of(s);
+        const float cv = a.elen[(uint64_t)i * n + j];
+        if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
+        const float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
+        dq[e] = line_sqdist(av, bv, cv, lam);
+    }
+    __syncthreads();
+    block_select_ordered_range(dq, total, w2, selpos, hist, scan);
+    __syncthreads();
+    float* wsq = a.ws + q * a.k;
+    const float lmax = a.lam_absmax;
+    unsigned long long c2 = 0;
+    float dmax = 0.0f;
+    for (uint32_t t = tid; t < w2; t += nt) {
+        const uint32_t e = selpos[t];
+        const uint32_t i = topS[e / n], j = e % n;
+        const uint32_t cell = i * n + j;
+        const uint32_t s = a.nbr[cell];
+        const float av = val_of(i), bv = val_of(s), cv = a.elen[cell];
+        a.sel[q * w2 + t] = cell;
+        wsq[i] = av;
+        wsq[s] = bv;
+        if (f.sel_out) {
+            f.sel_out[q * w2 + t] = cell;
+            f.ab_out[(q * w2 + t) * 2] = av;
+            f.ab_out[(q * w2 + t) * 2 + 1] = bv;
+        }
+        c2 += a.list_off[cell + 1] - a.list_off[cell];
+        const float bound = (1.0f + lmax) * fabsf(av) + (lmax * lmax + lmax) * fabsf(cv) + lmax * fabsf(bv);
+        dmax = fmaxf(dmax, bound);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(&s_scanned, c2);
+        atomicMax(reinterpret_cast<unsigned int*>(&s_dmax), __float_as_uint(dmax));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.meta[q].scanned = s_scanned;
+        a.meta[q].dmax = s_dmax;
+        a.meta[q].flag = 0;
+    }
+}
+
 }  // namespace dev
 
 size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
@@ -519,6 +784,65 @@ void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, 
     const size_t smem = select_fused_smem(a.k, a.n, w1, w2, a.dim, capc);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dev::k_select_fused<<<list_grid(nblocks, qlist != nullptr), dev::FS_THREADS, smem, st>>>(a, f);
+    CUDA_LAUNCH_CHECK();
+}
+
+
+// ---- split form -------------------------------------------------------------
+uint32_t select_need_capacity(uint32_t n, uint32_t w1) { return w1 * (n + 1); }
+uint32_t select_chunk_keys() { return dev::FS_MAX_KEYS; }
+
+static size_t top_need_smem(uint32_t k, uint32_t w1) {
+    return ((size_t)((w1 + 3) & ~3u) * 2 + dev::fs_nwords(k) + dev::FS_MAX_KEYS + 2048 + 64) * 4;
+}
+static size_t second_sel_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2) {
+    const uint32_t nw = dev::fs_nwords(k);
+    return ((size_t)nw + (nw + 1) / 2 + select_need_capacity(n, w1) + (size_t)w1 * n + w2 + w1 + 2048 + 64) * 4;
+}
+static size_t rows_smem(uint32_t dim) {
+    const uint32_t dimp = (dim + dev::RW_PW - 1) / dev::RW_PW * dev::RW_PW;
+    return ((size_t)dimp + (size_t)dev::RW_WARPS * dev::RW_NB * 32 * (dev::RW_PW + 4)) * 4;
+}
+
+bool select_split_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
+    return dim % 4 == 0 && dim <= 1024 && w1 <= 256 && w2 <= w1 * n && (uint64_t)w1 * (n + 1) <= 16384 &&
+           capc <= 1024 && top_need_smem(k, w1) <= 200 * 1024 && second_sel_smem(k, n, w1, w2) <= 200 * 1024;
+}
+
+void launch_rows(const float* C, const float* Y, uint32_t k, uint32_t dim, int chunks, const uint32_t* list,
+                 const uint32_t* cnt, uint32_t ld, uint32_t capc, float* out, uint32_t ldo, uint64_t nq,
+                 cudaStream_t st) {
+    if (nq == 0) return;
+    dev::RowsArgs r{C, Y, k, dim, chunks, list, cnt, ld, capc, out, ldo};
+    const size_t smem = rows_smem(dim);
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_rows<<<(unsigned)nq, dev::RW_WARPS * 32, smem, st>>>(r);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_top_need(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2,
+                     const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
+                     const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
+                     const float* vals, uint32_t* nid, uint32_t* nneed, uint32_t ldn, cudaStream_t st) {
+    if (nblocks == 0) return;
+    dev::FusedArgs f{Y, w1, w2, dev::FS_CS, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, nullptr, nullptr};
+    dev::NeedArgs na{vals, nid, nneed, ldn};
+    const size_t smem = top_need_smem(a.k, w1);
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_top_need, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_top_need<<<list_grid(nblocks, qlist != nullptr), dev::FS_THREADS, smem, st>>>(a, f, na);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_second_sel(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, const uint32_t* nid,
+                       const float* nval, const uint32_t* nneed, uint32_t ldn, uint32_t* sel_out, float* ab_out,
+                       cudaStream_t st) {
+    if (nq == 0) return;
+    dev::FusedArgs f{nullptr, w1, w2, dev::FS_CS, nullptr, nullptr, 0, nullptr, 0.0f, nullptr, nullptr,
+                     nullptr, nullptr, sel_out, ab_out};
+    dev::SecondArgs sa{nid, nval, nneed, ldn};
+    const size_t smem = second_sel_smem(a.k, a.n, w1, w2);
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_second_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::k_second_sel<<<(unsigned)nq, dev::FS_THREADS, smem, st>>>(a, f, sa);
     CUDA_LAUNCH_CHECK();
 }
 
