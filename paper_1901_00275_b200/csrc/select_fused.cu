@@ -583,9 +583,12 @@ __global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs
             }
             const float* vq = na.vals + q * FS_MAX_KEYS;
             for (uint32_t t = tid; t < ncent; t += nt) vals[t] = vq[t];
+            float* ysm = reinterpret_cast<float*>(hist);  // the query vector, briefly (hist is free here)
+            for (uint32_t d = tid; d < dim; d += nt) ysm[d] = f.Y[q * dim + d];
+            __syncthreads();
             if (tid == 0) {
                 float yn = 0.0f;
-                for (uint32_t d = 0; d < dim; d++) yn = fmaf(f.Y[q * dim + d], f.Y[q * dim + d], yn);
+                for (uint32_t d = 0; d < dim; d++) yn = fmaf(ysm[d], ysm[d], yn);
                 s_yn = yn;
                 s_w1max = 0u;
             }
@@ -619,11 +622,19 @@ __global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs
         // compacted in ascending id order
         for (uint32_t i = tid; i < nw; i += nt) bitmap[i] = 0;
         __syncthreads();
-        const uint32_t nn = w1 * (n + 1);
-        for (uint32_t e = tid; e < nn; e += nt) {
-            const uint32_t r = e / (n + 1), j = e % (n + 1);
-            const uint32_t c = j == 0 ? topS[r] : a.nbr[(uint64_t)topS[r] * n + (j - 1)];
-            atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+        // regions, then their neighbour rows (coalesced, up to 8 loads in flight per thread)
+        for (uint32_t r = tid; r < w1; r += nt) atomicOr(&bitmap[topS[r] >> 5], 1u << (topS[r] & 31));
+        const uint32_t ne = w1 * n;
+        for (uint32_t e0 = 0; e0 < ne; e0 += 8 * nt) {
+            uint32_t c[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint32_t e = e0 + u * nt + tid;
+                c[u] = e < ne ? __ldg(a.nbr + (uint64_t)topS[e / n] * n + e % n) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (c[u] != 0xffffffffu) atomicOr(&bitmap[c[u] >> 5], 1u << (c[u] & 31));
         }
         __syncthreads();
         const uint32_t per = (nw + nt - 1) / nt;
