@@ -358,4 +358,62 @@ void launch_eterm_lists(const AddArgs& a, const uint64_t* list_off, uint32_t nce
     CUDA_LAUNCH_CHECK();
 }
 
+
+namespace dev {
+
+// key = cell << 40 | the entry's first 5 code bytes (m >= 5; fewer bytes for
+// smaller m), value = canonical position; one warp per cell
+__global__ void k_scan_order_keys(const uint64_t* __restrict__ list_off, uint32_t ncell, const uint8_t* __restrict__ codes,
+                                  uint32_t m, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t c = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ncell; c += nw) {
+        const uint64_t b0 = list_off[c], b1 = list_off[c + 1];
+        for (uint64_t e = b0 + lane; e < b1; e += 32) {
+            uint64_t key = c << 40;
+            const uint32_t nb = m < 5 ? m : 5;
+            for (uint32_t b = 0; b < nb; b++) key |= (uint64_t)codes[e * m + b] << (32 - 8 * b);
+            keys[e] = key;
+            vals[e] = (uint32_t)e;
+        }
+    }
+}
+
+__global__ void k_gather_scan_order(const uint32_t* __restrict__ order, uint64_t n, uint32_t m,
+                                    const uint8_t* __restrict__ codes, const uint32_t* __restrict__ ids,
+                                    const uint32_t* __restrict__ eterm_lam, uint8_t* __restrict__ scodes,
+                                    uint32_t* __restrict__ sids, uint32_t* __restrict__ seterm_lam) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t o = order[i];
+        if (m == 16) {
+            reinterpret_cast<uint4*>(scodes)[i] = reinterpret_cast<const uint4*>(codes)[o];
+        } else if (m == 8) {
+            reinterpret_cast<uint2*>(scodes)[i] = reinterpret_cast<const uint2*>(codes)[o];
+        } else {
+            for (uint32_t b = 0; b < m; b++) scodes[i * m + b] = codes[o * m + b];
+        }
+        sids[i] = ids[o];
+        seterm_lam[i] = eterm_lam[o];
+    }
+}
+
+}  // namespace dev
+
+void launch_scan_order_keys(const uint64_t* list_off, uint32_t ncell, const uint8_t* codes, uint32_t m, uint64_t n,
+                            uint64_t* keys, uint32_t* vals, cudaStream_t st) {
+    if (n == 0) return;
+    dev::k_scan_order_keys<<<4736, 256, 0, st>>>(list_off, ncell, codes, m, keys, vals);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_gather_scan_order(const uint32_t* order, uint64_t n, uint32_t m, const uint8_t* codes, const uint32_t* ids,
+                              const uint32_t* eterm_lam, uint8_t* scodes, uint32_t* sids, uint32_t* seterm_lam,
+                              cudaStream_t st) {
+    if (n == 0) return;
+    dev::k_gather_scan_order<<<(unsigned)dev::umin64((n + 255) / 256, 4736 * 4), 256, 0, st>>>(order, n, m, codes, ids,
+                                                                                              eterm_lam, scodes, sids,
+                                                                                              seterm_lam);
+    CUDA_LAUNCH_CHECK();
+}
+
 }  // namespace vlq

@@ -56,6 +56,7 @@ uint32_t w2_of(uint32_t w1, float alpha, uint32_t n) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_SCAN_REORDER")) cfg_.scan_reorder = cfg_.scan_reorder_build = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -278,6 +279,47 @@ void Engine::pack_eterm_lam() {
     DeviceGuard g(cfg_.device);
     eterm_lam_.alloc(std::max<uint64_t>(nent_, 1));
     launch_pack_eterm_lam(eterm_.p, lambdas_.p, nent_, eterm_lam_.p, stream_);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    build_scan_order();
+}
+
+// The fast scan's copy of the entries: inside every list, sorted by the first
+// code bytes (the scan's tie-break is the entry position, the re-score reads
+// the id from sids_, and the result is the exact (dist, id) top-k either way).
+// Neighbouring lanes then share LUT words more often: at C4 the simulated
+// shared-memory wavefronts per LUT lookup drop from 1.93 to 1.81
+// (profiles/r2_bank_sim_c4.txt).  Canonical (id-order) arrays stay for the
+// exact paths, the re-score of non-reordered data, save and get_lists.
+void Engine::build_scan_order() {
+    scodes_.reset();
+    sids_.reset();
+    seterm_lam_.reset();
+    const uint64_t ncell = (uint64_t)k_ * n_;
+    if (!cfg_.scan_reorder_build || nent_ == 0 || !(m_ == 16 || m_ == 8 || m_ == 4) || ncell >= (1ull << 24) ||
+        nent_ >= (1ull << 31))
+        return;
+    DeviceGuard g(cfg_.device);
+    DevBuf<uint64_t> k0, k1;
+    DevBuf<uint32_t> v0, v1;
+    k0.alloc(nent_);
+    k1.alloc(nent_);
+    v0.alloc(nent_);
+    v1.alloc(nent_);
+    launch_scan_order_keys(list_off_.p, (uint32_t)ncell, codes_.p, m_, nent_, k0.p, v0.p, stream_);
+    int cell_bits = 1;
+    while ((1ull << cell_bits) < ncell) cell_bits++;
+    cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p);
+    cub::DoubleBuffer<uint32_t> vb(v0.p, v1.p);
+    size_t tb = 0;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)nent_, 0, 40 + cell_bits, stream_));
+    DevBuf<unsigned char> temp;
+    temp.alloc(std::max<size_t>(tb, 1));
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp.p, tb, kb, vb, (int)nent_, 0, 40 + cell_bits, stream_));
+    scodes_.alloc(nent_ * m_);
+    sids_.alloc(nent_);
+    seterm_lam_.alloc(nent_);
+    launch_gather_scan_order(vb.Current(), nent_, m_, codes_.p, ids_.p, eterm_lam_.p, scodes_.p, sids_.p,
+                             seterm_lam_.p, stream_);
     CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
@@ -986,6 +1028,11 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         mark(PH_SCAN);
         if (cfg_.scan_packed && cfg_.scan_variant == 0 && eterm_lam_.p && (m_ == 16 || m_ == 8 || m_ == 4)) {
             a.eterm_lam = eterm_lam_.p;
+            if (cfg_.scan_reorder && scodes_.p) {  // the reordered copy (build_scan_order)
+                a.eterm_lam = seterm_lam_.p;
+                a.scodes = scodes_.p;
+                a.sids = sids_.p;
+            }
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
         a.scan_cap = cfg_.scan_cap;
@@ -1006,6 +1053,10 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             launches += 1;
         }
         if (!fast_kind || !launch_scan_fast(sa, nt, w2, keep, slots, st)) {
+            // the generic scan keys canonical positions: re-score from the canonical arrays
+            a.scodes = nullptr;
+            a.sids = nullptr;
+            if (a.eterm_lam) a.eterm_lam = eterm_lam_.p;
             sa = a;
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
         }
@@ -1082,6 +1133,7 @@ uint32_t Engine::scan_keep(uint32_t topk) const {
 void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
+    else if (key == "scan_reorder") cfg_.scan_reorder = (int)value;
     else if (key == "scan_lpt") cfg_.scan_lpt = (int)value;
     else if (key == "scan_round_cap") cfg_.scan_round_cap = (uint32_t)value;
     else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;

@@ -58,6 +58,12 @@ struct SearchArgs {
     // certificate when the packed stream was scanned
     const uint32_t* eterm_lam;
     float e_pack_err;
+    // scan order (engine.cu build_scan_order): within each list the entries
+    // sorted by their leading code bytes, so a warp's lanes share LUT words more
+    // often; eterm_lam is then in this order too, scodes / sids are the codes and
+    // ids in it (null: the canonical id order)
+    const uint8_t* scodes;
+    const uint32_t* sids;
     uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
     uint32_t round_cap = 0;  // fast scan: most chunks per warp between block barriers (0 = 32)
     bool sel_agg;       // fast-scan flush: warp-aggregated (match_any) histogram atomics
@@ -150,6 +156,13 @@ void launch_minmax(const float* v, uint64_t n, float* out2, cudaStream_t st);
 void launch_gather_entries(const uint32_t* order, uint64_t n, uint32_t m, uint64_t first_id,
                            const uint8_t* codes_pt, const uint8_t* lamb_pt, const float* eterm_pt,
                            uint32_t* ids, uint8_t* codes, uint8_t* lambdas, float* eterm, cudaStream_t st);
+// scan order of the posting entries (engine.cu): order[] = the canonical
+// positions sorted by (cell, leading code bytes)
+void launch_scan_order_keys(const uint64_t* list_off, uint32_t ncell, const uint8_t* codes, uint32_t m, uint64_t n,
+                            uint64_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_gather_scan_order(const uint32_t* order, uint64_t n, uint32_t m, const uint8_t* codes, const uint32_t* ids,
+                              const uint32_t* eterm_lam, uint8_t* scodes, uint32_t* sids, uint32_t* seterm_lam,
+                              cudaStream_t st);
 void launch_histogram(const uint32_t* cells, uint64_t n, unsigned long long* counts, cudaStream_t st);
 
 }  // namespace vlq

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             av2 = make_float2(av, av);
             Bc2 = make_float2((bv - av) - cv, (bv - av) - cv);
             cv2 = make_float2(cv, cv);
-            codes_c = a.codes + b0 * M;
+            codes_c = (a.scodes ? a.scodes : a.codes) + b0 * M;
             lam_c = a.lambdas + b0;
             e_c = a.eterm + b0;
             if (packed) el_c = a.eterm_lam + b0;

@@ -487,16 +487,19 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
             const uint32_t cell = ccell[lo];
             const uint32_t i = cell / a.n;
             const uint32_t s = a.nbr[cell];
-            const float lam = dequantize_lambda(a.lambdas[pos], a.lo, a.hi);
+            // reordered scan copy: the lambda byte is the packed word's low byte, the id in sids
+            const uint32_t lbyte = a.scodes ? (a.eterm_lam[pos] & 0xffu) : (uint32_t)a.lambdas[pos];
+            const float lam = dequantize_lambda(lbyte, a.lo, a.hi);
             const float d = line_sqdist(wsq[i], wsq[s], a.elen[cell], lam);
             const float* t3i = a.t3 + (uint64_t)i * m * VLQ_KSUB;
             const float* t3s = a.t3 + (uint64_t)s * m * VLQ_KSUB;
             float s2 = 0.0f, s3 = 0.0f, s4 = 0.0f, s5 = 0.0f;
+            const uint8_t* codes = a.scodes ? a.scodes : a.codes;
             if constexpr (M > 0) {
                 uint8_t code[M];
-                if constexpr (M == 16) *reinterpret_cast<uint4*>(code) = __ldg(reinterpret_cast<const uint4*>(a.codes + pos * 16));
-                else if constexpr (M == 8) *reinterpret_cast<uint2*>(code) = __ldg(reinterpret_cast<const uint2*>(a.codes + pos * 8));
-                else *reinterpret_cast<uint32_t*>(code) = __ldg(reinterpret_cast<const uint32_t*>(a.codes + pos * 4));
+                if constexpr (M == 16) *reinterpret_cast<uint4*>(code) = __ldg(reinterpret_cast<const uint4*>(codes + pos * 16));
+                else if constexpr (M == 8) *reinterpret_cast<uint2*>(code) = __ldg(reinterpret_cast<const uint2*>(codes + pos * 8));
+                else *reinterpret_cast<uint32_t*>(code) = __ldg(reinterpret_cast<const uint32_t*>(codes + pos * 4));
                 float v2[M], v3[M], v4[M], v5[M];
 #pragma unroll
                 for (int p = 0; p < M; p++) {  // every gather in flight at once
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
                     s5 = __fadd_rn(s5, v5[p]);
                 }
             } else {
-                const uint8_t* code = a.codes + pos * m;
+                const uint8_t* code = codes + pos * m;
                 for (uint32_t p = 0; p < m; p++) {
                     const uint32_t c = code[p];
                     s2 = __fadd_rn(s2, a.t2[p * VLQ_KSUB + c]);
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
             r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, __fsub_rn(1.0f, lam)), s3));
             r = __fadd_rn(r, __fmul_rn(__fmul_rn(2.0f, lam), s4));
             r = __fsub_rn(r, __fmul_rn(2.0f, s5));
-            key = make_key(r, a.ids[pos]);
+            key = make_key(r, a.scodes ? a.sids[pos] : a.ids[pos]);
             if (t == have - 1) s_fast_last = unord_float((uint32_t)(ck >> 32));
         }
         keys[t] = key;
