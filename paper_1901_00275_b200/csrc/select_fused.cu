@@ -710,31 +710,16 @@ __global__ void __launch_bounds__(FS_THREADS) k_second_sel(SearchArgs a, FusedAr
         const uint32_t w = c >> 5;
         return nval[wpref[w] + __popc(bitmap[w] & ((1u << (c & 31)) - 1u))];
     };
-    // second_level_rank (search.cpp:38-78); the edges' neighbour ids and
-    // lengths loaded 8-deep (coalesced rows of the graph) before the math
-    for (uint32_t e0 = 0; e0 < total; e0 += 8 * nt) {
-        uint32_t sv[8];
-        float cvv[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const uint32_t e = e0 + u * nt + tid;
-            if (e < total) {
-                const uint64_t g = (uint64_t)topS[e / n] * n + e % n;
-                sv[u] = __ldg(a.nbr + g);
-                cvv[u] = __ldg(a.elen + g);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const uint32_t e = e0 + u * nt + tid;
-            if (e >= total) continue;
-            const float av = val_of(topS[e / n]);
-            const float bv = val_of(sv[u]);
-            const float cv = cvv[u];
-            if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
-            const float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
-            dq[e] = line_sqdist(av, bv, cv, lam);
-        }
+    // second_level_rank (search.cpp:38-78)
+    for (uint32_t e = tid; e < total; e += nt) {
+        const uint32_t i = topS[e / n], j = e % n;
+        const float av = val_of(i);
+        const uint32_t s = a.nbr[(uint64_t)i * n + j];
+        const float bv = val_of(s);
+        const float cv = a.elen[(uint64_t)i * n + j];
+        if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
+        const float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
+        dq[e] = line_sqdist(av, bv, cv, lam);
     }
     __syncthreads();
     block_select_ordered_range(dq, total, w2, selpos, hist, scan);
