@@ -76,8 +76,6 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
 
 Engine::~Engine() {
     if (flusher_.joinable()) flusher_.join();
-    for (auto& e : d2h_ev_)
-        if (e) cudaEventDestroy(e);
     for (auto& sl : prof_) {
         for (auto& e : sl.ev)
             if (e) cudaEventDestroy(e);
@@ -1400,38 +1398,19 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     // this call's D2H lands on them (flushed in the background meanwhile)
     if (flusher_.joinable()) flusher_.join();
     const auto t2 = now();
-    // the results come back in row chunks: the host copies chunk c out of the
-    // pinned staging while chunk c + 1 is still in flight; the device error
-    // flag travels ahead of them
-    if (!d2h_ev_[0])
-        for (auto& e : d2h_ev_) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    err_host_.alloc(64);
-    CUDA_CHECK(cudaMemcpyAsync(err_host_.p, err_.p, 4, cudaMemcpyDeviceToHost, st));
-    constexpr int NCH = 4;
-    for (int c = 0; c < NCH; c++) {
-        const uint64_t r0 = nq * c / NCH, r1 = nq * (c + 1) / NCH;
-        if (topk && r1 > r0) {
-            CUDA_CHECK(cudaMemcpyAsync(pi + r0 * topk * 8, si_.p + r0 * topk, (r1 - r0) * topk * 8,
-                                       cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaMemcpyAsync(pd + r0 * topk * 4, sd_.p + r0 * topk, (r1 - r0) * topk * 4,
-                                       cudaMemcpyDeviceToHost, st));
-        }
-        if (scanned && r1 > r0)
-            CUDA_CHECK(cudaMemcpyAsync(ps + r0 * 8, ss_.p + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, st));
-        CUDA_CHECK(cudaEventRecord(d2h_ev_[c], st));
+    if (topk) {
+        CUDA_CHECK(cudaMemcpyAsync(pi, si_.p, ib, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(pd, sd_.p, db, cudaMemcpyDeviceToHost, st));
     }
+    if (scanned) CUDA_CHECK(cudaMemcpyAsync(ps, ss_.p, sb, cudaMemcpyDeviceToHost, st));
     if (timing) CUDA_CHECK(cudaEventRecord(tev[3], st));
+    check_device_errors(st);
     const auto t3 = now();
-    for (int c = 0; c < NCH; c++) {
-        CUDA_CHECK(cudaEventSynchronize(d2h_ev_[c]));
-        if (c == 0 && *reinterpret_cast<volatile unsigned int*>(err_host_.p)) check_device_errors(st);  // throws
-        const uint64_t r0 = nq * c / NCH, r1 = nq * (c + 1) / NCH;
-        if (topk && r1 > r0) {
-            par_memcpy(ids + r0 * topk, pi + r0 * topk * 8, (r1 - r0) * topk * 8, Pinned::NoFlush);
-            par_memcpy(dists + r0 * topk, pd + r0 * topk * 4, (r1 - r0) * topk * 4, Pinned::NoFlush);
-        }
-        if (scanned && r1 > r0) par_memcpy(scanned + r0, ps + r0 * 8, (r1 - r0) * 8, Pinned::NoFlush);
+    if (topk) {
+        par_memcpy(ids, pi, ib, Pinned::NoFlush);
+        par_memcpy(dists, pd, db, Pinned::NoFlush);
     }
+    if (scanned) par_memcpy(scanned, ps, sb, Pinned::NoFlush);
     // evict the output staging lines the copy threads just read, off the
     // caller's critical path (joined before the next D2H into them)
     flusher_ = std::thread([pi, n = ib + db + sb] { flush_lines(pi, n); });

@@ -363,8 +363,6 @@ private:
     DevBuf<int64_t> si_;
     DevBuf<uint64_t> ss_;
     PinnedBuf pin_;
-    PinnedBuf err_host_;               // the device error flag, read back with the results
-    cudaEvent_t d2h_ev_[4] = {};        // search_host: result chunks landed
     std::thread flusher_;  // background cache flush of the host-search output staging
     // adaptive k': the previous fine stage's certificate-failure count lands
     // here asynchronously (read one call later; a stale value only delays
