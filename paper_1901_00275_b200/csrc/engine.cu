@@ -280,7 +280,18 @@ void Engine::pack_eterm_lam() {
     eterm_lam_.alloc(std::max<uint64_t>(nent_, 1));
     launch_pack_eterm_lam(eterm_.p, lambdas_.p, nent_, eterm_lam_.p, stream_);
     CUDA_CHECK(cudaStreamSynchronize(stream_));
-    build_scan_order();
+    try {
+        build_scan_order();
+    } catch (const CudaError&) {
+        // the reordered copy is an optimisation (24 B per entry of temporary
+        // and 20 B of permanent device memory): without room for it the fast
+        // scan reads the canonical arrays
+        scodes_.reset();
+        sids_.reset();
+        seterm_lam_.reset();
+        (void)cudaGetLastError();
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
 }
 
 // The fast scan's copy of the entries: inside every list, sorted by the first
