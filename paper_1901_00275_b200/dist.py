@@ -20,8 +20,10 @@ over all ranks).  Per batch
 3. every rank applies the gathered selection (its own scanned counts and
    certificate bound) and runs term5, the fused scan and the exact re-score
    for the whole batch on the cells it owns;
-4. the local exact top-k rows are all-gathered and merged by the K9 kernel
-   (vlq_merge_topk_device).
+4. the local exact top-k rows are exchanged BY QUERY SLICE (one all-to-all:
+   rank r receives every rank's rows of its slice), each rank merges its own
+   slice with the K9 kernel (vlq_merge_topk_device), and the merged slices
+   are all-gathered (slice_merge).
 
 `search_query_split` is the earlier schedule: only first_level_scan is split
 (top-w1 tables, 2.5 MB, all-gathered) and every rank repeats the exact
@@ -79,6 +81,41 @@ def gather_parts(local_ids, local_dists, group=None):
     _all_gather(gi, local_ids.contiguous(), group)
     _all_gather(gd, local_dists.contiguous(), group)
     return gi.view((world,) + tuple(local_ids.shape)), gd.view((world,) + tuple(local_dists.shape))
+
+
+def _all_to_all(out, inp, group=None):
+    """all_to_all_single over equal row blocks (host copies for gloo)."""
+    import torch.distributed as dist
+    if inp.is_cuda and dist.get_backend(group) != "nccl":
+        o = out.cpu()
+        dist.all_to_all_single(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, group=group)
+
+
+def slice_merge(local_ids, local_dists, group=None, merge_fn=None):
+    """(dist, id) merge of the per-shard top-k blocks BY QUERY SLICE: rank r
+    receives the rows of its slice (query_slice) from every rank (one
+    all-to-all: nq/G x k x 12 bytes from each peer instead of the whole
+    blocks), merges only those, and the merged slices are all-gathered.
+    Returns the merged [nq, k] (ids, dists) on every rank.  merge_fn(ids [G,
+    rows, k], dists) -> merged; default: the K9 kernel (merge_topk)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    nq, k = local_ids.shape
+    per = (nq + world - 1) // world
+    si = torch.full((world * per, k), -1, dtype=local_ids.dtype, device=local_ids.device)
+    sd = torch.full((world * per, k), float("inf"), dtype=local_dists.dtype, device=local_dists.device)
+    si[:nq] = local_ids
+    sd[:nq] = local_dists
+    ri, rd = torch.empty_like(si), torch.empty_like(sd)
+    _all_to_all(ri, si, group)
+    _all_to_all(rd, sd, group)
+    parts_i, parts_d = ri.view(world, per, k), rd.view(world, per, k)
+    mi, md = (merge_fn or merge_topk)(parts_i, parts_d)
+    return gather_rows(mi, nq, group), gather_rows(md, nq, group)
 
 
 def query_slice(nq: int, rank: int, world: int) -> tuple[int, int]:
@@ -200,6 +237,7 @@ class ShardedIndex:
         ids, dists, scanned = out
         self.index.search_fine_sel_device(d_queries.data_ptr(), nq, w1, alpha, k, sel.data_ptr(), ab.data_ptr(),
                                           ids.data_ptr(), dists.data_ptr(), scanned.data_ptr(), st)
-        gi, gd = gather_parts(ids, dists, self.group)
-        mi, md = merge_topk(gi, gd, st)
+        # merge by query slice: all-to-all of the slices' rows, each rank merges
+        # its own slice, the merged slices are all-gathered
+        mi, md = slice_merge(ids, dists, self.group, lambda pi, pd: merge_topk(pi, pd, st))
         return mi, md, scanned

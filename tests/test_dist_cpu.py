@@ -267,3 +267,56 @@ def test_shard_of_cell_matches_the_engine():
     assert counts.min() > 0.99 * counts.mean() and counts.max() < 1.01 * counts.mean()
     region = [shard_of_cell(17 * 32 + j, 8) for j in range(32)]
     assert len(set(region)) >= 6  # one region's lists land on most ranks
+
+
+def _worker_slice_merge(rank, world, port, name, params, out_path):
+    """dist.slice_merge (the select-split schedule's merge by query slice:
+    all-to-all of the slices' rows, per-rank merge of its slice, all-gather of
+    the merged slices) over oracle shard results."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle, vlq1
+    from paper_1901_00275_b200.dist import slice_merge
+    z, index_path, _ = load_golden(name)
+    ix = vlq1.read(index_path)
+    shard = oracle.OracleIndex(shard_of(ix, rank, world))
+
+    def np_merge(pi, pd):
+        mi, md = merge_np(pi.numpy(), pd.numpy())
+        return torch.from_numpy(mi), torch.from_numpy(md)
+
+    res = []
+    for w1, alpha, k in params:
+        ids, d, _ = shard.search(z["queries"], w1, alpha, k)
+        mi, md = slice_merge(torch.from_numpy(ids), torch.from_numpy(d), merge_fn=np_merge)
+        res.append((mi.numpy(), md.numpy()))
+    if rank == 0:
+        import pickle
+        with open(out_path, "wb") as f:
+            pickle.dump(res, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_slice_merge_equals_single_index(world, tmp_path):
+    import torch.multiprocessing as mp
+    from oracle import oracle
+    name = "accept_small"
+    params = [(16, 0.5, 10), (64, 0.25, 100)]
+    out = str(tmp_path / "merged.pkl")
+    mp.start_processes(_worker_slice_merge, args=(world, _free_port(), name, params, out), nprocs=world, join=True,
+                       start_method="spawn")
+    import pickle
+    with open(out, "rb") as f:
+        merged = pickle.load(f)
+    z, index_path, _ = load_golden(name)
+    o = oracle.OracleIndex.load(index_path)
+    for (w1, alpha, k), (mi, md) in zip(params, merged):
+        ids, d, _ = o.search(z["queries"], w1, alpha, k)
+        assert np.array_equal(mi, ids)
+        assert np.array_equal(np.asarray(md, np.float32).view(np.uint32), d.view(np.uint32))
