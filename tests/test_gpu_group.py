@@ -100,3 +100,17 @@ def test_group_errors(vlqadc):
         vlqadc.IndexGroup([0, 0, 0], shards=2)
     with pytest.raises(RuntimeError, match="index already holds a base set"):
         grp.add(regen_base(z))
+
+
+@pytest.mark.parametrize("k", [1500])
+def test_group_large_k_and_exact_scan(vlqadc, oracle_mod, k):
+    """k > 1024 (every shard's exact all-candidates path, merged by the group)
+    and the forced exact scan through a 3-shard group."""
+    z, index_path, _ = load_golden("m16")
+    o = oracle_mod.OracleIndex.load(index_path)
+    for kw in [dict(), dict(force_exact=True)]:
+        grp = vlqadc.IndexGroup.load(index_path, [0, 0, 0], **kw)
+        for w1, alpha, kk in [(16, 0.5, k), (8, 1.0, 100)]:
+            ids, d = grp.search(z["queries"][:30], w1=w1, alpha=alpha, k=kk)
+            oids, od, _ = o.search(z["queries"][:30], w1, alpha, kk)
+            assert np.array_equal(ids, oids) and same_f32(d, od), (kw, w1, alpha, kk)
