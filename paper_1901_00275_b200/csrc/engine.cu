@@ -881,7 +881,7 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
     // evaluation + first and second level fused per query
     if (w2 > 0 && tc_ && cfg_.tc_chunk_select && k_ >= cfg_.tc_search_min_k && k_ <= 262144 && w1 < k_ &&
         (k_ + 7) / 8 >= 2 * w1 &&
-        select_fused_supported(k_, n_, w1, w2, dim_, cfg_.tc_chunk_cap) && tmin8_.p) {
+        select_split_supported(k_, n_, w1, w2, dim_, cfg_.tc_chunk_cap) && tmin8_.p) {
         const uint32_t nchunk8 = ((k_ + 127) / 128) * 16;
         const float* x1 = nullptr;
         if (cfg_.tc_persist) {
@@ -898,37 +898,25 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
                             tch_.p, st);
         SearchArgs a = search_args();
         CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
-        if (cfg_.tc_select_split && select_split_supported(k_, n_, w1, w2, dim_, cfg_.tc_chunk_cap)) {
-            // split form: row kernels at full occupancy + light per-query selections
-            const uint32_t ldn = select_need_capacity(n_, w1), nk = select_chunk_keys();
-            svals_.alloc((uint64_t)nt * nk);
-            snid_.alloc((uint64_t)nt * ldn);
-            snval_.alloc((uint64_t)nt * ldn);
-            snneed_.alloc(nt);
-            launch_rows(centroids_.p, d_q, k_, dim_, 1, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, cfg_.tc_chunk_cap,
-                        svals_.p, nk, nt, st);
-            launch_top_need(a, nt, d_q, w1, w2, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmax_, nullptr, nullptr,
-                            qlist_.p, err_.p + 6, svals_.p, snid_.p, snneed_.p, ldn, st);
-            // certificate failures / chunk-list overflows: exact full rows, exact
-            // top-w1, then the needed ids from that top-w1
-            launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
-            launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
-            launch_top_need(a, nt, d_q, w1, w2, nullptr, nullptr, 0, nullptr, cmax_, qlist_.p, err_.p + 6, nullptr,
-                            nullptr, svals_.p, snid_.p, snneed_.p, ldn, st);
-            launch_rows(centroids_.p, d_q, k_, dim_, 0, snid_.p, snneed_.p, ldn, 0, snval_.p, ldn, nt, st);
-            launch_second_sel(a, nt, w1, w2, snid_.p, snval_.p, snneed_.p, ldn, sel_out, ab_out, st);
-            launches += 5;
-        } else {
-            launch_select_fused(a, nt, d_q, w1, w2, 8, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmax_, nullptr,
-                                nullptr, qlist_.p, err_.p + 6, sel_out, ab_out, st);
-            // certificate failures / chunk-list overflows: exact full rows, exact
-            // top-w1, then the fused kernel again from that top-w1
-            launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
-            launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
-            launch_select_fused(a, nt, d_q, w1, w2, 8, nullptr, nullptr, 0, nullptr, cmax_, qlist_.p, err_.p + 6,
-                                nullptr, nullptr, sel_out, ab_out, st);
-        }
-        launches += 6;
+        // row kernels at full occupancy + light per-query selections (select_fused.cu)
+        const uint32_t ldn = select_need_capacity(n_, w1), nk = select_chunk_keys();
+        svals_.alloc((uint64_t)nt * nk);
+        snid_.alloc((uint64_t)nt * ldn);
+        snval_.alloc((uint64_t)nt * ldn);
+        snneed_.alloc(nt);
+        launch_rows(centroids_.p, d_q, k_, dim_, 1, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, cfg_.tc_chunk_cap,
+                    svals_.p, nk, nt, st);
+        launch_top_need(a, nt, d_q, w1, w2, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmax_, nullptr, nullptr,
+                        qlist_.p, err_.p + 6, svals_.p, snid_.p, snneed_.p, ldn, st);
+        // certificate failures / chunk-list overflows: exact full rows, exact
+        // top-w1, then the needed ids from that top-w1
+        launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
+        launch_first_level_list(ws_.p, nt, k_, w1, top_.p, qlist_.p, err_.p + 6, st);
+        launch_top_need(a, nt, d_q, w1, w2, nullptr, nullptr, 0, nullptr, cmax_, qlist_.p, err_.p + 6, nullptr,
+                        nullptr, svals_.p, snid_.p, snneed_.p, ldn, st);
+        launch_rows(centroids_.p, d_q, k_, dim_, 0, snid_.p, snneed_.p, ldn, 0, snval_.p, ldn, nt, st);
+        launch_second_sel(a, nt, w1, w2, snid_.p, snval_.p, snneed_.p, ldn, sel_out, ab_out, st);
+        launches += 8;
         *fused = true;
         return true;
     }
@@ -1154,7 +1142,6 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "tc_pass1_single") cfg_.tc_pass1_single = (int)value;
     else if (key == "tc_pass2_single") cfg_.tc_pass2_single = (int)value;
     else if (key == "tc_chunk_select") cfg_.tc_chunk_select = (int)value;
-    else if (key == "tc_select_split") cfg_.tc_select_split = (int)value;
     else if (key == "tc_chunk_cap") cfg_.tc_chunk_cap = (uint32_t)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;

@@ -58,7 +58,6 @@ struct EngineConfig {
     int tc_pass2_single = 0;  // ... and the filter pass in 1xTF32 too (tau raised by both bounds; more candidates)
     int tc_chunk_select = 1;  // chunk-select coarse stage (one 1xTF32 pass of 8-centroid chunk minima, exact
                               // evaluation of the selected chunks, fused first + second level; select_fused.cu)
-    int tc_select_split = 1;  // chunk-select stage in split form (row kernels + selection kernels) vs one fused kernel
     uint32_t tc_chunk_cap = 256;  // selected chunks per query before the exact full-row fallback (study knob)
 };
 

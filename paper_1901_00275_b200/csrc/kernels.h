@@ -187,8 +187,6 @@ namespace vlq {
 // tensor-core coarse stage (coarse_tc.cu)
 bool coarse_tc_supported(uint32_t dim);
 // chunk-select coarse stage (select_fused.cu)
-size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc);
-bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc);
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
                          float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st);
 // split form of the fused kernel (select_fused.cu): row kernels + light
@@ -206,10 +204,6 @@ void launch_top_need(const SearchArgs& a, uint64_t nblocks, const float* Y, uint
 void launch_second_sel(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, const uint32_t* nid,
                        const float* nval, const uint32_t* nneed, uint32_t ldn, uint32_t* sel_out, float* ab_out,
                        cudaStream_t st);
-void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2, uint32_t cs,
-                         const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
-                         const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
-                         uint32_t* sel_out, float* ab_out, cudaStream_t st);
 bool coarse_tc_split_supported(uint32_t dim);
 void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
                                cudaStream_t st, int rna = 0);

@@ -7,13 +7,14 @@
 //   k_chunk_select             tau >= the w1-th smallest chunk minimum (histogram),
 //                              T = tau + 2.02 eps (eps = tc_eps, the TF32 bound);
 //                              compacts the chunks with minimum <= T
-//   k_select_fused             exact reference-order sqdist of every centroid in
-//                              those chunks -> exact top-w1 by (dist, id) with a
-//                              certificate; exact distances of the w1 regions'
-//                              neighbours (bitmap-deduplicated, kept in shared
-//                              memory); second_level_rank over the w1 n edges ->
-//                              the selected cells, their (a, b) pairs, the
-//                              scanned count and the |term1| bound
+//   k_rows (chunks)            exact reference-order sqdist of every centroid in
+//                              those chunks (barrier-free row kernel)
+//   k_top_need                 exact top-w1 by (dist, id) with a certificate;
+//                              the w1 regions' neighbours, bitmap-deduplicated
+//   k_rows (needed ids)        their exact distances
+//   k_second_sel               second_level_rank over the w1 n edges -> the
+//                              selected cells, their (a, b) pairs, the scanned
+//                              count and the |term1| bound
 //
 // Why the chunk set is complete (the certificate, checked per query): the w1
 // chunks whose minimum is <= tau each hold a centroid with approx <= tau, i.e.
@@ -22,8 +23,8 @@
 // chunks has approx > T, i.e. exact > T + |y|^2 - eps = tau + |y|^2 + 1.02 eps.
 // The kernel checks T + |y|^2 - eps > exact_w1 explicitly (in double); a query
 // that fails it (or whose chunk list overflows) is listed and takes the exact
-// full-row path (k_exact_rows + k_first_level_list), then this kernel again
-// in "top" mode from its exact top-w1.
+// full-row path (k_exact_rows + k_first_level_list), then k_top_need in
+// "top" mode from its exact top-w1.
 //
 // Versus the two-pass filter (1xTF32 chunk minima + 3xTF32 filter pass +
 // exact refine + k_exact_needed writing ~2k exact distances into a K-wide ws
@@ -39,9 +40,6 @@ namespace vlq {
 namespace dev {
 
 constexpr uint32_t FS_THREADS = 256;
-constexpr uint32_t FS_PW = 32;         // dimensions per staged row piece (one 128-byte line per row)
-constexpr uint32_t FS_RS = FS_PW + 4;  // staged row stride in floats (conflict-free LDS.128)
-constexpr uint32_t FS_BUF_FLOATS = 32 * FS_RS;  // one piece of 32 rows
 constexpr uint32_t FS_MAX_KEYS = 2048; // exactly evaluated chunk centroids per query
 constexpr uint32_t FS_CS = 8;          // centroids per chunk (TILEMIN8)
 
@@ -271,13 +269,6 @@ __device__ __forceinline__ void exact_rows_pipe_t(const float* __restrict__ C, u
     cp_async_wait<0>();
 }
 
-template <typename IdFn, typename OutFn>
-__device__ __forceinline__ void exact_rows_pipe(const float* __restrict__ C, uint32_t k, uint32_t dim,
-                                                const float* ys, float* wbuf, uint32_t cnt, IdFn&& id_of,
-                                                OutFn&& out) {
-    exact_rows_pipe_t<FS_PW, 2>(C, k, dim, ys, wbuf, cnt, threadIdx.x >> 5, blockDim.x >> 5, id_of, out);
-}
-
 struct FusedArgs {
     const float* Y;
     uint32_t w1, w2, cs;      // regions, cells, centroids per chunk
@@ -295,215 +286,13 @@ struct FusedArgs {
 };
 
 __host__ __device__ inline uint32_t fs_nwords(uint32_t k) { return (k + 31) / 32; }
-__host__ __device__ inline uint32_t fs_pow2(uint32_t x) {
-    uint32_t p = 1;
-    while (p < x) p <<= 1;
-    return p;
-}
-
-// dynamic shared memory layout (bytes), shared by host and device
-struct FusedLayout {
-    uint32_t ys, topS, u, bufs, total;
-    __host__ __device__ FusedLayout(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
-        const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1), ne = w1 * n;
-        const uint32_t dimp = (dim + FS_PW - 1) / FS_PW * FS_PW;
-        ys = 0;
-        topS = ys + dimp * 4;
-        u = (topS + w1 * 4 + 15) & ~15u;
-        // phase 1: chunk list + chunk-centroid distances + top positions;
-        // phase 2: bitmap (u32), word prefix (u16), needed values, needed ids / edge distances, positions
-        const uint32_t p1 = capc * 4 + FS_MAX_KEYS * 4 + w1 * 4;
-        const uint32_t p2 = nw * 4 + ((nw * 2 + 3) & ~3u) + nn * 4 + (nn > ne ? nn : ne) * 4 + w2 * 4;
-        bufs = (u + (p1 > p2 ? p1 : p2) + 15) & ~15u;
-        // per-warp row-piece double buffers; the selects' histogram (2048 + 40
-        // words) reuses this region outside the row evaluations
-        uint32_t b = (FS_THREADS / 32) * 2 * FS_BUF_FLOATS * 4;
-        if (b < 2088 * 4) b = 2088 * 4;
-        total = bufs + b;
-    }
-};
-
-__global__ void __launch_bounds__(FS_THREADS) k_select_fused(SearchArgs a, FusedArgs f) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ float s_yn;
-    __shared__ unsigned int s_w1max;
-    __shared__ unsigned long long s_scanned;
-    __shared__ float s_dmax;
-    const bool top_mode = f.qlist != nullptr;
-
-    const uint32_t _nb = top_mode ? *f.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
-    for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
-    const uint64_t q = top_mode ? f.qlist[_b] : _b;
-    const uint32_t k = a.k, n = a.n, dim = a.dim, w1 = f.w1, w2 = f.w2;
-    const FusedLayout lay(k, n, w1, w2, dim, f.capc);
-    float* ys = reinterpret_cast<float*>(smem + lay.ys);
-    uint32_t* topS = reinterpret_cast<uint32_t*>(smem + lay.topS);
-    const uint32_t tid = threadIdx.x, nt = blockDim.x;
-    float* wbuf = reinterpret_cast<float*>(smem + lay.bufs) + (tid >> 5) * 2 * FS_BUF_FLOATS;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + lay.bufs);  // aliases the row buffers (used apart)
-    uint32_t* scan = hist + 2048;
-    const uint32_t dimp = (dim + FS_PW - 1) / FS_PW * FS_PW;
-    for (uint32_t d = tid; d < dimp; d += nt) ys[d] = d < dim ? f.Y[q * dim + d] : 0.0f;
-    if (tid == 0) {
-        s_w1max = 0u;
-        s_scanned = 0;
-        s_dmax = 0.0f;
-    }
-    __syncthreads();
-
-    if (!top_mode) {
-        // ---- phase 1: exact distances of the selected chunks' centroids
-        const uint32_t nc = f.ccnt[q];
-        constexpr uint32_t cs = FS_CS;
-        const uint32_t ncent = nc * cs;
-        if (nc > f.capc || ncent > FS_MAX_KEYS || nc < w1) {
-            if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
-            continue;
-        }
-        // the chunk list is ascending, so position order == centroid id order
-        uint32_t* cls = reinterpret_cast<uint32_t*>(smem + lay.u);
-        float* vals = reinterpret_cast<float*>(cls + f.capc);
-        uint32_t* topPos = reinterpret_cast<uint32_t*>(vals + FS_MAX_KEYS);
-        for (uint32_t t = tid; t < nc; t += nt) cls[t] = f.clist[q * f.capc + t];
-        __syncthreads();
-        exact_rows_pipe(a.centroids, k, dim, ys, wbuf, ncent,
-                        [&](uint32_t t) { return cls[t / cs] * cs + (t & (cs - 1)); },
-                        [&](uint32_t t, float v) { vals[t] = v; });
-        if (tid == 0) {
-            float yn = 0.0f;
-            for (uint32_t d = 0; d < dim; d++) yn = fmaf(ys[d], ys[d], yn);
-            s_yn = yn;
-        }
-        __syncthreads();
-        // exact top-w1 by (dist, id): positions ascending == ids ascending
-        block_select_ordered_range(vals, ncent, w1, topPos, hist, scan);
-        __syncthreads();
-        float mx = 0.0f;
-        for (uint32_t r = tid; r < w1; r += nt) {
-            const uint32_t pos = topPos[r];
-            topS[r] = cls[pos / cs] * cs + (pos & (cs - 1));
-            mx = fmaxf(mx, vals[pos]);  // +inf (a padded id) fails the certificate below
-        }
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if ((tid & 31) == 0) atomicMax(&s_w1max, __float_as_uint(mx));  // distances >= 0
-        __syncthreads();
-        const float exact_w1 = __uint_as_float(s_w1max);
-        const float eps = tc_eps(s_yn, f.cmax, dim, false, /*rna=*/true);
-        const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
-        if (!(lower > (double)exact_w1)) {
-            if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
-            continue;
-        }
-        for (uint32_t r = tid; r < w1; r += nt) a.top[q * w1 + r] = topS[r];
-        __syncthreads();
-    } else {
-        for (uint32_t t = tid; t < w1; t += nt) topS[t] = a.top[q * w1 + t];
-        __syncthreads();
-    }
-
-    // ---- phase 2: exact distances of the regions and their neighbours
-    const uint32_t nw = fs_nwords(k), nn = w1 * (n + 1), total = w1 * n;
-    uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + lay.u);
-    uint16_t* wpref = reinterpret_cast<uint16_t*>(bitmap + nw);
-    float* nval = reinterpret_cast<float*>(bitmap + nw + (nw + 1) / 2);
-    uint32_t* nid = reinterpret_cast<uint32_t*>(nval + nn);
-    float* dq = reinterpret_cast<float*>(nid);  // the needed ids are dead once their values are in nval
-    uint32_t* selpos = nid + (nn > total ? nn : total);
-    for (uint32_t i = tid; i < nw; i += nt) bitmap[i] = 0;
-    __syncthreads();
-    for (uint32_t e = tid; e < nn; e += nt) {
-        const uint32_t r = e / (n + 1), j = e % (n + 1);
-        const uint32_t c = j == 0 ? topS[r] : a.nbr[(uint64_t)topS[r] * n + (j - 1)];
-        atomicOr(&bitmap[c >> 5], 1u << (c & 31));
-    }
-    __syncthreads();
-    uint32_t nneed;
-    {
-        const uint32_t per = (nw + nt - 1) / nt;
-        uint32_t local = 0;
-        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) local += __popc(bitmap[i]);
-        uint32_t run = block_excl_scan_u32(local, scan, &nneed);
-        for (uint32_t i = tid * per; i < min(nw, (tid + 1) * per); i++) {
-            wpref[i] = (uint16_t)run;
-            uint32_t w = bitmap[i];
-            while (w) {
-                const uint32_t b = __ffs(w) - 1;
-                nid[run++] = i * 32 + b;
-                w &= w - 1;
-            }
-        }
-    }
-    __syncthreads();
-    exact_rows_pipe(a.centroids, k, dim, ys, wbuf, nneed, [&](uint32_t t) { return nid[t]; },
-                    [&](uint32_t t, float v) { nval[t] = v; });
-    __syncthreads();
-    auto val_of = [&](uint32_t c) -> float {
-        const uint32_t w = c >> 5;
-        return nval[wpref[w] + __popc(bitmap[w] & ((1u << (c & 31)) - 1u))];
-    };
-    // second_level_rank (search.cpp:38-78): line-subregion distances of the
-    // w1 n edges, top-w2 by (dist, centroid id, edge rank) = edge position
-    for (uint32_t e = tid; e < total; e += nt) {
-        const uint32_t i = topS[e / n], j = e % n;
-        const float av = val_of(i);
-        const uint32_t s = a.nbr[(uint64_t)i * n + j];
-        const float bv = val_of(s);
-        const float cv = a.elen[(uint64_t)i * n + j];
-        if (!(cv > 0.0f)) atomicOr(a.error_flag, 1u);  // line_quant.cpp:10-12
-        const float lam = clamp_std(line_lambda(av, bv, cv), 0.0f, 1.0f);
-        dq[e] = line_sqdist(av, bv, cv, lam);
-    }
-    __syncthreads();
-    block_select_ordered_range(dq, total, w2, selpos, hist, scan);
-    __syncthreads();
-    // selected cells (ascending id), their (a, b) into the ws row (read by the
-    // scan and the exact re-score), the scanned count and the |term1| bound
-    // (k_second_level / k_apply_selection formulas)
-    float* wsq = a.ws + q * a.k;
-    const float lmax = a.lam_absmax;
-    unsigned long long cnt = 0;
-    float dmax = 0.0f;
-    for (uint32_t t = tid; t < w2; t += nt) {
-        const uint32_t e = selpos[t];
-        const uint32_t i = topS[e / n], j = e % n;
-        const uint32_t cell = i * n + j;
-        const uint32_t s = a.nbr[cell];
-        const float av = val_of(i), bv = val_of(s), cv = a.elen[cell];
-        a.sel[q * w2 + t] = cell;
-        wsq[i] = av;
-        wsq[s] = bv;
-        if (f.sel_out) {
-            f.sel_out[q * w2 + t] = cell;
-            f.ab_out[(q * w2 + t) * 2] = av;
-            f.ab_out[(q * w2 + t) * 2 + 1] = bv;
-        }
-        cnt += a.list_off[cell + 1] - a.list_off[cell];
-        const float bound = (1.0f + lmax) * fabsf(av) + (lmax * lmax + lmax) * fabsf(cv) + lmax * fabsf(bv);
-        dmax = fmaxf(dmax, bound);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    }
-    if ((tid & 31) == 0) {
-        atomicAdd(&s_scanned, cnt);
-        atomicMax(reinterpret_cast<unsigned int*>(&s_dmax), __float_as_uint(dmax));
-    }
-    __syncthreads();
-    if (tid == 0) {
-        a.meta[q].scanned = s_scanned;
-        a.meta[q].dmax = s_dmax;
-        a.meta[q].flag = 0;
-    }
-    __syncthreads();  // shared memory is reused by the next query
-    }
-}
-
 // ---------------------------------------------------------------------------
-// Split form of k_select_fused (the default): the exact centroid rows run in
-// kernels that do nothing else -- no block barriers, several CTAs per SM with
-// NB row pieces in flight per warp, so the gathered rows stream at L2 speed --
-// and the selections run in light per-query kernels:
+// The exact centroid rows run in kernels that do nothing else -- no block
+// barriers, several CTAs per SM with NB row pieces in flight per warp, so the
+// gathered rows stream at L2 speed -- and the selections run in light
+// per-query kernels.  (A single fused per-query kernel doing all of it measured
+// 1.55 ms at C4 against 1.39 ms for these four: its block-level selection
+// phases left the row loads idle.)
 //   k_rows (chunks)  exact distances of the kept chunks' centroids -> vals [q][t]
 //   k_top_need       exact top-w1 + certificate (chunk mode) or the exact
 //                    top-w1 of the fallback (top mode); the needed ids (regions
@@ -764,15 +553,6 @@ __global__ void __launch_bounds__(FS_THREADS) k_second_sel(SearchArgs a, FusedAr
 
 }  // namespace dev
 
-size_t select_fused_smem(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
-    return dev::FusedLayout(k, n, w1, w2, dim, capc).total;
-}
-
-bool select_fused_supported(uint32_t k, uint32_t n, uint32_t w1, uint32_t w2, uint32_t dim, uint32_t capc) {
-    return dim % 4 == 0 && dim <= 256 && w1 <= 256 && w2 <= w1 * n && (uint64_t)w1 * (n + 1) <= 8192 &&
-           capc <= 1024 && select_fused_smem(k, n, w1, w2, dim, capc) <= 200 * 1024;
-}
-
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
                          float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st) {
     if (nq == 0) return;
@@ -783,18 +563,6 @@ void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32
                                                                       T);
     else
         throw std::runtime_error("chunk_select: K above 262144");
-    CUDA_LAUNCH_CHECK();
-}
-
-void launch_select_fused(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2, uint32_t cs,
-                         const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
-                         const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
-                         uint32_t* sel_out, float* ab_out, cudaStream_t st) {
-    if (nblocks == 0) return;
-    dev::FusedArgs f{Y, w1, w2, cs, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, sel_out, ab_out};
-    const size_t smem = select_fused_smem(a.k, a.n, w1, w2, a.dim, capc);
-    CUDA_CHECK(cudaFuncSetAttribute(dev::k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dev::k_select_fused<<<list_grid(nblocks, qlist != nullptr), dev::FS_THREADS, smem, st>>>(a, f);
     CUDA_LAUNCH_CHECK();
 }
 

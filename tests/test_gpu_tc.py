@@ -128,13 +128,13 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
     # persistent / per-row-block coarse grids, 1xTF32 first pass, scan variants
     variants = [dict(tc_persist=1), dict(tc_persist=0), dict(tc_pass1_single=1),
                 dict(tc_pass1_single=1, tc_persist=0), dict(tc_chunk_select=0), dict(tc_chunk_select=0, tc_persist=0),
-                dict(tc_select_split=0), dict(tc_select_split=0, tc_chunk_cap=4), dict(tc_chunk_cap=4),
+                dict(tc_chunk_cap=4),
                 dict(scan_packed=0), dict(scan_slots=104), dict(scan_slots=4), dict(scan_slots=8),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1, tc_persist=0),
                 dict(cert_slack_milli=10**6, scan_retry=0), dict(cert_slack_milli=10**6)]
     for v in variants:
-        knobs = dict(tc_persist=1, tc_pass1_single=0, tc_chunk_select=1, tc_select_split=1, tc_chunk_cap=256,
+        knobs = dict(tc_persist=1, tc_pass1_single=0, tc_chunk_select=1, tc_chunk_cap=256,
                      scan_slots=0, scan_packed=1,
                      tc_pass2_single=0, scan_retry=1, cert_slack_milli=0)
         knobs.update(v)
@@ -196,8 +196,7 @@ def test_chunk_select_coarse_stage_paths_match_oracle(vlqadc, oracle_mod, tmp_pa
     ref = {g: o.search(q, g[0], g[1], g[2])[:2] for g in grid}
     idx.set_profiling(True)
     for knobs in [dict(tc_chunk_select=1, tc_chunk_cap=256), dict(tc_chunk_select=1, tc_chunk_cap=4),
-                  dict(tc_select_split=0, tc_chunk_cap=256), dict(tc_select_split=0, tc_chunk_cap=4),
-                  dict(tc_select_split=1, tc_chunk_select=0)]:
+                  dict(tc_chunk_select=0)]:
         for key, val in knobs.items():
             idx.set_tuning(key, val)
         for g in grid:
@@ -209,7 +208,6 @@ def test_chunk_select_coarse_stage_paths_match_oracle(vlqadc, oracle_mod, tmp_pa
             assert st["tc_fallbacks"] > 0  # the fallback path really ran
     idx.set_tuning("tc_chunk_select", 1)
     idx.set_tuning("tc_chunk_cap", 256)
-    idx.set_tuning("tc_select_split", 1)
     # select-split: this engine selects, a second engine on the same model scans
     import torch
     dq = torch.from_numpy(q).cuda()
