@@ -325,24 +325,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 float* tr = sMerge + (warp - 2) * 32 * 33;  // STORE: this warp's transpose tile
                 float cmin = __int_as_float(0x7f800000);
                 float c8[4] = {cmin, cmin, cmin, cmin};  // MODE 4: minima of 8-column chunks
-                if constexpr (MODE == 4) {
-                    // the 32 columns' norms as 8 broadcast float4 loads, d in packed
-                    // pairs (FFMA2: each element rounds like the scalar fmaf)
-                    const float4* n4 = reinterpret_cast<const float4*>(nrm + col);
 #pragma unroll
-                    for (int g = 0; g < 8; g++) {
-                        const float4 nn = __ldg(n4 + g);
-                        const float2 d0 = __ffma2_rn(make_float2(-2.0f, -2.0f),
-                                                     make_float2(__uint_as_float(acc[4 * g]), __uint_as_float(acc[4 * g + 1])),
-                                                     make_float2(nn.x, nn.y));
-                        const float2 d1 = __ffma2_rn(make_float2(-2.0f, -2.0f),
-                                                     make_float2(__uint_as_float(acc[4 * g + 2]), __uint_as_float(acc[4 * g + 3])),
-                                                     make_float2(nn.z, nn.w));
-                        c8[g >> 1] = fminf(c8[g >> 1], fminf(fminf(d0.x, d0.y), fminf(d1.x, d1.y)));
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < (MODE == 4 ? 0 : 32); j++) {
+                for (int j = 0; j < 32; j++) {
                     const uint32_t cidx = t * TN + col + j;
                     const float nj = MODE == 0 ? __ldg(nrm + col + j) : __shfl_sync(0xffffffffu, nv, j);
                     const float d = fmaf(-2.0f, __uint_as_float(acc[j]), nj);
