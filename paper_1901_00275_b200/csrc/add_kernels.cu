@@ -397,7 +397,63 @@ __global__ void k_gather_scan_order(const uint32_t* __restrict__ order, uint64_t
     }
 }
 
+// Co-occurrence of code values inside the fast scan's warp blocks (32
+// consecutive entries of a list from its start, one per lane), sampled every
+// `stride`-th list: cooc[p][a][b] (a < b) counts the blocks in which sub-space
+// p's codes a and b both occur, cooc[p][a][a] the blocks holding a.  One warp
+// per block; distinct values by __match_any_sync.
+__global__ void k_code_cooc(const uint64_t* __restrict__ list_off, uint32_t ncell, uint32_t stride,
+                            const uint8_t* __restrict__ codes, uint32_t m, unsigned int* __restrict__ cooc) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t c = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * stride; c < ncell;
+         c += nw * stride) {
+        const uint64_t b0 = list_off[c], b1 = list_off[c + 1];
+        for (uint64_t e0 = b0; e0 < b1; e0 += 32) {
+            const uint64_t e = e0 + lane;
+            const bool on = e < b1;
+            const unsigned act = __ballot_sync(0xffffffffu, on);
+            for (uint32_t p = 0; p < m; p++) {
+                const uint32_t v = on ? codes[e * m + p] : 256u + lane;
+                const unsigned peers = __match_any_sync(0xffffffffu, v);
+                const bool lead = on && (__ffs(peers) - 1) == (int)lane;
+                const unsigned leaders = __ballot_sync(0xffffffffu, lead) & act;
+                unsigned int* cp = cooc + (uint64_t)p * 65536u;
+                if (lead) atomicAdd(cp + v * 256u + v, 1u);
+                for (unsigned rest = leaders; rest; rest &= rest - 1) {  // warp-uniform loop
+                    const int j = __ffs(rest) - 1;
+                    const uint32_t o = __shfl_sync(0xffffffffu, v, j);
+                    if (lead && j > (int)lane) atomicAdd(cp + min(v, o) * 256u + max(v, o), 1u);
+                }
+            }
+        }
+    }
+}
+
+// codes[e][p] <- perm[p][codes[e][p]] (the scan copy's code relabeling)
+__global__ void k_relabel_codes(uint8_t* __restrict__ codes, uint64_t n, uint32_t m, const uint8_t* __restrict__ perm) {
+    __shared__ uint8_t tab[16 * 256];
+    for (uint32_t i = threadIdx.x; i < m * 256u; i += blockDim.x) tab[i] = perm[i];
+    __syncthreads();
+    const uint64_t total = n * m;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)
+        codes[i] = tab[(uint32_t)(i % m) * 256u + codes[i]];
+}
+
 }  // namespace dev
+
+void launch_code_cooc(const uint64_t* list_off, uint32_t ncell, uint32_t stride, const uint8_t* codes, uint32_t m,
+                      unsigned int* cooc, cudaStream_t st) {
+    if (ncell == 0) return;
+    dev::k_code_cooc<<<4736, 256, 0, st>>>(list_off, ncell, stride, codes, m, cooc);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_relabel_codes(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* perm, cudaStream_t st) {
+    if (n == 0) return;
+    dev::k_relabel_codes<<<(unsigned)dev::umin64((n * m + 255) / 256, 4736 * 4), 256, 0, st>>>(codes, n, m, perm);
+    CUDA_LAUNCH_CHECK();
+}
 
 void launch_scan_order_keys(const uint64_t* list_off, uint32_t ncell, const uint8_t* codes, uint32_t m, uint64_t n,
                             uint64_t* keys, uint32_t* vals, cudaStream_t st) {

@@ -57,6 +57,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (const char* v = std::getenv("VLQ_SCAN_VARIANT")) cfg_.scan_variant = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_U")) cfg_.scan_slots = std::atoi(v);
     if (const char* v = std::getenv("VLQ_SCAN_REORDER")) cfg_.scan_reorder = cfg_.scan_reorder_build = std::atoi(v);
+    if (const char* v = std::getenv("VLQ_SCAN_RELABEL")) cfg_.scan_relabel = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC")) cfg_.use_tc = std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_MIN_K")) cfg_.tc_min_k = cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
     if (const char* v = std::getenv("VLQ_TC_SEARCH_MIN_K")) cfg_.tc_search_min_k = (uint32_t)std::atoi(v);
@@ -289,6 +290,8 @@ void Engine::pack_eterm_lam() {
         scodes_.reset();
         sids_.reset();
         seterm_lam_.reset();
+        code_perm_.reset();
+        code_inv_.reset();
         (void)cudaGetLastError();
         CUDA_CHECK(cudaStreamSynchronize(stream_));
     }
@@ -305,6 +308,8 @@ void Engine::build_scan_order() {
     scodes_.reset();
     sids_.reset();
     seterm_lam_.reset();
+    code_perm_.reset();
+    code_inv_.reset();
     const uint64_t ncell = (uint64_t)k_ * n_;
     if (!cfg_.scan_reorder_build || nent_ == 0 || !(m_ == 16 || m_ == 8 || m_ == 4) || ncell >= (1ull << 24) ||
         nent_ >= (1ull << 31))
@@ -331,6 +336,92 @@ void Engine::build_scan_order() {
     seterm_lam_.alloc(nent_);
     launch_gather_scan_order(vb.Current(), nent_, m_, codes_.p, ids_.p, eterm_lam_.p, scodes_.p, sids_.p,
                              seterm_lam_.p, stream_);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    if (cfg_.scan_relabel) choose_code_banks();
+}
+
+// One sub-space's 256 code values onto the 32 shared-memory banks, 8 values
+// per bank, so that values which occur together in a warp block rarely share
+// a bank.  W[a][b] = the blocks holding both a and b (sampled).  Greedy in
+// descending frequency (each value to the open bank with the least
+// co-occurrence weight), then pairwise swaps while one lowers the total.
+// Slot = bank + 32 * (rank inside the bank), so the LUT word of a relabeled
+// value v sits in bank v mod 32.
+static void choose_banks_1(const unsigned int* cooc, uint8_t* perm) {
+    constexpr int V = 256, B = 32, PER = V / B;
+    std::vector<double> W((size_t)V * V, 0.0), cost((size_t)V * B, 0.0);
+    std::vector<double> f(V);
+    for (int a = 0; a < V; a++) {
+        f[a] = cooc[a * V + a];
+        for (int b = a + 1; b < V; b++) W[(size_t)a * V + b] = W[(size_t)b * V + a] = cooc[a * V + b];
+    }
+    std::vector<int> order(V), bank(V, -1), size(B, 0);
+    for (int i = 0; i < V; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return f[x] > f[y]; });
+    for (int c : order) {
+        int best = -1;
+        for (int b = 0; b < B; b++)
+            if (size[b] < PER && (best < 0 || cost[(size_t)c * B + b] < cost[(size_t)c * B + best])) best = b;
+        bank[c] = best;
+        size[best]++;
+        for (int x = 0; x < V; x++) cost[(size_t)x * B + best] += W[(size_t)x * V + c];
+    }
+    for (int pass = 0; pass < 16; pass++) {
+        bool improved = false;
+        for (int a = 0; a < V; a++)
+            for (int b = a + 1; b < V; b++) {
+                const int ba = bank[a], bb = bank[b];
+                if (ba == bb) continue;
+                const double wab = W[(size_t)a * V + b];
+                const double d = (cost[(size_t)a * B + bb] - wab) - cost[(size_t)a * B + ba] +
+                                 (cost[(size_t)b * B + ba] - wab) - cost[(size_t)b * B + bb];
+                if (d < -1e-9) {
+                    for (int x = 0; x < V; x++) {
+                        cost[(size_t)x * B + ba] += W[(size_t)x * V + b] - W[(size_t)x * V + a];
+                        cost[(size_t)x * B + bb] += W[(size_t)x * V + a] - W[(size_t)x * V + b];
+                    }
+                    bank[a] = bb;
+                    bank[b] = ba;
+                    improved = true;
+                }
+            }
+        if (!improved) break;
+    }
+    int cnt[B] = {0};
+    for (int c = 0; c < V; c++) perm[c] = (uint8_t)(bank[c] + B * cnt[bank[c]]++);
+}
+
+// The fast scan's LUT lookups are random 8-bit indices: a warp's lookup costs
+// one shared-memory wavefront per distinct LUT word in its most-hit bank.
+// Relabeling the copy's code bytes per sub-space (the scan writes the LUT at
+// the relabeled positions, the re-score maps back through code_inv) spreads
+// the values that co-occur in a warp block over different banks; the order of
+// the copy, the LUT values and every sum are unchanged, so results are too.
+// Statistics from a sample of ~32M entries (every stride-th list).
+void Engine::choose_code_banks() {
+    if (!scodes_.p || m_ > 16 || nent_ == 0) return;
+    DeviceGuard g(cfg_.device);
+    const uint64_t ncell = (uint64_t)k_ * n_;
+    const uint32_t stride = (uint32_t)std::max<uint64_t>(1, nent_ >> 25);
+    DevBuf<unsigned int> cooc;
+    cooc.alloc((uint64_t)m_ * 65536);
+    CUDA_CHECK(cudaMemsetAsync(cooc.p, 0, (size_t)m_ * 65536 * 4, stream_));
+    launch_code_cooc(list_off_.p, (uint32_t)ncell, stride, scodes_.p, m_, cooc.p, stream_);
+    std::vector<unsigned int> h((size_t)m_ * 65536);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), cooc.p, h.size() * 4, cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    std::vector<uint8_t> perm((size_t)m_ * 256), inv((size_t)m_ * 256);
+    std::vector<std::thread> th;
+    for (uint32_t p = 0; p < m_; p++)
+        th.emplace_back([&, p] { choose_banks_1(h.data() + (size_t)p * 65536, perm.data() + (size_t)p * 256); });
+    for (auto& t : th) t.join();
+    for (uint32_t p = 0; p < m_; p++)
+        for (uint32_t c = 0; c < 256; c++) inv[p * 256 + perm[p * 256 + c]] = (uint8_t)c;
+    code_perm_.alloc(perm.size());
+    code_inv_.alloc(inv.size());
+    CUDA_CHECK(cudaMemcpyAsync(code_perm_.p, perm.data(), perm.size(), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaMemcpyAsync(code_inv_.p, inv.data(), inv.size(), cudaMemcpyHostToDevice, stream_));
+    launch_relabel_codes(scodes_.p, nent_, m_, code_perm_.p, stream_);
     CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
@@ -1031,6 +1122,8 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
                 a.eterm_lam = seterm_lam_.p;
                 a.scodes = scodes_.p;
                 a.sids = sids_.p;
+                a.code_perm = code_perm_.p;
+                a.code_inv = code_inv_.p;
             }
             a.e_pack_err = std::ldexp(emax_, -15) * 1.0001f;  // |e - e'| <= 2^-15 |e|
         }
@@ -1055,6 +1148,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             // the generic scan keys canonical positions: re-score from the canonical arrays
             a.scodes = nullptr;
             a.sids = nullptr;
+            a.code_perm = a.code_inv = nullptr;
             if (a.eterm_lam) a.eterm_lam = eterm_lam_.p;
             sa = a;
             launch_scan(a, nt, w2, keep, 2 * keep, 8, true, nullptr, nullptr, st);
@@ -1133,6 +1227,10 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     if (key == "scan_variant") cfg_.scan_variant = (int)value;
     else if (key == "scan_slots") cfg_.scan_slots = (int)value;
     else if (key == "scan_reorder") cfg_.scan_reorder = (int)value;
+    else if (key == "scan_relabel") {  // rebuilds the scan copy with / without the relabeling
+        cfg_.scan_relabel = (int)value;
+        if (scodes_.p) build_scan_order();
+    }
     else if (key == "scan_lpt") cfg_.scan_lpt = (int)value;
     else if (key == "scan_round_cap") cfg_.scan_round_cap = (uint32_t)value;
     else if (key == "cert_slack_milli") cfg_.cert_slack = (float)value * 1e-3f;

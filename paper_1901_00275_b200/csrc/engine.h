@@ -43,6 +43,8 @@ struct EngineConfig {
     uint32_t scan_cap = 0;       // study knob: fast-scan candidate buffer per CTA (0 = 2048 keys)
     int scan_reorder = 1;        // the fast scan reads the within-list reordered copy (build_scan_order)
     int scan_reorder_build = 1;  // build that copy at add / load (env VLQ_SCAN_REORDER=0 skips it)
+    int scan_relabel = 1;        // relabel the copy's code bytes so co-occurring values use distinct LUT banks
+                                 // (at add / load; env VLQ_SCAN_RELABEL=0 skips it)
     int scan_lpt = 1;            // fast scan + re-score visit a tile's queries longest first (by scanned count)
     uint32_t scan_round_cap = 0; // study knob: most chunks per warp between the fast scan's block barriers (0 = 32)
     int scan_retry = 1;          // certificate failures: fast scan again with 4x k' before the exact scan
@@ -263,6 +265,7 @@ private:
     void compute_eterm();
     void pack_eterm_lam();
     void build_scan_order();
+    void choose_code_banks();
     AddArgs add_args() const;
     SearchArgs search_args() const;
     enum Stage { STAGE_ALL = 0, STAGE_COARSE = 1, STAGE_FINE = 2, STAGE_SELECT = 3, STAGE_FINE_SEL = 4 };
@@ -348,6 +351,7 @@ private:
     DevBuf<uint32_t> eterm_lam_;  // packed e-term | lambda byte (v6 scan stream)
     DevBuf<uint8_t> scodes_;      // the fast scan's reordered copy: codes, ids, packed stream
     DevBuf<uint32_t> sids_, seterm_lam_;
+    DevBuf<uint8_t> code_perm_, code_inv_;  // [m][256] relabeling of scodes_ (choose_code_banks), empty: none
     DevBuf<unsigned int> err_;  // [0] error flag, [1] emax bits, [2] flagged count, [3..4] minmax
 
     // IVFADC baseline lists (region-major; ids ascending within a list)

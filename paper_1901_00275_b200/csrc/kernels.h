@@ -64,6 +64,11 @@ struct SearchArgs {
     // ids in it (null: the canonical id order)
     const uint8_t* scodes;
     const uint32_t* sids;
+    // scodes' byte values are relabeled per sub-space (engine.cu
+    // choose_code_banks): code_perm [m][256] maps a code to its scodes value
+    // (the scan stores LUT[p][perm[p][c]] = term5[p][c]), code_inv back
+    const uint8_t* code_perm;
+    const uint8_t* code_inv;
     uint32_t scan_cap;  // fast-scan candidate buffer (keys per CTA); 0 = default
     uint32_t round_cap = 0;  // fast scan: most chunks per warp between block barriers (0 = 32)
     bool sel_agg;       // fast-scan flush: warp-aggregated (match_any) histogram atomics
@@ -158,6 +163,9 @@ void launch_gather_entries(const uint32_t* order, uint64_t n, uint32_t m, uint64
                            uint32_t* ids, uint8_t* codes, uint8_t* lambdas, float* eterm, cudaStream_t st);
 // scan order of the posting entries (engine.cu): order[] = the canonical
 // positions sorted by (cell, leading code bytes)
+void launch_code_cooc(const uint64_t* list_off, uint32_t ncell, uint32_t stride, const uint8_t* codes, uint32_t m,
+                      unsigned int* cooc, cudaStream_t st);
+void launch_relabel_codes(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* perm, cudaStream_t st);
 void launch_scan_order_keys(const uint64_t* list_off, uint32_t ncell, const uint8_t* codes, uint32_t m, uint64_t n,
                             uint64_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_gather_scan_order(const uint32_t* order, uint64_t n, uint32_t m, const uint8_t* codes, const uint32_t* ids,

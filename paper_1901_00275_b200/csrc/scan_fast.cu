@@ -184,7 +184,7 @@ template <int M>
 __device__ __forceinline__ float lut_at(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], int p) {
     const uint32_t word = w[p >> 2];
     const int k = p & 3;
-    const uint32_t b = k == 0 ? (word & 0xffu) : (k == 3 ? (word >> 24) : __byte_perm(word, 0u, 0x4440u + k));
+    const uint32_t b = __byte_perm(word, 0u, 0x4440u + k);  // PRMT, then one IMAD (b * 4 + table base)
     return reinterpret_cast<const float*>(lut)[p * 256 + b];
 }
 
@@ -205,9 +205,11 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     const uint32_t _nb = a.qlist ? *a.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
     for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
     const uint64_t q = a.qlist ? a.qlist[_b] : _b;
-    unsigned char* lut = smem;
-    constexpr uint32_t LUT_B = 4 * 256 * M;
-    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + LUT_B);        // cap keys
+    // static shared memory: the table's address is a link-time constant, so a
+    // lookup's LDS takes [byte * 4 + imm] with no base register add
+    __shared__ __align__(16) float s_lut[256 * M];
+    unsigned char* lut = reinterpret_cast<unsigned char*>(s_lut);
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem);                 // cap keys
     uint32_t* cpref = reinterpret_cast<uint32_t*>(cbuf + cap);         // w2 + 1
     __shared__ uint32_t hist[256];
     __shared__ unsigned int s_misc[48];
@@ -215,8 +217,14 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     __shared__ unsigned long long s_tau;
 
     // 1. the query's term5 table (one copy per sub-space)
-    const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
-    for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    if (a.code_perm) {  // relabeled scan codes: LUT[p][perm[p][c]] = term5[p][c]
+        const float* t5s = a.t5 + q * M * VLQ_KSUB;
+        for (uint32_t i = threadIdx.x; i < 256u * M; i += blockDim.x)
+            reinterpret_cast<float*>(lut)[(i & ~255u) | __ldg(a.code_perm + i)] = __ldg(t5s + i);
+    } else {
+        const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
+        for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);
+    }
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
     {
@@ -440,7 +448,7 @@ template <int M>
 static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
     // block-shared candidate buffer (keys): 2048 unless the scan_cap knob says otherwise
     const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 2048u, 4 * keep);
-    const size_t smem = 4 * 256 * (size_t)M + (size_t)cap * 8 + ((size_t)w2 + 1) * 4;
+    const size_t smem = (size_t)cap * 8 + ((size_t)w2 + 1) * 4;  // + the static 4 * 256 * M B table
     // su: slots per lane (4 / 6 / 8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
     auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
               : su == 8 ? dev::k_scan_fast2<M, 8, 3>

@@ -456,6 +456,10 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
     uint64_t* cstart = keys + keep;                        // w2: list start of selected cell t
     uint32_t* ccell = reinterpret_cast<uint32_t*>(cstart + w2);
     __shared__ float s_fast_last;
+    __shared__ uint8_t s_inv[16 * VLQ_KSUB];  // code_inv (relabeled scan codes -> canonical codes)
+    if (a.code_inv)
+        for (uint32_t i = threadIdx.x; i < a.m * VLQ_KSUB; i += blockDim.x) s_inv[i] = a.code_inv[i];
+    __syncthreads();
 
     const uint32_t _nb = a.qlist ? *a.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
     for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
                 float v2[M], v3[M], v4[M], v5[M];
 #pragma unroll
                 for (int p = 0; p < M; p++) {  // every gather in flight at once
-                    const uint32_t c = code[p];
+                    const uint32_t c = a.code_inv ? s_inv[p * VLQ_KSUB + code[p]] : code[p];
                     v2[p] = __ldg(a.t2 + p * VLQ_KSUB + c);
                     v3[p] = __ldg(t3i + p * VLQ_KSUB + c);
                     v4[p] = __ldg(t3s + p * VLQ_KSUB + c);
@@ -519,7 +523,7 @@ __global__ void __launch_bounds__(256) k_rescore(SearchArgs a, uint32_t w2, uint
             } else {
                 const uint8_t* code = codes + pos * m;
                 for (uint32_t p = 0; p < m; p++) {
-                    const uint32_t c = code[p];
+                    const uint32_t c = a.code_inv ? s_inv[p * VLQ_KSUB + code[p]] : code[p];
                     s2 = __fadd_rn(s2, a.t2[p * VLQ_KSUB + c]);
                     s3 = __fadd_rn(s3, t3i[p * VLQ_KSUB + c]);
                     s4 = __fadd_rn(s4, t3s[p * VLQ_KSUB + c]);

@@ -85,12 +85,14 @@ def test_exhaustive_search_equals_full_scan(vlqadc, oracle_mod):
 
 
 @pytest.mark.parametrize("seed,knobs", [(0, {}), (1, {}), (2, {"scan_slots": 8}), (3, {"scan_variant": 1}),
-                                        (4, {"scan_slots": 104}), (5, {"cert_slack_milli": 10**6})])
+                                        (4, {"scan_slots": 104}), (5, {"cert_slack_milli": 10**6}),
+                                        (6, {"scan_relabel": 0}), (7, {"scan_reorder": 0})])
 def test_random_parameters_match_oracle(vlqadc, oracle_mod, seed, knobs):
     """Random (w1, alpha, k) vs the oracle: the fused fast scan (6 / 8 / 4
     slots per lane, 3 or 4 CTAs per SM), the generic warp-buffer scan, and a widened
     certificate that sends every query through the retry pass and the exact
-    scan -- results must not change."""
+    scan, the scan copy without its code relabeling and the canonical arrays
+    -- results must not change."""
     rng = np.random.default_rng(seed)
     for name in ALL_CASES:
         z, index_path, _ = load_golden(name)
