@@ -193,6 +193,8 @@ __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an ord
     return __uint_as_float((ub & 0x80000000u) ? (ub & 0x7fffffffu) : ~ub);
 }
 
+constexpr uint32_t SCAN_STAGE_MAX = 1024;  // selected cells per query whose parameters are staged in shared memory
+
 template <int M, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
@@ -227,6 +229,30 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     }
     // 2. chunk prefix over the selected cells (chunks never straddle cells)
     const uint32_t* selq = a.sel + q * w2;
+    const float* wsq = a.ws + q * a.k;
+    // per-cell parameters staged once per query (all threads, loads in
+    // parallel) instead of a dependent global-load chain whenever a warp
+    // enters a cell: list start, length, a = |y - c_i|^2, B = (b - a) - c, c
+    const bool staged = w2 <= SCAN_STAGE_MAX;
+    uint32_t* p_pos = cpref + w2 + 1;
+    uint32_t* p_len = p_pos + w2;
+    float* p_av = reinterpret_cast<float*>(p_len + w2);
+    float* p_bc = p_av + w2;
+    float* p_cv = p_bc + w2;
+    if (staged) {
+        for (uint32_t t = threadIdx.x; t < w2; t += blockDim.x) {
+            const uint32_t cell = selq[t];
+            const uint64_t b0 = a.list_off[cell];
+            const float av = wsq[cell / a.n];
+            const float bv = wsq[a.nbr[cell]];
+            const float cv = a.elen[cell];
+            p_pos[t] = (uint32_t)b0;
+            p_len[t] = (uint32_t)(a.list_off[cell + 1] - b0);
+            p_av[t] = av;
+            p_bc[t] = (bv - av) - cv;
+            p_cv[t] = cv;
+        }
+    }
     {
         const uint32_t per = (w2 + blockDim.x - 1) / blockDim.x;
         uint32_t local = 0;
@@ -263,7 +289,6 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
         }
         t = lo;
     }
-    const float* wsq = a.ws + q * a.k;
     const float2 delta2 = make_float2(a.lam_delta, a.lam_delta), lam02 = make_float2(a.lam0, a.lam0);
     const float2 m2 = make_float2(-2.0f, -2.0f);
     uint32_t L = 0, pos0 = 0;
@@ -277,7 +302,19 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
 
     auto locate = [&](uint32_t g) {  // walks t forward to the cell holding chunk g
         while (cpref[t + 1] <= g) t++;
-        if (t != loaded_t) {
+        if (t != loaded_t && staged) {
+            loaded_t = t;
+            L = p_len[t];
+            pos0 = p_pos[t];
+            const float av = p_av[t], bc = p_bc[t], cv = p_cv[t];
+            av2 = make_float2(av, av);
+            Bc2 = make_float2(bc, bc);
+            cv2 = make_float2(cv, cv);
+            codes_c = (a.scodes ? a.scodes : a.codes) + (uint64_t)pos0 * M;
+            lam_c = a.lambdas + pos0;
+            e_c = a.eterm + pos0;
+            if (packed) el_c = a.eterm_lam + pos0;
+        } else if (t != loaded_t) {
             loaded_t = t;
             const uint32_t cell = selq[t];
             const uint64_t b0 = a.list_off[cell];
@@ -448,7 +485,8 @@ template <int M>
 static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep, int su, cudaStream_t st) {
     // block-shared candidate buffer (keys): 2048 unless the scan_cap knob says otherwise
     const uint32_t cap = std::max<uint32_t>(a.scan_cap ? a.scan_cap : 2048u, 4 * keep);
-    const size_t smem = (size_t)cap * 8 + ((size_t)w2 + 1) * 4;  // + the static 4 * 256 * M B table
+    // + the static 4 * 256 * M B table; + 20 B per selected cell of staged parameters
+    const size_t smem = (size_t)cap * 8 + ((size_t)w2 + 1) * 4 + (w2 <= dev::SCAN_STAGE_MAX ? (size_t)w2 * 20 : 0);
     // su: slots per lane (4 / 6 / 8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
     auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
               : su == 8 ? dev::k_scan_fast2<M, 8, 3>
