@@ -1,3 +1,7 @@
+# Offline model of the fast scan's LUT bank conflicts under a per-sub-space code
+# relabeling (co-occurrence partition, as engine.cu choose_code_banks): train on a
+# fraction of the dumped lists (scripts/code_dump.py), evaluate on the rest.
+# usage: python scripts/bank_perm_sim.py 0.85
 import numpy as np, sys
 z = np.load('gpurun_out/codes_c4.npz')
 counts, codes = z['counts'].astype(np.int64), z['codes']
