@@ -722,9 +722,12 @@ def run_group(args, rank, world):
         raise SystemExit(f"bench: --gpus {N} but {torch.cuda.device_count()} visible GPUs")
     udev = sorted(set(devices))
     # S-way list sharding x N/S replicas (each replica searches 1/(N/S) of the
-    # batch): pure sharding up to 2 GPUs, 2 replicas of an N/2-way sharding
-    # from 4 (the per-GPU work that does not shrink with the shard halves)
-    S = int(os.environ.get("VLQ_GROUP_SHARDS", str(N if N <= 2 else N // 2)))
+    # batch): 2-way list sharding, N/2 replicas of it.  Measured member by
+    # member at C4 (profiles/r2_shard_probe_c4_final2.jsonl),
+    # N = 8: S = 2 x R = 4 projects 6.6x, S = 4 x R = 2 6.0x, S = 8 5.3x --
+    # the per-GPU work that does not shrink with the shard (selection, term5,
+    # re-score, the scan's per-query prologue) is done for fewer queries
+    S = int(os.environ.get("VLQ_GROUP_SHARDS", str(min(N, 2))))
     from paper_1901_00275_b200 import vlqadc
     w = WORKLOADS[args.workload]
     cfg = config_of(args, w, N)

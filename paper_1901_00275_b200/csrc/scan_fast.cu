@@ -220,9 +220,17 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
 
     // 1. the query's term5 table (one copy per sub-space)
     if (a.code_perm) {  // relabeled scan codes: LUT[p][perm[p][c]] = term5[p][c]
-        const float* t5s = a.t5 + q * M * VLQ_KSUB;
-        for (uint32_t i = threadIdx.x; i < 256u * M; i += blockDim.x)
-            reinterpret_cast<float*>(lut)[(i & ~255u) | __ldg(a.code_perm + i)] = __ldg(t5s + i);
+        const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
+        const uint32_t* pq4 = reinterpret_cast<const uint32_t*>(a.code_perm);
+        float* lf = reinterpret_cast<float*>(lut);
+        for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) {  // 4 values + their 4 slots per load
+            const float4 v = __ldg(t5q + i);
+            const uint32_t pw = __ldg(pq4 + i), b = (i * 4) & ~255u;
+            lf[b | (pw & 0xffu)] = v.x;
+            lf[b | ((pw >> 8) & 0xffu)] = v.y;
+            lf[b | ((pw >> 16) & 0xffu)] = v.z;
+            lf[b | (pw >> 24)] = v.w;
+        }
     } else {
         const float4* t5q = reinterpret_cast<const float4*>(a.t5 + q * M * VLQ_KSUB);
         for (uint32_t i = threadIdx.x; i < 64u * M; i += blockDim.x) reinterpret_cast<float4*>(lut)[i] = __ldg(t5q + i);

@@ -24,7 +24,7 @@ def same_f32(a, b):
     return np.array_equal(np.asarray(a, np.float32).view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
 
 
-@pytest.mark.parametrize("G,S", [(1, 0), (2, 0), (3, 0), (5, 0), (4, 2), (6, 3), (4, 1)])
+@pytest.mark.parametrize("G,S", [(1, 0), (2, 0), (3, 0), (5, 0), (4, 2), (6, 3), (4, 1), (8, 2)])
 @pytest.mark.parametrize("name", ["accept_small", "m16", "unclamped"])
 def test_group_search_matches_reference_golden(vlqadc, name, G, S):
     """G members as G / S replicas of an S-way list sharding (S = 0: G)."""
