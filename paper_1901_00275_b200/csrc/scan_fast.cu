@@ -397,14 +397,19 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
                     dist[u + 1] = d.y;
                 }
             }
+            bool near = false;  // any of the lane's entries at or below the threshold distance
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t idx = o + u * 32 + lane;
-                if (idx < L && dist[u] <= taud) {  // rare after the first rounds: exact key test
-                    uint32_t ub = __float_as_uint(dist[u]);
-                    ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
-                    const uint64_t key = ((uint64_t)ub << 32) | (pos0 + idx);
-                    if (key < tau) tk |= 1u << u;
+            for (int u = 0; u < U; u++) near |= (o + u * 32 + lane < L) & (dist[u] <= taud);
+            if (__any_sync(0xffffffffu, near)) {  // rare after the first rounds: exact key test
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t idx = o + u * 32 + lane;
+                    if (idx < L && dist[u] <= taud) {
+                        uint32_t ub = __float_as_uint(dist[u]);
+                        ub ^= (uint32_t)((int32_t)ub >> 31) | 0x80000000u;  // order-preserving
+                        const uint64_t key = ((uint64_t)ub << 32) | (pos0 + idx);
+                        if (key < tau) tk |= 1u << u;
+                    }
                 }
             }
             const uint32_t any = __ballot_sync(0xffffffffu, tk != 0);
