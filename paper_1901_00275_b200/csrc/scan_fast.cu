@@ -357,11 +357,21 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
             // issues its U x 2-3 loads back to back)
             if (packed) {  // one 4-byte word: e-term (low 8 mantissa bits dropped) | lambda byte
                 uint32_t le[U];
+                if (o + CH <= L) {  // warp-uniform: a whole chunk, one base address + immediate offsets
+                    const uint8_t* cb = codes_c + (size_t)(o + lane) * M;
+                    const uint32_t* eb = el_c + o + lane;
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const uint32_t ic = min(o + u * 32 + lane, L - 1);  // clamped: the tail re-reads entry L-1
-                    load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
-                    le[u] = __ldg(el_c + ic);
+                    for (int u = 0; u < U; u++) {
+                        load_code_vec<M>(cb + u * 32 * M, cw[u]);
+                        le[u] = __ldg(eb + u * 32);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const uint32_t ic = min(o + u * 32 + lane, L - 1);  // clamped: the tail re-reads entry L-1
+                        load_code_vec<M>(codes_c + (size_t)ic * M, cw[u]);
+                        le[u] = __ldg(el_c + ic);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
