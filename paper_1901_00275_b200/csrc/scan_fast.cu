@@ -178,8 +178,9 @@ __global__ void k_pack_eterm_lam(const float* __restrict__ eterm, const uint8_t*
         out[e] = (__float_as_uint(eterm[e]) & ~0xffu) | (uint32_t)lambdas[e];
 }
 
-// LUT[p][code_p]: the byte is extracted with one LOP3 / PRMT / SHF and the
-// shared load scales it (LDS [R.X4 + imm]), so a lookup is 2 instructions
+// LUT[p][code_p]: one PRMT extracts the byte, one IMAD forms byte * 4 + table
+// base, the LDS carries p * 1 KB as its immediate -- 3 instructions per lookup
+// (bytes 0 and 3 written as AND / shift compiled to 4)
 template <int M>
 __device__ __forceinline__ float lut_at(const unsigned char* lut, const uint32_t (&w)[(M + 3) / 4], int p) {
     const uint32_t word = w[p >> 2];
@@ -207,8 +208,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t
     const uint32_t _nb = a.qlist ? *a.qcount : gridDim.x;  // list launches: a small grid strides over the device-side count
     for (uint32_t _b = blockIdx.x; _b < _nb; _b += gridDim.x) {
     const uint64_t q = a.qlist ? a.qlist[_b] : _b;
-    // static shared memory: the table's address is a link-time constant, so a
-    // lookup's LDS takes [byte * 4 + imm] with no base register add
+    // the query's table (16 KB at m = 16) in static shared memory
     __shared__ __align__(16) float s_lut[256 * M];
     unsigned char* lut = reinterpret_cast<unsigned char*>(s_lut);
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem);                 // cap keys
