@@ -171,6 +171,13 @@ uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n);
  * (vlq_config.shard_rank / shard_count): ((cell * 0x9E3779B97F4A7C15) mod 2^64
  * >> 40) mod shards.  Host-only, no device needed. */
 uint32_t vlq_shard_of_cell(uint32_t cell, uint32_t shards);
+/* The fast scan's bank-aware code relabeling (built at add / load; no reference
+ * counterpart, results do not depend on it): from m sub-spaces' 256 x 256
+ * co-occurrence counts of code values in 32-entry warp blocks (upper triangle,
+ * diagonal = occurrences), perm[p * 256 + c] = the value code c of sub-space p
+ * takes in the scan copy; values v with equal v mod 32 share a shared-memory
+ * bank, 8 per bank.  Host-only, no device needed. */
+int vlq_code_banks(const uint32_t* cooc, uint32_t m, uint8_t* perm);
 
 /* Streamed Index.add of the engine's counter-based synthetic generator
  * (the reference's Gaussian-mixture law, dataset.cpp:13-44): rows are

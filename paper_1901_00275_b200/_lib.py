@@ -62,6 +62,7 @@ _SIGS = {
                                                   c_vp]),
     "vlq_w2": (c_u32, [c_u32, c_f32, c_u32]),
     "vlq_shard_of_cell": (c_u32, [c_u32, c_u32]),
+    "vlq_code_banks": (c_i32, [c_vp, c_u32, c_vp]),
     "vlq_engine_sync": (c_i32, [c_vp, c_vp]),
     "vlq_engine_info": (c_i32, [c_vp, ctypes.POINTER(VlqInfo)]),
     "vlq_engine_add_synthetic": (c_i32, [c_vp, c_u64, c_u32, c_f32, c_u64]),

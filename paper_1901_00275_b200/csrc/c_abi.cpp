@@ -459,6 +459,13 @@ uint32_t vlq_w2(uint32_t w1, float alpha, uint32_t n) { return vlq::w2_of(w1, al
 
 uint32_t vlq_shard_of_cell(uint32_t cell, uint32_t shards) { return shards ? vlq::shard_of_cell(cell, shards) : 0u; }
 
+int vlq_code_banks(const uint32_t* cooc, uint32_t m, uint8_t* perm) {
+    if (!cooc || !perm) return fail(VLQ_ERR_INVALID, "code_banks: NULL argument");
+    return guarded([&] {
+        for (uint32_t p = 0; p < m; p++) vlq::choose_code_banks_1(cooc + (size_t)p * 65536, perm + (size_t)p * 256);
+    });
+}
+
 
 // ---- multi-GPU group --------------------------------------------------------
 

@@ -347,7 +347,7 @@ void Engine::build_scan_order() {
 // co-occurrence weight), then pairwise swaps while one lowers the total.
 // Slot = bank + 32 * (rank inside the bank), so the LUT word of a relabeled
 // value v sits in bank v mod 32.
-static void choose_banks_1(const unsigned int* cooc, uint8_t* perm) {
+void choose_code_banks_1(const unsigned int* cooc, uint8_t* perm) {
     constexpr int V = 256, B = 32, PER = V / B;
     std::vector<double> W((size_t)V * V, 0.0), cost((size_t)V * B, 0.0);
     std::vector<double> f(V);
@@ -413,7 +413,7 @@ void Engine::choose_code_banks() {
     std::vector<uint8_t> perm((size_t)m_ * 256), inv((size_t)m_ * 256);
     std::vector<std::thread> th;
     for (uint32_t p = 0; p < m_; p++)
-        th.emplace_back([&, p] { choose_banks_1(h.data() + (size_t)p * 65536, perm.data() + (size_t)p * 256); });
+        th.emplace_back([&, p] { choose_code_banks_1(h.data() + (size_t)p * 65536, perm.data() + (size_t)p * 256); });
     for (auto& t : th) t.join();
     for (uint32_t p = 0; p < m_; p++)
         for (uint32_t c = 0; c < 256; c++) inv[p * 256 + perm[p * 256 + c]] = (uint8_t)c;

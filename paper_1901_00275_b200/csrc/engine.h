@@ -26,6 +26,11 @@ __host__ __device__ inline uint32_t shard_of_cell(uint32_t cell, uint32_t shards
     return (uint32_t)((((uint64_t)cell * 0x9E3779B97F4A7C15ull) >> 40) % shards);
 }
 
+// One sub-space's bank-aware code relabeling (engine.cu): cooc = 256 x 256
+// co-occurrence counts (upper triangle + diagonal), perm[c] = c's new value;
+// value v's LUT word sits in bank v mod 32, 8 values per bank.
+void choose_code_banks_1(const unsigned int* cooc, uint8_t* perm);
+
 struct EngineConfig {
     int device = 0;
     int shard_rank = 0;    // this engine holds the posting lists c with shard_of_cell(c) == shard_rank

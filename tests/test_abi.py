@@ -92,3 +92,33 @@ def test_vecs_roundtrip(tmp_path):
         vlqadc.write_vecs(b + 0.5, str(tmp_path / "c.bvecs"))
     with pytest.raises(RuntimeError, match="cannot open"):
         vlqadc.read_vecs(str(tmp_path / "missing.fvecs"))
+
+
+def test_code_bank_relabeling_is_a_balanced_permutation():
+    """Host logic of the fast scan's code relabeling (engine.cu
+    choose_code_banks): every sub-space's map is a permutation of 0..255 with
+    8 values per bank (v mod 32), and values that always occur together --
+    planted here as 32 groups of 8 -- are spread over 8 different banks."""
+    from paper_1901_00275_b200 import _lib
+    lib = _lib.lib()
+    m = 3
+    rng = np.random.default_rng(0)
+    cooc = np.zeros((m, 256, 256), np.uint32)
+    groups = [rng.permutation(256).reshape(32, 8) for _ in range(m)]
+    for p in range(m):
+        noise = rng.integers(0, 3, (256, 256)).astype(np.uint32)
+        cooc[p] = np.triu(noise, 1)
+        for g in groups[p]:
+            for i in range(8):
+                for j in range(i + 1, 8):
+                    a, b = sorted((int(g[i]), int(g[j])))
+                    cooc[p, a, b] += 1000
+        cooc[p][np.arange(256), np.arange(256)] = 500
+    perm = np.zeros((m, 256), np.uint8)
+    assert lib.vlq_code_banks(cooc.ctypes.data, m, perm.ctypes.data) == 0
+    for p in range(m):
+        assert sorted(perm[p].tolist()) == list(range(256))
+        assert np.array_equal(np.bincount(perm[p] % 32, minlength=32), np.full(32, 8))
+        for g in groups[p]:
+            assert len(set((perm[p][g] % 32).tolist())) == 8, (p, g)
+    assert lib.vlq_code_banks(None, 1, perm.ctypes.data) != 0
