@@ -665,7 +665,10 @@ void launch_rescore(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t keep
     auto fn = a.m == 16 ? dev::k_rescore<16> : a.m == 8 ? dev::k_rescore<8> : a.m == 4 ? dev::k_rescore<4>
                                                                                           : dev::k_rescore<0>;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), 256, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
+    // one thread per survivor: 128-thread CTAs for k' <= 128 (twice the CTAs
+    // resident, every thread gathering), 256 above
+    const unsigned threads = keep <= 128 ? 128u : 256u;
+    fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), threads, smem, st>>>(a, w2, keep, topk, out_ids, out_d);
     CUDA_LAUNCH_CHECK();
 }
 
