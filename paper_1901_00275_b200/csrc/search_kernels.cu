@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(256) k_apply_selection(SearchArgs a, uint32_t 
 // term5 table (query_term5): t5[q][p][j] = dot(y_p, PQ[p][j]) in order; also
 // S5max = sum_p max_j |t5| for the certificate.
 // ---------------------------------------------------------------------------
+template <int DS>  // sub-space width when known at compile time (unrolled dot products), else 0
 __global__ void __launch_bounds__(256) k_term5(float cert_slack, const float* __restrict__ Y, const float* __restrict__ pqT,
                                                uint32_t dim, uint32_t m, float* __restrict__ t5,
                                                QueryMeta* __restrict__ meta) {
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(256) k_term5(float cert_slack, const float* __
     extern __shared__ float ys[];
     __shared__ float s_max[8 * 16];
     const uint64_t q = blockIdx.x;
-    const uint32_t dsub = dim / m, j = threadIdx.x, lane = j & 31u, warp = j >> 5;
+    const uint32_t dsub = DS > 0 ? (uint32_t)DS : dim / m, j = threadIdx.x, lane = j & 31u, warp = j >> 5;
     for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) ys[d] = Y[q * dim + d];
     __syncthreads();
     float s5 = 0.0f;  // thread 0's running S5max
@@ -265,7 +266,15 @@ __global__ void __launch_bounds__(256) k_term5(float cert_slack, const float* __
                 const float* c = pqT + (uint64_t)p * dsub * VLQ_KSUB + j;
                 const float* y = ys + p * dsub;
                 float acc = 0.0f;
-                for (uint32_t t = 0; t < dsub; t++) acc = dot_step(acc, y[t], c[(uint64_t)t * VLQ_KSUB]);
+                if constexpr (DS > 0) {
+                    float cv[DS];
+#pragma unroll
+                    for (int t = 0; t < DS; t++) cv[t] = __ldg(c + t * VLQ_KSUB);
+#pragma unroll
+                    for (int t = 0; t < DS; t++) acc = dot_step(acc, y[t], cv[t]);
+                } else {
+                    for (uint32_t t = 0; t < dsub; t++) acc = dot_step(acc, y[t], c[(uint64_t)t * VLQ_KSUB]);
+                }
                 t5[(q * m + p) * VLQ_KSUB + j] = acc;
                 mx[pp] = fabsf(acc);
             }
@@ -622,7 +631,10 @@ void launch_apply_selection_parts(const SearchArgs& a, uint64_t nq, uint32_t w2,
 
 void launch_term5(float cert_slack, const float* Y, const float* pqT, uint32_t dim, uint32_t m, float* t5, QueryMeta* meta,
                   uint64_t nq, cudaStream_t st) {
-    dev::k_term5<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(cert_slack, Y, pqT, dim, m, t5, meta);
+    const uint32_t ds = dim / m;
+    auto fn = ds == 4 ? dev::k_term5<4> : ds == 6 ? dev::k_term5<6> : ds == 8 ? dev::k_term5<8>
+              : ds == 16 ? dev::k_term5<16> : dev::k_term5<0>;
+    fn<<<(unsigned)nq, 256, dim * sizeof(float), st>>>(cert_slack, Y, pqT, dim, m, t5, meta);
     CUDA_LAUNCH_CHECK();
 }
 
