@@ -1449,6 +1449,23 @@ static bool par_memcpy(void* dst, const void* src, size_t bytes, Pinned pinned, 
     return ok;
 }
 
+// Touch every page of a (typically freshly allocated) host output buffer so
+// its page faults -- the kernel zeroing ~3000 pages for 12 MB of results --
+// happen while the GPU is still searching, not inside the final copy.
+void par_prefault(void* dst, size_t bytes) {
+    if (!dst || bytes == 0) return;
+    const size_t kMin = 1u << 20;
+    CopyPool& pool = CopyPool::get();
+    const unsigned nt = (unsigned)std::max<size_t>(1, std::min<size_t>(pool.workers() + 1, bytes / kMin));
+    const size_t per = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
+    auto touch = [&](unsigned t) {
+        volatile char* d = static_cast<volatile char*>(dst);
+        for (size_t o = t * per; o < std::min(bytes, (size_t)(t + 1) * per); o += 4096) d[o] = 0;
+    };
+    if (nt <= 1) touch(0);
+    else pool.run(nt, touch);
+}
+
 void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, uint32_t topk, int64_t* ids,
                          float* dists, uint64_t* scanned) {
     if (!model_ok_) throw std::runtime_error("search: no model loaded");
@@ -1490,6 +1507,11 @@ void Engine::search_host(const float* q, uint64_t nq, uint32_t w1, float alpha, 
     if (timing) CUDA_CHECK(cudaEventRecord(tev[1], st));
     search_device(sq_.p, nq, w1, alpha, topk, si_.p, sd_.p, ss_.p, st);
     if (timing) CUDA_CHECK(cudaEventRecord(tev[2], st));
+    if (topk) {  // overlapped with the search
+        par_prefault(ids, ib);
+        par_prefault(dists, db);
+    }
+    if (scanned) par_prefault(scanned, sb);
     // the previous call's output lines must be out of the CPU caches before
     // this call's D2H lands on them (flushed in the background meanwhile)
     if (flusher_.joinable()) flusher_.join();

@@ -31,6 +31,10 @@ __host__ __device__ inline uint32_t shard_of_cell(uint32_t cell, uint32_t shards
 // value v's LUT word sits in bank v mod 32, 8 values per bank.
 void choose_code_banks_1(const unsigned int* cooc, uint8_t* perm);
 
+// Touch every 4 KB page of a host output buffer (parallel), so its first-touch
+// page faults can overlap with device work (engine.cu).
+void par_prefault(void* dst, size_t bytes);
+
 struct EngineConfig {
     int device = 0;
     int shard_rank = 0;    // this engine holds the posting lists c with shard_of_cell(c) == shard_rank

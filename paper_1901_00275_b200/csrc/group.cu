@@ -369,6 +369,9 @@ void Group::search_host(const float* q, uint64_t nq, uint32_t dim, uint32_t w1, 
     upload_queries(q, nq, dim, /*validate=*/true);
     reserve(nq, w2_of(w1, alpha, eng_[0]->n()), k);
     enqueue_search(nq, w1, alpha, k);
+    par_prefault(ids, nq * k * 8);  // the output pages fault in while the GPUs search
+    par_prefault(dists, nq * k * 4);
+    if (scanned) par_prefault(scanned, nq * 8);
     check_errors();
     last_k_ = k;
     results(ids, dists, scanned);
