@@ -28,6 +28,7 @@ searching the same index (exported as VLQ1) on a bounded query sample.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -709,7 +710,8 @@ def run_group(args, rank, world):
     import torch.distributed as dist
     N = args.gpus
     if world > 1:
-        dist.init_process_group("gloo")
+        # the other ranks wait out rank 0's whole run (1B-point adds included)
+        dist.init_process_group("gloo", timeout=datetime.timedelta(hours=3))
         if rank != 0:
             dist.barrier()  # rank 0 has finished
             dist.destroy_process_group()
