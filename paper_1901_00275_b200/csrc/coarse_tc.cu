@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // operands, <= 2^-11 relative each, instead of truncating them, <= 2^-10)
 __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, uint32_t dim, uint32_t ntiles,
                                      float* __restrict__ out, float* __restrict__ out_lo, float* __restrict__ norm_out,
-                                     int rna) {
+                                     int rna, const float* __restrict__ mu) {
     const uint32_t nchunk = dim / 4;
     const uint64_t total = (uint64_t)ntiles * TC_N * nchunk;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
@@ -434,6 +434,10 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
         const uint32_t tile = (uint32_t)(row / TC_N), r = (uint32_t)(row % TC_N);
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (row < k) v = reinterpret_cast<const float4*>(C + row * dim)[c];
+        if (mu && row < k) {  // centered copy: fl(x - mu) per component
+            const float4 m = reinterpret_cast<const float4*>(mu)[c];
+            v = make_float4(v.x - m.x, v.y - m.y, v.z - m.z, v.w - m.w);
+        }
         const uint64_t off = (uint64_t)tile * TC_N * dim + (r >> 3) * (nchunk * 32) + c * 32 + (r & 7) * 4;
         *reinterpret_cast<float4*>(out + off) =
             rna ? make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w)) : v;
@@ -447,7 +451,10 @@ __global__ void k_relayout_centroids(const float* __restrict__ C, uint32_t k, ui
          row += (uint64_t)gridDim.x * blockDim.x) {
         float acc = 0.0f;
         if (row < k)
-            for (uint32_t d = 0; d < dim; d++) acc = dot_step(acc, C[row * dim + d], C[row * dim + d]);
+            for (uint32_t d = 0; d < dim; d++) {
+                const float x = mu ? C[row * dim + d] - mu[d] : C[row * dim + d];
+                acc = dot_step(acc, x, x);
+            }
         if (norm_out) norm_out[row] = row < k ? acc : __int_as_float(0x7f800000);
     }
 }
@@ -509,9 +516,9 @@ bool coarse_tc_supported(uint32_t dim) { return coarse_tc_fits(dim, false); }
 bool coarse_tc_split_supported(uint32_t dim) { return coarse_tc_fits(dim, true); }
 
 void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
-                               cudaStream_t st, int rna) {
+                               cudaStream_t st, int rna, const float* mu) {
     const uint32_t ntiles = (k + dev::TC_N - 1) / dev::TC_N;
-    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, out_lo, norm_out, rna);
+    dev::k_relayout_centroids<<<1184, 256, 0, st>>>(C, k, dim, ntiles, out, out_lo, norm_out, rna, mu);
     CUDA_LAUNCH_CHECK();
 }
 

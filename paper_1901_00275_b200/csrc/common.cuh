@@ -103,15 +103,19 @@ __device__ __forceinline__ uint64_t make_key(float f, uint32_t idx) {
 // <= 3 * 2^-21 from the dropped lo.lo term and truncated lo parts; the fp32
 // norm and the sequential sqdist each add D u |.|; x 1.5 safety factor.
 // rna: both operands were rounded to TF32 beforehand (cvt.rna, <= 2^-11 each).
+// centered: both operands were shifted by a common mu in fp32 (y' = fl(y - mu),
+// c' = fl(c - mu); xnorm2 = |y'|^2, cmax = max |c'|): | |y' - c'|^2 - |y - c|^2 |
+// <= 2 u s |y - c| + u^2 s^2 <= 3 u s^2 more.
 __device__ __forceinline__ float tc_eps(float xnorm2, float cmax, uint32_t dim, bool split = false,
-                                        bool rna = false) {
+                                        bool rna = false, bool centered = false) {
     // 1xTF32: each operand keeps 10 mantissa bits (<= 2^-10 relative per factor, truncated;
     // <= 2^-11 rounded); 3xTF32: the dropped lo.lo term and the truncated lo parts leave <= 3 * 2^-21
     const float xn = sqrtf(xnorm2);
     const float s = xn + cmax;
     const float u = 5.9604645e-08f;
     const float rel = split ? 1.430511474609375e-06f : (rna ? 9.765625e-4f : 1.953125e-3f);
-    return 1.5f * (2.0f * (rel + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + 2.0f * u * s * s) + 1e-30f;
+    const float cu = centered ? 5.0f : 2.0f;
+    return 1.5f * (2.0f * (rel + dim * u) * xn * cmax + dim * u * (s * s + cmax * cmax) + cu * u * s * s) + 1e-30f;
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }

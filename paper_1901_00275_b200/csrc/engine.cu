@@ -221,6 +221,30 @@ void Engine::upload_model() {
             mx = std::max(mx, s);
         }
         cmax_ = (float)(std::sqrt(mx) * (1.0 + 1e-6)) + 1e-30f;
+        // centered copy for the chunk-select pass: mu = the centroid mean,
+        // c' = fl(c - mu) (the kernels subtract in fp32 the same way)
+        std::vector<double> acc(dim_, 0.0);
+        for (uint32_t i = 0; i < k_; i++)
+            for (uint32_t d = 0; d < dim_; d++) acc[d] += model_.centroids[(size_t)i * dim_ + d];
+        std::vector<float> mu(dim_);
+        for (uint32_t d = 0; d < dim_; d++) mu[d] = (float)(acc[d] / k_);
+        double mxc = 0.0;
+        for (uint32_t i = 0; i < k_; i++) {
+            double s = 0.0;
+            for (uint32_t d = 0; d < dim_; d++) {
+                const float c = model_.centroids[(size_t)i * dim_ + d] - mu[d];
+                s += (double)c * c;
+            }
+            mxc = std::max(mxc, s);
+        }
+        cmaxc_ = (float)(std::sqrt(mxc) * (1.0 + 1e-6)) + 1e-30f;
+        mu_.alloc(dim_);
+        CUDA_CHECK(cudaMemcpyAsync(mu_.p, mu.data(), (size_t)dim_ * 4, cudaMemcpyHostToDevice, stream_));
+        cent_tcc_.alloc((size_t)ntiles * 128 * dim_);
+        cnorm_tcc_.alloc((size_t)ntiles * 128);
+        launch_relayout_centroids(centroids_.p, k_, dim_, cent_tcc_.p, nullptr, cnorm_tcc_.p, stream_, /*rna=*/1,
+                                  mu_.p);
+        CUDA_CHECK(cudaStreamSynchronize(stream_));  // mu (host) is freed at scope exit
     }
     CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
@@ -975,18 +999,22 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         select_split_supported(k_, n_, w1, w2, dim_, cfg_.tc_chunk_cap) && tmin8_.p) {
         const uint32_t nchunk8 = ((k_ + 127) / 128) * 16;
         const float* x1 = nullptr;
+        // centered operands (queries relaid out here, so the persistent form only)
+        const bool cen = cfg_.tc_center && cfg_.tc_persist && cent_tcc_.p;
+        const float* mu = cen ? mu_.p : nullptr;
+        const float cmx = cen ? cmaxc_ : cmax_;
         if (cfg_.tc_persist) {
             const uint64_t rows = ((nt + 127) / 128) * 128;
             if (!xtc1_.p || xtc1_.n < rows * dim_) xtc1_.alloc(rows * dim_);
-            launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st, /*rna=*/1);
+            launch_relayout_centroids(d_q, (uint32_t)nt, dim_, xtc1_.p, nullptr, nullptr, st, /*rna=*/1, mu);
             x1 = xtc1_.p;
             launches += 1;
         }
-        launch_coarse_tc(4, d_q, nt, dim_, cent_tc_.p, nullptr, cnorm_tc_.p, k_, tmin8_.p, nchunk8, nullptr, nullptr,
-                         st, nullptr, nullptr, 0, x1, nullptr);
+        launch_coarse_tc(4, d_q, nt, dim_, cen ? cent_tcc_.p : cent_tc_.p, nullptr, cen ? cnorm_tcc_.p : cnorm_tc_.p,
+                         k_, tmin8_.p, nchunk8, nullptr, nullptr, st, nullptr, nullptr, 0, x1, nullptr);
         mark(PH_FIRST);  // the coarse phase is the tensor-core GEMM alone (its roofline in bench.py)
-        launch_chunk_select(tmin8_.p, nt, nchunk8, w1, d_q, dim_, cmax_, cfg_.tc_chunk_cap, clist_.p, ccnt_.p,
-                            tch_.p, st);
+        launch_chunk_select(tmin8_.p, nt, nchunk8, w1, d_q, dim_, cmx, cfg_.tc_chunk_cap, clist_.p, ccnt_.p,
+                            tch_.p, st, mu);
         SearchArgs a = search_args();
         CUDA_CHECK(cudaMemsetAsync(err_.p + 6, 0, 4, st));
         // row kernels at full occupancy + light per-query selections (select_fused.cu)
@@ -997,8 +1025,8 @@ bool Engine::coarse_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2
         snneed_.alloc(nt);
         launch_rows(centroids_.p, d_q, k_, dim_, 1, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, cfg_.tc_chunk_cap,
                     svals_.p, nk, nt, st);
-        launch_top_need(a, nt, d_q, w1, w2, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmax_, nullptr, nullptr,
-                        qlist_.p, err_.p + 6, svals_.p, snid_.p, snneed_.p, ldn, st);
+        launch_top_need(a, nt, d_q, w1, w2, clist_.p, ccnt_.p, cfg_.tc_chunk_cap, tch_.p, cmx, nullptr, nullptr,
+                        qlist_.p, err_.p + 6, svals_.p, snid_.p, snneed_.p, ldn, st, mu);
         // certificate failures / chunk-list overflows: exact full rows, exact
         // top-w1, then the needed ids from that top-w1
         launch_exact_rows(d_q, nt, dim_, centroids_.p, k_, ws_.p, qlist_.p, err_.p + 6, st);
@@ -1241,6 +1269,7 @@ void Engine::set_tuning(const std::string& key, int64_t value) {
     else if (key == "tc_pass2_single") cfg_.tc_pass2_single = (int)value;
     else if (key == "tc_chunk_select") cfg_.tc_chunk_select = (int)value;
     else if (key == "tc_chunk_cap") cfg_.tc_chunk_cap = (uint32_t)value;
+    else if (key == "tc_center") cfg_.tc_center = (int)value;
     else if (key == "scan_packed") cfg_.scan_packed = (int)value;
     else if (key == "scan_keep_min") cfg_.scan_keep_min = (uint32_t)value;
     else if (key == "scan_cap") cfg_.scan_cap = (uint32_t)value;

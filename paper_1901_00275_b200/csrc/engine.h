@@ -70,6 +70,8 @@ struct EngineConfig {
     int tc_chunk_select = 1;  // chunk-select coarse stage (one 1xTF32 pass of 8-centroid chunk minima, exact
                               // evaluation of the selected chunks, fused first + second level; select_fused.cu)
     uint32_t tc_chunk_cap = 256;  // selected chunks per query before the exact full-row fallback (study knob)
+    int tc_center = 1;  // chunk-select pass on centered operands (queries and centroids minus the centroid mean):
+                        // a smaller TF32 bound, fewer chunks evaluated exactly
 };
 
 // Trained quantizers (a VLQ1 "model": an index with zero points).
@@ -352,6 +354,8 @@ private:
     DevBuf<float> cent_hi_, cent_lo_;   // 3xTF32 split halves (search coarse stage)
     bool tc_ = false, tc_split_ = false;
     float cmax_ = 0.0f;  // max centroid norm (certificate bound)
+    DevBuf<float> mu_, cent_tcc_, cnorm_tcc_;  // centroid mean; centered TF32 copy + norms (chunk-select pass)
+    float cmaxc_ = 0.0f;                       // max centered centroid norm
     DevBuf<uint32_t> nbr_;
     DevBuf<uint64_t> list_off_;
     DevBuf<uint8_t> codes_, lambdas_;

@@ -196,7 +196,8 @@ namespace vlq {
 bool coarse_tc_supported(uint32_t dim);
 // chunk-select coarse stage (select_fused.cu)
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
-                         float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st);
+                         float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st,
+                         const float* mu = nullptr);
 // split form of the fused kernel (select_fused.cu): row kernels + light
 // per-query selection kernels; ldn = select_need_capacity(n, w1)
 uint32_t select_need_capacity(uint32_t n, uint32_t w1);
@@ -208,13 +209,14 @@ void launch_rows(const float* C, const float* Y, uint32_t k, uint32_t dim, int c
 void launch_top_need(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2,
                      const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
                      const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
-                     const float* vals, uint32_t* nid, uint32_t* nneed, uint32_t ldn, cudaStream_t st);
+                     const float* vals, uint32_t* nid, uint32_t* nneed, uint32_t ldn, cudaStream_t st,
+                     const float* mu = nullptr);
 void launch_second_sel(const SearchArgs& a, uint64_t nq, uint32_t w1, uint32_t w2, const uint32_t* nid,
                        const float* nval, const uint32_t* nneed, uint32_t ldn, uint32_t* sel_out, float* ab_out,
                        cudaStream_t st);
 bool coarse_tc_split_supported(uint32_t dim);
 void launch_relayout_centroids(const float* C, uint32_t k, uint32_t dim, float* out, float* out_lo, float* norm_out,
-                               cudaStream_t st, int rna = 0);
+                               cudaStream_t st, int rna = 0, const float* mu = nullptr);
 void launch_relayout_khalf(const float* C, uint32_t k, uint32_t dim, float* out_hi, float* out_lo, cudaStream_t st);
 void launch_coarse_tc(int mode, const float* X, uint64_t nx, uint32_t dim, const float* cent_tc, const float* cent_lo,
                       const float* cnorm, uint32_t k, float* out_row, uint64_t ldo, uint32_t* top_idx, float* top_d,

@@ -58,7 +58,8 @@ template <int VPT, int NT>
 __global__ void __launch_bounds__(NT) k_chunk_select(const float* __restrict__ tmin, uint32_t nchunk, uint32_t L,
                                                      const float* __restrict__ Y, uint32_t dim, float cmax,
                                                      uint32_t capc, uint32_t* __restrict__ clist,
-                                                     uint32_t* __restrict__ ccnt, float* __restrict__ Tout) {
+                                                     uint32_t* __restrict__ ccnt, float* __restrict__ Tout,
+                                                     const float* __restrict__ mu) {
     constexpr uint32_t NB = 2048, NWARP = NT / 32;
     __shared__ uint32_t hist[NB];
     __shared__ uint32_t scan[40];
@@ -130,9 +131,12 @@ __global__ void __launch_bounds__(NT) k_chunk_select(const float* __restrict__ t
     if (lane == 0) atomicMax(&s_tau, tmax);
     __syncthreads();
     if (tid == 0) {
-        float yn = 0.0f;
-        for (uint32_t d = 0; d < dim; d++) yn = fmaf(Y[q * dim + d], Y[q * dim + d], yn);
-        s_T = unord_float(s_tau) + 2.02f * tc_eps(yn, cmax, dim, false, /*rna=*/true);
+        float yn = 0.0f;  // |y'|^2 of the (centered) tensor-core operand
+        for (uint32_t d = 0; d < dim; d++) {
+            const float y = mu ? Y[q * dim + d] - mu[d] : Y[q * dim + d];
+            yn = fmaf(y, y, yn);
+        }
+        s_T = unord_float(s_tau) + 2.02f * tc_eps(yn, cmax, dim, false, /*rna=*/true, mu != nullptr);
     }
     __syncthreads();
     const float T = s_T;
@@ -283,6 +287,7 @@ struct FusedArgs {
     unsigned int* nflag;
     uint32_t* sel_out;        // optional select-split hand-off: cells [nq, w2]
     float* ab_out;            //                                 (a, b) [nq, w2, 2]
+    const float* mu = nullptr;  // centered tensor-core operands (chunk mode): the common shift
 };
 
 __host__ __device__ inline uint32_t fs_nwords(uint32_t k) { return (k + 31) / 32; }
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs
             const float* vq = na.vals + q * FS_MAX_KEYS;
             for (uint32_t t = tid; t < ncent; t += nt) vals[t] = vq[t];
             float* ysm = reinterpret_cast<float*>(hist);  // the query vector, briefly (hist is free here)
-            for (uint32_t d = tid; d < dim; d += nt) ysm[d] = f.Y[q * dim + d];
+            for (uint32_t d = tid; d < dim; d += nt) ysm[d] = f.mu ? f.Y[q * dim + d] - f.mu[d] : f.Y[q * dim + d];
             __syncthreads();
             if (tid == 0) {
                 float yn = 0.0f;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs
             if ((tid & 31) == 0) atomicMax(&s_w1max, __float_as_uint(mx));  // distances >= 0
             __syncthreads();
             const float exact_w1 = __uint_as_float(s_w1max);
-            const float eps = tc_eps(s_yn, f.cmax, dim, false, /*rna=*/true);
+            const float eps = tc_eps(s_yn, f.cmax, dim, false, /*rna=*/true, f.mu != nullptr);
             const double lower = (double)f.T[q] + (double)s_yn - (double)eps;
             if (!(lower > (double)exact_w1)) {
                 if (tid == 0) f.flagged[atomicAdd(f.nflag, 1u)] = (uint32_t)q;
@@ -554,13 +559,15 @@ __global__ void __launch_bounds__(FS_THREADS) k_second_sel(SearchArgs a, FusedAr
 }  // namespace dev
 
 void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32_t L, const float* Y, uint32_t dim,
-                         float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st) {
+                         float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st,
+                         const float* mu) {
     if (nq == 0) return;
     if (nchunk <= 16 * 512)
-        dev::k_chunk_select<16, 512><<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T);
+        dev::k_chunk_select<16, 512><<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T,
+                                                                    mu);
     else if (nchunk <= 32 * 1024)
         dev::k_chunk_select<32, 1024><<<(unsigned)nq, 1024, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt,
-                                                                      T);
+                                                                      T, mu);
     else
         throw std::runtime_error("chunk_select: K above 262144");
     CUDA_LAUNCH_CHECK();
@@ -602,9 +609,11 @@ void launch_rows(const float* C, const float* Y, uint32_t k, uint32_t dim, int c
 void launch_top_need(const SearchArgs& a, uint64_t nblocks, const float* Y, uint32_t w1, uint32_t w2,
                      const uint32_t* clist, const uint32_t* ccnt, uint32_t capc, const float* T, float cmax,
                      const uint32_t* qlist, const unsigned int* qcount, uint32_t* flagged, unsigned int* nflag,
-                     const float* vals, uint32_t* nid, uint32_t* nneed, uint32_t ldn, cudaStream_t st) {
+                     const float* vals, uint32_t* nid, uint32_t* nneed, uint32_t ldn, cudaStream_t st,
+                     const float* mu) {
     if (nblocks == 0) return;
-    dev::FusedArgs f{Y, w1, w2, dev::FS_CS, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, nullptr, nullptr};
+    dev::FusedArgs f{Y, w1, w2, dev::FS_CS, clist, ccnt, capc, T, cmax, qlist, qcount, flagged, nflag, nullptr, nullptr,
+                     mu};
     dev::NeedArgs na{vals, nid, nneed, ldn};
     const size_t smem = top_need_smem(a.k, w1);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_top_need, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -128,13 +128,13 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
     # persistent / per-row-block coarse grids, 1xTF32 first pass, scan variants
     variants = [dict(tc_persist=1), dict(tc_persist=0), dict(tc_pass1_single=1),
                 dict(tc_pass1_single=1, tc_persist=0), dict(tc_chunk_select=0), dict(tc_chunk_select=0, tc_persist=0),
-                dict(tc_chunk_cap=4),
+                dict(tc_chunk_cap=4), dict(tc_center=0),
                 dict(scan_packed=0), dict(scan_slots=104), dict(scan_slots=4), dict(scan_slots=8),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1, tc_persist=0),
                 dict(cert_slack_milli=10**6, scan_retry=0), dict(cert_slack_milli=10**6)]
     for v in variants:
-        knobs = dict(tc_persist=1, tc_pass1_single=0, tc_chunk_select=1, tc_chunk_cap=256,
+        knobs = dict(tc_persist=1, tc_pass1_single=0, tc_chunk_select=1, tc_chunk_cap=256, tc_center=1,
                      scan_slots=0, scan_packed=1,
                      tc_pass2_single=0, scan_retry=1, cert_slack_milli=0)
         knobs.update(v)
@@ -196,7 +196,8 @@ def test_chunk_select_coarse_stage_paths_match_oracle(vlqadc, oracle_mod, tmp_pa
     ref = {g: o.search(q, g[0], g[1], g[2])[:2] for g in grid}
     idx.set_profiling(True)
     for knobs in [dict(tc_chunk_select=1, tc_chunk_cap=256), dict(tc_chunk_select=1, tc_chunk_cap=4),
-                  dict(tc_chunk_select=0)]:
+                  dict(tc_chunk_select=1, tc_chunk_cap=256, tc_center=0), dict(tc_persist=0),
+                  dict(tc_persist=1, tc_center=1, tc_chunk_select=0)]:
         for key, val in knobs.items():
             idx.set_tuning(key, val)
         for g in grid:
@@ -226,3 +227,31 @@ def test_chunk_select_coarse_stage_paths_match_oracle(vlqadc, oracle_mod, tmp_pa
     torch.cuda.synchronize()
     oids, od = ref[(w1, alpha, k)]
     assert np.array_equal(ids.cpu().numpy(), oids) and same_f32(dd.cpu().numpy(), od)
+
+
+@pytest.mark.parametrize("dim", [96, 128])
+def test_chunk_select_centered_operands_on_offset_data(vlqadc, oracle_mod, tmp_path, dim):
+    """Data far from the origin (every coordinate + 40): the TF32 bound of the
+    uncentered chunk pass grows with |y| |c| until every query overflows its
+    chunk list and takes the exact full-row fallback; on centered operands
+    (queries and centroids minus the centroid mean) the bound is that of the
+    data's spread, no query falls back, and both stay bit-exact with the
+    oracle."""
+    base = vlqadc.gen_synthetic(40000, dim, clusters=3000, spread=0.05, seed=55) + np.float32(40.0)
+    q = vlqadc.gen_synthetic(96, dim, clusters=3000, spread=0.05, seed=56) + np.float32(40.0)
+    idx = vlqadc.Index.train(base, k=16384, n=32, m=8, iters=2, seed=8)
+    idx.add(base)
+    path = str(tmp_path / f"off{dim}.vlq")
+    idx.save(path)
+    o = oracle_mod.OracleIndex.load(path)
+    idx.set_profiling(True)
+    fallbacks = {}
+    for center in (1, 0):
+        idx.set_tuning("tc_center", center)
+        idx.stats(reset=True)
+        for w1, alpha, k in [(64, 0.25, 100), (16, 0.5, 10)]:
+            ids_, d_ = idx.search(q, w1=w1, alpha=alpha, k=k)
+            oids, od, _ = o.search(q, w1, alpha, k)
+            assert np.array_equal(ids_, oids) and same_f32(d_, od), (dim, center, w1)
+        fallbacks[center] = idx.stats(reset=True)["tc_fallbacks"]
+    assert fallbacks[1] == 0 and fallbacks[0] > 0, fallbacks
