@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(NT) k_chunk_select(const float* __restrict__ t
     __shared__ uint32_t hist[NB];
     __shared__ uint32_t scan[40];
     __shared__ uint32_t segc[VPT * NWARP];
-    __shared__ float s_T;
+    __shared__ float s_T, s_yn;
     __shared__ unsigned int s_mn, s_mx, s_bin, s_tau;
     const uint64_t q = blockIdx.x;
     const float* row = tmin + q * nchunk;
@@ -75,6 +75,16 @@ __global__ void __launch_bounds__(NT) k_chunk_select(const float* __restrict__ t
     for (int j = 0; j < VPT; j++) {
         const uint32_t i = j * NT + tid;
         v[j] = i < nchunk ? row[i] : INF;
+    }
+    if (warp == 0) {  // |y'|^2 of the (centered) tensor-core operand, lane-parallel (any fp32 order: the
+                      // bound's D u s^2 term covers its rounding), read by thread 0 after the barriers below
+        float part = 0.0f;
+        for (uint32_t d = lane; d < dim; d += 32) {
+            const float y = mu ? Y[q * dim + d] - mu[d] : Y[q * dim + d];
+            part = fmaf(y, y, part);
+        }
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) s_yn = part;
     }
     for (uint32_t b = tid; b < NB; b += NT) hist[b] = 0;
     // row min / max over the finite values (padded centroids give +inf)
@@ -131,12 +141,7 @@ __global__ void __launch_bounds__(NT) k_chunk_select(const float* __restrict__ t
     if (lane == 0) atomicMax(&s_tau, tmax);
     __syncthreads();
     if (tid == 0) {
-        float yn = 0.0f;  // |y'|^2 of the (centered) tensor-core operand
-        for (uint32_t d = 0; d < dim; d++) {
-            const float y = mu ? Y[q * dim + d] - mu[d] : Y[q * dim + d];
-            yn = fmaf(y, y, yn);
-        }
-        s_T = unord_float(s_tau) + 2.02f * tc_eps(yn, cmax, dim, false, /*rna=*/true, mu != nullptr);
+        s_T = unord_float(s_tau) + 2.02f * tc_eps(s_yn, cmax, dim, false, /*rna=*/true, mu != nullptr);
     }
     __syncthreads();
     const float T = s_T;
@@ -377,14 +382,17 @@ __global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs
             }
             const float* vq = na.vals + q * FS_MAX_KEYS;
             for (uint32_t t = tid; t < ncent; t += nt) vals[t] = vq[t];
-            float* ysm = reinterpret_cast<float*>(hist);  // the query vector, briefly (hist is free here)
-            for (uint32_t d = tid; d < dim; d += nt) ysm[d] = f.mu ? f.Y[q * dim + d] - f.mu[d] : f.Y[q * dim + d];
-            __syncthreads();
-            if (tid == 0) {
-                float yn = 0.0f;
-                for (uint32_t d = 0; d < dim; d++) yn = fmaf(ysm[d], ysm[d], yn);
-                s_yn = yn;
-                s_w1max = 0u;
+            if (tid < 32) {  // |y'|^2, lane-parallel (any fp32 order: covered by the bound's D u s^2 term)
+                float part = 0.0f;
+                for (uint32_t d = tid; d < dim; d += 32) {
+                    const float y = f.mu ? f.Y[q * dim + d] - f.mu[d] : f.Y[q * dim + d];
+                    part = fmaf(y, y, part);
+                }
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                if (tid == 0) {
+                    s_yn = part;
+                    s_w1max = 0u;
+                }
             }
             __syncthreads();
             // exact top-w1 by (dist, id): the chunk list is ascending, so position order == id order
