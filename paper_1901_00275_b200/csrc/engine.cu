@@ -1159,7 +1159,7 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
         a.round_cap = cfg_.scan_round_cap;
         a.sel_agg = cfg_.scan_sel_agg != 0;
         a.flush_exact = cfg_.scan_flush_exact != 0;
-        const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 6);
+        const int slots = cfg_.scan_slots ? cfg_.scan_slots : (cfg_.shard_count >= 4 ? 104 : 306);
         // fast_kind: the fused fast scan ran (the only kernel with the retry indirection)
         const bool fast_kind = cfg_.scan_variant == 0 && (m_ == 16 || m_ == 8 || m_ == 4) && w2 <= 4096 &&
                                keep <= 512;
@@ -1200,7 +1200,8 @@ bool Engine::fine_tile(const float* d_q, uint64_t nt, uint32_t w1, uint32_t w2, 
             r.cand = cand2_.p;
             r.qlist = qlist_.p;
             r.qcount = err_.p + 2;
-            launch_scan_fast(r, nt, w2, keep2, slots, st);
+            // few queries: the 8-warp CTAs finish each one sooner
+            launch_scan_fast(r, nt, w2, keep2, slots == 306 ? 6 : slots, st);
             launch_rescore(r, nt, w2, keep2, topk, d_ids, d_dists, st);
             CUDA_CHECK(cudaMemsetAsync(cnt2_.p, 0, 4, st));
             launch_compact_flags(meta_.p, nt, qlist2_.p, cnt2_.p, st);

@@ -43,8 +43,9 @@ struct EngineConfig {
     uint32_t max_tile = 16384;
     int force_exact = 0;   // 1: skip the fast scan, run the exact scan for every query
     int scan_variant = 0;  // 0 default (fused fast scan + exact re-score), 1 generic warp-buffer scan
-    int scan_slots = 0;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8; +100 = 4 CTAs/SM);
-                           // 0 = auto: 6 (3 CTAs/SM), or 104 on shards of >= 4 (1/4 or less of the
+    int scan_slots = 0;    // entry-slots per lane per chunk of the fast scan (4 / 6 / 8; +100 = 4 CTAs/SM;
+                           // 306 = 6 slots in 6-warp CTAs, 4 per SM);
+                           // 0 = auto: 306, or 104 on shards of >= 4 (1/4 or less of the
                            // entries per query: measured 3% faster at 8 shards, neutral unsharded)
     float cert_slack = 0.0f;  // test knob (cert_slack_milli): widens the re-score certificate -> retry / exact paths
     int scan_sel_agg = 0;        // study knob: warp-aggregated histogram atomics in the flush select

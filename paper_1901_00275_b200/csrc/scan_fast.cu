@@ -196,8 +196,8 @@ __device__ __forceinline__ float key_dist(uint64_t key) {  // distance of an ord
 
 constexpr uint32_t SCAN_STAGE_MAX = 1024;  // selected cells per query whose parameters are staged in shared memory
 
-template <int M, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
+template <int M, int U, int MINB, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) k_scan_fast2(SearchArgs a, uint32_t w2, uint32_t keep, uint32_t cap) {
     static_assert(U % 2 == 0, "entries are processed in pairs");
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = (M + 3) / 4;
@@ -511,13 +511,19 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
     // + the static 4 * 256 * M B table; + 20 B per selected cell of staged parameters
     const size_t smem = (size_t)cap * 8 + ((size_t)w2 + 1) * 4 + (w2 <= dev::SCAN_STAGE_MAX ? (size_t)w2 * 20 : 0);
     // su: slots per lane (4 / 6 / 8); su + 100: the same with 4 CTAs/SM register budget (64 regs)
+    // 306: 6 slots, 6 warps per CTA, 4 CTAs (queries) per SM at 80 registers -- the
+    // same 24 warps per SM as 8 x 3, spread over 4 queries instead of 3
+    // (measured: 16.40 vs 16.51 ms at C4, -2.6 to -5.3% at C1-C3; 5 x 5 and
+    // 4 x 6 were slower, profiles/r2_study_occ_c4.jsonl)
     auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
               : su == 8 ? dev::k_scan_fast2<M, 8, 3>
               : su == 104 ? dev::k_scan_fast2<M, 4, 4>
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
+              : su == 306 ? dev::k_scan_fast2<M, 6, 4, 192>
                           : dev::k_scan_fast2<M, 6, 3>;
+    const int threads = su == 306 ? 192 : 256;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), 256, smem, st>>>(a, w2, keep, cap);
+    fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), threads, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -130,6 +130,7 @@ def test_tc_two_pass_coarse_filter_deep_dims(vlqadc, oracle_mod, tmp_path, dim):
                 dict(tc_pass1_single=1, tc_persist=0), dict(tc_chunk_select=0), dict(tc_chunk_select=0, tc_persist=0),
                 dict(tc_chunk_cap=4), dict(tc_center=0),
                 dict(scan_packed=0), dict(scan_slots=104), dict(scan_slots=4), dict(scan_slots=8),
+                dict(scan_slots=6), dict(scan_slots=306),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1),
                 dict(tc_chunk_select=0, tc_pass1_single=1, tc_pass2_single=1, tc_persist=0),
                 dict(cert_slack_milli=10**6, scan_retry=0), dict(cert_slack_milli=10**6)]
