@@ -1,7 +1,7 @@
 // Fused PQ-ADC list scan, fast path (K4 of DESIGN.md; search.cpp:92-120,
 // 154-162 + select_topk :122-140).
 //
-// One CTA (8 warps, 3 CTAs per SM) per query.  The query's selected cells are
+// One CTA (6 warps, 4 CTAs per SM; 8 x 3 for the retry) per query.  The query's selected cells are
 // cut into chunks of 32 U entries (chunks never straddle cells); a block
 // prefix over the chunk counts gives every warp a balanced contiguous chunk
 // range.  Per entry (lane-parallel, every load warp-coalesced: 16 B code and
