@@ -30,7 +30,6 @@
 // exact refine + k_exact_needed writing ~2k exact distances into a K-wide ws
 // row per query): one tensor-core pass instead of two (the 3xTF32 pass issued
 // 3x the MMAs), and the needed exact distances live in shared memory only.
-#include <cstdlib>
 #include <stdexcept>
 
 #include "async.cuh"
@@ -571,13 +570,10 @@ void launch_chunk_select(const float* tmin, uint64_t nq, uint32_t nchunk, uint32
                          float cmax, uint32_t capc, uint32_t* clist, uint32_t* ccnt, float* T, cudaStream_t st,
                          const float* mu) {
     if (nq == 0) return;
-    const char* shp = std::getenv("VLQ_CS_SHAPE");
-    const int shape = shp ? std::atoi(shp) : 0;
-    if (shape == 1 && nchunk <= 32 * 256)
+    // K <= 65536: 32 values per thread in 256-thread CTAs (C3: 1.441 -> 1.424 ms of
+    // first level vs 16 x 512; 8 x 1024 1.466 ms, profiles/r2_study_cs_shape_c3.jsonl)
+    if (nchunk <= 32 * 256)
         dev::k_chunk_select<32, 256><<<(unsigned)nq, 256, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T,
-                                                                    mu);
-    else if (shape == 3 && nchunk <= 8 * 1024)
-        dev::k_chunk_select<8, 1024><<<(unsigned)nq, 1024, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T,
                                                                     mu);
     else if (nchunk <= 16 * 512)
         dev::k_chunk_select<16, 512><<<(unsigned)nq, 512, 0, st>>>(tmin, nchunk, L, Y, dim, cmax, capc, clist, ccnt, T,
