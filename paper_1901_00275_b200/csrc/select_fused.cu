@@ -39,7 +39,8 @@
 namespace vlq {
 namespace dev {
 
-constexpr uint32_t FS_THREADS = 256;
+constexpr uint32_t FS_THREADS = 256;  // k_second_sel
+constexpr uint32_t TN_THREADS = 128;  // k_top_need
 constexpr uint32_t FS_MAX_KEYS = 2048; // exactly evaluated chunk centroids per query
 constexpr uint32_t FS_CS = 8;          // centroids per chunk (TILEMIN8)
 
@@ -312,7 +313,10 @@ __host__ __device__ inline uint32_t fs_nwords(uint32_t k) { return (k + 31) / 32
 //                    scanned count, |term1| bound
 // ---------------------------------------------------------------------------
 constexpr uint32_t RW_WARPS = 4;   // warps per query CTA of the row kernels
-constexpr uint32_t RW_PW = 16, RW_NB = 4;
+// NB = 3 pieces in flight per warp (30 KB per CTA, 7 CTAs per SM): C3 first
+// level 1.402 -> 1.376 ms against NB = 4 (5 CTAs per SM); 4 x 2, 8 x 2 equal,
+// 2 x 4 and 2 x 2 slower (profiles/r2_study_rows_shape_c3.jsonl)
+constexpr uint32_t RW_PW = 16, RW_NB = 3;
 
 struct RowsArgs {
     const float* C;
@@ -327,12 +331,13 @@ struct RowsArgs {
     uint32_t ldo;
 };
 
-__global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowsArgs r) {
+template <int WARPS, int NB>
+__global__ void __launch_bounds__(WARPS * 32) k_rows(RowsArgs r) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint64_t q = blockIdx.x;
     const uint32_t dim = r.dim, dimp = (dim + RW_PW - 1) / RW_PW * RW_PW;
     float* ys = reinterpret_cast<float*>(smem);
-    float* wbuf = ys + dimp + (threadIdx.x >> 5) * RW_NB * 32 * (RW_PW + 4);
+    float* wbuf = ys + dimp + (threadIdx.x >> 5) * NB * 32 * (RW_PW + 4);
     for (uint32_t d = threadIdx.x; d < dimp; d += blockDim.x) ys[d] = d < dim ? r.Y[q * dim + d] : 0.0f;
     uint32_t cnt = r.cnt[q];
     if (r.chunks) cnt = (cnt > r.capc || cnt * FS_CS > FS_MAX_KEYS) ? 0u : cnt * FS_CS;  // overflow: k_top_need flags it
@@ -340,13 +345,13 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowsArgs r) {
     const uint32_t* lq = r.list + q * r.ld;
     float* oq = r.out + q * r.ldo;
     if (r.chunks)
-        exact_rows_pipe_t<RW_PW, RW_NB>(
-            r.C, r.k, dim, ys, wbuf, cnt, threadIdx.x >> 5, RW_WARPS,
+        exact_rows_pipe_t<RW_PW, NB>(
+            r.C, r.k, dim, ys, wbuf, cnt, threadIdx.x >> 5, WARPS,
             [&](uint32_t t) { return __ldg(lq + t / FS_CS) * FS_CS + (t & (FS_CS - 1)); },
             [&](uint32_t t, float v) { oq[t] = v; });
     else
-        exact_rows_pipe_t<RW_PW, RW_NB>(
-            r.C, r.k, dim, ys, wbuf, cnt, threadIdx.x >> 5, RW_WARPS, [&](uint32_t t) { return __ldg(lq + t); },
+        exact_rows_pipe_t<RW_PW, NB>(
+            r.C, r.k, dim, ys, wbuf, cnt, threadIdx.x >> 5, WARPS, [&](uint32_t t) { return __ldg(lq + t); },
             [&](uint32_t t, float v) { oq[t] = v; });
 }
 
@@ -357,7 +362,7 @@ struct NeedArgs {
     uint32_t ldn;
 };
 
-__global__ void __launch_bounds__(FS_THREADS) k_top_need(SearchArgs a, FusedArgs f, NeedArgs na) {
+__global__ void __launch_bounds__(TN_THREADS) k_top_need(SearchArgs a, FusedArgs f, NeedArgs na) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ float s_yn;
     __shared__ unsigned int s_w1max;
@@ -613,9 +618,10 @@ void launch_rows(const float* C, const float* Y, uint32_t k, uint32_t dim, int c
                  cudaStream_t st) {
     if (nq == 0) return;
     dev::RowsArgs r{C, Y, k, dim, chunks, list, cnt, ld, capc, out, ldo};
+    auto fn = dev::k_rows<dev::RW_WARPS, dev::RW_NB>;
     const size_t smem = rows_smem(dim);
-    CUDA_CHECK(cudaFuncSetAttribute(dev::k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dev::k_rows<<<(unsigned)nq, dev::RW_WARPS * 32, smem, st>>>(r);
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)nq, dev::RW_WARPS * 32, smem, st>>>(r);
     CUDA_LAUNCH_CHECK();
 }
 
@@ -630,7 +636,10 @@ void launch_top_need(const SearchArgs& a, uint64_t nblocks, const float* Y, uint
     dev::NeedArgs na{vals, nid, nneed, ldn};
     const size_t smem = top_need_smem(a.k, w1);
     CUDA_CHECK(cudaFuncSetAttribute(dev::k_top_need, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dev::k_top_need<<<list_grid(nblocks, qlist != nullptr), dev::FS_THREADS, smem, st>>>(a, f, na);
+    // 128 threads: 64 registers per thread cap 256-thread CTAs at 4 queries per
+    // SM; 8 x 4 warps run twice as many queries (C3 first level 1.424 -> 1.402
+    // ms; k_second_sel at 128 was slower, profiles/r2_study_fs_threads_c3.jsonl)
+    dev::k_top_need<<<list_grid(nblocks, qlist != nullptr), dev::TN_THREADS, smem, st>>>(a, f, na);
     CUDA_LAUNCH_CHECK();
 }
 
