@@ -520,8 +520,9 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
               : su == 104 ? dev::k_scan_fast2<M, 4, 4>
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
               : su == 306 ? dev::k_scan_fast2<M, 6, 4, 192>
+              : su == 356 ? dev::k_scan_fast2<M, 6, 5, 192>
                           : dev::k_scan_fast2<M, 6, 3>;
-    const int threads = su == 306 ? 192 : 256;
+    const int threads = (su == 306 || su == 356) ? 192 : 256;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), threads, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
