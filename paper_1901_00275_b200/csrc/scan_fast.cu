@@ -514,15 +514,15 @@ static void launch_fast2(const SearchArgs& a, uint64_t nq, uint32_t w2, uint32_t
     // 306: 6 slots, 6 warps per CTA, 4 CTAs (queries) per SM at 80 registers -- the
     // same 24 warps per SM as 8 x 3, spread over 4 queries instead of 3
     // (measured: 16.40 vs 16.51 ms at C4, -2.6 to -5.3% at C1-C3; 5 x 5 and
-    // 4 x 6 were slower, profiles/r2_study_occ_c4.jsonl)
+    // 4 x 6 were slower, profiles/r2_study_occ_c4.jsonl; 6 x 5 at 64 registers
+    // spills and was 25% slower, profiles/r2_study_scan_6x5_c4.jsonl)
     auto fn = su == 4 ? dev::k_scan_fast2<M, 4, 3>
               : su == 8 ? dev::k_scan_fast2<M, 8, 3>
               : su == 104 ? dev::k_scan_fast2<M, 4, 4>
               : su == 106 ? dev::k_scan_fast2<M, 6, 4>
               : su == 306 ? dev::k_scan_fast2<M, 6, 4, 192>
-              : su == 356 ? dev::k_scan_fast2<M, 6, 5, 192>
                           : dev::k_scan_fast2<M, 6, 3>;
-    const int threads = (su == 306 || su == 356) ? 192 : 256;
+    const int threads = su == 306 ? 192 : 256;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<list_grid(nq, a.qlist != nullptr && !a.qorder), threads, smem, st>>>(a, w2, keep, cap);
     CUDA_LAUNCH_CHECK();
